@@ -1,0 +1,158 @@
+/* gscan.h -- C-ABI of the B200-native gScan 2D convex hull path.
+ *
+ * Drop-in boundary for the reference's hot path
+ *   hull2d::full_pipeline(std::span<const Point2>, const PipelineConfig&) -> PipelineResult
+ *   (/root/reference/proj/include/hull2d/pipeline.hpp:72-123)
+ * re-expressed as the north-star entry `hull(xs, ys, n) -> ordered hull vertex
+ * indices`. The reference is a header-only C++20 library with no exported
+ * symbols, so these entry points are what its FFI (a ctypes/cffi/JNI/cgo
+ * binding) would bind. Plain pointers and sizes only.
+ *
+ * Output semantics (pipeline.hpp:19-26): the CCW sequence of strict hull
+ * vertices starting at the anchor (lowest point: min y, then min x),
+ * collinear boundary points excluded, one vertex for a single distinct point,
+ * two for a collinear set. Each vertex is reported as the index of its FIRST
+ * occurrence in the input (the reference deduplicates keeping the first
+ * occurrence, angular.hpp:115-133, and compacts stably, prefilter.hpp:65-76).
+ * Results are bit-identical to the reference on the same input.
+ *
+ * Errors (errors.hpp:9-49 -> status codes): EmptyInput (pipeline.hpp:73) ->
+ * GSCAN_E_EMPTY_INPUT, ZeroChunks (pipeline.hpp:74) -> GSCAN_E_ZERO_CHUNKS.
+ * Non-finite coordinates are a precondition violation, as in the reference
+ * (SPEC.md:330), and are not checked.
+ *
+ * Threading: calls on distinct handles are independent; calls on one handle
+ * are serialised by the caller. The library owns device scratch per handle and
+ * does not allocate per call once a handle has seen its largest n.
+ */
+#ifndef GSCAN_H
+#define GSCAN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GSCAN_ABI_VERSION 1
+
+/* Status codes. */
+enum {
+    GSCAN_OK = 0,
+    GSCAN_E_EMPTY_INPUT = 1, /* hull2d::EmptyInput  (pipeline.hpp:73) */
+    GSCAN_E_ZERO_CHUNKS = 2, /* hull2d::ZeroChunks  (pipeline.hpp:74) */
+    GSCAN_E_CAPACITY = 3,    /* out_cap < hull size; *out_len holds the size needed */
+    GSCAN_E_CUDA = 4,        /* CUDA runtime failure (gscan_last_error has text) */
+    GSCAN_E_INVALID = 5,     /* NULL pointer / bad argument */
+    GSCAN_E_TOO_LARGE = 6,   /* n >= 2^32 (indices are 32-bit on the device) */
+    GSCAN_E_NO_DEVICE = 7,   /* no CUDA device / extension built without GPU */
+    GSCAN_E_INTERNAL = 8     /* device-side consistency check failed */
+};
+
+/* hull2d::PipelineConfig (pipeline.hpp:41-46). */
+typedef struct gscan_config {
+    uint64_t chunk_count;  /* slices per region in round 2; default 1024 */
+    int32_t enable_round1; /* quadrilateral pretest; default 1 */
+    int32_t enable_round2; /* sorted-region discard; default 1 */
+    int32_t chunked;       /* 1: discard_chunked (default); 0: discard_sequential */
+    int32_t reserved;      /* must be 0 */
+} gscan_config;
+
+/* hull2d::StageStats (pipeline.hpp:28-39). Times are device time measured
+ * with CUDA events on the call's stream, per reference stage. */
+typedef struct gscan_stats {
+    uint64_t n_input;
+    uint64_t n_after_round1; /* pre-dedup survivors of round 1 (pipeline.hpp:93) */
+    uint64_t n_after_round2; /* post-dedup, post-round-2 buffer (pipeline.hpp:109) */
+    uint64_t hull_size;
+    double t_round1_ms;
+    double t_annotate_ms;
+    double t_sort_ms;
+    double t_round2_ms;
+    double t_finalize_ms;
+    double t_total_ms;
+} gscan_stats;
+
+typedef struct gscan_handle gscan_handle;
+
+/* Fills the reference defaults (chunk_count 1024, both rounds, chunked). */
+void gscan_config_default(gscan_config* cfg);
+
+/* Handle lifetime. device < 0 selects the current device. */
+int gscan_create(int device, gscan_handle** out);
+int gscan_destroy(gscan_handle* h);
+/* Pre-allocates device scratch for inputs of up to n points. */
+int gscan_reserve(gscan_handle* h, uint64_t n);
+/* Uses `stream` (a cudaStream_t; NULL = the handle's own stream) for later calls. */
+int gscan_set_stream(gscan_handle* h, void* stream);
+
+/* Host-buffer entry: copies xs/ys (n doubles each) to the device, runs the
+ * pipeline, copies the index list back. cfg may be NULL (defaults); stats may
+ * be NULL. On GSCAN_E_CAPACITY nothing is written to out_idx. */
+int gscan_hull_f64(gscan_handle* h, const double* xs, const double* ys, uint64_t n,
+                   const gscan_config* cfg, uint64_t* out_idx, uint64_t out_cap,
+                   uint64_t* out_len, gscan_stats* stats);
+
+/* Device-buffer entry: d_xs/d_ys are device pointers; the index list is left
+ * in d_out_idx (device, uint32). Synchronises the handle's stream before
+ * returning (hull size is needed on the host). */
+int gscan_hull_f64_device(gscan_handle* h, const double* d_xs, const double* d_ys, uint64_t n,
+                          const gscan_config* cfg, uint32_t* d_out_idx, uint64_t out_cap,
+                          uint64_t* out_len, gscan_stats* stats);
+
+/* North-star convenience entry: hull(xs, ys, n) with a lazily created
+ * per-process handle on the current device and the default config. */
+int gscan_hull(const double* xs, const double* ys, uint64_t n, uint64_t* out_idx,
+               uint64_t out_cap, uint64_t* out_len);
+
+/* ---- stage entry points (device pointers), for stage-level parity ---- */
+
+/* find_extremes (prefilter.hpp:28-39) + select_anchor on all points
+ * (angular.hpp:40-49): out[0..3] = i_minx, i_miny, i_maxx, i_maxy; out[4] = anchor. */
+int gscan_stage_extremes(gscan_handle* h, const double* d_xs, const double* d_ys, uint64_t n,
+                         uint64_t out[5]);
+/* classify_quad + compact (prefilter.hpp:47-76): survivor input indices in
+ * input order into d_out (device uint32, capacity n); *n_out = count. */
+int gscan_stage_round1(gscan_handle* h, const double* d_xs, const double* d_ys, uint64_t n,
+                       uint32_t* d_out, uint64_t* n_out);
+/* annotate + sort_by_angle (angular.hpp:118-194) of ALL n points (round 1
+ * skipped): buffer entries as input indices into d_out (device uint32,
+ * capacity n); *len = buffer size. */
+int gscan_stage_sorted(gscan_handle* h, const double* d_xs, const double* d_ys, uint64_t n,
+                       uint32_t* d_out, uint64_t* len);
+/* split_regions + discard flags (discard.hpp:79-124) over the sorted buffer of
+ * all n points (round 1 skipped): d_flags (device uint8, capacity n) gets one
+ * keep flag per buffer entry; *longest = split index. */
+int gscan_stage_discard(gscan_handle* h, const double* d_xs, const double* d_ys, uint64_t n,
+                        uint64_t chunk_count, int chunked, uint8_t* d_flags, uint64_t* longest,
+                        uint64_t* len);
+
+/* ---- device self-checks ---- */
+
+/* glibc-identical atan2 (paper_1508_05931_b200/csrc/glibc_atan2.h) on the
+ * device: out[i] = atan2(y[i], x[i]); device pointers. */
+int gscan_device_atan2(gscan_handle* h, const double* d_y, const double* d_x, double* d_out,
+                       uint64_t n);
+
+/* ---- introspection ---- */
+const char* gscan_status_string(int status);
+const char* gscan_last_error(const gscan_handle* h);
+/* Number of kernels the handle launched in its last pipeline call. */
+uint64_t gscan_last_launch_count(const gscan_handle* h);
+/* Per-kernel event timing of the last call (ms), `names` entries, in launch
+ * order; returns the number of records (<= cap). Requires gscan_set_profiling. */
+int gscan_set_profiling(gscan_handle* h, int enabled);
+int gscan_last_kernel_times(const gscan_handle* h, const char** names, double* ms, int cap);
+
+/* ---- harness helpers (host) ---- */
+enum { GSCAN_GEN_SQUARE = 0, GSCAN_GEN_DISK = 1, GSCAN_GEN_CIRCLE = 2, GSCAN_GEN_COLLINEAR = 3 };
+/* datagen::gen_* (datagen.hpp:32-91), bit-identical to the reference. */
+int gscan_generate(int kind, uint64_t n, uint64_t seed, double* xs, double* ys);
+/* tests/support.hpp:54-63 gen_grid. */
+int gscan_generate_grid(uint64_t n, uint64_t seed, int lo, int hi, double* xs, double* ys);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GSCAN_H */

@@ -1,0 +1,132 @@
+// Device primitives shared by the gScan kernels (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "glibc_atan2.h"
+
+namespace gscan {
+
+constexpr int kBlock = 256;   // threads per CTA for the streaming kernels
+constexpr int kWarps = kBlock / 32;
+constexpr uint32_t kDead = 0xffffffffu;        // index marker: duplicate dropped
+constexpr uint64_t kKeyDrop = ~0ull;           // sort key marker: coincides with anchor
+
+// ---------------------------------------------------------------------------
+// Exact predicates. Every op is an explicit round-to-nearest intrinsic so the
+// compiler cannot contract a*b-c*d into an FMA: the reference's cross() is
+// plain double arithmetic without FMA (geom.hpp:19-21).
+
+// (b.x-a.x)(c.y-a.y) - (b.y-a.y)(c.x-a.x), geom.hpp:19-21.
+__device__ __forceinline__ double cross_rn(double ax, double ay, double bx, double by, double cx,
+                                           double cy) {
+  return __dsub_rn(__dmul_rn(__dsub_rn(bx, ax), __dsub_rn(cy, ay)),
+                   __dmul_rn(__dsub_rn(by, ay), __dsub_rn(cx, ax)));
+}
+
+// Same value with the edge vector (ex, ey) = (b.x-a.x, b.y-a.y) precomputed
+// (identical rounding: the subtraction is the same operation).
+__device__ __forceinline__ double cross_edge(double ax, double ay, double ex, double ey, double cx,
+                                             double cy) {
+  return __dsub_rn(__dmul_rn(ex, __dsub_rn(cy, ay)), __dmul_rn(ey, __dsub_rn(cx, ax)));
+}
+
+// dist2 = dx*dx + dy*dy, geom.hpp:42 (no FMA).
+__device__ __forceinline__ double dist2_rn(double dx, double dy) {
+  return __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
+}
+
+__device__ __forceinline__ uint64_t dbits(double d) { return (uint64_t)__double_as_longlong(d); }
+__device__ __forceinline__ double bitsd(uint64_t u) { return __longlong_as_double((long long)u); }
+
+// ---------------------------------------------------------------------------
+// Decoupled look-back (single-pass chained scan) over per-tile aggregates.
+// Status word: bits 62-63 = flag, low 62 bits = value.
+constexpr uint64_t kFlagAgg = 1ull << 62;
+constexpr uint64_t kFlagPre = 2ull << 62;
+constexpr uint64_t kValMask = (1ull << 62) - 1;
+
+__device__ __forceinline__ uint64_t ld_volatile(const uint64_t* p) {
+  return *reinterpret_cast<const volatile uint64_t*>(p);
+}
+__device__ __forceinline__ void st_volatile(uint64_t* p, uint64_t v) {
+  *reinterpret_cast<volatile uint64_t*>(p) = v;
+}
+
+// Called by all 32 lanes of ONE warp. Publishes `agg` for `tile` and returns
+// the exclusive prefix of all earlier tiles (same value in every lane).
+__device__ __forceinline__ uint64_t lookback_exclusive(uint64_t* status, uint32_t tile,
+                                                       uint64_t agg) {
+  const int lane = threadIdx.x & 31;
+  if (tile == 0) {
+    if (lane == 0) {
+      __threadfence();
+      st_volatile(&status[0], kFlagPre | agg);
+    }
+    return 0;
+  }
+  if (lane == 0) {
+    __threadfence();
+    st_volatile(&status[tile], kFlagAgg | agg);
+  }
+  uint64_t excl = 0;
+  int64_t look = (int64_t)tile - 1;
+  while (true) {
+    const int64_t t = look - lane;
+    uint64_t w = kFlagPre;  // lanes past tile 0 read as an empty prefix
+    if (t >= 0) {
+      do {
+        w = ld_volatile(&status[t]);
+      } while ((w >> 62) == 0);
+    }
+    const uint32_t pre_mask = __ballot_sync(0xffffffffu, (w & kFlagPre) != 0);
+    const int first_pre = pre_mask ? (__ffs(pre_mask) - 1) : 32;
+    uint64_t v = (lane <= first_pre && t >= 0) ? (w & kValMask) : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    excl += v;
+    if (pre_mask) break;
+    look -= 32;
+  }
+  if (lane == 0) {
+    __threadfence();
+    st_volatile(&status[tile], kFlagPre | (excl + agg));
+  }
+  return excl;
+}
+
+// ---------------------------------------------------------------------------
+// Block-wide exclusive scan of one uint32 per thread (kBlock threads).
+__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* smem_warp,
+                                                         uint32_t* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) smem_warp[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t s = (lane < kWarps) ? smem_warp[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += y;
+    }
+    if (lane < kWarps) smem_warp[lane] = s;  // inclusive warp prefix
+  }
+  __syncthreads();
+  const uint32_t warp_excl = warp ? smem_warp[warp - 1] : 0;
+  if (total) *total = smem_warp[kWarps - 1];
+  return warp_excl + x - v;
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+}  // namespace gscan

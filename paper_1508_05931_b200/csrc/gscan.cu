@@ -1,0 +1,689 @@
+// Host orchestration and C-ABI of the B200 gScan hull path (include/gscan.h).
+//
+// One call = the reference's full_pipeline (pipeline.hpp:72-123) as a chain
+// of sm_100a kernels on one stream:
+//   K1 extremes+anchor -> K2 quad filter + stable compaction -> K3 polar keys
+//   + bucket histogram -> bucket offsets (scan) -> scatter -> K4 per-bucket
+//   sort + dedup -> split_regions -> K5 round-2 walks -> stable compaction
+//   -> K7 Graham scan.
+// Sizes that steer launches are read back at most twice per call.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/gscan.h"
+#include "kernels.cuh"
+
+using namespace gscan;
+
+namespace {
+
+constexpr double kPi = 3.14159265358979323846;
+
+struct KernelTime {
+  const char* name;
+  cudaEvent_t a, b;
+};
+
+}  // namespace
+
+struct gscan_handle {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int sm_count = 148;
+  uint64_t cap = 0;  // points
+  uint64_t nb_cap = 0;
+  std::string err;
+  uint64_t launches = 0;
+  bool profiling = false;
+  std::vector<KernelTime> ktimes;
+  size_t kt_used = 0;
+
+  // device buffers
+  double *d_xs = nullptr, *d_ys = nullptr;
+  uint32_t* surv = nullptr;
+  uint64_t* keys = nullptr;
+  uint64_t* bkey = nullptr;
+  uint32_t* bval = nullptr;
+  double *A_x = nullptr, *A_y = nullptr;
+  uint32_t* A_i = nullptr;
+  double *C_x = nullptr, *C_y = nullptr;
+  uint32_t* C_i = nullptr;
+  uint8_t* flags = nullptr;
+  uint32_t* stack = nullptr;
+  uint32_t* d_out = nullptr;
+  uint64_t* status = nullptr;
+  uint64_t status_cap = 0;
+  uint32_t *hist = nullptr, *bstart = nullptr, *cursor = nullptr, *oversize = nullptr;
+  BucketBest* best = nullptr;
+  ExtAcc* partials = nullptr;
+  ExtResult* ext = nullptr;
+  Counters* ctr = nullptr;
+  unsigned long long* scratch64 = nullptr;  // [0] max bits, [1] min pos (as u32 in low half)
+  Counters* h_ctr = nullptr;  // pinned mirror
+  uint32_t* h_out = nullptr;  // pinned staging for indices
+  uint64_t h_out_cap = 0;
+  cudaEvent_t ev[8] = {};
+};
+
+namespace {
+
+int fail(gscan_handle* h, int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (h) h->err = buf;
+  return code;
+}
+
+#define CU(call)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return fail(h, GSCAN_E_CUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                  __FILE__, __LINE__);                                                    \
+  } while (0)
+
+template <typename T>
+void dfree(T*& p) {
+  if (p) cudaFree(p);
+  p = nullptr;
+}
+
+void free_buffers(gscan_handle* h) {
+  dfree(h->d_xs); dfree(h->d_ys); dfree(h->surv); dfree(h->keys); dfree(h->bkey);
+  dfree(h->bval); dfree(h->A_x); dfree(h->A_y); dfree(h->A_i); dfree(h->C_x); dfree(h->C_y);
+  dfree(h->C_i); dfree(h->flags); dfree(h->stack); dfree(h->d_out); dfree(h->status);
+  dfree(h->hist); dfree(h->bstart); dfree(h->cursor); dfree(h->oversize); dfree(h->best);
+  h->cap = 0;
+  h->nb_cap = 0;
+  h->status_cap = 0;
+}
+
+uint32_t buckets_for(uint64_t n) {
+  uint64_t want = (n + 511) / 512;
+  uint32_t nb = 1;
+  while (nb < want && nb < (1u << 24)) nb <<= 1;
+  return nb;
+}
+
+int reserve(gscan_handle* h, uint64_t n) {
+  if (n <= h->cap) return GSCAN_OK;
+  free_buffers(h);
+  const uint64_t m = n + 1;
+  CU(cudaMalloc(&h->d_xs, m * 8));
+  CU(cudaMalloc(&h->d_ys, m * 8));
+  CU(cudaMalloc(&h->surv, m * 4));
+  CU(cudaMalloc(&h->keys, m * 8));
+  CU(cudaMalloc(&h->bkey, m * 8));
+  CU(cudaMalloc(&h->bval, m * 4));
+  CU(cudaMalloc(&h->A_x, m * 8));
+  CU(cudaMalloc(&h->A_y, m * 8));
+  CU(cudaMalloc(&h->A_i, m * 4));
+  CU(cudaMalloc(&h->C_x, m * 8));
+  CU(cudaMalloc(&h->C_y, m * 8));
+  CU(cudaMalloc(&h->C_i, m * 4));
+  CU(cudaMalloc(&h->flags, m));
+  CU(cudaMalloc(&h->stack, m * 4));
+  CU(cudaMalloc(&h->d_out, m * 4));
+  const uint32_t nb = buckets_for(n);
+  h->nb_cap = nb;
+  CU(cudaMalloc(&h->hist, (nb + 2) * 4));
+  CU(cudaMalloc(&h->bstart, (nb + 2) * 4));
+  CU(cudaMalloc(&h->cursor, (nb + 2) * 4));
+  CU(cudaMalloc(&h->oversize, (nb + 2) * 4));
+  CU(cudaMalloc(&h->best, (nb + 2) * sizeof(BucketBest)));
+  const uint64_t tiles = (m + kCompactTile - 1) / kCompactTile + 64;
+  h->status_cap = tiles;
+  CU(cudaMalloc(&h->status, tiles * 8));
+  h->cap = n;
+  return GSCAN_OK;
+}
+
+// ---- launch bookkeeping (counts every kernel; optional per-kernel events) ----
+struct Launch {
+  gscan_handle* h;
+  const char* name;
+  KernelTime* kt = nullptr;
+  Launch(gscan_handle* hh, const char* nm) : h(hh), name(nm) {
+    ++h->launches;
+    if (h->profiling) {
+      if (h->kt_used == h->ktimes.size()) {
+        KernelTime t{};
+        cudaEventCreate(&t.a);
+        cudaEventCreate(&t.b);
+        h->ktimes.push_back(t);
+      }
+      kt = &h->ktimes[h->kt_used++];
+      kt->name = nm;
+      cudaEventRecord(kt->a, h->stream);
+    }
+  }
+  ~Launch() {
+    if (kt) cudaEventRecord(kt->b, h->stream);
+  }
+};
+
+int reset_lookback(gscan_handle* h, uint64_t tiles) {
+  if (tiles > h->status_cap) return fail(h, GSCAN_E_INTERNAL, "look-back status too small");
+  CU(cudaMemsetAsync(h->status, 0, tiles * 8, h->stream));
+  CU(cudaMemsetAsync(&h->ctr->tile_ticket, 0, 4, h->stream));
+  return GSCAN_OK;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+int sync_counters(gscan_handle* h) {
+  CU(cudaMemcpyAsync(h->h_ctr, h->ctr, sizeof(Counters), cudaMemcpyDeviceToHost, h->stream));
+  CU(cudaStreamSynchronize(h->stream));
+  return GSCAN_OK;
+}
+
+#define TRY(x)                  \
+  do {                          \
+    int rc_ = (x);              \
+    if (rc_ != GSCAN_OK) return rc_; \
+  } while (0)
+
+// K1 + K2 (round 1). Leaves survivors in h->surv and n1 in ctr.
+int stage_round1(gscan_handle* h, const double* xs, const double* ys, uint32_t n, int enable) {
+  const bool vec = aligned16(xs) && aligned16(ys);
+  {
+    const uint32_t grid =
+        std::max(1u, std::min<uint32_t>((n + kBlock * 8 - 1) / (kBlock * 8), h->sm_count * 8));
+    Launch L(h, "k_extremes");
+    if (vec) k_extremes<true><<<grid, kBlock, 0, h->stream>>>(xs, ys, n, h->partials, h->ext, h->ctr);
+    else k_extremes<false><<<grid, kBlock, 0, h->stream>>>(xs, ys, n, h->partials, h->ext, h->ctr);
+  }
+  const uint64_t tiles = (n + kFilterTile - 1) / kFilterTile;
+  TRY(reset_lookback(h, tiles));
+  {
+    Launch L(h, "k_filter_compact");
+    if (vec)
+      k_filter_compact<true><<<tiles, kBlock, 0, h->stream>>>(xs, ys, n, h->ext, enable, h->status,
+                                                              h->surv, h->ctr);
+    else
+      k_filter_compact<false><<<tiles, kBlock, 0, h->stream>>>(xs, ys, n, h->ext, enable,
+                                                               h->status, h->surv, h->ctr);
+  }
+  CU(cudaGetLastError());
+  return GSCAN_OK;
+}
+
+// K3 .. K4: keys, bucket offsets, scatter, per-bucket sort + dedup, anchor
+// at position 0, split_regions. Leaves the annotated buffer in A_*.
+int stage_annotate_sort(gscan_handle* h, const double* xs, const double* ys, uint32_t n,
+                        int t_annot_ev, int t_sort_ev) {
+  const uint32_t nb = buckets_for(n);
+  const double scale = (double)nb / kPi;
+  CU(cudaMemsetAsync(h->hist, 0, (nb + 1) * 4, h->stream));
+  {
+    const uint32_t grid = std::max(1u, std::min<uint32_t>((n + kBlock - 1) / kBlock, h->sm_count * 16));
+    Launch L(h, "k_keys");
+    k_keys<<<grid, kBlock, 0, h->stream>>>(xs, ys, h->surv, h->ext, h->ctr, h->keys, h->hist,
+                                           scale, nb, h->ctr);
+  }
+  if (t_annot_ev >= 0) CU(cudaEventRecord(h->ev[t_annot_ev], h->stream));
+  const uint64_t stiles = (nb + 1 + kScanTile - 1) / kScanTile;
+  TRY(reset_lookback(h, stiles));
+  {
+    Launch L(h, "k_scan_u32");
+    k_scan_u32<<<stiles, kBlock, 0, h->stream>>>(h->hist, nb, h->bstart, h->status, h->ctr);
+  }
+  CU(cudaMemcpyAsync(h->cursor, h->bstart, nb * 4, cudaMemcpyDeviceToDevice, h->stream));
+  {
+    const uint32_t grid = std::max(1u, std::min<uint32_t>((n + kBlock - 1) / kBlock, h->sm_count * 16));
+    Launch L(h, "k_scatter");
+    k_scatter<<<grid, kBlock, 0, h->stream>>>(h->keys, h->surv, h->ctr, h->cursor, scale, nb,
+                                              h->bkey, h->bval);
+  }
+  {
+    const size_t smem = (size_t)kSortCap * (8 + 8 + 4 + 4);
+    Launch L(h, "k_bucket_sort");
+    k_bucket_sort<<<nb, kSortBlock, smem, h->stream>>>(xs, ys, h->bstart, h->bkey, h->bval, h->ext,
+                                                       nb, h->A_x, h->A_y, h->A_i, h->best,
+                                                       h->oversize, h->ctr);
+  }
+  {
+    Launch L(h, "k_bucket_sort_big");
+    k_bucket_sort_big<<<8, 32, 0, h->stream>>>(xs, ys, h->bstart, h->bkey, h->bval, h->ext,
+                                               h->oversize, h->ctr, h->A_x, h->A_y, h->A_i,
+                                               h->best, h->ctr);
+  }
+  {
+    Launch L(h, "k_put_anchor");
+    k_put_anchor<<<1, 1, 0, h->stream>>>(h->ext, h->bstart, nb, h->A_x, h->A_y, h->A_i, h->ctr);
+  }
+  {
+    Launch L(h, "k_longest");
+    k_longest<<<1, 1024, 0, h->stream>>>(h->best, nb, h->ctr);
+  }
+  CU(cudaGetLastError());
+  TRY(sync_counters(h));
+  if (h->h_ctr->dead) {
+    // duplicates: compact the buffer, then split_regions over final positions
+    const uint32_t m = h->h_ctr->m_total;
+    const uint64_t tiles = (m + kCompactTile - 1) / kCompactTile;
+    TRY(reset_lookback(h, tiles));
+    {
+      Launch L(h, "k_compact_dedup");
+      k_compact_xyi<0><<<tiles, kBlock, 0, h->stream>>>(h->A_x, h->A_y, h->A_i, nullptr, nullptr,
+                                                        m, h->C_x, h->C_y, h->C_i, h->status,
+                                                        h->ctr, &h->ctr->m_total);
+    }
+    std::swap(h->A_x, h->C_x);
+    std::swap(h->A_y, h->C_y);
+    std::swap(h->A_i, h->C_i);
+    TRY(sync_counters(h));
+    const uint32_t m2 = h->h_ctr->m_total;
+    CU(cudaMemsetAsync(h->scratch64, 0, 8, h->stream));
+    CU(cudaMemsetAsync(h->scratch64 + 1, 0xff, 8, h->stream));
+    const uint32_t grid = std::max(1u, std::min<uint32_t>((m2 + kBlock - 1) / kBlock, h->sm_count * 8));
+    {
+      Launch L(h, "k_longest_scan0");
+      k_longest_scan<<<grid, kBlock, 0, h->stream>>>(h->A_x, h->A_y, m2, h->scratch64,
+                                                     reinterpret_cast<uint32_t*>(h->scratch64 + 1), 0);
+    }
+    {
+      Launch L(h, "k_longest_scan1");
+      k_longest_scan<<<grid, kBlock, 0, h->stream>>>(h->A_x, h->A_y, m2, h->scratch64,
+                                                     reinterpret_cast<uint32_t*>(h->scratch64 + 1), 1);
+    }
+    CU(cudaMemcpyAsync(&h->ctr->longest, h->scratch64 + 1, 4, cudaMemcpyDeviceToDevice, h->stream));
+    TRY(sync_counters(h));
+  }
+  if (t_sort_ev >= 0) CU(cudaEventRecord(h->ev[t_sort_ev], h->stream));
+  return GSCAN_OK;
+}
+
+// Round 2 over A_* (M entries). Result in R (pointers returned), n2 in ctr.
+int stage_round2(gscan_handle* h, const gscan_config& cfg, double** Rx, double** Ry,
+                 uint32_t** Ri) {
+  const uint32_t m = h->h_ctr->m_total;
+  if (!cfg.enable_round2 || m < 2) {
+    *Rx = h->A_x; *Ry = h->A_y; *Ri = h->A_i;
+    CU(cudaMemcpyAsync(&h->ctr->n2, &h->ctr->m_total, 4, cudaMemcpyDeviceToDevice, h->stream));
+    return GSCAN_OK;
+  }
+  const uint32_t l = h->h_ctr->longest;
+  if (l < 1 || l >= m) return fail(h, GSCAN_E_INTERNAL, "split index %u out of range (M=%u)", l, m);
+  SliceGeom g{};
+  g.l = l;
+  g.m = m;
+  g.chunked = cfg.chunked ? 1 : 0;
+  const uint64_t c = cfg.chunk_count;
+  const uint32_t m_right = l - 1, m_left = m - 1 - l;
+  if (cfg.chunked) {
+    if (m_right > 1) {
+      g.step_r = (uint32_t)((m_right + c - 1) / c);
+      g.n_right = (m_right + g.step_r - 1) / g.step_r;
+    }
+    if (m_left > 1) {
+      g.step_l = (uint32_t)((m_left + c - 1) / c);
+      g.n_left = (m_left + g.step_l - 1) / g.step_l;
+    }
+  } else {
+    g.n_right = (l >= 2) ? 1 : 0;
+    g.n_left = (l + 2 <= m - 1) ? 1 : 0;
+  }
+  CU(cudaMemsetAsync(h->flags, 1, m, h->stream));
+  const uint32_t slices = g.n_right + g.n_left;
+  if (slices) {
+    const uint32_t grid = (slices * 32 + kBlock - 1) / kBlock;
+    Launch L(h, "k_round2_walk");
+    k_round2_walk<<<grid, kBlock, 0, h->stream>>>(h->A_x, h->A_y, g, h->flags);
+  }
+  const uint64_t tiles = (m + kCompactTile - 1) / kCompactTile;
+  TRY(reset_lookback(h, tiles));
+  {
+    Launch L(h, "k_compact_round2");
+    k_compact_xyi<1><<<tiles, kBlock, 0, h->stream>>>(h->A_x, h->A_y, h->A_i, h->flags, nullptr, m,
+                                                      h->C_x, h->C_y, h->C_i, h->status, h->ctr,
+                                                      &h->ctr->n2);
+  }
+  CU(cudaGetLastError());
+  *Rx = h->C_x; *Ry = h->C_y; *Ri = h->C_i;
+  return GSCAN_OK;
+}
+
+int validate(gscan_handle* h, uint64_t n, const gscan_config& cfg) {
+  if (!h) return GSCAN_E_INVALID;
+  if (n == 0) return fail(h, GSCAN_E_EMPTY_INPUT, "full_pipeline: no points");
+  if (cfg.chunk_count == 0) return fail(h, GSCAN_E_ZERO_CHUNKS, "full_pipeline: chunk_count must be positive");
+  if (n >= 0xffffffffull) return fail(h, GSCAN_E_TOO_LARGE, "n = %llu exceeds 2^32-2", (unsigned long long)n);
+  return GSCAN_OK;
+}
+
+float ev_ms(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, a, b);
+  return ms;
+}
+
+// Full pipeline on device-resident SoA input. Hull indices left in h->d_out.
+int run_pipeline(gscan_handle* h, const double* xs, const double* ys, uint64_t n64,
+                 const gscan_config& cfg, uint64_t* hull_size, gscan_stats* st) {
+  TRY(validate(h, n64, cfg));
+  TRY(reserve(h, n64));
+  const uint32_t n = (uint32_t)n64;
+  h->launches = 0;
+  h->kt_used = 0;
+  CU(cudaEventRecord(h->ev[0], h->stream));
+  CU(cudaMemsetAsync(h->ctr, 0, sizeof(Counters), h->stream));
+  TRY(stage_round1(h, xs, ys, n, cfg.enable_round1));
+  CU(cudaEventRecord(h->ev[1], h->stream));
+  TRY(stage_annotate_sort(h, xs, ys, n, 2, 3));
+  double *Rx, *Ry;
+  uint32_t* Ri;
+  TRY(stage_round2(h, cfg, &Rx, &Ry, &Ri));
+  CU(cudaEventRecord(h->ev[4], h->stream));
+  {
+    Launch L(h, "k_graham_seq");
+    k_graham_seq<<<1, 32, 0, h->stream>>>(Rx, Ry, Ri, &h->ctr->n2, h->stack, h->d_out, h->ctr);
+  }
+  CU(cudaGetLastError());
+  CU(cudaEventRecord(h->ev[5], h->stream));
+  TRY(sync_counters(h));
+  const Counters& c = *h->h_ctr;
+  *hull_size = c.hull;
+  if (st) {
+    st->n_input = n64;
+    st->n_after_round1 = c.n1;
+    st->n_after_round2 = c.n2;
+    st->hull_size = c.hull;
+    st->t_round1_ms = ev_ms(h->ev[0], h->ev[1]);
+    st->t_annotate_ms = ev_ms(h->ev[1], h->ev[2]);
+    st->t_sort_ms = ev_ms(h->ev[2], h->ev[3]);
+    st->t_round2_ms = ev_ms(h->ev[3], h->ev[4]);
+    st->t_finalize_ms = ev_ms(h->ev[4], h->ev[5]);
+    st->t_total_ms = ev_ms(h->ev[0], h->ev[5]);
+  }
+  return GSCAN_OK;
+}
+
+gscan_config resolve(const gscan_config* cfg) {
+  gscan_config c;
+  gscan_config_default(&c);
+  if (cfg) c = *cfg;
+  return c;
+}
+
+std::mutex g_default_mu;
+gscan_handle* g_default = nullptr;
+
+}  // namespace
+
+// ============================================================================
+// C-ABI
+
+extern "C" {
+
+void gscan_config_default(gscan_config* cfg) {
+  if (!cfg) return;
+  cfg->chunk_count = 1024;
+  cfg->enable_round1 = 1;
+  cfg->enable_round2 = 1;
+  cfg->chunked = 1;
+  cfg->reserved = 0;
+}
+
+const char* gscan_status_string(int s) {
+  switch (s) {
+    case GSCAN_OK: return "ok";
+    case GSCAN_E_EMPTY_INPUT: return "empty input";
+    case GSCAN_E_ZERO_CHUNKS: return "chunk_count must be positive";
+    case GSCAN_E_CAPACITY: return "output capacity too small";
+    case GSCAN_E_CUDA: return "CUDA error";
+    case GSCAN_E_INVALID: return "invalid argument";
+    case GSCAN_E_TOO_LARGE: return "input too large";
+    case GSCAN_E_NO_DEVICE: return "no CUDA device";
+    case GSCAN_E_INTERNAL: return "internal consistency check failed";
+    default: return "unknown status";
+  }
+}
+
+const char* gscan_last_error(const gscan_handle* h) { return h ? h->err.c_str() : ""; }
+uint64_t gscan_last_launch_count(const gscan_handle* h) { return h ? h->launches : 0; }
+
+int gscan_create(int device, gscan_handle** out) {
+  if (!out) return GSCAN_E_INVALID;
+  *out = nullptr;
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) return GSCAN_E_NO_DEVICE;
+  gscan_handle* h = new gscan_handle();
+  if (device < 0) cudaGetDevice(&device);
+  h->device = device;
+  int rc = GSCAN_OK;
+  auto init = [&]() -> int {
+    CU(cudaSetDevice(device));
+    CU(cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, device));
+    CU(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+    h->own_stream = true;
+    CU(cudaMalloc(&h->partials, sizeof(ExtAcc) * h->sm_count * 8));
+    CU(cudaMalloc(&h->ext, sizeof(ExtResult)));
+    CU(cudaMalloc(&h->ctr, sizeof(Counters)));
+    CU(cudaMemset(h->ctr, 0, sizeof(Counters)));
+    CU(cudaMalloc(&h->scratch64, 16));
+    CU(cudaMallocHost(&h->h_ctr, sizeof(Counters)));
+    for (auto& e : h->ev) CU(cudaEventCreate(&e));
+    CU(cudaFuncSetAttribute(k_bucket_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            kSortCap * (8 + 8 + 4 + 4)));
+    return GSCAN_OK;
+  };
+  rc = init();
+  if (rc != GSCAN_OK) {
+    gscan_destroy(h);
+    return rc;
+  }
+  *out = h;
+  return GSCAN_OK;
+}
+
+int gscan_destroy(gscan_handle* h) {
+  if (!h) return GSCAN_OK;
+  cudaSetDevice(h->device);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  free_buffers(h);
+  dfree(h->partials); dfree(h->ext); dfree(h->ctr); dfree(h->scratch64);
+  if (h->h_ctr) cudaFreeHost(h->h_ctr);
+  if (h->h_out) cudaFreeHost(h->h_out);
+  for (auto& e : h->ev) if (e) cudaEventDestroy(e);
+  for (auto& k : h->ktimes) { cudaEventDestroy(k.a); cudaEventDestroy(k.b); }
+  if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+  return GSCAN_OK;
+}
+
+int gscan_reserve(gscan_handle* h, uint64_t n) {
+  if (!h) return GSCAN_E_INVALID;
+  CU(cudaSetDevice(h->device));
+  return reserve(h, n);
+}
+
+int gscan_set_stream(gscan_handle* h, void* stream) {
+  if (!h) return GSCAN_E_INVALID;
+  if (stream) {
+    if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+    h->stream = static_cast<cudaStream_t>(stream);
+    h->own_stream = false;
+  }
+  return GSCAN_OK;
+}
+
+int gscan_set_profiling(gscan_handle* h, int enabled) {
+  if (!h) return GSCAN_E_INVALID;
+  h->profiling = enabled != 0;
+  return GSCAN_OK;
+}
+
+int gscan_last_kernel_times(const gscan_handle* h, const char** names, double* ms, int cap) {
+  if (!h) return 0;
+  int k = 0;
+  for (size_t i = 0; i < h->kt_used && k < cap; ++i, ++k) {
+    if (names) names[k] = h->ktimes[i].name;
+    if (ms) ms[k] = ev_ms(h->ktimes[i].a, h->ktimes[i].b);
+  }
+  return k;
+}
+
+int gscan_hull_f64_device(gscan_handle* h, const double* d_xs, const double* d_ys, uint64_t n,
+                          const gscan_config* cfg, uint32_t* d_out_idx, uint64_t out_cap,
+                          uint64_t* out_len, gscan_stats* stats) {
+  if (!h || (!d_xs && n) || (!d_ys && n)) return GSCAN_E_INVALID;
+  CU(cudaSetDevice(h->device));
+  const gscan_config c = resolve(cfg);
+  uint64_t hs = 0;
+  TRY(run_pipeline(h, d_xs, d_ys, n, c, &hs, stats));
+  if (out_len) *out_len = hs;
+  if (hs > out_cap) return fail(h, GSCAN_E_CAPACITY, "hull has %llu vertices, capacity %llu",
+                                (unsigned long long)hs, (unsigned long long)out_cap);
+  if (d_out_idx && hs) {
+    CU(cudaMemcpyAsync(d_out_idx, h->d_out, hs * 4, cudaMemcpyDeviceToDevice, h->stream));
+    CU(cudaStreamSynchronize(h->stream));
+  }
+  return GSCAN_OK;
+}
+
+int gscan_hull_f64(gscan_handle* h, const double* xs, const double* ys, uint64_t n,
+                   const gscan_config* cfg, uint64_t* out_idx, uint64_t out_cap,
+                   uint64_t* out_len, gscan_stats* stats) {
+  if (!h || (n && (!xs || !ys))) return GSCAN_E_INVALID;
+  CU(cudaSetDevice(h->device));
+  const gscan_config c = resolve(cfg);
+  TRY(validate(h, n, c));
+  TRY(reserve(h, n));
+  CU(cudaMemcpyAsync(h->d_xs, xs, n * 8, cudaMemcpyHostToDevice, h->stream));
+  CU(cudaMemcpyAsync(h->d_ys, ys, n * 8, cudaMemcpyHostToDevice, h->stream));
+  uint64_t hs = 0;
+  TRY(run_pipeline(h, h->d_xs, h->d_ys, n, c, &hs, stats));
+  if (out_len) *out_len = hs;
+  if (hs > out_cap) return fail(h, GSCAN_E_CAPACITY, "hull has %llu vertices, capacity %llu",
+                                (unsigned long long)hs, (unsigned long long)out_cap);
+  if (!out_idx || hs == 0) return GSCAN_OK;
+  if (hs > h->h_out_cap) {
+    if (h->h_out) cudaFreeHost(h->h_out);
+    h->h_out = nullptr;
+    CU(cudaMallocHost(&h->h_out, hs * 4));
+    h->h_out_cap = hs;
+  }
+  CU(cudaMemcpyAsync(h->h_out, h->d_out, hs * 4, cudaMemcpyDeviceToHost, h->stream));
+  CU(cudaStreamSynchronize(h->stream));
+  for (uint64_t i = 0; i < hs; ++i) out_idx[i] = h->h_out[i];
+  return GSCAN_OK;
+}
+
+int gscan_hull(const double* xs, const double* ys, uint64_t n, uint64_t* out_idx,
+               uint64_t out_cap, uint64_t* out_len) {
+  std::lock_guard<std::mutex> lock(g_default_mu);
+  if (!g_default) {
+    const int rc = gscan_create(-1, &g_default);
+    if (rc != GSCAN_OK) return rc;
+  }
+  return gscan_hull_f64(g_default, xs, ys, n, nullptr, out_idx, out_cap, out_len, nullptr);
+}
+
+// ---- stage entry points ----
+
+int gscan_stage_extremes(gscan_handle* h, const double* d_xs, const double* d_ys, uint64_t n,
+                         uint64_t out[5]) {
+  if (!h || !out) return GSCAN_E_INVALID;
+  gscan_config c;
+  gscan_config_default(&c);
+  TRY(validate(h, n, c));
+  CU(cudaSetDevice(h->device));
+  TRY(reserve(h, n));
+  CU(cudaMemsetAsync(h->ctr, 0, sizeof(Counters), h->stream));
+  TRY(stage_round1(h, d_xs, d_ys, (uint32_t)n, 1));
+  ExtResult r;
+  CU(cudaMemcpyAsync(&r, h->ext, sizeof r, cudaMemcpyDeviceToHost, h->stream));
+  CU(cudaStreamSynchronize(h->stream));
+  for (int k = 0; k < 5; ++k) out[k] = r.idx[k];
+  return GSCAN_OK;
+}
+
+int gscan_stage_round1(gscan_handle* h, const double* d_xs, const double* d_ys, uint64_t n,
+                       uint32_t* d_out, uint64_t* n_out) {
+  if (!h || !d_out || !n_out) return GSCAN_E_INVALID;
+  gscan_config c;
+  gscan_config_default(&c);
+  TRY(validate(h, n, c));
+  CU(cudaSetDevice(h->device));
+  TRY(reserve(h, n));
+  CU(cudaMemsetAsync(h->ctr, 0, sizeof(Counters), h->stream));
+  TRY(stage_round1(h, d_xs, d_ys, (uint32_t)n, 1));
+  TRY(sync_counters(h));
+  *n_out = h->h_ctr->n1;
+  CU(cudaMemcpyAsync(d_out, h->surv, (size_t)h->h_ctr->n1 * 4, cudaMemcpyDeviceToDevice, h->stream));
+  CU(cudaStreamSynchronize(h->stream));
+  return GSCAN_OK;
+}
+
+int gscan_stage_sorted(gscan_handle* h, const double* d_xs, const double* d_ys, uint64_t n,
+                       uint32_t* d_out, uint64_t* len) {
+  if (!h || !d_out || !len) return GSCAN_E_INVALID;
+  gscan_config c;
+  gscan_config_default(&c);
+  TRY(validate(h, n, c));
+  CU(cudaSetDevice(h->device));
+  TRY(reserve(h, n));
+  CU(cudaMemsetAsync(h->ctr, 0, sizeof(Counters), h->stream));
+  TRY(stage_round1(h, d_xs, d_ys, (uint32_t)n, 0));
+  TRY(stage_annotate_sort(h, d_xs, d_ys, (uint32_t)n, -1, -1));
+  const uint32_t m = h->h_ctr->m_total;
+  *len = m;
+  CU(cudaMemcpyAsync(d_out, h->A_i, (size_t)m * 4, cudaMemcpyDeviceToDevice, h->stream));
+  CU(cudaStreamSynchronize(h->stream));
+  return GSCAN_OK;
+}
+
+int gscan_stage_discard(gscan_handle* h, const double* d_xs, const double* d_ys, uint64_t n,
+                        uint64_t chunk_count, int chunked, uint8_t* d_flags, uint64_t* longest,
+                        uint64_t* len) {
+  if (!h || !d_flags || !longest || !len) return GSCAN_E_INVALID;
+  gscan_config c;
+  gscan_config_default(&c);
+  c.chunk_count = chunk_count;
+  c.chunked = chunked;
+  c.enable_round1 = 0;
+  TRY(validate(h, n, c));
+  CU(cudaSetDevice(h->device));
+  TRY(reserve(h, n));
+  CU(cudaMemsetAsync(h->ctr, 0, sizeof(Counters), h->stream));
+  TRY(stage_round1(h, d_xs, d_ys, (uint32_t)n, 0));
+  TRY(stage_annotate_sort(h, d_xs, d_ys, (uint32_t)n, -1, -1));
+  const uint32_t m = h->h_ctr->m_total;
+  if (m < 2) return fail(h, GSCAN_E_INVALID, "split_regions: need at least 2 annotated points");
+  double *Rx, *Ry;
+  uint32_t* Ri;
+  TRY(stage_round2(h, c, &Rx, &Ry, &Ri));
+  CU(cudaMemcpyAsync(d_flags, h->flags, m, cudaMemcpyDeviceToDevice, h->stream));
+  CU(cudaStreamSynchronize(h->stream));
+  *longest = h->h_ctr->longest;
+  *len = m;
+  return GSCAN_OK;
+}
+
+int gscan_device_atan2(gscan_handle* h, const double* d_y, const double* d_x, double* d_out,
+                       uint64_t n) {
+  if (!h || !d_y || !d_x || !d_out) return GSCAN_E_INVALID;
+  CU(cudaSetDevice(h->device));
+  if (n) {
+    const uint32_t grid = (uint32_t)std::min<uint64_t>((n + kBlock - 1) / kBlock, h->sm_count * 16);
+    k_atan2<<<grid, kBlock, 0, h->stream>>>(d_y, d_x, d_out, n);
+    CU(cudaGetLastError());
+  }
+  CU(cudaStreamSynchronize(h->stream));
+  return GSCAN_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,825 @@
+// gScan hull kernels for sm_100a. Each kernel cites the reference stage it
+// replaces (/root/reference/proj/include/hull2d/...). Data layout in HBM is
+// SoA float64 (xs, ys) in, uint32 input indices through the pipeline.
+#pragma once
+#include <cuda_runtime.h>
+#include <float.h>
+#include <stdint.h>
+
+#include "device_common.cuh"
+
+namespace gscan {
+
+// Result of K1 (extremes + anchor), device resident.
+struct ExtResult {
+  uint32_t idx[5];  // i_minx, i_miny, i_maxx, i_maxy, anchor
+  uint32_t pad;
+  double qx[4], qy[4];
+  double ax, ay;
+};
+
+// Per-call device counters (one cache line each would be overkill; these
+// are touched by a handful of threads).
+struct Counters {
+  uint32_t n1;          // round-1 survivors
+  uint32_t tile_ticket; // dynamic tile ids for look-back kernels
+  uint32_t ext_ticket;  // last-block detection for K1
+  uint32_t dead;        // duplicates removed during the bucket sort
+  uint32_t n_oversize;  // buckets too large for the shared-memory sort
+  uint32_t n2;          // round-2 survivors
+  uint32_t hull;        // hull size
+  uint32_t longest;     // split_regions().longest (buffer position)
+  uint32_t m_total;     // annotated buffer size M (anchor included)
+  uint32_t graham_fail; // certificate failures (diagnostics)
+  uint32_t anchor_dups; // survivors coinciding with the anchor
+  uint32_t pad[5];
+};
+
+// ===========================================================================
+// K1: find_extremes (prefilter.hpp:28-39) + select_anchor (angular.hpp:40-49)
+// in one pass. Strict compares with lowest-index ties. The global lowest
+// point is select_anchor(round-1 survivors) as well: it can never be strictly
+// inside the quadrilateral, and compaction keeps order.
+struct ExtAcc {
+  double minx, miny, maxx, maxy, ly, lx;
+  uint32_t iminx, iminy, imaxx, imaxy, il;
+};
+
+__device__ __forceinline__ void ext_init(ExtAcc& a) {
+  a.minx = a.miny = a.ly = a.lx = DBL_MAX;
+  a.maxx = a.maxy = -DBL_MAX;
+  a.iminx = a.iminy = a.imaxx = a.imaxy = a.il = 0xffffffffu;
+}
+
+// Within one thread indices only grow, so strict compares keep the first.
+__device__ __forceinline__ void ext_push(ExtAcc& a, double x, double y, uint32_t i) {
+  if (x < a.minx || a.iminx == 0xffffffffu) { a.minx = x; a.iminx = i; }
+  if (y < a.miny || a.iminy == 0xffffffffu) { a.miny = y; a.iminy = i; }
+  if (x > a.maxx || a.imaxx == 0xffffffffu) { a.maxx = x; a.imaxx = i; }
+  if (y > a.maxy || a.imaxy == 0xffffffffu) { a.maxy = y; a.imaxy = i; }
+  if (a.il == 0xffffffffu || y < a.ly || (y == a.ly && x < a.lx)) { a.ly = y; a.lx = x; a.il = i; }
+}
+
+__device__ __forceinline__ bool arg_better_min(double v, uint32_t i, double bv, uint32_t bi) {
+  if (i == 0xffffffffu) return false;
+  if (bi == 0xffffffffu) return true;
+  return v < bv || (v == bv && i < bi);
+}
+__device__ __forceinline__ bool arg_better_max(double v, uint32_t i, double bv, uint32_t bi) {
+  if (i == 0xffffffffu) return false;
+  if (bi == 0xffffffffu) return true;
+  return v > bv || (v == bv && i < bi);
+}
+
+__device__ __forceinline__ void ext_merge(ExtAcc& a, const ExtAcc& b) {
+  if (arg_better_min(b.minx, b.iminx, a.minx, a.iminx)) { a.minx = b.minx; a.iminx = b.iminx; }
+  if (arg_better_min(b.miny, b.iminy, a.miny, a.iminy)) { a.miny = b.miny; a.iminy = b.iminy; }
+  if (arg_better_max(b.maxx, b.imaxx, a.maxx, a.imaxx)) { a.maxx = b.maxx; a.imaxx = b.imaxx; }
+  if (arg_better_max(b.maxy, b.imaxy, a.maxy, a.imaxy)) { a.maxy = b.maxy; a.imaxy = b.imaxy; }
+  bool take = false;
+  if (b.il != 0xffffffffu) {
+    if (a.il == 0xffffffffu) take = true;
+    else if (b.ly < a.ly) take = true;
+    else if (b.ly == a.ly && (b.lx < a.lx || (b.lx == a.lx && b.il < a.il))) take = true;
+  }
+  if (take) { a.ly = b.ly; a.lx = b.lx; a.il = b.il; }
+}
+
+__device__ __forceinline__ ExtAcc ext_shfl(const ExtAcc& a, int o) {
+  ExtAcc b;
+  b.minx = __shfl_xor_sync(0xffffffffu, a.minx, o);
+  b.miny = __shfl_xor_sync(0xffffffffu, a.miny, o);
+  b.maxx = __shfl_xor_sync(0xffffffffu, a.maxx, o);
+  b.maxy = __shfl_xor_sync(0xffffffffu, a.maxy, o);
+  b.ly = __shfl_xor_sync(0xffffffffu, a.ly, o);
+  b.lx = __shfl_xor_sync(0xffffffffu, a.lx, o);
+  b.iminx = __shfl_xor_sync(0xffffffffu, a.iminx, o);
+  b.iminy = __shfl_xor_sync(0xffffffffu, a.iminy, o);
+  b.imaxx = __shfl_xor_sync(0xffffffffu, a.imaxx, o);
+  b.imaxy = __shfl_xor_sync(0xffffffffu, a.imaxy, o);
+  b.il = __shfl_xor_sync(0xffffffffu, a.il, o);
+  return b;
+}
+
+// Grid-stride over 128-bit pairs of (xs, ys) with 4 pairs in flight per
+// thread; block partials are reduced by the last CTA to finish.
+template <bool kVec>
+__global__ void __launch_bounds__(kBlock) k_extremes(const double* __restrict__ xs,
+                                                     const double* __restrict__ ys, uint32_t n,
+                                                     ExtAcc* __restrict__ partials,
+                                                     ExtResult* __restrict__ out,
+                                                     Counters* __restrict__ ctr) {
+  ExtAcc acc;
+  ext_init(acc);
+  const uint32_t tid = blockIdx.x * kBlock + threadIdx.x;
+  const uint32_t nthreads = gridDim.x * kBlock;
+  if (kVec) {
+    const double2* x2 = reinterpret_cast<const double2*>(xs);
+    const double2* y2 = reinterpret_cast<const double2*>(ys);
+    const uint32_t npairs = n / 2;
+    uint32_t p = tid;
+    for (; p + 3 * nthreads < npairs; p += 4 * nthreads) {
+      double2 vx[4], vy[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        vx[u] = __ldcs(&x2[p + u * nthreads]);
+        vy[u] = __ldcs(&y2[p + u * nthreads]);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t i = 2 * (p + u * nthreads);
+        ext_push(acc, vx[u].x, vy[u].x, i);
+        ext_push(acc, vx[u].y, vy[u].y, i + 1);
+      }
+    }
+    for (; p < npairs; p += nthreads) {
+      const double2 vx = __ldcs(&x2[p]), vy = __ldcs(&y2[p]);
+      ext_push(acc, vx.x, vy.x, 2 * p);
+      ext_push(acc, vx.y, vy.y, 2 * p + 1);
+    }
+    if ((n & 1) && tid == 0) ext_push(acc, xs[n - 1], ys[n - 1], n - 1);
+  } else {
+    for (uint32_t i = tid; i < n; i += nthreads) ext_push(acc, xs[i], ys[i], i);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ext_merge(acc, ext_shfl(acc, o));
+  __shared__ ExtAcc s_w[kWarps];
+  __shared__ bool s_last;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) s_w[warp] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < kWarps; ++w) ext_merge(acc, s_w[w]);
+    partials[blockIdx.x] = acc;
+    __threadfence();
+    const uint32_t t = atomicAdd(&ctr->ext_ticket, 1u);
+    s_last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  // last CTA: reduce all partials
+  __threadfence();
+  ExtAcc a;
+  ext_init(a);
+  for (uint32_t b = threadIdx.x; b < gridDim.x; b += kBlock) {
+    ExtAcc pb;
+    const volatile ExtAcc* vp = &partials[b];
+    pb.minx = vp->minx; pb.miny = vp->miny; pb.maxx = vp->maxx; pb.maxy = vp->maxy;
+    pb.ly = vp->ly; pb.lx = vp->lx;
+    pb.iminx = vp->iminx; pb.iminy = vp->iminy; pb.imaxx = vp->imaxx; pb.imaxy = vp->imaxy;
+    pb.il = vp->il;
+    ext_merge(a, pb);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ext_merge(a, ext_shfl(a, o));
+  __syncthreads();
+  if (lane == 0) s_w[warp] = a;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < kWarps; ++w) ext_merge(a, s_w[w]);
+    out->idx[0] = a.iminx; out->idx[1] = a.iminy; out->idx[2] = a.imaxx; out->idx[3] = a.imaxy;
+    out->idx[4] = a.il;
+    for (int k = 0; k < 4; ++k) { out->qx[k] = xs[out->idx[k]]; out->qy[k] = ys[out->idx[k]]; }
+    out->ax = a.lx;
+    out->ay = a.ly;
+    ctr->ext_ticket = 0;  // ready for the next launch
+  }
+}
+
+// ===========================================================================
+// K2: classify_quad (prefilter.hpp:47-63) fused with the stable compaction
+// `compact` (prefilter.hpp:65-76). Each tile of 4096 points is read exactly
+// once (128-bit loads), ranked with warp ballots, and its survivors' input
+// indices are placed with a decoupled look-back; no flag array exists.
+constexpr int kFilterPairs = 8;  // double2 per thread -> 16 points per thread
+constexpr int kFilterTile = kBlock * kFilterPairs * 2;
+
+__device__ __forceinline__ bool quad_keep(const double* qx, const double* qy, const double* ex,
+                                          const double* ey, double x, double y) {
+  // flag 0 iff strictly Left of all four directed edges (short-circuit as in
+  // the reference; the result is the same either way)
+  if (!(cross_edge(qx[0], qy[0], ex[0], ey[0], x, y) > 0.0)) return true;
+  if (!(cross_edge(qx[1], qy[1], ex[1], ey[1], x, y) > 0.0)) return true;
+  if (!(cross_edge(qx[2], qy[2], ex[2], ey[2], x, y) > 0.0)) return true;
+  if (!(cross_edge(qx[3], qy[3], ex[3], ey[3], x, y) > 0.0)) return true;
+  return false;
+}
+
+template <bool kVec>
+__global__ void __launch_bounds__(kBlock) k_filter_compact(
+    const double* __restrict__ xs, const double* __restrict__ ys, uint32_t n,
+    const ExtResult* __restrict__ ext, int enable_round1, uint64_t* __restrict__ status,
+    uint32_t* __restrict__ out_idx, Counters* __restrict__ ctr) {
+  __shared__ uint32_t s_tile;
+  __shared__ uint32_t s_cnt[kFilterPairs][kWarps];
+  __shared__ uint32_t s_excl, s_total;
+  __shared__ uint32_t s_out[kFilterTile];
+  if (threadIdx.x == 0) s_tile = atomicAdd(&ctr->tile_ticket, 1u);
+  double qx[4], qy[4], ex[4], ey[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) { qx[k] = ext->qx[k]; qy[k] = ext->qy[k]; }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {  // edge q_k -> q_{k+1}, same subtraction as cross()
+    ex[k] = __dsub_rn(qx[(k + 1) & 3], qx[k]);
+    ey[k] = __dsub_rn(qy[(k + 1) & 3], qy[k]);
+  }
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const uint32_t base = tile * (uint32_t)kFilterTile;  // first point of the tile
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t lt = lanemask_lt();
+
+  uint32_t b0[kFilterPairs], b1[kFilterPairs];
+  if (kVec) {
+    const double2* x2 = reinterpret_cast<const double2*>(xs);
+    const double2* y2 = reinterpret_cast<const double2*>(ys);
+    double2 vx[kFilterPairs], vy[kFilterPairs];
+#pragma unroll
+    for (int k = 0; k < kFilterPairs; ++k) {
+      const uint32_t i0 = base + 2u * (k * kBlock + threadIdx.x);
+      if (i0 + 1 < n) {
+        vx[k] = __ldcs(&x2[i0 >> 1]);
+        vy[k] = __ldcs(&y2[i0 >> 1]);
+      } else if (i0 < n) {
+        vx[k].x = xs[i0]; vy[k].x = ys[i0]; vx[k].y = 0.0; vy[k].y = 0.0;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kFilterPairs; ++k) {
+      const uint32_t i0 = base + 2u * (k * kBlock + threadIdx.x);
+      const bool k0 = i0 < n && (!enable_round1 || quad_keep(qx, qy, ex, ey, vx[k].x, vy[k].x));
+      const bool k1 =
+          i0 + 1 < n && (!enable_round1 || quad_keep(qx, qy, ex, ey, vx[k].y, vy[k].y));
+      b0[k] = __ballot_sync(0xffffffffu, k0);
+      b1[k] = __ballot_sync(0xffffffffu, k1);
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < kFilterPairs; ++k) {
+      const uint32_t i0 = base + 2u * (k * kBlock + threadIdx.x);
+      bool k0 = false, k1 = false;
+      if (i0 < n) k0 = !enable_round1 || quad_keep(qx, qy, ex, ey, xs[i0], ys[i0]);
+      if (i0 + 1 < n) k1 = !enable_round1 || quad_keep(qx, qy, ex, ey, xs[i0 + 1], ys[i0 + 1]);
+      b0[k] = __ballot_sync(0xffffffffu, k0);
+      b1[k] = __ballot_sync(0xffffffffu, k1);
+    }
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < kFilterPairs; ++k) s_cnt[k][warp] = __popc(b0[k]) + __popc(b1[k]);
+  }
+  __syncthreads();
+  // exclusive scan of the 64 (stripe, warp) counts in point order, by warp 0
+  if (warp == 0) {
+    uint32_t v0 = s_cnt[lane >> 3][lane & 7];
+    uint32_t v1 = s_cnt[4 + (lane >> 3)][lane & 7];
+    uint32_t x0 = v0, x1 = v1;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y0 = __shfl_up_sync(0xffffffffu, x0, o);
+      const uint32_t y1 = __shfl_up_sync(0xffffffffu, x1, o);
+      if (lane >= o) { x0 += y0; x1 += y1; }
+    }
+    const uint32_t tot0 = __shfl_sync(0xffffffffu, x0, 31);
+    const uint32_t tot1 = __shfl_sync(0xffffffffu, x1, 31);
+    s_cnt[lane >> 3][lane & 7] = x0 - v0;
+    s_cnt[4 + (lane >> 3)][lane & 7] = tot0 + x1 - v1;
+    const uint32_t agg = tot0 + tot1;
+    const uint64_t excl = lookback_exclusive(status, tile, agg);
+    if (lane == 0) {
+      s_excl = (uint32_t)excl;
+      s_total = agg;
+      if (base + kFilterTile >= n) ctr->n1 = (uint32_t)(excl + agg);  // last tile
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < kFilterPairs; ++k) {
+    const uint32_t i0 = base + 2u * (k * kBlock + threadIdx.x);
+    uint32_t r = s_cnt[k][warp] + __popc(b0[k] & lt) + __popc(b1[k] & lt);
+    if (b0[k] & (1u << lane)) s_out[r++] = i0;
+    if (b1[k] & (1u << lane)) s_out[r] = i0 + 1;
+  }
+  __syncthreads();
+  const uint32_t total = s_total, off = s_excl;
+  for (uint32_t r = threadIdx.x; r < total; r += kBlock) out_idx[off + r] = s_out[r];
+}
+
+// ===========================================================================
+// K3: polar keys (annotate's key map, angular.hpp:135-146 / polar_key,
+// geom.hpp:38-43) for every round-1 survivor, with the anchor coincidence
+// test (geom.hpp:39) and a bucket histogram for the angle sort. The key is
+// the bit pattern of glibc's atan2 result (angles lie in [0, pi] because the
+// anchor is the lowest point; -0.0 is folded onto +0.0 so it ties with 0.0 as
+// in the reference's double compare). Monotone bucket map: floor(angle*B/pi).
+__device__ __forceinline__ uint32_t bucket_of(uint64_t key, double scale, uint32_t nb) {
+  const double b = __dmul_rn(bitsd(key), scale);
+  const uint32_t bi = (uint32_t)b;
+  return bi < nb ? bi : nb - 1;
+}
+
+__global__ void __launch_bounds__(kBlock) k_keys(const double* __restrict__ xs,
+                                                 const double* __restrict__ ys,
+                                                 const uint32_t* __restrict__ surv,
+                                                 const ExtResult* __restrict__ ext,
+                                                 const Counters* __restrict__ ctr_in,
+                                                 uint64_t* __restrict__ keys,
+                                                 uint32_t* __restrict__ hist, double scale,
+                                                 uint32_t nb, Counters* __restrict__ ctr) {
+  const uint32_t n1 = ctr_in->n1;
+  const double ax = ext->ax, ay = ext->ay;
+  uint32_t drops = 0;
+  for (uint32_t j = blockIdx.x * kBlock + threadIdx.x; j < n1; j += gridDim.x * kBlock) {
+    const uint32_t i = surv[j];
+    const double x = xs[i], y = ys[i];
+    uint64_t key;
+    uint32_t b;
+    if (x == ax && y == ay) {
+      key = kKeyDrop;
+      b = nb;
+      ++drops;
+    } else {
+      const double dx = __dsub_rn(x, ax), dy = __dsub_rn(y, ay);
+      const double ang = glibc_atan2(dy, dx);
+      key = (ang == 0.0) ? 0ull : dbits(ang);
+      b = bucket_of(key, scale, nb);
+    }
+    keys[j] = key;
+    // warp-aggregated histogram increment
+    const uint32_t active = __activemask();
+    const uint32_t peers = __match_any_sync(active, b);
+    const int leader = __ffs(peers) - 1;
+    if ((threadIdx.x & 31) == leader) atomicAdd(&hist[b], (uint32_t)__popc(peers));
+  }
+  if (drops) atomicAdd(&ctr->anchor_dups, drops);
+}
+
+// ===========================================================================
+// Device-wide exclusive scan of uint32 counts (decoupled look-back); used for
+// bucket offsets. out[i] = sum(in[0..i)); out[n] = total when n_out > n.
+constexpr int kScanItems = 8;
+constexpr int kScanTile = kBlock * kScanItems;
+
+__global__ void __launch_bounds__(kBlock) k_scan_u32(const uint32_t* __restrict__ in, uint32_t n,
+                                                     uint32_t* __restrict__ out,
+                                                     uint64_t* __restrict__ status,
+                                                     Counters* __restrict__ ctr) {
+  __shared__ uint32_t s_tile, s_warp[kWarps], s_excl;
+  if (threadIdx.x == 0) s_tile = atomicAdd(&ctr->tile_ticket, 1u);
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const uint32_t base = tile * kScanTile + threadIdx.x * kScanItems;
+  uint32_t v[kScanItems];
+  uint32_t sum = 0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    v[k] = (base + k < n) ? in[base + k] : 0u;
+    sum += v[k];
+  }
+  uint32_t total;
+  const uint32_t texcl = block_exclusive_scan(sum, s_warp, &total);
+  if (threadIdx.x < 32) {
+    const uint64_t e = lookback_exclusive(status, tile, total);
+    if (threadIdx.x == 0) s_excl = (uint32_t)e;
+  }
+  __syncthreads();
+  uint32_t run = s_excl + texcl;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    if (base + k <= n) out[base + k] = run;  // out[n] = grand total
+    run += v[k];
+  }
+}
+
+// Scatter keys into their buckets (positions claimed with atomics; the order
+// inside a bucket is fixed afterwards by a total-order sort).
+__global__ void __launch_bounds__(kBlock) k_scatter(const uint64_t* __restrict__ keys,
+                                                    const uint32_t* __restrict__ surv,
+                                                    const Counters* __restrict__ ctr,
+                                                    uint32_t* __restrict__ cursor, double scale,
+                                                    uint32_t nb, uint64_t* __restrict__ bkey,
+                                                    uint32_t* __restrict__ bval) {
+  const uint32_t n1 = ctr->n1;
+  for (uint32_t j = blockIdx.x * kBlock + threadIdx.x; j < n1; j += gridDim.x * kBlock) {
+    const uint64_t key = keys[j];
+    if (key == kKeyDrop) continue;
+    const uint32_t b = bucket_of(key, scale, nb);
+    const uint32_t pos = atomicAdd(&cursor[b], 1u);
+    bkey[pos] = key;
+    bval[pos] = surv[j];
+  }
+}
+
+// ===========================================================================
+// K4: per-bucket total-order sort = sort_by_angle's stable (angle, dist2)
+// order (angular.hpp:154-194) with the input index as the final tie-break
+// (equivalent to stability over the index-ordered survivors), plus annotate's
+// dedup (angular.hpp:118-133): exact duplicates share (angle, dist2), so the
+// later occurrences inside an equal-key run are dropped.
+// Writes the annotated buffer (positions 1.. ; 0 is the anchor).
+constexpr int kSortBlock = 128;
+constexpr int kSortCap = 2048;
+
+struct BucketBest {  // per-bucket farthest point for split_regions
+  uint64_t d2bits;
+  uint32_t pos;
+  uint32_t pad;
+};
+
+__device__ __forceinline__ bool key_less(uint64_t ka, double da, uint32_t ia, uint64_t kb,
+                                         double db, uint32_t ib) {
+  if (ka != kb) return ka < kb;
+  if (da != db) return da < db;
+  return ia < ib;
+}
+
+__global__ void __launch_bounds__(kSortBlock) k_bucket_sort(
+    const double* __restrict__ xs, const double* __restrict__ ys,
+    const uint32_t* __restrict__ bstart, const uint64_t* __restrict__ bkey,
+    const uint32_t* __restrict__ bval, const ExtResult* __restrict__ ext, uint32_t nb,
+    double* __restrict__ A_x, double* __restrict__ A_y, uint32_t* __restrict__ A_idx,
+    BucketBest* __restrict__ best, uint32_t* __restrict__ oversize, Counters* __restrict__ ctr) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint64_t* s_key = reinterpret_cast<uint64_t*>(smem);
+  double* s_d2 = reinterpret_cast<double*>(s_key + kSortCap);
+  uint32_t* s_idx = reinterpret_cast<uint32_t*>(s_d2 + kSortCap);
+  uint32_t* s_rank = s_idx + kSortCap;
+  __shared__ uint64_t s_bd2[kSortBlock / 32];
+  __shared__ uint32_t s_bpos[kSortBlock / 32];
+  __shared__ uint32_t s_dead;
+  const uint32_t b = blockIdx.x;
+  const uint32_t start = bstart[b], end = bstart[b + 1];
+  const uint32_t s = end - start;
+  if (threadIdx.x == 0) best[b].d2bits = 0, best[b].pos = 0xffffffffu;
+  if (s == 0) return;
+  if (s > (uint32_t)kSortCap) {
+    if (threadIdx.x == 0) {
+      const uint32_t k = atomicAdd(&ctr->n_oversize, 1u);
+      oversize[k] = b;
+    }
+    return;
+  }
+  const double ax = ext->ax, ay = ext->ay;
+  if (threadIdx.x == 0) s_dead = 0;
+  for (uint32_t k = threadIdx.x; k < s; k += kSortBlock) {
+    const uint32_t i = bval[start + k];
+    s_key[k] = bkey[start + k];
+    s_idx[k] = i;
+    s_d2[k] = dist2_rn(__dsub_rn(xs[i], ax), __dsub_rn(ys[i], ay));
+  }
+  __syncthreads();
+  // rank sort: rank(e) = #{j : j < e in (key, dist2, idx)}
+  for (uint32_t e = threadIdx.x; e < s; e += kSortBlock) {
+    const uint64_t ke = s_key[e];
+    const double de = s_d2[e];
+    const uint32_t ie = s_idx[e];
+    uint32_t r = 0;
+    for (uint32_t j = 0; j < s; ++j) {
+      const uint64_t kj = s_key[j];
+      r += (kj < ke) || (kj == ke && (s_d2[j] < de || (s_d2[j] == de && s_idx[j] < ie)));
+    }
+    s_rank[r] = e;
+  }
+  __syncthreads();
+  uint64_t my_best = 0;
+  uint32_t my_pos = 0xffffffffu;
+  uint32_t dead = 0;
+  for (uint32_t r = threadIdx.x; r < s; r += kSortBlock) {
+    const uint32_t e = s_rank[r];
+    const uint32_t i = s_idx[e];
+    const double x = xs[i], y = ys[i];
+    bool is_dead = false;
+    // duplicates: earlier entries of the same (key, dist2) run with equal coords
+    for (int32_t q = (int32_t)r - 1; q >= 0; --q) {
+      const uint32_t f = s_rank[q];
+      if (s_key[f] != s_key[e] || s_d2[f] != s_d2[e]) break;
+      const uint32_t fi = s_idx[f];
+      if (xs[fi] == x && ys[fi] == y) { is_dead = true; break; }
+    }
+    const uint32_t pos = 1 + start + r;
+    A_x[pos] = x;
+    A_y[pos] = y;
+    A_idx[pos] = is_dead ? kDead : i;
+    if (is_dead) {
+      ++dead;
+    } else {
+      const uint64_t d2b = dbits(s_d2[e]);
+      if (d2b > my_best || (d2b == my_best && pos < my_pos)) { my_best = d2b; my_pos = pos; }
+    }
+  }
+  // block argmax of dist2, first position on ties
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const uint64_t ob = __shfl_xor_sync(0xffffffffu, my_best, o);
+    const uint32_t op = __shfl_xor_sync(0xffffffffu, my_pos, o);
+    if (ob > my_best || (ob == my_best && op < my_pos)) { my_best = ob; my_pos = op; }
+  }
+  if ((threadIdx.x & 31) == 0) { s_bd2[threadIdx.x >> 5] = my_best; s_bpos[threadIdx.x >> 5] = my_pos; }
+  if (dead) atomicAdd(&s_dead, dead);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint64_t bb = s_bd2[0];
+    uint32_t bp = s_bpos[0];
+    for (int w = 1; w < kSortBlock / 32; ++w)
+      if (s_bd2[w] > bb || (s_bd2[w] == bb && s_bpos[w] < bp)) { bb = s_bd2[w]; bp = s_bpos[w]; }
+    best[b].d2bits = bb;
+    best[b].pos = bp;
+    if (s_dead) atomicAdd(&ctr->dead, s_dead);
+  }
+}
+
+// Fallback for buckets larger than the shared-memory capacity (degenerate
+// inputs with long equal-angle runs): heap sort in global memory by one
+// thread per bucket, then the same dedup / write-out. Correct, not fast.
+__device__ __forceinline__ bool glob_less(const uint64_t* k, const uint32_t* v, const double* xs,
+                                          const double* ys, double ax, double ay, uint32_t a,
+                                          uint32_t b) {
+  if (k[a] != k[b]) return k[a] < k[b];
+  const double da = dist2_rn(__dsub_rn(xs[v[a]], ax), __dsub_rn(ys[v[a]], ay));
+  const double db = dist2_rn(__dsub_rn(xs[v[b]], ax), __dsub_rn(ys[v[b]], ay));
+  if (da != db) return da < db;
+  return v[a] < v[b];
+}
+
+__global__ void k_bucket_sort_big(const double* __restrict__ xs, const double* __restrict__ ys,
+                                  const uint32_t* __restrict__ bstart, uint64_t* bkey,
+                                  uint32_t* bval, const ExtResult* __restrict__ ext,
+                                  const uint32_t* __restrict__ oversize,
+                                  const Counters* __restrict__ ctr_in, double* __restrict__ A_x,
+                                  double* __restrict__ A_y, uint32_t* __restrict__ A_idx,
+                                  BucketBest* __restrict__ best, Counters* __restrict__ ctr) {
+  const uint32_t nov = ctr_in->n_oversize;
+  const double ax = ext->ax, ay = ext->ay;
+  for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < nov; w += gridDim.x * blockDim.x) {
+    const uint32_t b = oversize[w];
+    const uint32_t start = bstart[b], s = bstart[b + 1] - start;
+    uint64_t* k = bkey + start;
+    uint32_t* v = bval + start;
+    // heap sort ascending
+    auto sift = [&](uint32_t root, uint32_t len) {
+      while (true) {
+        uint32_t c = 2 * root + 1;
+        if (c >= len) break;
+        if (c + 1 < len && glob_less(k, v, xs, ys, ax, ay, c, c + 1)) ++c;
+        if (!glob_less(k, v, xs, ys, ax, ay, root, c)) break;
+        const uint64_t tk = k[root]; k[root] = k[c]; k[c] = tk;
+        const uint32_t tv = v[root]; v[root] = v[c]; v[c] = tv;
+        root = c;
+      }
+    };
+    for (int64_t r = (int64_t)s / 2 - 1; r >= 0; --r) sift((uint32_t)r, s);
+    for (uint32_t len = s; len > 1; --len) {
+      const uint64_t tk = k[0]; k[0] = k[len - 1]; k[len - 1] = tk;
+      const uint32_t tv = v[0]; v[0] = v[len - 1]; v[len - 1] = tv;
+      sift(0, len - 1);
+    }
+    uint64_t bb = 0;
+    uint32_t bp = 0xffffffffu, dead = 0;
+    uint32_t run_start = 0;
+    for (uint32_t r = 0; r < s; ++r) {
+      const uint32_t i = v[r];
+      const double x = xs[i], y = ys[i];
+      const double d2 = dist2_rn(__dsub_rn(x, ax), __dsub_rn(y, ay));
+      if (r > 0) {
+        const uint32_t pi = v[r - 1];
+        const double pd2 = dist2_rn(__dsub_rn(xs[pi], ax), __dsub_rn(ys[pi], ay));
+        if (k[r - 1] != k[r] || pd2 != d2) run_start = r;
+      }
+      bool is_dead = false;
+      for (uint32_t q = run_start; q < r; ++q)
+        if (xs[v[q]] == x && ys[v[q]] == y) { is_dead = true; break; }
+      const uint32_t pos = 1 + start + r;
+      A_x[pos] = x;
+      A_y[pos] = y;
+      A_idx[pos] = is_dead ? kDead : i;
+      if (is_dead) ++dead;
+      else if (dbits(d2) > bb || bp == 0xffffffffu) { bb = dbits(d2); bp = pos; }
+    }
+    best[b].d2bits = bb;
+    best[b].pos = bp;
+    if (dead) atomicAdd(&ctr->dead, dead);
+  }
+}
+
+// Anchor into position 0 of the annotated buffer, M = 1 + sorted count.
+__global__ void k_put_anchor(const ExtResult* __restrict__ ext, const uint32_t* __restrict__ bstart,
+                             uint32_t nb, double* A_x, double* A_y, uint32_t* A_idx,
+                             Counters* __restrict__ ctr) {
+  A_x[0] = ext->ax;
+  A_y[0] = ext->ay;
+  A_idx[0] = ext->idx[4];
+  ctr->m_total = 1 + bstart[nb];
+}
+
+// split_regions (angular.hpp:197-204): first position >= 1 with maximal
+// dist2, from the per-bucket bests (buckets are in position order).
+__global__ void __launch_bounds__(1024) k_longest(const BucketBest* __restrict__ best,
+                                                  uint32_t nb, Counters* __restrict__ ctr) {
+  uint64_t bb = 0;
+  uint32_t bp = 0xffffffffu;
+  for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) {
+    const BucketBest r = best[b];
+    if (r.pos == 0xffffffffu) continue;
+    if (bp == 0xffffffffu || r.d2bits > bb || (r.d2bits == bb && r.pos < bp)) {
+      bb = r.d2bits; bp = r.pos;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const uint64_t ob = __shfl_xor_sync(0xffffffffu, bb, o);
+    const uint32_t op = __shfl_xor_sync(0xffffffffu, bp, o);
+    if (op != 0xffffffffu && (bp == 0xffffffffu || ob > bb || (ob == bb && op < bp))) {
+      bb = ob; bp = op;
+    }
+  }
+  __shared__ uint64_t s_b[32];
+  __shared__ uint32_t s_p[32];
+  if ((threadIdx.x & 31) == 0) { s_b[threadIdx.x >> 5] = bb; s_p[threadIdx.x >> 5] = bp; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+      if (s_p[w] != 0xffffffffu && (bp == 0xffffffffu || s_b[w] > bb || (s_b[w] == bb && s_p[w] < bp))) {
+        bb = s_b[w]; bp = s_p[w];
+      }
+    }
+    ctr->longest = bp;
+  }
+}
+
+// Position-wise split_regions over a compacted buffer (used after duplicates
+// were removed, when bucket positions shifted).
+__global__ void k_longest_scan(const double* __restrict__ A_x, const double* __restrict__ A_y,
+                               uint32_t m, unsigned long long* __restrict__ best_bits,
+                               uint32_t* __restrict__ best_pos, int phase) {
+  const double ax = A_x[0], ay = A_y[0];
+  for (uint32_t p = 1 + blockIdx.x * blockDim.x + threadIdx.x; p < m; p += gridDim.x * blockDim.x) {
+    const double d2 = dist2_rn(__dsub_rn(A_x[p], ax), __dsub_rn(A_y[p], ay));
+    if (phase == 0) atomicMax(best_bits, (unsigned long long)dbits(d2));
+    else if (dbits(d2) == *best_bits) atomicMin(best_pos, p);
+  }
+}
+
+// ===========================================================================
+// Stable compaction by flag (generic): keeps entries whose keep(i) is true,
+// preserving order; copies (x, y, idx) triples. Used for duplicate removal
+// (keep = idx != kDead) and for stable_compact after round 2
+// (discard.hpp:128-145, keep = flag).
+constexpr int kCompactItems = 8;
+constexpr int kCompactTile = kBlock * kCompactItems;
+
+template <int kMode>  // 0: keep idx != kDead; 1: keep flags[i] != 0
+__global__ void __launch_bounds__(kBlock) k_compact_xyi(
+    const double* __restrict__ in_x, const double* __restrict__ in_y,
+    const uint32_t* __restrict__ in_i, const uint8_t* __restrict__ flags, const uint32_t* n_dev,
+    uint32_t n_host, double* __restrict__ out_x, double* __restrict__ out_y,
+    uint32_t* __restrict__ out_i, uint64_t* __restrict__ status, Counters* __restrict__ ctr,
+    uint32_t* __restrict__ n_out) {
+  __shared__ uint32_t s_tile, s_warp[kWarps], s_excl;
+  const uint32_t n = n_dev ? *n_dev : n_host;
+  if (threadIdx.x == 0) s_tile = atomicAdd(&ctr->tile_ticket, 1u);
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const uint32_t base = tile * kCompactTile;
+  // blocked arrangement: thread t owns items base + t*kItems .. +kItems-1
+  const uint32_t first = base + threadIdx.x * kCompactItems;
+  bool keep[kCompactItems];
+  uint32_t cnt = 0;
+#pragma unroll
+  for (int k = 0; k < kCompactItems; ++k) {
+    const uint32_t i = first + k;
+    bool kp = false;
+    if (i < n) kp = (kMode == 0) ? (in_i[i] != kDead) : (flags[i] != 0);
+    keep[k] = kp;
+    cnt += kp;
+  }
+  uint32_t total;
+  const uint32_t texcl = block_exclusive_scan(cnt, s_warp, &total);
+  if (threadIdx.x < 32) {
+    const uint64_t e = lookback_exclusive(status, tile, total);
+    if (threadIdx.x == 0) {
+      s_excl = (uint32_t)e;
+      if (base + kCompactTile >= n) *n_out = (uint32_t)(e + total);
+    }
+  }
+  __syncthreads();
+  uint32_t o = s_excl + texcl;
+#pragma unroll
+  for (int k = 0; k < kCompactItems; ++k) {
+    if (keep[k]) {
+      const uint32_t i = first + k;
+      out_x[o] = in_x[i];
+      out_y[o] = in_y[i];
+      out_i[o] = in_i[i];
+      ++o;
+    }
+  }
+}
+
+// ===========================================================================
+// K5: round-2 region walks (discard.hpp:36-66, 79-124) -- one warp per slice.
+// The warp evaluates orient(temp, P_l, P_i) for 32 consecutive walk
+// positions against the current temp; every lane before the first
+// non-discarded lane is discarded (it was tested against that same temp),
+// and the first non-discarded lane becomes the new temp. Exact: identical
+// decisions to the sequential loop.
+struct SliceGeom {
+  uint32_t l;         // longest (buffer position)
+  uint32_t m;         // buffer size M
+  uint32_t chunked;
+  uint32_t n_right;   // slices in the right region
+  uint32_t n_left;    // slices in the left region
+  uint32_t step_r, step_l;
+  uint32_t pad;
+};
+
+__global__ void __launch_bounds__(kBlock) k_round2_walk(const double* __restrict__ A_x,
+                                                        const double* __restrict__ A_y,
+                                                        SliceGeom g, uint8_t* __restrict__ flags) {
+  const uint32_t slice = (blockIdx.x * kBlock + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (slice >= g.n_right + g.n_left) return;
+  uint32_t seed, start, count;
+  int dir;
+  if (slice < g.n_right) {
+    dir = 1;
+    if (g.chunked) {
+      const uint32_t begin = 1 + slice * g.step_r;
+      const uint32_t end = min(begin + g.step_r, g.l);
+      seed = begin; start = begin + 1; count = end - begin - 1;
+    } else {
+      seed = 0; start = 1; count = g.l - 1;
+    }
+  } else {
+    dir = -1;
+    const uint32_t s = slice - g.n_right;
+    const uint32_t m_left = g.m - 1 - g.l;
+    if (g.chunked) {
+      const uint32_t pos = s * g.step_l;
+      seed = g.m - 1 - pos;
+      const uint32_t off = min(pos + g.step_l - 1, m_left - 1);
+      const uint32_t lo = g.m - 1 - off;
+      start = seed - 1; count = seed - lo;
+    } else {
+      seed = g.m - 1; start = g.m - 2; count = g.m - 2 - g.l;
+    }
+  }
+  const double lx = A_x[g.l], ly = A_y[g.l];
+  double tx = A_x[seed], ty = A_y[seed];
+  uint32_t i = 0;
+  while (i < count) {
+    const uint32_t off = i + lane;
+    const bool valid = off < count;
+    const uint32_t pos = (dir > 0) ? start + off : start - off;
+    double px = 0.0, py = 0.0;
+    if (valid) { px = A_x[pos]; py = A_y[pos]; }
+    const double c = cross_rn(tx, ty, lx, ly, px, py);
+    const bool discard = valid && ((dir > 0) ? (c > 0.0) : (c < 0.0));
+    const uint32_t keep_mask = __ballot_sync(0xffffffffu, valid && !discard);
+    if (keep_mask == 0) {
+      if (valid) flags[pos] = 0;
+      i += 32;
+      continue;
+    }
+    const int k = __ffs(keep_mask) - 1;
+    if (lane < k) flags[pos] = 0;
+    tx = __shfl_sync(0xffffffffu, px, k);
+    ty = __shfl_sync(0xffffffffu, py, k);
+    i += k + 1;
+  }
+}
+
+// ===========================================================================
+// K7 (v1): graham_finalize (pipeline.hpp:57-67) -- the exact sequential stack
+// scan, run by one device thread (no host stage).
+__global__ void k_graham_seq(const double* __restrict__ R_x, const double* __restrict__ R_y,
+                             const uint32_t* __restrict__ R_i, const uint32_t* n_dev,
+                             uint32_t* __restrict__ stack, uint32_t* __restrict__ out_idx,
+                             Counters* __restrict__ ctr) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  const uint32_t n = *n_dev;
+  uint32_t top = 0;
+  double s1x = 0, s1y = 0, s2x = 0, s2y = 0;  // stack[top-1], stack[top-2]
+  for (uint32_t i = 0; i < n; ++i) {
+    const double px = R_x[i], py = R_y[i];
+    while (top >= 2 && !(cross_rn(s2x, s2y, s1x, s1y, px, py) > 0.0)) {
+      --top;
+      s1x = s2x; s1y = s2y;
+      if (top >= 2) { const uint32_t q = stack[top - 2]; s2x = R_x[q]; s2y = R_y[q]; }
+    }
+    stack[top++] = i;
+    s2x = s1x; s2y = s1y;
+    s1x = px; s1y = py;
+  }
+  for (uint32_t k = 0; k < top; ++k) out_idx[k] = R_i[stack[k]];
+  ctr->hull = top;
+}
+
+// Device self-check: glibc-identical atan2.
+__global__ void k_atan2(const double* __restrict__ y, const double* __restrict__ x,
+                        double* __restrict__ out, uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = glibc_atan2(y[i], x[i]);
+}
+
+}  // namespace gscan
