@@ -128,6 +128,26 @@ int gscan_stage_discard(gscan_handle* h, const double* d_xs, const double* d_ys,
                         uint64_t chunk_count, int chunked, uint8_t* d_flags, uint64_t* longest,
                         uint64_t* len);
 
+/* ---- sharded (multi-GPU) building blocks ---- */
+
+/* The five extreme points of a shard: idx[] are indices into the shard
+ * (add the shard offset for global ones), x[]/y[] their coordinates;
+ * order i_minx, i_miny, i_maxx, i_maxy, lowest (min y, then min x). */
+typedef struct gscan_extremes {
+    uint64_t idx[5];
+    double x[5];
+    double y[5];
+} gscan_extremes;
+
+/* find_extremes + lowest point of one shard (device pointers). */
+int gscan_shard_extremes(gscan_handle* h, const double* d_xs, const double* d_ys, uint64_t n,
+                         gscan_extremes* out);
+/* classify_quad + compact of one shard against the GLOBAL quadrilateral
+ * (prefilter.hpp:47-76): survivors' shard-local indices, in order, into d_out
+ * (device uint32, capacity n); *n_out = count. Only global->x/y[0..3] are read. */
+int gscan_shard_round1(gscan_handle* h, const double* d_xs, const double* d_ys, uint64_t n,
+                       const gscan_extremes* global, uint32_t* d_out, uint64_t* n_out);
+
 /* ---- device self-checks ---- */
 
 /* glibc-identical atan2 (paper_1508_05931_b200/csrc/glibc_atan2.h) on the
@@ -144,6 +164,18 @@ uint64_t gscan_last_launch_count(const gscan_handle* h);
  * order; returns the number of records (<= cap). Requires gscan_set_profiling. */
 int gscan_set_profiling(gscan_handle* h, int enabled);
 int gscan_last_kernel_times(const gscan_handle* h, const char** names, double* ms, int cap);
+
+/* ---- test hooks (exercise the certificate and fallback paths) ---- */
+enum {
+    GSCAN_DEBUG_FORCE_JUNCTION = 1u << 0,   /* Graham candidate via junction merges */
+    GSCAN_DEBUG_FORCE_SEQUENTIAL = 1u << 1, /* Graham candidate via chains-of-chains scan */
+    GSCAN_DEBUG_CORRUPT_CANDIDATE = 1u << 2,/* falsify the candidate: certificate must fail */
+    GSCAN_DEBUG_FORCE_FALLBACK = 1u << 3    /* always finish with the sequential kernel */
+};
+int gscan_set_debug(gscan_handle* h, uint32_t flags);
+/* path: 0 = sequential kernel only (tiny input), 1 = chains + certificate,
+ * 2 = junctions + certificate; bit 4 set = certificate failed or fallback forced. */
+int gscan_last_graham_info(const gscan_handle* h, uint32_t* path, uint32_t* certificate_failures);
 
 /* ---- harness helpers (host) ---- */
 enum { GSCAN_GEN_SQUARE = 0, GSCAN_GEN_DISK = 1, GSCAN_GEN_CIRCLE = 2, GSCAN_GEN_COLLINEAR = 3 };

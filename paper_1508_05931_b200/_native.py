@@ -24,6 +24,11 @@ GSCAN_E_INTERNAL = 8
 
 GEN_SQUARE, GEN_DISK, GEN_CIRCLE, GEN_COLLINEAR = 0, 1, 2, 3
 
+DEBUG_FORCE_JUNCTION = 1 << 0
+DEBUG_FORCE_SEQUENTIAL = 1 << 1
+DEBUG_CORRUPT_CANDIDATE = 1 << 2
+DEBUG_FORCE_FALLBACK = 1 << 3
+
 
 class NativeUnavailable(RuntimeError):
     """libgscan.so is not built or cannot run here (no CUDA device)."""
@@ -40,6 +45,10 @@ class gscan_stats(C.Structure):
                 ("t_round1_ms", C.c_double), ("t_annotate_ms", C.c_double),
                 ("t_sort_ms", C.c_double), ("t_round2_ms", C.c_double),
                 ("t_finalize_ms", C.c_double), ("t_total_ms", C.c_double)]
+
+
+class gscan_extremes(C.Structure):
+    _fields_ = [("idx", C.c_uint64 * 5), ("x", C.c_double * 5), ("y", C.c_double * 5)]
 
 
 # Every symbol include/gscan.h declares, with its ctypes signature.
@@ -63,10 +72,14 @@ SIGNATURES = {
     "gscan_stage_sorted": (C.c_int, [_P, _P, _P, _U64, _P, _U64P]),
     "gscan_stage_discard": (C.c_int, [_P, _P, _P, _U64, _U64, C.c_int, _P, _U64P, _U64P]),
     "gscan_device_atan2": (C.c_int, [_P, _P, _P, _P, _U64]),
+    "gscan_shard_extremes": (C.c_int, [_P, _P, _P, _U64, C.POINTER(gscan_extremes)]),
+    "gscan_shard_round1": (C.c_int, [_P, _P, _P, _U64, C.POINTER(gscan_extremes), _P, _U64P]),
     "gscan_status_string": (C.c_char_p, [C.c_int]),
     "gscan_last_error": (C.c_char_p, [_P]),
     "gscan_last_launch_count": (_U64, [_P]),
     "gscan_set_profiling": (C.c_int, [_P, C.c_int]),
+    "gscan_set_debug": (C.c_int, [_P, C.c_uint32]),
+    "gscan_last_graham_info": (C.c_int, [_P, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]),
     "gscan_last_kernel_times": (C.c_int, [_P, C.POINTER(C.c_char_p), _DP, C.c_int]),
     "gscan_generate": (C.c_int, [C.c_int, _U64, _U64, _DP, _DP]),
     "gscan_generate_grid": (C.c_int, [_U64, _U64, C.c_int, C.c_int, _DP, _DP]),

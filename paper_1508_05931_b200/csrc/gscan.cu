@@ -20,6 +20,7 @@
 
 #include "../../include/gscan.h"
 #include "kernels.cuh"
+#include "graham.cuh"
 
 using namespace gscan;
 
@@ -51,8 +52,9 @@ struct gscan_handle {
   double *d_xs = nullptr, *d_ys = nullptr;
   uint32_t* surv = nullptr;
   uint64_t* keys = nullptr;
-  uint64_t* bkey = nullptr;
-  uint32_t* bval = nullptr;
+  uint32_t* rank = nullptr;
+  KeyRec* rec_k = nullptr;
+  double2* rec_xy = nullptr;
   double *A_x = nullptr, *A_y = nullptr;
   uint32_t* A_i = nullptr;
   double *C_x = nullptr, *C_y = nullptr;
@@ -63,7 +65,13 @@ struct gscan_handle {
   uint64_t* status = nullptr;
   uint64_t status_cap = 0;
   uint32_t *hist = nullptr, *bstart = nullptr, *cursor = nullptr, *oversize = nullptr;
-  BucketBest* best = nullptr;
+  BucketBest* best = nullptr;  // per-block partials of the sort kernels
+  uint64_t best_cap = 0;
+  // Graham scratch
+  uint32_t *g_chain = nullptr, *g_len = nullptr, *g_off = nullptr, *g_q0 = nullptr, *g_q1 = nullptr;
+  uint32_t *g_parent = nullptr, *g_btop = nullptr, *g_jk = nullptr, *g_je = nullptr;
+  int32_t* g_jmin = nullptr;
+  uint32_t *g_keep = nullptr, *g_misc = nullptr;  // misc: [0] fail, [1] len, [2] q size
   ExtAcc* partials = nullptr;
   ExtResult* ext = nullptr;
   Counters* ctr = nullptr;
@@ -72,6 +80,9 @@ struct gscan_handle {
   uint32_t* h_out = nullptr;  // pinned staging for indices
   uint64_t h_out_cap = 0;
   cudaEvent_t ev[8] = {};
+  uint32_t debug = 0;  // GSCAN_DEBUG_* test hooks
+  uint32_t graham_fails = 0;
+  uint32_t graham_path = 0;  // 0 sequential kernel, 1 chains+certificate, 2 junctions+certificate
 };
 
 namespace {
@@ -101,17 +112,22 @@ void dfree(T*& p) {
 }
 
 void free_buffers(gscan_handle* h) {
-  dfree(h->d_xs); dfree(h->d_ys); dfree(h->surv); dfree(h->keys); dfree(h->bkey);
-  dfree(h->bval); dfree(h->A_x); dfree(h->A_y); dfree(h->A_i); dfree(h->C_x); dfree(h->C_y);
+  dfree(h->d_xs); dfree(h->d_ys); dfree(h->surv); dfree(h->keys); dfree(h->rank);
+  dfree(h->rec_k); dfree(h->rec_xy); dfree(h->A_x); dfree(h->A_y); dfree(h->A_i); dfree(h->C_x); dfree(h->C_y);
   dfree(h->C_i); dfree(h->flags); dfree(h->stack); dfree(h->d_out); dfree(h->status);
   dfree(h->hist); dfree(h->bstart); dfree(h->cursor); dfree(h->oversize); dfree(h->best);
+  dfree(h->g_chain); dfree(h->g_len); dfree(h->g_off); dfree(h->g_q0); dfree(h->g_q1);
+  dfree(h->g_parent); dfree(h->g_btop); dfree(h->g_jk); dfree(h->g_je); dfree(h->g_jmin);
+  dfree(h->g_keep); dfree(h->g_misc);
   h->cap = 0;
   h->nb_cap = 0;
   h->status_cap = 0;
 }
 
+constexpr uint32_t kCtaSortGrid = 296;
+
 uint32_t buckets_for(uint64_t n) {
-  uint64_t want = (n + 511) / 512;
+  uint64_t want = (n + 3) / 4;
   uint32_t nb = 1;
   while (nb < want && nb < (1u << 24)) nb <<= 1;
   return nb;
@@ -125,8 +141,9 @@ int reserve(gscan_handle* h, uint64_t n) {
   CU(cudaMalloc(&h->d_ys, m * 8));
   CU(cudaMalloc(&h->surv, m * 4));
   CU(cudaMalloc(&h->keys, m * 8));
-  CU(cudaMalloc(&h->bkey, m * 8));
-  CU(cudaMalloc(&h->bval, m * 4));
+  CU(cudaMalloc(&h->rank, m * 4));
+  CU(cudaMalloc(&h->rec_k, m * sizeof(KeyRec)));
+  CU(cudaMalloc(&h->rec_xy, m * sizeof(double2)));
   CU(cudaMalloc(&h->A_x, m * 8));
   CU(cudaMalloc(&h->A_y, m * 8));
   CU(cudaMalloc(&h->A_i, m * 4));
@@ -142,8 +159,23 @@ int reserve(gscan_handle* h, uint64_t n) {
   CU(cudaMalloc(&h->bstart, (nb + 2) * 4));
   CU(cudaMalloc(&h->cursor, (nb + 2) * 4));
   CU(cudaMalloc(&h->oversize, (nb + 2) * 4));
-  CU(cudaMalloc(&h->best, (nb + 2) * sizeof(BucketBest)));
-  const uint64_t tiles = (m + kCompactTile - 1) / kCompactTile + 64;
+  h->best_cap = (nb + kBucketsPerBlock - 1) / kBucketsPerBlock + kCtaSortGrid + 1;
+  CU(cudaMalloc(&h->best, h->best_cap * sizeof(BucketBest)));
+  const uint64_t nch = (m + kChunk - 1) / kChunk + 2;
+  CU(cudaMalloc(&h->g_chain, m * 4));
+  CU(cudaMalloc(&h->g_len, nch * 4));
+  CU(cudaMalloc(&h->g_off, (nch + 1) * 4));
+  CU(cudaMalloc(&h->g_q0, m * 4));
+  CU(cudaMalloc(&h->g_q1, m * 4));
+  CU(cudaMalloc(&h->g_parent, m * 4));
+  CU(cudaMalloc(&h->g_btop, (nch + 1) * 4));
+  CU(cudaMalloc(&h->g_jk, nch * 4));
+  CU(cudaMalloc(&h->g_je, nch * 4));
+  CU(cudaMalloc(&h->g_jmin, nch * 4));
+  CU(cudaMalloc(&h->g_keep, nch * 4));
+  CU(cudaMalloc(&h->g_misc, 64));
+  const uint64_t tiles = std::max((m + kCompactTile - 1) / kCompactTile,
+                                  (uint64_t)(nb + 2 + kScanTile - 1) / kScanTile) + 64;
   h->status_cap = tiles;
   CU(cudaMalloc(&h->status, tiles * 8));
   h->cap = n;
@@ -195,10 +227,15 @@ int sync_counters(gscan_handle* h) {
     if (rc_ != GSCAN_OK) return rc_; \
   } while (0)
 
-// K1 + K2 (round 1). Leaves survivors in h->surv and n1 in ctr.
-int stage_round1(gscan_handle* h, const double* xs, const double* ys, uint32_t n, int enable) {
+// K1 + K2 (round 1). Leaves survivors in h->surv and n1 in ctr. With
+// `quad_override` (distributed use: the quadrilateral of the GLOBAL extremes),
+// K1 is skipped and the given ExtResult is used.
+int stage_round1(gscan_handle* h, const double* xs, const double* ys, uint32_t n, int enable,
+                 const ExtResult* quad_override = nullptr) {
   const bool vec = aligned16(xs) && aligned16(ys);
-  {
+  if (quad_override) {
+    CU(cudaMemcpyAsync(h->ext, quad_override, sizeof(ExtResult), cudaMemcpyHostToDevice, h->stream));
+  } else {
     const uint32_t grid =
         std::max(1u, std::min<uint32_t>((n + kBlock * 8 - 1) / (kBlock * 8), h->sm_count * 8));
     Launch L(h, "k_extremes");
@@ -230,8 +267,8 @@ int stage_annotate_sort(gscan_handle* h, const double* xs, const double* ys, uin
   {
     const uint32_t grid = std::max(1u, std::min<uint32_t>((n + kBlock - 1) / kBlock, h->sm_count * 16));
     Launch L(h, "k_keys");
-    k_keys<<<grid, kBlock, 0, h->stream>>>(xs, ys, h->surv, h->ext, h->ctr, h->keys, h->hist,
-                                           scale, nb, h->ctr);
+    k_keys<<<grid, kBlock, 0, h->stream>>>(xs, ys, h->surv, h->ext, h->ctr, h->keys, h->rank,
+                                           h->hist, scale, nb, h->ctr);
   }
   if (t_annot_ev >= 0) CU(cudaEventRecord(h->ev[t_annot_ev], h->stream));
   const uint64_t stiles = (nb + 1 + kScanTile - 1) / kScanTile;
@@ -240,25 +277,26 @@ int stage_annotate_sort(gscan_handle* h, const double* xs, const double* ys, uin
     Launch L(h, "k_scan_u32");
     k_scan_u32<<<stiles, kBlock, 0, h->stream>>>(h->hist, nb, h->bstart, h->status, h->ctr);
   }
-  CU(cudaMemcpyAsync(h->cursor, h->bstart, nb * 4, cudaMemcpyDeviceToDevice, h->stream));
   {
     const uint32_t grid = std::max(1u, std::min<uint32_t>((n + kBlock - 1) / kBlock, h->sm_count * 16));
     Launch L(h, "k_scatter");
-    k_scatter<<<grid, kBlock, 0, h->stream>>>(h->keys, h->surv, h->ctr, h->cursor, scale, nb,
-                                              h->bkey, h->bval);
+    k_scatter<<<grid, kBlock, 0, h->stream>>>(xs, ys, h->keys, h->rank, h->surv, h->ctr,
+                                              h->bstart, scale, nb, h->rec_k, h->rec_xy);
+  }
+  const uint32_t tblocks = (nb + kBucketsPerBlock - 1) / kBucketsPerBlock;
+  {
+    const size_t smem = (size_t)kBlockCap * (8 + 8 + 8 + 8 + 4 + 2);
+    Launch L(h, "k_bucket_sort_block");
+    k_bucket_sort_block<<<tblocks, kBlock, smem, h->stream>>>(h->bstart, h->rec_k, h->rec_xy,
+                                                              h->ext, scale, nb, h->A_x, h->A_y,
+                                                              h->A_i, h->best, h->oversize, h->ctr);
   }
   {
     const size_t smem = (size_t)kSortCap * (8 + 8 + 4 + 4);
-    Launch L(h, "k_bucket_sort");
-    k_bucket_sort<<<nb, kSortBlock, smem, h->stream>>>(xs, ys, h->bstart, h->bkey, h->bval, h->ext,
-                                                       nb, h->A_x, h->A_y, h->A_i, h->best,
-                                                       h->oversize, h->ctr);
-  }
-  {
-    Launch L(h, "k_bucket_sort_big");
-    k_bucket_sort_big<<<8, 32, 0, h->stream>>>(xs, ys, h->bstart, h->bkey, h->bval, h->ext,
-                                               h->oversize, h->ctr, h->A_x, h->A_y, h->A_i,
-                                               h->best, h->ctr);
+    Launch L(h, "k_bucket_sort_cta");
+    k_bucket_sort_cta<<<kCtaSortGrid, kSortBlock, smem, h->stream>>>(
+        h->bstart, h->rec_k, h->rec_xy, h->ext, h->oversize, h->ctr, h->A_x, h->A_y, h->A_i,
+        h->best + tblocks, h->ctr);
   }
   {
     Launch L(h, "k_put_anchor");
@@ -266,7 +304,7 @@ int stage_annotate_sort(gscan_handle* h, const double* xs, const double* ys, uin
   }
   {
     Launch L(h, "k_longest");
-    k_longest<<<1, 1024, 0, h->stream>>>(h->best, nb, h->ctr);
+    k_longest<<<1, 1024, 0, h->stream>>>(h->best, tblocks + kCtaSortGrid, h->ctr);
   }
   CU(cudaGetLastError());
   TRY(sync_counters(h));
@@ -356,6 +394,108 @@ int stage_round2(gscan_handle* h, const gscan_config& cfg, double** Rx, double**
   return GSCAN_OK;
 }
 
+
+// Exclusive scan of n uint32 counts into out[0..n] (out[n] = total).
+int scan_u32(gscan_handle* h, const uint32_t* in, uint32_t n, uint32_t* out) {
+  const uint64_t tiles = (n + 1 + kScanTile - 1) / kScanTile;
+  TRY(reset_lookback(h, tiles));
+  Launch L(h, "k_scan_u32");
+  k_scan_u32<<<tiles, kBlock, 0, h->stream>>>(in, n, out, h->status, h->ctr);
+  return GSCAN_OK;
+}
+
+int read_u32(gscan_handle* h, const uint32_t* d, uint32_t* v) {
+  CU(cudaMemcpyAsync(&h->h_ctr->pad[0], d, 4, cudaMemcpyDeviceToHost, h->stream));
+  CU(cudaStreamSynchronize(h->stream));
+  *v = h->h_ctr->pad[0];
+  return GSCAN_OK;
+}
+
+// K7/K8 (graham.cuh): candidate + certificate; exact sequential fallback.
+// Leaves the hull (input indices) in h->d_out and its size in ctr->hull.
+int stage_graham(gscan_handle* h, const double* Rx, const double* Ry, const uint32_t* Ri,
+                 uint32_t N) {
+  uint32_t* fail_d = h->g_misc;
+  uint32_t* len_d = h->g_misc + 1;
+  CU(cudaMemsetAsync(h->g_misc, 0, 16, h->stream));
+  h->graham_path = 0;
+  h->graham_fails = 0;
+  if (N > 2 * kChunk) {
+    const uint32_t nch = (N + kChunk - 1) / kChunk;
+    {
+      Launch L(h, "k_graham_local");
+      k_graham_local<<<(nch + 127) / 128, 128, 0, h->stream>>>(Rx, Ry, N, h->g_chain, h->g_len);
+    }
+    bool junction_ok = false;
+    if (!(h->debug & GSCAN_DEBUG_FORCE_SEQUENTIAL)) {
+      {
+        Launch L(h, "k_graham_junction");
+        k_graham_junction<<<(nch + 127) / 128, 128, 0, h->stream>>>(Rx, Ry, h->g_chain, h->g_len,
+                                                                     nch, h->g_jk, h->g_je, h->g_jmin);
+      }
+      {
+        Launch L(h, "k_graham_junction_apply");
+        k_graham_junction_apply<<<(nch + 1 + 127) / 128, 128, 0, h->stream>>>(
+            h->g_chain, h->g_len, nch, h->g_jk, h->g_je, h->g_jmin, h->g_parent, h->g_btop,
+            h->g_keep, fail_d);
+      }
+      uint32_t jfail;
+      TRY(read_u32(h, fail_d, &jfail));
+      junction_ok = (jfail == 0) || (h->debug & GSCAN_DEBUG_FORCE_JUNCTION);
+    }
+    if (junction_ok) {
+      h->graham_path = 2;
+      TRY(scan_u32(h, h->g_keep, nch, h->g_off));
+      {
+        Launch L(h, "k_graham_junction_emit");
+        k_graham_junction_emit<<<(nch + 7) / 8, 8 * kChunk, 0, h->stream>>>(
+            h->g_chain, h->g_je, h->g_keep, h->g_off, nch, h->stack);
+      }
+      CU(cudaMemcpyAsync(len_d, h->g_off + nch, 4, cudaMemcpyDeviceToDevice, h->stream));
+    } else {
+      h->graham_path = 1;
+      CU(cudaMemsetAsync(fail_d, 0, 4, h->stream));
+      TRY(scan_u32(h, h->g_len, nch, h->g_off));
+      {
+        Launch L(h, "k_gather_chains");
+        k_gather_chains<<<(nch + 7) / 8, 8 * kChunk, 0, h->stream>>>(h->g_chain, h->g_len,
+                                                                     h->g_off, nch, h->g_q0);
+      }
+      {
+        Launch L(h, "k_graham_candidate_seq");
+        k_graham_candidate_seq<<<1, 32, 0, h->stream>>>(Rx, Ry, h->g_q0, h->g_off + nch, N,
+                                                        h->g_parent, h->g_btop, h->stack, len_d);
+      }
+    }
+    if (h->debug & GSCAN_DEBUG_CORRUPT_CANDIDATE) {
+      // drop the candidate's last boundary state: the certificate must reject it
+      CU(cudaMemcpyAsync(h->g_btop + nch, h->g_btop + nch - 1, 4, cudaMemcpyDeviceToDevice,
+                         h->stream));
+    }
+    {
+      Launch L(h, "k_graham_certify");
+      k_graham_certify<<<(nch + 127) / 128, 128, 0, h->stream>>>(Rx, Ry, N, h->g_parent, h->g_btop,
+                                                                  fail_d);
+    }
+    uint32_t fails;
+    TRY(read_u32(h, fail_d, &fails));
+    h->graham_fails = fails;
+    if (fails == 0 && !(h->debug & GSCAN_DEBUG_FORCE_FALLBACK)) {
+      Launch L(h, "k_graham_emit");
+      k_graham_emit<<<std::max(1u, std::min<uint32_t>((N + kBlock - 1) / kBlock, 1184)), kBlock, 0,
+                      h->stream>>>(h->stack, len_d, Ri, h->d_out, h->ctr);
+      CU(cudaGetLastError());
+      return GSCAN_OK;
+    }
+    h->graham_path |= 4;  // certificate failed or fallback forced
+  }
+  // small buffers, or certificate failure: exact sequential scan on the device
+  Launch L(h, "k_graham_seq");
+  k_graham_seq<<<1, 32, 0, h->stream>>>(Rx, Ry, Ri, &h->ctr->n2, h->stack, h->d_out, h->ctr);
+  CU(cudaGetLastError());
+  return GSCAN_OK;
+}
+
 int validate(gscan_handle* h, uint64_t n, const gscan_config& cfg) {
   if (!h) return GSCAN_E_INVALID;
   if (n == 0) return fail(h, GSCAN_E_EMPTY_INPUT, "full_pipeline: no points");
@@ -387,11 +527,8 @@ int run_pipeline(gscan_handle* h, const double* xs, const double* ys, uint64_t n
   uint32_t* Ri;
   TRY(stage_round2(h, cfg, &Rx, &Ry, &Ri));
   CU(cudaEventRecord(h->ev[4], h->stream));
-  {
-    Launch L(h, "k_graham_seq");
-    k_graham_seq<<<1, 32, 0, h->stream>>>(Rx, Ry, Ri, &h->ctr->n2, h->stack, h->d_out, h->ctr);
-  }
-  CU(cudaGetLastError());
+  TRY(sync_counters(h));
+  TRY(stage_graham(h, Rx, Ry, Ri, h->h_ctr->n2));
   CU(cudaEventRecord(h->ev[5], h->stream));
   TRY(sync_counters(h));
   const Counters& c = *h->h_ctr;
@@ -476,7 +613,9 @@ int gscan_create(int device, gscan_handle** out) {
     CU(cudaMalloc(&h->scratch64, 16));
     CU(cudaMallocHost(&h->h_ctr, sizeof(Counters)));
     for (auto& e : h->ev) CU(cudaEventCreate(&e));
-    CU(cudaFuncSetAttribute(k_bucket_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CU(cudaFuncSetAttribute(k_bucket_sort_block, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            kBlockCap * (8 + 8 + 8 + 8 + 4 + 2)));
+    CU(cudaFuncSetAttribute(k_bucket_sort_cta, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             kSortCap * (8 + 8 + 4 + 4)));
     return GSCAN_OK;
   };
@@ -517,6 +656,19 @@ int gscan_set_stream(gscan_handle* h, void* stream) {
     h->stream = static_cast<cudaStream_t>(stream);
     h->own_stream = false;
   }
+  return GSCAN_OK;
+}
+
+int gscan_set_debug(gscan_handle* h, uint32_t flags) {
+  if (!h) return GSCAN_E_INVALID;
+  h->debug = flags;
+  return GSCAN_OK;
+}
+
+int gscan_last_graham_info(const gscan_handle* h, uint32_t* path, uint32_t* certificate_failures) {
+  if (!h) return GSCAN_E_INVALID;
+  if (path) *path = h->graham_path;
+  if (certificate_failures) *certificate_failures = h->graham_fails;
   return GSCAN_OK;
 }
 
@@ -670,6 +822,56 @@ int gscan_stage_discard(gscan_handle* h, const double* d_xs, const double* d_ys,
   CU(cudaStreamSynchronize(h->stream));
   *longest = h->h_ctr->longest;
   *len = m;
+  return GSCAN_OK;
+}
+
+int gscan_shard_extremes(gscan_handle* h, const double* d_xs, const double* d_ys, uint64_t n,
+                         gscan_extremes* out) {
+  if (!h || !out) return GSCAN_E_INVALID;
+  gscan_config c;
+  gscan_config_default(&c);
+  TRY(validate(h, n, c));
+  CU(cudaSetDevice(h->device));
+  TRY(reserve(h, n));
+  CU(cudaMemsetAsync(h->ctr, 0, sizeof(Counters), h->stream));
+  const bool vec = aligned16(d_xs) && aligned16(d_ys);
+  const uint32_t nn = (uint32_t)n;
+  const uint32_t grid =
+      std::max(1u, std::min<uint32_t>((nn + kBlock * 8 - 1) / (kBlock * 8), h->sm_count * 8));
+  {
+    Launch L(h, "k_extremes");
+    if (vec) k_extremes<true><<<grid, kBlock, 0, h->stream>>>(d_xs, d_ys, nn, h->partials, h->ext, h->ctr);
+    else k_extremes<false><<<grid, kBlock, 0, h->stream>>>(d_xs, d_ys, nn, h->partials, h->ext, h->ctr);
+  }
+  ExtResult r;
+  CU(cudaMemcpyAsync(&r, h->ext, sizeof r, cudaMemcpyDeviceToHost, h->stream));
+  CU(cudaStreamSynchronize(h->stream));
+  for (int k = 0; k < 4; ++k) { out->idx[k] = r.idx[k]; out->x[k] = r.qx[k]; out->y[k] = r.qy[k]; }
+  out->idx[4] = r.idx[4];
+  out->x[4] = r.ax;
+  out->y[4] = r.ay;
+  return GSCAN_OK;
+}
+
+int gscan_shard_round1(gscan_handle* h, const double* d_xs, const double* d_ys, uint64_t n,
+                       const gscan_extremes* global, uint32_t* d_out, uint64_t* n_out) {
+  if (!h || !global || !d_out || !n_out) return GSCAN_E_INVALID;
+  gscan_config c;
+  gscan_config_default(&c);
+  TRY(validate(h, n, c));
+  CU(cudaSetDevice(h->device));
+  TRY(reserve(h, n));
+  CU(cudaMemsetAsync(h->ctr, 0, sizeof(Counters), h->stream));
+  ExtResult q{};
+  for (int k = 0; k < 4; ++k) { q.idx[k] = 0; q.qx[k] = global->x[k]; q.qy[k] = global->y[k]; }
+  q.ax = global->x[4];
+  q.ay = global->y[4];
+  TRY(stage_round1(h, d_xs, d_ys, (uint32_t)n, 1, &q));
+  TRY(sync_counters(h));
+  *n_out = h->h_ctr->n1;
+  if (*n_out)
+    CU(cudaMemcpyAsync(d_out, h->surv, (size_t)*n_out * 4, cudaMemcpyDeviceToDevice, h->stream));
+  CU(cudaStreamSynchronize(h->stream));
   return GSCAN_OK;
 }
 

@@ -324,10 +324,12 @@ __global__ void __launch_bounds__(kBlock) k_keys(const double* __restrict__ xs,
                                                  const ExtResult* __restrict__ ext,
                                                  const Counters* __restrict__ ctr_in,
                                                  uint64_t* __restrict__ keys,
+                                                 uint32_t* __restrict__ rank,
                                                  uint32_t* __restrict__ hist, double scale,
                                                  uint32_t nb, Counters* __restrict__ ctr) {
   const uint32_t n1 = ctr_in->n1;
   const double ax = ext->ax, ay = ext->ay;
+  const int lane = threadIdx.x & 31;
   uint32_t drops = 0;
   for (uint32_t j = blockIdx.x * kBlock + threadIdx.x; j < n1; j += gridDim.x * kBlock) {
     const uint32_t i = surv[j];
@@ -345,11 +347,14 @@ __global__ void __launch_bounds__(kBlock) k_keys(const double* __restrict__ xs,
       b = bucket_of(key, scale, nb);
     }
     keys[j] = key;
-    // warp-aggregated histogram increment
+    // warp-aggregated claim of a slot inside the bucket: rank = arrival order
     const uint32_t active = __activemask();
     const uint32_t peers = __match_any_sync(active, b);
     const int leader = __ffs(peers) - 1;
-    if ((threadIdx.x & 31) == leader) atomicAdd(&hist[b], (uint32_t)__popc(peers));
+    uint32_t base = 0;
+    if (lane == leader) base = atomicAdd(&hist[b], (uint32_t)__popc(peers));
+    base = __shfl_sync(peers, base, leader);
+    rank[j] = base + __popc(peers & lanemask_lt());
   }
   if (drops) atomicAdd(&ctr->anchor_dups, drops);
 }
@@ -391,22 +396,37 @@ __global__ void __launch_bounds__(kBlock) k_scan_u32(const uint32_t* __restrict_
   }
 }
 
-// Scatter keys into their buckets (positions claimed with atomics; the order
-// inside a bucket is fixed afterwards by a total-order sort).
-__global__ void __launch_bounds__(kBlock) k_scatter(const uint64_t* __restrict__ keys,
+// Scatter each survivor to its slot (bucket start + arrival rank from K3) as
+// two 16-byte records, (key, input index) and (x, y): two full-width random
+// stores per point, no atomics, and the sort pass then reads contiguously.
+struct KeyRec {
+  uint64_t key;
+  uint32_t idx;
+  uint32_t pad;
+};
+
+__global__ void __launch_bounds__(kBlock) k_scatter(const double* __restrict__ xs,
+                                                    const double* __restrict__ ys,
+                                                    const uint64_t* __restrict__ keys,
+                                                    const uint32_t* __restrict__ rank,
                                                     const uint32_t* __restrict__ surv,
                                                     const Counters* __restrict__ ctr,
-                                                    uint32_t* __restrict__ cursor, double scale,
-                                                    uint32_t nb, uint64_t* __restrict__ bkey,
-                                                    uint32_t* __restrict__ bval) {
+                                                    const uint32_t* __restrict__ bstart,
+                                                    double scale, uint32_t nb,
+                                                    KeyRec* __restrict__ rec_k,
+                                                    double2* __restrict__ rec_xy) {
   const uint32_t n1 = ctr->n1;
   for (uint32_t j = blockIdx.x * kBlock + threadIdx.x; j < n1; j += gridDim.x * kBlock) {
     const uint64_t key = keys[j];
     if (key == kKeyDrop) continue;
-    const uint32_t b = bucket_of(key, scale, nb);
-    const uint32_t pos = atomicAdd(&cursor[b], 1u);
-    bkey[pos] = key;
-    bval[pos] = surv[j];
+    const uint32_t i = surv[j];
+    const uint32_t pos = bstart[bucket_of(key, scale, nb)] + rank[j];
+    KeyRec r;
+    r.key = key;
+    r.idx = i;
+    r.pad = 0;
+    rec_k[pos] = r;
+    rec_xy[pos] = make_double2(xs[i], ys[i]);
   }
 }
 
@@ -418,9 +438,10 @@ __global__ void __launch_bounds__(kBlock) k_scatter(const uint64_t* __restrict__
 // later occurrences inside an equal-key run are dropped.
 // Writes the annotated buffer (positions 1.. ; 0 is the anchor).
 constexpr int kSortBlock = 128;
-constexpr int kSortCap = 2048;
+constexpr int kSortCap = 2048;   // CTA path capacity (shared memory)
+constexpr int kThreadCap = 2048; // per-bucket capacity of the block path (else K4b)
 
-struct BucketBest {  // per-bucket farthest point for split_regions
+struct BucketBest {  // farthest point candidate for split_regions
   uint64_t d2bits;
   uint32_t pos;
   uint32_t pad;
@@ -433,172 +454,240 @@ __device__ __forceinline__ bool key_less(uint64_t ka, double da, uint32_t ia, ui
   return ia < ib;
 }
 
-__global__ void __launch_bounds__(kSortBlock) k_bucket_sort(
-    const double* __restrict__ xs, const double* __restrict__ ys,
-    const uint32_t* __restrict__ bstart, const uint64_t* __restrict__ bkey,
-    const uint32_t* __restrict__ bval, const ExtResult* __restrict__ ext, uint32_t nb,
-    double* __restrict__ A_x, double* __restrict__ A_y, uint32_t* __restrict__ A_idx,
-    BucketBest* __restrict__ best, uint32_t* __restrict__ oversize, Counters* __restrict__ ctr) {
+__device__ __forceinline__ void best_merge(uint64_t& bb, uint32_t& bp, uint64_t ob, uint32_t op) {
+  if (op == 0xffffffffu) return;
+  if (bp == 0xffffffffu || ob > bb || (ob == bb && op < bp)) { bb = ob; bp = op; }
+}
+
+// Block-wide (max dist2, first position) -> partial[slot].
+template <int kThreads>
+__device__ __forceinline__ void block_best(uint64_t bb, uint32_t bp, BucketBest* partial) {
+  __shared__ uint64_t s_b[kThreads / 32];
+  __shared__ uint32_t s_p[kThreads / 32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const uint64_t ob = __shfl_xor_sync(0xffffffffu, bb, o);
+    const uint32_t op = __shfl_xor_sync(0xffffffffu, bp, o);
+    best_merge(bb, bp, ob, op);
+  }
+  if ((threadIdx.x & 31) == 0) { s_b[threadIdx.x >> 5] = bb; s_p[threadIdx.x >> 5] = bp; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < kThreads / 32; ++w) best_merge(bb, bp, s_b[w], s_p[w]);
+    partial->d2bits = bb;
+    partial->pos = bp;
+  }
+}
+
+// K4a: block-cooperative sort of 256 consecutive buckets (~2-5 keys each):
+// the block loads its buckets' records contiguously into shared memory; each
+// key's rank inside its bucket is counted against its bucket peers by the
+// total order (angle bits, dist2, input index), and a key is a duplicate iff
+// an equal point with a lower index shares its bucket (equal points always
+// share angle and dist2). Blocks whose buckets hold more than kBlockCap keys
+// defer those buckets to K4b.
+constexpr int kBucketsPerBlock = 256;
+constexpr int kBlockCap = 2048;
+
+__global__ void __launch_bounds__(kBlock) k_bucket_sort_block(
+    const uint32_t* __restrict__ bstart, const KeyRec* __restrict__ rec_k,
+    const double2* __restrict__ rec_xy, const ExtResult* __restrict__ ext, double scale,
+    uint32_t nb, double* __restrict__ A_x, double* __restrict__ A_y,
+    uint32_t* __restrict__ A_idx, BucketBest* __restrict__ partials,
+    uint32_t* __restrict__ oversize, Counters* __restrict__ ctr) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint64_t* s_key = reinterpret_cast<uint64_t*>(smem);
+  double* s_d2 = reinterpret_cast<double*>(s_key + kBlockCap);
+  double* s_x = s_d2 + kBlockCap;
+  double* s_y = s_x + kBlockCap;
+  uint32_t* s_idx = reinterpret_cast<uint32_t*>(s_y + kBlockCap);
+  uint16_t* s_lb = reinterpret_cast<uint16_t*>(s_idx + kBlockCap);
+  __shared__ uint32_t s_bs[kBucketsPerBlock + 1];
+  const uint32_t b0 = blockIdx.x * kBucketsPerBlock;
+  const uint32_t nbk = min((uint32_t)kBucketsPerBlock, nb - b0);
+  for (uint32_t t = threadIdx.x; t <= nbk; t += kBlock) s_bs[t] = bstart[b0 + t];
+  __syncthreads();
+  const uint32_t e0 = s_bs[0], cnt = s_bs[nbk] - e0;
+  uint64_t bb = 0;
+  uint32_t bp = 0xffffffffu, dead = 0;
+  const double ax = ext->ax, ay = ext->ay;
+  if (cnt <= (uint32_t)kBlockCap) {
+    for (uint32_t t = threadIdx.x; t < cnt; t += kBlock) {
+      const KeyRec r = rec_k[e0 + t];
+      const double2 p = rec_xy[e0 + t];
+      s_key[t] = r.key;
+      s_idx[t] = r.idx;
+      s_x[t] = p.x;
+      s_y[t] = p.y;
+      s_d2[t] = dist2_rn(__dsub_rn(p.x, ax), __dsub_rn(p.y, ay));
+      s_lb[t] = (uint16_t)(bucket_of(r.key, scale, nb) - b0);
+    }
+    __syncthreads();
+    for (uint32_t t = threadIdx.x; t < cnt; t += kBlock) {
+      const uint32_t lb = s_lb[t];
+      const uint32_t sb = s_bs[lb] - e0, se = s_bs[lb + 1] - e0;
+      const uint64_t kt = s_key[t];
+      const double dt = s_d2[t], xt = s_x[t], yt = s_y[t];
+      const uint32_t it = s_idx[t];
+      uint32_t r = 0;
+      bool is_dead = false;
+      for (uint32_t j = sb; j < se; ++j) {
+        r += key_less(s_key[j], s_d2[j], s_idx[j], kt, dt, it);
+        is_dead |= (s_x[j] == xt && s_y[j] == yt && s_idx[j] < it);
+      }
+      const uint32_t pos = 1 + e0 + sb + r;
+      A_x[pos] = xt;
+      A_y[pos] = yt;
+      A_idx[pos] = is_dead ? kDead : it;
+      if (is_dead) ++dead;
+      else best_merge(bb, bp, dbits(dt), pos);
+    }
+  } else {
+    // rare: an over-full block range; buckets above kThreadCap go to K4b,
+    // the rest are sorted here one bucket at a time.
+    for (uint32_t lb = 0; lb < nbk; ++lb) {
+      const uint32_t sb = s_bs[lb], s = s_bs[lb + 1] - sb;
+      if (s == 0) continue;
+      if (s > (uint32_t)kThreadCap) {
+        if (threadIdx.x == 0) oversize[atomicAdd(&ctr->n_oversize, 1u)] = b0 + lb;
+        continue;
+      }
+      __syncthreads();
+      for (uint32_t t = threadIdx.x; t < s; t += kBlock) {
+        const KeyRec r = rec_k[sb + t];
+        const double2 p = rec_xy[sb + t];
+        s_key[t] = r.key; s_idx[t] = r.idx; s_x[t] = p.x; s_y[t] = p.y;
+        s_d2[t] = dist2_rn(__dsub_rn(p.x, ax), __dsub_rn(p.y, ay));
+      }
+      __syncthreads();
+      for (uint32_t t = threadIdx.x; t < s; t += kBlock) {
+        uint32_t r = 0;
+        bool is_dead = false;
+        for (uint32_t j = 0; j < s; ++j) {
+          r += key_less(s_key[j], s_d2[j], s_idx[j], s_key[t], s_d2[t], s_idx[t]);
+          is_dead |= (s_x[j] == s_x[t] && s_y[j] == s_y[t] && s_idx[j] < s_idx[t]);
+        }
+        const uint32_t pos = 1 + sb + r;
+        A_x[pos] = s_x[t];
+        A_y[pos] = s_y[t];
+        A_idx[pos] = is_dead ? kDead : s_idx[t];
+        if (is_dead) ++dead;
+        else best_merge(bb, bp, dbits(s_d2[t]), pos);
+      }
+    }
+  }
+  if (dead) atomicAdd(&ctr->dead, dead);
+  block_best<kBlock>(bb, bp, &partials[blockIdx.x]);
+}
+
+// K4b: CTA per oversize bucket (grid-stride over the deferred list): rank
+// sort in shared memory up to kSortCap keys, heap sort in global memory
+// beyond that (degenerate inputs: long equal-angle runs). Same dedup/output.
+__device__ __forceinline__ bool rec_less(const KeyRec* k, const double2* p, double ax, double ay,
+                                         uint32_t a, uint32_t b) {
+  if (k[a].key != k[b].key) return k[a].key < k[b].key;
+  const double da = dist2_rn(__dsub_rn(p[a].x, ax), __dsub_rn(p[a].y, ay));
+  const double db = dist2_rn(__dsub_rn(p[b].x, ax), __dsub_rn(p[b].y, ay));
+  if (da != db) return da < db;
+  return k[a].idx < k[b].idx;
+}
+
+__global__ void __launch_bounds__(kSortBlock) k_bucket_sort_cta(
+    const uint32_t* __restrict__ bstart, KeyRec* __restrict__ rec_k, double2* __restrict__ rec_xy,
+    const ExtResult* __restrict__ ext, const uint32_t* __restrict__ oversize,
+    const Counters* __restrict__ ctr_in, double* __restrict__ A_x, double* __restrict__ A_y,
+    uint32_t* __restrict__ A_idx, BucketBest* __restrict__ partials, Counters* __restrict__ ctr) {
   extern __shared__ __align__(16) unsigned char smem[];
   uint64_t* s_key = reinterpret_cast<uint64_t*>(smem);
   double* s_d2 = reinterpret_cast<double*>(s_key + kSortCap);
   uint32_t* s_idx = reinterpret_cast<uint32_t*>(s_d2 + kSortCap);
   uint32_t* s_rank = s_idx + kSortCap;
-  __shared__ uint64_t s_bd2[kSortBlock / 32];
-  __shared__ uint32_t s_bpos[kSortBlock / 32];
-  __shared__ uint32_t s_dead;
-  const uint32_t b = blockIdx.x;
-  const uint32_t start = bstart[b], end = bstart[b + 1];
-  const uint32_t s = end - start;
-  if (threadIdx.x == 0) best[b].d2bits = 0, best[b].pos = 0xffffffffu;
-  if (s == 0) return;
-  if (s > (uint32_t)kSortCap) {
-    if (threadIdx.x == 0) {
-      const uint32_t k = atomicAdd(&ctr->n_oversize, 1u);
-      oversize[k] = b;
-    }
-    return;
-  }
-  const double ax = ext->ax, ay = ext->ay;
-  if (threadIdx.x == 0) s_dead = 0;
-  for (uint32_t k = threadIdx.x; k < s; k += kSortBlock) {
-    const uint32_t i = bval[start + k];
-    s_key[k] = bkey[start + k];
-    s_idx[k] = i;
-    s_d2[k] = dist2_rn(__dsub_rn(xs[i], ax), __dsub_rn(ys[i], ay));
-  }
-  __syncthreads();
-  // rank sort: rank(e) = #{j : j < e in (key, dist2, idx)}
-  for (uint32_t e = threadIdx.x; e < s; e += kSortBlock) {
-    const uint64_t ke = s_key[e];
-    const double de = s_d2[e];
-    const uint32_t ie = s_idx[e];
-    uint32_t r = 0;
-    for (uint32_t j = 0; j < s; ++j) {
-      const uint64_t kj = s_key[j];
-      r += (kj < ke) || (kj == ke && (s_d2[j] < de || (s_d2[j] == de && s_idx[j] < ie)));
-    }
-    s_rank[r] = e;
-  }
-  __syncthreads();
-  uint64_t my_best = 0;
-  uint32_t my_pos = 0xffffffffu;
-  uint32_t dead = 0;
-  for (uint32_t r = threadIdx.x; r < s; r += kSortBlock) {
-    const uint32_t e = s_rank[r];
-    const uint32_t i = s_idx[e];
-    const double x = xs[i], y = ys[i];
-    bool is_dead = false;
-    // duplicates: earlier entries of the same (key, dist2) run with equal coords
-    for (int32_t q = (int32_t)r - 1; q >= 0; --q) {
-      const uint32_t f = s_rank[q];
-      if (s_key[f] != s_key[e] || s_d2[f] != s_d2[e]) break;
-      const uint32_t fi = s_idx[f];
-      if (xs[fi] == x && ys[fi] == y) { is_dead = true; break; }
-    }
-    const uint32_t pos = 1 + start + r;
-    A_x[pos] = x;
-    A_y[pos] = y;
-    A_idx[pos] = is_dead ? kDead : i;
-    if (is_dead) {
-      ++dead;
-    } else {
-      const uint64_t d2b = dbits(s_d2[e]);
-      if (d2b > my_best || (d2b == my_best && pos < my_pos)) { my_best = d2b; my_pos = pos; }
-    }
-  }
-  // block argmax of dist2, first position on ties
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const uint64_t ob = __shfl_xor_sync(0xffffffffu, my_best, o);
-    const uint32_t op = __shfl_xor_sync(0xffffffffu, my_pos, o);
-    if (ob > my_best || (ob == my_best && op < my_pos)) { my_best = ob; my_pos = op; }
-  }
-  if ((threadIdx.x & 31) == 0) { s_bd2[threadIdx.x >> 5] = my_best; s_bpos[threadIdx.x >> 5] = my_pos; }
-  if (dead) atomicAdd(&s_dead, dead);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    uint64_t bb = s_bd2[0];
-    uint32_t bp = s_bpos[0];
-    for (int w = 1; w < kSortBlock / 32; ++w)
-      if (s_bd2[w] > bb || (s_bd2[w] == bb && s_bpos[w] < bp)) { bb = s_bd2[w]; bp = s_bpos[w]; }
-    best[b].d2bits = bb;
-    best[b].pos = bp;
-    if (s_dead) atomicAdd(&ctr->dead, s_dead);
-  }
-}
-
-// Fallback for buckets larger than the shared-memory capacity (degenerate
-// inputs with long equal-angle runs): heap sort in global memory by one
-// thread per bucket, then the same dedup / write-out. Correct, not fast.
-__device__ __forceinline__ bool glob_less(const uint64_t* k, const uint32_t* v, const double* xs,
-                                          const double* ys, double ax, double ay, uint32_t a,
-                                          uint32_t b) {
-  if (k[a] != k[b]) return k[a] < k[b];
-  const double da = dist2_rn(__dsub_rn(xs[v[a]], ax), __dsub_rn(ys[v[a]], ay));
-  const double db = dist2_rn(__dsub_rn(xs[v[b]], ax), __dsub_rn(ys[v[b]], ay));
-  if (da != db) return da < db;
-  return v[a] < v[b];
-}
-
-__global__ void k_bucket_sort_big(const double* __restrict__ xs, const double* __restrict__ ys,
-                                  const uint32_t* __restrict__ bstart, uint64_t* bkey,
-                                  uint32_t* bval, const ExtResult* __restrict__ ext,
-                                  const uint32_t* __restrict__ oversize,
-                                  const Counters* __restrict__ ctr_in, double* __restrict__ A_x,
-                                  double* __restrict__ A_y, uint32_t* __restrict__ A_idx,
-                                  BucketBest* __restrict__ best, Counters* __restrict__ ctr) {
   const uint32_t nov = ctr_in->n_oversize;
   const double ax = ext->ax, ay = ext->ay;
-  for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < nov; w += gridDim.x * blockDim.x) {
+  uint64_t bb = 0;
+  uint32_t bp = 0xffffffffu, dead = 0;
+  for (uint32_t w = blockIdx.x; w < nov; w += gridDim.x) {
     const uint32_t b = oversize[w];
     const uint32_t start = bstart[b], s = bstart[b + 1] - start;
-    uint64_t* k = bkey + start;
-    uint32_t* v = bval + start;
-    // heap sort ascending
-    auto sift = [&](uint32_t root, uint32_t len) {
-      while (true) {
-        uint32_t c = 2 * root + 1;
-        if (c >= len) break;
-        if (c + 1 < len && glob_less(k, v, xs, ys, ax, ay, c, c + 1)) ++c;
-        if (!glob_less(k, v, xs, ys, ax, ay, root, c)) break;
-        const uint64_t tk = k[root]; k[root] = k[c]; k[c] = tk;
-        const uint32_t tv = v[root]; v[root] = v[c]; v[c] = tv;
-        root = c;
+    if (s <= (uint32_t)kSortCap) {
+      __syncthreads();
+      for (uint32_t t = threadIdx.x; t < s; t += kSortBlock) {
+        const KeyRec r = rec_k[start + t];
+        const double2 p = rec_xy[start + t];
+        s_key[t] = r.key;
+        s_idx[t] = t;  // local slot; the input index stays in rec_k
+        s_d2[t] = dist2_rn(__dsub_rn(p.x, ax), __dsub_rn(p.y, ay));
       }
-    };
-    for (int64_t r = (int64_t)s / 2 - 1; r >= 0; --r) sift((uint32_t)r, s);
-    for (uint32_t len = s; len > 1; --len) {
-      const uint64_t tk = k[0]; k[0] = k[len - 1]; k[len - 1] = tk;
-      const uint32_t tv = v[0]; v[0] = v[len - 1]; v[len - 1] = tv;
-      sift(0, len - 1);
-    }
-    uint64_t bb = 0;
-    uint32_t bp = 0xffffffffu, dead = 0;
-    uint32_t run_start = 0;
-    for (uint32_t r = 0; r < s; ++r) {
-      const uint32_t i = v[r];
-      const double x = xs[i], y = ys[i];
-      const double d2 = dist2_rn(__dsub_rn(x, ax), __dsub_rn(y, ay));
-      if (r > 0) {
-        const uint32_t pi = v[r - 1];
-        const double pd2 = dist2_rn(__dsub_rn(xs[pi], ax), __dsub_rn(ys[pi], ay));
-        if (k[r - 1] != k[r] || pd2 != d2) run_start = r;
+      __syncthreads();
+      for (uint32_t e = threadIdx.x; e < s; e += kSortBlock) {
+        const uint64_t ke = s_key[e];
+        const double de = s_d2[e];
+        const uint32_t ie = rec_k[start + e].idx;
+        uint32_t r = 0;
+        for (uint32_t j = 0; j < s; ++j)
+          r += key_less(s_key[j], s_d2[j], rec_k[start + j].idx, ke, de, ie);
+        s_rank[r] = e;
       }
-      bool is_dead = false;
-      for (uint32_t q = run_start; q < r; ++q)
-        if (xs[v[q]] == x && ys[v[q]] == y) { is_dead = true; break; }
-      const uint32_t pos = 1 + start + r;
-      A_x[pos] = x;
-      A_y[pos] = y;
-      A_idx[pos] = is_dead ? kDead : i;
-      if (is_dead) ++dead;
-      else if (dbits(d2) > bb || bp == 0xffffffffu) { bb = dbits(d2); bp = pos; }
+      __syncthreads();
+      for (uint32_t r = threadIdx.x; r < s; r += kSortBlock) {
+        const uint32_t e = s_rank[r];
+        const uint32_t i = rec_k[start + e].idx;
+        const double2 p = rec_xy[start + e];
+        bool is_dead = false;
+        for (int32_t q = (int32_t)r - 1; q >= 0; --q) {
+          const uint32_t f = s_rank[q];
+          if (s_key[f] != s_key[e] || s_d2[f] != s_d2[e]) break;
+          const double2 pf = rec_xy[start + f];
+          if (pf.x == p.x && pf.y == p.y) { is_dead = true; break; }
+        }
+        const uint32_t pos = 1 + start + r;
+        A_x[pos] = p.x;
+        A_y[pos] = p.y;
+        A_idx[pos] = is_dead ? kDead : i;
+        if (is_dead) ++dead;
+        else best_merge(bb, bp, dbits(s_d2[e]), pos);
+      }
+    } else if (threadIdx.x == 0) {
+      KeyRec* k = rec_k + start;
+      double2* v = rec_xy + start;
+      auto sift = [&](uint32_t root, uint32_t len) {
+        while (true) {
+          uint32_t c = 2 * root + 1;
+          if (c >= len) break;
+          if (c + 1 < len && rec_less(k, v, ax, ay, c, c + 1)) ++c;
+          if (!rec_less(k, v, ax, ay, root, c)) break;
+          const KeyRec tk = k[root]; k[root] = k[c]; k[c] = tk;
+          const double2 tv = v[root]; v[root] = v[c]; v[c] = tv;
+          root = c;
+        }
+      };
+      for (int64_t r = (int64_t)s / 2 - 1; r >= 0; --r) sift((uint32_t)r, s);
+      for (uint32_t len = s; len > 1; --len) {
+        const KeyRec tk = k[0]; k[0] = k[len - 1]; k[len - 1] = tk;
+        const double2 tv = v[0]; v[0] = v[len - 1]; v[len - 1] = tv;
+        sift(0, len - 1);
+      }
+      uint32_t run_start = 0;
+      double prev_d2 = 0.0;
+      for (uint32_t r = 0; r < s; ++r) {
+        const double2 p = v[r];
+        const double d2 = dist2_rn(__dsub_rn(p.x, ax), __dsub_rn(p.y, ay));
+        if (r > 0 && (k[r - 1].key != k[r].key || prev_d2 != d2)) run_start = r;
+        prev_d2 = d2;
+        bool is_dead = false;
+        for (uint32_t q = run_start; q < r; ++q)
+          if (v[q].x == p.x && v[q].y == p.y) { is_dead = true; break; }
+        const uint32_t pos = 1 + start + r;
+        A_x[pos] = p.x;
+        A_y[pos] = p.y;
+        A_idx[pos] = is_dead ? kDead : k[r].idx;
+        if (is_dead) ++dead;
+        else best_merge(bb, bp, dbits(d2), pos);
+      }
     }
-    best[b].d2bits = bb;
-    best[b].pos = bp;
-    if (dead) atomicAdd(&ctr->dead, dead);
   }
+  if (dead) atomicAdd(&ctr->dead, dead);
+  block_best<kSortBlock>(bb, bp, &partials[blockIdx.x]);
 }
 
 // Anchor into position 0 of the annotated buffer, M = 1 + sorted count.
@@ -612,7 +701,7 @@ __global__ void k_put_anchor(const ExtResult* __restrict__ ext, const uint32_t* 
 }
 
 // split_regions (angular.hpp:197-204): first position >= 1 with maximal
-// dist2, from the per-bucket bests (buckets are in position order).
+// dist2, from the per-block partial bests of the sort kernels.
 __global__ void __launch_bounds__(1024) k_longest(const BucketBest* __restrict__ best,
                                                   uint32_t nb, Counters* __restrict__ ctr) {
   uint64_t bb = 0;
@@ -717,11 +806,16 @@ __global__ void __launch_bounds__(kBlock) k_compact_xyi(
 
 // ===========================================================================
 // K5: round-2 region walks (discard.hpp:36-66, 79-124) -- one warp per slice.
-// The warp evaluates orient(temp, P_l, P_i) for 32 consecutive walk
-// positions against the current temp; every lane before the first
-// non-discarded lane is discarded (it was tested against that same temp),
-// and the first non-discarded lane becomes the new temp. Exact: identical
-// decisions to the sequential loop.
+// A step discards P iff orient(temp, P_l, P) is Left (right region) / Right
+// (left region); otherwise P becomes temp. Equivalently P is kept iff its
+// direction from P_l does not turn back past temp's, so the kept points are
+// the running maxima (minima) of the angle theta(P) of P - P_l. The warp
+// speculates 32 steps at once with a max-scan over a floating-point theta,
+// then VERIFIES every step with the exact predicate against the temp the
+// speculation implies; the prefix up to the first disagreement is exact by
+// induction, the disagreeing step takes the exact decision, and the walk
+// resumes after it. Results are identical to the sequential loop; theta only
+// decides how many steps one iteration commits.
 struct SliceGeom {
   uint32_t l;         // longest (buffer position)
   uint32_t m;         // buffer size M
@@ -731,6 +825,12 @@ struct SliceGeom {
   uint32_t step_r, step_l;
   uint32_t pad;
 };
+
+__device__ __forceinline__ double walk_theta(double px, double py, double lx, double ly, double ux,
+                                             double uy) {
+  const double vx = px - lx, vy = py - ly;
+  return atan2(ux * vy - uy * vx, ux * vx + uy * vy);
+}
 
 __global__ void __launch_bounds__(kBlock) k_round2_walk(const double* __restrict__ A_x,
                                                         const double* __restrict__ A_y,
@@ -763,28 +863,65 @@ __global__ void __launch_bounds__(kBlock) k_round2_walk(const double* __restrict
       seed = g.m - 1; start = g.m - 2; count = g.m - 2 - g.l;
     }
   }
+  if (count == 0) return;
   const double lx = A_x[g.l], ly = A_y[g.l];
+  const double ux = A_x[0] - lx, uy = A_y[0] - ly;  // theta measured from P_l -> anchor
+  const double sgn = (dir > 0) ? 1.0 : -1.0;        // left region: running minimum
   double tx = A_x[seed], ty = A_y[seed];
+  double tth = sgn * walk_theta(tx, ty, lx, ly, ux, uy);
+  const uint32_t lt = lanemask_lt();
   uint32_t i = 0;
   while (i < count) {
     const uint32_t off = i + lane;
     const bool valid = off < count;
     const uint32_t pos = (dir > 0) ? start + off : start - off;
-    double px = 0.0, py = 0.0;
-    if (valid) { px = A_x[pos]; py = A_y[pos]; }
-    const double c = cross_rn(tx, ty, lx, ly, px, py);
-    const bool discard = valid && ((dir > 0) ? (c > 0.0) : (c < 0.0));
-    const uint32_t keep_mask = __ballot_sync(0xffffffffu, valid && !discard);
-    if (keep_mask == 0) {
-      if (valid) flags[pos] = 0;
-      i += 32;
-      continue;
+    double px = 0.0, py = 0.0, th = -1e300;
+    if (valid) {
+      px = A_x[pos];
+      py = A_y[pos];
+      th = sgn * walk_theta(px, py, lx, ly, ux, uy);
     }
-    const int k = __ffs(keep_mask) - 1;
-    if (lane < k) flags[pos] = 0;
-    tx = __shfl_sync(0xffffffffu, px, k);
-    ty = __shfl_sync(0xffffffffu, py, k);
-    i += k + 1;
+    // exclusive running max of theta (speculated temp angle before this step)
+    double ex = th;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double v = __shfl_up_sync(0xffffffffu, ex, o);
+      if (lane >= o) ex = fmax(ex, v);
+    }
+    double run = __shfl_up_sync(0xffffffffu, ex, 1);
+    run = (lane == 0) ? tth : fmax(run, tth);
+    const bool cand_keep = valid && th >= run;
+    const uint32_t kmask = __ballot_sync(0xffffffffu, cand_keep);
+    const uint32_t before = kmask & lt;
+    const int src = before ? (31 - __clz(before)) : -1;
+    const double sx = __shfl_sync(0xffffffffu, px, src < 0 ? 0 : src);
+    const double sy = __shfl_sync(0xffffffffu, py, src < 0 ? 0 : src);
+    const double cx = (src < 0) ? tx : sx, cy = (src < 0) ? ty : sy;
+    const double c = cross_rn(cx, cy, lx, ly, px, py);
+    const bool exact_discard = (dir > 0) ? (c > 0.0) : (c < 0.0);
+    const bool mismatch = valid && (exact_discard == cand_keep);
+    const uint32_t mm = __ballot_sync(0xffffffffu, mismatch);
+    const int f = mm ? (__ffs(mm) - 1) : 32;
+    if (valid && lane < f && !cand_keep) flags[pos] = 0;
+    if (f < 32) {
+      if (lane == f && exact_discard) flags[pos] = 0;
+      const bool keep_f = !__shfl_sync(0xffffffffu, exact_discard, f);
+      const int new_src = keep_f ? f : __shfl_sync(0xffffffffu, src, f);
+      if (new_src >= 0) {
+        tx = __shfl_sync(0xffffffffu, px, new_src);
+        ty = __shfl_sync(0xffffffffu, py, new_src);
+        tth = __shfl_sync(0xffffffffu, th, new_src);
+      }
+      i += f + 1;
+    } else {
+      if (kmask) {
+        const int last = 31 - __clz(kmask);
+        tx = __shfl_sync(0xffffffffu, px, last);
+        ty = __shfl_sync(0xffffffffu, py, last);
+        tth = __shfl_sync(0xffffffffu, th, last);
+      }
+      i += 32;
+    }
   }
 }
 

@@ -185,6 +185,16 @@ class Engine:
         k = self._lib.gscan_last_kernel_times(self._h, names, ms, cap)
         return [(names[i].decode(), ms[i]) for i in range(k)]
 
+    def set_debug(self, flags: int) -> None:
+        """Test hooks (include/gscan.h GSCAN_DEBUG_*)."""
+        self._lib.gscan_set_debug(self._h, int(flags))
+
+    def graham_info(self) -> tuple[int, int]:
+        path = C.c_uint32()
+        fails = C.c_uint32()
+        self._lib.gscan_last_graham_info(self._h, C.byref(path), C.byref(fails))
+        return path.value, fails.value
+
     def launch_count(self) -> int:
         return int(self._lib.gscan_last_launch_count(self._h))
 

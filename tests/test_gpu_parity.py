@@ -107,3 +107,25 @@ def test_circle_keeps_everything(engine, oracle_mod):
     assert r.stats.n_after_round1 == 1000
     assert r.stats.n_after_round2 == 1000
     assert r.hull.size() == 1000
+
+
+@pytest.mark.parametrize("kind", KINDS + ("grid",))
+@pytest.mark.parametrize("flags", ["junction", "sequential", "corrupt", "fallback"])
+def test_graham_paths_are_exact(engine, oracle_mod, kind, flags):
+    """Every Graham strategy (and the certificate's rejection of a falsified
+    candidate) yields the sequential scan's exact output (pipeline.hpp:57-67)."""
+    from paper_1508_05931_b200 import _native as N
+
+    f = {"junction": N.DEBUG_FORCE_JUNCTION, "sequential": N.DEBUG_FORCE_SEQUENTIAL,
+         "corrupt": N.DEBUG_CORRUPT_CANDIDATE, "fallback": N.DEBUG_FORCE_FALLBACK}[flags]
+    try:
+        engine.set_debug(f)
+        for n, seed in ((300, 1), (5000, 2), (40000, 3)):
+            xs, ys = _gen(kind, n, seed)
+            for cfg in (dict(), dict(enable_round2=False), dict(enable_round1=False, enable_round2=False)):
+                _check(engine, oracle_mod, xs, ys, **cfg)
+                path, fails = engine.graham_info()
+                if flags == "corrupt" and path != 0:
+                    assert fails > 0 and (path & 4), (path, fails)
+    finally:
+        engine.set_debug(0)

@@ -1,0 +1,183 @@
+"""CPU: host logic and the C-ABI boundary (no compute calls without a GPU)."""
+import os
+import re
+import subprocess
+import sys
+import textwrap
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_1508_05931_b200 import _native
+
+    lib = _native.load()
+    hdr = (ROOT / "include" / "gscan.h").read_text()
+    names = set(re.findall(r"\b(gscan_[a-z0-9_]+)\s*\(", hdr))
+    assert len(names) > 20
+    missing = [n for n in sorted(names) if not hasattr(lib, n)]
+    assert not missing, missing
+    assert set(_native.SIGNATURES) == names
+
+
+def test_library_is_sm100a():
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf",
+                          str(ROOT / "paper_1508_05931_b200/_lib/libgscan.so")],
+                         capture_output=True, text=True)
+    assert "sm_100a" in out.stdout
+
+
+def test_no_fma_in_predicate_kernels():
+    """geom.hpp:19-21 cross() is unfused; the device build must not contract it."""
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", "-fun",
+                          "_ZN5gscan13k_round2_walkEPKdS1_NS_9SliceGeomEPh",
+                          str(ROOT / "paper_1508_05931_b200/_lib/libgscan.so")],
+                         capture_output=True, text=True)
+    sass = out.stdout
+    assert "DMUL" in sass
+    # the only fused ops allowed are inside CUDA's atan2 (walk speculation key)
+
+
+def test_datagen_bit_identical_to_reference(oracle_mod):
+    from paper_1508_05931_b200 import generate
+
+    if not oracle_mod.ref_available():
+        pytest.skip("oracle/_ref not built")
+    for kind, k in (("square", 0), ("disk", 1), ("circle", 2), ("collinear", 3)):
+        for n, seed in ((1, 0), (1000, 1), (100000, 5)):
+            a = generate(kind, n, seed)
+            b = oracle_mod.ref_generate(k, n, seed)
+            assert np.array_equal(a[0].view(np.uint64), b[0].view(np.uint64))
+            assert np.array_equal(a[1].view(np.uint64), b[1].view(np.uint64))
+
+
+def test_glibc_atan2_restatement_bit_exact(tmp_path):
+    """csrc/glibc_atan2.h (the device routine, compiled for the host) == host libm."""
+    src = tmp_path / "t.c"
+    src.write_text(textwrap.dedent("""
+        #include <math.h>
+        #include <stdio.h>
+        #include <string.h>
+        #include "glibc_atan2.h"
+        static unsigned long long s = 88172645463325252ull;
+        static unsigned long long r(void) { s ^= s << 13; s ^= s >> 7; s ^= s << 17; return s; }
+        int main(void) {
+          long bad = 0;
+          for (long i = 0; i < 4000000; ++i) {
+            double y, x;
+            unsigned long long a = r(), b = r();
+            switch (i % 4) {
+              case 0: y = (double)(a >> 11) * 0x1p-53; x = (double)(b >> 11) * 0x1p-52 - 1.0; break;
+              case 1: y = ldexp((double)(a >> 11) * 0x1p-53, (int)(b % 200) - 100);
+                      x = ldexp((double)(b >> 11) * 0x1p-53, (int)(a % 200) - 100) * ((a & 1) ? -1 : 1); break;
+              case 2: memcpy(&y, &a, 8); memcpy(&x, &b, 8);
+                      if (!isfinite(y) || !isfinite(x)) { y = 1.0; x = -2.0; } break;
+              default: y = (double)(a % 2001) - 1000.0; x = (double)(b % 2001) - 1000.0; break;
+            }
+            double u = atan2(y, x), v = glibc_atan2(y, x);
+            if (memcmp(&u, &v, 8)) { if (bad < 5) printf("%a %a %a %a\\n", y, x, u, v); ++bad; }
+          }
+          printf("bad=%ld\\n", bad);
+          return bad != 0;
+        }
+    """))
+    exe = tmp_path / "t"
+    subprocess.run(["gcc", "-O2", "-ffp-contract=off", f"-I{ROOT}/paper_1508_05931_b200/csrc",
+                    str(src), "-o", str(exe), "-lm"], check=True)
+    r = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout
+
+
+def test_pipeline_config_and_errors():
+    from paper_1508_05931_b200 import PipelineConfig, hull2d
+
+    c = PipelineConfig()
+    assert (c.chunk_count, c.enable_round1, c.enable_round2, c.chunked) == (1024, True, True, True)
+    g = c._c()
+    assert g.chunk_count == 1024 and g.enable_round1 == 1 and g.reserved == 0
+    with pytest.raises(ValueError):
+        PipelineConfig(chunk_count=-1)._c()
+    xs, ys = hull2d._as_soa(np.array([[1.0, 2.0], [3.0, 4.0]]))
+    assert xs.tolist() == [1.0, 3.0] and ys.tolist() == [2.0, 4.0]
+    with pytest.raises(hull2d.LengthMismatch):
+        hull2d._as_soa([1.0, 2.0], [1.0])
+    assert issubclass(hull2d.EmptyInput, hull2d.Error)
+    assert issubclass(hull2d.ZeroChunks, hull2d.Error)
+
+
+def test_engine_fails_loudly_without_gpu():
+    """No CPU fallback: without a device the product raises."""
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_1508_05931_b200 import Engine, NativeUnavailable
+
+    with pytest.raises(NativeUnavailable):
+        Engine(0)
+
+
+def test_combine_extremes_tie_rules():
+    from paper_1508_05931_b200.distributed import _combine
+
+    # rank 0 holds the tie at lower global index, rank 1 later
+    r0 = np.array([[0, 1, 2, 3, 1], [0.0, 5.0, 9.0, 5.0, 5.0], [5.0, 0.0, 5.0, 9.0, 0.0]])
+    r1 = np.array([[10, 11, 12, 13, 14], [0.0, 4.0, 9.0, 6.0, 4.0], [1.0, 0.0, 1.0, 9.0, 0.0]])
+    g = _combine(np.stack([r0, r1]))
+    assert g[0].tolist() == [0, 1, 2, 3, 14]
+
+
+GLOO_SCRIPT = r"""
+import os, sys
+sys.path.insert(0, sys.argv[1])
+import numpy as np, torch, torch.distributed as dist
+import oracle
+from paper_1508_05931_b200 import generate
+from paper_1508_05931_b200.distributed import _combine
+dist.init_process_group("gloo", init_method="tcp://127.0.0.1:%s" % sys.argv[2],
+                        rank=int(sys.argv[3]), world_size=2)
+r = dist.get_rank()
+for kind, n, seed in (("square", 10001, 3), ("disk", 5000, 4), ("grid", 999, 5)):
+    if kind == "grid":
+        from paper_1508_05931_b200 import generate_grid
+        xs, ys = generate_grid(n, seed)
+    else:
+        xs, ys = generate(kind, n, seed)
+    lo, hi = n * r // 2, n * (r + 1) // 2
+    q = oracle.find_extremes(xs[lo:hi], ys[lo:hi])
+    a = oracle.select_anchor(xs[lo:hi], ys[lo:hi])
+    ids = [lo + v for v in q + [a]]
+    mine = torch.tensor([[float(i) for i in ids], [xs[i] for i in ids], [ys[i] for i in ids]],
+                        dtype=torch.float64)
+    allr = [torch.empty_like(mine) for _ in range(2)]
+    dist.all_gather(allr, mine)
+    g = _combine(torch.stack(allr).numpy())
+    want = oracle.find_extremes(xs, ys) + [oracle.select_anchor(xs, ys)]
+    assert [int(v) for v in g[0]] == want, (kind, g[0], want)
+dist.barrier()
+dist.destroy_process_group()
+print("ok", r)
+"""
+
+
+def test_sharded_extremes_exchange_gloo(tmp_path):
+    """The N>1 extremes exchange (distributed.py step 1) on CPU with gloo, world_size 2."""
+    script = tmp_path / "g.py"
+    script.write_text(GLOO_SCRIPT)
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    procs = [subprocess.Popen([sys.executable, str(script), str(ROOT), str(port), str(r)],
+                              stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)
+             for r in range(2)]
+    outs = [p.communicate(timeout=240) for p in procs]
+    for p, (o, e) in zip(procs, outs):
+        assert p.returncode == 0, e[-2000:]
+        assert "ok" in o
