@@ -170,11 +170,13 @@ enum {
     GSCAN_DEBUG_FORCE_JUNCTION = 1u << 0,   /* Graham candidate via junction merges */
     GSCAN_DEBUG_FORCE_SEQUENTIAL = 1u << 1, /* Graham candidate via chains-of-chains scan */
     GSCAN_DEBUG_CORRUPT_CANDIDATE = 1u << 2,/* falsify the candidate: certificate must fail */
-    GSCAN_DEBUG_FORCE_FALLBACK = 1u << 3    /* always finish with the sequential kernel */
+    GSCAN_DEBUG_FORCE_FALLBACK = 1u << 3,   /* always finish with the sequential kernel */
+    GSCAN_DEBUG_FORCE_PREFIX = 1u << 4      /* Graham candidate via prefix scan of states */
 };
 int gscan_set_debug(gscan_handle* h, uint32_t flags);
-/* path: 0 = sequential kernel only (tiny input), 1 = chains + certificate,
- * 2 = junctions + certificate; bit 4 set = certificate failed or fallback forced. */
+/* path: 0 = sequential kernel only (tiny input), 1 = chain scan + certificate,
+ * 2 = junctions + certificate, 3 = prefix-scanned states + certificate;
+ * bit 4 set = certificate failed or fallback forced. */
 int gscan_last_graham_info(const gscan_handle* h, uint32_t* path, uint32_t* certificate_failures);
 
 /* ---- harness helpers (host) ---- */

@@ -28,6 +28,7 @@ DEBUG_FORCE_JUNCTION = 1 << 0
 DEBUG_FORCE_SEQUENTIAL = 1 << 1
 DEBUG_CORRUPT_CANDIDATE = 1 << 2
 DEBUG_FORCE_FALLBACK = 1 << 3
+DEBUG_FORCE_PREFIX = 1 << 4
 
 
 class NativeUnavailable(RuntimeError):

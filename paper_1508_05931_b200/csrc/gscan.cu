@@ -53,8 +53,7 @@ struct gscan_handle {
   uint32_t* surv = nullptr;
   uint64_t* keys = nullptr;
   uint32_t* rank = nullptr;
-  KeyRec* rec_k = nullptr;
-  double2* rec_xy = nullptr;
+  PtRec* rec = nullptr;
   double *A_x = nullptr, *A_y = nullptr;
   uint32_t* A_i = nullptr;
   double *C_x = nullptr, *C_y = nullptr;
@@ -71,7 +70,10 @@ struct gscan_handle {
   uint32_t *g_chain = nullptr, *g_len = nullptr, *g_off = nullptr, *g_q0 = nullptr, *g_q1 = nullptr;
   uint32_t *g_parent = nullptr, *g_btop = nullptr, *g_jk = nullptr, *g_je = nullptr;
   int32_t* g_jmin = nullptr;
-  uint32_t *g_keep = nullptr, *g_misc = nullptr;  // misc: [0] fail, [1] len, [2] q size
+  uint32_t *g_keep = nullptr, *g_misc = nullptr;  // misc: [0] fail, [1] len, [2] ovf, [3] which
+  uint32_t *g_stA = nullptr, *g_stB = nullptr, *g_lenA = nullptr, *g_lenB = nullptr,
+           *g_scr = nullptr;
+  uint64_t g_st_cap = 0, g_len_cap = 0;  // entries per state buffer / per length array
   ExtAcc* partials = nullptr;
   ExtResult* ext = nullptr;
   Counters* ctr = nullptr;
@@ -113,12 +115,15 @@ void dfree(T*& p) {
 
 void free_buffers(gscan_handle* h) {
   dfree(h->d_xs); dfree(h->d_ys); dfree(h->surv); dfree(h->keys); dfree(h->rank);
-  dfree(h->rec_k); dfree(h->rec_xy); dfree(h->A_x); dfree(h->A_y); dfree(h->A_i); dfree(h->C_x); dfree(h->C_y);
+  dfree(h->rec); dfree(h->A_x); dfree(h->A_y); dfree(h->A_i); dfree(h->C_x); dfree(h->C_y);
   dfree(h->C_i); dfree(h->flags); dfree(h->stack); dfree(h->d_out); dfree(h->status);
   dfree(h->hist); dfree(h->bstart); dfree(h->cursor); dfree(h->oversize); dfree(h->best);
   dfree(h->g_chain); dfree(h->g_len); dfree(h->g_off); dfree(h->g_q0); dfree(h->g_q1);
   dfree(h->g_parent); dfree(h->g_btop); dfree(h->g_jk); dfree(h->g_je); dfree(h->g_jmin);
   dfree(h->g_keep); dfree(h->g_misc);
+  dfree(h->g_stA); dfree(h->g_stB); dfree(h->g_lenA); dfree(h->g_lenB); dfree(h->g_scr);
+  h->g_st_cap = 0;
+  h->g_len_cap = 0;
   h->cap = 0;
   h->nb_cap = 0;
   h->status_cap = 0;
@@ -142,8 +147,7 @@ int reserve(gscan_handle* h, uint64_t n) {
   CU(cudaMalloc(&h->surv, m * 4));
   CU(cudaMalloc(&h->keys, m * 8));
   CU(cudaMalloc(&h->rank, m * 4));
-  CU(cudaMalloc(&h->rec_k, m * sizeof(KeyRec)));
-  CU(cudaMalloc(&h->rec_xy, m * sizeof(double2)));
+  CU(cudaMalloc(&h->rec, m * sizeof(PtRec)));
   CU(cudaMalloc(&h->A_x, m * 8));
   CU(cudaMalloc(&h->A_y, m * 8));
   CU(cudaMalloc(&h->A_i, m * 4));
@@ -231,7 +235,7 @@ int sync_counters(gscan_handle* h) {
 // `quad_override` (distributed use: the quadrilateral of the GLOBAL extremes),
 // K1 is skipped and the given ExtResult is used.
 int stage_round1(gscan_handle* h, const double* xs, const double* ys, uint32_t n, int enable,
-                 const ExtResult* quad_override = nullptr) {
+                 const ExtResult* quad_override = nullptr, bool ordered = false) {
   const bool vec = aligned16(xs) && aligned16(ys);
   if (quad_override) {
     CU(cudaMemcpyAsync(h->ext, quad_override, sizeof(ExtResult), cudaMemcpyHostToDevice, h->stream));
@@ -243,15 +247,15 @@ int stage_round1(gscan_handle* h, const double* xs, const double* ys, uint32_t n
     else k_extremes<false><<<grid, kBlock, 0, h->stream>>>(xs, ys, n, h->partials, h->ext, h->ctr);
   }
   const uint64_t tiles = (n + kFilterTile - 1) / kFilterTile;
-  TRY(reset_lookback(h, tiles));
+  if (ordered) TRY(reset_lookback(h, tiles));
   {
     Launch L(h, "k_filter_compact");
-    if (vec)
-      k_filter_compact<true><<<tiles, kBlock, 0, h->stream>>>(xs, ys, n, h->ext, enable, h->status,
-                                                              h->surv, h->ctr);
-    else
-      k_filter_compact<false><<<tiles, kBlock, 0, h->stream>>>(xs, ys, n, h->ext, enable,
-                                                               h->status, h->surv, h->ctr);
+#define K2_ARGS xs, ys, n, h->ext, enable, h->status, h->surv, h->ctr
+    if (vec && ordered) k_filter_compact<true, true><<<tiles, kBlock, 0, h->stream>>>(K2_ARGS);
+    else if (vec) k_filter_compact<true, false><<<tiles, kBlock, 0, h->stream>>>(K2_ARGS);
+    else if (ordered) k_filter_compact<false, true><<<tiles, kBlock, 0, h->stream>>>(K2_ARGS);
+    else k_filter_compact<false, false><<<tiles, kBlock, 0, h->stream>>>(K2_ARGS);
+#undef K2_ARGS
   }
   CU(cudaGetLastError());
   return GSCAN_OK;
@@ -281,22 +285,22 @@ int stage_annotate_sort(gscan_handle* h, const double* xs, const double* ys, uin
     const uint32_t grid = std::max(1u, std::min<uint32_t>((n + kBlock - 1) / kBlock, h->sm_count * 16));
     Launch L(h, "k_scatter");
     k_scatter<<<grid, kBlock, 0, h->stream>>>(xs, ys, h->keys, h->rank, h->surv, h->ctr,
-                                              h->bstart, scale, nb, h->rec_k, h->rec_xy);
+                                              h->bstart, scale, nb, h->rec);
   }
   const uint32_t tblocks = (nb + kBucketsPerBlock - 1) / kBucketsPerBlock;
   {
     const size_t smem = (size_t)kBlockCap * (8 + 8 + 8 + 8 + 4 + 2);
     Launch L(h, "k_bucket_sort_block");
-    k_bucket_sort_block<<<tblocks, kBlock, smem, h->stream>>>(h->bstart, h->rec_k, h->rec_xy,
-                                                              h->ext, scale, nb, h->A_x, h->A_y,
-                                                              h->A_i, h->best, h->oversize, h->ctr);
+    k_bucket_sort_block<<<tblocks, kBlock, smem, h->stream>>>(h->bstart, h->rec, h->ext, scale, nb,
+                                                              h->A_x, h->A_y, h->A_i, h->best,
+                                                              h->oversize, h->ctr);
   }
   {
     const size_t smem = (size_t)kSortCap * (8 + 8 + 4 + 4);
     Launch L(h, "k_bucket_sort_cta");
     k_bucket_sort_cta<<<kCtaSortGrid, kSortBlock, smem, h->stream>>>(
-        h->bstart, h->rec_k, h->rec_xy, h->ext, h->oversize, h->ctr, h->A_x, h->A_y, h->A_i,
-        h->best + tblocks, h->ctr);
+        h->bstart, h->rec, h->ext, h->oversize, h->ctr, h->A_x, h->A_y, h->A_i, h->best + tblocks,
+        h->ctr);
   }
   {
     Launch L(h, "k_put_anchor");
@@ -413,6 +417,86 @@ int read_u32(gscan_handle* h, const uint32_t* d, uint32_t* v) {
 
 // K7/K8 (graham.cuh): candidate + certificate; exact sequential fallback.
 // Leaves the hull (input indices) in h->d_out and its size in ctr->hull.
+// Candidate strategies: junctions (convex-position inputs: chains don't
+// shrink), prefix scan of explicit states (chains shrink: square/disk), and
+// the warp sequential scan over the chains (prefix states too large).
+constexpr uint64_t kPrefixBudget = 1ull << 26;  // entries per explicit-state buffer
+
+int graham_seq_fallback(gscan_handle* h, const double* Rx, const double* Ry, const uint32_t* Ri) {
+  h->graham_path |= 4;
+  Launch L(h, "k_graham_seq");
+  k_graham_seq<<<1, 32, 0, h->stream>>>(Rx, Ry, Ri, &h->ctr->n2, h->stack, h->d_out, h->ctr);
+  CU(cudaGetLastError());
+  return GSCAN_OK;
+}
+
+int graham_prefix(gscan_handle* h, const double* Rx, const double* Ry, const uint32_t* Ri,
+                  uint32_t N, uint32_t nch, uint32_t q0, bool* done) {
+  *done = false;
+  const uint64_t cap = (uint64_t)q0 + 64;
+  const uint64_t need = (uint64_t)nch * cap;
+  const uint64_t need_scr = (uint64_t)nch * (cap + kChunk + 32);
+  if (need > kPrefixBudget) return GSCAN_OK;
+  if (need_scr > h->g_st_cap || need > h->g_st_cap || nch > h->g_len_cap) {
+    dfree(h->g_stA); dfree(h->g_stB); dfree(h->g_lenA); dfree(h->g_lenB); dfree(h->g_scr);
+    const uint64_t c2 = std::max(need_scr, need) * 5 / 4 + 1024;
+    const uint64_t l2 = (uint64_t)nch * 5 / 4 + 64;
+    CU(cudaMalloc(&h->g_stA, c2 * 4));
+    CU(cudaMalloc(&h->g_stB, c2 * 4));
+    CU(cudaMalloc(&h->g_scr, c2 * 4));
+    CU(cudaMalloc(&h->g_lenA, l2 * 4));
+    CU(cudaMalloc(&h->g_lenB, l2 * 4));
+    h->g_st_cap = c2;
+    h->g_len_cap = l2;
+  }
+  uint32_t* ovf = h->g_misc + 2;
+  uint32_t* which = h->g_misc + 3;
+  CU(cudaMemsetAsync(ovf, 0, 8, h->stream));
+  int per_sm = 0;
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_graham_prefix, kPrefixWarps * 32, 0));
+  const uint32_t want = (nch + kPrefixWarps - 1) / kPrefixWarps;
+  const uint32_t grid = std::max(1u, std::min<uint32_t>(want, (uint32_t)(per_sm * h->sm_count)));
+  uint32_t capu = (uint32_t)cap;
+  void* args[] = {(void*)&Rx, (void*)&Ry, (void*)&h->g_chain, (void*)&h->g_len, (void*)&nch,
+                  (void*)&h->g_stA, (void*)&h->g_stB, (void*)&h->g_lenA, (void*)&h->g_lenB,
+                  (void*)&capu, (void*)&ovf, (void*)&which};
+  {
+    Launch L(h, "k_graham_prefix");
+    CU(cudaLaunchCooperativeKernel((void*)k_graham_prefix, grid, kPrefixWarps * 32, args, 0,
+                                   h->stream));
+  }
+  uint32_t fl[2];
+  CU(cudaMemcpyAsync(fl, ovf, 8, cudaMemcpyDeviceToHost, h->stream));
+  CU(cudaStreamSynchronize(h->stream));
+  if (fl[0]) return GSCAN_OK;  // overflow (cannot happen with cap = q0 + 64; kept as a guard)
+  const uint32_t* st = fl[1] ? h->g_stB : h->g_stA;
+  const uint32_t* len = fl[1] ? h->g_lenB : h->g_lenA;
+  uint32_t* fail_d = h->g_misc;
+  CU(cudaMemsetAsync(fail_d, 0, 4, h->stream));
+  if (h->debug & GSCAN_DEBUG_CORRUPT_CANDIDATE) {
+    // falsify the final state (empty it): the certificate must reject it
+    CU(cudaMemsetAsync((void*)(len + nch - 1), 0, 4, h->stream));
+  }
+  {
+    Launch L(h, "k_graham_certify_explicit");
+    k_graham_certify_explicit<<<(nch + kCertWarps - 1) / kCertWarps, kCertWarps * 32, 0,
+                                h->stream>>>(Rx, Ry, N, st, len, capu, h->g_scr, fail_d);
+  }
+  uint32_t fails;
+  TRY(read_u32(h, fail_d, &fails));
+  h->graham_fails = fails;
+  h->graham_path = 3;
+  if (fails || (h->debug & GSCAN_DEBUG_FORCE_FALLBACK)) return GSCAN_OK;
+  {
+    Launch L(h, "k_graham_emit_explicit");
+    k_graham_emit_explicit<<<std::max(1u, std::min<uint32_t>((q0 + kBlock - 1) / kBlock, 1184)),
+                             kBlock, 0, h->stream>>>(st, len, nch - 1, capu, Ri, h->d_out, h->ctr);
+  }
+  CU(cudaGetLastError());
+  *done = true;
+  return GSCAN_OK;
+}
+
 int stage_graham(gscan_handle* h, const double* Rx, const double* Ry, const uint32_t* Ri,
                  uint32_t N) {
   uint32_t* fail_d = h->g_misc;
@@ -420,80 +504,94 @@ int stage_graham(gscan_handle* h, const double* Rx, const double* Ry, const uint
   CU(cudaMemsetAsync(h->g_misc, 0, 16, h->stream));
   h->graham_path = 0;
   h->graham_fails = 0;
-  if (N > 2 * kChunk) {
-    const uint32_t nch = (N + kChunk - 1) / kChunk;
-    {
-      Launch L(h, "k_graham_local");
-      k_graham_local<<<(nch + 127) / 128, 128, 0, h->stream>>>(Rx, Ry, N, h->g_chain, h->g_len);
-    }
-    bool junction_ok = false;
-    if (!(h->debug & GSCAN_DEBUG_FORCE_SEQUENTIAL)) {
-      {
-        Launch L(h, "k_graham_junction");
-        k_graham_junction<<<(nch + 127) / 128, 128, 0, h->stream>>>(Rx, Ry, h->g_chain, h->g_len,
-                                                                     nch, h->g_jk, h->g_je, h->g_jmin);
-      }
-      {
-        Launch L(h, "k_graham_junction_apply");
-        k_graham_junction_apply<<<(nch + 1 + 127) / 128, 128, 0, h->stream>>>(
-            h->g_chain, h->g_len, nch, h->g_jk, h->g_je, h->g_jmin, h->g_parent, h->g_btop,
-            h->g_keep, fail_d);
-      }
-      uint32_t jfail;
-      TRY(read_u32(h, fail_d, &jfail));
-      junction_ok = (jfail == 0) || (h->debug & GSCAN_DEBUG_FORCE_JUNCTION);
-    }
-    if (junction_ok) {
-      h->graham_path = 2;
-      TRY(scan_u32(h, h->g_keep, nch, h->g_off));
-      {
-        Launch L(h, "k_graham_junction_emit");
-        k_graham_junction_emit<<<(nch + 7) / 8, 8 * kChunk, 0, h->stream>>>(
-            h->g_chain, h->g_je, h->g_keep, h->g_off, nch, h->stack);
-      }
-      CU(cudaMemcpyAsync(len_d, h->g_off + nch, 4, cudaMemcpyDeviceToDevice, h->stream));
-    } else {
-      h->graham_path = 1;
-      CU(cudaMemsetAsync(fail_d, 0, 4, h->stream));
-      TRY(scan_u32(h, h->g_len, nch, h->g_off));
-      {
-        Launch L(h, "k_gather_chains");
-        k_gather_chains<<<(nch + 7) / 8, 8 * kChunk, 0, h->stream>>>(h->g_chain, h->g_len,
-                                                                     h->g_off, nch, h->g_q0);
-      }
-      {
-        Launch L(h, "k_graham_candidate_seq");
-        k_graham_candidate_seq<<<1, 32, 0, h->stream>>>(Rx, Ry, h->g_q0, h->g_off + nch, N,
-                                                        h->g_parent, h->g_btop, h->stack, len_d);
-      }
-    }
-    if (h->debug & GSCAN_DEBUG_CORRUPT_CANDIDATE) {
-      // drop the candidate's last boundary state: the certificate must reject it
-      CU(cudaMemcpyAsync(h->g_btop + nch, h->g_btop + nch - 1, 4, cudaMemcpyDeviceToDevice,
-                         h->stream));
-    }
-    {
-      Launch L(h, "k_graham_certify");
-      k_graham_certify<<<(nch + 127) / 128, 128, 0, h->stream>>>(Rx, Ry, N, h->g_parent, h->g_btop,
-                                                                  fail_d);
-    }
-    uint32_t fails;
-    TRY(read_u32(h, fail_d, &fails));
-    h->graham_fails = fails;
-    if (fails == 0 && !(h->debug & GSCAN_DEBUG_FORCE_FALLBACK)) {
-      Launch L(h, "k_graham_emit");
-      k_graham_emit<<<std::max(1u, std::min<uint32_t>((N + kBlock - 1) / kBlock, 1184)), kBlock, 0,
-                      h->stream>>>(h->stack, len_d, Ri, h->d_out, h->ctr);
-      CU(cudaGetLastError());
-      return GSCAN_OK;
-    }
-    h->graham_path |= 4;  // certificate failed or fallback forced
+  if (N <= 2 * kChunk) {  // tiny buffer: the sequential kernel is the fastest exact path
+    TRY(graham_seq_fallback(h, Rx, Ry, Ri));
+    h->graham_path = 0;
+    return GSCAN_OK;
   }
-  // small buffers, or certificate failure: exact sequential scan on the device
-  Launch L(h, "k_graham_seq");
-  k_graham_seq<<<1, 32, 0, h->stream>>>(Rx, Ry, Ri, &h->ctr->n2, h->stack, h->d_out, h->ctr);
-  CU(cudaGetLastError());
-  return GSCAN_OK;
+  const uint32_t nch = (N + kChunk - 1) / kChunk;
+  {
+    Launch L(h, "k_graham_local");
+    k_graham_local<<<(nch + kLocalWarps - 1) / kLocalWarps, kLocalWarps * 32, 0, h->stream>>>(
+        Rx, Ry, N, h->g_chain, h->g_len);
+  }
+  TRY(scan_u32(h, h->g_len, nch, h->g_off));
+  uint32_t q0;
+  TRY(read_u32(h, h->g_off + nch, &q0));
+  const bool force_j = h->debug & GSCAN_DEBUG_FORCE_JUNCTION;
+  const bool force_s = h->debug & GSCAN_DEBUG_FORCE_SEQUENTIAL;
+  const bool force_p = h->debug & GSCAN_DEBUG_FORCE_PREFIX;
+  bool junction_ok = false;
+  if (force_j || (!force_s && !force_p && q0 > N / 2)) {
+    {
+      Launch L(h, "k_graham_junction");
+      k_graham_junction<<<(nch + 127) / 128, 128, 0, h->stream>>>(Rx, Ry, h->g_chain, h->g_len,
+                                                                   nch, h->g_jk, h->g_je, h->g_jmin);
+    }
+    {
+      Launch L(h, "k_graham_junction_apply");
+      k_graham_junction_apply<<<(nch + 1 + 127) / 128, 128, 0, h->stream>>>(
+          h->g_chain, h->g_len, nch, h->g_jk, h->g_je, h->g_jmin, h->g_parent, h->g_btop,
+          h->g_keep, fail_d);
+    }
+    uint32_t jfail;
+    TRY(read_u32(h, fail_d, &jfail));
+    junction_ok = (jfail == 0) || force_j;
+  }
+  if (!junction_ok && !force_s) {
+    bool done = false;
+    TRY(graham_prefix(h, Rx, Ry, Ri, N, nch, q0, &done));
+    if (done) return GSCAN_OK;
+    if (h->graham_path == 3) return graham_seq_fallback(h, Rx, Ry, Ri);  // certificate failed
+  }
+  CU(cudaMemsetAsync(fail_d, 0, 4, h->stream));
+  if (junction_ok) {
+    h->graham_path = 2;
+    TRY(scan_u32(h, h->g_keep, nch, h->g_off));
+    {
+      Launch L(h, "k_graham_junction_emit");
+      k_graham_junction_emit<<<(nch + 7) / 8, 8 * kChunk, 0, h->stream>>>(
+          h->g_chain, h->g_je, h->g_keep, h->g_off, nch, h->stack);
+    }
+    CU(cudaMemcpyAsync(len_d, h->g_off + nch, 4, cudaMemcpyDeviceToDevice, h->stream));
+  } else {
+    h->graham_path = 1;
+    {
+      Launch L(h, "k_gather_chains");
+      k_gather_chains<<<(nch + 7) / 8, 8 * kChunk, 0, h->stream>>>(h->g_chain, h->g_len,
+                                                                   h->g_off, nch, h->g_q0);
+    }
+    {
+      Launch L(h, "k_graham_candidate_seq");
+      k_graham_candidate_seq<<<1, 32, kCandSmem, h->stream>>>(Rx, Ry, h->g_q0, h->g_off + nch, N,
+                                                              h->g_parent, h->g_btop, h->stack,
+                                                              len_d);
+    }
+    uint32_t clen;
+    TRY(read_u32(h, len_d, &clen));
+    if (clen == kNone) return graham_seq_fallback(h, Rx, Ry, Ri);
+  }
+  if (h->debug & GSCAN_DEBUG_CORRUPT_CANDIDATE) {
+    // drop the candidate's last boundary state: the certificate must reject it
+    CU(cudaMemcpyAsync(h->g_btop + nch, h->g_btop + nch - 1, 4, cudaMemcpyDeviceToDevice,
+                       h->stream));
+  }
+  {
+    Launch L(h, "k_graham_certify");
+    k_graham_certify<<<(nch + kCertWarps - 1) / kCertWarps, kCertWarps * 32, 0, h->stream>>>(
+        Rx, Ry, N, h->g_parent, h->g_btop, fail_d);
+  }
+  uint32_t fails;
+  TRY(read_u32(h, fail_d, &fails));
+  h->graham_fails = fails;
+  if (fails == 0 && !(h->debug & GSCAN_DEBUG_FORCE_FALLBACK)) {
+    Launch L(h, "k_graham_emit");
+    k_graham_emit<<<std::max(1u, std::min<uint32_t>((N + kBlock - 1) / kBlock, 1184)), kBlock, 0,
+                    h->stream>>>(h->stack, len_d, Ri, h->d_out, h->ctr);
+    CU(cudaGetLastError());
+    return GSCAN_OK;
+  }
+  return graham_seq_fallback(h, Rx, Ry, Ri);
 }
 
 int validate(gscan_handle* h, uint64_t n, const gscan_config& cfg) {
@@ -613,6 +711,8 @@ int gscan_create(int device, gscan_handle** out) {
     CU(cudaMalloc(&h->scratch64, 16));
     CU(cudaMallocHost(&h->h_ctr, sizeof(Counters)));
     for (auto& e : h->ev) CU(cudaEventCreate(&e));
+    CU(cudaFuncSetAttribute(k_graham_candidate_seq, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)kCandSmem));
     CU(cudaFuncSetAttribute(k_bucket_sort_block, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             kBlockCap * (8 + 8 + 8 + 8 + 4 + 2)));
     CU(cudaFuncSetAttribute(k_bucket_sort_cta, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -772,7 +872,7 @@ int gscan_stage_round1(gscan_handle* h, const double* d_xs, const double* d_ys, 
   CU(cudaSetDevice(h->device));
   TRY(reserve(h, n));
   CU(cudaMemsetAsync(h->ctr, 0, sizeof(Counters), h->stream));
-  TRY(stage_round1(h, d_xs, d_ys, (uint32_t)n, 1));
+  TRY(stage_round1(h, d_xs, d_ys, (uint32_t)n, 1, nullptr, /*ordered=*/true));
   TRY(sync_counters(h));
   *n_out = h->h_ctr->n1;
   CU(cudaMemcpyAsync(d_out, h->surv, (size_t)h->h_ctr->n1 * 4, cudaMemcpyDeviceToDevice, h->stream));
@@ -866,7 +966,7 @@ int gscan_shard_round1(gscan_handle* h, const double* d_xs, const double* d_ys, 
   for (int k = 0; k < 4; ++k) { q.idx[k] = 0; q.qx[k] = global->x[k]; q.qy[k] = global->y[k]; }
   q.ax = global->x[4];
   q.ay = global->y[4];
-  TRY(stage_round1(h, d_xs, d_ys, (uint32_t)n, 1, &q));
+  TRY(stage_round1(h, d_xs, d_ys, (uint32_t)n, 1, &q, /*ordered=*/true));
   TRY(sync_counters(h));
   *n_out = h->h_ctr->n1;
   if (*n_out)

@@ -205,8 +205,12 @@ __device__ __forceinline__ bool quad_keep(const double* qx, const double* qy, co
   return false;
 }
 
-template <bool kVec>
-__global__ void __launch_bounds__(kBlock) k_filter_compact(
+// kOrdered = true: decoupled look-back, survivors in input order (stage API,
+// prefilter.hpp:65-76 compact). kOrdered = false: each CTA reserves its output
+// range with one atomic -- the pipeline's choice, because every later stage
+// orders points by (angle, dist2, input index) and never by survivor slot.
+template <bool kVec, bool kOrdered>
+__global__ void __launch_bounds__(kBlock, 3) k_filter_compact(
     const double* __restrict__ xs, const double* __restrict__ ys, uint32_t n,
     const ExtResult* __restrict__ ext, int enable_round1, uint64_t* __restrict__ status,
     uint32_t* __restrict__ out_idx, Counters* __restrict__ ctr) {
@@ -214,7 +218,7 @@ __global__ void __launch_bounds__(kBlock) k_filter_compact(
   __shared__ uint32_t s_cnt[kFilterPairs][kWarps];
   __shared__ uint32_t s_excl, s_total;
   __shared__ uint32_t s_out[kFilterTile];
-  if (threadIdx.x == 0) s_tile = atomicAdd(&ctr->tile_ticket, 1u);
+  if (threadIdx.x == 0) s_tile = kOrdered ? atomicAdd(&ctr->tile_ticket, 1u) : blockIdx.x;
   double qx[4], qy[4], ex[4], ey[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) { qx[k] = ext->qx[k]; qy[k] = ext->qy[k]; }
@@ -285,11 +289,16 @@ __global__ void __launch_bounds__(kBlock) k_filter_compact(
     s_cnt[lane >> 3][lane & 7] = x0 - v0;
     s_cnt[4 + (lane >> 3)][lane & 7] = tot0 + x1 - v1;
     const uint32_t agg = tot0 + tot1;
-    const uint64_t excl = lookback_exclusive(status, tile, agg);
-    if (lane == 0) {
-      s_excl = (uint32_t)excl;
+    if (kOrdered) {
+      const uint64_t excl = lookback_exclusive(status, tile, agg);
+      if (lane == 0) {
+        s_excl = (uint32_t)excl;
+        s_total = agg;
+        if (base + kFilterTile >= n) ctr->n1 = (uint32_t)(excl + agg);  // last tile
+      }
+    } else if (lane == 0) {
+      s_excl = agg ? atomicAdd(&ctr->n1, agg) : 0u;
       s_total = agg;
-      if (base + kFilterTile >= n) ctr->n1 = (uint32_t)(excl + agg);  // last tile
     }
   }
   __syncthreads();
@@ -397,13 +406,38 @@ __global__ void __launch_bounds__(kBlock) k_scan_u32(const uint32_t* __restrict_
 }
 
 // Scatter each survivor to its slot (bucket start + arrival rank from K3) as
-// two 16-byte records, (key, input index) and (x, y): two full-width random
-// stores per point, no atomics, and the sort pass then reads contiguously.
-struct KeyRec {
+// ONE 32-byte record {key, x, y, input index} written with a single 256-bit
+// store (STG.E.256): a full L2 sector per point, so the random write needs
+// no read-for-ownership of a partially written sector; no atomics.
+struct __align__(32) PtRec {
   uint64_t key;
+  double x, y;
   uint32_t idx;
   uint32_t pad;
 };
+
+__device__ __forceinline__ void st_rec256(PtRec* p, uint64_t key, double x, double y, uint32_t idx) {
+  asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p),
+               "r"((uint32_t)key), "r"((uint32_t)(key >> 32)),
+               "r"((uint32_t)dbits(x)), "r"((uint32_t)(dbits(x) >> 32)),
+               "r"((uint32_t)dbits(y)), "r"((uint32_t)(dbits(y) >> 32)), "r"(idx), "r"(0u)
+               : "memory");
+}
+
+__device__ __forceinline__ PtRec ld_rec256(const PtRec* p) {
+  uint32_t v[8];
+  asm volatile("ld.global.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+                 "=r"(v[6]), "=r"(v[7])
+               : "l"(p));
+  PtRec r;
+  r.key = (uint64_t)v[0] | ((uint64_t)v[1] << 32);
+  r.x = bitsd((uint64_t)v[2] | ((uint64_t)v[3] << 32));
+  r.y = bitsd((uint64_t)v[4] | ((uint64_t)v[5] << 32));
+  r.idx = v[6];
+  r.pad = 0;
+  return r;
+}
 
 __global__ void __launch_bounds__(kBlock) k_scatter(const double* __restrict__ xs,
                                                     const double* __restrict__ ys,
@@ -413,20 +447,14 @@ __global__ void __launch_bounds__(kBlock) k_scatter(const double* __restrict__ x
                                                     const Counters* __restrict__ ctr,
                                                     const uint32_t* __restrict__ bstart,
                                                     double scale, uint32_t nb,
-                                                    KeyRec* __restrict__ rec_k,
-                                                    double2* __restrict__ rec_xy) {
+                                                    PtRec* __restrict__ rec) {
   const uint32_t n1 = ctr->n1;
   for (uint32_t j = blockIdx.x * kBlock + threadIdx.x; j < n1; j += gridDim.x * kBlock) {
     const uint64_t key = keys[j];
     if (key == kKeyDrop) continue;
     const uint32_t i = surv[j];
     const uint32_t pos = bstart[bucket_of(key, scale, nb)] + rank[j];
-    KeyRec r;
-    r.key = key;
-    r.idx = i;
-    r.pad = 0;
-    rec_k[pos] = r;
-    rec_xy[pos] = make_double2(xs[i], ys[i]);
+    st_rec256(&rec[pos], key, xs[i], ys[i], i);
   }
 }
 
@@ -439,7 +467,6 @@ __global__ void __launch_bounds__(kBlock) k_scatter(const double* __restrict__ x
 // Writes the annotated buffer (positions 1.. ; 0 is the anchor).
 constexpr int kSortBlock = 128;
 constexpr int kSortCap = 2048;   // CTA path capacity (shared memory)
-constexpr int kThreadCap = 2048; // per-bucket capacity of the block path (else K4b)
 
 struct BucketBest {  // farthest point candidate for split_regions
   uint64_t d2bits;
@@ -486,12 +513,12 @@ __device__ __forceinline__ void block_best(uint64_t bb, uint32_t bp, BucketBest*
 // an equal point with a lower index shares its bucket (equal points always
 // share angle and dist2). Blocks whose buckets hold more than kBlockCap keys
 // defer those buckets to K4b.
-constexpr int kBucketsPerBlock = 256;
-constexpr int kBlockCap = 2048;
+constexpr int kBucketsPerBlock = 128;
+constexpr int kBlockCap = 1024;
 
 __global__ void __launch_bounds__(kBlock) k_bucket_sort_block(
-    const uint32_t* __restrict__ bstart, const KeyRec* __restrict__ rec_k,
-    const double2* __restrict__ rec_xy, const ExtResult* __restrict__ ext, double scale,
+    const uint32_t* __restrict__ bstart, const PtRec* __restrict__ rec,
+    const ExtResult* __restrict__ ext, double scale,
     uint32_t nb, double* __restrict__ A_x, double* __restrict__ A_y,
     uint32_t* __restrict__ A_idx, BucketBest* __restrict__ partials,
     uint32_t* __restrict__ oversize, Counters* __restrict__ ctr) {
@@ -513,13 +540,12 @@ __global__ void __launch_bounds__(kBlock) k_bucket_sort_block(
   const double ax = ext->ax, ay = ext->ay;
   if (cnt <= (uint32_t)kBlockCap) {
     for (uint32_t t = threadIdx.x; t < cnt; t += kBlock) {
-      const KeyRec r = rec_k[e0 + t];
-      const double2 p = rec_xy[e0 + t];
+      const PtRec r = ld_rec256(&rec[e0 + t]);
       s_key[t] = r.key;
       s_idx[t] = r.idx;
-      s_x[t] = p.x;
-      s_y[t] = p.y;
-      s_d2[t] = dist2_rn(__dsub_rn(p.x, ax), __dsub_rn(p.y, ay));
+      s_x[t] = r.x;
+      s_y[t] = r.y;
+      s_d2[t] = dist2_rn(__dsub_rn(r.x, ax), __dsub_rn(r.y, ay));
       s_lb[t] = (uint16_t)(bucket_of(r.key, scale, nb) - b0);
     }
     __syncthreads();
@@ -543,21 +569,20 @@ __global__ void __launch_bounds__(kBlock) k_bucket_sort_block(
       else best_merge(bb, bp, dbits(dt), pos);
     }
   } else {
-    // rare: an over-full block range; buckets above kThreadCap go to K4b,
+    // rare: an over-full block range; buckets above kBlockCap go to K4b,
     // the rest are sorted here one bucket at a time.
     for (uint32_t lb = 0; lb < nbk; ++lb) {
       const uint32_t sb = s_bs[lb], s = s_bs[lb + 1] - sb;
       if (s == 0) continue;
-      if (s > (uint32_t)kThreadCap) {
+      if (s > (uint32_t)kBlockCap) {
         if (threadIdx.x == 0) oversize[atomicAdd(&ctr->n_oversize, 1u)] = b0 + lb;
         continue;
       }
       __syncthreads();
       for (uint32_t t = threadIdx.x; t < s; t += kBlock) {
-        const KeyRec r = rec_k[sb + t];
-        const double2 p = rec_xy[sb + t];
-        s_key[t] = r.key; s_idx[t] = r.idx; s_x[t] = p.x; s_y[t] = p.y;
-        s_d2[t] = dist2_rn(__dsub_rn(p.x, ax), __dsub_rn(p.y, ay));
+        const PtRec r = ld_rec256(&rec[sb + t]);
+        s_key[t] = r.key; s_idx[t] = r.idx; s_x[t] = r.x; s_y[t] = r.y;
+        s_d2[t] = dist2_rn(__dsub_rn(r.x, ax), __dsub_rn(r.y, ay));
       }
       __syncthreads();
       for (uint32_t t = threadIdx.x; t < s; t += kBlock) {
@@ -583,17 +608,17 @@ __global__ void __launch_bounds__(kBlock) k_bucket_sort_block(
 // K4b: CTA per oversize bucket (grid-stride over the deferred list): rank
 // sort in shared memory up to kSortCap keys, heap sort in global memory
 // beyond that (degenerate inputs: long equal-angle runs). Same dedup/output.
-__device__ __forceinline__ bool rec_less(const KeyRec* k, const double2* p, double ax, double ay,
-                                         uint32_t a, uint32_t b) {
+__device__ __forceinline__ bool rec_less(const PtRec* k, double ax, double ay, uint32_t a,
+                                         uint32_t b) {
   if (k[a].key != k[b].key) return k[a].key < k[b].key;
-  const double da = dist2_rn(__dsub_rn(p[a].x, ax), __dsub_rn(p[a].y, ay));
-  const double db = dist2_rn(__dsub_rn(p[b].x, ax), __dsub_rn(p[b].y, ay));
+  const double da = dist2_rn(__dsub_rn(k[a].x, ax), __dsub_rn(k[a].y, ay));
+  const double db = dist2_rn(__dsub_rn(k[b].x, ax), __dsub_rn(k[b].y, ay));
   if (da != db) return da < db;
   return k[a].idx < k[b].idx;
 }
 
 __global__ void __launch_bounds__(kSortBlock) k_bucket_sort_cta(
-    const uint32_t* __restrict__ bstart, KeyRec* __restrict__ rec_k, double2* __restrict__ rec_xy,
+    const uint32_t* __restrict__ bstart, PtRec* __restrict__ rec,
     const ExtResult* __restrict__ ext, const uint32_t* __restrict__ oversize,
     const Counters* __restrict__ ctr_in, double* __restrict__ A_x, double* __restrict__ A_y,
     uint32_t* __restrict__ A_idx, BucketBest* __restrict__ partials, Counters* __restrict__ ctr) {
@@ -609,77 +634,70 @@ __global__ void __launch_bounds__(kSortBlock) k_bucket_sort_cta(
   for (uint32_t w = blockIdx.x; w < nov; w += gridDim.x) {
     const uint32_t b = oversize[w];
     const uint32_t start = bstart[b], s = bstart[b + 1] - start;
+    const PtRec* R = rec + start;
     if (s <= (uint32_t)kSortCap) {
       __syncthreads();
       for (uint32_t t = threadIdx.x; t < s; t += kSortBlock) {
-        const KeyRec r = rec_k[start + t];
-        const double2 p = rec_xy[start + t];
-        s_key[t] = r.key;
-        s_idx[t] = t;  // local slot; the input index stays in rec_k
-        s_d2[t] = dist2_rn(__dsub_rn(p.x, ax), __dsub_rn(p.y, ay));
+        s_key[t] = R[t].key;
+        s_idx[t] = R[t].idx;
+        s_d2[t] = dist2_rn(__dsub_rn(R[t].x, ax), __dsub_rn(R[t].y, ay));
       }
       __syncthreads();
       for (uint32_t e = threadIdx.x; e < s; e += kSortBlock) {
         const uint64_t ke = s_key[e];
         const double de = s_d2[e];
-        const uint32_t ie = rec_k[start + e].idx;
+        const uint32_t ie = s_idx[e];
         uint32_t r = 0;
-        for (uint32_t j = 0; j < s; ++j)
-          r += key_less(s_key[j], s_d2[j], rec_k[start + j].idx, ke, de, ie);
+        for (uint32_t j = 0; j < s; ++j) r += key_less(s_key[j], s_d2[j], s_idx[j], ke, de, ie);
         s_rank[r] = e;
       }
       __syncthreads();
       for (uint32_t r = threadIdx.x; r < s; r += kSortBlock) {
         const uint32_t e = s_rank[r];
-        const uint32_t i = rec_k[start + e].idx;
-        const double2 p = rec_xy[start + e];
+        const double px = R[e].x, py = R[e].y;
         bool is_dead = false;
         for (int32_t q = (int32_t)r - 1; q >= 0; --q) {
           const uint32_t f = s_rank[q];
           if (s_key[f] != s_key[e] || s_d2[f] != s_d2[e]) break;
-          const double2 pf = rec_xy[start + f];
-          if (pf.x == p.x && pf.y == p.y) { is_dead = true; break; }
+          if (R[f].x == px && R[f].y == py) { is_dead = true; break; }
         }
         const uint32_t pos = 1 + start + r;
-        A_x[pos] = p.x;
-        A_y[pos] = p.y;
-        A_idx[pos] = is_dead ? kDead : i;
+        A_x[pos] = px;
+        A_y[pos] = py;
+        A_idx[pos] = is_dead ? kDead : s_idx[e];
         if (is_dead) ++dead;
         else best_merge(bb, bp, dbits(s_d2[e]), pos);
       }
     } else if (threadIdx.x == 0) {
-      KeyRec* k = rec_k + start;
-      double2* v = rec_xy + start;
+      PtRec* k = rec + start;
       auto sift = [&](uint32_t root, uint32_t len) {
         while (true) {
           uint32_t c = 2 * root + 1;
           if (c >= len) break;
-          if (c + 1 < len && rec_less(k, v, ax, ay, c, c + 1)) ++c;
-          if (!rec_less(k, v, ax, ay, root, c)) break;
-          const KeyRec tk = k[root]; k[root] = k[c]; k[c] = tk;
-          const double2 tv = v[root]; v[root] = v[c]; v[c] = tv;
+          if (c + 1 < len && rec_less(k, ax, ay, c, c + 1)) ++c;
+          if (!rec_less(k, ax, ay, root, c)) break;
+          const PtRec t = k[root]; k[root] = k[c]; k[c] = t;
           root = c;
         }
       };
       for (int64_t r = (int64_t)s / 2 - 1; r >= 0; --r) sift((uint32_t)r, s);
       for (uint32_t len = s; len > 1; --len) {
-        const KeyRec tk = k[0]; k[0] = k[len - 1]; k[len - 1] = tk;
-        const double2 tv = v[0]; v[0] = v[len - 1]; v[len - 1] = tv;
+        const PtRec t = k[0]; k[0] = k[len - 1]; k[len - 1] = t;
         sift(0, len - 1);
       }
       uint32_t run_start = 0;
       double prev_d2 = 0.0;
       for (uint32_t r = 0; r < s; ++r) {
-        const double2 p = v[r];
-        const double d2 = dist2_rn(__dsub_rn(p.x, ax), __dsub_rn(p.y, ay));
+        const double px = k[r].x, py = k[r].y;
+        const double d2 = dist2_rn(__dsub_rn(px, ax), __dsub_rn(py, ay));
         if (r > 0 && (k[r - 1].key != k[r].key || prev_d2 != d2)) run_start = r;
         prev_d2 = d2;
         bool is_dead = false;
         for (uint32_t q = run_start; q < r; ++q)
-          if (v[q].x == p.x && v[q].y == p.y) { is_dead = true; break; }
+          if (k[q].x == px && k[q].y == py) { is_dead = true; break; }
         const uint32_t pos = 1 + start + r;
-        A_x[pos] = p.x;
-        A_y[pos] = p.y;
+        A_x[pos] = px;
+        A_y[pos] = py;
         A_idx[pos] = is_dead ? kDead : k[r].idx;
         if (is_dead) ++dead;
         else best_merge(bb, bp, dbits(d2), pos);

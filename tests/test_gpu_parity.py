@@ -110,14 +110,15 @@ def test_circle_keeps_everything(engine, oracle_mod):
 
 
 @pytest.mark.parametrize("kind", KINDS + ("grid",))
-@pytest.mark.parametrize("flags", ["junction", "sequential", "corrupt", "fallback"])
+@pytest.mark.parametrize("flags", ["junction", "sequential", "prefix", "corrupt", "fallback"])
 def test_graham_paths_are_exact(engine, oracle_mod, kind, flags):
     """Every Graham strategy (and the certificate's rejection of a falsified
     candidate) yields the sequential scan's exact output (pipeline.hpp:57-67)."""
     from paper_1508_05931_b200 import _native as N
 
     f = {"junction": N.DEBUG_FORCE_JUNCTION, "sequential": N.DEBUG_FORCE_SEQUENTIAL,
-         "corrupt": N.DEBUG_CORRUPT_CANDIDATE, "fallback": N.DEBUG_FORCE_FALLBACK}[flags]
+         "prefix": N.DEBUG_FORCE_PREFIX, "corrupt": N.DEBUG_CORRUPT_CANDIDATE,
+         "fallback": N.DEBUG_FORCE_FALLBACK}[flags]
     try:
         engine.set_debug(f)
         for n, seed in ((300, 1), (5000, 2), (40000, 3)):
