@@ -132,7 +132,7 @@ void free_buffers(gscan_handle* h) {
 constexpr uint32_t kCtaSortGrid = 296;
 
 uint32_t buckets_for(uint64_t n) {
-  uint64_t want = (n + 3) / 4;
+  uint64_t want = (n + 7) / 8;
   uint32_t nb = 1;
   while (nb < want && nb < (1u << 24)) nb <<= 1;
   return nb;
@@ -261,14 +261,40 @@ int stage_round1(gscan_handle* h, const double* xs, const double* ys, uint32_t n
   return GSCAN_OK;
 }
 
-// K3 .. K4: keys, bucket offsets, scatter, per-bucket sort + dedup, anchor
-// at position 0, split_regions. Leaves the annotated buffer in A_*.
-int stage_annotate_sort(gscan_handle* h, const double* xs, const double* ys, uint32_t n,
-                        int t_annot_ev, int t_sort_ev) {
+// K1 + fused K2/K3 (pipeline path): extremes, then filter + keys + bucket
+// ranks in one pass. Leaves survivors/keys/ranks and n1, hist filled.
+int stage_round1_keys(gscan_handle* h, const double* xs, const double* ys, uint32_t n, int enable) {
+  const bool vec = aligned16(xs) && aligned16(ys);
+  {
+    const uint32_t grid =
+        std::max(1u, std::min<uint32_t>((n + kBlock * 8 - 1) / (kBlock * 8), h->sm_count * 8));
+    Launch L(h, "k_extremes");
+    if (vec) k_extremes<true><<<grid, kBlock, 0, h->stream>>>(xs, ys, n, h->partials, h->ext, h->ctr);
+    else k_extremes<false><<<grid, kBlock, 0, h->stream>>>(xs, ys, n, h->partials, h->ext, h->ctr);
+  }
   const uint32_t nb = buckets_for(n);
   const double scale = (double)nb / kPi;
   CU(cudaMemsetAsync(h->hist, 0, (nb + 1) * 4, h->stream));
+  const uint64_t tiles = (n + kFusedTile - 1) / kFusedTile;
   {
+    Launch L(h, "k_filter_keys");
+#define KF_ARGS xs, ys, n, h->ext, enable, scale, nb, h->hist, h->surv, h->keys, h->rank, h->ctr
+    if (vec) k_filter_keys<true><<<tiles, kBlock, 0, h->stream>>>(KF_ARGS);
+    else k_filter_keys<false><<<tiles, kBlock, 0, h->stream>>>(KF_ARGS);
+#undef KF_ARGS
+  }
+  CU(cudaGetLastError());
+  return GSCAN_OK;
+}
+
+// K3 .. K4: keys, bucket offsets, scatter, per-bucket sort + dedup, anchor
+// at position 0, split_regions. Leaves the annotated buffer in A_*.
+int stage_annotate_sort(gscan_handle* h, const double* xs, const double* ys, uint32_t n,
+                        int t_annot_ev, int t_sort_ev, bool keys_done = false) {
+  const uint32_t nb = buckets_for(n);
+  const double scale = (double)nb / kPi;
+  if (!keys_done) CU(cudaMemsetAsync(h->hist, 0, (nb + 1) * 4, h->stream));
+  if (!keys_done) {
     const uint32_t grid = std::max(1u, std::min<uint32_t>((n + kBlock - 1) / kBlock, h->sm_count * 16));
     Launch L(h, "k_keys");
     k_keys<<<grid, kBlock, 0, h->stream>>>(xs, ys, h->surv, h->ext, h->ctr, h->keys, h->rank,
@@ -381,9 +407,8 @@ int stage_round2(gscan_handle* h, const gscan_config& cfg, double** Rx, double**
   CU(cudaMemsetAsync(h->flags, 1, m, h->stream));
   const uint32_t slices = g.n_right + g.n_left;
   if (slices) {
-    const uint32_t grid = (slices * 32 + kBlock - 1) / kBlock;
-    Launch L(h, "k_round2_walk");
-    k_round2_walk<<<grid, kBlock, 0, h->stream>>>(h->A_x, h->A_y, g, h->flags);
+    Launch L(h, "k_round2_block");
+    k_round2_block<<<slices, kWalkBlock, 0, h->stream>>>(h->A_x, h->A_y, g, h->flags);
   }
   const uint64_t tiles = (m + kCompactTile - 1) / kCompactTile;
   TRY(reset_lookback(h, tiles));
@@ -618,9 +643,10 @@ int run_pipeline(gscan_handle* h, const double* xs, const double* ys, uint64_t n
   h->kt_used = 0;
   CU(cudaEventRecord(h->ev[0], h->stream));
   CU(cudaMemsetAsync(h->ctr, 0, sizeof(Counters), h->stream));
-  TRY(stage_round1(h, xs, ys, n, cfg.enable_round1));
+  TRY(stage_round1_keys(h, xs, ys, n, cfg.enable_round1));
   CU(cudaEventRecord(h->ev[1], h->stream));
-  TRY(stage_annotate_sort(h, xs, ys, n, 2, 3));
+  CU(cudaEventRecord(h->ev[2], h->stream));  // annotate (keys) is fused into round 1
+  TRY(stage_annotate_sort(h, xs, ys, n, -1, 3, /*keys_done=*/true));
   double *Rx, *Ry;
   uint32_t* Ri;
   TRY(stage_round2(h, cfg, &Rx, &Ry, &Ri));

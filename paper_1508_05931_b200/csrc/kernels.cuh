@@ -369,6 +369,132 @@ __global__ void __launch_bounds__(kBlock) k_keys(const double* __restrict__ xs,
 }
 
 // ===========================================================================
+// K2+K3 fused (the pipeline's round-1 kernel): classify_quad + compact
+// (prefilter.hpp:47-76) AND, for each survivor, its polar key (geom.hpp:38-43
+// via the glibc-identical atan2), its angle bucket and its arrival rank in the
+// bucket. The FP64 key work hides under the tile's HBM stream. Each CTA
+// reserves its output range with one atomic (survivor order is irrelevant:
+// the sort orders by (angle, dist2, input index)).
+constexpr int kFusedPairs = 4;                       // 8 points per thread
+constexpr int kFusedTile = kBlock * kFusedPairs * 2; // 2048 points per CTA
+
+template <bool kVec>
+__global__ void __launch_bounds__(kBlock, 3) k_filter_keys(
+    const double* __restrict__ xs, const double* __restrict__ ys, uint32_t n,
+    const ExtResult* __restrict__ ext, int enable_round1, double scale, uint32_t nb,
+    uint32_t* __restrict__ hist, uint32_t* __restrict__ out_idx, uint64_t* __restrict__ keys,
+    uint32_t* __restrict__ rank, Counters* __restrict__ ctr) {
+  __shared__ uint32_t s_cnt[kFusedPairs][kWarps];
+  __shared__ uint32_t s_excl, s_total;
+  __shared__ uint32_t s_idx[kFusedTile];
+  __shared__ uint32_t s_rank[kFusedTile];
+  __shared__ uint64_t s_key[kFusedTile];
+  double qx[4], qy[4], ex[4], ey[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) { qx[k] = ext->qx[k]; qy[k] = ext->qy[k]; }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    ex[k] = __dsub_rn(qx[(k + 1) & 3], qx[k]);
+    ey[k] = __dsub_rn(qy[(k + 1) & 3], qy[k]);
+  }
+  const double ax = ext->ax, ay = ext->ay;
+  const uint32_t base = blockIdx.x * (uint32_t)kFusedTile;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t lt = lanemask_lt();
+  double vx[kFusedPairs][2], vy[kFusedPairs][2];
+  if (kVec) {
+    const double2* x2 = reinterpret_cast<const double2*>(xs);
+    const double2* y2 = reinterpret_cast<const double2*>(ys);
+#pragma unroll
+    for (int k = 0; k < kFusedPairs; ++k) {
+      const uint32_t i0 = base + 2u * (k * kBlock + threadIdx.x);
+      if (i0 + 1 < n) {
+        const double2 a = __ldcs(&x2[i0 >> 1]), b = __ldcs(&y2[i0 >> 1]);
+        vx[k][0] = a.x; vx[k][1] = a.y; vy[k][0] = b.x; vy[k][1] = b.y;
+      } else if (i0 < n) {
+        vx[k][0] = xs[i0]; vy[k][0] = ys[i0]; vx[k][1] = 0.0; vy[k][1] = 0.0;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < kFusedPairs; ++k) {
+      const uint32_t i0 = base + 2u * (k * kBlock + threadIdx.x);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        vx[k][h] = (i0 + h < n) ? xs[i0 + h] : 0.0;
+        vy[k][h] = (i0 + h < n) ? ys[i0 + h] : 0.0;
+      }
+    }
+  }
+  uint32_t b0[kFusedPairs], b1[kFusedPairs];
+#pragma unroll
+  for (int k = 0; k < kFusedPairs; ++k) {
+    const uint32_t i0 = base + 2u * (k * kBlock + threadIdx.x);
+    const bool k0 = i0 < n && (!enable_round1 || quad_keep(qx, qy, ex, ey, vx[k][0], vy[k][0]));
+    const bool k1 = i0 + 1 < n && (!enable_round1 || quad_keep(qx, qy, ex, ey, vx[k][1], vy[k][1]));
+    b0[k] = __ballot_sync(0xffffffffu, k0);
+    b1[k] = __ballot_sync(0xffffffffu, k1);
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < kFusedPairs; ++k) s_cnt[k][warp] = __popc(b0[k]) + __popc(b1[k]);
+  }
+  __syncthreads();
+  if (warp == 0) {  // exclusive scan of the 32 (stripe, warp) counts in point order
+    const uint32_t v = s_cnt[lane >> 3][lane & 7];
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    const uint32_t tot = __shfl_sync(0xffffffffu, x, 31);
+    s_cnt[lane >> 3][lane & 7] = x - v;
+    if (lane == 0) {
+      s_total = tot;
+      s_excl = tot ? atomicAdd(&ctr->n1, tot) : 0u;
+    }
+  }
+  __syncthreads();
+  // keys for this thread's survivors; rank = arrival order in the bucket
+  uint32_t drops = 0;
+#pragma unroll
+  for (int k = 0; k < kFusedPairs; ++k) {
+    uint32_t r = s_cnt[k][warp] + __popc(b0[k] & lt) + __popc(b1[k] & lt);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint32_t m = h ? b1[k] : b0[k];
+      if (m & (1u << lane)) {
+        const double x = vx[k][h], y = vy[k][h];
+        uint64_t key;
+        uint32_t b;
+        if (x == ax && y == ay) {
+          key = kKeyDrop;
+          b = nb;
+          ++drops;
+        } else {
+          const double ang = glibc_atan2(__dsub_rn(y, ay), __dsub_rn(x, ax));
+          key = (ang == 0.0) ? 0ull : dbits(ang);
+          b = bucket_of(key, scale, nb);
+        }
+        s_idx[r] = base + 2u * (k * kBlock + threadIdx.x) + h;
+        s_key[r] = key;
+        s_rank[r] = atomicAdd(&hist[b], 1u);
+        ++r;
+      }
+    }
+  }
+  if (drops) atomicAdd(&ctr->anchor_dups, drops);
+  __syncthreads();
+  const uint32_t total = s_total, off = s_excl;
+  for (uint32_t r = threadIdx.x; r < total; r += kBlock) {
+    out_idx[off + r] = s_idx[r];
+    keys[off + r] = s_key[r];
+    rank[off + r] = s_rank[r];
+  }
+}
+
+// ===========================================================================
 // Device-wide exclusive scan of uint32 counts (decoupled look-back); used for
 // bucket offsets. out[i] = sum(in[0..i)); out[n] = total when n_out > n.
 constexpr int kScanItems = 8;
@@ -420,8 +546,7 @@ __device__ __forceinline__ void st_rec256(PtRec* p, uint64_t key, double x, doub
   asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p),
                "r"((uint32_t)key), "r"((uint32_t)(key >> 32)),
                "r"((uint32_t)dbits(x)), "r"((uint32_t)(dbits(x) >> 32)),
-               "r"((uint32_t)dbits(y)), "r"((uint32_t)(dbits(y) >> 32)), "r"(idx), "r"(0u)
-               : "memory");
+               "r"((uint32_t)dbits(y)), "r"((uint32_t)(dbits(y) >> 32)), "r"(idx), "r"(0u));
 }
 
 __device__ __forceinline__ PtRec ld_rec256(const PtRec* p) {
@@ -439,6 +564,8 @@ __device__ __forceinline__ PtRec ld_rec256(const PtRec* p) {
   return r;
 }
 
+constexpr int kScatterItems = 4;
+
 __global__ void __launch_bounds__(kBlock) k_scatter(const double* __restrict__ xs,
                                                     const double* __restrict__ ys,
                                                     const uint64_t* __restrict__ keys,
@@ -449,12 +576,29 @@ __global__ void __launch_bounds__(kBlock) k_scatter(const double* __restrict__ x
                                                     double scale, uint32_t nb,
                                                     PtRec* __restrict__ rec) {
   const uint32_t n1 = ctr->n1;
-  for (uint32_t j = blockIdx.x * kBlock + threadIdx.x; j < n1; j += gridDim.x * kBlock) {
-    const uint64_t key = keys[j];
-    if (key == kKeyDrop) continue;
-    const uint32_t i = surv[j];
-    const uint32_t pos = bstart[bucket_of(key, scale, nb)] + rank[j];
-    st_rec256(&rec[pos], key, xs[i], ys[i], i);
+  const uint32_t stride = gridDim.x * kBlock * kScatterItems;
+  for (uint32_t j0 = blockIdx.x * kBlock * kScatterItems + threadIdx.x; j0 < n1; j0 += stride) {
+    // three dependent load levels, issued kScatterItems-wide for MLP
+    uint64_t key[kScatterItems];
+    uint32_t i[kScatterItems], rk[kScatterItems], pos[kScatterItems];
+    double x[kScatterItems], y[kScatterItems];
+#pragma unroll
+    for (int u = 0; u < kScatterItems; ++u) {
+      const uint32_t j = j0 + u * kBlock;
+      key[u] = kKeyDrop;
+      if (j < n1) { key[u] = keys[j]; i[u] = surv[j]; rk[u] = rank[j]; }
+    }
+#pragma unroll
+    for (int u = 0; u < kScatterItems; ++u) {
+      if (key[u] != kKeyDrop) {
+        pos[u] = bstart[bucket_of(key[u], scale, nb)] + rk[u];
+        x[u] = xs[i[u]];
+        y[u] = ys[i[u]];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kScatterItems; ++u)
+      if (key[u] != kKeyDrop) st_rec256(&rec[pos[u]], key[u], x[u], y[u], i[u]);
   }
 }
 
@@ -534,72 +678,61 @@ __global__ void __launch_bounds__(kBlock) k_bucket_sort_block(
   const uint32_t nbk = min((uint32_t)kBucketsPerBlock, nb - b0);
   for (uint32_t t = threadIdx.x; t <= nbk; t += kBlock) s_bs[t] = bstart[b0 + t];
   __syncthreads();
-  const uint32_t e0 = s_bs[0], cnt = s_bs[nbk] - e0;
   uint64_t bb = 0;
   uint32_t bp = 0xffffffffu, dead = 0;
   const double ax = ext->ax, ay = ext->ay;
-  if (cnt <= (uint32_t)kBlockCap) {
-    for (uint32_t t = threadIdx.x; t < cnt; t += kBlock) {
-      const PtRec r = ld_rec256(&rec[e0 + t]);
-      s_key[t] = r.key;
-      s_idx[t] = r.idx;
-      s_x[t] = r.x;
-      s_y[t] = r.y;
-      s_d2[t] = dist2_rn(__dsub_rn(r.x, ax), __dsub_rn(r.y, ay));
-      s_lb[t] = (uint16_t)(bucket_of(r.key, scale, nb) - b0);
+  __shared__ uint32_t s_win;
+  // windows of consecutive buckets holding at most kBlockCap keys (usually
+  // one window covers all kBucketsPerBlock buckets)
+  uint32_t lb0 = 0;
+  while (lb0 < nbk) {
+    // largest lb1 with s_bs[lb1] - s_bs[lb0] <= kBlockCap (bucket starts are monotone)
+    if (threadIdx.x == 0) s_win = lb0;
+    __syncthreads();
+    for (uint32_t t = lb0 + 1 + threadIdx.x; t <= nbk; t += kBlock)
+      if (s_bs[t] - s_bs[lb0] <= (uint32_t)kBlockCap) atomicMax(&s_win, t);
+    __syncthreads();
+    if (threadIdx.x == 0 && s_win == lb0) {  // one bucket above capacity: defer to K4b
+      if (s_bs[lb0 + 1] > s_bs[lb0]) oversize[atomicAdd(&ctr->n_oversize, 1u)] = b0 + lb0;
+      s_win = (lb0 + 1) | 0x80000000u;
     }
     __syncthreads();
-    for (uint32_t t = threadIdx.x; t < cnt; t += kBlock) {
-      const uint32_t lb = s_lb[t];
-      const uint32_t sb = s_bs[lb] - e0, se = s_bs[lb + 1] - e0;
-      const uint64_t kt = s_key[t];
-      const double dt = s_d2[t], xt = s_x[t], yt = s_y[t];
-      const uint32_t it = s_idx[t];
-      uint32_t r = 0;
-      bool is_dead = false;
-      for (uint32_t j = sb; j < se; ++j) {
-        r += key_less(s_key[j], s_d2[j], s_idx[j], kt, dt, it);
-        is_dead |= (s_x[j] == xt && s_y[j] == yt && s_idx[j] < it);
-      }
-      const uint32_t pos = 1 + e0 + sb + r;
-      A_x[pos] = xt;
-      A_y[pos] = yt;
-      A_idx[pos] = is_dead ? kDead : it;
-      if (is_dead) ++dead;
-      else best_merge(bb, bp, dbits(dt), pos);
-    }
-  } else {
-    // rare: an over-full block range; buckets above kBlockCap go to K4b,
-    // the rest are sorted here one bucket at a time.
-    for (uint32_t lb = 0; lb < nbk; ++lb) {
-      const uint32_t sb = s_bs[lb], s = s_bs[lb + 1] - sb;
-      if (s == 0) continue;
-      if (s > (uint32_t)kBlockCap) {
-        if (threadIdx.x == 0) oversize[atomicAdd(&ctr->n_oversize, 1u)] = b0 + lb;
-        continue;
-      }
-      __syncthreads();
-      for (uint32_t t = threadIdx.x; t < s; t += kBlock) {
-        const PtRec r = ld_rec256(&rec[sb + t]);
-        s_key[t] = r.key; s_idx[t] = r.idx; s_x[t] = r.x; s_y[t] = r.y;
+    const uint32_t wv = s_win;
+    const uint32_t lb1 = wv & 0x7fffffffu;
+    if (!(wv & 0x80000000u)) {
+      const uint32_t e0 = s_bs[lb0], cnt = s_bs[lb1] - e0;
+      for (uint32_t t = threadIdx.x; t < cnt; t += kBlock) {
+        const PtRec r = ld_rec256(&rec[e0 + t]);
+        s_key[t] = r.key;
+        s_idx[t] = r.idx;
+        s_x[t] = r.x;
+        s_y[t] = r.y;
         s_d2[t] = dist2_rn(__dsub_rn(r.x, ax), __dsub_rn(r.y, ay));
+        s_lb[t] = (uint16_t)(bucket_of(r.key, scale, nb) - b0);
       }
       __syncthreads();
-      for (uint32_t t = threadIdx.x; t < s; t += kBlock) {
+      for (uint32_t t = threadIdx.x; t < cnt; t += kBlock) {
+        const uint32_t lb = s_lb[t];
+        const uint32_t sb = s_bs[lb] - e0, se = s_bs[lb + 1] - e0;
+        const uint64_t kt = s_key[t];
+        const double dt = s_d2[t], xt = s_x[t], yt = s_y[t];
+        const uint32_t it = s_idx[t];
         uint32_t r = 0;
         bool is_dead = false;
-        for (uint32_t j = 0; j < s; ++j) {
-          r += key_less(s_key[j], s_d2[j], s_idx[j], s_key[t], s_d2[t], s_idx[t]);
-          is_dead |= (s_x[j] == s_x[t] && s_y[j] == s_y[t] && s_idx[j] < s_idx[t]);
+        for (uint32_t j = sb; j < se; ++j) {
+          r += key_less(s_key[j], s_d2[j], s_idx[j], kt, dt, it);
+          is_dead |= (s_x[j] == xt && s_y[j] == yt && s_idx[j] < it);
         }
-        const uint32_t pos = 1 + sb + r;
-        A_x[pos] = s_x[t];
-        A_y[pos] = s_y[t];
-        A_idx[pos] = is_dead ? kDead : s_idx[t];
+        const uint32_t pos = 1 + e0 + sb + r;
+        A_x[pos] = xt;
+        A_y[pos] = yt;
+        A_idx[pos] = is_dead ? kDead : it;
         if (is_dead) ++dead;
-        else best_merge(bb, bp, dbits(s_d2[t]), pos);
+        else best_merge(bb, bp, dbits(dt), pos);
       }
     }
+    __syncthreads();
+    lb0 = lb1;
   }
   if (dead) atomicAdd(&ctr->dead, dead);
   block_best<kBlock>(bb, bp, &partials[blockIdx.x]);
@@ -939,6 +1072,175 @@ __global__ void __launch_bounds__(kBlock) k_round2_walk(const double* __restrict
         tth = __shfl_sync(0xffffffffu, th, last);
       }
       i += 32;
+    }
+  }
+}
+
+// K5 (block version): one CTA per slice, 1024 walk steps per window. Same
+// speculate-then-verify contract as the warp version above, with a block-wide
+// max-scan of (phi', walk index): phi' is a pseudo-angle of P - P_l (one
+// division, monotone in the true angle; sign-flipped for the left region),
+// the running maximum's element is the speculated temp of every step, each
+// step is verified with the exact orient(), and the window restarts after the
+// first disagreement with the exact decision applied.
+constexpr int kWalkBlock = 256;
+constexpr int kWalkItems = 4;
+constexpr int kWalkWin = kWalkBlock * kWalkItems;
+
+__device__ __forceinline__ double pseudo_angle(double px, double py, double lx, double ly,
+                                               double ux, double uy) {
+  const double vx = px - lx, vy = py - ly;
+  const double c = ux * vx + uy * vy;   // along P_l -> anchor
+  const double sn = ux * vy - uy * vx;  // across
+  const double as = fabs(sn), den = fabs(c) + as;
+  if (den == 0.0) return 0.0;
+  const double t = 1.0 - c / den;      // [0, 2], increasing with the angle from u
+  return sn >= 0.0 ? t : -t;
+}
+
+struct MaxPair {  // running maximum by (phi, walk index): the latest maximum wins
+  double v;
+  int32_t k;
+};
+__device__ __forceinline__ MaxPair mp_max(MaxPair a, MaxPair b) {
+  return (b.v > a.v || (b.v == a.v && b.k > a.k)) ? b : a;
+}
+
+__global__ void __launch_bounds__(kWalkBlock) k_round2_block(const double* __restrict__ A_x,
+                                                             const double* __restrict__ A_y,
+                                                             SliceGeom g,
+                                                             uint8_t* __restrict__ flags) {
+  const uint32_t slice = blockIdx.x;
+  uint32_t seed, start, count;
+  int dir;
+  if (slice < g.n_right) {
+    dir = 1;
+    if (g.chunked) {
+      const uint32_t begin = 1 + slice * g.step_r;
+      const uint32_t end = min(begin + g.step_r, g.l);
+      seed = begin; start = begin + 1; count = end - begin - 1;
+    } else {
+      seed = 0; start = 1; count = g.l - 1;
+    }
+  } else {
+    dir = -1;
+    const uint32_t sl = slice - g.n_right;
+    const uint32_t m_left = g.m - 1 - g.l;
+    if (g.chunked) {
+      const uint32_t pos = sl * g.step_l;
+      seed = g.m - 1 - pos;
+      const uint32_t off = min(pos + g.step_l - 1, m_left - 1);
+      const uint32_t lo = g.m - 1 - off;
+      start = seed - 1; count = seed - lo;
+    } else {
+      seed = g.m - 1; start = g.m - 2; count = g.m - 2 - g.l;
+    }
+  }
+  if (count == 0) return;
+  __shared__ MaxPair s_wm[kWalkBlock / 32];
+  __shared__ int32_t s_first;
+  __shared__ MaxPair s_carry;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double lx = A_x[g.l], ly = A_y[g.l];
+  const double ux = A_x[0] - lx, uy = A_y[0] - ly;
+  const double sgn = (dir > 0) ? 1.0 : -1.0;
+  // walk index -1 = the seed; position of walk index k: start +- k
+  auto wpos = [&](int32_t k) -> uint32_t {
+    return k < 0 ? seed : ((dir > 0) ? start + (uint32_t)k : start - (uint32_t)k);
+  };
+  MaxPair carry;
+  carry.v = sgn * pseudo_angle(A_x[seed], A_y[seed], lx, ly, ux, uy);
+  carry.k = -1;
+  int32_t w0 = 0;
+  while (w0 < (int32_t)count) {
+    // load this thread's kWalkItems consecutive walk steps
+    double px[kWalkItems], py[kWalkItems], ph[kWalkItems];
+    bool val[kWalkItems];
+    const int32_t k0 = w0 + threadIdx.x * kWalkItems;
+#pragma unroll
+    for (int u = 0; u < kWalkItems; ++u) {
+      const int32_t k = k0 + u;
+      val[u] = k < (int32_t)count;
+      if (val[u]) {
+        const uint32_t p = wpos(k);
+        px[u] = A_x[p];
+        py[u] = A_y[p];
+        ph[u] = sgn * pseudo_angle(px[u], py[u], lx, ly, ux, uy);
+      } else {
+        px[u] = py[u] = 0.0;
+        ph[u] = -1e300;
+      }
+    }
+    // thread aggregate, then block exclusive max-scan
+    MaxPair agg{-1e300, INT32_MIN};
+#pragma unroll
+    for (int u = 0; u < kWalkItems; ++u)
+      if (val[u]) agg = mp_max(agg, MaxPair{ph[u], k0 + u});
+    MaxPair inc = agg;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      MaxPair y;
+      y.v = __shfl_up_sync(0xffffffffu, inc.v, o);
+      y.k = __shfl_up_sync(0xffffffffu, inc.k, o);
+      if (lane >= o) inc = mp_max(inc, y);
+    }
+    if (lane == 31) s_wm[warp] = inc;
+    if (threadIdx.x == 0) s_first = INT32_MAX;
+    __syncthreads();
+    MaxPair ex = carry;
+    for (int w = 0; w < warp; ++w) ex = mp_max(ex, s_wm[w]);
+    MaxPair prev;
+    prev.v = __shfl_up_sync(0xffffffffu, inc.v, 1);
+    prev.k = __shfl_up_sync(0xffffffffu, inc.k, 1);
+    if (lane > 0) ex = mp_max(ex, prev);
+    // per step: speculated temp = running max before it; verify exactly
+    bool cand_keep[kWalkItems], ex_disc[kWalkItems];
+    int32_t tk[kWalkItems];
+#pragma unroll
+    for (int u = 0; u < kWalkItems; ++u) {
+      tk[u] = ex.k;
+      cand_keep[u] = val[u] && ph[u] >= ex.v;
+      ex_disc[u] = false;
+      if (val[u]) {
+        const uint32_t tp = wpos(ex.k);
+        const double c = cross_rn(A_x[tp], A_y[tp], lx, ly, px[u], py[u]);
+        ex_disc[u] = (dir > 0) ? (c > 0.0) : (c < 0.0);
+        if (ex_disc[u] == cand_keep[u]) atomicMin(&s_first, k0 + u);
+        ex = mp_max(ex, MaxPair{ph[u], k0 + u});
+      }
+    }
+    __syncthreads();
+    const int32_t f = s_first;
+#pragma unroll
+    for (int u = 0; u < kWalkItems; ++u) {
+      const int32_t k = k0 + u;
+      if (!val[u] || k > f) continue;
+      const bool disc = (k < f) ? !cand_keep[u] : ex_disc[u];
+      if (disc) flags[wpos(k)] = 0;
+      if (k == f) {  // the exact decision fixes the temp after step f
+        MaxPair nc;
+        if (ex_disc[u]) {
+          const uint32_t tp = wpos(tk[u]);
+          nc.v = sgn * pseudo_angle(A_x[tp], A_y[tp], lx, ly, ux, uy);
+          nc.k = tk[u];
+        } else {
+          nc.v = ph[u];
+          nc.k = k;
+        }
+        s_carry = nc;
+      }
+    }
+    if (f == INT32_MAX) {
+      // whole window verified: carry = running max through the window
+      MaxPair tot = carry;
+      for (int w = 0; w < kWalkBlock / 32; ++w) tot = mp_max(tot, s_wm[w]);
+      carry = tot;
+      w0 += kWalkWin;
+      __syncthreads();
+    } else {
+      __syncthreads();
+      carry = s_carry;
+      w0 = f + 1;
     }
   }
 }

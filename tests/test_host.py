@@ -34,7 +34,7 @@ def test_library_is_sm100a():
 def test_no_fma_in_predicate_kernels():
     """geom.hpp:19-21 cross() is unfused; the device build must not contract it."""
     out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", "-fun",
-                          "_ZN5gscan13k_round2_walkEPKdS1_NS_9SliceGeomEPh",
+                          "_ZN5gscan14k_round2_blockEPKdS1_NS_9SliceGeomEPh",
                           str(ROOT / "paper_1508_05931_b200/_lib/libgscan.so")],
                          capture_output=True, text=True)
     sass = out.stdout
