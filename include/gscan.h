@@ -171,13 +171,24 @@ enum {
     GSCAN_DEBUG_FORCE_SEQUENTIAL = 1u << 1, /* Graham candidate via chains-of-chains scan */
     GSCAN_DEBUG_CORRUPT_CANDIDATE = 1u << 2,/* falsify the candidate: certificate must fail */
     GSCAN_DEBUG_FORCE_FALLBACK = 1u << 3,   /* always finish with the sequential kernel */
-    GSCAN_DEBUG_FORCE_PREFIX = 1u << 4      /* Graham candidate via prefix scan of states */
+    GSCAN_DEBUG_FORCE_PREFIX = 1u << 4,     /* Graham candidate via prefix scan of states */
+    GSCAN_DEBUG_FULL_SORT = 1u << 5,        /* skip the sparse round-2 path: sort every survivor */
+    GSCAN_DEBUG_SPARSE_DROP = 1u << 6       /* sparse path walks no candidates: its verification
+                                               must reject the result and the call falls back */
 };
 int gscan_set_debug(gscan_handle* h, uint32_t flags);
 /* path: 0 = sequential kernel only (tiny input), 1 = chain scan + certificate,
  * 2 = junctions + certificate, 3 = prefix-scanned states + certificate;
  * bit 4 set = certificate failed or fallback forced. */
 int gscan_last_graham_info(const gscan_handle* h, uint32_t* path, uint32_t* certificate_failures);
+
+/* Sparse round-2 path of the last call (the default for n >= 65536 with the
+ * default toggles): used = 1 when its result was returned; fail_bits != 0
+ * when it declined and the full sort ran instead (tie for the farthest point,
+ * duplicates, a failed verification, ...); n_walked = points it sorted and
+ * walked exactly (gathered + candidates + anchor). */
+int gscan_last_sparse_info(const gscan_handle* h, uint32_t* used, uint32_t* fail_bits,
+                           uint32_t* n_walked);
 
 /* ---- harness helpers (host) ---- */
 enum { GSCAN_GEN_SQUARE = 0, GSCAN_GEN_DISK = 1, GSCAN_GEN_CIRCLE = 2, GSCAN_GEN_COLLINEAR = 3 };

@@ -29,6 +29,8 @@ DEBUG_FORCE_SEQUENTIAL = 1 << 1
 DEBUG_CORRUPT_CANDIDATE = 1 << 2
 DEBUG_FORCE_FALLBACK = 1 << 3
 DEBUG_FORCE_PREFIX = 1 << 4
+DEBUG_FULL_SORT = 1 << 5
+DEBUG_SPARSE_DROP = 1 << 6
 
 
 class NativeUnavailable(RuntimeError):
@@ -81,6 +83,8 @@ SIGNATURES = {
     "gscan_set_profiling": (C.c_int, [_P, C.c_int]),
     "gscan_set_debug": (C.c_int, [_P, C.c_uint32]),
     "gscan_last_graham_info": (C.c_int, [_P, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]),
+    "gscan_last_sparse_info": (C.c_int, [_P, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32),
+                                         C.POINTER(C.c_uint32)]),
     "gscan_last_kernel_times": (C.c_int, [_P, C.POINTER(C.c_char_p), _DP, C.c_int]),
     "gscan_generate": (C.c_int, [C.c_int, _U64, _U64, _DP, _DP]),
     "gscan_generate_grid": (C.c_int, [_U64, _U64, C.c_int, C.c_int, _DP, _DP]),

@@ -13,6 +13,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -21,6 +22,7 @@
 #include "../../include/gscan.h"
 #include "kernels.cuh"
 #include "graham.cuh"
+#include "sparse.cuh"
 
 using namespace gscan;
 
@@ -85,6 +87,31 @@ struct gscan_handle {
   uint32_t debug = 0;  // GSCAN_DEBUG_* test hooks
   uint32_t graham_fails = 0;
   uint32_t graham_path = 0;  // 0 sequential kernel, 1 chains+certificate, 2 junctions+certificate
+
+  // sparse round-2 path (sparse.cuh)
+  int sp_grid = 0;
+  double* sp_th = nullptr;   // bucket boundary angles, kSpBuckets + 1 (per call)
+  double* sp_cdf = nullptr;  // sampled pseudo-angle CDF, kSpCells + 1 (per call)
+  uint32_t* sp_cells = nullptr;  // sample counts per cell
+  uint32_t* sp_big = nullptr;    // candidate buckets for the CTA sorter
+  uint32_t *sp_gcount = nullptr, *sp_ccount = nullptr, *sp_hcount = nullptr;  // per-CTA emissions
+  uint64_t* sp_dup2 = nullptr;   // partitioned hash list (n)
+  bool sp_debug = false, sp_no_dup = false;
+  uint16_t* sp_codes = nullptr;  // per-point bucket code (n)
+  uint32_t *sp_hist_part = nullptr, *sp_phi_part = nullptr, *sp_part_off = nullptr;
+  SpD2* sp_d2 = nullptr;
+  uint32_t *sp_hist = nullptr, *sp_bstart = nullptr, *sp_gbits = nullptr, *sp_glist = nullptr,
+           *sp_gcnt = nullptr, *sp_phimax = nullptr, *sp_prefmax = nullptr, *sp_slice = nullptr,
+           *sp_ccnt = nullptr, *sp_cstart = nullptr, *sp_wcnt = nullptr, *sp_wstart = nullptr,
+           *sp_rlo = nullptr;
+  uint32_t *sp_seglo = nullptr, *sp_seghi = nullptr;
+  uint64_t sp_seg_cap = 0;
+  SpState* sp_st = nullptr;
+  SpState* h_sp = nullptr;  // pinned mirror
+  // n-sized
+  uint32_t *sp_eb = nullptr, *sp_Wb = nullptr, *sp_Ws = nullptr, *sp_Rb = nullptr;
+  uint64_t* sp_dup = nullptr;  // per-CTA hash lists (n)
+  uint32_t sp_used = 0, sp_fail = 0, sp_walked = 0, sp_calls = 0, sp_fallbacks = 0;
 };
 
 namespace {
@@ -122,6 +149,8 @@ void free_buffers(gscan_handle* h) {
   dfree(h->g_parent); dfree(h->g_btop); dfree(h->g_jk); dfree(h->g_je); dfree(h->g_jmin);
   dfree(h->g_keep); dfree(h->g_misc);
   dfree(h->g_stA); dfree(h->g_stB); dfree(h->g_lenA); dfree(h->g_lenB); dfree(h->g_scr);
+  dfree(h->sp_eb); dfree(h->sp_Wb); dfree(h->sp_Ws); dfree(h->sp_Rb); dfree(h->sp_dup);
+  dfree(h->sp_codes); dfree(h->sp_dup2);
   h->g_st_cap = 0;
   h->g_len_cap = 0;
   h->cap = 0;
@@ -182,6 +211,13 @@ int reserve(gscan_handle* h, uint64_t n) {
                                   (uint64_t)(nb + 2 + kScanTile - 1) / kScanTile) + 64;
   h->status_cap = tiles;
   CU(cudaMalloc(&h->status, tiles * 8));
+  CU(cudaMalloc(&h->sp_eb, m * 4));
+  CU(cudaMalloc(&h->sp_Wb, m * 4));
+  CU(cudaMalloc(&h->sp_Ws, m * 4));
+  CU(cudaMalloc(&h->sp_Rb, m * 4));
+  CU(cudaMalloc(&h->sp_dup, (m + 4096) * 8));
+  CU(cudaMalloc(&h->sp_dup2, (m + 4096) * 8));
+  CU(cudaMalloc(&h->sp_codes, (m + 1) * sizeof(uint16_t)));
   h->cap = n;
   return GSCAN_OK;
 }
@@ -633,6 +669,289 @@ float ev_ms(cudaEvent_t a, cudaEvent_t b) {
   return ms;
 }
 
+// ---------------------------------------------------------------------------
+// Sparse round-2 path (sparse.cuh). Returns GSCAN_OK with *ok = false when the
+// path declined (fail bits in h->sp_fail): the caller then runs the full sort.
+constexpr uint64_t kSparseMinN = 1u << 16;
+
+bool sparse_eligible(const gscan_handle* h, uint64_t n, const gscan_config& cfg) {
+  return n >= kSparseMinN && cfg.enable_round1 && cfg.enable_round2 && cfg.chunked &&
+         !(h->debug & GSCAN_DEBUG_FULL_SORT);
+}
+
+int sparse_init(gscan_handle* h) {
+  if (h->sp_st) return GSCAN_OK;
+  const uint32_t nb = kSpBuckets, G = (uint32_t)h->sp_grid;
+  CU(cudaMalloc(&h->sp_th, (nb + 1) * 8));
+  CU(cudaMalloc(&h->sp_cdf, (kSpCells + 1) * 8));
+  CU(cudaMalloc(&h->sp_cells, kSpCells * 4));
+  CU(cudaMalloc(&h->sp_big, nb * 4));
+  CU(cudaMalloc(&h->sp_gcount, G * 4));
+  CU(cudaMalloc(&h->sp_ccount, G * 4));
+  CU(cudaMalloc(&h->sp_hcount, G * 4));
+  h->sp_debug = getenv("GSCAN_SP_DEBUG") != nullptr;
+  // measurement hook only: skipping the duplicate check is exact only for
+  // duplicate-free inputs
+  h->sp_no_dup = getenv("GSCAN_SP_NODUP") != nullptr;
+  CU(cudaMalloc(&h->sp_hist_part, (size_t)G * nb * 4));
+  CU(cudaMalloc(&h->sp_phi_part, (size_t)G * nb * 4));
+  CU(cudaMalloc(&h->sp_part_off, ((size_t)G * kSpParts + 1) * 4));
+  CU(cudaMalloc(&h->sp_d2, G * sizeof(SpD2)));
+  uint32_t** nb_bufs[] = {&h->sp_hist, &h->sp_bstart, &h->sp_glist, &h->sp_gcnt, &h->sp_phimax,
+                          &h->sp_prefmax, &h->sp_slice, &h->sp_ccnt, &h->sp_cstart, &h->sp_wcnt,
+                          &h->sp_wstart, &h->sp_rlo};
+  for (uint32_t** b : nb_bufs) CU(cudaMalloc(b, (nb + 2) * 4));
+  CU(cudaMalloc(&h->sp_gbits, nb / 8));
+  CU(cudaMalloc(&h->sp_st, sizeof(SpState)));
+  CU(cudaMallocHost(&h->h_sp, sizeof(SpState)));
+  return GSCAN_OK;
+}
+
+int run_sparse(gscan_handle* h, const double* xs, const double* ys, uint32_t n,
+               const gscan_config& cfg, uint64_t* hull_size, gscan_stats* st, bool* ok) {
+  *ok = false;
+  TRY(sparse_init(h));
+  ++h->sp_calls;
+  const uint32_t nb = kSpBuckets;
+  const uint32_t G = (uint32_t)h->sp_grid;
+  const bool vec = aligned16(xs) && aligned16(ys);
+  const bool drop = (h->debug & GSCAN_DEBUG_SPARSE_DROP) != 0;
+  const uint64_t c = cfg.chunk_count;
+  const uint64_t nslices = 2 * std::min<uint64_t>(c, n);
+  if (nslices + 2 > h->sp_seg_cap) {
+    dfree(h->sp_seglo);
+    dfree(h->sp_seghi);
+    CU(cudaMalloc(&h->sp_seglo, (nslices + 2) * 4));
+    CU(cudaMalloc(&h->sp_seghi, (nslices + 2) * 4));
+    h->sp_seg_cap = nslices + 2;
+  }
+  // per-CTA emission region: bound on the points one streaming CTA visits
+  const uint32_t nth = G * (uint32_t)kSpThreads;
+  const uint32_t cap = 2u * (uint32_t)kSpThreads * ((n / 2 + nth - 1) / nth) + 2;
+  const size_t smem_nb = (size_t)nb * 4;
+  cudaStream_t s = h->stream;
+  CU(cudaEventRecord(h->ev[0], s));
+  CU(cudaMemsetAsync(h->ctr, 0, sizeof(Counters), s));
+  CU(cudaMemsetAsync(h->sp_st, 0, sizeof(SpState), s));
+  CU(cudaMemsetAsync(h->sp_gcnt, 0, nb * 4, s));
+  CU(cudaMemsetAsync(h->sp_ccnt, 0, nb * 4, s));
+  CU(cudaMemsetAsync(h->sp_prefmax, 0, nb * 4, s));
+  CU(cudaMemsetAsync(h->sp_slice, 0xff, nb * 4, s));
+  CU(cudaMemsetAsync(h->sp_cells, 0, kSpCells * 4, s));
+  {
+    const uint32_t grid =
+        std::max(1u, std::min<uint32_t>((n + kBlock * 8 - 1) / (kBlock * 8), h->sm_count * 8));
+    Launch L(h, "k_extremes");
+    if (vec) k_extremes<true><<<grid, kBlock, 0, s>>>(xs, ys, n, h->partials, h->ext, h->ctr);
+    else k_extremes<false><<<grid, kBlock, 0, s>>>(xs, ys, n, h->partials, h->ext, h->ctr);
+  }
+  {
+    Launch L(h, "k_sp_sample");
+    k_sp_sample<<<kSpSample / 1024, 1024, 0, s>>>(xs, ys, n, h->ext, h->sp_cells);
+  }
+  {
+    Launch L(h, "k_sp_cdf");
+    k_sp_cdf<<<1, kSpCells, 0, s>>>(h->sp_cells, h->sp_cdf);
+  }
+  {
+    Launch L(h, "k_sp_theta");
+    k_sp_theta<<<(nb + 1 + 255) / 256, 256, 0, s>>>(h->sp_cdf, h->sp_th, h->sp_st);
+  }
+  {
+    Launch L(h, "k_sp_hist");
+#define A2 xs, ys, n, h->ext, h->sp_cdf, h->sp_th, h->sp_codes, h->sp_hist_part, h->sp_d2, h->ctr
+    if (vec) k_sp_hist<true><<<G, kSpThreads, smem_nb, s>>>(A2);
+    else k_sp_hist<false><<<G, kSpThreads, smem_nb, s>>>(A2);
+#undef A2
+  }
+  {
+    Launch L(h, "k_sp_reduce_hist");
+    k_sp_reduce_cols<false><<<(nb + 255) / 256, 256, 0, s>>>(h->sp_hist_part, G, nb, h->sp_hist);
+  }
+  {
+    Launch L(h, "k_sp_plan_pl");
+    k_sp_plan_pl<<<1, 256, 0, s>>>(xs, ys, h->sp_d2, G, h->sp_st);
+  }
+  TRY(scan_u32(h, h->sp_hist, nb, h->sp_bstart));
+  {
+    Launch L(h, "k_sp_plan_bl");
+    k_sp_plan_bl<<<1, 32, 0, s>>>(h->ext, h->sp_cdf, h->sp_th, h->sp_bstart, h->sp_st);
+  }
+  {
+    Launch L(h, "k_sp_lrank");
+    k_sp_lrank<<<h->sm_count * 8, 256, 0, s>>>(xs, ys, h->sp_codes, n, h->ext, h->sp_st);
+  }
+  {
+    Launch L(h, "k_sp_steps");
+    k_sp_steps<<<1, 32, 0, s>>>(h->sp_bstart, c, h->sp_st);
+  }
+  {
+    Launch L(h, "k_sp_gbits");
+    k_sp_gbits<<<(nb / 32 + 255) / 256, 256, 0, s>>>(h->sp_bstart, h->sp_st, h->sp_gbits,
+                                                     h->sp_glist);
+  }
+  CU(cudaEventRecord(h->ev[1], s));
+  // F3 -> G in (surv, sp_eb), hash lists in sp_dup
+  {
+    Launch L(h, "k_sp_phi");
+#define A3 xs, ys, h->sp_codes, n, cap, h->ext, h->sp_gbits, h->sp_st, h->sp_phi_part, h->surv, \
+           h->sp_eb, h->sp_gcount, h->sp_dup, h->sp_hcount, h->sp_part_off
+    if (vec) k_sp_phi<true><<<G, kSpThreads, smem_nb, s>>>(A3);
+    else k_sp_phi<false><<<G, kSpThreads, smem_nb, s>>>(A3);
+#undef A3
+  }
+  {
+    Launch L(h, "k_sp_reduce_phi");
+    k_sp_reduce_cols<true><<<(nb + 255) / 256, 256, 0, s>>>(h->sp_phi_part, G, nb, h->sp_phimax);
+  }
+  const bool dup_check = !h->sp_no_dup;
+  if (dup_check) {
+    TRY(scan_u32(h, h->sp_part_off, kSpParts * G, h->sp_part_off));
+    {
+      Launch L(h, "k_sp_dup_part");
+      k_sp_dup_part<<<G, 1024, kSpDupPartSmem, s>>>(h->sp_dup, h->sp_hcount, cap, h->sp_part_off,
+                                                    h->sp_st, h->sp_dup2);
+    }
+    {
+      Launch L(h, "k_sp_dups");
+      k_sp_dups<<<kSpParts, 512, kSpDupSlots * 8, s>>>(h->sp_dup2, h->sp_part_off, G, h->sp_st);
+    }
+  }
+  {
+    Launch L(h, "k_sp_place_g");
+    k_sp_emit_place<0><<<dim3(16, G), 256, 0, s>>>(xs, ys, h->surv, h->sp_eb, nullptr,
+                                                   h->sp_gcount, cap, h->sp_gcnt, h->sp_bstart,
+                                                   h->ext, h->sp_st, h->rec);
+  }
+  {
+    Launch L(h, "k_sp_sort_gathered");
+    k_sp_sort_gathered<<<h->sm_count * 2, kSpSortThreads, kSpSortSmem, s>>>(
+        h->sp_glist, h->sp_bstart, h->sp_hist, h->sp_gcnt, h->rec, h->ext, h->sp_st, h->A_x,
+        h->A_y, h->A_i);
+  }
+  {
+    Launch L(h, "k_sp_slices");
+    k_sp_slices<<<(uint32_t)((nslices * 32 + 255) / 256), 256, 0, s>>>(
+        h->sp_st, h->sp_bstart, h->sp_gbits, h->sp_phimax, h->A_x, h->A_y, h->ext, h->sp_prefmax,
+        h->sp_slice);
+  }
+  CU(cudaEventRecord(h->ev[2], s));
+  // F4 -> C in (surv, sp_eb); codes of candidates marked
+  {
+    Launch L(h, "k_sp_cand");
+#define A4 xs, ys, h->sp_codes, n, cap, h->ext, h->sp_gbits, h->sp_prefmax, h->sp_st, h->surv, \
+           h->sp_eb, h->sp_ccount, drop
+    if (vec) k_sp_cand<true><<<G, kSpThreads, smem_nb, s>>>(A4);
+    else k_sp_cand<false><<<G, kSpThreads, smem_nb, s>>>(A4);
+#undef A4
+  }
+  {
+    Launch L(h, "k_sp_rank_c");
+    k_sp_emit_place<1><<<dim3(4, G), 256, 0, s>>>(xs, ys, h->surv, h->sp_eb, h->rank, h->sp_ccount,
+                                                  cap, h->sp_ccnt, nullptr, h->ext, h->sp_st,
+                                                  h->rec);
+  }
+  TRY(scan_u32(h, h->sp_ccnt, nb, h->sp_cstart));
+  {
+    Launch L(h, "k_sp_place_c");
+    k_sp_emit_place<2><<<dim3(4, G), 256, 0, s>>>(xs, ys, h->surv, h->sp_eb, h->rank, h->sp_ccount,
+                                                  cap, nullptr, h->sp_cstart, h->ext, h->sp_st,
+                                                  h->rec);
+  }
+  {
+    Launch L(h, "k_sp_wcount");
+    k_sp_wcount<<<(nb + 255) / 256, 256, 0, s>>>(h->sp_gbits, h->sp_hist, h->sp_ccnt, h->sp_wcnt);
+  }
+  TRY(scan_u32(h, h->sp_wcnt, nb, h->sp_wstart));
+  {
+    Launch L(h, "k_sp_place_cand");
+    k_sp_place_cand<<<nb / 8, 256, 0, s>>>(h->rec, h->sp_cstart, h->sp_wstart, h->sp_slice,
+                                           h->ext, h->sp_st, h->sp_big, h->C_x, h->C_y, h->C_i,
+                                           h->sp_Wb, h->sp_Ws, h->flags);
+  }
+  {
+    Launch L(h, "k_sp_sort_cand_big");
+    k_sp_sort_cand_big<<<h->sm_count, kSpSortThreads, kSpSortSmem, s>>>(
+        h->sp_big, h->rec, h->sp_cstart, h->sp_wstart, h->sp_slice, h->ext, h->sp_st, h->C_x,
+        h->C_y, h->C_i, h->sp_Wb, h->sp_Ws, h->flags);
+  }
+  {
+    Launch L(h, "k_sp_place_gathered");
+    k_sp_place_gathered<<<h->sm_count * 4, 256, 0, s>>>(
+        h->sp_glist, h->sp_bstart, h->sp_hist, h->sp_wstart, h->A_x, h->A_y, h->A_i, h->ext,
+        h->sp_st, h->C_x, h->C_y, h->C_i, h->sp_Wb, h->sp_Ws, h->flags);
+  }
+  CU(cudaEventRecord(h->ev[3], s));
+  {
+    Launch L(h, "k_sp_segments");
+    k_sp_segments<<<h->sm_count * 8, kBlock, 0, s>>>(h->sp_Ws, h->sp_st, h->sp_seglo, h->sp_seghi);
+  }
+  {
+    Launch L(h, "k_sp_walk");
+    k_sp_walk<<<(uint32_t)nslices, kWalkBlock, 0, s>>>(h->C_x, h->C_y, h->sp_seglo, h->sp_seghi,
+                                                       h->sp_st, h->ext, h->flags);
+  }
+  {
+    const uint64_t tiles = (uint64_t)n / kCompactTile + 2;
+    TRY(reset_lookback(h, tiles));
+    Launch L(h, "k_sp_compact");
+    k_sp_compact<<<(uint32_t)tiles, kBlock, 0, s>>>(h->C_x, h->C_y, h->C_i, h->sp_Wb, h->flags,
+                                                    h->sp_st, h->A_x, h->A_y, h->A_i, h->sp_Rb,
+                                                    h->status, h->ctr);
+  }
+  {
+    Launch L(h, "k_sp_rlo");
+    k_sp_rlo<<<h->sm_count * 8, kBlock, 0, s>>>(h->sp_Rb, h->sp_st, h->sp_rlo);
+  }
+  {
+    Launch L(h, "k_sp_verify");
+#define A6 xs, ys, h->sp_codes, n, h->sp_gbits, h->sp_rlo, h->A_x, h->A_y, h->sp_st
+    if (vec) k_sp_verify<true><<<G, kSpThreads, smem_nb + 4, s>>>(A6);
+    else k_sp_verify<false><<<G, kSpThreads, smem_nb + 4, s>>>(A6);
+#undef A6
+  }
+  CU(cudaGetLastError());
+  CU(cudaEventRecord(h->ev[4], s));
+  CU(cudaMemcpyAsync(h->h_sp, h->sp_st, sizeof(SpState), cudaMemcpyDeviceToHost, s));
+  CU(cudaMemcpyAsync(&h->ctr->n2, &h->sp_st->n_r, 4, cudaMemcpyDeviceToDevice, s));
+  TRY(sync_counters(h));
+  const SpState sp = *h->h_sp;
+  if (h->sp_debug) {
+    fprintf(stderr,
+            "[sparse] fail=%#x m=%u M=%u b_l=%u l=%u/%u l_idx=%u ties=%u step=%u,%u slices=%u+%u "
+            "n_gb=%u n_g=%u max_g=%u n_c=%u n_w=%u n_r=%u dups=%u vfail=%u why=%u bigc=%u\n",
+            sp.fail, sp.m, sp.M, sp.b_l, sp.l, sp.l_check, sp.l_idx, sp.ties, sp.step_r, sp.step_l,
+            sp.n_right, sp.n_left, sp.n_gb, sp.n_g, sp.max_g, sp.n_c, sp.n_w, sp.n_r, sp.dups,
+            sp.verify_fail, sp.why, sp.n_bigc);
+  }
+  h->sp_fail = sp.fail;
+  h->sp_walked = sp.n_w;
+  if (sp.fail) {
+    ++h->sp_fallbacks;
+    return GSCAN_OK;
+  }
+  TRY(stage_graham(h, h->A_x, h->A_y, h->A_i, sp.n_r));
+  CU(cudaEventRecord(h->ev[5], s));
+  TRY(sync_counters(h));
+  const Counters& cc = *h->h_ctr;
+  *hull_size = cc.hull;
+  if (st) {
+    st->n_input = n;
+    st->n_after_round1 = cc.n1;
+    st->n_after_round2 = sp.n_r;
+    st->hull_size = cc.hull;
+    st->t_round1_ms = ev_ms(h->ev[0], h->ev[1]);
+    st->t_annotate_ms = ev_ms(h->ev[1], h->ev[2]);
+    st->t_sort_ms = ev_ms(h->ev[2], h->ev[3]);
+    st->t_round2_ms = ev_ms(h->ev[3], h->ev[4]);
+    st->t_finalize_ms = ev_ms(h->ev[4], h->ev[5]);
+    st->t_total_ms = ev_ms(h->ev[0], h->ev[5]);
+  }
+  h->sp_used = 1;
+  *ok = true;
+  return GSCAN_OK;
+}
+
 // Full pipeline on device-resident SoA input. Hull indices left in h->d_out.
 int run_pipeline(gscan_handle* h, const double* xs, const double* ys, uint64_t n64,
                  const gscan_config& cfg, uint64_t* hull_size, gscan_stats* st) {
@@ -641,6 +960,13 @@ int run_pipeline(gscan_handle* h, const double* xs, const double* ys, uint64_t n
   const uint32_t n = (uint32_t)n64;
   h->launches = 0;
   h->kt_used = 0;
+  h->sp_used = 0;
+  h->sp_fail = 0;
+  if (sparse_eligible(h, n64, cfg)) {
+    bool ok = false;
+    TRY(run_sparse(h, xs, ys, n, cfg, hull_size, st, &ok));
+    if (ok) return GSCAN_OK;
+  }
   CU(cudaEventRecord(h->ev[0], h->stream));
   CU(cudaMemsetAsync(h->ctr, 0, sizeof(Counters), h->stream));
   TRY(stage_round1_keys(h, xs, ys, n, cfg.enable_round1));
@@ -743,6 +1069,24 @@ int gscan_create(int device, gscan_handle** out) {
                             kBlockCap * (8 + 8 + 8 + 8 + 4 + 2)));
     CU(cudaFuncSetAttribute(k_bucket_sort_cta, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             kSortCap * (8 + 8 + 4 + 4)));
+    const int nbs = (int)(kSpBuckets * 4);
+    CU(cudaFuncSetAttribute(k_sp_hist<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, nbs));
+    CU(cudaFuncSetAttribute(k_sp_hist<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, nbs));
+    CU(cudaFuncSetAttribute(k_sp_phi<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, nbs));
+    CU(cudaFuncSetAttribute(k_sp_phi<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, nbs));
+    CU(cudaFuncSetAttribute(k_sp_cand<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, nbs));
+    CU(cudaFuncSetAttribute(k_sp_cand<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, nbs));
+    CU(cudaFuncSetAttribute(k_sp_verify<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, nbs + 4));
+    CU(cudaFuncSetAttribute(k_sp_verify<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, nbs + 4));
+    CU(cudaFuncSetAttribute(k_sp_sort_gathered, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)kSpSortSmem));
+    CU(cudaFuncSetAttribute(k_sp_sort_cand_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)kSpSortSmem));
+    CU(cudaFuncSetAttribute(k_sp_dups, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)(kSpDupSlots * 8)));
+    CU(cudaFuncSetAttribute(k_sp_dup_part, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)kSpDupPartSmem));
+    h->sp_grid = h->sm_count;
     return GSCAN_OK;
   };
   rc = init();
@@ -760,6 +1104,12 @@ int gscan_destroy(gscan_handle* h) {
   if (h->stream) cudaStreamSynchronize(h->stream);
   free_buffers(h);
   dfree(h->partials); dfree(h->ext); dfree(h->ctr); dfree(h->scratch64);
+  dfree(h->sp_th); dfree(h->sp_cdf); dfree(h->sp_cells); dfree(h->sp_big); dfree(h->sp_gcount); dfree(h->sp_ccount); dfree(h->sp_hcount); dfree(h->sp_hist_part); dfree(h->sp_phi_part); dfree(h->sp_part_off);
+  dfree(h->sp_d2); dfree(h->sp_hist); dfree(h->sp_bstart); dfree(h->sp_gbits); dfree(h->sp_glist);
+  dfree(h->sp_gcnt); dfree(h->sp_phimax); dfree(h->sp_prefmax); dfree(h->sp_slice);
+  dfree(h->sp_ccnt); dfree(h->sp_cstart); dfree(h->sp_wcnt); dfree(h->sp_wstart); dfree(h->sp_rlo);
+  dfree(h->sp_seglo); dfree(h->sp_seghi); dfree(h->sp_st);
+  if (h->h_sp) cudaFreeHost(h->h_sp);
   if (h->h_ctr) cudaFreeHost(h->h_ctr);
   if (h->h_out) cudaFreeHost(h->h_out);
   for (auto& e : h->ev) if (e) cudaEventDestroy(e);
@@ -795,6 +1145,15 @@ int gscan_last_graham_info(const gscan_handle* h, uint32_t* path, uint32_t* cert
   if (!h) return GSCAN_E_INVALID;
   if (path) *path = h->graham_path;
   if (certificate_failures) *certificate_failures = h->graham_fails;
+  return GSCAN_OK;
+}
+
+int gscan_last_sparse_info(const gscan_handle* h, uint32_t* used, uint32_t* fail_bits,
+                           uint32_t* n_walked) {
+  if (!h) return GSCAN_E_INVALID;
+  if (used) *used = h->sp_used;
+  if (fail_bits) *fail_bits = h->sp_fail;
+  if (n_walked) *n_walked = h->sp_walked;
   return GSCAN_OK;
 }
 

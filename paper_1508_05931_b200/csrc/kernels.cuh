@@ -560,7 +560,7 @@ __device__ __forceinline__ PtRec ld_rec256(const PtRec* p) {
   r.x = bitsd((uint64_t)v[2] | ((uint64_t)v[3] << 32));
   r.y = bitsd((uint64_t)v[4] | ((uint64_t)v[5] << 32));
   r.idx = v[6];
-  r.pad = 0;
+  r.pad = v[7];
   return r;
 }
 

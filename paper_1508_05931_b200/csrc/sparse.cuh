@@ -1,0 +1,1594 @@
+// Sparse round 2: the pipeline's default path (gscan.cu run_sparse).
+//
+// The reference sorts EVERY round-1 survivor by (angle, dist2) and then walks
+// 2 x chunk_count slices of that order (angular.hpp:154-194,
+// discard.hpp:90-124); on a 20M square 13.3M survivors are sorted and 21K
+// remain. Only the slice STRUCTURE needs every survivor -- slices are cut by
+// rank -- and ranks need only counts. So this path:
+//
+//   map        a strided sample of round-1 survivors -> angle buckets of about
+//              equal occupancy (k_sp_sample / k_sp_cdf / k_sp_theta).
+//   F2         one pass (k_sp_hist): round-1 test, each survivor's bucket
+//              (a monotone function of its glibc atan2 key, sp_bucket) into
+//              a per-CTA shared-memory histogram and a per-point u16 code,
+//              argmax dist2 (split_regions' P_l).
+//   plan       bucket starts = exact ranks of every bucket; P_l's exact
+//              position from its own bucket (codes-only pass k_sp_lrank);
+//              slice steps; every bucket that holds a slice seed (or P_l) is
+//              GATHERED: all its points are sorted exactly.
+//   F3         one pass (k_sp_phi): gathered points are emitted; every other
+//              survivor folds its walk angle phi (angle of P - P_l) into a
+//              per-CTA bucket maximum; every survivor's 64-bit coordinate
+//              hash goes to a per-CTA list (duplicate check).
+//   sort G     gathered points exactly ordered -> every seed and, per
+//              non-gathered bucket, the running maximum of phi over
+//              everything before it in its slice (k_sp_slices).
+//   F4         one pass (k_sp_cand): a non-gathered survivor whose phi is not
+//              below its bucket's prefix maximum (minus kSpTol) is a
+//              CANDIDATE.
+//   walk       candidates + gathered points, exactly ordered, walked slice
+//              by slice with the reference's exact predicate (k_sp_walk).
+//   F6         one pass (k_sp_verify): every survivor that was NOT walked
+//              must be discarded by the reference walk: strictly inside
+//              against every kept point that can be its walk state
+//              (discard.hpp:36-66), checked with the exact predicate.
+//   dups       the hash lists are partitioned (k_sp_dup_part) and checked
+//              for equal hashes (k_sp_dups): annotate's dedup
+//              (angular.hpp:118-133) would change ranks.
+//
+// Why the result is the reference's, bit for bit: by induction along each
+// slice, the reference's walk state before any point equals the last kept
+// point before it. Walked points see that state in our walk too (skipped
+// points never become state because they are discarded), and every skipped
+// point is verified to be discarded against every state it could see. Any
+// doubt -- a tie for P_l, a possible duplicate, a failed verification, an
+// oversized bucket -- sets a fail bit and the call reruns the full sort
+// path, which is exact by construction. The fast path never guesses.
+#pragma once
+#include "kernels.cuh"
+
+namespace gscan {
+
+constexpr uint32_t kSpBuckets = 48u * 1024u;  // coarse angle buckets (u32 smem arrays)
+constexpr int kSpThreads = 512;               // persistent streaming CTAs, one per SM
+constexpr uint32_t kSpPartBits = 11;          // duplicate-check hash partitions
+constexpr uint32_t kSpParts = 1u << kSpPartBits;
+constexpr double kSpTol = 1e-7;               // candidate tolerance on phi (pseudo-angle units)
+constexpr uint32_t kSpGatherCap = 4096;       // largest bucket sorted in smem
+constexpr uint32_t kSpDupSlotBits = 14;
+constexpr uint32_t kSpDupSlots = 1u << kSpDupSlotBits;  // dup-check hash set slots (smem, 8 B)
+constexpr uint32_t kSpDupRound = 6144;        // entries per hash-set round (load <= 0.375)
+constexpr uint32_t kSpPartChunk = 8192;       // entries per partitioning chunk (smem)
+constexpr size_t kSpDupPartSmem = (size_t)kSpPartChunk * 16 + (size_t)kSpParts * 12;
+
+enum : uint32_t {
+  kSpFailTie = 1u,        // several points share the maximal dist2
+  kSpFailStep = 2u,       // (unused)
+  kSpFailTiny = 4u,       // a region with <= 1 point (reference skips its walk)
+  kSpFailDup = 8u,        // possible duplicate points (dedup changes ranks)
+  kSpFailVerify = 16u,    // a skipped point would not be discarded
+  kSpFailCap = 32u,       // a gathered bucket / dup partition exceeds capacity
+  kSpFailInternal = 64u,  // inconsistent counts (should not happen)
+  kSpFailFew = 128u,      // too few points for the bucket structure
+};
+
+struct SpD2 {        // per-CTA farthest-point candidate
+  uint64_t d2;       // bits of dist2 (non-negative double: bit order = value order)
+  uint32_t idx;      // input index
+  uint32_t ties;     // points of this CTA at exactly d2
+};
+
+struct SpState {
+  double lx, ly;       // P_l
+  uint64_t d2max;
+  uint32_t l_idx;      // input index of P_l
+  uint32_t ties;
+  uint32_t m;          // points in buckets = M - 1 (anchor excluded, no dedup)
+  uint32_t M;
+  uint32_t b_l;
+  uint32_t l;          // exact position of P_l
+  uint32_t l_below;    // points of P_l's bucket ordered before P_l
+  uint32_t l_check;    // P_l's position as found by the gathered sort
+  uint32_t step_r, step_l, n_right, n_left;
+  uint32_t fail;
+  uint32_t n_g;        // gathered elements emitted
+  uint32_t n_c;        // candidates emitted
+  uint32_t n_gb;       // gathered buckets
+  uint32_t n_w;        // walk array size (anchor included)
+  uint32_t n_r;        // kept (round-2 output size)
+  uint32_t dups;
+  uint32_t verify_fail;
+  uint32_t why;        // first internal-failure site (debug)
+  uint32_t n_bigc;     // candidate buckets sorted by the CTA sorter
+  uint32_t max_g;      // largest gathered bucket
+  uint32_t pad[3];
+};
+
+// ---------------------------------------------------------------------------
+// Bucket map. Buckets are angle intervals: bucket(A) = #{k in [1, nb-1] :
+// th[k] <= A} for the glibc atan2 key angle A (-0 folded) and an increasing
+// table th[] -- monotone in A, so buckets never invert the reference order,
+// whatever th[] holds. th[] is chosen per call so that buckets hold about
+// equal numbers of survivors: th[k] = theta(Finv(k/nb)) where s(dx, dy) =
+// (1 - dx/(|dx|+dy))/2 is a pseudo-angle (monotone in the angle, theta its
+// inverse) and F is a piecewise-linear CDF of s over kSpCells cells, built
+// from a fixed sample of round-1 survivors (k_sp_sample).
+// Fast path: v = F(s)*nb from one approximate division; bucket = floor(v)
+// unless v is within kSpGuard of an integer -- s is within 1e-13 of s(A)
+// (division and glibc atan2 errors, the latter < 1 ulp), and even a cell
+// holding every point moves v by < 1e-5 per 1e-13 of s -- else the exact key
+// is computed and compared with th[].
+constexpr int kSpCells = 1024;
+constexpr double kSpGuardV = 1e-4;
+
+__device__ __forceinline__ uint64_t angle_key(double dx, double dy) {
+  const double a = glibc_atan2(dy, dx);
+  return (a == 0.0) ? 0ull : dbits(a);
+}
+
+// 1/d to ~1e-13 relative: hardware approximation + one Newton step. Used only
+// where a guard band or the exact verification absorbs the error.
+__device__ __forceinline__ double sp_rcp(double d) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+  const double e = __fma_rn(-d, r, 1.0);
+  return __fma_rn(r, e, r);
+}
+
+// pseudo-angle s in [0, 1] (approximate; < 0 when undefined)
+__device__ __forceinline__ double sp_s(double dx, double dy) {
+  const double den = __dadd_rn(fabs(dx), dy);
+  if (!(den > 1e-290)) return -1.0;
+  return __dmul_rn(__dsub_rn(1.0, __dmul_rn(dx, sp_rcp(den))), 0.5);
+}
+
+// cdf: kSpCells + 1 increasing values from 0 to 1 (shared memory)
+__device__ __forceinline__ uint32_t sp_bucket(double dx, double dy, const double* __restrict__ cdf,
+                                              const double* __restrict__ th) {
+  const double s = sp_s(dx, dy);
+  uint32_t k = 0;
+  if (s >= 0.0 && s <= 1.0) {
+    const double u = __dmul_rn(s, (double)kSpCells);
+    uint32_t j = (uint32_t)u;
+    if (j > kSpCells - 1) j = kSpCells - 1;
+    const double c0 = cdf[j], c1 = cdf[j + 1];
+    const double v = __dmul_rn(__fma_rn(__dsub_rn(u, (double)j), __dsub_rn(c1, c0), c0),
+                               (double)kSpBuckets);
+    if (v >= 0.0 && v < (double)kSpBuckets) {
+      k = (uint32_t)v;
+      const double f = __dsub_rn(v, (double)k);
+      if (f > kSpGuardV && f < 1.0 - kSpGuardV) return k;
+    } else if (v >= (double)kSpBuckets) {
+      k = kSpBuckets - 1;
+    }
+  }
+  const double a = bitsd(angle_key(dx, dy));
+  while (k > 0 && a < th[k]) --k;
+  while (k + 1 < kSpBuckets && a >= th[k + 1]) ++k;
+  return k;
+}
+
+__device__ __forceinline__ uint32_t ord_f(float f) {
+  const uint32_t u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+// 0 encodes "no value" (below every float)
+__device__ __forceinline__ double unord_f(uint32_t u) {
+  if (u == 0) return -1e300;
+  return (double)__uint_as_float((u & 0x80000000u) ? (u & 0x7fffffffu) : ~u);
+}
+
+// Coordinate hash with -0.0 folded onto +0.0 (annotate's CoordSet compares
+// folded bits, angular.hpp:99-101): equal points hash equally.
+// 64-bit coordinate hash with -0.0 folded onto +0.0 (annotate's CoordSet
+// compares folded bits, angular.hpp:99-101): equal points hash equally, so
+// equal hashes are the only possible duplicates.
+__device__ __forceinline__ uint64_t coord_hash64(double x, double y) {
+  const uint64_t a = dbits(x == 0.0 ? 0.0 : x), b = dbits(y == 0.0 ? 0.0 : y);
+  uint64_t z = a ^ (b * 0x9e3779b97f4a7c15ull);
+  z ^= z >> 30; z *= 0xbf58476d1ce4e5b9ull;
+  z ^= z >> 27; z *= 0x94d049bb133111ebull;
+  z ^= z >> 31;
+  return z;
+}
+
+
+// Walk angle of P around P_l, measured from u = anchor - P_l (kernels.cuh
+// pseudo_angle), signed by region: right region keeps running maxima of
+// +phi, left region of -phi.
+__device__ __forceinline__ double sp_phi(double px, double py, double lx, double ly, double ux,
+                                         double uy, bool right) {
+  const double vx = __dsub_rn(px, lx), vy = __dsub_rn(py, ly);
+  const double c = __fma_rn(ux, vx, __dmul_rn(uy, vy));   // along P_l -> anchor
+  const double sn = __fma_rn(ux, vy, -__dmul_rn(uy, vx)); // across
+  const double den = fabs(c) + fabs(sn);
+  if (!(den > 1e-290)) return 0.0;
+  const double t = 1.0 - c * sp_rcp(den);                 // [0, 2], increasing with the angle
+  const double p = sn >= 0.0 ? t : -t;
+  return right ? p : -p;
+}
+
+// Streaming helper: visits every point i of [0, n) once across the grid,
+// 128-bit loads, kPairs pairs in flight per thread. f(x, y, i).
+template <bool kVec, int kPairs, typename F>
+__device__ __forceinline__ void sp_stream(const double* __restrict__ xs,
+                                          const double* __restrict__ ys, uint32_t n, F&& f) {
+  const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t nth = gridDim.x * blockDim.x;
+  if (kVec) {
+    const double2* x2 = reinterpret_cast<const double2*>(xs);
+    const double2* y2 = reinterpret_cast<const double2*>(ys);
+    const uint32_t np = n / 2;
+    uint32_t p = tid;
+    for (; p + (kPairs - 1) * nth < np; p += kPairs * nth) {
+      double2 vx[kPairs], vy[kPairs];
+#pragma unroll
+      for (int u = 0; u < kPairs; ++u) {
+        vx[u] = __ldcs(&x2[p + u * nth]);
+        vy[u] = __ldcs(&y2[p + u * nth]);
+      }
+#pragma unroll
+      for (int u = 0; u < kPairs; ++u) {
+        const uint32_t i = 2 * (p + u * nth);
+        f(vx[u].x, vy[u].x, i);
+        f(vx[u].y, vy[u].y, i + 1);
+      }
+    }
+    for (; p < np; p += nth) {
+      const double2 vx = __ldcs(&x2[p]), vy = __ldcs(&y2[p]);
+      f(vx.x, vy.x, 2 * p);
+      f(vx.y, vy.y, 2 * p + 1);
+    }
+    if ((n & 1) && tid == nth - 1) f(xs[n - 1], ys[n - 1], n - 1);
+  } else {
+    for (uint32_t i = tid; i < n; i += nth) f(xs[i], ys[i], i);
+  }
+}
+
+// Same visit order, with each point's u16 bucket code from F2 (0xffff: not
+// in the buffer). f(x, y, code, i).
+template <bool kVec, int kPairs, typename F>
+__device__ __forceinline__ void sp_stream_coded(const double* __restrict__ xs,
+                                                const double* __restrict__ ys,
+                                                const uint16_t* __restrict__ codes, uint32_t n,
+                                                F&& f) {
+  const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t nth = gridDim.x * blockDim.x;
+  if (kVec) {
+    const double2* x2 = reinterpret_cast<const double2*>(xs);
+    const double2* y2 = reinterpret_cast<const double2*>(ys);
+    const uint32_t* c2 = reinterpret_cast<const uint32_t*>(codes);
+    const uint32_t np = n / 2;
+    uint32_t p = tid;
+    for (; p + (kPairs - 1) * nth < np; p += kPairs * nth) {
+      double2 vx[kPairs], vy[kPairs];
+      uint32_t vc[kPairs];
+#pragma unroll
+      for (int u = 0; u < kPairs; ++u) vc[u] = __ldcs(&c2[p + u * nth]);
+#pragma unroll
+      for (int u = 0; u < kPairs; ++u) {
+        vx[u] = __ldcs(&x2[p + u * nth]);
+        vy[u] = __ldcs(&y2[p + u * nth]);
+      }
+#pragma unroll
+      for (int u = 0; u < kPairs; ++u) {
+        const uint32_t i = 2 * (p + u * nth);
+        f(vx[u].x, vy[u].x, vc[u] & 0xffffu, i);
+        f(vx[u].y, vy[u].y, vc[u] >> 16, i + 1);
+      }
+    }
+    for (; p < np; p += nth) {
+      const uint32_t vc = c2[p];
+      const double2 vx = __ldcs(&x2[p]), vy = __ldcs(&y2[p]);
+      f(vx.x, vy.x, vc & 0xffffu, 2 * p);
+      f(vx.y, vy.y, vc >> 16, 2 * p + 1);
+    }
+    if ((n & 1) && tid == nth - 1) f(xs[n - 1], ys[n - 1], (uint32_t)codes[n - 1], n - 1);
+  } else {
+    for (uint32_t i = tid; i < n; i += nth) f(xs[i], ys[i], (uint32_t)codes[i], i);
+  }
+}
+constexpr uint32_t kSpNoCode = 0xffffu;
+constexpr uint32_t kSpCandCode = 0xfffeu;  // set by F4 on candidates
+
+struct SpQuad {  // round-1 quadrilateral with hoisted edge vectors + anchor
+  double qx[4], qy[4], ex[4], ey[4], ax, ay;
+  uint32_t aidx;
+};
+
+__device__ __forceinline__ void load_quad(const ExtResult* ext, SpQuad& q) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k) { q.qx[k] = ext->qx[k]; q.qy[k] = ext->qy[k]; }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    q.ex[k] = __dsub_rn(q.qx[(k + 1) & 3], q.qx[k]);
+    q.ey[k] = __dsub_rn(q.qy[(k + 1) & 3], q.qy[k]);
+  }
+  q.ax = ext->ax;
+  q.ay = ext->ay;
+  q.aidx = ext->idx[4];
+}
+
+// ===========================================================================
+// Bucket map construction (after K1): a fixed strided sample of the input,
+// its round-1 survivors' pseudo-angles counted in kSpCells cells ->
+// piecewise-linear CDF (every cell gets a small floor so it stays strictly
+// increasing) -> th[k] = theta(Finv(k/nb)).
+constexpr uint32_t kSpSample = 1u << 16;
+
+__global__ void __launch_bounds__(1024) k_sp_sample(const double* __restrict__ xs,
+                                                    const double* __restrict__ ys, uint32_t n,
+                                                    const ExtResult* __restrict__ ext,
+                                                    uint32_t* __restrict__ cell_cnt) {
+  __shared__ uint32_t s_cnt[kSpCells];
+  for (uint32_t j = threadIdx.x; j < kSpCells; j += blockDim.x) s_cnt[j] = 0;
+  SpQuad q;
+  load_quad(ext, q);
+  __syncthreads();
+  const uint32_t ns = min(n, kSpSample);
+  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < ns; k += gridDim.x * blockDim.x) {
+    const uint32_t i = (uint32_t)(((uint64_t)k * n) / ns);
+    const double x = xs[i], y = ys[i];
+    if (!quad_keep(q.qx, q.qy, q.ex, q.ey, x, y) || (x == q.ax && y == q.ay)) continue;
+    const double sv = sp_s(__dsub_rn(x, q.ax), __dsub_rn(y, q.ay));
+    if (sv < 0.0 || sv > 1.0) continue;
+    uint32_t j = (uint32_t)(sv * kSpCells);
+    if (j > kSpCells - 1) j = kSpCells - 1;
+    atomicAdd(&s_cnt[j], 1u);
+  }
+  __syncthreads();
+  for (uint32_t j = threadIdx.x; j < kSpCells; j += blockDim.x)
+    if (s_cnt[j]) atomicAdd(&cell_cnt[j], s_cnt[j]);
+}
+
+// One CTA of kSpCells threads: inclusive scan of the floored counts -> CDF.
+__global__ void __launch_bounds__(kSpCells) k_sp_cdf(const uint32_t* __restrict__ cell_cnt,
+                                                     double* __restrict__ cdf) {
+  __shared__ double s_w[32];
+  const double floor_w = 0.02;  // per-cell floor, in sample units
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double v = (double)cell_cnt[threadIdx.x] + floor_w, x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_w[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    double t = s_w[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double y = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += y;
+    }
+    s_w[lane] = t;
+  }
+  __syncthreads();
+  const double incl = x + (warp ? s_w[warp - 1] : 0.0), tot = s_w[31];
+  cdf[threadIdx.x + 1] = (threadIdx.x + 1 == kSpCells) ? 1.0 : incl / tot;
+  if (threadIdx.x == 0) cdf[0] = 0.0;
+}
+
+__global__ void __launch_bounds__(256) k_sp_theta(const double* __restrict__ cdf,
+                                                  double* __restrict__ th,
+                                                  SpState* __restrict__ st) {
+  __shared__ double s_cdf[kSpCells + 1];
+  for (uint32_t j = threadIdx.x; j <= kSpCells; j += blockDim.x) s_cdf[j] = cdf[j];
+  __syncthreads();
+  auto theta_of = [&](uint32_t kk) -> double {
+    if (kk == 0) return 0.0;
+    if (kk >= kSpBuckets) return 3.141592653589793;
+    const double y = (double)kk / (double)kSpBuckets;
+    uint32_t lo = 0, hi = kSpCells - 1;  // cell j with cdf[j] <= y < cdf[j+1]
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi + 1) >> 1;
+      if (s_cdf[mid] <= y) lo = mid;
+      else hi = mid - 1;
+    }
+    const double fr = (y - s_cdf[lo]) / (s_cdf[lo + 1] - s_cdf[lo]);
+    const double sv = ((double)lo + fr) / (double)kSpCells;
+    const double t = 1.0 - 2.0 * sv;
+    return atan2(1.0 - fabs(t), t);
+  };
+  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k <= kSpBuckets;
+       k += gridDim.x * blockDim.x) {
+    const double a = theta_of(k);
+    th[k] = a;
+    if (k > 0 && !(a > theta_of(k - 1))) atomicOr(&st->fail, kSpFailInternal);
+  }
+}
+
+// Column reduction of per-CTA arrays: out[b] = sum / max over rows.
+template <bool kMax>
+__global__ void k_sp_reduce_cols(const uint32_t* __restrict__ part, uint32_t rows, uint32_t cols,
+                                 uint32_t* __restrict__ out) {
+  const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= cols) return;
+  uint32_t v = 0;
+  for (uint32_t r = 0; r < rows; ++r) {
+    const uint32_t x = part[(size_t)r * cols + b];
+    v = kMax ? max(v, x) : v + x;
+  }
+  out[b] = v;
+}
+
+// ===========================================================================
+// F2: round 1 + bucket histogram + argmax dist2 + hash-partition counts.
+// The quad test is classify_quad (prefilter.hpp:47-63); n_after_round1 counts
+// every survivor (pipeline.hpp:93); points equal to the anchor leave the
+// buffer (annotate, angular.hpp:118-133) and are not bucketed.
+template <bool kVec>
+__global__ void __launch_bounds__(kSpThreads, 1) k_sp_hist(
+    const double* __restrict__ xs, const double* __restrict__ ys, uint32_t n,
+    const ExtResult* __restrict__ ext, const double* __restrict__ cdf,
+    const double* __restrict__ th, uint16_t* __restrict__ codes, uint32_t* __restrict__ hist_part,
+    SpD2* __restrict__ d2part, Counters* __restrict__ ctr) {
+  extern __shared__ uint32_t s_hist[];  // kSpBuckets
+  __shared__ double s_cdf[kSpCells + 1];
+  for (uint32_t b = threadIdx.x; b < kSpBuckets; b += blockDim.x) s_hist[b] = 0;
+  for (uint32_t j = threadIdx.x; j <= kSpCells; j += blockDim.x) s_cdf[j] = cdf[j];
+  SpQuad q;
+  load_quad(ext, q);
+  __syncthreads();
+  uint32_t n1 = 0, bidx = 0xffffffffu, bties = 0;
+  uint64_t bd2 = 0;
+  auto visit = [&](double x, double y, uint32_t i) -> uint32_t {
+    if (!quad_keep(q.qx, q.qy, q.ex, q.ey, x, y)) return kSpNoCode;
+    ++n1;
+    if (x == q.ax && y == q.ay) return kSpNoCode;
+    const double dx = __dsub_rn(x, q.ax), dy = __dsub_rn(y, q.ay);
+    const uint32_t b = sp_bucket(dx, dy, s_cdf, th);
+    atomicAdd(&s_hist[b], 1u);
+    const uint64_t d2 = dbits(dist2_rn(dx, dy));
+    if (bidx == 0xffffffffu || d2 > bd2) { bd2 = d2; bidx = i; bties = 1; }
+    else if (d2 == bd2) { ++bties; if (i < bidx) bidx = i; }
+    return b;
+  };
+  {
+    const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t nth = gridDim.x * blockDim.x;
+    if (kVec) {
+      const double2* x2 = reinterpret_cast<const double2*>(xs);
+      const double2* y2 = reinterpret_cast<const double2*>(ys);
+      uint32_t* c2 = reinterpret_cast<uint32_t*>(codes);
+      const uint32_t np = n / 2;
+      uint32_t p = tid;
+      constexpr int kP = 4;
+      for (; p + (kP - 1) * nth < np; p += kP * nth) {
+        double2 vx[kP], vy[kP];
+#pragma unroll
+        for (int u = 0; u < kP; ++u) {
+          vx[u] = __ldcs(&x2[p + u * nth]);
+          vy[u] = __ldcs(&y2[p + u * nth]);
+        }
+#pragma unroll
+        for (int u = 0; u < kP; ++u) {
+          const uint32_t i = 2 * (p + u * nth);
+          const uint32_t c0 = visit(vx[u].x, vy[u].x, i);
+          const uint32_t c1 = visit(vx[u].y, vy[u].y, i + 1);
+          c2[p + u * nth] = c0 | (c1 << 16);
+        }
+      }
+      for (; p < np; p += nth) {
+        const double2 vx = __ldcs(&x2[p]), vy = __ldcs(&y2[p]);
+        const uint32_t c0 = visit(vx.x, vy.x, 2 * p);
+        const uint32_t c1 = visit(vx.y, vy.y, 2 * p + 1);
+        c2[p] = c0 | (c1 << 16);
+      }
+      if ((n & 1) && tid == nth - 1) codes[n - 1] = (uint16_t)visit(xs[n - 1], ys[n - 1], n - 1);
+    } else {
+      for (uint32_t i = tid; i < n; i += nth) codes[i] = (uint16_t)visit(xs[i], ys[i], i);
+    }
+  }
+  // block reductions: n1 (sum), (d2 max, ties)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    n1 += __shfl_xor_sync(0xffffffffu, n1, o);
+    const uint64_t od = __shfl_xor_sync(0xffffffffu, bd2, o);
+    const uint32_t oi = __shfl_xor_sync(0xffffffffu, bidx, o);
+    const uint32_t ot = __shfl_xor_sync(0xffffffffu, bties, o);
+    if (oi != 0xffffffffu) {
+      if (bidx == 0xffffffffu || od > bd2) { bd2 = od; bidx = oi; bties = ot; }
+      else if (od == bd2) { bties += ot; if (oi < bidx) bidx = oi; }
+    }
+  }
+  __shared__ uint64_t s_d[32];
+  __shared__ uint32_t s_i[32], s_t[32], s_n[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) { s_d[warp] = bd2; s_i[warp] = bidx; s_t[warp] = bties; s_n[warp] = n1; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t tot = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      tot += s_n[w];
+      if (w == 0) continue;
+      if (s_i[w] == 0xffffffffu) continue;
+      if (bidx == 0xffffffffu || s_d[w] > bd2) { bd2 = s_d[w]; bidx = s_i[w]; bties = s_t[w]; }
+      else if (s_d[w] == bd2) { bties += s_t[w]; if (s_i[w] < bidx) bidx = s_i[w]; }
+    }
+    d2part[blockIdx.x] = SpD2{bd2, bidx, bidx == 0xffffffffu ? 0u : bties};
+    if (tot) atomicAdd(&ctr->n1, tot);
+  }
+  uint32_t* hp = hist_part + (size_t)blockIdx.x * kSpBuckets;
+  for (uint32_t b = threadIdx.x; b < kSpBuckets; b += blockDim.x) hp[b] = s_hist[b];
+}
+
+// ceil(a / b) for b > 0
+__device__ __forceinline__ uint32_t cdiv(uint32_t a, uint32_t b) { return (a + b - 1) / b; }
+
+// Does [lo, hi] (positions, lo <= hi) contain 1 + s*step for some s >= 0?
+__device__ __forceinline__ bool has_right_seed(uint32_t lo, uint32_t hi, uint32_t step) {
+  if (step == 0) return false;
+  const uint32_t a = lo - 1, b = hi - 1;  // offsets from position 1
+  return (b / step) * step >= a;
+}
+// Does [lo, hi] contain M-1 - s*step for some s >= 0?
+__device__ __forceinline__ bool has_left_seed(uint32_t lo, uint32_t hi, uint32_t M, uint32_t step) {
+  if (step == 0) return false;
+  const uint32_t a = M - 1 - hi, b = M - 1 - lo;
+  return (b / step) * step >= a;
+}
+
+// ===========================================================================
+// Plan. Slices follow discard_chunked (discard.hpp:90-124): right region
+// positions 1..l-1 cut every step_r = ceil((l-1)/c) from position 1; left
+// region l+1..M-1 cut every step_l = ceil((M-1-l)/c) downward from M-1.
+// (a) P_l from the per-CTA partials (split_regions, angular.hpp:197-204:
+// first maximal dist2 -- a tie would need the exact order, so it declines).
+__global__ void __launch_bounds__(256) k_sp_plan_pl(const double* __restrict__ xs,
+                                                    const double* __restrict__ ys,
+                                                    const SpD2* __restrict__ d2part, uint32_t nparts,
+                                                    SpState* __restrict__ st) {
+  __shared__ uint64_t s_d[8];
+  __shared__ uint32_t s_i[8], s_t[8];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint64_t bd = 0;
+  uint32_t bi = 0xffffffffu, bt = 0;
+  for (uint32_t c = threadIdx.x; c < nparts; c += blockDim.x) {
+    const SpD2 p = d2part[c];
+    if (p.idx == 0xffffffffu) continue;
+    if (bi == 0xffffffffu || p.d2 > bd) { bd = p.d2; bi = p.idx; bt = p.ties; }
+    else if (p.d2 == bd) { bt += p.ties; if (p.idx < bi) bi = p.idx; }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const uint64_t od = __shfl_xor_sync(0xffffffffu, bd, o);
+    const uint32_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    const uint32_t ot = __shfl_xor_sync(0xffffffffu, bt, o);
+    if (oi != 0xffffffffu) {
+      if (bi == 0xffffffffu || od > bd) { bd = od; bi = oi; bt = ot; }
+      else if (od == bd) { bt += ot; if (oi < bi) bi = oi; }
+    }
+  }
+  if (lane == 0) { s_d[warp] = bd; s_i[warp] = bi; s_t[warp] = bt; }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  for (int w = 1; w < 8; ++w) {
+    if (s_i[w] == 0xffffffffu) continue;
+    if (bi == 0xffffffffu || s_d[w] > bd) { bd = s_d[w]; bi = s_i[w]; bt = s_t[w]; }
+    else if (s_d[w] == bd) { bt += s_t[w]; if (s_i[w] < bi) bi = s_i[w]; }
+  }
+  st->d2max = bd;
+  st->l_idx = bi;
+  st->ties = bt;
+  if (bi == 0xffffffffu) st->fail |= kSpFailFew;
+  else if (bt != 1) st->fail |= kSpFailTie;
+  if (bi != 0xffffffffu) { st->lx = xs[bi]; st->ly = ys[bi]; }
+}
+
+// (b) after the bucket scan: M and P_l's bucket.
+__global__ void k_sp_plan_bl(const ExtResult* __restrict__ ext, const double* __restrict__ cdf,
+                             const double* __restrict__ th, const uint32_t* __restrict__ bstart,
+                             SpState* __restrict__ st) {
+  if (threadIdx.x != 0) return;
+  const uint32_t m = bstart[kSpBuckets];
+  st->m = m;
+  st->M = m + 1;
+  if (st->fail) return;
+  st->b_l = sp_bucket(__dsub_rn(st->lx, ext->ax), __dsub_rn(st->ly, ext->ay), cdf, th);
+}
+
+// (c) P_l's exact position: the points of its bucket ordered before it by the
+// total order (angle key, dist2, index) -- a codes-only pass; only P_l's
+// bucket (~m/nb points) computes keys.
+__global__ void __launch_bounds__(256) k_sp_lrank(const double* __restrict__ xs,
+                                                  const double* __restrict__ ys,
+                                                  const uint16_t* __restrict__ codes, uint32_t n,
+                                                  const ExtResult* __restrict__ ext,
+                                                  SpState* __restrict__ st) {
+  if (st->fail) return;
+  const uint32_t b_l = st->b_l, l_idx = st->l_idx;
+  const double ax = ext->ax, ay = ext->ay;
+  const double ldx = __dsub_rn(st->lx, ax), ldy = __dsub_rn(st->ly, ay);
+  const uint64_t lkey = angle_key(ldx, ldy);
+  const double ld2 = dist2_rn(ldx, ldy);
+  const uint32_t* c2 = reinterpret_cast<const uint32_t*>(codes);
+  const uint32_t npairs = (n + 1) / 2;
+  uint32_t below = 0;
+  for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < npairs; p += gridDim.x * blockDim.x) {
+    const uint32_t cw = (2 * p + 1 < n) ? __ldcs(&c2[p]) : (uint32_t)codes[2 * p] | 0xffff0000u;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (((cw >> (16 * h)) & 0xffffu) != b_l) continue;
+      const uint32_t i = 2 * p + h;
+      if (i == l_idx) continue;
+      const double dx = __dsub_rn(xs[i], ax), dy = __dsub_rn(ys[i], ay);
+      below += key_less(angle_key(dx, dy), dist2_rn(dx, dy), i, lkey, ld2, l_idx);
+    }
+  }
+  if (below) atomicAdd(&st->l_below, below);
+}
+
+// (d) slice geometry from the exact l.
+__global__ void k_sp_steps(const uint32_t* __restrict__ bstart, uint64_t chunk_count,
+                           SpState* __restrict__ st) {
+  if (threadIdx.x != 0 || st->fail) return;
+  const uint32_t l = 1 + bstart[st->b_l] + st->l_below, M = st->M;
+  st->l = l;
+  const uint32_t c = (uint32_t)(chunk_count < 0xffffffffull ? chunk_count : 0xffffffffull);
+  const uint32_t mr = l - 1, ml = M - 1 - l;
+  if (mr < 2 || ml < 2) { st->fail |= kSpFailTiny; return; }
+  st->step_r = cdiv(mr, c);
+  st->n_right = cdiv(mr, st->step_r);
+  st->step_l = cdiv(ml, c);
+  st->n_left = cdiv(ml, st->step_l);
+}
+
+// (e) gathered buckets: P_l's bucket and every bucket holding a seed.
+__global__ void __launch_bounds__(256) k_sp_gbits(const uint32_t* __restrict__ bstart,
+                                                  SpState* __restrict__ st,
+                                                  uint32_t* __restrict__ gbits,
+                                                  uint32_t* __restrict__ glist) {
+  const uint32_t w = blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= kSpBuckets / 32) return;
+  const bool ok = !st->fail;
+  const uint32_t b_l = st->b_l, M = st->M, sr = st->step_r, sl = st->step_l;
+  uint32_t bits = 0;
+  if (ok) {
+    for (uint32_t k = 0; k < 32; ++k) {
+      const uint32_t b = w * 32 + k;
+      const uint32_t lo = 1 + bstart[b], hi = bstart[b + 1];
+      if (hi < lo) continue;  // empty
+      bool g = (b == b_l);
+      if (b < b_l) g = has_right_seed(lo, hi, sr);
+      if (b > b_l) g = has_left_seed(lo, hi, M, sl);
+      if (g) bits |= 1u << k;
+    }
+  }
+  gbits[w] = bits;
+  const uint32_t cnt = __popc(bits);
+  if (cnt) {
+    const uint32_t at = atomicAdd(&st->n_gb, cnt);
+    uint32_t k = 0;
+    for (uint32_t bb = bits; bb; bb &= bb - 1) glist[at + k++] = w * 32 + (__ffs(bb) - 1);
+  }
+}
+
+__device__ __forceinline__ bool sp_gathered(const uint32_t* g, uint32_t b) {
+  return (g[b >> 5] >> (b & 31)) & 1u;
+}
+
+// Per-CTA emission regions: CTA c of a streaming pass owns slots
+// [c * cap, (c + 1) * cap); cap bounds the points one CTA visits. Slots are
+// claimed with a shared-memory counter (warp-aggregated), so the streaming
+// loops never wait on a global atomic.
+__device__ __forceinline__ uint32_t warp_claim(uint32_t* s_counter, bool want) {
+  const uint32_t act = __activemask();
+  const uint32_t em = __ballot_sync(act, want);
+  if (!em) return 0;
+  const int lane = threadIdx.x & 31;
+  const int leader = __ffs(em) - 1;
+  uint32_t base = 0;
+  if (lane == leader) base = atomicAdd(s_counter, (uint32_t)__popc(em));
+  base = __shfl_sync(act, base, leader);
+  return base + __popc(em & lanemask_lt());
+}
+
+// ===========================================================================
+// F3: gathered points are emitted (index, bucket); other survivors fold phi
+// into the per-CTA bucket maximum; every bucketed survivor's 64-bit hash goes
+// to the CTA's hash list, counted per partition.
+template <bool kVec>
+__global__ void __launch_bounds__(kSpThreads, 1) k_sp_phi(
+    const double* __restrict__ xs, const double* __restrict__ ys,
+    const uint16_t* __restrict__ codes, uint32_t n, uint32_t cap, const ExtResult* __restrict__ ext,
+    const uint32_t* __restrict__ gbits, SpState* __restrict__ st, uint32_t* __restrict__ phi_part,
+    uint32_t* __restrict__ g_idx, uint32_t* __restrict__ g_b, uint32_t* __restrict__ g_count,
+    uint64_t* __restrict__ hlist, uint32_t* __restrict__ h_count, uint32_t* __restrict__ part_cnt) {
+  extern __shared__ uint32_t s_phi[];  // kSpBuckets
+  __shared__ uint32_t s_g[kSpBuckets / 32];
+  __shared__ uint32_t s_part[kSpParts];
+  __shared__ uint32_t s_ng, s_nh;
+  if (st->fail) return;
+  for (uint32_t b = threadIdx.x; b < kSpBuckets; b += blockDim.x) s_phi[b] = 0;
+  for (uint32_t w = threadIdx.x; w < kSpBuckets / 32; w += blockDim.x) s_g[w] = gbits[w];
+  for (uint32_t p = threadIdx.x; p < kSpParts; p += blockDim.x) s_part[p] = 0;
+  if (threadIdx.x == 0) { s_ng = 0; s_nh = 0; }
+  const double lx = st->lx, ly = st->ly;
+  const double ux = __dsub_rn(ext->ax, lx), uy = __dsub_rn(ext->ay, ly);
+  const uint32_t b_l = st->b_l;
+  const size_t base = (size_t)blockIdx.x * cap;
+  __syncthreads();
+  sp_stream_coded<kVec, 4>(xs, ys, codes, n, [&](double x, double y, uint32_t b, uint32_t i) {
+    const bool surv = b != kSpNoCode;
+    bool emit = false;
+    uint64_t h = 0;
+    if (surv) {
+      h = coord_hash64(x, y);
+      atomicAdd(&s_part[(uint32_t)(h >> (64 - kSpPartBits))], 1u);
+      if (sp_gathered(s_g, b)) {
+        emit = true;
+      } else {
+        const double ph = sp_phi(x, y, lx, ly, ux, uy, b < b_l);
+        atomicMax(&s_phi[b], ord_f(__double2float_rd(ph)));
+      }
+    }
+    const uint32_t jh = warp_claim(&s_nh, surv);
+    if (surv) hlist[base + jh] = h;
+    const uint32_t jg = warp_claim(&s_ng, emit);
+    if (emit) { g_idx[base + jg] = i; g_b[base + jg] = b; }
+  });
+  __syncthreads();
+  uint32_t* pp = phi_part + (size_t)blockIdx.x * kSpBuckets;
+  for (uint32_t b = threadIdx.x; b < kSpBuckets; b += blockDim.x) pp[b] = s_phi[b];
+  for (uint32_t p = threadIdx.x; p < kSpParts; p += blockDim.x)
+    part_cnt[(size_t)p * gridDim.x + blockIdx.x] = s_part[p];  // partition-major
+  if (threadIdx.x == 0) {
+    g_count[blockIdx.x] = s_ng;
+    h_count[blockIdx.x] = s_nh;
+    atomicAdd(&st->n_g, s_ng);
+  }
+}
+
+// Duplicate check, step 1: CTA c moves its hash list into the partitions
+// (offsets part_off[p * C + c], partition-major exclusive scan), chunk by
+// chunk through shared memory so that every partition gets a contiguous run.
+__global__ void __launch_bounds__(1024) k_sp_dup_part(const uint64_t* __restrict__ hlist,
+                                                      const uint32_t* __restrict__ h_count,
+                                                      uint32_t cap, const uint32_t* __restrict__ part_off,
+                                                      const SpState* __restrict__ st,
+                                                      uint64_t* __restrict__ parted) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint64_t* s_in = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* s_out = s_in + kSpPartChunk;
+  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_out + kSpPartChunk);
+  uint32_t* s_off = s_cnt + kSpParts;
+  uint32_t* s_cur = s_off + kSpParts;
+  __shared__ uint32_t s_w[32];
+  if (st->fail) return;
+  const uint32_t c = blockIdx.x, C = gridDim.x;
+  const uint32_t cnt = h_count[c];
+  const uint64_t* src = hlist + (size_t)c * cap;
+  for (uint32_t p = threadIdx.x; p < kSpParts; p += blockDim.x) s_cur[p] = part_off[(size_t)p * C + c];
+  for (uint32_t c0 = 0; c0 < cnt; c0 += kSpPartChunk) {
+    const uint32_t len = min(kSpPartChunk, cnt - c0);
+    for (uint32_t p = threadIdx.x; p < kSpParts; p += blockDim.x) s_cnt[p] = 0;
+    __syncthreads();
+    for (uint32_t t = threadIdx.x; t < len; t += blockDim.x) {
+      const uint64_t h = src[c0 + t];
+      s_in[t] = h;
+      atomicAdd(&s_cnt[(uint32_t)(h >> (64 - kSpPartBits))], 1u);
+    }
+    __syncthreads();
+    // exclusive scan of the partition counts (kSpParts = 2 x blockDim)
+    {
+      const uint32_t a = s_cnt[2 * threadIdx.x], b = s_cnt[2 * threadIdx.x + 1];
+      const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+      uint32_t x = a + b;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (lane == 31) s_w[warp] = x;
+      __syncthreads();
+      if (warp == 0) {
+        uint32_t v = s_w[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, v, o);
+          if (lane >= o) v += y;
+        }
+        s_w[lane] = v;
+      }
+      __syncthreads();
+      const uint32_t ex = x - (a + b) + (warp ? s_w[warp - 1] : 0);
+      s_off[2 * threadIdx.x] = ex;
+      s_off[2 * threadIdx.x + 1] = ex + a;
+    }
+    __syncthreads();
+    for (uint32_t t = threadIdx.x; t < len; t += blockDim.x) {
+      const uint64_t h = s_in[t];
+      const uint32_t p = (uint32_t)(h >> (64 - kSpPartBits));
+      s_out[atomicAdd(&s_off[p], 1u)] = h;  // s_off[p] ends at the next run's start
+    }
+    __syncthreads();
+    for (uint32_t t = threadIdx.x; t < len; t += blockDim.x) {
+      const uint64_t h = s_out[t];
+      const uint32_t p = (uint32_t)(h >> (64 - kSpPartBits));
+      const uint32_t run0 = s_off[p] - s_cnt[p];
+      parted[s_cur[p] + (t - run0)] = h;
+    }
+    __syncthreads();
+    for (uint32_t p = threadIdx.x; p < kSpParts; p += blockDim.x) s_cur[p] += s_cnt[p];
+  }
+}
+
+// Duplicate check, step 2: CTA per partition, open-addressing set of the
+// 64-bit hashes in shared memory (in rounds over sub-ranges of the hash);
+// an equal hash means a possible duplicate -> the full path (exact).
+__global__ void __launch_bounds__(512) k_sp_dups(const uint64_t* __restrict__ parted,
+                                                 const uint32_t* __restrict__ part_off,
+                                                 uint32_t nparts_cta, SpState* __restrict__ st) {
+  extern __shared__ unsigned long long s_e[];  // kSpDupSlots
+  if (st->fail) return;
+  const uint32_t total = st->m;
+  const uint32_t p = blockIdx.x;
+  const uint32_t lo = part_off[(size_t)p * nparts_cta];
+  const uint32_t hi = (p + 1 < kSpParts) ? part_off[(size_t)(p + 1) * nparts_cta] : total;
+  const uint32_t rounds = (hi - lo + kSpDupRound - 1) / kSpDupRound;
+  bool dup = false, full = false;
+  for (uint32_t r = 0; r < rounds; ++r) {
+    for (uint32_t k = threadIdx.x; k < kSpDupSlots; k += blockDim.x) s_e[k] = ~0ull;
+    __syncthreads();
+    for (uint32_t e = lo + threadIdx.x; e < hi && !dup && !full; e += blockDim.x) {
+      const uint64_t h = parted[e];
+      const uint32_t mid = (uint32_t)(h >> 20) & 0xffffu;  // bits below the partition
+      if ((uint32_t)(((uint64_t)mid * rounds) >> 16) != r) continue;
+      uint32_t slot = (uint32_t)h & (kSpDupSlots - 1);
+      for (uint32_t probe = 0;; ++probe) {
+        if (probe == kSpDupSlots / 2) { full = true; break; }
+        const unsigned long long prev = atomicCAS(&s_e[slot], ~0ull, (unsigned long long)h);
+        if (prev == ~0ull) break;
+        if (prev == h) { dup = true; break; }
+        slot = (slot + 1) & (kSpDupSlots - 1);
+      }
+    }
+    if (__syncthreads_or(dup || full)) break;
+  }
+  if (dup) { atomicAdd(&st->dups, 1u); atomicOr(&st->fail, kSpFailDup); }
+  if (full) atomicOr(&st->fail, kSpFailCap);
+}
+
+// Emitted elements (per-CTA regions) -> bucket slots start[b] + rank as
+// 32-byte records {exact key, x, y, idx, bucket}; the glibc-exact atan2 runs
+// here, densely. rank: arrival order (atomic on cnt[b]); with store_rank the
+// rank is only recorded (first phase of a two-phase placement).
+template <int kPhase>  // 0: rank + scatter (start known), 1: rank only, 2: scatter with stored rank
+__global__ void __launch_bounds__(256) k_sp_emit_place(
+    const double* __restrict__ xs, const double* __restrict__ ys, const uint32_t* __restrict__ e_idx,
+    const uint32_t* __restrict__ e_b, uint32_t* __restrict__ e_rank,
+    const uint32_t* __restrict__ e_count, uint32_t cap, uint32_t* __restrict__ cnt,
+    const uint32_t* __restrict__ start, const ExtResult* __restrict__ ext,
+    const SpState* __restrict__ st, PtRec* __restrict__ rec) {
+  if (st->fail) return;
+  const uint32_t c = blockIdx.y;
+  const uint32_t ne = e_count[c];
+  const size_t base = (size_t)c * cap;
+  const double ax = ext->ax, ay = ext->ay;
+  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < ne; k += gridDim.x * blockDim.x) {
+    const uint32_t b = e_b[base + k];
+    uint32_t r;
+    if (kPhase == 2) r = e_rank[base + k];
+    else r = atomicAdd(&cnt[b], 1u);
+    if (kPhase == 1) { e_rank[base + k] = r; continue; }
+    const uint32_t i = e_idx[base + k];
+    PtRec o;
+    o.x = xs[i];
+    o.y = ys[i];
+    o.key = angle_key(__dsub_rn(o.x, ax), __dsub_rn(o.y, ay));
+    o.idx = i;
+    o.pad = b;
+    rec[start[b] + r] = o;
+  }
+}
+
+// CTA-wide exact sort of one bucket's records (cnt <= kSpGatherCap) in shared
+// memory: bitonic sort of a permutation under the total order (angle key,
+// dist2, input index) -- the reference's stable (angle, dist2) order,
+// angular.hpp:154-194. out(rank, x, y, idx) receives every element; returns
+// true when two elements are equal points (annotate's dedup would drop one).
+constexpr int kSpSortThreads = 512;
+constexpr size_t kSpSortSmem = (size_t)kSpGatherCap * (8 + 8 + 8 + 8 + 4 + 2);
+
+template <typename Out>
+__device__ bool cta_sort_bucket(const PtRec* __restrict__ R, uint32_t cnt, double ax, double ay,
+                                unsigned char* smem, Out&& out) {
+  uint64_t* s_key = reinterpret_cast<uint64_t*>(smem);
+  double* s_d2 = reinterpret_cast<double*>(s_key + kSpGatherCap);
+  double* s_x = s_d2 + kSpGatherCap;
+  double* s_y = s_x + kSpGatherCap;
+  uint32_t* s_idx = reinterpret_cast<uint32_t*>(s_y + kSpGatherCap);
+  uint16_t* s_perm = reinterpret_cast<uint16_t*>(s_idx + kSpGatherCap);
+  uint32_t P = 32;
+  while (P < cnt) P <<= 1;
+  __syncthreads();
+  for (uint32_t t = threadIdx.x; t < P; t += blockDim.x) {
+    s_perm[t] = (uint16_t)t;
+    if (t < cnt) {
+      const PtRec r = ld_rec256(&R[t]);
+      s_key[t] = r.key;
+      s_x[t] = r.x;
+      s_y[t] = r.y;
+      s_idx[t] = r.idx;
+      s_d2[t] = dist2_rn(__dsub_rn(r.x, ax), __dsub_rn(r.y, ay));
+    }
+  }
+  __syncthreads();
+  auto less = [&](uint32_t a, uint32_t b) -> bool {
+    if (a >= cnt) return false;
+    if (b >= cnt) return true;
+    return key_less(s_key[a], s_d2[a], s_idx[a], s_key[b], s_d2[b], s_idx[b]);
+  };
+  for (uint32_t k = 2; k <= P; k <<= 1) {
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) {
+        const uint32_t ixj = i ^ j;
+        if (ixj > i) {
+          const uint32_t ea = s_perm[i], eb = s_perm[ixj];
+          const bool up = (i & k) == 0;
+          if (up ? less(eb, ea) : less(ea, eb)) { s_perm[i] = (uint16_t)eb; s_perm[ixj] = (uint16_t)ea; }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  bool dup = false;
+  for (uint32_t r = threadIdx.x; r < cnt; r += blockDim.x) {
+    const uint32_t e = s_perm[r];
+    for (int32_t q = (int32_t)r - 1; q >= 0; --q) {  // equal points share (key, dist2)
+      const uint32_t f = s_perm[q];
+      if (s_key[f] != s_key[e] || s_d2[f] != s_d2[e]) break;
+      if (s_x[f] == s_x[e] && s_y[f] == s_y[e]) { dup = true; break; }
+    }
+    out(r, s_x[e], s_y[e], s_idx[e]);
+  }
+  return dup;
+}
+
+// Gathered buckets, CTA per bucket: exact positions 1 + bstart[b] + rank in
+// the annotated-buffer space A; records the exact position of P_l.
+__global__ void __launch_bounds__(kSpSortThreads) k_sp_sort_gathered(
+    const uint32_t* __restrict__ glist, const uint32_t* __restrict__ bstart,
+    const uint32_t* __restrict__ hist, const uint32_t* __restrict__ gcnt,
+    const PtRec* __restrict__ rec, const ExtResult* __restrict__ ext, SpState* __restrict__ st,
+    double* __restrict__ A_x, double* __restrict__ A_y, uint32_t* __restrict__ A_i) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  if (st->fail) return;
+  const uint32_t ngb = st->n_gb, l_idx = st->l_idx;
+  const double ax = ext->ax, ay = ext->ay;
+  for (uint32_t g = blockIdx.x; g < ngb; g += gridDim.x) {
+    const uint32_t b = glist[g];
+    const uint32_t s0 = bstart[b], cnt = hist[b];
+    if (gcnt[b] != cnt) {  // every point of a gathered bucket must have been emitted
+      if (threadIdx.x == 0) { atomicOr(&st->fail, kSpFailInternal); atomicMax(&st->why, 1u); }
+      return;
+    }
+    if (threadIdx.x == 0) atomicMax(&st->max_g, cnt);
+    if (cnt > kSpGatherCap) {
+      if (threadIdx.x == 0) { atomicOr(&st->fail, kSpFailCap); atomicMax(&st->why, 4u); }
+      return;
+    }
+    const bool dup = cta_sort_bucket(rec + s0, cnt, ax, ay, smem,
+                                     [&](uint32_t r, double x, double y, uint32_t idx) {
+      const uint32_t pos = 1 + s0 + r;
+      A_x[pos] = x;
+      A_y[pos] = y;
+      A_i[pos] = idx;
+      if (idx == l_idx) st->l_check = pos;
+    });
+    if (dup) atomicOr(&st->fail, kSpFailDup);
+  }
+}
+
+// Position -> bucket (the non-empty bucket holding it): largest b with
+// bstart[b] <= pos - 1.
+__device__ __forceinline__ uint32_t bucket_of_pos(const uint32_t* __restrict__ bstart, uint32_t pos) {
+  uint32_t lo = 0, hi = kSpBuckets - 1;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi + 1) >> 1;
+    if (bstart[mid] <= pos - 1) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+// Slice s (global numbering: right 0..n_right-1, left n_right + s): positions
+// [lo, hi] and its seed.
+struct SliceSpan {
+  uint32_t lo, hi, seed;
+  bool right;
+};
+__device__ __forceinline__ SliceSpan slice_span(const SpState& st, uint32_t s) {
+  SliceSpan r;
+  if (s < st.n_right) {
+    r.right = true;
+    r.lo = 1 + s * st.step_r;
+    r.hi = min(r.lo + st.step_r, st.l) - 1;
+    r.seed = r.lo;
+  } else {
+    r.right = false;
+    const uint32_t k = s - st.n_right;
+    const uint32_t ml = st.M - 1 - st.l;
+    r.hi = st.M - 1 - k * st.step_l;
+    r.lo = st.M - 1 - min(k * st.step_l + st.step_l - 1, ml - 1);
+    r.seed = r.hi;
+  }
+  return r;
+}
+
+// One warp per slice: the head of the slice (its points inside the seed's
+// gathered bucket, exact positions), then an exclusive running maximum of
+// phi over the slice's buckets in walk order -> prefmax[b] and slice_of[b]
+// for every non-gathered bucket. Gathered buckets inside a slice (possible
+// when the step was ambiguous) contribute nothing (conservative).
+__global__ void __launch_bounds__(256) k_sp_slices(
+    const SpState* __restrict__ st_, const uint32_t* __restrict__ bstart,
+    const uint32_t* __restrict__ gbits, const uint32_t* __restrict__ phimax,
+    const double* __restrict__ A_x, const double* __restrict__ A_y,
+    const ExtResult* __restrict__ ext, uint32_t* __restrict__ prefmax,
+    uint32_t* __restrict__ slice_of) {
+  const SpState st = *st_;
+  if (st.fail) return;
+  const uint32_t s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (s >= st.n_right + st.n_left) return;
+  const SliceSpan sp = slice_span(st, s);
+  const double lx = st.lx, ly = st.ly;
+  const double ux = __dsub_rn(ext->ax, lx), uy = __dsub_rn(ext->ay, ly);
+  const uint32_t bs = bucket_of_pos(bstart, sp.seed);
+  // head: slice positions inside the seed's bucket
+  uint32_t h0, h1;  // inclusive position range
+  if (sp.right) { h0 = sp.seed; h1 = min(sp.hi, bstart[bs + 1]); }
+  else { h0 = max(sp.lo, 1 + bstart[bs]); h1 = sp.seed; }
+  double hm = -1e300;
+  for (uint32_t p = h0 + lane; p <= h1; p += 32) hm = fmax(hm, sp_phi(A_x[p], A_y[p], lx, ly, ux, uy, sp.right));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) hm = fmax(hm, __shfl_xor_sync(0xffffffffu, hm, o));
+  uint32_t run = ord_f(__double2float_rd(hm));
+  // buckets after the seed's bucket up to the bucket holding the slice's last
+  // walk position; a non-gathered one there ends exactly at the slice end
+  // (otherwise it would hold the next seed and be gathered)
+  const uint32_t be = bucket_of_pos(bstart, sp.right ? sp.hi : sp.lo);
+  if (sp.right) {
+    for (uint32_t b0 = bs + 1; b0 <= be; b0 += 32) {
+      const uint32_t b = b0 + lane;
+      const bool in = b <= be && !sp_gathered(gbits, b);
+      uint32_t v = in ? phimax[b] : 0u;
+      uint32_t inc = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc = max(inc, y);
+      }
+      const uint32_t up = __shfl_up_sync(0xffffffffu, inc, 1);
+      const uint32_t excl = max(run, lane ? up : 0u);
+      if (in) { prefmax[b] = excl; slice_of[b] = s; }
+      run = max(run, __shfl_sync(0xffffffffu, inc, 31));
+    }
+  } else {
+    // walk order descending: buckets bs-1 down to be
+    for (int32_t b0 = (int32_t)bs - 1; b0 >= (int32_t)be; b0 -= 32) {
+      const int32_t b = b0 - lane;
+      const bool in = b >= (int32_t)be && !sp_gathered(gbits, (uint32_t)b);
+      uint32_t v = in ? phimax[b] : 0u;
+      uint32_t inc = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc = max(inc, y);
+      }
+      const uint32_t up = __shfl_up_sync(0xffffffffu, inc, 1);
+      const uint32_t excl = max(run, lane ? up : 0u);
+      if (in) { prefmax[b] = excl; slice_of[b] = s; }
+      run = max(run, __shfl_sync(0xffffffffu, inc, 31));
+    }
+  }
+}
+
+// ===========================================================================
+// F4: candidates = non-gathered survivors whose phi is not below their
+// bucket's exclusive prefix maximum (minus kSpTol); emitted to the CTA's
+// region and marked in the codes (the verification skips them).
+__device__ __forceinline__ bool sp_is_candidate(double ph, uint32_t pm, bool drop) {
+  return !drop && ph >= unord_f(pm) - kSpTol;
+}
+
+template <bool kVec>
+__global__ void __launch_bounds__(kSpThreads, 1) k_sp_cand(
+    const double* __restrict__ xs, const double* __restrict__ ys, uint16_t* __restrict__ codes,
+    uint32_t n, uint32_t cap, const ExtResult* __restrict__ ext, const uint32_t* __restrict__ gbits,
+    const uint32_t* __restrict__ prefmax, SpState* __restrict__ st, uint32_t* __restrict__ c_idx,
+    uint32_t* __restrict__ c_b, uint32_t* __restrict__ c_count, bool drop) {
+  extern __shared__ uint32_t s_pm[];  // kSpBuckets
+  __shared__ uint32_t s_g[kSpBuckets / 32];
+  __shared__ uint32_t s_nc;
+  if (st->fail) return;
+  for (uint32_t b = threadIdx.x; b < kSpBuckets; b += blockDim.x) s_pm[b] = prefmax[b];
+  for (uint32_t w = threadIdx.x; w < kSpBuckets / 32; w += blockDim.x) s_g[w] = gbits[w];
+  if (threadIdx.x == 0) s_nc = 0;
+  const double lx = st->lx, ly = st->ly;
+  const double ux = __dsub_rn(ext->ax, lx), uy = __dsub_rn(ext->ay, ly);
+  const uint32_t b_l = st->b_l;
+  const size_t base = (size_t)blockIdx.x * cap;
+  __syncthreads();
+  sp_stream_coded<kVec, 4>(xs, ys, codes, n, [&](double x, double y, uint32_t b, uint32_t i) {
+    bool emit = false;
+    if (b != kSpNoCode && !sp_gathered(s_g, b))
+      emit = sp_is_candidate(sp_phi(x, y, lx, ly, ux, uy, b < b_l), s_pm[b], drop);
+    const uint32_t j = warp_claim(&s_nc, emit);
+    if (emit) {
+      c_idx[base + j] = i;
+      c_b[base + j] = b;
+      codes[i] = (uint16_t)kSpCandCode;
+    }
+  });
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    c_count[blockIdx.x] = s_nc;
+    atomicAdd(&st->n_c, s_nc);
+  }
+}
+
+// Walk-array bucket sizes: gathered buckets bring all their points, others
+// their candidates.
+__global__ void k_sp_wcount(const uint32_t* __restrict__ gbits, const uint32_t* __restrict__ hist,
+                            const uint32_t* __restrict__ ccnt, uint32_t* __restrict__ wcnt) {
+  const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < kSpBuckets) wcnt[b] = sp_gathered(gbits, b) ? hist[b] : ccnt[b];
+}
+
+__device__ __forceinline__ uint32_t slice_of_pos(const SpState& st, uint32_t p) {
+  if (p == 0 || p == st.l) return kNone;
+  if (p < st.l) return (p - 1) / st.step_r;
+  return st.n_right + (st.M - 1 - p) / st.step_l;
+}
+
+// Candidates, warp per bucket: up to 32 per bucket are ranked in registers
+// by the exact total order and written to the walk array W at
+// 1 + wstart[b] + rank; larger buckets go to a list for the CTA sorter.
+// Equal points -> fail.
+__global__ void __launch_bounds__(256) k_sp_place_cand(
+    const PtRec* __restrict__ crec, const uint32_t* __restrict__ cstart,
+    const uint32_t* __restrict__ wstart, const uint32_t* __restrict__ slice_of,
+    const ExtResult* __restrict__ ext, SpState* __restrict__ st, uint32_t* __restrict__ big,
+    double* __restrict__ W_x, double* __restrict__ W_y, uint32_t* __restrict__ W_i,
+    uint32_t* __restrict__ W_b, uint32_t* __restrict__ W_s, uint8_t* __restrict__ flags) {
+  if (st->fail) return;
+  const double ax = ext->ax, ay = ext->ay;
+  const int lane = threadIdx.x & 31;
+  const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
+  for (uint32_t b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < kSpBuckets; b += nwarps) {
+    const uint32_t c0 = cstart[b], cnt = cstart[b + 1] - c0;
+    if (cnt == 0) continue;
+    const uint32_t sl = slice_of[b];
+    if (sl == kNone) {
+      if (lane == 0) { atomicOr(&st->fail, kSpFailInternal); atomicMax(&st->why, 3u); }
+      continue;
+    }
+    if (cnt > 32) {
+      if (lane == 0) big[atomicAdd(&st->n_bigc, 1u)] = b;
+      continue;
+    }
+    PtRec r{};
+    double d = 0.0;
+    if ((uint32_t)lane < cnt) {
+      r = ld_rec256(&crec[c0 + lane]);
+      d = dist2_rn(__dsub_rn(r.x, ax), __dsub_rn(r.y, ay));
+    }
+    uint32_t rk = 0;
+    bool dup = false;
+    for (uint32_t k = 0; k < cnt; ++k) {
+      const uint64_t ok = __shfl_sync(0xffffffffu, r.key, k);
+      const double od = __shfl_sync(0xffffffffu, d, k);
+      const uint32_t oi = __shfl_sync(0xffffffffu, r.idx, k);
+      const double ox = __shfl_sync(0xffffffffu, r.x, k);
+      const double oy = __shfl_sync(0xffffffffu, r.y, k);
+      if ((uint32_t)lane < cnt && k != (uint32_t)lane) {
+        rk += key_less(ok, od, oi, r.key, d, r.idx);
+        dup |= (ox == r.x && oy == r.y);
+      }
+    }
+    if (__any_sync(0xffffffffu, dup) && lane == 0) atomicOr(&st->fail, kSpFailDup);
+    if ((uint32_t)lane < cnt) {
+      const uint32_t w = 1 + wstart[b] + rk;
+      W_x[w] = r.x;
+      W_y[w] = r.y;
+      W_i[w] = r.idx;
+      W_b[w] = b;
+      W_s[w] = sl;
+      flags[w] = 1;
+    }
+  }
+}
+
+// Candidate buckets with more than 32 candidates: CTA sorter.
+__global__ void __launch_bounds__(kSpSortThreads) k_sp_sort_cand_big(
+    const uint32_t* __restrict__ big, const PtRec* __restrict__ crec,
+    const uint32_t* __restrict__ cstart, const uint32_t* __restrict__ wstart,
+    const uint32_t* __restrict__ slice_of, const ExtResult* __restrict__ ext,
+    SpState* __restrict__ st, double* __restrict__ W_x, double* __restrict__ W_y,
+    uint32_t* __restrict__ W_i, uint32_t* __restrict__ W_b, uint32_t* __restrict__ W_s,
+    uint8_t* __restrict__ flags) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  if (st->fail) return;
+  const uint32_t nbig = st->n_bigc;
+  const double ax = ext->ax, ay = ext->ay;
+  for (uint32_t g = blockIdx.x; g < nbig; g += gridDim.x) {
+    const uint32_t b = big[g];
+    const uint32_t c0 = cstart[b], cnt = cstart[b + 1] - c0;
+    if (cnt > kSpGatherCap) {
+      if (threadIdx.x == 0) { atomicOr(&st->fail, kSpFailCap); atomicMax(&st->why, 5u); }
+      return;
+    }
+    const uint32_t w0 = 1 + wstart[b], sl = slice_of[b];
+    const bool dup = cta_sort_bucket(crec + c0, cnt, ax, ay, smem,
+                                     [&](uint32_t r, double x, double y, uint32_t idx) {
+      W_x[w0 + r] = x;
+      W_y[w0 + r] = y;
+      W_i[w0 + r] = idx;
+      W_b[w0 + r] = b;
+      W_s[w0 + r] = sl;
+      flags[w0 + r] = 1;
+    });
+    if (dup) atomicOr(&st->fail, kSpFailDup);
+  }
+}
+
+// Gathered buckets: copy their exactly placed points from A to W (CTA per
+// gathered bucket); W[0] = anchor.
+__global__ void __launch_bounds__(256) k_sp_place_gathered(
+    const uint32_t* __restrict__ glist, const uint32_t* __restrict__ bstart,
+    const uint32_t* __restrict__ hist, const uint32_t* __restrict__ wstart,
+    const double* __restrict__ A_x, const double* __restrict__ A_y,
+    const uint32_t* __restrict__ A_i, const ExtResult* __restrict__ ext, SpState* __restrict__ st_,
+    double* __restrict__ W_x, double* __restrict__ W_y, uint32_t* __restrict__ W_i,
+    uint32_t* __restrict__ W_b, uint32_t* __restrict__ W_s, uint8_t* __restrict__ flags) {
+  const SpState st = *st_;
+  if (st.fail) return;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    flags[0] = 1;
+    W_x[0] = ext->ax;
+    W_y[0] = ext->ay;
+    W_i[0] = ext->idx[4];
+    W_b[0] = kNone;
+    W_s[0] = kNone;
+    st_->n_w = 1 + wstart[kSpBuckets];
+    if (st.l_check != st.l) { atomicOr(&st_->fail, kSpFailInternal); atomicMax(&st_->why, 2u); }
+  }
+  for (uint32_t g = blockIdx.x; g < st.n_gb; g += gridDim.x) {
+    const uint32_t b = glist[g];
+    const uint32_t s0 = bstart[b], cnt = hist[b], w0 = wstart[b];
+    for (uint32_t r = threadIdx.x; r < cnt; r += blockDim.x) {
+      const uint32_t p = 1 + s0 + r, w = 1 + w0 + r;
+      W_x[w] = A_x[p];
+      W_y[w] = A_y[p];
+      W_i[w] = A_i[p];
+      W_b[w] = b;
+      W_s[w] = slice_of_pos(st, p);
+      flags[w] = 1;
+    }
+  }
+}
+
+// Slice segments in W: seg_lo[s] = first W index of slice s, seg_hi[s] = one
+// past its last (slices are contiguous because W is exactly ordered).
+__global__ void k_sp_segments(const uint32_t* __restrict__ W_s, const SpState* __restrict__ st,
+                              uint32_t* __restrict__ seg_lo, uint32_t* __restrict__ seg_hi) {
+  if (st->fail) return;
+  const uint32_t nw = st->n_w;
+  for (uint32_t j = 1 + blockIdx.x * blockDim.x + threadIdx.x; j < nw; j += gridDim.x * blockDim.x) {
+    const uint32_t s = W_s[j];
+    if (s == kNone) continue;
+    if (W_s[j - 1] != s) seg_lo[s] = j;
+    if (j + 1 == nw || W_s[j + 1] != s) seg_hi[s] = j + 1;
+  }
+}
+
+// Round-2 walk (discard.hpp:36-66) of one slice over its walked points in W:
+// CTA per slice; the speculate-and-verify scheme of k_round2_block with an
+// explicit segment. Right slices walk ascending from their first element,
+// left slices descending from their last.
+__global__ void __launch_bounds__(kWalkBlock) k_sp_walk(
+    const double* __restrict__ A_x, const double* __restrict__ A_y,
+    const uint32_t* __restrict__ seg_lo, const uint32_t* __restrict__ seg_hi,
+    const SpState* __restrict__ st_, const ExtResult* __restrict__ ext,
+    uint8_t* __restrict__ flags) {
+  const SpState& st = *st_;
+  if (st.fail) return;
+  const uint32_t slice = blockIdx.x;
+  if (slice >= st.n_right + st.n_left) return;
+  const uint32_t lo = seg_lo[slice], hi = seg_hi[slice];
+  const int dir = slice < st.n_right ? 1 : -1;
+  const uint32_t seed = dir > 0 ? lo : hi - 1;
+  const uint32_t start = dir > 0 ? lo + 1 : hi - 2;
+  const uint32_t count = hi - lo - 1;
+  if (count == 0 || count > 0x7fffffffu) return;
+  __shared__ MaxPair s_wm[kWalkBlock / 32];
+  __shared__ int32_t s_first;
+  __shared__ MaxPair s_carry;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double lx = st.lx, ly = st.ly;
+  const double ux = ext->ax - lx, uy = ext->ay - ly;
+  const double sgn = (dir > 0) ? 1.0 : -1.0;
+  auto wpos = [&](int32_t k) -> uint32_t {
+    return k < 0 ? seed : ((dir > 0) ? start + (uint32_t)k : start - (uint32_t)k);
+  };
+  MaxPair carry;
+  carry.v = sgn * pseudo_angle(A_x[seed], A_y[seed], lx, ly, ux, uy);
+  carry.k = -1;
+  int32_t w0 = 0;
+  while (w0 < (int32_t)count) {
+    double px[kWalkItems], py[kWalkItems], ph[kWalkItems];
+    bool val[kWalkItems];
+    const int32_t k0 = w0 + threadIdx.x * kWalkItems;
+#pragma unroll
+    for (int u = 0; u < kWalkItems; ++u) {
+      const int32_t k = k0 + u;
+      val[u] = k < (int32_t)count;
+      if (val[u]) {
+        const uint32_t p = wpos(k);
+        px[u] = A_x[p];
+        py[u] = A_y[p];
+        ph[u] = sgn * pseudo_angle(px[u], py[u], lx, ly, ux, uy);
+      } else {
+        px[u] = py[u] = 0.0;
+        ph[u] = -1e300;
+      }
+    }
+    MaxPair agg{-1e300, INT32_MIN};
+#pragma unroll
+    for (int u = 0; u < kWalkItems; ++u)
+      if (val[u]) agg = mp_max(agg, MaxPair{ph[u], k0 + u});
+    MaxPair inc = agg;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      MaxPair y;
+      y.v = __shfl_up_sync(0xffffffffu, inc.v, o);
+      y.k = __shfl_up_sync(0xffffffffu, inc.k, o);
+      if (lane >= o) inc = mp_max(inc, y);
+    }
+    if (lane == 31) s_wm[warp] = inc;
+    if (threadIdx.x == 0) s_first = INT32_MAX;
+    __syncthreads();
+    MaxPair ex = carry;
+    for (int w = 0; w < warp; ++w) ex = mp_max(ex, s_wm[w]);
+    MaxPair prev;
+    prev.v = __shfl_up_sync(0xffffffffu, inc.v, 1);
+    prev.k = __shfl_up_sync(0xffffffffu, inc.k, 1);
+    if (lane > 0) ex = mp_max(ex, prev);
+    bool cand_keep[kWalkItems], ex_disc[kWalkItems];
+    int32_t tk[kWalkItems];
+#pragma unroll
+    for (int u = 0; u < kWalkItems; ++u) {
+      tk[u] = ex.k;
+      cand_keep[u] = val[u] && ph[u] >= ex.v;
+      ex_disc[u] = false;
+      if (val[u]) {
+        const uint32_t tp = wpos(ex.k);
+        const double c = cross_rn(A_x[tp], A_y[tp], lx, ly, px[u], py[u]);
+        ex_disc[u] = (dir > 0) ? (c > 0.0) : (c < 0.0);
+        if (ex_disc[u] == cand_keep[u]) atomicMin(&s_first, k0 + u);
+        ex = mp_max(ex, MaxPair{ph[u], k0 + u});
+      }
+    }
+    __syncthreads();
+    const int32_t f = s_first;
+#pragma unroll
+    for (int u = 0; u < kWalkItems; ++u) {
+      const int32_t k = k0 + u;
+      if (!val[u] || k > f) continue;
+      const bool disc = (k < f) ? !cand_keep[u] : ex_disc[u];
+      if (disc) flags[wpos(k)] = 0;
+      if (k == f) {
+        MaxPair nc;
+        if (ex_disc[u]) {
+          const uint32_t tp = wpos(tk[u]);
+          nc.v = sgn * pseudo_angle(A_x[tp], A_y[tp], lx, ly, ux, uy);
+          nc.k = tk[u];
+        } else {
+          nc.v = ph[u];
+          nc.k = k;
+        }
+        s_carry = nc;
+      }
+    }
+    if (f == INT32_MAX) {
+      MaxPair tot = carry;
+      for (int w = 0; w < kWalkBlock / 32; ++w) tot = mp_max(tot, s_wm[w]);
+      carry = tot;
+      w0 += kWalkWin;
+      __syncthreads();
+    } else {
+      __syncthreads();
+      carry = s_carry;
+      w0 = f + 1;
+    }
+  }
+}
+
+// R bucket index: rlo[b] = first R position whose bucket >= b (anchor = -1).
+__global__ void k_sp_rlo(const uint32_t* __restrict__ R_b, const SpState* __restrict__ st,
+                         uint32_t* __restrict__ rlo) {
+  if (st->fail) return;
+  const uint32_t nr = st->n_r;
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j <= nr; j += gridDim.x * blockDim.x) {
+    const int64_t prev = (j == 0) ? -2 : (j == 1 ? -1 : (int64_t)R_b[j - 1]);
+    const int64_t cur = (j == nr) ? (int64_t)kSpBuckets : (j == 0 ? -1 : (int64_t)R_b[j]);
+    for (int64_t b = prev + 1; b <= cur; ++b)
+      if (b >= 0) rlo[b] = j;
+  }
+}
+
+// ===========================================================================
+// F6: every survivor that was not walked must be discarded by the reference
+// walk. Its walk state is the last kept point before it in its slice: the
+// last kept point before its bucket or a kept point of its own bucket
+// (discard.hpp:44-50, 58-64); it must be strictly inside against all of them.
+// The kept points' loads are issued for 8 points at once (memory-level
+// parallelism).
+template <bool kVec>
+__global__ void __launch_bounds__(kSpThreads, 1) k_sp_verify(
+    const double* __restrict__ xs, const double* __restrict__ ys,
+    const uint16_t* __restrict__ codes, uint32_t n, const uint32_t* __restrict__ gbits,
+    const uint32_t* __restrict__ rlo, const double* __restrict__ R_x,
+    const double* __restrict__ R_y, SpState* __restrict__ st) {
+  extern __shared__ uint32_t s_rlo[];  // kSpBuckets + 1
+  __shared__ uint32_t s_g[kSpBuckets / 32];
+  if (st->fail) return;
+  for (uint32_t b = threadIdx.x; b <= kSpBuckets; b += blockDim.x) s_rlo[b] = rlo[b];
+  for (uint32_t w = threadIdx.x; w < kSpBuckets / 32; w += blockDim.x) s_g[w] = gbits[w];
+  const double lx = st->lx, ly = st->ly;
+  const uint32_t b_l = st->b_l;
+  __syncthreads();
+  uint32_t bad = 0;
+  auto check8 = [&](const double* px, const double* py, const uint32_t* pc, int cnt) {
+    uint32_t jb[8], j0[8], j1[8];
+    bool act[8];
+    double tx[8], ty[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const uint32_t b = pc[u];
+      act[u] = u < cnt && b < kSpCandCode && !sp_gathered(s_g, b);
+      jb[u] = 0;
+      j0[u] = j1[u] = 0;
+      if (act[u]) {
+        j0[u] = s_rlo[b];
+        j1[u] = s_rlo[b + 1];
+        jb[u] = (b < b_l) ? j0[u] - 1 : j1[u];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      tx[u] = act[u] ? R_x[jb[u]] : 0.0;
+      ty[u] = act[u] ? R_y[jb[u]] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (!act[u]) continue;
+      const bool right = pc[u] < b_l;
+      double c = cross_rn(tx[u], ty[u], lx, ly, px[u], py[u]);
+      bool ok = right ? (c > 0.0) : (c < 0.0);
+      for (uint32_t j = j0[u]; j < j1[u]; ++j) {
+        c = cross_rn(R_x[j], R_y[j], lx, ly, px[u], py[u]);
+        ok = ok && (right ? (c > 0.0) : (c < 0.0));
+      }
+      bad += !ok;
+    }
+  };
+  const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t nth = gridDim.x * blockDim.x;
+  if (kVec) {
+    const double2* x2 = reinterpret_cast<const double2*>(xs);
+    const double2* y2 = reinterpret_cast<const double2*>(ys);
+    const uint32_t* c2 = reinterpret_cast<const uint32_t*>(codes);
+    const uint32_t np = n / 2;
+    for (uint32_t p = tid; p < np; p += 4 * nth) {
+      double px[8], py[8];
+      uint32_t pc[8];
+      int cnt = 0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t q = p + u * nth;
+        if (q < np) {
+          const uint32_t cw = __ldcs(&c2[q]);
+          pc[2 * u] = cw & 0xffffu;
+          pc[2 * u + 1] = cw >> 16;
+          cnt = 2 * u + 2;
+        } else {
+          pc[2 * u] = pc[2 * u + 1] = kSpNoCode;
+        }
+      }
+      // coordinates only for pairs that hold a point to verify
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t q = p + u * nth;
+        const bool need = (pc[2 * u] < kSpCandCode) || (pc[2 * u + 1] < kSpCandCode);
+        if (q < np && need) {
+          const double2 vx = __ldcs(&x2[q]), vy = __ldcs(&y2[q]);
+          px[2 * u] = vx.x; px[2 * u + 1] = vx.y;
+          py[2 * u] = vy.x; py[2 * u + 1] = vy.y;
+        } else {
+          px[2 * u] = px[2 * u + 1] = py[2 * u] = py[2 * u + 1] = 0.0;
+          pc[2 * u] = pc[2 * u + 1] = kSpNoCode;
+        }
+      }
+      check8(px, py, pc, cnt);
+    }
+    if ((n & 1) && tid == nth - 1) {
+      double px[8] = {xs[n - 1]}, py[8] = {ys[n - 1]};
+      uint32_t pc[8] = {codes[n - 1]};
+      check8(px, py, pc, 1);
+    }
+  } else {
+    for (uint32_t i0 = tid * 8; i0 < n; i0 += nth * 8) {
+      double px[8], py[8];
+      uint32_t pc[8];
+      const int cnt = (int)min(8u, n - i0);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const bool v = u < cnt;
+        pc[u] = v ? codes[i0 + u] : kSpNoCode;
+        px[u] = (v && pc[u] < kSpCandCode) ? xs[i0 + u] : 0.0;
+        py[u] = (v && pc[u] < kSpCandCode) ? ys[i0 + u] : 0.0;
+      }
+      check8(px, py, pc, cnt);
+    }
+  }
+  if (bad) {
+    atomicAdd(&st->verify_fail, bad);
+    atomicOr(&st->fail, kSpFailVerify);
+  }
+}
+
+// Stable compaction of the walk array by its keep flags (stable_compact,
+// discard.hpp:128-145), carrying bucket ids; n from / to the state.
+__global__ void __launch_bounds__(kBlock) k_sp_compact(
+    const double* __restrict__ in_x, const double* __restrict__ in_y,
+    const uint32_t* __restrict__ in_i, const uint32_t* __restrict__ in_b,
+    const uint8_t* __restrict__ flags, SpState* __restrict__ st, double* __restrict__ out_x,
+    double* __restrict__ out_y, uint32_t* __restrict__ out_i, uint32_t* __restrict__ out_b,
+    uint64_t* __restrict__ status, Counters* __restrict__ ctr) {
+  __shared__ uint32_t s_tile, s_warp[kWarps], s_excl;
+  if (st->fail) return;
+  const uint32_t n = st->n_w;
+  if (threadIdx.x == 0) s_tile = atomicAdd(&ctr->tile_ticket, 1u);
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const uint32_t base = tile * kCompactTile;
+  if (base >= n) return;
+  const uint32_t first = base + threadIdx.x * kCompactItems;
+  bool keep[kCompactItems];
+  uint32_t cnt = 0;
+#pragma unroll
+  for (int k = 0; k < kCompactItems; ++k) {
+    const uint32_t i = first + k;
+    keep[k] = i < n && flags[i] != 0;
+    cnt += keep[k];
+  }
+  uint32_t total;
+  const uint32_t texcl = block_exclusive_scan(cnt, s_warp, &total);
+  if (threadIdx.x < 32) {
+    const uint64_t e = lookback_exclusive(status, tile, total);
+    if (threadIdx.x == 0) {
+      s_excl = (uint32_t)e;
+      if (base + kCompactTile >= n) st->n_r = (uint32_t)(e + total);
+    }
+  }
+  __syncthreads();
+  uint32_t o = s_excl + texcl;
+#pragma unroll
+  for (int k = 0; k < kCompactItems; ++k) {
+    if (keep[k]) {
+      const uint32_t i = first + k;
+      out_x[o] = in_x[i];
+      out_y[o] = in_y[i];
+      out_i[o] = in_i[i];
+      out_b[o] = in_b[i];
+      ++o;
+    }
+  }
+}
+
+}  // namespace gscan

@@ -195,6 +195,12 @@ class Engine:
         self._lib.gscan_last_graham_info(self._h, C.byref(path), C.byref(fails))
         return path.value, fails.value
 
+    def sparse_info(self) -> tuple[int, int, int]:
+        """(used, fail_bits, n_walked) of the last call's sparse round-2 path."""
+        u, f, w = C.c_uint32(), C.c_uint32(), C.c_uint32()
+        self._lib.gscan_last_sparse_info(self._h, C.byref(u), C.byref(f), C.byref(w))
+        return u.value, f.value, w.value
+
     def launch_count(self) -> int:
         return int(self._lib.gscan_last_launch_count(self._h))
 
