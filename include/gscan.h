@@ -173,12 +173,15 @@ enum {
     GSCAN_DEBUG_FORCE_FALLBACK = 1u << 3,   /* always finish with the sequential kernel */
     GSCAN_DEBUG_FORCE_PREFIX = 1u << 4,     /* Graham candidate via prefix scan of states */
     GSCAN_DEBUG_FULL_SORT = 1u << 5,        /* skip the sparse round-2 path: sort every survivor */
-    GSCAN_DEBUG_SPARSE_DROP = 1u << 6       /* sparse path walks no candidates: its verification
+    GSCAN_DEBUG_SPARSE_DROP = 1u << 6,      /* sparse path walks no candidates: its verification
                                                must reject the result and the call falls back */
+    GSCAN_DEBUG_SPARSE_VERIFY = 1u << 7     /* sparse path: always run the verification pass,
+                                               even when the error-bound certificate holds */
 };
 int gscan_set_debug(gscan_handle* h, uint32_t flags);
 /* path: 0 = sequential kernel only (tiny input), 1 = chain scan + certificate,
- * 2 = junctions + certificate, 3 = prefix-scanned states + certificate;
+ * 2 = junctions + certificate, 3 = prefix-scanned states + certificate,
+ * 8 = tree of thread-sequential chain scans + certificate (pop-heavy buffers);
  * bit 4 set = certificate failed or fallback forced. */
 int gscan_last_graham_info(const gscan_handle* h, uint32_t* path, uint32_t* certificate_failures);
 

@@ -31,6 +31,7 @@ DEBUG_FORCE_FALLBACK = 1 << 3
 DEBUG_FORCE_PREFIX = 1 << 4
 DEBUG_FULL_SORT = 1 << 5
 DEBUG_SPARSE_DROP = 1 << 6
+DEBUG_SPARSE_VERIFY = 1 << 7
 
 
 class NativeUnavailable(RuntimeError):

@@ -23,6 +23,7 @@
 #include "kernels.cuh"
 #include "graham.cuh"
 #include "sparse.cuh"
+#include "graham_tree.cuh"
 
 using namespace gscan;
 
@@ -97,6 +98,7 @@ struct gscan_handle {
   uint32_t *sp_gcount = nullptr, *sp_ccount = nullptr, *sp_hcount = nullptr;  // per-CTA emissions
   uint64_t* sp_dup2 = nullptr;   // partitioned hash list (n)
   bool sp_debug = false, sp_no_dup = false;
+  uint32_t sp_cert = 0;
   uint16_t* sp_codes = nullptr;  // per-point bucket code (n)
   uint32_t *sp_hist_part = nullptr, *sp_phi_part = nullptr, *sp_part_off = nullptr;
   SpD2* sp_d2 = nullptr;
@@ -109,9 +111,12 @@ struct gscan_handle {
   SpState* sp_st = nullptr;
   SpState* h_sp = nullptr;  // pinned mirror
   // n-sized
-  uint32_t *sp_eb = nullptr, *sp_Wb = nullptr, *sp_Ws = nullptr, *sp_Rb = nullptr;
+  uint32_t *sp_eb = nullptr, *sp_Wb = nullptr, *sp_Ws = nullptr, *sp_Rb = nullptr, *sp_Rs = nullptr;
   uint64_t* sp_dup = nullptr;  // per-CTA hash lists (n)
   uint32_t sp_used = 0, sp_fail = 0, sp_walked = 0, sp_calls = 0, sp_fallbacks = 0;
+  // Graham tree strategy pool (graham_tree.cuh)
+  uint32_t* gt_pool = nullptr;
+  uint64_t gt_cap = 0;
 };
 
 namespace {
@@ -149,8 +154,9 @@ void free_buffers(gscan_handle* h) {
   dfree(h->g_parent); dfree(h->g_btop); dfree(h->g_jk); dfree(h->g_je); dfree(h->g_jmin);
   dfree(h->g_keep); dfree(h->g_misc);
   dfree(h->g_stA); dfree(h->g_stB); dfree(h->g_lenA); dfree(h->g_lenB); dfree(h->g_scr);
-  dfree(h->sp_eb); dfree(h->sp_Wb); dfree(h->sp_Ws); dfree(h->sp_Rb); dfree(h->sp_dup);
-  dfree(h->sp_codes); dfree(h->sp_dup2);
+  dfree(h->sp_eb); dfree(h->sp_Wb); dfree(h->sp_Ws); dfree(h->sp_Rb); dfree(h->sp_Rs); dfree(h->sp_dup);
+  dfree(h->sp_codes); dfree(h->sp_dup2); dfree(h->gt_pool);
+  h->gt_cap = 0;
   h->g_st_cap = 0;
   h->g_len_cap = 0;
   h->cap = 0;
@@ -215,6 +221,7 @@ int reserve(gscan_handle* h, uint64_t n) {
   CU(cudaMalloc(&h->sp_Wb, m * 4));
   CU(cudaMalloc(&h->sp_Ws, m * 4));
   CU(cudaMalloc(&h->sp_Rb, m * 4));
+  CU(cudaMalloc(&h->sp_Rs, m * 4));
   CU(cudaMalloc(&h->sp_dup, (m + 4096) * 8));
   CU(cudaMalloc(&h->sp_dup2, (m + 4096) * 8));
   CU(cudaMalloc(&h->sp_codes, (m + 1) * sizeof(uint16_t)));
@@ -558,6 +565,102 @@ int graham_prefix(gscan_handle* h, const double* Rx, const double* Ry, const uin
   return GSCAN_OK;
 }
 
+// Tree strategy (graham_tree.cuh) for pop-heavy buffers. *done = false when
+// the local chains do not shrink (convex position): the caller then takes the
+// junction / prefix / sequential strategies.
+int graham_tree(gscan_handle* h, const double* Rx, const double* Ry, const uint32_t* Ri,
+                uint32_t N, bool* done) {
+  *done = false;
+  constexpr int kMaxLevels = 16;
+  const uint64_t need = (uint64_t)N * 6 + 4096 * kMaxLevels;
+  if (need > h->gt_cap) {
+    dfree(h->gt_pool);
+    CU(cudaMalloc(&h->gt_pool, need * 4));
+    h->gt_cap = need;
+  }
+  uint32_t* pool = h->gt_pool;
+  uint64_t used = 0;
+  auto take = [&](uint64_t cnt) { uint32_t* p = pool + used; used += (cnt + 31) & ~31ull; return p; };
+  uint32_t* parent = take(N);
+  uint32_t* tmp = take(N);
+  uint32_t* fstack = take(kTreeTop + 32);
+  struct Level { const uint32_t* Q; uint32_t nq, nch; uint32_t* off; uint32_t* bt; uint32_t* up; };
+  Level L[kMaxLevels + 1];
+  L[0].Q = nullptr;
+  L[0].nq = N;
+  L[0].up = nullptr;
+  int K = 0;
+  while (true) {
+    Level& lv = L[K];
+    lv.nch = (lv.nq + kTreeChunk - 1) / kTreeChunk;
+    if (used + (uint64_t)lv.nch * kTreeChunk * 3 + 3 * lv.nch + 64 > h->gt_cap) return GSCAN_OK;
+    uint32_t* chain_q = take((uint64_t)lv.nch * kTreeChunk);
+    uint32_t* len = take(lv.nch + 1);
+    lv.off = take(lv.nch + 2);
+    lv.bt = take(lv.nch + 2);
+    {
+      Launch Lk(h, "k_gr_local");
+      k_gr_local<<<(lv.nch + kTreeCta - 1) / kTreeCta, kTreeCta, kTreeSmem, h->stream>>>(
+          lv.Q, lv.nq, Rx, Ry, chain_q, len);
+    }
+    TRY(scan_u32(h, len, lv.nch, lv.off));
+    uint32_t total;
+    TRY(read_u32(h, lv.off + lv.nch, &total));
+    if (K == 0 && total * 5 > (uint64_t)N * 3) return GSCAN_OK;  // not pop-heavy
+    if (K + 1 > kMaxLevels || total * 5 > (uint64_t)lv.nq * 4) return GSCAN_OK;
+    Level& nx = L[K + 1];
+    uint32_t* Qn = take(total);
+    nx.up = take(total);
+    nx.Q = Qn;
+    nx.nq = total;
+    {
+      Launch Lk(h, "k_gr_gather");
+      k_gr_gather<<<(lv.nch + 7) / 8, 8 * kTreeChunk, 0, h->stream>>>(lv.Q, chain_q, len, lv.off,
+                                                                      lv.nch, Qn, nx.up);
+    }
+    ++K;
+    if (total <= kTreeTop) break;
+  }
+  uint32_t* fail_d = h->g_misc;
+  uint32_t* len_d = h->g_misc + 1;
+  CU(cudaMemsetAsync(h->g_misc, 0, 16, h->stream));
+  {
+    Launch Lk(h, "k_gr_top");
+    k_gr_top<<<1, 128, 0, h->stream>>>(L[K].Q, L[K].up, L[K - 1].off + L[K - 1].nch,
+                                       L[K - 1].nch, Rx, Ry, parent, L[K - 1].bt, len_d, fstack);
+  }
+  for (int j = K - 1; j >= 1; --j) {
+    Launch Lk(h, "k_gr_down");
+    k_gr_down<<<(L[j - 1].nch + kTreeCta - 1) / kTreeCta, kTreeCta, kTreeSmem, h->stream>>>(
+        L[j].Q, L[j - 1].off, L[j - 1].nch, L[j].bt, Rx, Ry, parent, L[j - 1].bt);
+    CU(cudaMemcpyAsync(L[j - 1].bt + L[j - 1].nch, L[j].bt + L[j].nch, 4, cudaMemcpyDeviceToDevice,
+                       h->stream));
+  }
+  if (h->debug & GSCAN_DEBUG_CORRUPT_CANDIDATE) {
+    // drop the candidate's last boundary state: the certificate must reject it
+    CU(cudaMemcpyAsync(L[0].bt + L[0].nch, L[0].bt + L[0].nch - 1, 4, cudaMemcpyDeviceToDevice,
+                       h->stream));
+  }
+  {
+    Launch Lk(h, "k_gr_certify");
+    k_gr_certify<<<(L[0].nch + kTreeCta - 1) / kTreeCta, kTreeCta, kTreeSmem, h->stream>>>(
+        N, Rx, Ry, parent, L[0].bt, fail_d);
+  }
+  uint32_t fails;
+  TRY(read_u32(h, fail_d, &fails));
+  h->graham_fails = fails;
+  h->graham_path = 8;
+  if (fails || (h->debug & GSCAN_DEBUG_FORCE_FALLBACK)) return graham_seq_fallback(h, Rx, Ry, Ri);
+  {
+    Launch Lk(h, "k_gr_emit");
+    k_gr_emit<<<1, 1024, 0, h->stream>>>(L[0].bt + L[0].nch, parent, fstack, len_d, Ri, tmp,
+                                         h->d_out, h->ctr);
+  }
+  CU(cudaGetLastError());
+  *done = true;
+  return GSCAN_OK;
+}
+
 int stage_graham(gscan_handle* h, const double* Rx, const double* Ry, const uint32_t* Ri,
                  uint32_t N) {
   uint32_t* fail_d = h->g_misc;
@@ -569,6 +672,13 @@ int stage_graham(gscan_handle* h, const double* Rx, const double* Ry, const uint
     TRY(graham_seq_fallback(h, Rx, Ry, Ri));
     h->graham_path = 0;
     return GSCAN_OK;
+  }
+  const bool forced = h->debug & (GSCAN_DEBUG_FORCE_JUNCTION | GSCAN_DEBUG_FORCE_SEQUENTIAL |
+                                  GSCAN_DEBUG_FORCE_PREFIX);
+  if (!forced) {
+    bool done = false;
+    TRY(graham_tree(h, Rx, Ry, Ri, N, &done));
+    if (done || (h->graham_path & 8)) return GSCAN_OK;
   }
   const uint32_t nch = (N + kChunk - 1) / kChunk;
   {
@@ -677,6 +787,19 @@ constexpr uint64_t kSparseMinN = 1u << 16;
 bool sparse_eligible(const gscan_handle* h, uint64_t n, const gscan_config& cfg) {
   return n >= kSparseMinN && cfg.enable_round1 && cfg.enable_round2 && cfg.chunked &&
          !(h->debug & GSCAN_DEBUG_FULL_SORT);
+}
+
+double __longlong_as_double_host(uint64_t u) {
+  double d;
+  memcpy(&d, &u, 8);
+  return d;
+}
+float unord_host(uint32_t u) {
+  if (u == 0 || u == 0xffffffffu) return 0.f;
+  const uint32_t b = (u & 0x80000000u) ? (u & 0x7fffffffu) : ~u;
+  float f;
+  memcpy(&f, &b, 4);
+  return f;
 }
 
 int sparse_init(gscan_handle* h) {
@@ -895,13 +1018,21 @@ int run_sparse(gscan_handle* h, const double* xs, const double* ys, uint32_t n,
     const uint64_t tiles = (uint64_t)n / kCompactTile + 2;
     TRY(reset_lookback(h, tiles));
     Launch L(h, "k_sp_compact");
-    k_sp_compact<<<(uint32_t)tiles, kBlock, 0, s>>>(h->C_x, h->C_y, h->C_i, h->sp_Wb, h->flags,
-                                                    h->sp_st, h->A_x, h->A_y, h->A_i, h->sp_Rb,
-                                                    h->status, h->ctr);
+    k_sp_compact<<<(uint32_t)tiles, kBlock, 0, s>>>(h->C_x, h->C_y, h->C_i, h->sp_Wb, h->sp_Ws,
+                                                    h->flags, h->sp_st, h->A_x, h->A_y, h->A_i,
+                                                    h->sp_Rb, h->sp_Rs, h->status, h->ctr);
   }
   {
     Launch L(h, "k_sp_rlo");
     k_sp_rlo<<<h->sm_count * 8, kBlock, 0, s>>>(h->sp_Rb, h->sp_st, h->sp_rlo);
+  }
+  {
+    Launch L(h, "k_sp_cert_stats");
+    k_sp_cert_stats<<<h->sm_count, 256, 0, s>>>(h->A_x, h->A_y, h->sp_Rs, h->sp_st);
+  }
+  {
+    Launch L(h, "k_sp_cert_decide");
+    k_sp_cert_decide<<<1, 32, 0, s>>>(h->sp_st, drop || (h->debug & GSCAN_DEBUG_SPARSE_VERIFY));
   }
   {
     Launch L(h, "k_sp_verify");
@@ -919,13 +1050,15 @@ int run_sparse(gscan_handle* h, const double* xs, const double* ys, uint32_t n,
   if (h->sp_debug) {
     fprintf(stderr,
             "[sparse] fail=%#x m=%u M=%u b_l=%u l=%u/%u l_idx=%u ties=%u step=%u,%u slices=%u+%u "
-            "n_gb=%u n_g=%u max_g=%u n_c=%u n_w=%u n_r=%u dups=%u vfail=%u why=%u bigc=%u\n",
+            "n_gb=%u n_g=%u max_g=%u n_c=%u n_w=%u n_r=%u dups=%u vfail=%u why=%u bigc=%u cert=%u kmax=%u rho=%.3g phi=[%.4f,%.4f]\n",
             sp.fail, sp.m, sp.M, sp.b_l, sp.l, sp.l_check, sp.l_idx, sp.ties, sp.step_r, sp.step_l,
             sp.n_right, sp.n_left, sp.n_gb, sp.n_g, sp.max_g, sp.n_c, sp.n_w, sp.n_r, sp.dups,
-            sp.verify_fail, sp.why, sp.n_bigc);
+            sp.verify_fail, sp.why, sp.n_bigc, sp.cert, sp.k_max, sqrt(__longlong_as_double_host(sp.rho2_bits)),
+            unord_host(sp.phi_lo), unord_host(sp.phi_hi));
   }
   h->sp_fail = sp.fail;
   h->sp_walked = sp.n_w;
+  h->sp_cert = sp.cert;
   if (sp.fail) {
     ++h->sp_fallbacks;
     return GSCAN_OK;
@@ -1086,6 +1219,9 @@ int gscan_create(int device, gscan_handle** out) {
                             (int)(kSpDupSlots * 8)));
     CU(cudaFuncSetAttribute(k_sp_dup_part, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)kSpDupPartSmem));
+    CU(cudaFuncSetAttribute(k_gr_local, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTreeSmem));
+    CU(cudaFuncSetAttribute(k_gr_down, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTreeSmem));
+    CU(cudaFuncSetAttribute(k_gr_certify, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTreeSmem));
     h->sp_grid = h->sm_count;
     return GSCAN_OK;
   };

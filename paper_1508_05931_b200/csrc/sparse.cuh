@@ -101,7 +101,14 @@ struct SpState {
   uint32_t why;        // first internal-failure site (debug)
   uint32_t n_bigc;     // candidate buckets sorted by the CTA sorter
   uint32_t max_g;      // largest gathered bucket
-  uint32_t pad[3];
+  uint32_t need_verify;  // 1: the error-bound certificate did not hold -> run F6
+  uint32_t k_max;      // most kept points in one slice
+  uint32_t phi_lo, phi_hi;  // range of phi over bucketed survivors (ordered floats)
+  uint64_t rho2_bits;  // min |v|^2 over kept slice points (bits; non-negative double)
+  double r02;          // (1e-3 * bounding-box diagonal)^2: closer points are always walked
+  double dmax2;        // bounding-box diagonal^2
+  uint32_t cert;       // 1: certificate holds (F6 skipped)
+  uint32_t pad2;
 };
 
 // ---------------------------------------------------------------------------
@@ -126,12 +133,15 @@ __device__ __forceinline__ uint64_t angle_key(double dx, double dy) {
   return (a == 0.0) ? 0ull : dbits(a);
 }
 
-// 1/d to ~1e-13 relative: hardware approximation + one Newton step. Used only
-// where a guard band or the exact verification absorbs the error.
+// 1/d to a few ulps: hardware approximation + two Newton steps (the error
+// squares per step). Used only where a guard band, the certificate's e_phi
+// term or the exact verification absorbs the error.
 __device__ __forceinline__ double sp_rcp(double d) {
   double r;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
-  const double e = __fma_rn(-d, r, 1.0);
+  double e = __fma_rn(-d, r, 1.0);
+  r = __fma_rn(r, e, r);
+  e = __fma_rn(-d, r, 1.0);
   return __fma_rn(r, e, r);
 }
 
@@ -206,6 +216,19 @@ __device__ __forceinline__ double sp_phi(double px, double py, double lx, double
   const double t = 1.0 - c * sp_rcp(den);                 // [0, 2], increasing with the angle
   const double p = sn >= 0.0 ? t : -t;
   return right ? p : -p;
+}
+
+// Raw walk angle (pseudo-angle of P - P_l from u, CCW positive) and |P - P_l|^2.
+__device__ __forceinline__ double sp_phi_raw(double px, double py, double lx, double ly, double ux,
+                                             double uy, double* v2) {
+  const double vx = __dsub_rn(px, lx), vy = __dsub_rn(py, ly);
+  *v2 = __fma_rn(vx, vx, __dmul_rn(vy, vy));
+  const double c = __fma_rn(ux, vx, __dmul_rn(uy, vy));
+  const double sn = __fma_rn(ux, vy, -__dmul_rn(uy, vx));
+  const double den = fabs(c) + fabs(sn);
+  if (!(den > 1e-290)) return 0.0;
+  const double t = 1.0 - c * sp_rcp(den);
+  return sn >= 0.0 ? t : -t;
 }
 
 // Streaming helper: visits every point i of [0, n) once across the grid,
@@ -587,6 +610,14 @@ __global__ void k_sp_plan_bl(const ExtResult* __restrict__ ext, const double* __
   st->M = m + 1;
   if (st->fail) return;
   st->b_l = sp_bucket(__dsub_rn(st->lx, ext->ax), __dsub_rn(st->ly, ext->ay), cdf, th);
+  // bounding box of the input: qx[0] = min x, qy[1] = min y, qx[2] = max x, qy[3] = max y
+  const double wx = ext->qx[2] - ext->qx[0], wy = ext->qy[3] - ext->qy[1];
+  const double d2 = (wx * wx + wy * wy) * (1.0 + 1e-9);
+  st->dmax2 = d2;
+  st->r02 = 1e-6 * d2;
+  st->phi_lo = 0xffffffffu;
+  st->phi_hi = 0u;
+  st->rho2_bits = 0x7fefffffffffffffull;
 }
 
 // (c) P_l's exact position: the points of its bucket ordered before it by the
@@ -708,7 +739,9 @@ __global__ void __launch_bounds__(kSpThreads, 1) k_sp_phi(
   const double lx = st->lx, ly = st->ly;
   const double ux = __dsub_rn(ext->ax, lx), uy = __dsub_rn(ext->ay, ly);
   const uint32_t b_l = st->b_l;
+  const double r02 = st->r02;
   const size_t base = (size_t)blockIdx.x * cap;
+  double plo = 3.0, phi_ = -3.0;
   __syncthreads();
   sp_stream_coded<kVec, 4>(xs, ys, codes, n, [&](double x, double y, uint32_t b, uint32_t i) {
     const bool surv = b != kSpNoCode;
@@ -717,11 +750,14 @@ __global__ void __launch_bounds__(kSpThreads, 1) k_sp_phi(
     if (surv) {
       h = coord_hash64(x, y);
       atomicAdd(&s_part[(uint32_t)(h >> (64 - kSpPartBits))], 1u);
+      double v2;
+      const double raw = sp_phi_raw(x, y, lx, ly, ux, uy, &v2);
+      plo = fmin(plo, raw);
+      phi_ = fmax(phi_, raw);
       if (sp_gathered(s_g, b)) {
         emit = true;
-      } else {
-        const double ph = sp_phi(x, y, lx, ly, ux, uy, b < b_l);
-        atomicMax(&s_phi[b], ord_f(__double2float_rd(ph)));
+      } else if (v2 >= r02) {  // points within r0 of P_l never raise a maximum (certificate)
+        atomicMax(&s_phi[b], ord_f(__double2float_rd(b < b_l ? raw : -raw)));
       }
     }
     const uint32_t jh = warp_claim(&s_nh, surv);
@@ -738,6 +774,15 @@ __global__ void __launch_bounds__(kSpThreads, 1) k_sp_phi(
     g_count[blockIdx.x] = s_ng;
     h_count[blockIdx.x] = s_nh;
     atomicAdd(&st->n_g, s_ng);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    plo = fmin(plo, __shfl_xor_sync(0xffffffffu, plo, o));
+    phi_ = fmax(phi_, __shfl_xor_sync(0xffffffffu, phi_, o));
+  }
+  if ((threadIdx.x & 31) == 0 && plo <= phi_) {
+    atomicMin(&st->phi_lo, ord_f(__double2float_rd(plo)));
+    atomicMax(&st->phi_hi, ord_f(__double2float_ru(phi_)));
   }
 }
 
@@ -1043,7 +1088,11 @@ __global__ void __launch_bounds__(256) k_sp_slices(
   if (sp.right) { h0 = sp.seed; h1 = min(sp.hi, bstart[bs + 1]); }
   else { h0 = max(sp.lo, 1 + bstart[bs]); h1 = sp.seed; }
   double hm = -1e300;
-  for (uint32_t p = h0 + lane; p <= h1; p += 32) hm = fmax(hm, sp_phi(A_x[p], A_y[p], lx, ly, ux, uy, sp.right));
+  for (uint32_t p = h0 + lane; p <= h1; p += 32) {
+    double v2;
+    const double raw = sp_phi_raw(A_x[p], A_y[p], lx, ly, ux, uy, &v2);
+    if (v2 >= st.r02) hm = fmax(hm, sp.right ? raw : -raw);
+  }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) hm = fmax(hm, __shfl_xor_sync(0xffffffffu, hm, o));
   uint32_t run = ord_f(__double2float_rd(hm));
@@ -1111,12 +1160,16 @@ __global__ void __launch_bounds__(kSpThreads, 1) k_sp_cand(
   const double lx = st->lx, ly = st->ly;
   const double ux = __dsub_rn(ext->ax, lx), uy = __dsub_rn(ext->ay, ly);
   const uint32_t b_l = st->b_l;
+  const double r02 = st->r02;
   const size_t base = (size_t)blockIdx.x * cap;
   __syncthreads();
   sp_stream_coded<kVec, 4>(xs, ys, codes, n, [&](double x, double y, uint32_t b, uint32_t i) {
     bool emit = false;
-    if (b != kSpNoCode && !sp_gathered(s_g, b))
-      emit = sp_is_candidate(sp_phi(x, y, lx, ly, ux, uy, b < b_l), s_pm[b], drop);
+    if (b != kSpNoCode && !sp_gathered(s_g, b)) {
+      double v2;
+      const double raw = sp_phi_raw(x, y, lx, ly, ux, uy, &v2);
+      emit = (v2 < r02) || sp_is_candidate(b < b_l ? raw : -raw, s_pm[b], drop);
+    }
     const uint32_t j = warp_claim(&s_nc, emit);
     if (emit) {
       c_idx[base + j] = i;
@@ -1422,6 +1475,82 @@ __global__ void k_sp_rlo(const uint32_t* __restrict__ R_b, const SpState* __rest
 }
 
 // ===========================================================================
+// Error-bound certificate: when it holds, every survivor that was not walked
+// is PROVABLY discarded by the reference walk, and F6 is skipped.
+// Setting (right region; left mirrored): p not walked means phi(p) <
+// prefmax(b) - kSpTol, where prefmax(b) <= phi(q*) for a point q* earlier in
+// p's slice with |q* - P_l| >= r0 (F3 / k_sp_slices exclude closer points,
+// F4 walks them). alpha = exact angle of P - P_l. The reference's orient() is
+// off by at most 4.3 eps |v(t)| |q - t| (two rounded differences, two
+// products, one difference), so one decision moves the walk state's alpha
+// backwards by at most asin(4.3 eps (1 + |v(t)| / |v(q)|)): once when q* is
+// decided and once per later state change (<= K_max kept points per slice);
+// p is discarded once alpha(state) - alpha(p) exceeds the same bound for p.
+// dphi/dalpha <= 1, so a phi gap bounds the alpha gap. Therefore
+//   kSpTol > K_max * asin(4.3 eps (1 + D / rho)) + 2 asin(4.3 eps (1 + D / r0)) + 2 e_phi
+// (D: bounding-box diagonal, rho: closest kept slice point to P_l, e_phi: phi
+// evaluation error) proves every skipped point discarded, provided all angle
+// gaps stay below pi - 1e-3 (checked from the phi range).
+__global__ void __launch_bounds__(256) k_sp_cert_stats(const double* __restrict__ R_x,
+                                                       const double* __restrict__ R_y,
+                                                       const uint32_t* __restrict__ R_s,
+                                                       SpState* __restrict__ st) {
+  if (st->fail) return;
+  const uint32_t nr = st->n_r;
+  const double lx = st->lx, ly = st->ly;
+  uint64_t best = 0x7fefffffffffffffull;
+  uint32_t kmax = 0;
+  for (uint32_t j = 1 + blockIdx.x * blockDim.x + threadIdx.x; j < nr; j += gridDim.x * blockDim.x) {
+    const uint32_t sl = R_s[j];
+    if (sl == kNone) continue;  // anchor / P_l
+    const double vx = __dsub_rn(R_x[j], lx), vy = __dsub_rn(R_y[j], ly);
+    const uint64_t v2 = dbits(vx * vx + vy * vy);
+    best = v2 < best ? v2 : best;
+    if (R_s[j - 1] != sl) {  // first kept point of its slice: count the run
+      uint32_t k = j + 1;
+      while (k < nr && R_s[k] == sl) ++k;
+      kmax = max(kmax, k - j);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const uint64_t ob = __shfl_xor_sync(0xffffffffu, best, o);
+    best = ob < best ? ob : best;
+    kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin((unsigned long long*)&st->rho2_bits, (unsigned long long)best);
+    atomicMax(&st->k_max, kmax);
+  }
+}
+
+__device__ __forceinline__ double angle_of_pseudo(double ph) {
+  const double a = fabs(ph);
+  const double t = (a <= 1.0) ? atan2(a, 1.0 - a) : 3.141592653589793 - atan2(2.0 - a, a - 1.0);
+  return ph >= 0.0 ? t : -t;
+}
+
+__global__ void k_sp_cert_decide(SpState* __restrict__ st, bool force_verify) {
+  if (threadIdx.x != 0 || st->fail) return;
+  const double eps = 1.1102230246251565e-16;
+  const double D = sqrt(st->dmax2) * (1.0 + 1e-9);
+  const double r0 = sqrt(st->r02) * (1.0 - 1e-9);
+  const double rho = sqrt(bitsd(st->rho2_bits)) * (1.0 - 1e-9);
+  bool ok = !force_verify && rho > 0.0 && r0 > 0.0 && st->phi_lo != 0xffffffffu;
+  if (ok) {
+    const double x1 = 4.3 * eps * (1.0 + D / rho), x2 = 4.3 * eps * (1.0 + D / r0);
+    ok = x1 < 0.01 && x2 < 0.01;
+    const double m = (double)(st->k_max + 1) * x1 * 1.01 + 2.0 * x2 * 1.01 + 2.0 * 1e-11;
+    ok = ok && m < kSpTol;
+    const double w = angle_of_pseudo((double)unord_f(st->phi_hi) + 1e-9) -
+                     angle_of_pseudo((double)unord_f(st->phi_lo) - 1e-9);
+    ok = ok && w < 3.141592653589793 - 1e-3;
+  }
+  st->cert = ok ? 1u : 0u;
+  st->need_verify = ok ? 0u : 1u;
+}
+
+// ===========================================================================
 // F6: every survivor that was not walked must be discarded by the reference
 // walk. Its walk state is the last kept point before it in its slice: the
 // last kept point before its bucket or a kept point of its own bucket
@@ -1436,7 +1565,7 @@ __global__ void __launch_bounds__(kSpThreads, 1) k_sp_verify(
     const double* __restrict__ R_y, SpState* __restrict__ st) {
   extern __shared__ uint32_t s_rlo[];  // kSpBuckets + 1
   __shared__ uint32_t s_g[kSpBuckets / 32];
-  if (st->fail) return;
+  if (st->fail || !st->need_verify) return;
   for (uint32_t b = threadIdx.x; b <= kSpBuckets; b += blockDim.x) s_rlo[b] = rlo[b];
   for (uint32_t w = threadIdx.x; w < kSpBuckets / 32; w += blockDim.x) s_g[w] = gbits[w];
   const double lx = st->lx, ly = st->ly;
@@ -1547,9 +1676,10 @@ __global__ void __launch_bounds__(kSpThreads, 1) k_sp_verify(
 __global__ void __launch_bounds__(kBlock) k_sp_compact(
     const double* __restrict__ in_x, const double* __restrict__ in_y,
     const uint32_t* __restrict__ in_i, const uint32_t* __restrict__ in_b,
-    const uint8_t* __restrict__ flags, SpState* __restrict__ st, double* __restrict__ out_x,
-    double* __restrict__ out_y, uint32_t* __restrict__ out_i, uint32_t* __restrict__ out_b,
-    uint64_t* __restrict__ status, Counters* __restrict__ ctr) {
+    const uint32_t* __restrict__ in_s, const uint8_t* __restrict__ flags, SpState* __restrict__ st,
+    double* __restrict__ out_x, double* __restrict__ out_y, uint32_t* __restrict__ out_i,
+    uint32_t* __restrict__ out_b, uint32_t* __restrict__ out_s, uint64_t* __restrict__ status,
+    Counters* __restrict__ ctr) {
   __shared__ uint32_t s_tile, s_warp[kWarps], s_excl;
   if (st->fail) return;
   const uint32_t n = st->n_w;
@@ -1586,6 +1716,7 @@ __global__ void __launch_bounds__(kBlock) k_sp_compact(
       out_y[o] = in_y[i];
       out_i[o] = in_i[i];
       out_b[o] = in_b[i];
+      out_s[o] = in_s[i];
       ++o;
     }
   }

@@ -55,6 +55,9 @@ def main():
     got, sg, _ = run(eng, xs, ys, N.DEBUG_SPARSE_DROP)
     used, fail, walked = eng.sparse_info()
     print(f"drop: same={np.array_equal(want, got)} used={used} fail={fail:#x}")
+    got, sg, _ = run(eng, xs, ys, N.DEBUG_SPARSE_VERIFY)
+    used, fail, walked = eng.sparse_info()
+    print(f"forced verify: same={np.array_equal(want, got)} used={used} fail={fail:#x}")
     eng.set_debug(0)
     eng.set_profiling(True)
     xs, ys = generate("square", n, 1)
