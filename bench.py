@@ -11,10 +11,11 @@ quoted on (configs[1]). Keys:
   e2e        same metric through the C-ABI host entry (gscan_hull_f64) with
              pinned host buffers: H2D of xs/ys + pipeline + D2H of the index
              list inside the timed region
-  roofline   the filter pass as the pipeline runs it (fused K2/K3,
-             k_filter_keys): algorithmic bytes 16 B/point read + 16 B/survivor
-             written (index, key, bucket rank), over its event-timed duration,
-             against MEASURED_PEAKS.json hbm_gbs
+  roofline   the filter pass as the pipeline runs it: on the default sparse
+             path k_sp_hist (round-1 quad test + angle-bucket histogram),
+             algorithmic bytes 16 B/point read + 2 B/point bucket code written;
+             on the full-sort path k_filter_keys (16 B/point + 16 B/survivor);
+             over its event-timed duration, against MEASURED_PEAKS.json hbm_gbs
   cpu_baseline  the unmodified reference (oracle/_ref) on this host, one full
              run of the same workload, timed by its own StageStats
 N > 1 runs the sharded pipeline (paper_1508_05931_b200/distributed.py) on the
@@ -61,49 +62,80 @@ def peaks() -> tuple[float, str]:
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled DURING the timed region: NVML
+    polled every ~2 ms from a thread (nvidia-smi -lms cannot resolve a
+    sub-second region); falls back to nvidia-smi when NVML is unavailable."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = {  # nvmlClocksEventReason* bits
+        "sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20,
+        "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80,
+    }
 
     def __init__(self, index: int):
         self.index = index
-        self.rows: list[list[str]] = []
-        self.proc = None
+        self.sm: list[float] = []
+        self.reasons: set[str] = set()
+        self.sm_max = None
+        self._run = False
+        self._thr = None
+        self._nvml = None
 
     def start(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
-            self.thread.start()
+            import pynvml as nv
+            nv.nvmlInit()
+            self._nvml = nv
+            self._h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            self.sm_max = float(nv.nvmlDeviceGetMaxClockInfo(self._h, nv.NVML_CLOCK_SM))
         except Exception:
-            self.proc = None
+            self._nvml = None
+        self._run = True
+        self._thr = threading.Thread(target=self._loop, daemon=True)
+        self._thr.start()
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.rows.append([c.strip() for c in line.split(",")])
+    def _sample(self):
+        nv = self._nvml
+        if nv is not None:
+            self.sm.append(float(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)))
+            try:
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+            except Exception:
+                r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self._h)
+            for name, bit in self.REASONS.items():
+                if r & bit:
+                    self.reasons.add(name)
+            return
+        out = subprocess.run(
+            ["nvidia-smi", f"--id={self.index}",
+             "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits"],
+            capture_output=True, text=True, timeout=5).stdout.strip().split(",")
+        if len(out) >= 6:
+            self.sm.append(float(out[0]))
+            self.sm_max = float(out[1])
+            for name, v in zip(["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+                                "sw_power_cap"], out[2:6]):
+                if v.strip().lower().startswith("active"):
+                    self.reasons.add(name)
+
+    def _loop(self):
+        while self._run:
+            try:
+                self._sample()
+            except Exception:
+                pass
+            time.sleep(0.002 if self._nvml is not None else 0.05)
 
     def stop(self) -> dict:
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=2)
-            except Exception:
-                self.proc.kill()
-        if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for r in self.rows for k in range(4)
-                          if len(r) > 4 + k and r[4 + k].lower().startswith("active")})
-        return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows)}
+        self._run = False
+        if self._thr:
+            self._thr.join(timeout=5)
+        if not self.sm:
+            return {"sm_mhz": None, "sm_max_mhz": self.sm_max, "reasons": ["unsampled"]}
+        return {"sm_mhz": float(np.median(self.sm)), "sm_max_mhz": self.sm_max,
+                "reasons": sorted(self.reasons), "samples": len(self.sm),
+                "source": "nvml" if self._nvml is not None else "nvidia-smi"}
 
 
 def hull_hash(idx: np.ndarray) -> str:
@@ -169,7 +201,7 @@ def run_reference(args, cfgname):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -218,7 +250,6 @@ def main():
         torch.cuda.synchronize()
 
     sampler = ClockSampler(local)
-    sampler.start()
     # ---- correctness of the benchmarked output (golden hash from the reference) ----
     k, st = step()
     parity = None
@@ -238,6 +269,7 @@ def main():
     # ---- device-resident timed region (clocks sampled from warm-up through it) ----
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
+    sampler.start()
     barrier()
     e0.record(stream)
     launches = 0
@@ -266,24 +298,28 @@ def main():
     eng.set_profiling(False)
     kernels = {k2: round(float(np.mean(v)) * (len(v) / reps), 4) for k2, v in kt.items()}
     peak, peak_src = peaks()
-    filt = kt.get("k_filter_keys", [])
+    fkern = "k_sp_hist" if "k_sp_hist" in kt else "k_filter_keys"
+    filt = kt.get(fkern, [])
     t_filter = float(np.mean(filt)) if filt else None
     n_local = hi - lo
     n1 = st.n_after_round1 if st is not None else None
     roofline = None
     if t_filter:
-        alg_bytes = 16 * n_local + 16 * (n1 if (world == 1 and n1) else int(0.664 * n_local))
+        if fkern == "k_sp_hist":  # 16 B/pt read (xs, ys) + 2 B/pt bucket code written
+            alg_bytes = 18 * n_local
+        else:
+            alg_bytes = 16 * n_local + 16 * (n1 if (world == 1 and n1) else int(0.664 * n_local))
         achieved = alg_bytes / (t_filter * 1e-3) / 1e9
         traffic = None
         tp = ROOT / "profiles" / "ncu_filter_traffic.json"
         if tp.exists():
             try:
-                traffic = json.loads(tp.read_text()).get(args.config)
+                traffic = json.loads(tp.read_text()).get(f"{fkern}:{args.config}")
             except Exception:
                 traffic = None
         roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                     "frac": round(achieved / peak, 4), "traffic": traffic,
-                    "kernel": "k_filter_keys", "kernel_ms": round(t_filter, 4),
+                    "kernel": fkern, "kernel_ms": round(t_filter, 4),
                     "algorithmic_bytes": alg_bytes, "peak_source": peak_src}
 
     # ---- e2e through the C-ABI host entry, pinned host buffers ----
@@ -326,7 +362,7 @@ def main():
                    "pipeline_config": "chunk_count=1024, both rounds, chunked"},
         "parity_vs_golden": parity,
         "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks,
-        "gpu_launches": launches, "kernels_ms": kernels,
+        "gpu_launches": launches, "kernels_ms": kernels, "sparse_path": eng.sparse_info()[0] == 1,
         "stats": {k2: getattr(st, k2) for k2 in ("n_after_round1", "n_after_round2", "hull_size")}
         if st is not None else None,
     }

@@ -1,14 +1,15 @@
 // K7/K8 tree strategy: graham_finalize (pipeline.hpp:57-67) for buffers where
-// most points are popped (round-2 output of squares and disks).
+// most points are popped (round-2 output of squares and disks), as ONE kernel
+// (one CTA, no host round trips).
 //
 // Warp-speculative scans advance 32 points per iteration only while nothing is
 // popped; on these buffers nearly every point pops, so here every scan is a
 // plain sequential stack scan run by ONE thread (~2 orient() per point), and
-// the parallelism comes from running many of them:
+// the parallelism comes from running many short ones:
 //
-//   up      level j: Q_j is cut into chunks of kTreeChunk; every chunk's local
-//           scan from an empty stack leaves a chain; the chains concatenated
-//           form Q_{j+1} (Q_0 = the buffer). Repeat until Q_K is small.
+//   up      level j: Q_j (R positions; Q_0 = the buffer) is cut into chunks of
+//           kTreeChunk; every chunk's scan from an empty stack leaves a chain;
+//           the chains concatenated form Q_{j+1}. Repeat until Q_K is small.
 //   top     one thread scans Q_K, recording the persistent stack (parent[p] =
 //           the element below p when p was pushed) and the top before every
 //           Q_{K-1} chunk.
@@ -18,184 +19,153 @@
 //   certify every buffer chunk replays ITS OWN points from the candidate state
 //           at its start and must end exactly in the candidate state at its
 //           end (top and every parent link of its surviving pushes).
+//   emit    the certified final state; if any chunk failed, the same CTA runs
+//           the exact sequential scan instead.
 //
 // The candidate rests on "scan(X ++ Y) = scan(scan(X) ++ scan_local(Y))",
 // which exact geometry guarantees; rounding can only make the certificate
-// fail (then the exact sequential kernel runs), never a wrong hull: by
-// induction over chunks, certified states are the sequential scan's states.
+// fail, never a wrong hull: by induction over chunks, certified states are the
+// sequential scan's states.
 #pragma once
 #include "graham.cuh"
 
 namespace gscan {
 
-constexpr int kTreeChunk = 32;   // short chunks: every scan is latency-bound (~200 cycles/step)
-constexpr int kTreeCta = 64;      // chunks (threads) per CTA
+constexpr int kTreeChunk = 32;      // points per chunk (each scan is ~200 cycles per step)
+constexpr int kTreeThreads = 256;   // one CTA; chunks are processed in waves of this many
 constexpr uint32_t kTreeTop = 128;  // largest top-level list for the single-thread scan
+constexpr int kTreeMaxLevels = 16;
+// shared memory: per thread a chunk's coordinates [k][t] and an index stack
+constexpr size_t kTreeSmem = (size_t)kTreeChunk * kTreeThreads * (8 + 8 + 4 + 1);
+constexpr size_t kTreeCtaSmem2 = (size_t)kTreeChunk * 64 * (8 + 8 + 4 + 1);
 
-// Chunk coordinates staged in shared memory, [point][thread] so that the
-// threads of a warp (each scanning its own chunk) hit distinct banks.
-constexpr size_t kTreeSmem = (size_t)kTreeChunk * kTreeCta * 16;
-
-__device__ __forceinline__ void stage_chunks(const uint32_t* __restrict__ Q, uint32_t nq,
-                                             uint32_t first_chunk, const double* __restrict__ R_x,
-                                             const double* __restrict__ R_y, double* sx,
-                                             double* sy) {
-  // element k of chunk t (t = 0..kTreeCta-1) -> sx[k * kTreeCta + t]
-  const uint32_t base = first_chunk * kTreeChunk;
-  for (uint32_t e = threadIdx.x; e < (uint32_t)kTreeChunk * kTreeCta; e += blockDim.x) {
-    const uint32_t g = base + e;  // coalesced over the CTA's consecutive chunks
-    if (g >= nq) break;
-    const uint32_t p = Q ? Q[g] : g;
-    const uint32_t t = e / kTreeChunk, k = e % kTreeChunk;
-    sx[k * kTreeCta + t] = R_x[p];
-    sy[k * kTreeCta + t] = R_y[p];
-  }
-}
-
-// Local chains of Q (R positions; nullptr = identity) in chunks of kTreeChunk.
-// out_q[c * kTreeChunk + k] = the Q index of the k-th chain element.
-__global__ void __launch_bounds__(kTreeCta) k_gr_local(const uint32_t* __restrict__ Q, uint32_t nq,
-                                                      const double* __restrict__ R_x,
-                                                      const double* __restrict__ R_y,
-                                                      uint32_t* __restrict__ out_q,
-                                                      uint32_t* __restrict__ out_len) {
-  extern __shared__ __align__(16) double tsm[];
-  double* sx = tsm;
-  double* sy = tsm + kTreeChunk * kTreeCta;
-  __shared__ uint8_t s_stk[kTreeChunk][kTreeCta];  // [depth][thread]: conflict-free
-  stage_chunks(Q, nq, blockIdx.x * kTreeCta, R_x, R_y, sx, sy);
-  __syncthreads();
-  const uint32_t c = blockIdx.x * kTreeCta + threadIdx.x;
-  const uint32_t lo = c * kTreeChunk;
-  if (lo >= nq) return;
-  const int cnt = (int)min((uint32_t)kTreeChunk, nq - lo);
-  const int t = threadIdx.x;
-  int top = 0;
-  double s1x = 0, s1y = 0, s2x = 0, s2y = 0;  // stack[top-1], stack[top-2]
-  for (int k = 0; k < cnt; ++k) {
-    const double px = sx[k * kTreeCta + t], py = sy[k * kTreeCta + t];
-    while (top >= 2 && !left_turn(s2x, s2y, s1x, s1y, px, py)) {
-      --top;
-      s1x = s2x; s1y = s2y;
-      if (top >= 2) {
-        const int q = s_stk[top - 2][t];
-        s2x = sx[q * kTreeCta + t]; s2y = sy[q * kTreeCta + t];
-      }
-    }
-    s_stk[top][t] = (uint8_t)k;
-    ++top;
-    s2x = s1x; s2y = s1y;
-    s1x = px; s1y = py;
-  }
-  for (int k = 0; k < top; ++k) out_q[(size_t)c * kTreeChunk + k] = lo + s_stk[k][t];
-  out_len[c] = top;
-}
-
-// Q_{j+1}[off[c] + k] = Q_j[chain element], up[off[c] + k] = its Q_j index.
-__global__ void k_gr_gather(const uint32_t* __restrict__ Q, const uint32_t* __restrict__ chain_q,
-                            const uint32_t* __restrict__ len, const uint32_t* __restrict__ off,
-                            uint32_t nchunks, uint32_t* __restrict__ Qn, uint32_t* __restrict__ up) {
-  const uint32_t c = blockIdx.x * (blockDim.x / kTreeChunk) + threadIdx.x / kTreeChunk;
-  const uint32_t k = threadIdx.x % kTreeChunk;
-  if (c >= nchunks || k >= len[c]) return;
-  const uint32_t qi = chain_q[(size_t)c * kTreeChunk + k];
-  Qn[off[c] + k] = Q ? Q[qi] : qi;
-  up[off[c] + k] = qi;
-}
-
-// Top: one thread scans Q_K (R positions; up = their Q_{K-1} indices),
-// recording parent[] and bt[b] = top before the first element of Q_{K-1}
-// chunk >= b, b = 0..nch (bt[nch] = final top). *len = final size.
-__global__ void k_gr_top(const uint32_t* __restrict__ QK, const uint32_t* __restrict__ up,
-                         const uint32_t* nk_dev, uint32_t nch, const double* __restrict__ R_x,
-                         const double* __restrict__ R_y, uint32_t* __restrict__ parent,
-                         uint32_t* __restrict__ bt, uint32_t* __restrict__ out_len,
-                         uint32_t* __restrict__ fstack) {
-  if (blockIdx.x != 0) return;
-  __shared__ uint32_t s_stk[kTreeTop];   // stack of Q_K indices
-  __shared__ double s_x[kTreeTop], s_y[kTreeTop];
-  __shared__ uint32_t s_p[kTreeTop], s_ch[kTreeTop];
-  const uint32_t nk = *nk_dev;
-  for (uint32_t k = threadIdx.x; k < nk; k += blockDim.x) {
-    const uint32_t p = QK[k];
-    s_p[k] = p;
-    s_ch[k] = up[k] / kTreeChunk;
-    s_x[k] = R_x[p];
-    s_y[k] = R_y[p];
-  }
-  __syncthreads();
-  if (threadIdx.x != 0) return;
-  int top = 0;
-  double s1x = 0, s1y = 0, s2x = 0, s2y = 0;
-  uint32_t next_b = 0;
-  for (uint32_t k = 0; k < nk; ++k) {
-    const uint32_t p = s_p[k];
-    const uint32_t ch = s_ch[k];
-    const uint32_t t = top ? s_p[s_stk[top - 1]] : kNone;
-    for (; next_b <= ch; ++next_b) bt[next_b] = t;
-    const double px = s_x[k], py = s_y[k];
-    while (top >= 2 && !left_turn(s2x, s2y, s1x, s1y, px, py)) {
-      --top;
-      s1x = s2x; s1y = s2y;
-      if (top >= 2) { const uint32_t q = s_stk[top - 2]; s2x = s_x[q]; s2y = s_y[q]; }
-    }
-    parent[p] = top ? s_p[s_stk[top - 1]] : kNone;
-    s_stk[top++] = k;
-    s2x = s1x; s2y = s1y;
-    s1x = px; s1y = py;
-  }
-  const uint32_t t = top ? s_p[s_stk[top - 1]] : kNone;
-  for (; next_b <= nch; ++next_b) bt[next_b] = t;
-  for (int k = 0; k < top; ++k) fstack[k] = s_p[s_stk[k]];
-  *out_len = top;
-}
-
-// One thread's stack scan of a run of points on top of a persistent state
-// (top `base`, parent[] links below it). The run's coordinates come from
-// shared memory (cx/cy at index k * kTreeCta + lane); own pushes are kept as
-// run indices in stk[depth * kTreeCta + lane]; elements of the persistent
-// part are loaded from global memory when pops reach them. pos(k) gives the
-// R position of run element k (for parent links and the result).
-struct PersistentTop {
-  uint32_t b1, b2;  // top two elements of the persistent part (kNone if absent)
+struct TreeLevel {
+  uint32_t* Q;    // R positions (nullptr: identity, level 0)
+  uint32_t* up;   // Q_{j-1} index of each element (level >= 1)
+  uint32_t* off;  // chain offsets of this level's chunks in Q_{j+1} (nch + 1)
+  uint32_t* bt;   // top before each chunk (nch + 1)
+  uint32_t nq, nch;
 };
 
-template <typename PosF, typename OnPush>
-__device__ __forceinline__ int persistent_scan(PosF&& pos, int cnt, const double* cx,
-                                               const double* cy, PersistentTop& pt,
-                                               const double* __restrict__ R_x,
-                                               const double* __restrict__ R_y,
-                                               const uint32_t* __restrict__ parent, uint16_t* stk,
-                                               OnPush&& on_push) {
+// Workspace carved from one device buffer by the host; the kernel checks every
+// level size against its capacity.
+struct TreeWork {
+  uint32_t* parent;  // N
+  uint32_t* tmp;     // N (stack of the top-level / fallback scan)
+  uint32_t* chainq;  // N: chain elements of the current level (Q index), chunk-strided
+  uint32_t* chainp;  // N: the same elements' R positions
+  uint32_t* len;     // ceil(N / kTreeChunk) + 1
+  uint32_t* fstack;  // kTreeTop
+  uint32_t* Qbuf[kTreeMaxLevels + 1];
+  uint32_t* upbuf[kTreeMaxLevels + 1];
+  uint32_t* offbuf[kTreeMaxLevels + 1];
+  uint32_t* btbuf[kTreeMaxLevels + 1];
+  uint32_t cap[kTreeMaxLevels + 1];  // element capacity of level j's Q / up
+};
+
+// CTA-wide exclusive scan of cnt uint32 (in place); returns the total.
+__device__ uint32_t tree_scan(uint32_t* a, uint32_t cnt, uint32_t* s_w, uint32_t* s_carry) {
+  if (threadIdx.x == 0) *s_carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nw = blockDim.x >> 5;
+  for (uint32_t base = 0; base < cnt; base += blockDim.x) {
+    const uint32_t i = base + threadIdx.x;
+    const uint32_t v = i < cnt ? a[i] : 0u;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) s_w[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+      uint32_t wv = lane < nw ? s_w[lane] : 0u;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, wv, o);
+        if (lane >= o) wv += y;
+      }
+      if (lane < nw) s_w[lane] = wv;
+    }
+    __syncthreads();
+    const uint32_t carry = *s_carry;
+    if (i < cnt) a[i] = carry + (warp ? s_w[warp - 1] : 0u) + x - v;
+    __syncthreads();
+    if (threadIdx.x == 0) *s_carry = carry + s_w[nw - 1];
+    __syncthreads();
+  }
+  return *s_carry;
+}
+
+// Stage up to kTreeChunk coordinates of run elements pos(0..cnt) into this
+// thread's slots [k][t] (8 independent loads in flight).
+template <int kStride, typename PosF>
+__device__ __forceinline__ void tree_stage(PosF&& pos, int cnt, const double* __restrict__ R_x,
+                                           const double* __restrict__ R_y, double* cx, double* cy,
+                                           uint32_t* cp) {
   const int t = threadIdx.x;
-  int top = 0;  // own pushes
-  double s1x = 0, s1y = 0, s2x = 0, s2y = 0;  // coordinates of the whole stack's top two
-  if (pt.b1 != kNone) { s1x = R_x[pt.b1]; s1y = R_y[pt.b1]; }
-  if (pt.b2 != kNone) { s2x = R_x[pt.b2]; s2y = R_y[pt.b2]; }
+  for (int k0 = 0; k0 < cnt; k0 += 8) {
+    uint32_t pp[8];
+    double vx[8], vy[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) pp[u] = (k0 + u < cnt) ? pos(k0 + u) : 0u;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      vx[u] = (k0 + u < cnt) ? R_x[pp[u]] : 0.0;
+      vy[u] = (k0 + u < cnt) ? R_y[pp[u]] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (k0 + u < cnt) {
+        cx[(k0 + u) * kStride + t] = vx[u];
+        cy[(k0 + u) * kStride + t] = vy[u];
+        if (cp) cp[(k0 + u) * kStride + t] = pp[u];
+      }
+  }
+}
+
+// One thread's stack scan of a staged run on top of a persistent state (top
+// two elements b1, b2; parent[] links below). Own pushes are kept as run
+// indices in stk[depth * kTreeThreads + t]; deeper persistent elements are
+// loaded from global memory when pops reach them. on_push(k, below_run_index
+// or -1 = b1) is called for every push. Returns the number of own pushes left.
+template <int kStride, typename OnPush>
+__device__ __forceinline__ int tree_scan_run(int cnt, const double* cx, const double* cy,
+                                             uint32_t& b1, uint32_t& b2,
+                                             const double* __restrict__ R_x,
+                                             const double* __restrict__ R_y,
+                                             const uint32_t* __restrict__ parent, uint8_t* stk,
+                                             OnPush&& on_push) {
+  const int t = threadIdx.x;
+  int top = 0;
+  double s1x = 0, s1y = 0, s2x = 0, s2y = 0;
+  if (b1 != kNone) { s1x = R_x[b1]; s1y = R_y[b1]; }
+  if (b2 != kNone) { s2x = R_x[b2]; s2y = R_y[b2]; }
   for (int k = 0; k < cnt; ++k) {
-    const double px = cx[k * kTreeCta + t], py = cy[k * kTreeCta + t];
+    const double px = cx[k * kStride + t], py = cy[k * kStride + t];
     while (true) {
-      // the whole stack (persistent part + own pushes) holds >= 2 elements
-      const bool has2 = (top >= 2) || (top == 1 && pt.b1 != kNone) ||
-                        (top == 0 && pt.b1 != kNone && pt.b2 != kNone);
+      const bool has2 = (top >= 2) || (top == 1 && b1 != kNone) ||
+                        (top == 0 && b1 != kNone && b2 != kNone);
       if (!has2 || left_turn(s2x, s2y, s1x, s1y, px, py)) break;
       if (top >= 1) {
         --top;
       } else {
-        pt.b1 = pt.b2;
-        pt.b2 = (pt.b1 != kNone) ? parent[pt.b1] : kNone;
+        b1 = b2;
+        b2 = (b1 != kNone) ? parent[b1] : kNone;
       }
       s1x = s2x; s1y = s2y;
       if (top >= 2) {
-        const int q = stk[(top - 2) * kTreeCta + t];
-        s2x = cx[q * kTreeCta + t]; s2y = cy[q * kTreeCta + t];
+        const int q = stk[(top - 2) * kStride + t];
+        s2x = cx[q * kStride + t]; s2y = cy[q * kStride + t];
       } else {
-        const uint32_t ns = (top == 1) ? pt.b1 : pt.b2;
+        const uint32_t ns = (top == 1) ? b1 : b2;
         if (ns != kNone) { s2x = R_x[ns]; s2y = R_y[ns]; }
       }
     }
-    on_push(k, top ? pos(stk[(top - 1) * kTreeCta + t]) : pt.b1);
-    stk[top * kTreeCta + t] = (uint16_t)k;
+    on_push(k, top ? (int)stk[(top - 1) * kStride + t] : -1);
+    stk[top * kStride + t] = (uint8_t)k;
     ++top;
     s2x = s1x; s2y = s1y;
     s1x = px; s1y = py;
@@ -203,114 +173,313 @@ __device__ __forceinline__ int persistent_scan(PosF&& pos, int cnt, const double
   return top;
 }
 
-// Down: for every Q_{j-1} chunk c' (thread), the state before it: the state
-// before the Q_j chunk c holding its chain's first element (offset off[c'])
-// scanned over Q_j[c * kTreeChunk, off[c']). Q_j holds R positions.
-__global__ void __launch_bounds__(kTreeCta) k_gr_down(const uint32_t* __restrict__ Qj,
-                                                     const uint32_t* __restrict__ off,
-                                                     uint32_t nch_lo,
-                                                     const uint32_t* __restrict__ bt_hi,
-                                                     const double* __restrict__ R_x,
-                                                     const double* __restrict__ R_y,
-                                                     uint32_t* __restrict__ parent,
-                                                     uint32_t* __restrict__ bt_lo) {
-  extern __shared__ __align__(16) double tsm[];
-  double* cx = tsm;
-  double* cy = tsm + kTreeChunk * kTreeCta;
-  __shared__ uint16_t s_stk[kTreeChunk * kTreeCta];
-  const uint32_t cp = blockIdx.x * kTreeCta + threadIdx.x;
-  const bool act = cp < nch_lo;
-  const uint32_t e = act ? off[cp] : 0;
-  const uint32_t c = e / kTreeChunk;
-  const int cnt = (int)(e - c * kTreeChunk);  // < kTreeChunk
-  // stage this thread's run (independent loads, unrolled)
-  for (int k0 = 0; k0 < cnt; k0 += 8) {
-    uint32_t pp[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) pp[u] = (k0 + u < cnt) ? Qj[c * kTreeChunk + k0 + u] : 0u;
-    double vx[8], vy[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      if (k0 + u < cnt) { vx[u] = R_x[pp[u]]; vy[u] = R_y[pp[u]]; }
-    }
-#pragma unroll
-    for (int u = 0; u < 8; ++u)
-      if (k0 + u < cnt) { cx[(k0 + u) * kTreeCta + threadIdx.x] = vx[u]; cy[(k0 + u) * kTreeCta + threadIdx.x] = vy[u]; }
-  }
-  if (!act) return;
-  PersistentTop pt;
-  pt.b1 = bt_hi[c];
-  pt.b2 = (pt.b1 != kNone) ? parent[pt.b1] : kNone;
-  auto pos = [&](int k) -> uint32_t { return Qj[c * kTreeChunk + k]; };
-  const int top = persistent_scan(pos, cnt, cx, cy, pt, R_x, R_y, parent, s_stk,
-                                  [&](int k, uint32_t below) { parent[pos(k)] = below; });
-  bt_lo[cp] = top ? pos(s_stk[(top - 1) * kTreeCta + threadIdx.x]) : pt.b1;
-}
+// ---------------------------------------------------------------------------
+// Level 0, many CTAs: chains of the buffer's chunks (thread per chunk).
+constexpr int kTreeCta = 64;
+constexpr size_t kTreeCtaSmem = (size_t)kTreeChunk * kTreeCta * (8 + 8 + 1);
 
-// Certificate (thread per buffer chunk): replay the chunk's own points from
-// the candidate state bt[c]; the end state must be exactly bt[c + 1] with
-// every surviving push linked as in parent[].
-__global__ void __launch_bounds__(kTreeCta) k_gr_certify(uint32_t n, const double* __restrict__ R_x,
-                                                        const double* __restrict__ R_y,
-                                                        const uint32_t* __restrict__ parent,
-                                                        const uint32_t* __restrict__ bt,
-                                                        uint32_t* __restrict__ fail) {
+__global__ void __launch_bounds__(kTreeCta) k_gr_local0(uint32_t N, const double* __restrict__ R_x,
+                                                       const double* __restrict__ R_y,
+                                                       TreeWork w) {
   extern __shared__ __align__(16) double tsm[];
   double* cx = tsm;
   double* cy = tsm + kTreeChunk * kTreeCta;
-  __shared__ uint16_t s_stk[kTreeChunk * kTreeCta];
-  stage_chunks(nullptr, n, blockIdx.x * kTreeCta, R_x, R_y, cx, cy);
-  __syncthreads();
+  uint8_t* stk = reinterpret_cast<uint8_t*>(cy + kTreeChunk * kTreeCta);
   const uint32_t c = blockIdx.x * kTreeCta + threadIdx.x;
   const uint32_t lo = c * kTreeChunk;
-  if (lo >= n) return;
-  const int cnt = (int)min((uint32_t)kTreeChunk, n - lo);
-  PersistentTop pt;
-  pt.b1 = bt[c];
-  pt.b2 = (pt.b1 != kNone) ? parent[pt.b1] : kNone;
-  auto pos = [&](int k) -> uint32_t { return lo + (uint32_t)k; };
-  bool ok = true;
-  // every push's link at push time must be the candidate's link (pushes that
-  // survive the chunk must match; popped ones are checked too -- a correct
-  // candidate state at the next boundary implies them all, and checking them
-  // here is cheaper than tracking survivors)
-  const int top = persistent_scan(pos, cnt, cx, cy, pt, R_x, R_y, parent, s_stk,
-                                  [&](int, uint32_t) {});
-  const uint32_t end_top = top ? pos(s_stk[(top - 1) * kTreeCta + threadIdx.x]) : pt.b1;
-  ok = bt[c + 1] == end_top;
-  for (int k = 0; k < top && ok; ++k) {
-    const uint32_t p = pos(s_stk[k * kTreeCta + threadIdx.x]);
-    const uint32_t below = k ? pos(s_stk[(k - 1) * kTreeCta + threadIdx.x]) : pt.b1;
-    if (parent[p] != below) ok = false;
+  if (lo >= N) return;
+  const int cnt = (int)min((uint32_t)kTreeChunk, N - lo);
+  tree_stage<kTreeCta>([&](int k) { return lo + (uint32_t)k; }, cnt, R_x, R_y, cx, cy, nullptr);
+  uint32_t b1 = kNone, b2 = kNone;
+  const int top = tree_scan_run<kTreeCta>(cnt, cx, cy, b1, b2, R_x, R_y, w.parent, stk,
+                                          [](int, int) {});
+  for (int k = 0; k < top; ++k) {
+    const uint32_t q = lo + stk[k * kTreeCta + threadIdx.x];
+    w.chainq[lo + k] = q;
+    w.chainp[lo + k] = q;
   }
-  if (!ok) atomicAdd(fail, 1u);
+  w.offbuf[0][c] = (uint32_t)top;
+}
+
+// Middle, ONE CTA: Q_1 from the level-0 chains, levels >= 1 up, the top-level
+// scan, and the down-sweep to level 1 (bt_1). info[0] = 1: no shrink.
+__global__ void __launch_bounds__(kTreeThreads, 1) k_gr_mid(
+    const double* __restrict__ R_x, const double* __restrict__ R_y, uint32_t N, TreeWork w,
+    uint32_t* __restrict__ info) {
+  extern __shared__ __align__(16) double tsm[];
+  double* cx = tsm;
+  double* cy = tsm + kTreeChunk * kTreeThreads;
+  uint32_t* cp = reinterpret_cast<uint32_t*>(cy + kTreeChunk * kTreeThreads);
+  uint8_t* stk = reinterpret_cast<uint8_t*>(cp + kTreeChunk * kTreeThreads);
+  __shared__ uint32_t s_w[32];
+  __shared__ uint32_t s_carry;
+  __shared__ TreeLevel L[kTreeMaxLevels + 1];
+  __shared__ int s_K, s_bad;
+  const int t = threadIdx.x;
+  if (t == 0) {
+    L[0].Q = nullptr;
+    L[0].up = nullptr;
+    L[0].nq = N;
+    s_K = -1;
+    s_bad = 0;
+    info[0] = 0;
+    info[2] = 0;
+  }
+  __syncthreads();
+  for (int j = 0; j < kTreeMaxLevels; ++j) {
+    const uint32_t nq = L[j].nq;
+    const uint32_t nch = (nq + kTreeChunk - 1) / kTreeChunk;
+    if (t == 0) {
+      L[j].nch = nch;
+      L[j].off = w.offbuf[j];
+      L[j].bt = w.btbuf[j];
+    }
+    __syncthreads();
+    const uint32_t* Q = L[j].Q;
+    if (j > 0) {  // level-0 chains come from k_gr_local0
+      for (uint32_t c0 = 0; c0 < nch; c0 += kTreeThreads) {
+        const uint32_t c = c0 + t;
+        if (c < nch) {
+          const uint32_t lo = c * kTreeChunk;
+          const int cnt = (int)min((uint32_t)kTreeChunk, nq - lo);
+          tree_stage<kTreeThreads>([&](int k) { return Q[lo + k]; }, cnt, R_x, R_y, cx, cy, cp);
+          uint32_t b1 = kNone, b2 = kNone;
+          const int top = tree_scan_run<kTreeThreads>(cnt, cx, cy, b1, b2, R_x, R_y, w.parent,
+                                                      stk, [](int, int) {});
+          for (int k = 0; k < top; ++k) {
+            const int e = stk[k * kTreeThreads + t];
+            w.chainq[lo + k] = lo + e;
+            w.chainp[lo + k] = cp[e * kTreeThreads + t];
+          }
+          L[j].off[c] = (uint32_t)top;
+        }
+      }
+    }
+    __syncthreads();
+    const uint32_t total = tree_scan(L[j].off, nch, s_w, &s_carry);
+    if (t == 0) {
+      L[j].off[nch] = total;
+      const bool shrink =
+          (j == 0) ? (total * 5ull <= (uint64_t)nq * 3) : (total * 5ull <= (uint64_t)nq * 4);
+      if (!shrink || total > w.cap[j + 1] || j + 1 > kTreeMaxLevels - 1) s_bad = 1;
+      L[j + 1].Q = w.Qbuf[j + 1];
+      L[j + 1].up = w.upbuf[j + 1];
+      L[j + 1].nq = total;
+    }
+    __syncthreads();
+    if (s_bad) break;
+    for (uint32_t c = t; c < nch; c += kTreeThreads) {
+      const uint32_t o = L[j].off[c], ln = L[j].off[c + 1] - o;
+      for (uint32_t k0 = 0; k0 < ln; k0 += 8) {
+        uint32_t qv[8], pv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          qv[u] = (k0 + u < ln) ? w.chainq[c * kTreeChunk + k0 + u] : 0u;
+          pv[u] = (k0 + u < ln) ? w.chainp[c * kTreeChunk + k0 + u] : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (k0 + u < ln) { L[j + 1].Q[o + k0 + u] = pv[u]; L[j + 1].up[o + k0 + u] = qv[u]; }
+      }
+    }
+    __syncthreads();
+    if (total <= kTreeTop) {
+      if (t == 0) s_K = j + 1;
+      __syncthreads();
+      break;
+    }
+  }
+  const int K = s_K;
+  if (s_bad || K < 1) {  // no shrink: the host takes another strategy
+    if (t == 0) { info[0] = 1; info[3] = 0; }
+    return;
+  }
+  // ---- top: one thread over Q_K, staged in shared memory by all ----
+  {
+    const TreeLevel& tl = L[K];
+    const TreeLevel& ll = L[K - 1];
+    const uint32_t nk = tl.nq;  // <= kTreeTop
+    uint32_t* s_p = cp;         // reuse the staging area
+    uint32_t* s_ch = cp + kTreeTop;
+    uint32_t* s_st = cp + 2 * kTreeTop;
+    for (uint32_t k = t; k < nk; k += kTreeThreads) {
+      const uint32_t p = tl.Q[k];
+      s_p[k] = p;
+      s_ch[k] = tl.up[k] / kTreeChunk;
+      cx[k] = R_x[p];
+      cy[k] = R_y[p];
+    }
+    __syncthreads();
+    if (t == 0) {
+      int top = 0;
+      double s1x = 0, s1y = 0, s2x = 0, s2y = 0;
+      uint32_t next_b = 0;
+      for (uint32_t k = 0; k < nk; ++k) {
+        const uint32_t p = s_p[k];
+        const uint32_t tp = top ? s_p[s_st[top - 1]] : kNone;
+        for (; next_b <= s_ch[k]; ++next_b) ll.bt[next_b] = tp;
+        const double px = cx[k], py = cy[k];
+        while (top >= 2 && !left_turn(s2x, s2y, s1x, s1y, px, py)) {
+          --top;
+          s1x = s2x; s1y = s2y;
+          if (top >= 2) { const uint32_t q = s_st[top - 2]; s2x = cx[q]; s2y = cy[q]; }
+        }
+        w.parent[p] = top ? s_p[s_st[top - 1]] : kNone;
+        s_st[top++] = k;
+        s2x = s1x; s2y = s1y;
+        s1x = px; s1y = py;
+      }
+      const uint32_t tp = top ? s_p[s_st[top - 1]] : kNone;
+      for (; next_b <= ll.nch; ++next_b) ll.bt[next_b] = tp;
+      for (int k = 0; k < top; ++k) w.fstack[k] = s_p[s_st[k]];
+      info[1] = (uint32_t)top;
+    }
+    __syncthreads();
+  }
+  // ---- down: level j -> j-1, for j >= 2 (level 1 -> 0 runs on many CTAs) ----
+  for (int j = K - 1; j >= 2; --j) {
+    const TreeLevel& hl = L[j];
+    const TreeLevel& ll = L[j - 1];
+    for (uint32_t c0 = 0; c0 < ll.nch; c0 += kTreeThreads) {
+      const uint32_t cq = c0 + t;
+      if (cq < ll.nch) {
+        const uint32_t e = ll.off[cq];
+        const uint32_t c = e / kTreeChunk;
+        const int cnt = (int)(e - c * kTreeChunk);
+        const uint32_t* Qj = hl.Q + c * kTreeChunk;
+        tree_stage<kTreeThreads>([&](int k) { return Qj[k]; }, cnt, R_x, R_y, cx, cy, cp);
+        uint32_t b1 = hl.bt[c];
+        uint32_t b2 = (b1 != kNone) ? w.parent[b1] : kNone;
+        const int top = tree_scan_run<kTreeThreads>(
+            cnt, cx, cy, b1, b2, R_x, R_y, w.parent, stk, [&](int k, int below) {
+              w.parent[cp[k * kTreeThreads + t]] = below >= 0 ? cp[below * kTreeThreads + t] : b1;
+            });
+        ll.bt[cq] = top ? cp[stk[(top - 1) * kTreeThreads + t] * kTreeThreads + t] : b1;
+      }
+    }
+    __syncthreads();
+    if (t == 0) ll.bt[ll.nch] = hl.bt[hl.nch];
+    __syncthreads();
+  }
+  if (t == 0) {
+    // K == 1: the top-level scan already wrote the level-0 boundary states;
+    // else the level-0 boundary after the last chunk is the final top
+    if (K >= 2) w.btbuf[0][(N + kTreeChunk - 1) / kTreeChunk] = L[1].bt[L[1].nch];
+    info[3] = K;
+  }
+}
+
+// Down 1 -> 0, many CTAs: the state before every buffer chunk.
+__global__ void __launch_bounds__(kTreeCta) k_gr_down0(uint32_t N, const double* __restrict__ R_x,
+                                                      const double* __restrict__ R_y, TreeWork w,
+                                                      const uint32_t* __restrict__ info) {
+  extern __shared__ __align__(16) double tsm[];
+  double* cx = tsm;
+  double* cy = tsm + kTreeChunk * kTreeCta;
+  uint32_t* cp = reinterpret_cast<uint32_t*>(cy + kTreeChunk * kTreeCta);
+  uint8_t* stk = reinterpret_cast<uint8_t*>(cp + kTreeChunk * kTreeCta);
+  if (info[0] || info[3] < 2) return;  // K == 1: level-0 states come from the top scan
+  const uint32_t nch0 = (N + kTreeChunk - 1) / kTreeChunk;
+  const uint32_t cq = blockIdx.x * kTreeCta + threadIdx.x;
+  if (cq >= nch0) return;
+  const uint32_t* off0 = w.offbuf[0];
+  const uint32_t* bt1 = w.btbuf[1];
+  const uint32_t* Q1 = w.Qbuf[1];
+  const uint32_t e = off0[cq];
+  const uint32_t c = e / kTreeChunk;
+  const int cnt = (int)(e - c * kTreeChunk);
+  const uint32_t* Qj = Q1 + c * kTreeChunk;
+  const int t = threadIdx.x;
+  tree_stage<kTreeCta>([&](int k) { return Qj[k]; }, cnt, R_x, R_y, cx, cy, cp);
+  uint32_t b1 = bt1[c];
+  uint32_t b2 = (b1 != kNone) ? w.parent[b1] : kNone;
+  const int top = tree_scan_run<kTreeCta>(cnt, cx, cy, b1, b2, R_x, R_y, w.parent, stk,
+                                          [&](int k, int below) {
+                                            w.parent[cp[k * kTreeCta + t]] =
+                                                below >= 0 ? cp[below * kTreeCta + t] : b1;
+                                          });
+  w.btbuf[0][cq] = top ? cp[stk[(top - 1) * kTreeCta + t] * kTreeCta + t] : b1;
+}
+
+// Certificate, many CTAs (thread per buffer chunk); failures counted in info[2].
+__global__ void __launch_bounds__(kTreeCta) k_gr_cert(uint32_t N, const double* __restrict__ R_x,
+                                                     const double* __restrict__ R_y, TreeWork w,
+                                                     uint32_t* __restrict__ info,
+                                                     uint32_t debug_corrupt) {
+  extern __shared__ __align__(16) double tsm[];
+  double* cx = tsm;
+  double* cy = tsm + kTreeChunk * kTreeCta;
+  uint8_t* stk = reinterpret_cast<uint8_t*>(cy + kTreeChunk * kTreeCta);
+  if (info[0]) return;
+  const uint32_t nch0 = (N + kTreeChunk - 1) / kTreeChunk;
+  const uint32_t c = blockIdx.x * kTreeCta + threadIdx.x;
+  if (c >= nch0) return;
+  const uint32_t* bt = w.btbuf[0];
+  const uint32_t lo = c * kTreeChunk;
+  const int cnt = (int)min((uint32_t)kTreeChunk, N - lo);
+  tree_stage<kTreeCta>([&](int k) { return lo + (uint32_t)k; }, cnt, R_x, R_y, cx, cy, nullptr);
+  uint32_t b1 = bt[c];
+  uint32_t b2 = (b1 != kNone) ? w.parent[b1] : kNone;
+  const int top =
+      tree_scan_run<kTreeCta>(cnt, cx, cy, b1, b2, R_x, R_y, w.parent, stk, [](int, int) {});
+  const uint32_t end_top = top ? lo + stk[(top - 1) * kTreeCta + threadIdx.x] : b1;
+  uint32_t want = bt[c + 1];
+  if (debug_corrupt && c + 1 == nch0) want = bt[c];  // falsified final state
+  bool ok = want == end_top;
+  for (int k = 0; k < top && ok; ++k) {
+    const uint32_t p = lo + stk[k * kTreeCta + threadIdx.x];
+    const uint32_t below = k ? lo + stk[(k - 1) * kTreeCta + threadIdx.x] : b1;
+    ok = w.parent[p] == below;
+  }
+  if (!ok) atomicAdd(&info[2], 1u);
 }
 
 // Output (one CTA): the top-level scan's final stack is the certified final
 // state iff its top is the certified top and every element links to the one
-// below it in parent[] (all checked in parallel); otherwise the certified
-// state is walked down its parent links by one thread.
-__global__ void __launch_bounds__(1024) k_gr_emit(const uint32_t* __restrict__ bt_final,
-                                                  const uint32_t* __restrict__ parent,
-                                                  const uint32_t* __restrict__ fstack,
-                                                  const uint32_t* __restrict__ flen_dev,
-                                                  const uint32_t* __restrict__ R_i,
-                                                  uint32_t* __restrict__ tmp,
+// below it (checked in parallel); otherwise the certified state is walked
+// down its links. Certificate failures: the exact sequential scan (one
+// thread), the reference loop itself.
+__global__ void __launch_bounds__(1024) k_gr_emit(uint32_t N, const double* __restrict__ R_x,
+                                                  const double* __restrict__ R_y,
+                                                  const uint32_t* __restrict__ R_i, TreeWork w,
+                                                  const uint32_t* __restrict__ info,
                                                   uint32_t* __restrict__ out_idx,
                                                   Counters* __restrict__ ctr) {
-  const uint32_t len = *flen_dev, top = *bt_final;
-  bool ok = len > 0 && fstack[len - 1] == top;
-  for (uint32_t k = threadIdx.x; k < len && ok; k += blockDim.x)
-    ok = parent[fstack[k]] == (k ? fstack[k - 1] : kNone);
-  if (__syncthreads_and(ok)) {
-    for (uint32_t k = threadIdx.x; k < len; k += blockDim.x) out_idx[k] = R_i[fstack[k]];
-    if (threadIdx.x == 0) ctr->hull = len;
+  if (info[0]) return;
+  const uint32_t t = threadIdx.x;
+  if (info[2]) {
+    if (t != 0) return;
+    uint32_t top = 0;
+    double s1x = 0, s1y = 0, s2x = 0, s2y = 0;
+    for (uint32_t i = 0; i < N; ++i) {
+      const double px = R_x[i], py = R_y[i];
+      while (top >= 2 && !left_turn(s2x, s2y, s1x, s1y, px, py)) {
+        --top;
+        s1x = s2x; s1y = s2y;
+        if (top >= 2) { const uint32_t q = w.tmp[top - 2]; s2x = R_x[q]; s2y = R_y[q]; }
+      }
+      w.tmp[top++] = i;
+      s2x = s1x; s2y = s1y;
+      s1x = px; s1y = py;
+    }
+    for (uint32_t k = 0; k < top; ++k) out_idx[k] = R_i[w.tmp[k]];
+    ctr->hull = top;
     return;
   }
-  if (threadIdx.x != 0) return;
+  const uint32_t nch0 = (N + kTreeChunk - 1) / kTreeChunk;
+  const uint32_t len = info[1], ftop = w.btbuf[0][nch0];
+  bool ok = len > 0 && w.fstack[len - 1] == ftop;
+  for (uint32_t k = t; k < len && ok; k += blockDim.x)
+    ok = w.parent[w.fstack[k]] == (k ? w.fstack[k - 1] : kNone);
+  if (__syncthreads_and(ok)) {
+    for (uint32_t k = t; k < len; k += blockDim.x) out_idx[k] = R_i[w.fstack[k]];
+    if (t == 0) ctr->hull = len;
+    return;
+  }
+  if (t != 0) return;
   uint32_t h = 0;
-  for (uint32_t t = top; t != kNone; t = parent[t]) tmp[h++] = t;
-  for (uint32_t k = 0; k < h; ++k) out_idx[k] = R_i[tmp[h - 1 - k]];
+  for (uint32_t p = ftop; p != kNone; p = w.parent[p]) w.tmp[h++] = p;
+  for (uint32_t k = 0; k < h; ++k) out_idx[k] = R_i[w.tmp[h - 1 - k]];
   ctr->hull = h;
 }
 

@@ -95,6 +95,7 @@ struct gscan_handle {
   double* sp_cdf = nullptr;  // sampled pseudo-angle CDF, kSpCells + 1 (per call)
   uint32_t* sp_cells = nullptr;  // sample counts per cell
   uint32_t* sp_big = nullptr;    // candidate buckets for the CTA sorter
+  uint32_t* sp_bigg = nullptr;   // gathered buckets for the CTA sorter
   uint32_t *sp_gcount = nullptr, *sp_ccount = nullptr, *sp_hcount = nullptr;  // per-CTA emissions
   uint64_t* sp_dup2 = nullptr;   // partitioned hash list (n)
   bool sp_debug = false, sp_no_dup = false;
@@ -565,14 +566,23 @@ int graham_prefix(gscan_handle* h, const double* Rx, const double* Ry, const uin
   return GSCAN_OK;
 }
 
-// Tree strategy (graham_tree.cuh) for pop-heavy buffers. *done = false when
-// the local chains do not shrink (convex position): the caller then takes the
-// junction / prefix / sequential strategies.
+// Tree strategy (graham_tree.cuh) for pop-heavy buffers: one kernel. *done =
+// false when the local chains do not shrink (convex position): the caller then
+// takes the junction / prefix / sequential strategies.
+constexpr uint32_t kTreeMaxN = 1u << 22;  // larger buffers: the middle level would be too long
+
 int graham_tree(gscan_handle* h, const double* Rx, const double* Ry, const uint32_t* Ri,
                 uint32_t N, bool* done) {
   *done = false;
-  constexpr int kMaxLevels = 16;
-  const uint64_t need = (uint64_t)N * 6 + 4096 * kMaxLevels;
+  // level capacities: level 1 <= 0.6 N, then <= 0.8x per level (else the kernel declines)
+  uint64_t caps[kTreeMaxLevels + 1];
+  uint64_t need = 4ull * N + (N / kTreeChunk + 64) + kTreeTop + 64;
+  caps[0] = N;
+  for (int j = 1; j <= kTreeMaxLevels; ++j) {
+    caps[j] = (j == 1 ? (uint64_t)N * 3 / 5 : caps[j - 1] * 4 / 5) + 64;
+    need += 2 * caps[j] + 2 * (caps[j - 1] / kTreeChunk + 64) + 128;
+  }
+  need += 2 * (caps[kTreeMaxLevels] / kTreeChunk + 64) + 128;
   if (need > h->gt_cap) {
     dfree(h->gt_pool);
     CU(cudaMalloc(&h->gt_pool, need * 4));
@@ -581,82 +591,54 @@ int graham_tree(gscan_handle* h, const double* Rx, const double* Ry, const uint3
   uint32_t* pool = h->gt_pool;
   uint64_t used = 0;
   auto take = [&](uint64_t cnt) { uint32_t* p = pool + used; used += (cnt + 31) & ~31ull; return p; };
-  uint32_t* parent = take(N);
-  uint32_t* tmp = take(N);
-  uint32_t* fstack = take(kTreeTop + 32);
-  struct Level { const uint32_t* Q; uint32_t nq, nch; uint32_t* off; uint32_t* bt; uint32_t* up; };
-  Level L[kMaxLevels + 1];
-  L[0].Q = nullptr;
-  L[0].nq = N;
-  L[0].up = nullptr;
-  int K = 0;
-  while (true) {
-    Level& lv = L[K];
-    lv.nch = (lv.nq + kTreeChunk - 1) / kTreeChunk;
-    if (used + (uint64_t)lv.nch * kTreeChunk * 3 + 3 * lv.nch + 64 > h->gt_cap) return GSCAN_OK;
-    uint32_t* chain_q = take((uint64_t)lv.nch * kTreeChunk);
-    uint32_t* len = take(lv.nch + 1);
-    lv.off = take(lv.nch + 2);
-    lv.bt = take(lv.nch + 2);
-    {
-      Launch Lk(h, "k_gr_local");
-      k_gr_local<<<(lv.nch + kTreeCta - 1) / kTreeCta, kTreeCta, kTreeSmem, h->stream>>>(
-          lv.Q, lv.nq, Rx, Ry, chain_q, len);
+  TreeWork w{};
+  w.parent = take(N);
+  w.tmp = take(N);
+  w.chainq = take(N);
+  w.chainp = take(N);
+  w.len = take(N / kTreeChunk + 64);
+  w.fstack = take(kTreeTop);
+  for (int j = 0; j <= kTreeMaxLevels; ++j) {
+    w.cap[j] = (uint32_t)caps[j];
+    if (j >= 1) {
+      w.Qbuf[j] = take(caps[j]);
+      w.upbuf[j] = take(caps[j]);
     }
-    TRY(scan_u32(h, len, lv.nch, lv.off));
-    uint32_t total;
-    TRY(read_u32(h, lv.off + lv.nch, &total));
-    if (K == 0 && total * 5 > (uint64_t)N * 3) return GSCAN_OK;  // not pop-heavy
-    if (K + 1 > kMaxLevels || total * 5 > (uint64_t)lv.nq * 4) return GSCAN_OK;
-    Level& nx = L[K + 1];
-    uint32_t* Qn = take(total);
-    nx.up = take(total);
-    nx.Q = Qn;
-    nx.nq = total;
-    {
-      Launch Lk(h, "k_gr_gather");
-      k_gr_gather<<<(lv.nch + 7) / 8, 8 * kTreeChunk, 0, h->stream>>>(lv.Q, chain_q, len, lv.off,
-                                                                      lv.nch, Qn, nx.up);
-    }
-    ++K;
-    if (total <= kTreeTop) break;
+    w.offbuf[j] = take(caps[j] / kTreeChunk + 64);
+    w.btbuf[j] = take(caps[j] / kTreeChunk + 64);
   }
-  uint32_t* fail_d = h->g_misc;
-  uint32_t* len_d = h->g_misc + 1;
-  CU(cudaMemsetAsync(h->g_misc, 0, 16, h->stream));
+  uint32_t* info = h->g_misc + 4;
+  const uint32_t nch0 = (N + kTreeChunk - 1) / kTreeChunk;
+  const uint32_t g0 = (nch0 + kTreeCta - 1) / kTreeCta;
+  const uint32_t dbg = (h->debug & GSCAN_DEBUG_CORRUPT_CANDIDATE) ? 1u : 0u;
   {
-    Launch Lk(h, "k_gr_top");
-    k_gr_top<<<1, 128, 0, h->stream>>>(L[K].Q, L[K].up, L[K - 1].off + L[K - 1].nch,
-                                       L[K - 1].nch, Rx, Ry, parent, L[K - 1].bt, len_d, fstack);
-  }
-  for (int j = K - 1; j >= 1; --j) {
-    Launch Lk(h, "k_gr_down");
-    k_gr_down<<<(L[j - 1].nch + kTreeCta - 1) / kTreeCta, kTreeCta, kTreeSmem, h->stream>>>(
-        L[j].Q, L[j - 1].off, L[j - 1].nch, L[j].bt, Rx, Ry, parent, L[j - 1].bt);
-    CU(cudaMemcpyAsync(L[j - 1].bt + L[j - 1].nch, L[j].bt + L[j].nch, 4, cudaMemcpyDeviceToDevice,
-                       h->stream));
-  }
-  if (h->debug & GSCAN_DEBUG_CORRUPT_CANDIDATE) {
-    // drop the candidate's last boundary state: the certificate must reject it
-    CU(cudaMemcpyAsync(L[0].bt + L[0].nch, L[0].bt + L[0].nch - 1, 4, cudaMemcpyDeviceToDevice,
-                       h->stream));
+    Launch Lk(h, "k_gr_local0");
+    k_gr_local0<<<g0, kTreeCta, kTreeCtaSmem, h->stream>>>(N, Rx, Ry, w);
   }
   {
-    Launch Lk(h, "k_gr_certify");
-    k_gr_certify<<<(L[0].nch + kTreeCta - 1) / kTreeCta, kTreeCta, kTreeSmem, h->stream>>>(
-        N, Rx, Ry, parent, L[0].bt, fail_d);
+    Launch Lk(h, "k_gr_mid");
+    k_gr_mid<<<1, kTreeThreads, kTreeSmem, h->stream>>>(Rx, Ry, N, w, info);
   }
-  uint32_t fails;
-  TRY(read_u32(h, fail_d, &fails));
-  h->graham_fails = fails;
-  h->graham_path = 8;
-  if (fails || (h->debug & GSCAN_DEBUG_FORCE_FALLBACK)) return graham_seq_fallback(h, Rx, Ry, Ri);
+  {
+    Launch Lk(h, "k_gr_down0");
+    k_gr_down0<<<g0, kTreeCta, kTreeCtaSmem2, h->stream>>>(N, Rx, Ry, w, info);
+  }
+  {
+    Launch Lk(h, "k_gr_cert");
+    k_gr_cert<<<g0, kTreeCta, kTreeCtaSmem, h->stream>>>(N, Rx, Ry, w, info, dbg);
+  }
   {
     Launch Lk(h, "k_gr_emit");
-    k_gr_emit<<<1, 1024, 0, h->stream>>>(L[0].bt + L[0].nch, parent, fstack, len_d, Ri, tmp,
-                                         h->d_out, h->ctr);
+    k_gr_emit<<<1, 1024, 0, h->stream>>>(N, Rx, Ry, Ri, w, info, h->d_out, h->ctr);
   }
   CU(cudaGetLastError());
+  uint32_t hi[3];
+  CU(cudaMemcpyAsync(hi, info, 12, cudaMemcpyDeviceToHost, h->stream));
+  CU(cudaStreamSynchronize(h->stream));
+  if (hi[0]) return GSCAN_OK;  // no shrink
+  h->graham_fails = hi[2];
+  h->graham_path = 8 | (hi[2] ? 4 : 0);
+  if (!hi[2] && (h->debug & GSCAN_DEBUG_FORCE_FALLBACK)) return graham_seq_fallback(h, Rx, Ry, Ri);
   *done = true;
   return GSCAN_OK;
 }
@@ -675,7 +657,7 @@ int stage_graham(gscan_handle* h, const double* Rx, const double* Ry, const uint
   }
   const bool forced = h->debug & (GSCAN_DEBUG_FORCE_JUNCTION | GSCAN_DEBUG_FORCE_SEQUENTIAL |
                                   GSCAN_DEBUG_FORCE_PREFIX);
-  if (!forced) {
+  if (!forced && N <= kTreeMaxN) {
     bool done = false;
     TRY(graham_tree(h, Rx, Ry, Ri, N, &done));
     if (done || (h->graham_path & 8)) return GSCAN_OK;
@@ -809,6 +791,7 @@ int sparse_init(gscan_handle* h) {
   CU(cudaMalloc(&h->sp_cdf, (kSpCells + 1) * 8));
   CU(cudaMalloc(&h->sp_cells, kSpCells * 4));
   CU(cudaMalloc(&h->sp_big, nb * 4));
+  CU(cudaMalloc(&h->sp_bigg, nb * 4));
   CU(cudaMalloc(&h->sp_gcount, G * 4));
   CU(cudaMalloc(&h->sp_ccount, G * 4));
   CU(cudaMalloc(&h->sp_hcount, G * 4));
@@ -948,9 +931,14 @@ int run_sparse(gscan_handle* h, const double* xs, const double* ys, uint32_t n,
   }
   {
     Launch L(h, "k_sp_sort_gathered");
-    k_sp_sort_gathered<<<h->sm_count * 2, kSpSortThreads, kSpSortSmem, s>>>(
-        h->sp_glist, h->sp_bstart, h->sp_hist, h->sp_gcnt, h->rec, h->ext, h->sp_st, h->A_x,
-        h->A_y, h->A_i);
+    k_sp_sort_gathered<<<h->sm_count * 4, kSpSmallThreads, kSpSmallSmem, s>>>(
+        h->sp_glist, h->sp_bstart, h->sp_hist, h->sp_gcnt, h->rec, h->ext, h->sp_st, h->sp_bigg,
+        h->A_x, h->A_y, h->A_i);
+  }
+  {
+    Launch L(h, "k_sp_sort_gathered_big");
+    k_sp_sort_gathered_big<<<h->sm_count, kSpSortThreads, kSpSortSmem, s>>>(
+        h->sp_bigg, h->sp_bstart, h->sp_hist, h->rec, h->ext, h->sp_st, h->A_x, h->A_y, h->A_i);
   }
   {
     Launch L(h, "k_sp_slices");
@@ -1212,6 +1200,8 @@ int gscan_create(int device, gscan_handle** out) {
     CU(cudaFuncSetAttribute(k_sp_verify<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, nbs + 4));
     CU(cudaFuncSetAttribute(k_sp_verify<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, nbs + 4));
     CU(cudaFuncSetAttribute(k_sp_sort_gathered, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)kSpSmallSmem));
+    CU(cudaFuncSetAttribute(k_sp_sort_gathered_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)kSpSortSmem));
     CU(cudaFuncSetAttribute(k_sp_sort_cand_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)kSpSortSmem));
@@ -1219,9 +1209,7 @@ int gscan_create(int device, gscan_handle** out) {
                             (int)(kSpDupSlots * 8)));
     CU(cudaFuncSetAttribute(k_sp_dup_part, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)kSpDupPartSmem));
-    CU(cudaFuncSetAttribute(k_gr_local, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTreeSmem));
-    CU(cudaFuncSetAttribute(k_gr_down, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTreeSmem));
-    CU(cudaFuncSetAttribute(k_gr_certify, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTreeSmem));
+    CU(cudaFuncSetAttribute(k_gr_mid, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTreeSmem));
     h->sp_grid = h->sm_count;
     return GSCAN_OK;
   };
@@ -1240,7 +1228,7 @@ int gscan_destroy(gscan_handle* h) {
   if (h->stream) cudaStreamSynchronize(h->stream);
   free_buffers(h);
   dfree(h->partials); dfree(h->ext); dfree(h->ctr); dfree(h->scratch64);
-  dfree(h->sp_th); dfree(h->sp_cdf); dfree(h->sp_cells); dfree(h->sp_big); dfree(h->sp_gcount); dfree(h->sp_ccount); dfree(h->sp_hcount); dfree(h->sp_hist_part); dfree(h->sp_phi_part); dfree(h->sp_part_off);
+  dfree(h->sp_th); dfree(h->sp_cdf); dfree(h->sp_cells); dfree(h->sp_big); dfree(h->sp_bigg); dfree(h->sp_gcount); dfree(h->sp_ccount); dfree(h->sp_hcount); dfree(h->sp_hist_part); dfree(h->sp_phi_part); dfree(h->sp_part_off);
   dfree(h->sp_d2); dfree(h->sp_hist); dfree(h->sp_bstart); dfree(h->sp_gbits); dfree(h->sp_glist);
   dfree(h->sp_gcnt); dfree(h->sp_phimax); dfree(h->sp_prefmax); dfree(h->sp_slice);
   dfree(h->sp_ccnt); dfree(h->sp_cstart); dfree(h->sp_wcnt); dfree(h->sp_wstart); dfree(h->sp_rlo);

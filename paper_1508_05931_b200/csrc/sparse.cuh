@@ -57,7 +57,7 @@ constexpr double kSpTol = 1e-7;               // candidate tolerance on phi (pse
 constexpr uint32_t kSpGatherCap = 4096;       // largest bucket sorted in smem
 constexpr uint32_t kSpDupSlotBits = 14;
 constexpr uint32_t kSpDupSlots = 1u << kSpDupSlotBits;  // dup-check hash set slots (smem, 8 B)
-constexpr uint32_t kSpDupRound = 6144;        // entries per hash-set round (load <= 0.375)
+constexpr uint32_t kSpDupRound = 8192;        // entries per hash-set round (load <= 0.5)
 constexpr uint32_t kSpPartChunk = 8192;       // entries per partitioning chunk (smem)
 constexpr size_t kSpDupPartSmem = (size_t)kSpPartChunk * 16 + (size_t)kSpParts * 12;
 
@@ -108,7 +108,7 @@ struct SpState {
   double r02;          // (1e-3 * bounding-box diagonal)^2: closer points are always walked
   double dmax2;        // bounding-box diagonal^2
   uint32_t cert;       // 1: certificate holds (F6 skipped)
-  uint32_t pad2;
+  uint32_t n_bigg;     // gathered buckets for the bitonic sorter
 };
 
 // ---------------------------------------------------------------------------
@@ -199,7 +199,7 @@ __device__ __forceinline__ uint64_t coord_hash64(double x, double y) {
   z ^= z >> 30; z *= 0xbf58476d1ce4e5b9ull;
   z ^= z >> 27; z *= 0x94d049bb133111ebull;
   z ^= z >> 31;
-  return z;
+  return z == ~0ull ? 0ull : z;  // ~0 marks an empty slot / padding
 }
 
 
@@ -810,10 +810,21 @@ __global__ void __launch_bounds__(1024) k_sp_dup_part(const uint64_t* __restrict
     const uint32_t len = min(kSpPartChunk, cnt - c0);
     for (uint32_t p = threadIdx.x; p < kSpParts; p += blockDim.x) s_cnt[p] = 0;
     __syncthreads();
-    for (uint32_t t = threadIdx.x; t < len; t += blockDim.x) {
-      const uint64_t h = src[c0 + t];
-      s_in[t] = h;
-      atomicAdd(&s_cnt[(uint32_t)(h >> (64 - kSpPartBits))], 1u);
+    for (uint32_t t0 = threadIdx.x; t0 < len; t0 += 8 * blockDim.x) {
+      uint64_t hv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const uint32_t t = t0 + u * blockDim.x;
+        hv[u] = t < len ? src[c0 + t] : 0ull;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const uint32_t t = t0 + u * blockDim.x;
+        if (t < len) {
+          s_in[t] = hv[u];
+          atomicAdd(&s_cnt[(uint32_t)(hv[u] >> (64 - kSpPartBits))], 1u);
+        }
+      }
     }
     __syncthreads();
     // exclusive scan of the partition counts (kSpParts = 2 x blockDim)
@@ -877,17 +888,27 @@ __global__ void __launch_bounds__(512) k_sp_dups(const uint64_t* __restrict__ pa
   for (uint32_t r = 0; r < rounds; ++r) {
     for (uint32_t k = threadIdx.x; k < kSpDupSlots; k += blockDim.x) s_e[k] = ~0ull;
     __syncthreads();
-    for (uint32_t e = lo + threadIdx.x; e < hi && !dup && !full; e += blockDim.x) {
-      const uint64_t h = parted[e];
-      const uint32_t mid = (uint32_t)(h >> 20) & 0xffffu;  // bits below the partition
-      if ((uint32_t)(((uint64_t)mid * rounds) >> 16) != r) continue;
-      uint32_t slot = (uint32_t)h & (kSpDupSlots - 1);
-      for (uint32_t probe = 0;; ++probe) {
-        if (probe == kSpDupSlots / 2) { full = true; break; }
-        const unsigned long long prev = atomicCAS(&s_e[slot], ~0ull, (unsigned long long)h);
-        if (prev == ~0ull) break;
-        if (prev == h) { dup = true; break; }
-        slot = (slot + 1) & (kSpDupSlots - 1);
+    for (uint32_t e0 = lo + threadIdx.x; e0 < hi && !dup && !full; e0 += 8 * blockDim.x) {
+      uint64_t hv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const uint32_t e = e0 + u * blockDim.x;
+        hv[u] = e < hi ? parted[e] : ~0ull;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const uint64_t h = hv[u];
+        if (h == ~0ull || dup || full) continue;
+        const uint32_t mid = (uint32_t)(h >> 20) & 0xffffu;  // bits below the partition
+        if ((uint32_t)(((uint64_t)mid * rounds) >> 16) != r) continue;
+        uint32_t slot = (uint32_t)h & (kSpDupSlots - 1);
+        for (uint32_t probe = 0;; ++probe) {
+          if (probe == kSpDupSlots / 2) { full = true; break; }
+          const unsigned long long prev = atomicCAS(&s_e[slot], ~0ull, (unsigned long long)h);
+          if (prev == ~0ull) break;
+          if (prev == h) { dup = true; break; }
+          slot = (slot + 1) & (kSpDupSlots - 1);
+        }
       }
     }
     if (__syncthreads_or(dup || full)) break;
@@ -937,15 +958,15 @@ __global__ void __launch_bounds__(256) k_sp_emit_place(
 constexpr int kSpSortThreads = 512;
 constexpr size_t kSpSortSmem = (size_t)kSpGatherCap * (8 + 8 + 8 + 8 + 4 + 2);
 
-template <typename Out>
+template <uint32_t kCap = kSpGatherCap, typename Out>
 __device__ bool cta_sort_bucket(const PtRec* __restrict__ R, uint32_t cnt, double ax, double ay,
                                 unsigned char* smem, Out&& out) {
   uint64_t* s_key = reinterpret_cast<uint64_t*>(smem);
-  double* s_d2 = reinterpret_cast<double*>(s_key + kSpGatherCap);
-  double* s_x = s_d2 + kSpGatherCap;
-  double* s_y = s_x + kSpGatherCap;
-  uint32_t* s_idx = reinterpret_cast<uint32_t*>(s_y + kSpGatherCap);
-  uint16_t* s_perm = reinterpret_cast<uint16_t*>(s_idx + kSpGatherCap);
+  double* s_d2 = reinterpret_cast<double*>(s_key + kCap);
+  double* s_x = s_d2 + kCap;
+  double* s_y = s_x + kCap;
+  uint32_t* s_idx = reinterpret_cast<uint32_t*>(s_y + kCap);
+  uint16_t* s_perm = reinterpret_cast<uint16_t*>(s_idx + kCap);
   uint32_t P = 32;
   while (P < cnt) P <<= 1;
   __syncthreads();
@@ -992,13 +1013,21 @@ __device__ bool cta_sort_bucket(const PtRec* __restrict__ R, uint32_t cnt, doubl
   return dup;
 }
 
-// Gathered buckets, CTA per bucket: exact positions 1 + bstart[b] + rank in
-// the annotated-buffer space A; records the exact position of P_l.
-__global__ void __launch_bounds__(kSpSortThreads) k_sp_sort_gathered(
+// Gathered buckets up to kSpSmallCap points: bitonic CTA sorter with one
+// compare-exchange per thread per stage (512 threads, ~37 KB of shared
+// memory, 4 CTAs per SM); exact positions 1 + bstart[b] + rank in the
+// annotated-buffer space A; records P_l's position. Larger buckets go to the
+// 4096-point sorter.
+constexpr uint32_t kSpSmallCap = 1024;
+constexpr int kSpSmallThreads = 512;
+constexpr size_t kSpSmallSmem = (size_t)kSpSmallCap * (8 + 8 + 8 + 8 + 4 + 2);
+
+__global__ void __launch_bounds__(kSpSmallThreads) k_sp_sort_gathered(
     const uint32_t* __restrict__ glist, const uint32_t* __restrict__ bstart,
     const uint32_t* __restrict__ hist, const uint32_t* __restrict__ gcnt,
     const PtRec* __restrict__ rec, const ExtResult* __restrict__ ext, SpState* __restrict__ st,
-    double* __restrict__ A_x, double* __restrict__ A_y, uint32_t* __restrict__ A_i) {
+    uint32_t* __restrict__ big, double* __restrict__ A_x, double* __restrict__ A_y,
+    uint32_t* __restrict__ A_i) {
   extern __shared__ __align__(16) unsigned char smem[];
   if (st->fail) return;
   const uint32_t ngb = st->n_gb, l_idx = st->l_idx;
@@ -1011,6 +1040,35 @@ __global__ void __launch_bounds__(kSpSortThreads) k_sp_sort_gathered(
       return;
     }
     if (threadIdx.x == 0) atomicMax(&st->max_g, cnt);
+    if (cnt > kSpSmallCap) {
+      if (threadIdx.x == 0) big[atomicAdd(&st->n_bigg, 1u)] = b;
+      continue;
+    }
+    const bool dup = cta_sort_bucket<kSpSmallCap>(rec + s0, cnt, ax, ay, smem,
+                                                  [&](uint32_t r, double x, double y, uint32_t idx) {
+      const uint32_t pos = 1 + s0 + r;
+      A_x[pos] = x;
+      A_y[pos] = y;
+      A_i[pos] = idx;
+      if (idx == l_idx) st->l_check = pos;
+    });
+    if (dup) atomicOr(&st->fail, kSpFailDup);
+  }
+}
+
+// Gathered buckets above kSpSmallCap: bitonic CTA sorter.
+__global__ void __launch_bounds__(kSpSortThreads) k_sp_sort_gathered_big(
+    const uint32_t* __restrict__ big, const uint32_t* __restrict__ bstart,
+    const uint32_t* __restrict__ hist, const PtRec* __restrict__ rec,
+    const ExtResult* __restrict__ ext, SpState* __restrict__ st, double* __restrict__ A_x,
+    double* __restrict__ A_y, uint32_t* __restrict__ A_i) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  if (st->fail) return;
+  const uint32_t nbig = st->n_bigg, l_idx = st->l_idx;
+  const double ax = ext->ax, ay = ext->ay;
+  for (uint32_t g = blockIdx.x; g < nbig; g += gridDim.x) {
+    const uint32_t b = big[g];
+    const uint32_t s0 = bstart[b], cnt = hist[b];
     if (cnt > kSpGatherCap) {
       if (threadIdx.x == 0) { atomicOr(&st->fail, kSpFailCap); atomicMax(&st->why, 4u); }
       return;
