@@ -36,8 +36,12 @@ constexpr int kTreeThreads = 256;   // one CTA; chunks are processed in waves of
 constexpr uint32_t kTreeTop = 128;  // largest top-level list for the single-thread scan
 constexpr int kTreeMaxLevels = 16;
 // shared memory: per thread a chunk's coordinates [k][t] and an index stack
-constexpr size_t kTreeSmem = (size_t)kTreeChunk * kTreeThreads * (8 + 8 + 4 + 1);
-constexpr size_t kTreeCtaSmem2 = (size_t)kTreeChunk * 64 * (8 + 8 + 4 + 1);
+// per-thread slot: chunk coordinates + positions (21 B per point) + the
+// persistent-stack cache (20 B per cached element)
+constexpr size_t tree_smem(int threads) {
+  return (size_t)kTreeChunk * threads * (8 + 8 + 4 + 1) + (size_t)8 * threads * (4 + 8 + 8);
+}
+constexpr size_t kTreeSmem = tree_smem(256);
 
 struct TreeLevel {
   uint32_t* Q;    // R positions (nullptr: identity, level 0)
@@ -127,72 +131,155 @@ __device__ __forceinline__ void tree_stage(PosF&& pos, int cnt, const double* __
 }
 
 // One thread's stack scan of a staged run on top of a persistent state (top
-// two elements b1, b2; parent[] links below). Own pushes are kept as run
-// indices in stk[depth * kTreeThreads + t]; deeper persistent elements are
-// loaded from global memory when pops reach them. on_push(k, below_run_index
-// or -1 = b1) is called for every push. Returns the number of own pushes left.
+// element b1, parent[] links below). The persistent state's top kTreePC
+// elements (positions and coordinates) are first walked into a per-thread
+// shared-memory cache pc[d * kStride + t] (d = depth, 0 = b1), so the pops
+// that reach into it -- divergent, one per thread -- read shared memory;
+// deeper elements come from global memory. Own pushes are kept as run
+// indices in stk[depth * kStride + t]. on_push(k, below_run_index or -1 =
+// persistent top) is called for every push. On return b1 = the persistent
+// part's top. Returns the number of own pushes left.
+constexpr int kTreePC = 8;
+
+template <int kStride>
+struct TreeCache {
+  uint32_t* pos;  // [kTreePC][kStride]
+  double* x;
+  double* y;
+};
+
 template <int kStride, typename OnPush>
 __device__ __forceinline__ int tree_scan_run(int cnt, const double* cx, const double* cy,
-                                             uint32_t& b1, uint32_t& b2,
-                                             const double* __restrict__ R_x,
+                                             uint32_t& b1, const double* __restrict__ R_x,
                                              const double* __restrict__ R_y,
                                              const uint32_t* __restrict__ parent, uint8_t* stk,
-                                             OnPush&& on_push) {
+                                             TreeCache<kStride> pc, OnPush&& on_push) {
   const int t = threadIdx.x;
+  // walk the persistent top into the cache (dependent parent loads, once)
+  int ncached = 0;
+  {
+    uint32_t p = b1;
+    uint32_t pp[kTreePC];
+#pragma unroll
+    for (int d = 0; d < kTreePC; ++d) {
+      pp[d] = p;
+      if (p != kNone) { ncached = d + 1; p = parent[p]; }
+    }
+    double vx[kTreePC], vy[kTreePC];
+#pragma unroll
+    for (int d = 0; d < kTreePC; ++d) {
+      vx[d] = (d < ncached) ? R_x[pp[d]] : 0.0;
+      vy[d] = (d < ncached) ? R_y[pp[d]] : 0.0;
+    }
+#pragma unroll
+    for (int d = 0; d < kTreePC; ++d) {
+      pc.pos[d * kStride + t] = (d < ncached) ? pp[d] : kNone;
+      pc.x[d * kStride + t] = vx[d];
+      pc.y[d * kStride + t] = vy[d];
+    }
+  }
+  // persistent element at depth d (d >= pd: already popped above it)
+  int pd = 0;  // persistent elements popped
+  uint32_t deep = kNone;  // position at depth pd when pd >= ncached (global walk)
+  auto pers_pos = [&](int d) -> uint32_t {  // d in {pd, pd + 1}
+    if (d < kTreePC) return pc.pos[d * kStride + t];
+    return kNone;  // handled by the caller through `deep`
+  };
+  uint32_t p1 = pers_pos(0);
+  uint32_t p2 = (ncached >= 2) ? pers_pos(1) : kNone;
   int top = 0;
   double s1x = 0, s1y = 0, s2x = 0, s2y = 0;
-  if (b1 != kNone) { s1x = R_x[b1]; s1y = R_y[b1]; }
-  if (b2 != kNone) { s2x = R_x[b2]; s2y = R_y[b2]; }
+  if (p1 != kNone) { s1x = pc.x[t]; s1y = pc.y[t]; }
+  if (p2 != kNone) {
+    if (kTreePC >= 2) { s2x = pc.x[kStride + t]; s2y = pc.y[kStride + t]; }
+  }
   for (int k = 0; k < cnt; ++k) {
     const double px = cx[k * kStride + t], py = cy[k * kStride + t];
     while (true) {
-      const bool has2 = (top >= 2) || (top == 1 && b1 != kNone) ||
-                        (top == 0 && b1 != kNone && b2 != kNone);
+      const bool has2 = (top >= 2) || (top == 1 && p1 != kNone) ||
+                        (top == 0 && p1 != kNone && p2 != kNone);
       if (!has2 || left_turn(s2x, s2y, s1x, s1y, px, py)) break;
       if (top >= 1) {
         --top;
-      } else {
-        b1 = b2;
-        b2 = (b1 != kNone) ? parent[b1] : kNone;
+      } else {  // pop the persistent top
+        ++pd;
+        p1 = p2;
+        const int d2 = pd + 1;  // depth of the new second element
+        if (d2 < ncached) {
+          p2 = pc.pos[d2 * kStride + t];
+        } else if (p1 != kNone && d2 >= kTreePC) {
+          p2 = parent[p1];
+          deep = p2;
+        } else {
+          p2 = kNone;
+        }
       }
       s1x = s2x; s1y = s2y;
       if (top >= 2) {
         const int q = stk[(top - 2) * kStride + t];
         s2x = cx[q * kStride + t]; s2y = cy[q * kStride + t];
+      } else if (top == 1) {
+        if (p1 != kNone) {
+          if (pd < kTreePC) { s2x = pc.x[pd * kStride + t]; s2y = pc.y[pd * kStride + t]; }
+          else { s2x = R_x[p1]; s2y = R_y[p1]; }
+        }
       } else {
-        const uint32_t ns = (top == 1) ? b1 : b2;
-        if (ns != kNone) { s2x = R_x[ns]; s2y = R_y[ns]; }
+        if (p2 != kNone) {
+          const int d2 = pd + 1;
+          if (d2 < kTreePC) { s2x = pc.x[d2 * kStride + t]; s2y = pc.y[d2 * kStride + t]; }
+          else { s2x = R_x[p2]; s2y = R_y[p2]; }
+        }
       }
     }
-    on_push(k, top ? (int)stk[(top - 1) * kStride + t] : -1);
+    on_push(k, top ? (int)stk[(top - 1) * kStride + t] : -1, p1);
     stk[top * kStride + t] = (uint8_t)k;
     ++top;
     s2x = s1x; s2y = s1y;
     s1x = px; s1y = py;
   }
+  (void)deep;
+  b1 = p1;
   return top;
 }
+
+// Shared-memory carve-up of one tree kernel: staging (coords, positions,
+// index stack) and the persistent cache, all [element][thread].
+template <int kStride>
+struct TreeSmem {
+  double *cx, *cy;
+  uint32_t* cp;
+  uint8_t* stk;
+  TreeCache<kStride> pc;
+  __device__ explicit TreeSmem(double* base) {
+    cx = base;
+    cy = cx + kTreeChunk * kStride;
+    pc.x = cy + kTreeChunk * kStride;
+    pc.y = pc.x + 8 * kStride;
+    cp = reinterpret_cast<uint32_t*>(pc.y + 8 * kStride);
+    pc.pos = cp + kTreeChunk * kStride;
+    stk = reinterpret_cast<uint8_t*>(pc.pos + 8 * kStride);
+  }
+};
 
 // ---------------------------------------------------------------------------
 // Level 0, many CTAs: chains of the buffer's chunks (thread per chunk).
 constexpr int kTreeCta = 64;
-constexpr size_t kTreeCtaSmem = (size_t)kTreeChunk * kTreeCta * (8 + 8 + 1);
+constexpr size_t kTreeCtaSmem = tree_smem(kTreeCta);
 
 __global__ void __launch_bounds__(kTreeCta) k_gr_local0(uint32_t N, const double* __restrict__ R_x,
                                                        const double* __restrict__ R_y,
                                                        TreeWork w) {
   extern __shared__ __align__(16) double tsm[];
-  double* cx = tsm;
-  double* cy = tsm + kTreeChunk * kTreeCta;
-  uint8_t* stk = reinterpret_cast<uint8_t*>(cy + kTreeChunk * kTreeCta);
+  TreeSmem<kTreeCta> sm(tsm);
+  uint8_t* stk = sm.stk;
   const uint32_t c = blockIdx.x * kTreeCta + threadIdx.x;
   const uint32_t lo = c * kTreeChunk;
   if (lo >= N) return;
   const int cnt = (int)min((uint32_t)kTreeChunk, N - lo);
-  tree_stage<kTreeCta>([&](int k) { return lo + (uint32_t)k; }, cnt, R_x, R_y, cx, cy, nullptr);
-  uint32_t b1 = kNone, b2 = kNone;
-  const int top = tree_scan_run<kTreeCta>(cnt, cx, cy, b1, b2, R_x, R_y, w.parent, stk,
-                                          [](int, int) {});
+  tree_stage<kTreeCta>([&](int k) { return lo + (uint32_t)k; }, cnt, R_x, R_y, sm.cx, sm.cy, nullptr);
+  uint32_t b1 = kNone;
+  const int top = tree_scan_run<kTreeCta>(cnt, sm.cx, sm.cy, b1, R_x, R_y, w.parent, stk, sm.pc,
+                                          [](int, int, uint32_t) {});
   for (int k = 0; k < top; ++k) {
     const uint32_t q = lo + stk[k * kTreeCta + threadIdx.x];
     w.chainq[lo + k] = q;
@@ -207,10 +294,11 @@ __global__ void __launch_bounds__(kTreeThreads, 1) k_gr_mid(
     const double* __restrict__ R_x, const double* __restrict__ R_y, uint32_t N, TreeWork w,
     uint32_t* __restrict__ info) {
   extern __shared__ __align__(16) double tsm[];
-  double* cx = tsm;
-  double* cy = tsm + kTreeChunk * kTreeThreads;
-  uint32_t* cp = reinterpret_cast<uint32_t*>(cy + kTreeChunk * kTreeThreads);
-  uint8_t* stk = reinterpret_cast<uint8_t*>(cp + kTreeChunk * kTreeThreads);
+  TreeSmem<kTreeThreads> sm(tsm);
+  double* cx = sm.cx;
+  double* cy = sm.cy;
+  uint32_t* cp = sm.cp;
+  uint8_t* stk = sm.stk;
   __shared__ uint32_t s_w[32];
   __shared__ uint32_t s_carry;
   __shared__ TreeLevel L[kTreeMaxLevels + 1];
@@ -243,9 +331,9 @@ __global__ void __launch_bounds__(kTreeThreads, 1) k_gr_mid(
           const uint32_t lo = c * kTreeChunk;
           const int cnt = (int)min((uint32_t)kTreeChunk, nq - lo);
           tree_stage<kTreeThreads>([&](int k) { return Q[lo + k]; }, cnt, R_x, R_y, cx, cy, cp);
-          uint32_t b1 = kNone, b2 = kNone;
-          const int top = tree_scan_run<kTreeThreads>(cnt, cx, cy, b1, b2, R_x, R_y, w.parent,
-                                                      stk, [](int, int) {});
+          uint32_t b1 = kNone;
+          const int top = tree_scan_run<kTreeThreads>(cnt, cx, cy, b1, R_x, R_y, w.parent, stk,
+                                                      sm.pc, [](int, int, uint32_t) {});
           for (int k = 0; k < top; ++k) {
             const int e = stk[k * kTreeThreads + t];
             w.chainq[lo + k] = lo + e;
@@ -349,10 +437,9 @@ __global__ void __launch_bounds__(kTreeThreads, 1) k_gr_mid(
         const uint32_t* Qj = hl.Q + c * kTreeChunk;
         tree_stage<kTreeThreads>([&](int k) { return Qj[k]; }, cnt, R_x, R_y, cx, cy, cp);
         uint32_t b1 = hl.bt[c];
-        uint32_t b2 = (b1 != kNone) ? w.parent[b1] : kNone;
         const int top = tree_scan_run<kTreeThreads>(
-            cnt, cx, cy, b1, b2, R_x, R_y, w.parent, stk, [&](int k, int below) {
-              w.parent[cp[k * kTreeThreads + t]] = below >= 0 ? cp[below * kTreeThreads + t] : b1;
+            cnt, cx, cy, b1, R_x, R_y, w.parent, stk, sm.pc, [&](int k, int below, uint32_t ptop) {
+              w.parent[cp[k * kTreeThreads + t]] = below >= 0 ? cp[below * kTreeThreads + t] : ptop;
             });
         ll.bt[cq] = top ? cp[stk[(top - 1) * kTreeThreads + t] * kTreeThreads + t] : b1;
       }
@@ -374,10 +461,11 @@ __global__ void __launch_bounds__(kTreeCta) k_gr_down0(uint32_t N, const double*
                                                       const double* __restrict__ R_y, TreeWork w,
                                                       const uint32_t* __restrict__ info) {
   extern __shared__ __align__(16) double tsm[];
-  double* cx = tsm;
-  double* cy = tsm + kTreeChunk * kTreeCta;
-  uint32_t* cp = reinterpret_cast<uint32_t*>(cy + kTreeChunk * kTreeCta);
-  uint8_t* stk = reinterpret_cast<uint8_t*>(cp + kTreeChunk * kTreeCta);
+  TreeSmem<kTreeCta> sm(tsm);
+  double* cx = sm.cx;
+  double* cy = sm.cy;
+  uint32_t* cp = sm.cp;
+  uint8_t* stk = sm.stk;
   if (info[0] || info[3] < 2) return;  // K == 1: level-0 states come from the top scan
   const uint32_t nch0 = (N + kTreeChunk - 1) / kTreeChunk;
   const uint32_t cq = blockIdx.x * kTreeCta + threadIdx.x;
@@ -392,11 +480,10 @@ __global__ void __launch_bounds__(kTreeCta) k_gr_down0(uint32_t N, const double*
   const int t = threadIdx.x;
   tree_stage<kTreeCta>([&](int k) { return Qj[k]; }, cnt, R_x, R_y, cx, cy, cp);
   uint32_t b1 = bt1[c];
-  uint32_t b2 = (b1 != kNone) ? w.parent[b1] : kNone;
-  const int top = tree_scan_run<kTreeCta>(cnt, cx, cy, b1, b2, R_x, R_y, w.parent, stk,
-                                          [&](int k, int below) {
+  const int top = tree_scan_run<kTreeCta>(cnt, cx, cy, b1, R_x, R_y, w.parent, stk, sm.pc,
+                                          [&](int k, int below, uint32_t ptop) {
                                             w.parent[cp[k * kTreeCta + t]] =
-                                                below >= 0 ? cp[below * kTreeCta + t] : b1;
+                                                below >= 0 ? cp[below * kTreeCta + t] : ptop;
                                           });
   w.btbuf[0][cq] = top ? cp[stk[(top - 1) * kTreeCta + t] * kTreeCta + t] : b1;
 }
@@ -407,9 +494,10 @@ __global__ void __launch_bounds__(kTreeCta) k_gr_cert(uint32_t N, const double* 
                                                      uint32_t* __restrict__ info,
                                                      uint32_t debug_corrupt) {
   extern __shared__ __align__(16) double tsm[];
-  double* cx = tsm;
-  double* cy = tsm + kTreeChunk * kTreeCta;
-  uint8_t* stk = reinterpret_cast<uint8_t*>(cy + kTreeChunk * kTreeCta);
+  TreeSmem<kTreeCta> sm(tsm);
+  double* cx = sm.cx;
+  double* cy = sm.cy;
+  uint8_t* stk = sm.stk;
   if (info[0]) return;
   const uint32_t nch0 = (N + kTreeChunk - 1) / kTreeChunk;
   const uint32_t c = blockIdx.x * kTreeCta + threadIdx.x;
@@ -419,9 +507,8 @@ __global__ void __launch_bounds__(kTreeCta) k_gr_cert(uint32_t N, const double* 
   const int cnt = (int)min((uint32_t)kTreeChunk, N - lo);
   tree_stage<kTreeCta>([&](int k) { return lo + (uint32_t)k; }, cnt, R_x, R_y, cx, cy, nullptr);
   uint32_t b1 = bt[c];
-  uint32_t b2 = (b1 != kNone) ? w.parent[b1] : kNone;
-  const int top =
-      tree_scan_run<kTreeCta>(cnt, cx, cy, b1, b2, R_x, R_y, w.parent, stk, [](int, int) {});
+  const int top = tree_scan_run<kTreeCta>(cnt, cx, cy, b1, R_x, R_y, w.parent, stk, sm.pc,
+                                          [](int, int, uint32_t) {});
   const uint32_t end_top = top ? lo + stk[(top - 1) * kTreeCta + threadIdx.x] : b1;
   uint32_t want = bt[c + 1];
   if (debug_corrupt && c + 1 == nch0) want = bt[c];  // falsified final state

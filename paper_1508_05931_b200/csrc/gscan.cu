@@ -621,7 +621,7 @@ int graham_tree(gscan_handle* h, const double* Rx, const double* Ry, const uint3
   }
   {
     Launch Lk(h, "k_gr_down0");
-    k_gr_down0<<<g0, kTreeCta, kTreeCtaSmem2, h->stream>>>(N, Rx, Ry, w, info);
+    k_gr_down0<<<g0, kTreeCta, kTreeCtaSmem, h->stream>>>(N, Rx, Ry, w, info);
   }
   {
     Launch Lk(h, "k_gr_cert");
@@ -857,7 +857,7 @@ int run_sparse(gscan_handle* h, const double* xs, const double* ys, uint32_t n,
   }
   {
     Launch L(h, "k_sp_cdf");
-    k_sp_cdf<<<1, kSpCells, 0, s>>>(h->sp_cells, h->sp_cdf);
+    k_sp_cdf<<<1, kSpCells / 2, 0, s>>>(h->sp_cells, h->sp_cdf);
   }
   {
     Launch L(h, "k_sp_theta");
@@ -1210,6 +1210,9 @@ int gscan_create(int device, gscan_handle** out) {
     CU(cudaFuncSetAttribute(k_sp_dup_part, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)kSpDupPartSmem));
     CU(cudaFuncSetAttribute(k_gr_mid, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTreeSmem));
+    CU(cudaFuncSetAttribute(k_gr_local0, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTreeCtaSmem));
+    CU(cudaFuncSetAttribute(k_gr_down0, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTreeCtaSmem));
+    CU(cudaFuncSetAttribute(k_gr_cert, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTreeCtaSmem));
     h->sp_grid = h->sm_count;
     return GSCAN_OK;
   };

@@ -125,7 +125,7 @@ struct SpState {
 // (division and glibc atan2 errors, the latter < 1 ulp), and even a cell
 // holding every point moves v by < 1e-5 per 1e-13 of s -- else the exact key
 // is computed and compared with th[].
-constexpr int kSpCells = 1024;
+constexpr int kSpCells = 2048;
 constexpr double kSpGuardV = 1e-4;
 
 __device__ __forceinline__ uint64_t angle_key(double dx, double dy) {
@@ -337,7 +337,7 @@ __device__ __forceinline__ void load_quad(const ExtResult* ext, SpQuad& q) {
 // its round-1 survivors' pseudo-angles counted in kSpCells cells ->
 // piecewise-linear CDF (every cell gets a small floor so it stays strictly
 // increasing) -> th[k] = theta(Finv(k/nb)).
-constexpr uint32_t kSpSample = 1u << 16;
+constexpr uint32_t kSpSample = 1u << 17;
 
 __global__ void __launch_bounds__(1024) k_sp_sample(const double* __restrict__ xs,
                                                     const double* __restrict__ ys, uint32_t n,
@@ -364,13 +364,16 @@ __global__ void __launch_bounds__(1024) k_sp_sample(const double* __restrict__ x
     if (s_cnt[j]) atomicAdd(&cell_cnt[j], s_cnt[j]);
 }
 
-// One CTA of kSpCells threads: inclusive scan of the floored counts -> CDF.
-__global__ void __launch_bounds__(kSpCells) k_sp_cdf(const uint32_t* __restrict__ cell_cnt,
-                                                     double* __restrict__ cdf) {
+// One CTA of kSpCells/2 threads (two cells each): inclusive scan of the
+// floored counts -> CDF.
+__global__ void __launch_bounds__(kSpCells / 2) k_sp_cdf(const uint32_t* __restrict__ cell_cnt,
+                                                         double* __restrict__ cdf) {
   __shared__ double s_w[32];
   const double floor_w = 0.02;  // per-cell floor, in sample units
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double v = (double)cell_cnt[threadIdx.x] + floor_w, x = v;
+  const double a = (double)cell_cnt[2 * threadIdx.x] + floor_w;
+  const double b = (double)cell_cnt[2 * threadIdx.x + 1] + floor_w;
+  double x = a + b;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const double y = __shfl_up_sync(0xffffffffu, x, o);
@@ -389,7 +392,9 @@ __global__ void __launch_bounds__(kSpCells) k_sp_cdf(const uint32_t* __restrict_
   }
   __syncthreads();
   const double incl = x + (warp ? s_w[warp - 1] : 0.0), tot = s_w[31];
-  cdf[threadIdx.x + 1] = (threadIdx.x + 1 == kSpCells) ? 1.0 : incl / tot;
+  const uint32_t j = 2 * threadIdx.x;
+  cdf[j + 1] = (incl - b) / tot;
+  cdf[j + 2] = (j + 2 == kSpCells) ? 1.0 : incl / tot;
   if (threadIdx.x == 0) cdf[0] = 0.0;
 }
 
@@ -1013,14 +1018,134 @@ __device__ bool cta_sort_bucket(const PtRec* __restrict__ R, uint32_t cnt, doubl
   return dup;
 }
 
-// Gathered buckets up to kSpSmallCap points: bitonic CTA sorter with one
-// compare-exchange per thread per stage (512 threads, ~37 KB of shared
-// memory, 4 CTAs per SM); exact positions 1 + bstart[b] + rank in the
-// annotated-buffer space A; records P_l's position. Larger buckets go to the
-// 4096-point sorter.
+// CTA-wide exact sort of one bucket (cnt <= kCap) in O(cnt): the angle keys
+// are spread over cnt sub-buckets by linear interpolation between the
+// bucket's min and max key (monotone in the key, so sub-buckets never invert
+// the order), counted, and every element is ranked against the members of its
+// own sub-bucket (about one) by the total order (angle key, dist2, input
+// index) -- the reference's stable (angle, dist2) order, angular.hpp:154-194.
+// out(rank, x, y, idx) receives every element; returns true when two elements
+// are equal points (annotate's dedup would drop one). Sub-buckets above
+// kSubMax members (clustered keys) flag `slow`: the caller re-sorts bitonically.
+template <uint32_t kCap, typename Out>
+__device__ bool cta_sort_bucket_sub(const PtRec* __restrict__ R, uint32_t cnt, double ax, double ay,
+                                    unsigned char* smem, bool* slow, Out&& out) {
+  constexpr uint32_t kSubMax = 64;
+  uint64_t* s_key = reinterpret_cast<uint64_t*>(smem);
+  double* s_d2 = reinterpret_cast<double*>(s_key + kCap);
+  double* s_x = s_d2 + kCap;
+  double* s_y = s_x + kCap;
+  uint32_t* s_idx = reinterpret_cast<uint32_t*>(s_y + kCap);
+  uint32_t* s_sub = s_idx + kCap;     // element -> sub-bucket
+  uint32_t* s_start = s_sub + kCap;   // sub-bucket counts -> starts (kCap + 1)
+  uint32_t* s_list = s_start + kCap + 1;  // members grouped by sub-bucket
+  __shared__ uint64_t s_kmin, s_kmax;
+  __shared__ uint32_t s_w[32], s_big;
+  if (threadIdx.x == 0) { s_kmin = ~0ull; s_kmax = 0; s_big = 0; }
+  __syncthreads();
+  uint64_t lmin = ~0ull, lmax = 0;
+  for (uint32_t t = threadIdx.x; t < cnt; t += blockDim.x) {
+    const PtRec r = ld_rec256(&R[t]);
+    s_key[t] = r.key;
+    s_x[t] = r.x;
+    s_y[t] = r.y;
+    s_idx[t] = r.idx;
+    s_d2[t] = dist2_rn(__dsub_rn(r.x, ax), __dsub_rn(r.y, ay));
+    lmin = r.key < lmin ? r.key : lmin;
+    lmax = r.key > lmax ? r.key : lmax;
+  }
+  for (uint32_t t = threadIdx.x; t <= cnt; t += blockDim.x) s_start[t] = 0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const uint64_t a2 = __shfl_xor_sync(0xffffffffu, lmin, o), b2 = __shfl_xor_sync(0xffffffffu, lmax, o);
+    lmin = a2 < lmin ? a2 : lmin;
+    lmax = b2 > lmax ? b2 : lmax;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin((unsigned long long*)&s_kmin, (unsigned long long)lmin);
+    atomicMax((unsigned long long*)&s_kmax, (unsigned long long)lmax);
+  }
+  __syncthreads();
+  // keys are non-negative doubles: value order = bit order
+  const double kmin = bitsd(s_kmin), kmax = bitsd(s_kmax);
+  const double scale = (kmax > kmin) ? (double)cnt / (kmax - kmin) : 0.0;
+  for (uint32_t t = threadIdx.x; t < cnt; t += blockDim.x) {
+    uint32_t j = (uint32_t)((bitsd(s_key[t]) - kmin) * scale);
+    j = j < cnt ? j : cnt - 1;
+    s_sub[t] = j;
+    atomicAdd(&s_start[j], 1u);
+  }
+  __syncthreads();
+  // exclusive scan of the sub-bucket counts (CTA-wide, chunked)
+  {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    uint32_t carry = 0;
+    for (uint32_t base = 0; base < cnt; base += blockDim.x) {
+      const uint32_t i = base + threadIdx.x;
+      const uint32_t v = i < cnt ? s_start[i] : 0u;
+      if (v > kSubMax) s_big = 1;
+      uint32_t x = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (lane == 31) s_w[warp] = x;
+      __syncthreads();
+      if (warp == 0) {
+        uint32_t wv = lane < nw ? s_w[lane] : 0u;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, wv, o);
+          if (lane >= o) wv += y;
+        }
+        if (lane < nw) s_w[lane] = wv;
+      }
+      __syncthreads();
+      if (i < cnt) s_start[i] = carry + (warp ? s_w[warp - 1] : 0u) + x - v;
+      carry += s_w[nw - 1];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) s_start[cnt] = carry;
+  }
+  __syncthreads();
+  if (s_big) { *slow = true; return false; }
+  // group members by sub-bucket (order inside a group is irrelevant: ranks
+  // come from comparisons), using s_d2's sign-free spare? no: a cursor copy
+  for (uint32_t t = threadIdx.x; t < cnt; t += blockDim.x) {
+    const uint32_t j = s_sub[t];
+    // claim a slot: the group's first free position (groups are tiny)
+    const uint32_t g0 = s_start[j], g1 = s_start[j + 1];
+    for (uint32_t q = g0; q < g1; ++q)
+      if (atomicCAS(&s_list[q], 0xffffffffu, t) == 0xffffffffu) break;
+  }
+  __syncthreads();
+  bool dup = false;
+  for (uint32_t t = threadIdx.x; t < cnt; t += blockDim.x) {
+    const uint32_t j = s_sub[t];
+    const uint32_t g0 = s_start[j], g1 = s_start[j + 1];
+    const uint64_t kt = s_key[t];
+    const double dt = s_d2[t];
+    const uint32_t it = s_idx[t];
+    uint32_t r = g0;
+    for (uint32_t q = g0; q < g1; ++q) {
+      const uint32_t u = s_list[q];
+      if (u == t) continue;
+      r += key_less(s_key[u], s_d2[u], s_idx[u], kt, dt, it);
+      dup |= (s_key[u] == kt && s_d2[u] == dt && s_x[u] == s_x[t] && s_y[u] == s_y[t]);
+    }
+    out(r, s_x[t], s_y[t], it);
+  }
+  return dup;
+}
+
+// Gathered buckets up to kSpSmallCap points (CTA per bucket, sub-bucket sort,
+// 4 CTAs per SM); clustered or larger buckets go to the bitonic sorter.
+// Exact positions 1 + bstart[b] + rank in the annotated-buffer space A;
+// records P_l's position.
 constexpr uint32_t kSpSmallCap = 1024;
-constexpr int kSpSmallThreads = 512;
-constexpr size_t kSpSmallSmem = (size_t)kSpSmallCap * (8 + 8 + 8 + 8 + 4 + 2);
+constexpr int kSpSmallThreads = 256;
+constexpr size_t kSpSmallSmem = (size_t)kSpSmallCap * (8 + 8 + 8 + 8 + 4 + 4 + 4 + 4) + 16;
 
 __global__ void __launch_bounds__(kSpSmallThreads) k_sp_sort_gathered(
     const uint32_t* __restrict__ glist, const uint32_t* __restrict__ bstart,
@@ -1032,6 +1157,8 @@ __global__ void __launch_bounds__(kSpSmallThreads) k_sp_sort_gathered(
   if (st->fail) return;
   const uint32_t ngb = st->n_gb, l_idx = st->l_idx;
   const double ax = ext->ax, ay = ext->ay;
+  uint32_t* s_list = reinterpret_cast<uint32_t*>(smem + (size_t)kSpSmallCap * (8 + 8 + 8 + 8 + 4 + 4)) +
+                     kSpSmallCap + 1;
   for (uint32_t g = blockIdx.x; g < ngb; g += gridDim.x) {
     const uint32_t b = glist[g];
     const uint32_t s0 = bstart[b], cnt = hist[b];
@@ -1044,14 +1171,21 @@ __global__ void __launch_bounds__(kSpSmallThreads) k_sp_sort_gathered(
       if (threadIdx.x == 0) big[atomicAdd(&st->n_bigg, 1u)] = b;
       continue;
     }
-    const bool dup = cta_sort_bucket<kSpSmallCap>(rec + s0, cnt, ax, ay, smem,
-                                                  [&](uint32_t r, double x, double y, uint32_t idx) {
+    __syncthreads();
+    for (uint32_t t = threadIdx.x; t < cnt; t += blockDim.x) s_list[t] = 0xffffffffu;
+    bool slow = false;
+    const bool dup = cta_sort_bucket_sub<kSpSmallCap>(rec + s0, cnt, ax, ay, smem, &slow,
+                                                      [&](uint32_t r, double x, double y, uint32_t idx) {
       const uint32_t pos = 1 + s0 + r;
       A_x[pos] = x;
       A_y[pos] = y;
       A_i[pos] = idx;
       if (idx == l_idx) st->l_check = pos;
     });
+    if (slow) {
+      if (threadIdx.x == 0) big[atomicAdd(&st->n_bigg, 1u)] = b;
+      continue;
+    }
     if (dup) atomicOr(&st->fail, kSpFailDup);
   }
 }
