@@ -31,10 +31,11 @@
 
 namespace gscan {
 
-constexpr int kTreeChunk = 32;      // points per chunk (each scan is ~200 cycles per step)
+constexpr int kTreeChunk = 32;      // level-0 chunk (many CTAs); also the staging capacity
+constexpr int kTreeChunkHi = 32;    // chunk of levels >= 1 (8 measured slower: shrink ~1.6x/level)
 constexpr int kTreeThreads = 256;   // one CTA; chunks are processed in waves of this many
 constexpr uint32_t kTreeTop = 128;  // largest top-level list for the single-thread scan
-constexpr int kTreeMaxLevels = 16;
+constexpr int kTreeMaxLevels = 32;
 // shared memory: per thread a chunk's coordinates [k][t] and an index stack
 // per-thread slot: chunk coordinates + positions (21 B per point) + the
 // persistent-stack cache (20 B per cached element)
@@ -304,6 +305,7 @@ __global__ void __launch_bounds__(kTreeThreads, 1) k_gr_mid(
   __shared__ TreeLevel L[kTreeMaxLevels + 1];
   __shared__ int s_K, s_bad;
   const int t = threadIdx.x;
+  long long t_start = clock64();
   if (t == 0) {
     L[0].Q = nullptr;
     L[0].up = nullptr;
@@ -316,7 +318,8 @@ __global__ void __launch_bounds__(kTreeThreads, 1) k_gr_mid(
   __syncthreads();
   for (int j = 0; j < kTreeMaxLevels; ++j) {
     const uint32_t nq = L[j].nq;
-    const uint32_t nch = (nq + kTreeChunk - 1) / kTreeChunk;
+    const uint32_t cs = (j == 0) ? kTreeChunk : kTreeChunkHi;
+    const uint32_t nch = (nq + cs - 1) / cs;
     if (t == 0) {
       L[j].nch = nch;
       L[j].off = w.offbuf[j];
@@ -328,8 +331,8 @@ __global__ void __launch_bounds__(kTreeThreads, 1) k_gr_mid(
       for (uint32_t c0 = 0; c0 < nch; c0 += kTreeThreads) {
         const uint32_t c = c0 + t;
         if (c < nch) {
-          const uint32_t lo = c * kTreeChunk;
-          const int cnt = (int)min((uint32_t)kTreeChunk, nq - lo);
+          const uint32_t lo = c * cs;
+          const int cnt = (int)min(cs, nq - lo);
           tree_stage<kTreeThreads>([&](int k) { return Q[lo + k]; }, cnt, R_x, R_y, cx, cy, cp);
           uint32_t b1 = kNone;
           const int top = tree_scan_run<kTreeThreads>(cnt, cx, cy, b1, R_x, R_y, w.parent, stk,
@@ -348,7 +351,7 @@ __global__ void __launch_bounds__(kTreeThreads, 1) k_gr_mid(
     if (t == 0) {
       L[j].off[nch] = total;
       const bool shrink =
-          (j == 0) ? (total * 5ull <= (uint64_t)nq * 3) : (total * 5ull <= (uint64_t)nq * 4);
+          (j == 0) ? (total * 20ull <= (uint64_t)nq * 17) : (total * 10ull <= (uint64_t)nq * 9);
       if (!shrink || total > w.cap[j + 1] || j + 1 > kTreeMaxLevels - 1) s_bad = 1;
       L[j + 1].Q = w.Qbuf[j + 1];
       L[j + 1].up = w.upbuf[j + 1];
@@ -362,8 +365,8 @@ __global__ void __launch_bounds__(kTreeThreads, 1) k_gr_mid(
         uint32_t qv[8], pv[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-          qv[u] = (k0 + u < ln) ? w.chainq[c * kTreeChunk + k0 + u] : 0u;
-          pv[u] = (k0 + u < ln) ? w.chainp[c * kTreeChunk + k0 + u] : 0u;
+          qv[u] = (k0 + u < ln) ? w.chainq[c * cs + k0 + u] : 0u;
+          pv[u] = (k0 + u < ln) ? w.chainp[c * cs + k0 + u] : 0u;
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u)
@@ -382,6 +385,10 @@ __global__ void __launch_bounds__(kTreeThreads, 1) k_gr_mid(
     if (t == 0) { info[0] = 1; info[3] = 0; }
     return;
   }
+  if (t == 0) {
+    info[8] = (uint32_t)(clock64() - t_start);
+    for (int j = 0; j <= K && j < 6; ++j) info[10 + j] = L[j].nq;
+  }
   // ---- top: one thread over Q_K, staged in shared memory by all ----
   {
     const TreeLevel& tl = L[K];
@@ -393,7 +400,7 @@ __global__ void __launch_bounds__(kTreeThreads, 1) k_gr_mid(
     for (uint32_t k = t; k < nk; k += kTreeThreads) {
       const uint32_t p = tl.Q[k];
       s_p[k] = p;
-      s_ch[k] = tl.up[k] / kTreeChunk;
+      s_ch[k] = tl.up[k] / (K - 1 == 0 ? kTreeChunk : kTreeChunkHi);
       cx[k] = R_x[p];
       cy[k] = R_y[p];
     }
@@ -424,6 +431,7 @@ __global__ void __launch_bounds__(kTreeThreads, 1) k_gr_mid(
     }
     __syncthreads();
   }
+  if (t == 0) info[9] = (uint32_t)(clock64() - t_start);
   // ---- down: level j -> j-1, for j >= 2 (level 1 -> 0 runs on many CTAs) ----
   for (int j = K - 1; j >= 2; --j) {
     const TreeLevel& hl = L[j];
@@ -432,9 +440,9 @@ __global__ void __launch_bounds__(kTreeThreads, 1) k_gr_mid(
       const uint32_t cq = c0 + t;
       if (cq < ll.nch) {
         const uint32_t e = ll.off[cq];
-        const uint32_t c = e / kTreeChunk;
-        const int cnt = (int)(e - c * kTreeChunk);
-        const uint32_t* Qj = hl.Q + c * kTreeChunk;
+        const uint32_t c = e / kTreeChunkHi;  // level j >= 2 > 0
+        const int cnt = (int)(e - c * kTreeChunkHi);
+        const uint32_t* Qj = hl.Q + c * kTreeChunkHi;
         tree_stage<kTreeThreads>([&](int k) { return Qj[k]; }, cnt, R_x, R_y, cx, cy, cp);
         uint32_t b1 = hl.bt[c];
         const int top = tree_scan_run<kTreeThreads>(
@@ -453,6 +461,7 @@ __global__ void __launch_bounds__(kTreeThreads, 1) k_gr_mid(
     // else the level-0 boundary after the last chunk is the final top
     if (K >= 2) w.btbuf[0][(N + kTreeChunk - 1) / kTreeChunk] = L[1].bt[L[1].nch];
     info[3] = K;
+    info[16] = (uint32_t)(clock64() - t_start);
   }
 }
 
@@ -474,9 +483,9 @@ __global__ void __launch_bounds__(kTreeCta) k_gr_down0(uint32_t N, const double*
   const uint32_t* bt1 = w.btbuf[1];
   const uint32_t* Q1 = w.Qbuf[1];
   const uint32_t e = off0[cq];
-  const uint32_t c = e / kTreeChunk;
-  const int cnt = (int)(e - c * kTreeChunk);
-  const uint32_t* Qj = Q1 + c * kTreeChunk;
+  const uint32_t c = e / kTreeChunkHi;  // chunks of Q_1
+  const int cnt = (int)(e - c * kTreeChunkHi);
+  const uint32_t* Qj = Q1 + c * kTreeChunkHi;
   const int t = threadIdx.x;
   tree_stage<kTreeCta>([&](int k) { return Qj[k]; }, cnt, R_x, R_y, cx, cy, cp);
   uint32_t b1 = bt1[c];
@@ -513,10 +522,17 @@ __global__ void __launch_bounds__(kTreeCta) k_gr_cert(uint32_t N, const double* 
   uint32_t want = bt[c + 1];
   if (debug_corrupt && c + 1 == nch0) want = bt[c];  // falsified final state
   bool ok = want == end_top;
-  for (int k = 0; k < top && ok; ++k) {
-    const uint32_t p = lo + stk[k * kTreeCta + threadIdx.x];
-    const uint32_t below = k ? lo + stk[(k - 1) * kTreeCta + threadIdx.x] : b1;
-    ok = w.parent[p] == below;
+  // surviving pushes must link as in parent[] (loads issued 8 at a time)
+  for (int k0 = 0; k0 < top && ok; k0 += 8) {
+    uint32_t lk[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      lk[u] = (k0 + u < top) ? w.parent[lo + stk[(k0 + u) * kTreeCta + threadIdx.x]] : 0u;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int k = k0 + u;
+      if (k < top) ok = ok && lk[u] == (k ? lo + stk[(k - 1) * kTreeCta + threadIdx.x] : b1);
+    }
   }
   if (!ok) atomicAdd(&info[2], 1u);
 }

@@ -38,9 +38,25 @@ struct KernelTime {
 
 }  // namespace
 
+struct SpGraphKey {
+  const double* xs = nullptr;
+  const double* ys = nullptr;
+  uint32_t n = 0;
+  uint64_t chunks = 0;
+  uint32_t debug = 0;
+  bool dup = true;
+  bool operator==(const SpGraphKey& o) const {
+    return xs == o.xs && ys == o.ys && n == o.n && chunks == o.chunks && debug == o.debug &&
+           dup == o.dup;
+  }
+};
+
 struct gscan_handle {
   int device = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t side = nullptr;          // duplicate check runs here, overlapping the tail
+  cudaStream_t cap_stream = nullptr;    // CUDA graph capture
+  cudaEvent_t ev_f3 = nullptr, ev_dup = nullptr;
   bool own_stream = false;
   int sm_count = 148;
   uint64_t cap = 0;  // points
@@ -98,9 +114,17 @@ struct gscan_handle {
   uint32_t* sp_bigg = nullptr;   // gathered buckets for the CTA sorter
   uint32_t *sp_gcount = nullptr, *sp_ccount = nullptr, *sp_hcount = nullptr;  // per-CTA emissions
   uint64_t* sp_dup2 = nullptr;   // partitioned hash list (n)
+  uint64_t* sp_side_status = nullptr;  // look-back status of the side stream's scan
+  Counters* sp_side_ticket = nullptr;
   bool sp_debug = false, sp_no_dup = false;
+  // captured CUDA graph of the sparse path (sparse_enqueue)
+  bool use_graphs = true, sp_graph_ok = false;
+  cudaGraphExec_t sp_graph_exec = nullptr;
+  SpGraphKey sp_key{};
+  uint64_t sp_graph_launches = 0;
   uint32_t sp_cert = 0;
   uint16_t* sp_codes = nullptr;  // per-point bucket code (n)
+  float* sp_phi32 = nullptr;     // per-point walk angle from F3 (n)
   uint32_t *sp_hist_part = nullptr, *sp_phi_part = nullptr, *sp_part_off = nullptr;
   SpD2* sp_d2 = nullptr;
   uint32_t *sp_hist = nullptr, *sp_bstart = nullptr, *sp_gbits = nullptr, *sp_glist = nullptr,
@@ -147,6 +171,7 @@ void dfree(T*& p) {
 }
 
 void free_buffers(gscan_handle* h) {
+  h->sp_graph_ok = false;
   dfree(h->d_xs); dfree(h->d_ys); dfree(h->surv); dfree(h->keys); dfree(h->rank);
   dfree(h->rec); dfree(h->A_x); dfree(h->A_y); dfree(h->A_i); dfree(h->C_x); dfree(h->C_y);
   dfree(h->C_i); dfree(h->flags); dfree(h->stack); dfree(h->d_out); dfree(h->status);
@@ -156,7 +181,7 @@ void free_buffers(gscan_handle* h) {
   dfree(h->g_keep); dfree(h->g_misc);
   dfree(h->g_stA); dfree(h->g_stB); dfree(h->g_lenA); dfree(h->g_lenB); dfree(h->g_scr);
   dfree(h->sp_eb); dfree(h->sp_Wb); dfree(h->sp_Ws); dfree(h->sp_Rb); dfree(h->sp_Rs); dfree(h->sp_dup);
-  dfree(h->sp_codes); dfree(h->sp_dup2); dfree(h->gt_pool);
+  dfree(h->sp_codes); dfree(h->sp_phi32); dfree(h->sp_dup2); dfree(h->gt_pool);
   h->gt_cap = 0;
   h->g_st_cap = 0;
   h->g_len_cap = 0;
@@ -213,7 +238,7 @@ int reserve(gscan_handle* h, uint64_t n) {
   CU(cudaMalloc(&h->g_je, nch * 4));
   CU(cudaMalloc(&h->g_jmin, nch * 4));
   CU(cudaMalloc(&h->g_keep, nch * 4));
-  CU(cudaMalloc(&h->g_misc, 64));
+  CU(cudaMalloc(&h->g_misc, 256));
   const uint64_t tiles = std::max((m + kCompactTile - 1) / kCompactTile,
                                   (uint64_t)(nb + 2 + kScanTile - 1) / kScanTile) + 64;
   h->status_cap = tiles;
@@ -226,6 +251,7 @@ int reserve(gscan_handle* h, uint64_t n) {
   CU(cudaMalloc(&h->sp_dup, (m + 4096) * 8));
   CU(cudaMalloc(&h->sp_dup2, (m + 4096) * 8));
   CU(cudaMalloc(&h->sp_codes, (m + 1) * sizeof(uint16_t)));
+  CU(cudaMalloc(&h->sp_phi32, (m + 1) * sizeof(float)));
   h->cap = n;
   return GSCAN_OK;
 }
@@ -235,7 +261,9 @@ struct Launch {
   gscan_handle* h;
   const char* name;
   KernelTime* kt = nullptr;
-  Launch(gscan_handle* hh, const char* nm) : h(hh), name(nm) {
+  cudaStream_t st;
+  Launch(gscan_handle* hh, const char* nm, cudaStream_t s = nullptr)
+      : h(hh), name(nm), st(s ? s : hh->stream) {
     ++h->launches;
     if (h->profiling) {
       if (h->kt_used == h->ktimes.size()) {
@@ -246,11 +274,11 @@ struct Launch {
       }
       kt = &h->ktimes[h->kt_used++];
       kt->name = nm;
-      cudaEventRecord(kt->a, h->stream);
+      cudaEventRecord(kt->a, st);
     }
   }
   ~Launch() {
-    if (kt) cudaEventRecord(kt->b, h->stream);
+    if (kt) cudaEventRecord(kt->b, st);
   }
 };
 
@@ -579,10 +607,10 @@ int graham_tree(gscan_handle* h, const double* Rx, const double* Ry, const uint3
   uint64_t need = 4ull * N + (N / kTreeChunk + 64) + kTreeTop + 64;
   caps[0] = N;
   for (int j = 1; j <= kTreeMaxLevels; ++j) {
-    caps[j] = (j == 1 ? (uint64_t)N * 3 / 5 : caps[j - 1] * 4 / 5) + 64;
-    need += 2 * caps[j] + 2 * (caps[j - 1] / kTreeChunk + 64) + 128;
+    caps[j] = (j == 1 ? (uint64_t)N * 17 / 20 : caps[j - 1] * 9 / 10) + 64;
+    need += 2 * caps[j] + 2 * (caps[j - 1] / kTreeChunkHi + 64) + 128;
   }
-  need += 2 * (caps[kTreeMaxLevels] / kTreeChunk + 64) + 128;
+  need += 2 * (caps[kTreeMaxLevels] / kTreeChunkHi + 64) + 128;
   if (need > h->gt_cap) {
     dfree(h->gt_pool);
     CU(cudaMalloc(&h->gt_pool, need * 4));
@@ -604,8 +632,8 @@ int graham_tree(gscan_handle* h, const double* Rx, const double* Ry, const uint3
       w.Qbuf[j] = take(caps[j]);
       w.upbuf[j] = take(caps[j]);
     }
-    w.offbuf[j] = take(caps[j] / kTreeChunk + 64);
-    w.btbuf[j] = take(caps[j] / kTreeChunk + 64);
+    w.offbuf[j] = take(caps[j] / (j == 0 ? kTreeChunk : kTreeChunkHi) + 64);
+    w.btbuf[j] = take(caps[j] / (j == 0 ? kTreeChunk : kTreeChunkHi) + 64);
   }
   uint32_t* info = h->g_misc + 4;
   const uint32_t nch0 = (N + kTreeChunk - 1) / kTreeChunk;
@@ -632,9 +660,13 @@ int graham_tree(gscan_handle* h, const double* Rx, const double* Ry, const uint3
     k_gr_emit<<<1, 1024, 0, h->stream>>>(N, Rx, Ry, Ri, w, info, h->d_out, h->ctr);
   }
   CU(cudaGetLastError());
-  uint32_t hi[3];
-  CU(cudaMemcpyAsync(hi, info, 12, cudaMemcpyDeviceToHost, h->stream));
+  uint32_t hi[17];
+  CU(cudaMemcpyAsync(hi, info, sizeof hi, cudaMemcpyDeviceToHost, h->stream));
   CU(cudaStreamSynchronize(h->stream));
+  if (h->sp_debug)
+    fprintf(stderr, "[tree] N=%u K=%u sizes=%u,%u,%u,%u,%u,%u.. cycles: up=%u top=%u down=%u fails=%u\n",
+            N, hi[3], hi[10], hi[11], hi[12], hi[13], hi[14], hi[15], hi[8], hi[9] - hi[8],
+            hi[16] - hi[9], hi[2]);
   if (hi[0]) return GSCAN_OK;  // no shrink
   h->graham_fails = hi[2];
   h->graham_path = 8 | (hi[2] ? 4 : 0);
@@ -793,6 +825,8 @@ int sparse_init(gscan_handle* h) {
   CU(cudaMalloc(&h->sp_big, nb * 4));
   CU(cudaMalloc(&h->sp_bigg, nb * 4));
   CU(cudaMalloc(&h->sp_gcount, G * 4));
+  CU(cudaMalloc(&h->sp_side_status, ((kSpParts * G + 1 + kScanTile - 1) / kScanTile + 64) * 8));
+  CU(cudaMalloc(&h->sp_side_ticket, sizeof(Counters)));
   CU(cudaMalloc(&h->sp_ccount, G * 4));
   CU(cudaMalloc(&h->sp_hcount, G * 4));
   h->sp_debug = getenv("GSCAN_SP_DEBUG") != nullptr;
@@ -813,30 +847,34 @@ int sparse_init(gscan_handle* h) {
   return GSCAN_OK;
 }
 
-int run_sparse(gscan_handle* h, const double* xs, const double* ys, uint32_t n,
-               const gscan_config& cfg, uint64_t* hull_size, gscan_stats* st, bool* ok) {
-  *ok = false;
-  TRY(sparse_init(h));
-  ++h->sp_calls;
+// Event record usable inside stream capture (as an external event node, so
+// elapsed times still work after graph launches) and outside of it.
+int rec_event(gscan_handle* h, cudaEvent_t e, cudaStream_t s) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  CU(cudaStreamIsCapturing(s, &cs));
+  if (cs == cudaStreamCaptureStatusActive) CU(cudaEventRecordWithFlags(e, s, cudaEventRecordExternal));
+  else CU(cudaEventRecord(e, s));
+  return GSCAN_OK;
+}
+
+// Enqueues the whole sparse path up to and including the verification and the
+// duplicate check's join, plus the SpState read-back: no host round trip
+// inside, fixed launch shapes for a given (input, n, config), so run_sparse
+// replays it as one captured CUDA graph.
+int sparse_enqueue(gscan_handle* h, const double* xs, const double* ys, uint32_t n,
+                   const gscan_config& cfg) {
   const uint32_t nb = kSpBuckets;
   const uint32_t G = (uint32_t)h->sp_grid;
   const bool vec = aligned16(xs) && aligned16(ys);
   const bool drop = (h->debug & GSCAN_DEBUG_SPARSE_DROP) != 0;
   const uint64_t c = cfg.chunk_count;
   const uint64_t nslices = 2 * std::min<uint64_t>(c, n);
-  if (nslices + 2 > h->sp_seg_cap) {
-    dfree(h->sp_seglo);
-    dfree(h->sp_seghi);
-    CU(cudaMalloc(&h->sp_seglo, (nslices + 2) * 4));
-    CU(cudaMalloc(&h->sp_seghi, (nslices + 2) * 4));
-    h->sp_seg_cap = nslices + 2;
-  }
   // per-CTA emission region: bound on the points one streaming CTA visits
   const uint32_t nth = G * (uint32_t)kSpThreads;
   const uint32_t cap = 2u * (uint32_t)kSpThreads * ((n / 2 + nth - 1) / nth) + 2;
   const size_t smem_nb = (size_t)nb * 4;
   cudaStream_t s = h->stream;
-  CU(cudaEventRecord(h->ev[0], s));
+  TRY(rec_event(h, h->ev[0], s));
   CU(cudaMemsetAsync(h->ctr, 0, sizeof(Counters), s));
   CU(cudaMemsetAsync(h->sp_st, 0, sizeof(SpState), s));
   CU(cudaMemsetAsync(h->sp_gcnt, 0, nb * 4, s));
@@ -896,12 +934,12 @@ int run_sparse(gscan_handle* h, const double* xs, const double* ys, uint32_t n,
     k_sp_gbits<<<(nb / 32 + 255) / 256, 256, 0, s>>>(h->sp_bstart, h->sp_st, h->sp_gbits,
                                                      h->sp_glist);
   }
-  CU(cudaEventRecord(h->ev[1], s));
+  TRY(rec_event(h, h->ev[1], s));
   // F3 -> G in (surv, sp_eb), hash lists in sp_dup
   {
     Launch L(h, "k_sp_phi");
 #define A3 xs, ys, h->sp_codes, n, cap, h->ext, h->sp_gbits, h->sp_st, h->sp_phi_part, h->surv, \
-           h->sp_eb, h->sp_gcount, h->sp_dup, h->sp_hcount, h->sp_part_off
+           h->sp_eb, h->sp_gcount, h->sp_dup, h->sp_hcount, h->sp_part_off, h->sp_phi32
     if (vec) k_sp_phi<true><<<G, kSpThreads, smem_nb, s>>>(A3);
     else k_sp_phi<false><<<G, kSpThreads, smem_nb, s>>>(A3);
 #undef A3
@@ -912,15 +950,27 @@ int run_sparse(gscan_handle* h, const double* xs, const double* ys, uint32_t n,
   }
   const bool dup_check = !h->sp_no_dup;
   if (dup_check) {
-    TRY(scan_u32(h, h->sp_part_off, kSpParts * G, h->sp_part_off));
+    // side stream: partition the hash lists and look for equal hashes while
+    // the main stream sorts, walks and scans; joined before the result counts
+    CU(cudaEventRecord(h->ev_f3, s));
+    CU(cudaStreamWaitEvent(h->side, h->ev_f3, 0));
     {
-      Launch L(h, "k_sp_dup_part");
-      k_sp_dup_part<<<G, 1024, kSpDupPartSmem, s>>>(h->sp_dup, h->sp_hcount, cap, h->sp_part_off,
-                                                    h->sp_st, h->sp_dup2);
+      const uint64_t tiles = ((uint64_t)kSpParts * G + 1 + kScanTile - 1) / kScanTile;
+      CU(cudaMemsetAsync(h->sp_side_status, 0, tiles * 8, h->side));
+      CU(cudaMemsetAsync(h->sp_side_ticket, 0, sizeof(Counters), h->side));
+      Launch L(h, "k_scan_u32(side)", h->side);
+      k_scan_u32<<<tiles, kBlock, 0, h->side>>>(h->sp_part_off, kSpParts * G, h->sp_part_off,
+                                               h->sp_side_status, h->sp_side_ticket);
     }
     {
-      Launch L(h, "k_sp_dups");
-      k_sp_dups<<<kSpParts, 512, kSpDupSlots * 8, s>>>(h->sp_dup2, h->sp_part_off, G, h->sp_st);
+      Launch L(h, "k_sp_dup_part", h->side);
+      k_sp_dup_part<<<G, 1024, kSpDupPartSmem, h->side>>>(h->sp_dup, h->sp_hcount, cap,
+                                                          h->sp_part_off, h->sp_st, h->sp_dup2);
+    }
+    {
+      Launch L(h, "k_sp_dups", h->side);
+      k_sp_dups<<<kSpParts, 512, kSpDupSlots * 8, h->side>>>(h->sp_dup2, h->sp_part_off, G,
+                                                             h->sp_st);
     }
   }
   {
@@ -937,7 +987,7 @@ int run_sparse(gscan_handle* h, const double* xs, const double* ys, uint32_t n,
   }
   {
     Launch L(h, "k_sp_sort_gathered_big");
-    k_sp_sort_gathered_big<<<h->sm_count, kSpSortThreads, kSpSortSmem, s>>>(
+    k_sp_sort_gathered_big<<<h->sm_count, kSpSortThreads, kSpBigSmem, s>>>(
         h->sp_bigg, h->sp_bstart, h->sp_hist, h->rec, h->ext, h->sp_st, h->A_x, h->A_y, h->A_i);
   }
   {
@@ -946,15 +996,13 @@ int run_sparse(gscan_handle* h, const double* xs, const double* ys, uint32_t n,
         h->sp_st, h->sp_bstart, h->sp_gbits, h->sp_phimax, h->A_x, h->A_y, h->ext, h->sp_prefmax,
         h->sp_slice);
   }
-  CU(cudaEventRecord(h->ev[2], s));
+  TRY(rec_event(h, h->ev[2], s));
   // F4 -> C in (surv, sp_eb); codes of candidates marked
   {
     Launch L(h, "k_sp_cand");
-#define A4 xs, ys, h->sp_codes, n, cap, h->ext, h->sp_gbits, h->sp_prefmax, h->sp_st, h->surv, \
-           h->sp_eb, h->sp_ccount, drop
-    if (vec) k_sp_cand<true><<<G, kSpThreads, smem_nb, s>>>(A4);
-    else k_sp_cand<false><<<G, kSpThreads, smem_nb, s>>>(A4);
-#undef A4
+    k_sp_cand<<<G, kSpThreads, smem_nb, s>>>(h->sp_codes, h->sp_phi32, n, cap, h->sp_gbits,
+                                             h->sp_prefmax, h->sp_st, h->surv, h->sp_eb,
+                                             h->sp_ccount, drop);
   }
   {
     Launch L(h, "k_sp_rank_c");
@@ -982,7 +1030,7 @@ int run_sparse(gscan_handle* h, const double* xs, const double* ys, uint32_t n,
   }
   {
     Launch L(h, "k_sp_sort_cand_big");
-    k_sp_sort_cand_big<<<h->sm_count, kSpSortThreads, kSpSortSmem, s>>>(
+    k_sp_sort_cand_big<<<h->sm_count, kSpSortThreads, kSpBigSmem, s>>>(
         h->sp_big, h->rec, h->sp_cstart, h->sp_wstart, h->sp_slice, h->ext, h->sp_st, h->C_x,
         h->C_y, h->C_i, h->sp_Wb, h->sp_Ws, h->flags);
   }
@@ -992,7 +1040,7 @@ int run_sparse(gscan_handle* h, const double* xs, const double* ys, uint32_t n,
         h->sp_glist, h->sp_bstart, h->sp_hist, h->sp_wstart, h->A_x, h->A_y, h->A_i, h->ext,
         h->sp_st, h->C_x, h->C_y, h->C_i, h->sp_Wb, h->sp_Ws, h->flags);
   }
-  CU(cudaEventRecord(h->ev[3], s));
+  TRY(rec_event(h, h->ev[3], s));
   {
     Launch L(h, "k_sp_segments");
     k_sp_segments<<<h->sm_count * 8, kBlock, 0, s>>>(h->sp_Ws, h->sp_st, h->sp_seglo, h->sp_seghi);
@@ -1029,10 +1077,76 @@ int run_sparse(gscan_handle* h, const double* xs, const double* ys, uint32_t n,
     else k_sp_verify<false><<<G, kSpThreads, smem_nb + 4, s>>>(A6);
 #undef A6
   }
-  CU(cudaGetLastError());
-  CU(cudaEventRecord(h->ev[4], s));
+  if (dup_check) {
+    CU(cudaEventRecord(h->ev_dup, h->side));
+    CU(cudaStreamWaitEvent(s, h->ev_dup, 0));  // the duplicate check joins here
+  }
+  TRY(rec_event(h, h->ev[4], s));
   CU(cudaMemcpyAsync(h->h_sp, h->sp_st, sizeof(SpState), cudaMemcpyDeviceToHost, s));
   CU(cudaMemcpyAsync(&h->ctr->n2, &h->sp_st->n_r, 4, cudaMemcpyDeviceToDevice, s));
+  return GSCAN_OK;
+}
+
+int run_sparse(gscan_handle* h, const double* xs, const double* ys, uint32_t n,
+               const gscan_config& cfg, uint64_t* hull_size, gscan_stats* st, bool* ok) {
+  *ok = false;
+  TRY(sparse_init(h));
+  ++h->sp_calls;
+  const uint64_t c = cfg.chunk_count;
+  const uint64_t nslices = 2 * std::min<uint64_t>(c, n);
+  if (nslices + 2 > h->sp_seg_cap) {
+    dfree(h->sp_seglo);
+    dfree(h->sp_seghi);
+    CU(cudaMalloc(&h->sp_seglo, (nslices + 2) * 4));
+    CU(cudaMalloc(&h->sp_seghi, (nslices + 2) * 4));
+    h->sp_seg_cap = nslices + 2;
+    h->sp_graph_ok = false;
+  }
+  cudaStream_t s = h->stream;
+  const bool dup_check = !h->sp_no_dup;
+  // one captured graph per (input, n, config): replayed while unchanged
+  const SpGraphKey key{xs, ys, n, c, h->debug, dup_check};
+  if (h->profiling || !h->use_graphs) {
+    TRY(sparse_enqueue(h, xs, ys, n, cfg));
+  } else {
+    if (!h->sp_graph_ok || !(key == h->sp_key)) {
+      if (h->sp_graph_exec) { cudaGraphExecDestroy(h->sp_graph_exec); h->sp_graph_exec = nullptr; }
+      h->sp_graph_ok = false;
+      const uint64_t l0 = h->launches;
+      // capture on the handle's private stream (the caller's stream may be
+      // the legacy default stream, which cannot be captured)
+      h->stream = h->cap_stream;
+      cudaError_t be = cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeRelaxed);
+      int rc = (be == cudaSuccess) ? sparse_enqueue(h, xs, ys, n, cfg) : GSCAN_E_CUDA;
+      cudaGraph_t graph = nullptr;
+      const cudaError_t ce = (be == cudaSuccess) ? cudaStreamEndCapture(h->stream, &graph) : be;
+      h->stream = s;
+      cudaError_t ie = cudaErrorUnknown;
+      if (rc == GSCAN_OK && ce == cudaSuccess) {
+        ie = cudaGraphInstantiate(&h->sp_graph_exec, graph, 0);
+      }
+      if (graph) cudaGraphDestroy(graph);
+      if (rc != GSCAN_OK || ce != cudaSuccess || ie != cudaSuccess) {
+        // capture unavailable here: run without graphs from now on
+        cudaGetLastError();
+        if (h->sp_debug)
+          fprintf(stderr, "[sparse] graph capture disabled: %s / %s / %s\n", h->err.c_str(),
+                  cudaGetErrorString(ce), cudaGetErrorString(ie));
+        h->use_graphs = false;
+        h->launches = l0;
+        if (h->sp_graph_exec) { cudaGraphExecDestroy(h->sp_graph_exec); h->sp_graph_exec = nullptr; }
+        TRY(sparse_enqueue(h, xs, ys, n, cfg));
+        goto enqueued;
+      }
+      h->sp_graph_launches = h->launches - l0;
+      h->launches = l0;
+      h->sp_key = key;
+      h->sp_graph_ok = true;
+    }
+    CU(cudaGraphLaunch(h->sp_graph_exec, s));
+    h->launches += h->sp_graph_launches;
+  }
+enqueued:
   TRY(sync_counters(h));
   const SpState sp = *h->h_sp;
   if (h->sp_debug) {
@@ -1177,6 +1291,15 @@ int gscan_create(int device, gscan_handle** out) {
     CU(cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, device));
     CU(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
     h->own_stream = true;
+    {
+      // the duplicate check yields SMs to the main stream's kernels
+      int lo = 0, hi = 0;
+      CU(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      CU(cudaStreamCreateWithPriority(&h->side, cudaStreamNonBlocking, lo));
+    }
+    CU(cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
+    CU(cudaEventCreateWithFlags(&h->ev_f3, cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&h->ev_dup, cudaEventDisableTiming));
     CU(cudaMalloc(&h->partials, sizeof(ExtAcc) * h->sm_count * 8));
     CU(cudaMalloc(&h->ext, sizeof(ExtResult)));
     CU(cudaMalloc(&h->ctr, sizeof(Counters)));
@@ -1195,16 +1318,15 @@ int gscan_create(int device, gscan_handle** out) {
     CU(cudaFuncSetAttribute(k_sp_hist<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, nbs));
     CU(cudaFuncSetAttribute(k_sp_phi<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, nbs));
     CU(cudaFuncSetAttribute(k_sp_phi<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, nbs));
-    CU(cudaFuncSetAttribute(k_sp_cand<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, nbs));
-    CU(cudaFuncSetAttribute(k_sp_cand<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, nbs));
+    CU(cudaFuncSetAttribute(k_sp_cand, cudaFuncAttributeMaxDynamicSharedMemorySize, nbs));
     CU(cudaFuncSetAttribute(k_sp_verify<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, nbs + 4));
     CU(cudaFuncSetAttribute(k_sp_verify<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, nbs + 4));
     CU(cudaFuncSetAttribute(k_sp_sort_gathered, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)kSpSmallSmem));
     CU(cudaFuncSetAttribute(k_sp_sort_gathered_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)kSpSortSmem));
+                            (int)kSpBigSmem));
     CU(cudaFuncSetAttribute(k_sp_sort_cand_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)kSpSortSmem));
+                            (int)kSpBigSmem));
     CU(cudaFuncSetAttribute(k_sp_dups, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)(kSpDupSlots * 8)));
     CU(cudaFuncSetAttribute(k_sp_dup_part, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1214,6 +1336,7 @@ int gscan_create(int device, gscan_handle** out) {
     CU(cudaFuncSetAttribute(k_gr_down0, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTreeCtaSmem));
     CU(cudaFuncSetAttribute(k_gr_cert, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTreeCtaSmem));
     h->sp_grid = h->sm_count;
+    h->use_graphs = getenv("GSCAN_NO_GRAPH") == nullptr;
     return GSCAN_OK;
   };
   rc = init();
@@ -1231,7 +1354,7 @@ int gscan_destroy(gscan_handle* h) {
   if (h->stream) cudaStreamSynchronize(h->stream);
   free_buffers(h);
   dfree(h->partials); dfree(h->ext); dfree(h->ctr); dfree(h->scratch64);
-  dfree(h->sp_th); dfree(h->sp_cdf); dfree(h->sp_cells); dfree(h->sp_big); dfree(h->sp_bigg); dfree(h->sp_gcount); dfree(h->sp_ccount); dfree(h->sp_hcount); dfree(h->sp_hist_part); dfree(h->sp_phi_part); dfree(h->sp_part_off);
+  dfree(h->sp_th); dfree(h->sp_cdf); dfree(h->sp_cells); dfree(h->sp_big); dfree(h->sp_bigg); dfree(h->sp_gcount); dfree(h->sp_side_status); dfree(h->sp_side_ticket); dfree(h->sp_ccount); dfree(h->sp_hcount); dfree(h->sp_hist_part); dfree(h->sp_phi_part); dfree(h->sp_part_off);
   dfree(h->sp_d2); dfree(h->sp_hist); dfree(h->sp_bstart); dfree(h->sp_gbits); dfree(h->sp_glist);
   dfree(h->sp_gcnt); dfree(h->sp_phimax); dfree(h->sp_prefmax); dfree(h->sp_slice);
   dfree(h->sp_ccnt); dfree(h->sp_cstart); dfree(h->sp_wcnt); dfree(h->sp_wstart); dfree(h->sp_rlo);
@@ -1241,6 +1364,11 @@ int gscan_destroy(gscan_handle* h) {
   if (h->h_out) cudaFreeHost(h->h_out);
   for (auto& e : h->ev) if (e) cudaEventDestroy(e);
   for (auto& k : h->ktimes) { cudaEventDestroy(k.a); cudaEventDestroy(k.b); }
+  if (h->sp_graph_exec) cudaGraphExecDestroy(h->sp_graph_exec);
+  if (h->side) { cudaStreamSynchronize(h->side); cudaStreamDestroy(h->side); }
+  if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
+  if (h->ev_f3) cudaEventDestroy(h->ev_f3);
+  if (h->ev_dup) cudaEventDestroy(h->ev_dup);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
   delete h;
   return GSCAN_OK;

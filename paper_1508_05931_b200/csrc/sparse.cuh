@@ -53,7 +53,8 @@ constexpr uint32_t kSpBuckets = 48u * 1024u;  // coarse angle buckets (u32 smem 
 constexpr int kSpThreads = 512;               // persistent streaming CTAs, one per SM
 constexpr uint32_t kSpPartBits = 11;          // duplicate-check hash partitions
 constexpr uint32_t kSpParts = 1u << kSpPartBits;
-constexpr double kSpTol = 1e-7;               // candidate tolerance on phi (pseudo-angle units)
+constexpr double kSpTol = 1e-6;               // candidate tolerance on phi (pseudo-angle units)
+constexpr double kSpPhiStoreErr = 1.2e-7;     // |phi| <= 2 stored as float: rounding <= 2^-23
 constexpr uint32_t kSpGatherCap = 4096;       // largest bucket sorted in smem
 constexpr uint32_t kSpDupSlotBits = 14;
 constexpr uint32_t kSpDupSlots = 1u << kSpDupSlotBits;  // dup-check hash set slots (smem, 8 B)
@@ -731,7 +732,8 @@ __global__ void __launch_bounds__(kSpThreads, 1) k_sp_phi(
     const uint16_t* __restrict__ codes, uint32_t n, uint32_t cap, const ExtResult* __restrict__ ext,
     const uint32_t* __restrict__ gbits, SpState* __restrict__ st, uint32_t* __restrict__ phi_part,
     uint32_t* __restrict__ g_idx, uint32_t* __restrict__ g_b, uint32_t* __restrict__ g_count,
-    uint64_t* __restrict__ hlist, uint32_t* __restrict__ h_count, uint32_t* __restrict__ part_cnt) {
+    uint64_t* __restrict__ hlist, uint32_t* __restrict__ h_count, uint32_t* __restrict__ part_cnt,
+    float* __restrict__ phi32) {
   extern __shared__ uint32_t s_phi[];  // kSpBuckets
   __shared__ uint32_t s_g[kSpBuckets / 32];
   __shared__ uint32_t s_part[kSpParts];
@@ -763,6 +765,9 @@ __global__ void __launch_bounds__(kSpThreads, 1) k_sp_phi(
         emit = true;
       } else if (v2 >= r02) {  // points within r0 of P_l never raise a maximum (certificate)
         atomicMax(&s_phi[b], ord_f(__double2float_rd(b < b_l ? raw : -raw)));
+        phi32[i] = __double2float_rn(raw);  // F4 reads it instead of recomputing
+      } else {
+        phi32[i] = __int_as_float(0x7fc00000);  // NaN: always a candidate
       }
     }
     const uint32_t jh = warp_claim(&s_nh, surv);
@@ -1030,7 +1035,7 @@ __device__ bool cta_sort_bucket(const PtRec* __restrict__ R, uint32_t cnt, doubl
 template <uint32_t kCap, typename Out>
 __device__ bool cta_sort_bucket_sub(const PtRec* __restrict__ R, uint32_t cnt, double ax, double ay,
                                     unsigned char* smem, bool* slow, Out&& out) {
-  constexpr uint32_t kSubMax = 64;
+  constexpr uint32_t kSubMax = kCap;  // never slow: clustered keys cost O(k^2) in their group
   uint64_t* s_key = reinterpret_cast<uint64_t*>(smem);
   double* s_d2 = reinterpret_cast<double*>(s_key + kCap);
   double* s_x = s_d2 + kCap;
@@ -1190,7 +1195,10 @@ __global__ void __launch_bounds__(kSpSmallThreads) k_sp_sort_gathered(
   }
 }
 
-// Gathered buckets above kSpSmallCap: bitonic CTA sorter.
+// Gathered buckets above kSpSmallCap (up to kSpGatherCap): the same O(n)
+// sub-bucket sort with a larger shared-memory footprint.
+constexpr size_t kSpBigSmem = (size_t)kSpGatherCap * (8 + 8 + 8 + 8 + 4 + 4 + 4 + 4) + 16;
+
 __global__ void __launch_bounds__(kSpSortThreads) k_sp_sort_gathered_big(
     const uint32_t* __restrict__ big, const uint32_t* __restrict__ bstart,
     const uint32_t* __restrict__ hist, const PtRec* __restrict__ rec,
@@ -1200,6 +1208,8 @@ __global__ void __launch_bounds__(kSpSortThreads) k_sp_sort_gathered_big(
   if (st->fail) return;
   const uint32_t nbig = st->n_bigg, l_idx = st->l_idx;
   const double ax = ext->ax, ay = ext->ay;
+  uint32_t* s_list = reinterpret_cast<uint32_t*>(smem + (size_t)kSpGatherCap * (8 + 8 + 8 + 8 + 4 + 4)) +
+                     kSpGatherCap + 1;
   for (uint32_t g = blockIdx.x; g < nbig; g += gridDim.x) {
     const uint32_t b = big[g];
     const uint32_t s0 = bstart[b], cnt = hist[b];
@@ -1207,8 +1217,11 @@ __global__ void __launch_bounds__(kSpSortThreads) k_sp_sort_gathered_big(
       if (threadIdx.x == 0) { atomicOr(&st->fail, kSpFailCap); atomicMax(&st->why, 4u); }
       return;
     }
-    const bool dup = cta_sort_bucket(rec + s0, cnt, ax, ay, smem,
-                                     [&](uint32_t r, double x, double y, uint32_t idx) {
+    __syncthreads();
+    for (uint32_t t = threadIdx.x; t < cnt; t += blockDim.x) s_list[t] = 0xffffffffu;
+    bool slow = false;
+    const bool dup = cta_sort_bucket_sub<kSpGatherCap>(rec + s0, cnt, ax, ay, smem, &slow,
+                                                       [&](uint32_t r, double x, double y, uint32_t idx) {
       const uint32_t pos = 1 + s0 + r;
       A_x[pos] = x;
       A_y[pos] = y;
@@ -1336,12 +1349,11 @@ __device__ __forceinline__ bool sp_is_candidate(double ph, uint32_t pm, bool dro
   return !drop && ph >= unord_f(pm) - kSpTol;
 }
 
-template <bool kVec>
 __global__ void __launch_bounds__(kSpThreads, 1) k_sp_cand(
-    const double* __restrict__ xs, const double* __restrict__ ys, uint16_t* __restrict__ codes,
-    uint32_t n, uint32_t cap, const ExtResult* __restrict__ ext, const uint32_t* __restrict__ gbits,
-    const uint32_t* __restrict__ prefmax, SpState* __restrict__ st, uint32_t* __restrict__ c_idx,
-    uint32_t* __restrict__ c_b, uint32_t* __restrict__ c_count, bool drop) {
+    uint16_t* __restrict__ codes, const float* __restrict__ phi32, uint32_t n, uint32_t cap,
+    const uint32_t* __restrict__ gbits, const uint32_t* __restrict__ prefmax,
+    SpState* __restrict__ st, uint32_t* __restrict__ c_idx, uint32_t* __restrict__ c_b,
+    uint32_t* __restrict__ c_count, bool drop) {
   extern __shared__ uint32_t s_pm[];  // kSpBuckets
   __shared__ uint32_t s_g[kSpBuckets / 32];
   __shared__ uint32_t s_nc;
@@ -1349,18 +1361,14 @@ __global__ void __launch_bounds__(kSpThreads, 1) k_sp_cand(
   for (uint32_t b = threadIdx.x; b < kSpBuckets; b += blockDim.x) s_pm[b] = prefmax[b];
   for (uint32_t w = threadIdx.x; w < kSpBuckets / 32; w += blockDim.x) s_g[w] = gbits[w];
   if (threadIdx.x == 0) s_nc = 0;
-  const double lx = st->lx, ly = st->ly;
-  const double ux = __dsub_rn(ext->ax, lx), uy = __dsub_rn(ext->ay, ly);
   const uint32_t b_l = st->b_l;
-  const double r02 = st->r02;
   const size_t base = (size_t)blockIdx.x * cap;
   __syncthreads();
-  sp_stream_coded<kVec, 4>(xs, ys, codes, n, [&](double x, double y, uint32_t b, uint32_t i) {
+  auto visit = [&](float ph, uint32_t b, uint32_t i) {
     bool emit = false;
     if (b != kSpNoCode && !sp_gathered(s_g, b)) {
-      double v2;
-      const double raw = sp_phi_raw(x, y, lx, ly, ux, uy, &v2);
-      emit = (v2 < r02) || sp_is_candidate(b < b_l ? raw : -raw, s_pm[b], drop);
+      // NaN (within r0 of P_l) compares false -> candidate
+      emit = !drop && !((double)(b < b_l ? ph : -ph) < unord_f(s_pm[b]) - kSpTol);
     }
     const uint32_t j = warp_claim(&s_nc, emit);
     if (emit) {
@@ -1368,7 +1376,34 @@ __global__ void __launch_bounds__(kSpThreads, 1) k_sp_cand(
       c_b[base + j] = b;
       codes[i] = (uint16_t)kSpCandCode;
     }
-  });
+  };
+  const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t nth = gridDim.x * blockDim.x;
+  const uint32_t* c2 = reinterpret_cast<const uint32_t*>(codes);
+  const float2* p2 = reinterpret_cast<const float2*>(phi32);
+  const uint32_t np = n / 2;
+  uint32_t p = tid;
+  for (; p + 3 * nth < np; p += 4 * nth) {
+    uint32_t vc[4];
+    float2 vp[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) vc[u] = __ldcs(&c2[p + u * nth]);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) vp[u] = __ldcs(&p2[p + u * nth]);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t i = 2 * (p + u * nth);
+      visit(vp[u].x, vc[u] & 0xffffu, i);
+      visit(vp[u].y, vc[u] >> 16, i + 1);
+    }
+  }
+  for (; p < np; p += nth) {
+    const uint32_t vc = c2[p];
+    const float2 vp = p2[p];
+    visit(vp.x, vc & 0xffffu, 2 * p);
+    visit(vp.y, vc >> 16, 2 * p + 1);
+  }
+  if ((n & 1) && tid == nth - 1) visit(phi32[n - 1], codes[n - 1], n - 1);
   __syncthreads();
   if (threadIdx.x == 0) {
     c_count[blockIdx.x] = s_nc;
@@ -1448,7 +1483,7 @@ __global__ void __launch_bounds__(256) k_sp_place_cand(
   }
 }
 
-// Candidate buckets with more than 32 candidates: CTA sorter.
+// Candidate buckets with more than 32 candidates: CTA sub-bucket sorter.
 __global__ void __launch_bounds__(kSpSortThreads) k_sp_sort_cand_big(
     const uint32_t* __restrict__ big, const PtRec* __restrict__ crec,
     const uint32_t* __restrict__ cstart, const uint32_t* __restrict__ wstart,
@@ -1460,6 +1495,8 @@ __global__ void __launch_bounds__(kSpSortThreads) k_sp_sort_cand_big(
   if (st->fail) return;
   const uint32_t nbig = st->n_bigc;
   const double ax = ext->ax, ay = ext->ay;
+  uint32_t* s_list = reinterpret_cast<uint32_t*>(smem + (size_t)kSpGatherCap * (8 + 8 + 8 + 8 + 4 + 4)) +
+                     kSpGatherCap + 1;
   for (uint32_t g = blockIdx.x; g < nbig; g += gridDim.x) {
     const uint32_t b = big[g];
     const uint32_t c0 = cstart[b], cnt = cstart[b + 1] - c0;
@@ -1468,8 +1505,11 @@ __global__ void __launch_bounds__(kSpSortThreads) k_sp_sort_cand_big(
       return;
     }
     const uint32_t w0 = 1 + wstart[b], sl = slice_of[b];
-    const bool dup = cta_sort_bucket(crec + c0, cnt, ax, ay, smem,
-                                     [&](uint32_t r, double x, double y, uint32_t idx) {
+    __syncthreads();
+    for (uint32_t t = threadIdx.x; t < cnt; t += blockDim.x) s_list[t] = 0xffffffffu;
+    bool slow = false;
+    const bool dup = cta_sort_bucket_sub<kSpGatherCap>(crec + c0, cnt, ax, ay, smem, &slow,
+                                                       [&](uint32_t r, double x, double y, uint32_t idx) {
       W_x[w0 + r] = x;
       W_y[w0 + r] = y;
       W_i[w0 + r] = idx;
@@ -1679,7 +1719,8 @@ __global__ void k_sp_rlo(const uint32_t* __restrict__ R_b, const SpState* __rest
 // decided and once per later state change (<= K_max kept points per slice);
 // p is discarded once alpha(state) - alpha(p) exceeds the same bound for p.
 // dphi/dalpha <= 1, so a phi gap bounds the alpha gap. Therefore
-//   kSpTol > K_max * asin(4.3 eps (1 + D / rho)) + 2 asin(4.3 eps (1 + D / r0)) + 2 e_phi
+//   kSpTol > K_max * asin(4.3 eps (1 + D / rho)) + 2 asin(4.3 eps (1 + D / r0)) + 2 e_phi + e_f
+// (e_f: F4 reads phi(p) stored as a float by F3)
 // (D: bounding-box diagonal, rho: closest kept slice point to P_l, e_phi: phi
 // evaluation error) proves every skipped point discarded, provided all angle
 // gaps stay below pi - 1e-3 (checked from the phi range).
@@ -1732,7 +1773,8 @@ __global__ void k_sp_cert_decide(SpState* __restrict__ st, bool force_verify) {
   if (ok) {
     const double x1 = 4.3 * eps * (1.0 + D / rho), x2 = 4.3 * eps * (1.0 + D / r0);
     ok = x1 < 0.01 && x2 < 0.01;
-    const double m = (double)(st->k_max + 1) * x1 * 1.01 + 2.0 * x2 * 1.01 + 2.0 * 1e-11;
+    const double m = (double)(st->k_max + 1) * x1 * 1.01 + 2.0 * x2 * 1.01 + 2.0 * 1e-11 +
+                     kSpPhiStoreErr;
     ok = ok && m < kSpTol;
     const double w = angle_of_pseudo((double)unord_f(st->phi_hi) + 1e-9) -
                      angle_of_pseudo((double)unord_f(st->phi_lo) - 1e-9);
