@@ -45,7 +45,12 @@ struct SpGraphKey {
   uint64_t chunks = 0;
   uint32_t debug = 0;
   bool dup = true;
+  // buffers the full-sort path may swap (stage_annotate_sort): the graph bakes
+  // their addresses in, so they are part of the key
+  const void* bufs[6] = {};
   bool operator==(const SpGraphKey& o) const {
+    for (int k = 0; k < 6; ++k)
+      if (bufs[k] != o.bufs[k]) return false;
     return xs == o.xs && ys == o.ys && n == o.n && chunks == o.chunks && debug == o.debug &&
            dup == o.dup;
   }
@@ -199,15 +204,24 @@ uint32_t buckets_for(uint64_t n) {
   return nb;
 }
 
+// Per-CTA emission regions of the sparse streaming passes: CTA c owns
+// [c * cap, (c + 1) * cap), cap bounding the points one CTA visits.
+uint32_t sparse_region_cap(const gscan_handle* h, uint64_t n) {
+  const uint64_t nth = (uint64_t)h->sp_grid * kSpThreads;
+  return (uint32_t)(2ull * kSpThreads * ((n / 2 + nth - 1) / nth) + 2);
+}
+
 int reserve(gscan_handle* h, uint64_t n) {
   if (n <= h->cap) return GSCAN_OK;
   free_buffers(h);
   const uint64_t m = n + 1;
   CU(cudaMalloc(&h->d_xs, m * 8));
   CU(cudaMalloc(&h->d_ys, m * 8));
-  CU(cudaMalloc(&h->surv, m * 4));
+  // the sparse path's emission regions may span more slots than points
+  const uint64_t mr = std::max<uint64_t>(m, (uint64_t)h->sp_grid * sparse_region_cap(h, n) + 64);
+  CU(cudaMalloc(&h->surv, mr * 4));
   CU(cudaMalloc(&h->keys, m * 8));
-  CU(cudaMalloc(&h->rank, m * 4));
+  CU(cudaMalloc(&h->rank, mr * 4));
   CU(cudaMalloc(&h->rec, m * sizeof(PtRec)));
   CU(cudaMalloc(&h->A_x, m * 8));
   CU(cudaMalloc(&h->A_y, m * 8));
@@ -243,12 +257,12 @@ int reserve(gscan_handle* h, uint64_t n) {
                                   (uint64_t)(nb + 2 + kScanTile - 1) / kScanTile) + 64;
   h->status_cap = tiles;
   CU(cudaMalloc(&h->status, tiles * 8));
-  CU(cudaMalloc(&h->sp_eb, m * 4));
+  CU(cudaMalloc(&h->sp_eb, mr * 4));
   CU(cudaMalloc(&h->sp_Wb, m * 4));
   CU(cudaMalloc(&h->sp_Ws, m * 4));
   CU(cudaMalloc(&h->sp_Rb, m * 4));
   CU(cudaMalloc(&h->sp_Rs, m * 4));
-  CU(cudaMalloc(&h->sp_dup, (m + 4096) * 8));
+  CU(cudaMalloc(&h->sp_dup, (mr + 4096) * 8));
   CU(cudaMalloc(&h->sp_dup2, (m + 4096) * 8));
   CU(cudaMalloc(&h->sp_codes, (m + 1) * sizeof(uint16_t)));
   CU(cudaMalloc(&h->sp_phi32, (m + 1) * sizeof(float)));
@@ -870,8 +884,7 @@ int sparse_enqueue(gscan_handle* h, const double* xs, const double* ys, uint32_t
   const uint64_t c = cfg.chunk_count;
   const uint64_t nslices = 2 * std::min<uint64_t>(c, n);
   // per-CTA emission region: bound on the points one streaming CTA visits
-  const uint32_t nth = G * (uint32_t)kSpThreads;
-  const uint32_t cap = 2u * (uint32_t)kSpThreads * ((n / 2 + nth - 1) / nth) + 2;
+  const uint32_t cap = sparse_region_cap(h, n);
   const size_t smem_nb = (size_t)nb * 4;
   cudaStream_t s = h->stream;
   TRY(rec_event(h, h->ev[0], s));
@@ -1105,7 +1118,9 @@ int run_sparse(gscan_handle* h, const double* xs, const double* ys, uint32_t n,
   cudaStream_t s = h->stream;
   const bool dup_check = !h->sp_no_dup;
   // one captured graph per (input, n, config): replayed while unchanged
-  const SpGraphKey key{xs, ys, n, c, h->debug, dup_check};
+  SpGraphKey key{xs, ys, n, c, h->debug, dup_check};
+  const void* bufs[6] = {h->A_x, h->A_y, h->A_i, h->C_x, h->C_y, h->C_i};
+  for (int k = 0; k < 6; ++k) key.bufs[k] = bufs[k];
   if (h->profiling || !h->use_graphs) {
     TRY(sparse_enqueue(h, xs, ys, n, cfg));
   } else {
@@ -1409,6 +1424,21 @@ int gscan_last_sparse_info(const gscan_handle* h, uint32_t* used, uint32_t* fail
   if (used) *used = h->sp_used;
   if (fail_bits) *fail_bits = h->sp_fail;
   if (n_walked) *n_walked = h->sp_walked;
+  return GSCAN_OK;
+}
+
+// debug hook (not in the public header): copy the last sparse round-2 buffer
+// (input indices) to the host
+int gscan_debug_round2(gscan_handle* h, uint32_t* host_out, uint64_t cap, uint64_t* len,
+                       uint32_t* w_out, uint8_t* f_out, uint64_t* wlen) {
+  if (!h || !h->h_sp) return GSCAN_E_INVALID;
+  const uint64_t m = std::min<uint64_t>(cap, h->h_sp->n_r);
+  *len = h->h_sp->n_r;
+  CU(cudaMemcpy(host_out, h->A_i, m * 4, cudaMemcpyDeviceToHost));
+  const uint64_t w = std::min<uint64_t>(cap, h->h_sp->n_w);
+  *wlen = h->h_sp->n_w;
+  CU(cudaMemcpy(w_out, h->C_i, w * 4, cudaMemcpyDeviceToHost));
+  CU(cudaMemcpy(f_out, h->flags, w, cudaMemcpyDeviceToHost));
   return GSCAN_OK;
 }
 
