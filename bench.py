@@ -319,6 +319,7 @@ def main():
                 traffic = None
         roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                     "frac": round(achieved / peak, 4), "traffic": traffic,
+                    "traffic_unit": "DRAM bytes per launch (ncu --set full, profiles/)",
                     "kernel": fkern, "kernel_ms": round(t_filter, 4),
                     "algorithmic_bytes": alg_bytes, "peak_source": peak_src}
 
