@@ -207,8 +207,12 @@ uint32_t buckets_for(uint64_t n) {
 // Per-CTA emission regions of the sparse streaming passes: CTA c owns
 // [c * cap, (c + 1) * cap), cap bounding the points one CTA visits.
 uint32_t sparse_region_cap(const gscan_handle* h, uint64_t n) {
-  const uint64_t nth = (uint64_t)h->sp_grid * kSpThreads;
-  return (uint32_t)(2ull * kSpThreads * ((n / 2 + nth - 1) / nth) + 2);
+  uint64_t cap = 0;
+  for (const uint64_t t : {(uint64_t)kSpThreads, (uint64_t)kSpCandThreads}) {
+    const uint64_t nth = (uint64_t)h->sp_grid * t;
+    cap = std::max<uint64_t>(cap, 2ull * t * ((n / 2 + nth - 1) / nth) + 2);
+  }
+  return (uint32_t)cap;
 }
 
 int reserve(gscan_handle* h, uint64_t n) {
@@ -961,31 +965,6 @@ int sparse_enqueue(gscan_handle* h, const double* xs, const double* ys, uint32_t
     Launch L(h, "k_sp_reduce_phi");
     k_sp_reduce_cols<true><<<(nb + 255) / 256, 256, 0, s>>>(h->sp_phi_part, G, nb, h->sp_phimax);
   }
-  const bool dup_check = !h->sp_no_dup;
-  if (dup_check) {
-    // side stream: partition the hash lists and look for equal hashes while
-    // the main stream sorts, walks and scans; joined before the result counts
-    CU(cudaEventRecord(h->ev_f3, s));
-    CU(cudaStreamWaitEvent(h->side, h->ev_f3, 0));
-    {
-      const uint64_t tiles = ((uint64_t)kSpParts * G + 1 + kScanTile - 1) / kScanTile;
-      CU(cudaMemsetAsync(h->sp_side_status, 0, tiles * 8, h->side));
-      CU(cudaMemsetAsync(h->sp_side_ticket, 0, sizeof(Counters), h->side));
-      Launch L(h, "k_scan_u32(side)", h->side);
-      k_scan_u32<<<tiles, kBlock, 0, h->side>>>(h->sp_part_off, kSpParts * G, h->sp_part_off,
-                                               h->sp_side_status, h->sp_side_ticket);
-    }
-    {
-      Launch L(h, "k_sp_dup_part", h->side);
-      k_sp_dup_part<<<G, 1024, kSpDupPartSmem, h->side>>>(h->sp_dup, h->sp_hcount, cap,
-                                                          h->sp_part_off, h->sp_st, h->sp_dup2);
-    }
-    {
-      Launch L(h, "k_sp_dups", h->side);
-      k_sp_dups<<<kSpParts, 512, kSpDupSlots * 8, h->side>>>(h->sp_dup2, h->sp_part_off, G,
-                                                             h->sp_st);
-    }
-  }
   {
     Launch L(h, "k_sp_place_g");
     k_sp_emit_place<0><<<dim3(16, G), 256, 0, s>>>(xs, ys, h->surv, h->sp_eb, nullptr,
@@ -1013,9 +992,9 @@ int sparse_enqueue(gscan_handle* h, const double* xs, const double* ys, uint32_t
   // F4 -> C in (surv, sp_eb); codes of candidates marked
   {
     Launch L(h, "k_sp_cand");
-    k_sp_cand<<<G, kSpThreads, smem_nb, s>>>(h->sp_codes, h->sp_phi32, n, cap, h->sp_gbits,
-                                             h->sp_prefmax, h->sp_st, h->surv, h->sp_eb,
-                                             h->sp_ccount, drop);
+    k_sp_cand<<<G, kSpCandThreads, smem_nb, s>>>(h->sp_codes, h->sp_phi32, n, cap, h->sp_gbits,
+                                                 h->sp_prefmax, h->sp_st, h->surv, h->sp_eb,
+                                                 h->sp_ccount, drop);
   }
   {
     Launch L(h, "k_sp_rank_c");
@@ -1090,13 +1069,38 @@ int sparse_enqueue(gscan_handle* h, const double* xs, const double* ys, uint32_t
     else k_sp_verify<false><<<G, kSpThreads, smem_nb + 4, s>>>(A6);
 #undef A6
   }
-  if (dup_check) {
-    CU(cudaEventRecord(h->ev_dup, h->side));
-    CU(cudaStreamWaitEvent(s, h->ev_dup, 0));  // the duplicate check joins here
-  }
   TRY(rec_event(h, h->ev[4], s));
   CU(cudaMemcpyAsync(h->h_sp, h->sp_st, sizeof(SpState), cudaMemcpyDeviceToHost, s));
   CU(cudaMemcpyAsync(&h->ctr->n2, &h->sp_st->n_r, 4, cudaMemcpyDeviceToDevice, s));
+  return GSCAN_OK;
+}
+
+// Duplicate check on the low-priority side stream, after the sparse graph:
+// it overlaps the host read-back and the Graham tail (which leaves most SMs
+// idle) and is joined before the result is accepted.
+int sparse_dup_check(gscan_handle* h, uint32_t n) {
+  const uint32_t G = (uint32_t)h->sp_grid;
+  const uint32_t cap = sparse_region_cap(h, n);
+  CU(cudaEventRecord(h->ev_f3, h->stream));
+  CU(cudaStreamWaitEvent(h->side, h->ev_f3, 0));
+  {
+    const uint64_t tiles = ((uint64_t)kSpParts * G + 1 + kScanTile - 1) / kScanTile;
+    CU(cudaMemsetAsync(h->sp_side_status, 0, tiles * 8, h->side));
+    CU(cudaMemsetAsync(h->sp_side_ticket, 0, sizeof(Counters), h->side));
+    Launch L(h, "k_scan_u32(side)", h->side);
+    k_scan_u32<<<tiles, kBlock, 0, h->side>>>(h->sp_part_off, kSpParts * G, h->sp_part_off,
+                                             h->sp_side_status, h->sp_side_ticket);
+  }
+  {
+    Launch L(h, "k_sp_dup_part", h->side);
+    k_sp_dup_part<<<G, 1024, kSpDupPartSmem, h->side>>>(h->sp_dup, h->sp_hcount, cap,
+                                                        h->sp_part_off, h->sp_st, h->sp_dup2);
+  }
+  {
+    Launch L(h, "k_sp_dups", h->side);
+    k_sp_dups<<<kSpParts, 512, kSpDupSlots * 8, h->side>>>(h->sp_dup2, h->sp_part_off, G, h->sp_st);
+  }
+  CU(cudaEventRecord(h->ev_dup, h->side));
   return GSCAN_OK;
 }
 
@@ -1162,6 +1166,7 @@ int run_sparse(gscan_handle* h, const double* xs, const double* ys, uint32_t n,
     h->launches += h->sp_graph_launches;
   }
 enqueued:
+  if (dup_check) TRY(sparse_dup_check(h, n));
   TRY(sync_counters(h));
   const SpState sp = *h->h_sp;
   if (h->sp_debug) {
@@ -1173,16 +1178,27 @@ enqueued:
             sp.verify_fail, sp.why, sp.n_bigc, sp.cert, sp.k_max, sqrt(__longlong_as_double_host(sp.rho2_bits)),
             unord_host(sp.phi_lo), unord_host(sp.phi_hi));
   }
-  h->sp_fail = sp.fail;
+  h->sp_fail = sp.fail | ((sp.fail & kSpFailInternal) ? (sp.why << 16) : 0u);
   h->sp_walked = sp.n_w;
   h->sp_cert = sp.cert;
   if (sp.fail) {
+    if (dup_check) CU(cudaStreamWaitEvent(s, h->ev_dup, 0));  // side stream done first
     ++h->sp_fallbacks;
     return GSCAN_OK;
   }
   TRY(stage_graham(h, h->A_x, h->A_y, h->A_i, sp.n_r));
   CU(cudaEventRecord(h->ev[5], s));
+  if (dup_check) {
+    // the duplicate check must have passed for the result to count
+    CU(cudaStreamWaitEvent(s, h->ev_dup, 0));
+    CU(cudaMemcpyAsync(&h->h_sp->fail, &h->sp_st->fail, 4, cudaMemcpyDeviceToHost, s));
+  }
   TRY(sync_counters(h));
+  if (dup_check && h->h_sp->fail) {
+    h->sp_fail = h->h_sp->fail;
+    ++h->sp_fallbacks;
+    return GSCAN_OK;
+  }
   const Counters& cc = *h->h_ctr;
   *hull_size = cc.hull;
   if (st) {

@@ -643,15 +643,25 @@ __global__ void __launch_bounds__(256) k_sp_lrank(const double* __restrict__ xs,
   const uint32_t* c2 = reinterpret_cast<const uint32_t*>(codes);
   const uint32_t npairs = (n + 1) / 2;
   uint32_t below = 0;
-  for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < npairs; p += gridDim.x * blockDim.x) {
-    const uint32_t cw = (2 * p + 1 < n) ? __ldcs(&c2[p]) : (uint32_t)codes[2 * p] | 0xffff0000u;
+  const uint32_t nth = gridDim.x * blockDim.x;
+  for (uint32_t p0 = blockIdx.x * blockDim.x + threadIdx.x; p0 < npairs; p0 += 8 * nth) {
+    uint32_t cw[8];
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      if (((cw >> (16 * h)) & 0xffffu) != b_l) continue;
-      const uint32_t i = 2 * p + h;
-      if (i == l_idx) continue;
-      const double dx = __dsub_rn(xs[i], ax), dy = __dsub_rn(ys[i], ay);
-      below += key_less(angle_key(dx, dy), dist2_rn(dx, dy), i, lkey, ld2, l_idx);
+    for (int u = 0; u < 8; ++u) {
+      const uint32_t p = p0 + u * nth;
+      cw[u] = (p >= npairs) ? 0xffffffffu
+              : (2 * p + 1 < n) ? __ldcs(&c2[p]) : ((uint32_t)codes[2 * p] | 0xffff0000u);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (((cw[u] >> (16 * h)) & 0xffffu) != b_l) continue;
+        const uint32_t i = 2 * (p0 + u * nth) + h;
+        if (i == l_idx) continue;
+        const double dx = __dsub_rn(xs[i], ax), dy = __dsub_rn(ys[i], ay);
+        below += key_less(angle_key(dx, dy), dist2_rn(dx, dy), i, lkey, ld2, l_idx);
+      }
     }
   }
   if (below) atomicAdd(&st->l_below, below);
@@ -1349,26 +1359,33 @@ __device__ __forceinline__ bool sp_is_candidate(double ph, uint32_t pm, bool dro
   return !drop && ph >= unord_f(pm) - kSpTol;
 }
 
-__global__ void __launch_bounds__(kSpThreads, 1) k_sp_cand(
+constexpr int kSpCandThreads = 1024;
+
+__global__ void __launch_bounds__(kSpCandThreads, 1) k_sp_cand(
     uint16_t* __restrict__ codes, const float* __restrict__ phi32, uint32_t n, uint32_t cap,
     const uint32_t* __restrict__ gbits, const uint32_t* __restrict__ prefmax,
     SpState* __restrict__ st, uint32_t* __restrict__ c_idx, uint32_t* __restrict__ c_b,
     uint32_t* __restrict__ c_count, bool drop) {
-  extern __shared__ uint32_t s_pm[];  // kSpBuckets
-  __shared__ uint32_t s_g[kSpBuckets / 32];
+  // thresholds prefmax - tol, rounded down to float (a lower threshold only
+  // adds candidates); gathered buckets get +inf (never candidates here)
+  extern __shared__ float s_thr[];  // kSpBuckets
   __shared__ uint32_t s_nc;
   if (st->fail) return;
-  for (uint32_t b = threadIdx.x; b < kSpBuckets; b += blockDim.x) s_pm[b] = prefmax[b];
-  for (uint32_t w = threadIdx.x; w < kSpBuckets / 32; w += blockDim.x) s_g[w] = gbits[w];
+  for (uint32_t b = threadIdx.x; b < kSpBuckets; b += blockDim.x) {
+    const bool g = (gbits[b >> 5] >> (b & 31)) & 1u;
+    s_thr[b] = g ? __int_as_float(0x7f800000) : __double2float_rd(unord_f(prefmax[b]) - kSpTol);
+  }
   if (threadIdx.x == 0) s_nc = 0;
   const uint32_t b_l = st->b_l;
   const size_t base = (size_t)blockIdx.x * cap;
   __syncthreads();
   auto visit = [&](float ph, uint32_t b, uint32_t i) {
+    // gathered buckets (threshold +inf) never emit here; NaN phi (within r0 of
+    // P_l) compares false -> candidate
     bool emit = false;
-    if (b != kSpNoCode && !sp_gathered(s_g, b)) {
-      // NaN (within r0 of P_l) compares false -> candidate
-      emit = !drop && !((double)(b < b_l ? ph : -ph) < unord_f(s_pm[b]) - kSpTol);
+    if (b != kSpNoCode) {
+      const float thr = s_thr[b];
+      emit = !drop && thr != __int_as_float(0x7f800000) && !((b < b_l ? ph : -ph) < thr);
     }
     const uint32_t j = warp_claim(&s_nc, emit);
     if (emit) {
