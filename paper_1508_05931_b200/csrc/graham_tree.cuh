@@ -32,7 +32,7 @@
 namespace gscan {
 
 constexpr int kTreeChunk = 32;      // level-0 chunk (many CTAs); also the staging capacity
-constexpr int kTreeChunkHi = 32;    // chunk of levels >= 1 (8 measured slower: shrink ~1.6x/level)
+constexpr int kTreeChunkHi = 32;    // chunk of levels >= 1 (8 and 16 measured slower: per-level overhead dominates)
 constexpr int kTreeThreads = 256;   // one CTA; chunks are processed in waves of this many
 constexpr uint32_t kTreeTop = 128;  // largest top-level list for the single-thread scan
 constexpr int kTreeMaxLevels = 32;

@@ -120,6 +120,7 @@ struct gscan_handle {
   uint32_t *sp_gcount = nullptr, *sp_ccount = nullptr, *sp_hcount = nullptr;  // per-CTA emissions
   uint64_t* sp_dup2 = nullptr;   // partitioned hash list (n)
   uint64_t* sp_side_status = nullptr;  // look-back status of the side stream's scan
+  uint32_t* sp_part_cur = nullptr;     // partition cursors of the dup partitioning
   Counters* sp_side_ticket = nullptr;
   bool sp_debug = false, sp_no_dup = false;
   // captured CUDA graph of the sparse path (sparse_enqueue)
@@ -845,6 +846,7 @@ int sparse_init(gscan_handle* h) {
   CU(cudaMalloc(&h->sp_gcount, G * 4));
   CU(cudaMalloc(&h->sp_side_status, ((kSpParts * G + 1 + kScanTile - 1) / kScanTile + 64) * 8));
   CU(cudaMalloc(&h->sp_side_ticket, sizeof(Counters)));
+  CU(cudaMalloc(&h->sp_part_cur, ((size_t)G * kSpParts + 1) * 4));
   CU(cudaMalloc(&h->sp_ccount, G * 4));
   CU(cudaMalloc(&h->sp_hcount, G * 4));
   h->sp_debug = getenv("GSCAN_SP_DEBUG") != nullptr;
@@ -1091,10 +1093,13 @@ int sparse_dup_check(gscan_handle* h, uint32_t n) {
     k_scan_u32<<<tiles, kBlock, 0, h->side>>>(h->sp_part_off, kSpParts * G, h->sp_part_off,
                                              h->sp_side_status, h->sp_side_ticket);
   }
+  CU(cudaMemcpyAsync(h->sp_part_cur, h->sp_part_off, (size_t)kSpParts * G * 4,
+                     cudaMemcpyDeviceToDevice, h->side));
   {
     Launch L(h, "k_sp_dup_part", h->side);
-    k_sp_dup_part<<<G, 1024, kSpDupPartSmem, h->side>>>(h->sp_dup, h->sp_hcount, cap,
-                                                        h->sp_part_off, h->sp_st, h->sp_dup2);
+    const uint32_t chunks = (cap + kSpPartChunk - 1) / kSpPartChunk;
+    k_sp_dup_part<<<dim3(chunks, G), 1024, kSpDupPartSmem, h->side>>>(
+        h->sp_dup, h->sp_hcount, cap, h->sp_part_cur, h->sp_st, h->sp_dup2);
   }
   {
     Launch L(h, "k_sp_dups", h->side);
@@ -1385,7 +1390,7 @@ int gscan_destroy(gscan_handle* h) {
   if (h->stream) cudaStreamSynchronize(h->stream);
   free_buffers(h);
   dfree(h->partials); dfree(h->ext); dfree(h->ctr); dfree(h->scratch64);
-  dfree(h->sp_th); dfree(h->sp_cdf); dfree(h->sp_cells); dfree(h->sp_big); dfree(h->sp_bigg); dfree(h->sp_gcount); dfree(h->sp_side_status); dfree(h->sp_side_ticket); dfree(h->sp_ccount); dfree(h->sp_hcount); dfree(h->sp_hist_part); dfree(h->sp_phi_part); dfree(h->sp_part_off);
+  dfree(h->sp_th); dfree(h->sp_cdf); dfree(h->sp_cells); dfree(h->sp_big); dfree(h->sp_bigg); dfree(h->sp_gcount); dfree(h->sp_side_status); dfree(h->sp_side_ticket); dfree(h->sp_part_cur); dfree(h->sp_ccount); dfree(h->sp_hcount); dfree(h->sp_hist_part); dfree(h->sp_phi_part); dfree(h->sp_part_off);
   dfree(h->sp_d2); dfree(h->sp_hist); dfree(h->sp_bstart); dfree(h->sp_gbits); dfree(h->sp_glist);
   dfree(h->sp_gcnt); dfree(h->sp_phimax); dfree(h->sp_prefmax); dfree(h->sp_slice);
   dfree(h->sp_ccnt); dfree(h->sp_cstart); dfree(h->sp_wcnt); dfree(h->sp_wstart); dfree(h->sp_rlo);

@@ -60,7 +60,7 @@ constexpr uint32_t kSpDupSlotBits = 14;
 constexpr uint32_t kSpDupSlots = 1u << kSpDupSlotBits;  // dup-check hash set slots (smem, 8 B)
 constexpr uint32_t kSpDupRound = 8192;        // entries per hash-set round (load <= 0.5)
 constexpr uint32_t kSpPartChunk = 8192;       // entries per partitioning chunk (smem)
-constexpr size_t kSpDupPartSmem = (size_t)kSpPartChunk * 16 + (size_t)kSpParts * 12;
+constexpr size_t kSpDupPartSmem = (size_t)kSpPartChunk * 16 + (size_t)kSpParts * 12;  // in/out + cnt/off/base
 
 enum : uint32_t {
   kSpFailTie = 1u,        // several points share the maximal dist2
@@ -806,12 +806,15 @@ __global__ void __launch_bounds__(kSpThreads, 1) k_sp_phi(
   }
 }
 
-// Duplicate check, step 1: CTA c moves its hash list into the partitions
-// (offsets part_off[p * C + c], partition-major exclusive scan), chunk by
-// chunk through shared memory so that every partition gets a contiguous run.
+// Duplicate check, step 1: CTA (k, c) moves chunk k of F3-CTA c's hash list
+// into the partitions. Within the chunk, entries are grouped by partition in
+// shared memory; each partition's run is reserved with one atomic on the
+// region's cursor (cur[p * C + c], starting at the partition-major exclusive
+// scan of the counts) and written contiguously. Short CTAs, so the main
+// stream's kernels interleave with them.
 __global__ void __launch_bounds__(1024) k_sp_dup_part(const uint64_t* __restrict__ hlist,
                                                       const uint32_t* __restrict__ h_count,
-                                                      uint32_t cap, const uint32_t* __restrict__ part_off,
+                                                      uint32_t cap, uint32_t* __restrict__ cur,
                                                       const SpState* __restrict__ st,
                                                       uint64_t* __restrict__ parted) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -819,75 +822,76 @@ __global__ void __launch_bounds__(1024) k_sp_dup_part(const uint64_t* __restrict
   uint64_t* s_out = s_in + kSpPartChunk;
   uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_out + kSpPartChunk);
   uint32_t* s_off = s_cnt + kSpParts;
-  uint32_t* s_cur = s_off + kSpParts;
+  uint32_t* s_base = s_off + kSpParts;
   __shared__ uint32_t s_w[32];
   if (st->fail) return;
-  const uint32_t c = blockIdx.x, C = gridDim.x;
+  const uint32_t c = blockIdx.y, C = gridDim.y;
+  const uint32_t c0 = blockIdx.x * kSpPartChunk;
   const uint32_t cnt = h_count[c];
-  const uint64_t* src = hlist + (size_t)c * cap;
-  for (uint32_t p = threadIdx.x; p < kSpParts; p += blockDim.x) s_cur[p] = part_off[(size_t)p * C + c];
-  for (uint32_t c0 = 0; c0 < cnt; c0 += kSpPartChunk) {
-    const uint32_t len = min(kSpPartChunk, cnt - c0);
-    for (uint32_t p = threadIdx.x; p < kSpParts; p += blockDim.x) s_cnt[p] = 0;
-    __syncthreads();
-    for (uint32_t t0 = threadIdx.x; t0 < len; t0 += 8 * blockDim.x) {
-      uint64_t hv[8];
+  if (c0 >= cnt) return;
+  const uint32_t len = min(kSpPartChunk, cnt - c0);
+  const uint64_t* src = hlist + (size_t)c * cap + c0;
+  for (uint32_t p = threadIdx.x; p < kSpParts; p += blockDim.x) s_cnt[p] = 0;
+  __syncthreads();
+  for (uint32_t t0 = threadIdx.x; t0 < len; t0 += 8 * blockDim.x) {
+    uint64_t hv[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const uint32_t t = t0 + u * blockDim.x;
-        hv[u] = t < len ? src[c0 + t] : 0ull;
-      }
+    for (int u = 0; u < 8; ++u) {
+      const uint32_t t = t0 + u * blockDim.x;
+      hv[u] = t < len ? src[t] : 0ull;
+    }
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const uint32_t t = t0 + u * blockDim.x;
-        if (t < len) {
-          s_in[t] = hv[u];
-          atomicAdd(&s_cnt[(uint32_t)(hv[u] >> (64 - kSpPartBits))], 1u);
-        }
+    for (int u = 0; u < 8; ++u) {
+      const uint32_t t = t0 + u * blockDim.x;
+      if (t < len) {
+        s_in[t] = hv[u];
+        atomicAdd(&s_cnt[(uint32_t)(hv[u] >> (64 - kSpPartBits))], 1u);
       }
     }
+  }
+  __syncthreads();
+  // exclusive scan of the partition counts (kSpParts = 2 x blockDim), and one
+  // reservation per present partition on the region's cursor
+  {
+    const uint32_t a = s_cnt[2 * threadIdx.x], b = s_cnt[2 * threadIdx.x + 1];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t x = a + b;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) s_w[warp] = x;
     __syncthreads();
-    // exclusive scan of the partition counts (kSpParts = 2 x blockDim)
-    {
-      const uint32_t a = s_cnt[2 * threadIdx.x], b = s_cnt[2 * threadIdx.x + 1];
-      const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-      uint32_t x = a + b;
+    if (warp == 0) {
+      uint32_t v = s_w[lane];
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
+        const uint32_t y = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += y;
       }
-      if (lane == 31) s_w[warp] = x;
-      __syncthreads();
-      if (warp == 0) {
-        uint32_t v = s_w[lane];
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const uint32_t y = __shfl_up_sync(0xffffffffu, v, o);
-          if (lane >= o) v += y;
-        }
-        s_w[lane] = v;
-      }
-      __syncthreads();
-      const uint32_t ex = x - (a + b) + (warp ? s_w[warp - 1] : 0);
-      s_off[2 * threadIdx.x] = ex;
-      s_off[2 * threadIdx.x + 1] = ex + a;
+      s_w[lane] = v;
     }
     __syncthreads();
-    for (uint32_t t = threadIdx.x; t < len; t += blockDim.x) {
-      const uint64_t h = s_in[t];
-      const uint32_t p = (uint32_t)(h >> (64 - kSpPartBits));
-      s_out[atomicAdd(&s_off[p], 1u)] = h;  // s_off[p] ends at the next run's start
-    }
-    __syncthreads();
-    for (uint32_t t = threadIdx.x; t < len; t += blockDim.x) {
-      const uint64_t h = s_out[t];
-      const uint32_t p = (uint32_t)(h >> (64 - kSpPartBits));
-      const uint32_t run0 = s_off[p] - s_cnt[p];
-      parted[s_cur[p] + (t - run0)] = h;
-    }
-    __syncthreads();
-    for (uint32_t p = threadIdx.x; p < kSpParts; p += blockDim.x) s_cur[p] += s_cnt[p];
+    const uint32_t ex = x - (a + b) + (warp ? s_w[warp - 1] : 0);
+    s_off[2 * threadIdx.x] = ex;
+    s_off[2 * threadIdx.x + 1] = ex + a;
+    const uint32_t p0 = 2 * threadIdx.x, p1 = p0 + 1;
+    s_base[p0] = a ? atomicAdd(&cur[(size_t)p0 * C + c], a) : 0u;
+    s_base[p1] = b ? atomicAdd(&cur[(size_t)p1 * C + c], b) : 0u;
+  }
+  __syncthreads();
+  for (uint32_t t = threadIdx.x; t < len; t += blockDim.x) {
+    const uint64_t h = s_in[t];
+    const uint32_t p = (uint32_t)(h >> (64 - kSpPartBits));
+    s_out[atomicAdd(&s_off[p], 1u)] = h;  // s_off[p] ends at the next run's start
+  }
+  __syncthreads();
+  for (uint32_t t = threadIdx.x; t < len; t += blockDim.x) {
+    const uint64_t h = s_out[t];
+    const uint32_t p = (uint32_t)(h >> (64 - kSpPartBits));
+    const uint32_t run0 = s_off[p] - s_cnt[p];
+    parted[s_base[p] + (t - run0)] = h;
   }
 }
 
