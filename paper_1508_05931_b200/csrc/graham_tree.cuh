@@ -194,12 +194,16 @@ __device__ __forceinline__ int tree_scan_run(int cnt, const double* cx, const do
   if (p2 != kNone) {
     if (kTreePC >= 2) { s2x = pc.x[kStride + t]; s2y = pc.y[kStride + t]; }
   }
-  for (int k = 0; k < cnt; ++k) {
-    const double px = cx[k * kStride + t], py = cy[k * kStride + t];
-    while (true) {
-      const bool has2 = (top >= 2) || (top == 1 && p1 != kNone) ||
-                        (top == 0 && p1 != kNone && p2 != kNone);
-      if (!has2 || left_turn(s2x, s2y, s1x, s1y, px, py)) break;
+  // One flat loop, each iteration one pop or one push: a warp of divergent
+  // scans then costs max over lanes of (pushes + pops) iterations instead of
+  // the sum over points of the lanes' largest pop run.
+  int k = 0;
+  double px = 0, py = 0;
+  if (cnt > 0) { px = cx[t]; py = cy[t]; }
+  while (k < cnt) {
+    const bool has2 = (top >= 2) || (top == 1 && p1 != kNone) ||
+                      (top == 0 && p1 != kNone && p2 != kNone);
+    if (has2 && !left_turn(s2x, s2y, s1x, s1y, px, py)) {
       if (top >= 1) {
         --top;
       } else {  // pop the persistent top
@@ -231,12 +235,14 @@ __device__ __forceinline__ int tree_scan_run(int cnt, const double* cx, const do
           else { s2x = R_x[p2]; s2y = R_y[p2]; }
         }
       }
+      continue;
     }
     on_push(k, top ? (int)stk[(top - 1) * kStride + t] : -1, p1);
     stk[top * kStride + t] = (uint8_t)k;
     ++top;
     s2x = s1x; s2y = s1y;
     s1x = px; s1y = py;
+    if (++k < cnt) { px = cx[k * kStride + t]; py = cy[k * kStride + t]; }
   }
   (void)deep;
   b1 = p1;

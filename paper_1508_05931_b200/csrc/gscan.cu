@@ -121,6 +121,7 @@ struct gscan_handle {
   uint64_t* sp_dup2 = nullptr;   // partitioned hash list (n)
   uint64_t* sp_side_status = nullptr;  // look-back status of the side stream's scan
   uint32_t* sp_part_cur = nullptr;     // partition cursors of the dup partitioning
+  uint32_t* sp_side_work = nullptr;    // work tickets of the two side kernels
   Counters* sp_side_ticket = nullptr;
   bool sp_debug = false, sp_no_dup = false;
   // captured CUDA graph of the sparse path (sparse_enqueue)
@@ -273,6 +274,12 @@ int reserve(gscan_handle* h, uint64_t n) {
   CU(cudaMalloc(&h->sp_phi32, (m + 1) * sizeof(float)));
   h->cap = n;
   return GSCAN_OK;
+}
+
+// Development switches: set and not "0".
+bool env_flag(const char* name) {
+  const char* v = getenv(name);
+  return v && *v && strcmp(v, "0") != 0;
 }
 
 // ---- launch bookkeeping (counts every kernel; optional per-kernel events) ----
@@ -847,12 +854,13 @@ int sparse_init(gscan_handle* h) {
   CU(cudaMalloc(&h->sp_side_status, ((kSpParts * G + 1 + kScanTile - 1) / kScanTile + 64) * 8));
   CU(cudaMalloc(&h->sp_side_ticket, sizeof(Counters)));
   CU(cudaMalloc(&h->sp_part_cur, ((size_t)G * kSpParts + 1) * 4));
+  CU(cudaMalloc(&h->sp_side_work, 4 * sizeof(uint32_t)));
   CU(cudaMalloc(&h->sp_ccount, G * 4));
   CU(cudaMalloc(&h->sp_hcount, G * 4));
-  h->sp_debug = getenv("GSCAN_SP_DEBUG") != nullptr;
+  h->sp_debug = env_flag("GSCAN_SP_DEBUG");
   // measurement hook only: skipping the duplicate check is exact only for
   // duplicate-free inputs
-  h->sp_no_dup = getenv("GSCAN_SP_NODUP") != nullptr;
+  h->sp_no_dup = env_flag("GSCAN_SP_NODUP");
   CU(cudaMalloc(&h->sp_hist_part, (size_t)G * nb * 4));
   CU(cudaMalloc(&h->sp_phi_part, (size_t)G * nb * 4));
   CU(cudaMalloc(&h->sp_part_off, ((size_t)G * kSpParts + 1) * 4));
@@ -1080,6 +1088,20 @@ int sparse_enqueue(gscan_handle* h, const double* xs, const double* ys, uint32_t
 // Duplicate check on the low-priority side stream, after the sparse graph:
 // it overlaps the host read-back and the Graham tail (which leaves most SMs
 // idle) and is joined before the result is accepted.
+// The side kernels run one CTA per SM except on kSideFreeSms SMs, each
+// reserving kSpSideSmem so that no Graham-tail CTA (kTreeCtaSmem) shares an SM
+// with them: those latency-bound CTAs get SMs of their own (sparse.cuh
+// side_take). Measured: 16-36 free SMs equally good; two smaller side CTAs
+// per SM, or leaving no SM free, slower.
+constexpr uint32_t kSideFreeSms = 24;
+constexpr size_t kSpSideSmem = 180 * 1024;
+static_assert(kSpSideSmem >= kSpDupPartSmem && kSpSideSmem >= kSpDupSlots * 8, "side smem");
+static_assert(kSpSideSmem + 1024 + kTreeCtaSmem + 1024 > 228 * 1024, "tree CTA would fit");
+uint32_t side_free_sms() {
+  static const int v = getenv("GSCAN_SIDE_FREE") ? atoi(getenv("GSCAN_SIDE_FREE")) : (int)kSideFreeSms;
+  return (uint32_t)v;
+}
+
 int sparse_dup_check(gscan_handle* h, uint32_t n) {
   const uint32_t G = (uint32_t)h->sp_grid;
   const uint32_t cap = sparse_region_cap(h, n);
@@ -1095,15 +1117,18 @@ int sparse_dup_check(gscan_handle* h, uint32_t n) {
   }
   CU(cudaMemcpyAsync(h->sp_part_cur, h->sp_part_off, (size_t)kSpParts * G * 4,
                      cudaMemcpyDeviceToDevice, h->side));
+  CU(cudaMemsetAsync(h->sp_side_work, 0, 2 * sizeof(uint32_t), h->side));
   {
     Launch L(h, "k_sp_dup_part", h->side);
     const uint32_t chunks = (cap + kSpPartChunk - 1) / kSpPartChunk;
-    k_sp_dup_part<<<dim3(chunks, G), 1024, kSpDupPartSmem, h->side>>>(
-        h->sp_dup, h->sp_hcount, cap, h->sp_part_cur, h->sp_st, h->sp_dup2);
+    k_sp_dup_part<<<h->sm_count, 1024, kSpSideSmem, h->side>>>(
+        h->sp_dup, h->sp_hcount, cap, chunks, G, h->sp_part_cur, h->sp_st, h->sp_dup2,
+        h->sp_side_work, side_free_sms());
   }
   {
     Launch L(h, "k_sp_dups", h->side);
-    k_sp_dups<<<kSpParts, 512, kSpDupSlots * 8, h->side>>>(h->sp_dup2, h->sp_part_off, G, h->sp_st);
+    k_sp_dups<<<h->sm_count, 512, kSpSideSmem, h->side>>>(h->sp_dup2, h->sp_part_off, G, h->sp_st,
+                                                              h->sp_side_work + 1, side_free_sms());
   }
   CU(cudaEventRecord(h->ev_dup, h->side));
   return GSCAN_OK;
@@ -1364,15 +1389,15 @@ int gscan_create(int device, gscan_handle** out) {
     CU(cudaFuncSetAttribute(k_sp_sort_cand_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)kSpBigSmem));
     CU(cudaFuncSetAttribute(k_sp_dups, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)(kSpDupSlots * 8)));
+                            (int)kSpSideSmem));
     CU(cudaFuncSetAttribute(k_sp_dup_part, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)kSpDupPartSmem));
+                            (int)kSpSideSmem));
     CU(cudaFuncSetAttribute(k_gr_mid, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTreeSmem));
     CU(cudaFuncSetAttribute(k_gr_local0, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTreeCtaSmem));
     CU(cudaFuncSetAttribute(k_gr_down0, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTreeCtaSmem));
     CU(cudaFuncSetAttribute(k_gr_cert, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTreeCtaSmem));
     h->sp_grid = h->sm_count;
-    h->use_graphs = getenv("GSCAN_NO_GRAPH") == nullptr;
+    h->use_graphs = !env_flag("GSCAN_NO_GRAPH");
     return GSCAN_OK;
   };
   rc = init();
@@ -1390,7 +1415,7 @@ int gscan_destroy(gscan_handle* h) {
   if (h->stream) cudaStreamSynchronize(h->stream);
   free_buffers(h);
   dfree(h->partials); dfree(h->ext); dfree(h->ctr); dfree(h->scratch64);
-  dfree(h->sp_th); dfree(h->sp_cdf); dfree(h->sp_cells); dfree(h->sp_big); dfree(h->sp_bigg); dfree(h->sp_gcount); dfree(h->sp_side_status); dfree(h->sp_side_ticket); dfree(h->sp_part_cur); dfree(h->sp_ccount); dfree(h->sp_hcount); dfree(h->sp_hist_part); dfree(h->sp_phi_part); dfree(h->sp_part_off);
+  dfree(h->sp_th); dfree(h->sp_cdf); dfree(h->sp_cells); dfree(h->sp_big); dfree(h->sp_bigg); dfree(h->sp_gcount); dfree(h->sp_side_status); dfree(h->sp_side_ticket); dfree(h->sp_part_cur); dfree(h->sp_side_work); dfree(h->sp_ccount); dfree(h->sp_hcount); dfree(h->sp_hist_part); dfree(h->sp_phi_part); dfree(h->sp_part_off);
   dfree(h->sp_d2); dfree(h->sp_hist); dfree(h->sp_bstart); dfree(h->sp_gbits); dfree(h->sp_glist);
   dfree(h->sp_gcnt); dfree(h->sp_phimax); dfree(h->sp_prefmax); dfree(h->sp_slice);
   dfree(h->sp_ccnt); dfree(h->sp_cstart); dfree(h->sp_wcnt); dfree(h->sp_wstart); dfree(h->sp_rlo);

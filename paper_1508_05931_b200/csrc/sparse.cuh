@@ -806,17 +806,37 @@ __global__ void __launch_bounds__(kSpThreads, 1) k_sp_phi(
   }
 }
 
-// Duplicate check, step 1: CTA (k, c) moves chunk k of F3-CTA c's hash list
-// into the partitions. Within the chunk, entries are grouped by partition in
-// shared memory; each partition's run is reserved with one atomic on the
-// region's cursor (cur[p * C + c], starting at the partition-major exclusive
-// scan of the counts) and written contiguously. Short CTAs, so the main
-// stream's kernels interleave with them.
+__device__ __forceinline__ uint32_t sm_id() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
+
+// Side-stream work distribution. The side kernels run one CTA per SM with
+// enough shared memory reserved that no Graham-tail CTA fits beside them;
+// CTAs placed on the first n_free SMs leave at once, so those SMs stay free
+// for the main stream's latency-bound kernels. Work items come from a ticket.
+__device__ __forceinline__ bool side_take(uint32_t* ticket, uint32_t* s_item, uint32_t n_items,
+                                          uint32_t& w) {
+  if (threadIdx.x == 0) *s_item = atomicAdd(ticket, 1u);
+  __syncthreads();
+  w = *s_item;
+  __syncthreads();  // everyone has read it (and finished the previous item)
+  return w < n_items;
+}
+
+// Duplicate check, step 1: work item (k, c) moves chunk k of F3-CTA c's hash
+// list into the partitions. Within the chunk, entries are grouped by
+// partition in shared memory; each partition's run is reserved with one
+// atomic on the region's cursor (cur[p * C + c], starting at the
+// partition-major exclusive scan of the counts) and written contiguously.
 __global__ void __launch_bounds__(1024) k_sp_dup_part(const uint64_t* __restrict__ hlist,
                                                       const uint32_t* __restrict__ h_count,
-                                                      uint32_t cap, uint32_t* __restrict__ cur,
+                                                      uint32_t cap, uint32_t chunks, uint32_t C,
+                                                      uint32_t* __restrict__ cur,
                                                       const SpState* __restrict__ st,
-                                                      uint64_t* __restrict__ parted) {
+                                                      uint64_t* __restrict__ parted,
+                                                      uint32_t* __restrict__ ticket, uint32_t n_free) {
   extern __shared__ __align__(16) unsigned char smem[];
   uint64_t* s_in = reinterpret_cast<uint64_t*>(smem);
   uint64_t* s_out = s_in + kSpPartChunk;
@@ -824,118 +844,128 @@ __global__ void __launch_bounds__(1024) k_sp_dup_part(const uint64_t* __restrict
   uint32_t* s_off = s_cnt + kSpParts;
   uint32_t* s_base = s_off + kSpParts;
   __shared__ uint32_t s_w[32];
-  if (st->fail) return;
-  const uint32_t c = blockIdx.y, C = gridDim.y;
-  const uint32_t c0 = blockIdx.x * kSpPartChunk;
-  const uint32_t cnt = h_count[c];
-  if (c0 >= cnt) return;
-  const uint32_t len = min(kSpPartChunk, cnt - c0);
-  const uint64_t* src = hlist + (size_t)c * cap + c0;
-  for (uint32_t p = threadIdx.x; p < kSpParts; p += blockDim.x) s_cnt[p] = 0;
-  __syncthreads();
-  for (uint32_t t0 = threadIdx.x; t0 < len; t0 += 8 * blockDim.x) {
-    uint64_t hv[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const uint32_t t = t0 + u * blockDim.x;
-      hv[u] = t < len ? src[t] : 0ull;
-    }
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const uint32_t t = t0 + u * blockDim.x;
-      if (t < len) {
-        s_in[t] = hv[u];
-        atomicAdd(&s_cnt[(uint32_t)(hv[u] >> (64 - kSpPartBits))], 1u);
-      }
-    }
-  }
-  __syncthreads();
-  // exclusive scan of the partition counts (kSpParts = 2 x blockDim), and one
-  // reservation per present partition on the region's cursor
-  {
-    const uint32_t a = s_cnt[2 * threadIdx.x], b = s_cnt[2 * threadIdx.x + 1];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint32_t x = a + b;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
-    }
-    if (lane == 31) s_w[warp] = x;
+  __shared__ uint32_t s_item;
+  if (st->fail || sm_id() < n_free) return;
+  uint32_t w;
+  while (side_take(ticket, &s_item, chunks * C, w)) {
+    const uint32_t c = w / chunks;
+    const uint32_t c0 = (w % chunks) * kSpPartChunk;
+    const uint32_t cnt = h_count[c];
+    if (c0 >= cnt) continue;  // uniform per CTA
+    const uint32_t len = min(kSpPartChunk, cnt - c0);
+    const uint64_t* src = hlist + (size_t)c * cap + c0;
+    for (uint32_t p = threadIdx.x; p < kSpParts; p += blockDim.x) s_cnt[p] = 0;
     __syncthreads();
-    if (warp == 0) {
-      uint32_t v = s_w[lane];
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, v, o);
-        if (lane >= o) v += y;
-      }
-      s_w[lane] = v;
-    }
-    __syncthreads();
-    const uint32_t ex = x - (a + b) + (warp ? s_w[warp - 1] : 0);
-    s_off[2 * threadIdx.x] = ex;
-    s_off[2 * threadIdx.x + 1] = ex + a;
-    const uint32_t p0 = 2 * threadIdx.x, p1 = p0 + 1;
-    s_base[p0] = a ? atomicAdd(&cur[(size_t)p0 * C + c], a) : 0u;
-    s_base[p1] = b ? atomicAdd(&cur[(size_t)p1 * C + c], b) : 0u;
-  }
-  __syncthreads();
-  for (uint32_t t = threadIdx.x; t < len; t += blockDim.x) {
-    const uint64_t h = s_in[t];
-    const uint32_t p = (uint32_t)(h >> (64 - kSpPartBits));
-    s_out[atomicAdd(&s_off[p], 1u)] = h;  // s_off[p] ends at the next run's start
-  }
-  __syncthreads();
-  for (uint32_t t = threadIdx.x; t < len; t += blockDim.x) {
-    const uint64_t h = s_out[t];
-    const uint32_t p = (uint32_t)(h >> (64 - kSpPartBits));
-    const uint32_t run0 = s_off[p] - s_cnt[p];
-    parted[s_base[p] + (t - run0)] = h;
-  }
-}
-
-// Duplicate check, step 2: CTA per partition, open-addressing set of the
-// 64-bit hashes in shared memory (in rounds over sub-ranges of the hash);
-// an equal hash means a possible duplicate -> the full path (exact).
-__global__ void __launch_bounds__(512) k_sp_dups(const uint64_t* __restrict__ parted,
-                                                 const uint32_t* __restrict__ part_off,
-                                                 uint32_t nparts_cta, SpState* __restrict__ st) {
-  extern __shared__ unsigned long long s_e[];  // kSpDupSlots
-  if (st->fail) return;
-  const uint32_t total = st->m;
-  const uint32_t p = blockIdx.x;
-  const uint32_t lo = part_off[(size_t)p * nparts_cta];
-  const uint32_t hi = (p + 1 < kSpParts) ? part_off[(size_t)(p + 1) * nparts_cta] : total;
-  const uint32_t rounds = (hi - lo + kSpDupRound - 1) / kSpDupRound;
-  bool dup = false, full = false;
-  for (uint32_t r = 0; r < rounds; ++r) {
-    for (uint32_t k = threadIdx.x; k < kSpDupSlots; k += blockDim.x) s_e[k] = ~0ull;
-    __syncthreads();
-    for (uint32_t e0 = lo + threadIdx.x; e0 < hi && !dup && !full; e0 += 8 * blockDim.x) {
+    for (uint32_t t0 = threadIdx.x; t0 < len; t0 += 8 * blockDim.x) {
       uint64_t hv[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        const uint32_t e = e0 + u * blockDim.x;
-        hv[u] = e < hi ? parted[e] : ~0ull;
+        const uint32_t t = t0 + u * blockDim.x;
+        hv[u] = t < len ? src[t] : 0ull;
       }
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        const uint64_t h = hv[u];
-        if (h == ~0ull || dup || full) continue;
-        const uint32_t mid = (uint32_t)(h >> 20) & 0xffffu;  // bits below the partition
-        if ((uint32_t)(((uint64_t)mid * rounds) >> 16) != r) continue;
-        uint32_t slot = (uint32_t)h & (kSpDupSlots - 1);
-        for (uint32_t probe = 0;; ++probe) {
-          if (probe == kSpDupSlots / 2) { full = true; break; }
-          const unsigned long long prev = atomicCAS(&s_e[slot], ~0ull, (unsigned long long)h);
-          if (prev == ~0ull) break;
-          if (prev == h) { dup = true; break; }
-          slot = (slot + 1) & (kSpDupSlots - 1);
+        const uint32_t t = t0 + u * blockDim.x;
+        if (t < len) {
+          s_in[t] = hv[u];
+          atomicAdd(&s_cnt[(uint32_t)(hv[u] >> (64 - kSpPartBits))], 1u);
         }
       }
     }
-    if (__syncthreads_or(dup || full)) break;
+    __syncthreads();
+    // exclusive scan of the partition counts (kSpParts = 2 x blockDim), and
+    // one reservation per present partition on the region's cursor
+    {
+      const uint32_t a = s_cnt[2 * threadIdx.x], b = s_cnt[2 * threadIdx.x + 1];
+      const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+      uint32_t x = a + b;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (lane == 31) s_w[warp] = x;
+      __syncthreads();
+      if (warp == 0) {
+        uint32_t v = s_w[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, v, o);
+          if (lane >= o) v += y;
+        }
+        s_w[lane] = v;
+      }
+      __syncthreads();
+      const uint32_t ex = x - (a + b) + (warp ? s_w[warp - 1] : 0);
+      s_off[2 * threadIdx.x] = ex;
+      s_off[2 * threadIdx.x + 1] = ex + a;
+      const uint32_t p0 = 2 * threadIdx.x, p1 = p0 + 1;
+      s_base[p0] = a ? atomicAdd(&cur[(size_t)p0 * C + c], a) : 0u;
+      s_base[p1] = b ? atomicAdd(&cur[(size_t)p1 * C + c], b) : 0u;
+    }
+    __syncthreads();
+    for (uint32_t t = threadIdx.x; t < len; t += blockDim.x) {
+      const uint64_t h = s_in[t];
+      const uint32_t p = (uint32_t)(h >> (64 - kSpPartBits));
+      s_out[atomicAdd(&s_off[p], 1u)] = h;  // s_off[p] ends at the next run's start
+    }
+    __syncthreads();
+    for (uint32_t t = threadIdx.x; t < len; t += blockDim.x) {
+      const uint64_t h = s_out[t];
+      const uint32_t p = (uint32_t)(h >> (64 - kSpPartBits));
+      const uint32_t run0 = s_off[p] - s_cnt[p];
+      parted[s_base[p] + (t - run0)] = h;
+    }
+  }
+}
+
+// Duplicate check, step 2: a partition per work item, open-addressing set of
+// its 64-bit hashes in shared memory (in rounds over sub-ranges of the hash);
+// an equal hash means a possible duplicate -> the full path (exact).
+__global__ void __launch_bounds__(512) k_sp_dups(const uint64_t* __restrict__ parted,
+                                                 const uint32_t* __restrict__ part_off,
+                                                 uint32_t nparts_cta, SpState* __restrict__ st,
+                                                 uint32_t* __restrict__ ticket, uint32_t n_free) {
+  extern __shared__ unsigned long long s_e[];  // kSpDupSlots
+  __shared__ uint32_t s_item;
+  if (st->fail || sm_id() < n_free) return;
+  const uint32_t total = st->m;
+  bool dup = false, full = false;
+  uint32_t p;
+  while (side_take(ticket, &s_item, kSpParts, p)) {
+    const uint32_t lo = part_off[(size_t)p * nparts_cta];
+    const uint32_t hi = (p + 1 < kSpParts) ? part_off[(size_t)(p + 1) * nparts_cta] : total;
+    const uint32_t rounds = (hi - lo + kSpDupRound - 1) / kSpDupRound;
+    bool stop = false;
+    for (uint32_t r = 0; r < rounds; ++r) {
+      for (uint32_t k = threadIdx.x; k < kSpDupSlots; k += blockDim.x) s_e[k] = ~0ull;
+      __syncthreads();
+      for (uint32_t e0 = lo + threadIdx.x; e0 < hi && !dup && !full; e0 += 8 * blockDim.x) {
+        uint64_t hv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const uint32_t e = e0 + u * blockDim.x;
+          hv[u] = e < hi ? parted[e] : ~0ull;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const uint64_t h = hv[u];
+          if (h == ~0ull || dup || full) continue;
+          const uint32_t mid = (uint32_t)(h >> 20) & 0xffffu;  // bits below the partition
+          if ((uint32_t)(((uint64_t)mid * rounds) >> 16) != r) continue;
+          uint32_t slot = (uint32_t)h & (kSpDupSlots - 1);
+          for (uint32_t probe = 0;; ++probe) {
+            if (probe == kSpDupSlots / 2) { full = true; break; }
+            const unsigned long long prev = atomicCAS(&s_e[slot], ~0ull, (unsigned long long)h);
+            if (prev == ~0ull) break;
+            if (prev == h) { dup = true; break; }
+            slot = (slot + 1) & (kSpDupSlots - 1);
+          }
+        }
+      }
+      if (__syncthreads_or(dup || full)) { stop = true; break; }
+    }
+    if (stop) break;  // uniform
   }
   if (dup) { atomicAdd(&st->dups, 1u); atomicOr(&st->fail, kSpFailDup); }
   if (full) atomicOr(&st->fail, kSpFailCap);
