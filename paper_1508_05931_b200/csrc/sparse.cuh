@@ -232,6 +232,24 @@ __device__ __forceinline__ double sp_phi_raw(double px, double py, double lx, do
   return sn >= 0.0 ? t : -t;
 }
 
+// Prefetch distance of the streaming passes, in loop iterations.
+constexpr int kSpPrefetch = 1;
+
+// Threads u < kPairs of a CTA prefetch run u of the CTA's grid-stride tile
+// kSpPrefetch iterations ahead (p: this thread's pair index, np pairs).
+template <int kPairs>
+__device__ __forceinline__ void sp_prefetch_next(const double2* x2, const double2* y2,
+                                                 const uint32_t* c2, uint32_t p, uint32_t np,
+                                                 uint32_t nth) {
+  if (threadIdx.x >= kPairs) return;
+  const uint32_t q = (p - threadIdx.x) + (uint32_t)(kSpPrefetch * kPairs + threadIdx.x) * nth;
+  if (q >= np) return;
+  const uint32_t len = min(blockDim.x, np - q);
+  l2_prefetch(&x2[q], len * 16);
+  l2_prefetch(&y2[q], len * 16);
+  if (c2 && len >= 4) l2_prefetch(&c2[q], (len & ~3u) * 4);
+}
+
 // Streaming helper: visits every point i of [0, n) once across the grid,
 // 128-bit loads, kPairs pairs in flight per thread. f(x, y, i).
 template <bool kVec, int kPairs, typename F>
@@ -285,6 +303,7 @@ __device__ __forceinline__ void sp_stream_coded(const double* __restrict__ xs,
     const uint32_t np = n / 2;
     uint32_t p = tid;
     for (; p + (kPairs - 1) * nth < np; p += kPairs * nth) {
+      sp_prefetch_next<kPairs>(x2, y2, c2, p, np, nth);
       double2 vx[kPairs], vy[kPairs];
       uint32_t vc[kPairs];
 #pragma unroll
@@ -442,6 +461,67 @@ __global__ void k_sp_reduce_cols(const uint32_t* __restrict__ part, uint32_t row
   out[b] = v;
 }
 
+// F2's per-point work for B points at once, as branch-free phases (quad test,
+// pseudo-angle, CDF lookup) so the independent FP64 chains interleave; only
+// the rare guard-band case branches (sp_bucket's exact fallback). Same
+// arithmetic, same result as visiting the points one by one.
+template <int B>
+__device__ __forceinline__ void f2_batch(const double (&x)[B], const double (&y)[B],
+                                         const uint32_t (&idx)[B], uint32_t (&code)[B],
+                                         const SpQuad& q, const double* s_cdf,
+                                         const double* __restrict__ th, uint32_t* s_hist,
+                                         uint32_t& n1, uint64_t& bd2, uint32_t& bidx,
+                                         uint32_t& bties) {
+  double dx[B], dy[B], u[B];
+  bool live[B], oks[B];
+#pragma unroll
+  for (int k = 0; k < B; ++k) {
+    bool inside = true;  // strictly Left of all four edges (classify_quad flag 0)
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      inside = inside & (cross_edge(q.qx[e], q.qy[e], q.ex[e], q.ey[e], x[k], y[k]) > 0.0);
+    n1 += inside ? 0u : 1u;
+    live[k] = !inside && !(x[k] == q.ax && y[k] == q.ay);
+    dx[k] = __dsub_rn(x[k], q.ax);
+    dy[k] = __dsub_rn(y[k], q.ay);
+    const double den = __dadd_rn(fabs(dx[k]), dy[k]);
+    const bool okd = den > 1e-290;
+    const double sv = __dmul_rn(__dsub_rn(1.0, __dmul_rn(dx[k], sp_rcp(okd ? den : 1.0))), 0.5);
+    oks[k] = okd && sv >= 0.0 && sv <= 1.0;
+    u[k] = __dmul_rn(oks[k] ? sv : 0.0, (double)kSpCells);
+  }
+  bool fast[B];
+#pragma unroll
+  for (int k = 0; k < B; ++k) {
+    uint32_t j = (uint32_t)u[k];
+    if (j > kSpCells - 1) j = kSpCells - 1;
+    const double c0 = s_cdf[j], c1 = s_cdf[j + 1];
+    const double v = __dmul_rn(__fma_rn(__dsub_rn(u[k], (double)j), __dsub_rn(c1, c0), c0),
+                               (double)kSpBuckets);
+    const bool inr = v >= 0.0 && v < (double)kSpBuckets;
+    const uint32_t b = inr ? (uint32_t)v : (v >= (double)kSpBuckets ? kSpBuckets - 1 : 0u);
+    const double f = __dsub_rn(v, (double)b);
+    fast[k] = oks[k] && inr && f > kSpGuardV && f < 1.0 - kSpGuardV;
+    code[k] = oks[k] ? b : 0u;
+  }
+#pragma unroll
+  for (int k = 0; k < B; ++k) {
+    if (!live[k]) { code[k] = kSpNoCode; continue; }
+    uint32_t b = code[k];
+    if (!fast[k]) {  // exact key against th[] (sp_bucket's fallback)
+      const double a = bitsd(angle_key(dx[k], dy[k]));
+      while (b > 0 && a < th[b]) --b;
+      while (b + 1 < kSpBuckets && a >= th[b + 1]) ++b;
+    }
+    code[k] = b;
+    atomicAdd(&s_hist[b], 1u);
+    const uint64_t d2 = dbits(dist2_rn(dx[k], dy[k]));
+    const uint32_t i = idx[k];
+    if (bidx == 0xffffffffu || d2 > bd2) { bd2 = d2; bidx = i; bties = 1; }
+    else if (d2 == bd2) { ++bties; if (i < bidx) bidx = i; }
+  }
+}
+
 // ===========================================================================
 // F2: round 1 + bucket histogram + argmax dist2 + hash-partition counts.
 // The quad test is classify_quad (prefilter.hpp:47-63); n_after_round1 counts
@@ -485,6 +565,7 @@ __global__ void __launch_bounds__(kSpThreads, 1) k_sp_hist(
       uint32_t p = tid;
       constexpr int kP = 4;
       for (; p + (kP - 1) * nth < np; p += kP * nth) {
+        sp_prefetch_next<kP>(x2, y2, nullptr, p, np, nth);
         double2 vx[kP], vy[kP];
 #pragma unroll
         for (int u = 0; u < kP; ++u) {
@@ -492,11 +573,15 @@ __global__ void __launch_bounds__(kSpThreads, 1) k_sp_hist(
           vy[u] = __ldcs(&y2[p + u * nth]);
         }
 #pragma unroll
-        for (int u = 0; u < kP; ++u) {
-          const uint32_t i = 2 * (p + u * nth);
-          const uint32_t c0 = visit(vx[u].x, vy[u].x, i);
-          const uint32_t c1 = visit(vx[u].y, vy[u].y, i + 1);
-          c2[p + u * nth] = c0 | (c1 << 16);
+        for (int g = 0; g < kP; g += 2) {  // batches of 4 points (8 measured slower)
+          const double bx[4] = {vx[g].x, vx[g].y, vx[g + 1].x, vx[g + 1].y};
+          const double by[4] = {vy[g].x, vy[g].y, vy[g + 1].x, vy[g + 1].y};
+          const uint32_t i0 = 2 * (p + g * nth), i1 = 2 * (p + (g + 1) * nth);
+          const uint32_t bi[4] = {i0, i0 + 1, i1, i1 + 1};
+          uint32_t bc[4];
+          f2_batch<4>(bx, by, bi, bc, q, s_cdf, th, s_hist, n1, bd2, bidx, bties);
+          c2[p + g * nth] = bc[0] | (bc[1] << 16);
+          c2[p + (g + 1) * nth] = bc[2] | (bc[3] << 16);
         }
       }
       for (; p < np; p += nth) {
@@ -732,6 +817,21 @@ __device__ __forceinline__ uint32_t warp_claim(uint32_t* s_counter, bool want) {
   return base + __popc(em & lanemask_lt());
 }
 
+// Full-warp claim of cnt slots per lane: one shared-memory atomic per warp;
+// returns this lane's first slot. All 32 lanes must call it.
+__device__ __forceinline__ uint32_t warp_scan_claim(uint32_t* s_counter, uint32_t cnt, uint32_t lane) {
+  uint32_t incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= (uint32_t)o) incl += y;
+  }
+  uint32_t base = 0;
+  if (lane == 31 && incl) base = atomicAdd(s_counter, incl);
+  base = __shfl_sync(0xffffffffu, base, 31);
+  return base + incl - cnt;
+}
+
 // ===========================================================================
 // F3: gathered points are emitted (index, bucket); other survivors fold phi
 // into the per-CTA bucket maximum; every bucketed survivor's 64-bit hash goes
@@ -760,7 +860,7 @@ __global__ void __launch_bounds__(kSpThreads, 1) k_sp_phi(
   const size_t base = (size_t)blockIdx.x * cap;
   double plo = 3.0, phi_ = -3.0;
   __syncthreads();
-  sp_stream_coded<kVec, 4>(xs, ys, codes, n, [&](double x, double y, uint32_t b, uint32_t i) {
+  auto visit = [&](double x, double y, uint32_t b, uint32_t i) {
     const bool surv = b != kSpNoCode;
     bool emit = false;
     uint64_t h = 0;
@@ -784,7 +884,102 @@ __global__ void __launch_bounds__(kSpThreads, 1) k_sp_phi(
     if (surv) hlist[base + jh] = h;
     const uint32_t jg = warp_claim(&s_ng, emit);
     if (emit) { g_idx[base + jg] = i; g_b[base + jg] = b; }
-  });
+  };
+  // batch of 4 points: the same work as visit() in branch-free phases, and one
+  // warp-scan claim per batch instead of a ballot claim per point
+  auto batch = [&](const double (&x)[4], const double (&y)[4], const uint32_t (&b)[4],
+                   const uint32_t (&idx)[4]) {
+    double raw[4], v2[4];
+    uint64_t h[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      h[k] = coord_hash64(x[k], y[k]);
+      const double vx = __dsub_rn(x[k], lx), vy = __dsub_rn(y[k], ly);
+      v2[k] = __fma_rn(vx, vx, __dmul_rn(vy, vy));
+      const double c = __fma_rn(ux, vx, __dmul_rn(uy, vy));
+      const double sn = __fma_rn(ux, vy, -__dmul_rn(uy, vx));
+      const double den = fabs(c) + fabs(sn);
+      const bool okd = den > 1e-290;
+      const double t = 1.0 - c * sp_rcp(okd ? den : 1.0);
+      raw[k] = okd ? (sn >= 0.0 ? t : -t) : 0.0;  // sp_phi_raw
+    }
+    uint32_t nh = 0, ng = 0;
+    bool gat[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const bool surv = b[k] != kSpNoCode;
+      gat[k] = false;
+      if (!surv) continue;
+      ++nh;
+      atomicAdd(&s_part[(uint32_t)(h[k] >> (64 - kSpPartBits))], 1u);
+      plo = fmin(plo, raw[k]);
+      phi_ = fmax(phi_, raw[k]);
+      gat[k] = sp_gathered(s_g, b[k]);
+      if (gat[k]) {
+        ++ng;
+      } else if (v2[k] >= r02) {  // points within r0 of P_l never raise a maximum (certificate)
+        atomicMax(&s_phi[b[k]], ord_f(__double2float_rd(b[k] < b_l ? raw[k] : -raw[k])));
+        phi32[idx[k]] = __double2float_rn(raw[k]);  // F4 reads it instead of recomputing
+      } else {
+        phi32[idx[k]] = __int_as_float(0x7fc00000);  // NaN: always a candidate
+      }
+    }
+    const uint32_t lane = threadIdx.x & 31;
+    uint32_t at = warp_scan_claim(&s_nh, nh, lane);
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (b[k] != kSpNoCode) hlist[base + at++] = h[k];
+    if (__any_sync(0xffffffffu, ng != 0)) {
+      uint32_t ag = warp_scan_claim(&s_ng, ng, lane);
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (gat[k]) { g_idx[base + ag] = idx[k]; g_b[base + ag] = b[k]; ++ag; }
+    }
+  };
+  {
+    const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t nth = gridDim.x * blockDim.x;
+    const uint32_t lane = threadIdx.x & 31;
+    if (kVec) {
+      const double2* x2 = reinterpret_cast<const double2*>(xs);
+      const double2* y2 = reinterpret_cast<const double2*>(ys);
+      const uint32_t* c2 = reinterpret_cast<const uint32_t*>(codes);
+      const uint32_t np = n / 2;
+      uint32_t p = tid;
+      constexpr int kP = 4;
+      // warp-uniform bound: the batch claims are warp-synchronous
+      for (; (p - lane) + 31 + (kP - 1) * nth < np; p += kP * nth) {
+        sp_prefetch_next<kP>(x2, y2, c2, p, np, nth);
+        double2 vx[kP], vy[kP];
+        uint32_t vc[kP];
+#pragma unroll
+        for (int u = 0; u < kP; ++u) vc[u] = __ldcs(&c2[p + u * nth]);
+#pragma unroll
+        for (int u = 0; u < kP; ++u) {
+          vx[u] = __ldcs(&x2[p + u * nth]);
+          vy[u] = __ldcs(&y2[p + u * nth]);
+        }
+#pragma unroll
+        for (int g = 0; g < kP; g += 2) {
+          const double bx[4] = {vx[g].x, vx[g].y, vx[g + 1].x, vx[g + 1].y};
+          const double by[4] = {vy[g].x, vy[g].y, vy[g + 1].x, vy[g + 1].y};
+          const uint32_t bb[4] = {vc[g] & 0xffffu, vc[g] >> 16, vc[g + 1] & 0xffffu, vc[g + 1] >> 16};
+          const uint32_t i0 = 2 * (p + g * nth), i1 = 2 * (p + (g + 1) * nth);
+          const uint32_t bi[4] = {i0, i0 + 1, i1, i1 + 1};
+          batch(bx, by, bb, bi);
+        }
+      }
+      for (; p < np; p += nth) {
+        const uint32_t vc = c2[p];
+        const double2 vx = __ldcs(&x2[p]), vy = __ldcs(&y2[p]);
+        visit(vx.x, vy.x, vc & 0xffffu, 2 * p);
+        visit(vx.y, vy.y, vc >> 16, 2 * p + 1);
+      }
+      if ((n & 1) && tid == nth - 1) visit(xs[n - 1], ys[n - 1], (uint32_t)codes[n - 1], n - 1);
+    } else {
+      for (uint32_t i = tid; i < n; i += nth) visit(xs[i], ys[i], (uint32_t)codes[i], i);
+    }
+  }
   __syncthreads();
   uint32_t* pp = phi_part + (size_t)blockIdx.x * kSpBuckets;
   for (uint32_t b = threadIdx.x; b < kSpBuckets; b += blockDim.x) pp[b] = s_phi[b];
