@@ -123,13 +123,6 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* s
   return warp_excl + x - v;
 }
 
-// L2 prefetch of a contiguous range (16 B aligned, multiple of 16 B) by the
-// bulk-copy engine: one instruction, no registers. The streaming passes issue
-// it for their next grid-stride tiles so the loads find them in L2.
-__device__ __forceinline__ void l2_prefetch(const void* p, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
-
 __device__ __forceinline__ uint32_t lanemask_lt() {
   uint32_t m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));

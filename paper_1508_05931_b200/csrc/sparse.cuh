@@ -232,24 +232,6 @@ __device__ __forceinline__ double sp_phi_raw(double px, double py, double lx, do
   return sn >= 0.0 ? t : -t;
 }
 
-// Prefetch distance of the streaming passes, in loop iterations.
-constexpr int kSpPrefetch = 1;
-
-// Threads u < kPairs of a CTA prefetch run u of the CTA's grid-stride tile
-// kSpPrefetch iterations ahead (p: this thread's pair index, np pairs).
-template <int kPairs>
-__device__ __forceinline__ void sp_prefetch_next(const double2* x2, const double2* y2,
-                                                 const uint32_t* c2, uint32_t p, uint32_t np,
-                                                 uint32_t nth) {
-  if (threadIdx.x >= kPairs) return;
-  const uint32_t q = (p - threadIdx.x) + (uint32_t)(kSpPrefetch * kPairs + threadIdx.x) * nth;
-  if (q >= np) return;
-  const uint32_t len = min(blockDim.x, np - q);
-  l2_prefetch(&x2[q], len * 16);
-  l2_prefetch(&y2[q], len * 16);
-  if (c2 && len >= 4) l2_prefetch(&c2[q], (len & ~3u) * 4);
-}
-
 // Streaming helper: visits every point i of [0, n) once across the grid,
 // 128-bit loads, kPairs pairs in flight per thread. f(x, y, i).
 template <bool kVec, int kPairs, typename F>
@@ -303,7 +285,6 @@ __device__ __forceinline__ void sp_stream_coded(const double* __restrict__ xs,
     const uint32_t np = n / 2;
     uint32_t p = tid;
     for (; p + (kPairs - 1) * nth < np; p += kPairs * nth) {
-      sp_prefetch_next<kPairs>(x2, y2, c2, p, np, nth);
       double2 vx[kPairs], vy[kPairs];
       uint32_t vc[kPairs];
 #pragma unroll
@@ -565,7 +546,6 @@ __global__ void __launch_bounds__(kSpThreads, 1) k_sp_hist(
       uint32_t p = tid;
       constexpr int kP = 4;
       for (; p + (kP - 1) * nth < np; p += kP * nth) {
-        sp_prefetch_next<kP>(x2, y2, nullptr, p, np, nth);
         double2 vx[kP], vy[kP];
 #pragma unroll
         for (int u = 0; u < kP; ++u) {
@@ -949,7 +929,6 @@ __global__ void __launch_bounds__(kSpThreads, 1) k_sp_phi(
       constexpr int kP = 4;
       // warp-uniform bound: the batch claims are warp-synchronous
       for (; (p - lane) + 31 + (kP - 1) * nth < np; p += kP * nth) {
-        sp_prefetch_next<kP>(x2, y2, c2, p, np, nth);
         double2 vx[kP], vy[kP];
         uint32_t vc[kP];
 #pragma unroll
