@@ -1,17 +1,17 @@
 // K7/K8 tree strategy: graham_finalize (pipeline.hpp:57-67) for buffers where
-// most points are popped (round-2 output of squares and disks), as ONE kernel
-// (one CTA, no host round trips).
+// most points are popped (round-2 output of squares and disks).
 //
 // Warp-speculative scans advance 32 points per iteration only while nothing is
 // popped; on these buffers nearly every point pops, so here every scan is a
-// plain sequential stack scan run by ONE thread (~2 orient() per point), and
-// the parallelism comes from running many short ones:
+// plain sequential stack scan run by ONE thread, and the parallelism comes
+// from running many short ones:
 //
-//   up      level j: Q_j (R positions; Q_0 = the buffer) is cut into chunks of
-//           kTreeChunk; every chunk's scan from an empty stack leaves a chain;
-//           the chains concatenated form Q_{j+1}. Repeat until Q_K is small.
+//   up      level j: Q_j (R positions + coordinates; Q_0 = the buffer) is cut
+//           into chunks of kTreeChunk; every chunk's scan from an empty stack
+//           leaves a chain; the chains concatenated form Q_{j+1}. Repeat until
+//           Q_K is small.
 //   top     one thread scans Q_K, recording the persistent stack (parent[p] =
-//           the element below p when p was pushed) and the top before every
+//           the element below p when p was pushed) and the state before every
 //           Q_{K-1} chunk.
 //   down    level j -> j-1: the state before a Q_{j-1} chunk is the state
 //           before the Q_j chunk holding its chain's first element, scanned
@@ -26,29 +26,50 @@
 // which exact geometry guarantees; rounding can only make the certificate
 // fail, never a wrong hull: by induction over chunks, certified states are the
 // sequential scan's states.
+//
+// Stack representation inside one scan: shared-memory rows [0, top) of the
+// thread's column (coordinates, R position, chunk index), on top of a chain in
+// global memory that starts at B (the element below row 0) and continues
+// through parent[]. A state handed between levels is a boundary record: its
+// top kTreePC rows (bottom-aligned) and the element below them. The chunk's
+// own points are staged in rows kTreePC.. and pushes overwrite rows in place
+// (a push lands at row <= kTreePC + k, never above the next unread point), so
+// the common pop and push are one shared-memory access each.
 #pragma once
 #include "graham.cuh"
 
 namespace gscan {
 
-constexpr int kTreeChunk = 32;      // level-0 chunk (many CTAs); also the staging capacity
-constexpr int kTreeChunkHi = 32;    // chunk of levels >= 1 (8 and 16 measured slower: per-level overhead dominates)
-constexpr int kTreeThreads = 256;   // one CTA; chunks are processed in waves of this many
+constexpr int kTreeChunk = 32;      // chunk length on every level
+constexpr int kTreeThreads = 256;   // the middle CTA; chunks are processed in waves of this many
 constexpr uint32_t kTreeTop = 128;  // largest top-level list for the single-thread scan
-constexpr int kTreeMaxLevels = 32;
-// shared memory: per thread a chunk's coordinates [k][t] and an index stack
-// per-thread slot: chunk coordinates + positions (21 B per point) + the
-// persistent-stack cache (20 B per cached element)
-constexpr size_t tree_smem(int threads) {
-  return (size_t)kTreeChunk * threads * (8 + 8 + 4 + 1) + (size_t)8 * threads * (4 + 8 + 8);
-}
-constexpr size_t kTreeSmem = tree_smem(256);
+constexpr int kTreeMaxLevels = 24;
+constexpr int kTreePC = 8;          // stack rows carried in a boundary record
+constexpr int kTreeRows = kTreePC + kTreeChunk;
+constexpr uint32_t kTreeHiCap = 1u << 18;  // level >= 1 capacity (larger: another strategy)
+constexpr uint8_t kTreeRec = 0xff;  // chunk index of a row loaded from a record
+
+// shared memory: per thread kTreeRows rows of (x, y, position, chunk index)
+constexpr size_t tree_smem(int threads) { return (size_t)kTreeRows * threads * (8 + 8 + 4 + 1); }
+constexpr size_t kTreeSmem = tree_smem(kTreeThreads);
+
+// Boundary records of one level: the state before each chunk.
+struct TreeRec {
+  uint32_t* n;      // rows recorded (<= kTreePC)
+  uint32_t* below;  // element below the recorded rows (kNone: none)
+  uint32_t* pos;    // [c * kTreePC + d], d = 0 the deepest recorded row
+  double* x;
+  double* y;
+};
 
 struct TreeLevel {
-  uint32_t* Q;    // R positions (nullptr: identity, level 0)
+  uint32_t* Qp;  // R positions (level >= 1)
+  double* Qx;
+  double* Qy;
   uint32_t* up;   // Q_{j-1} index of each element (level >= 1)
   uint32_t* off;  // chain offsets of this level's chunks in Q_{j+1} (nch + 1)
   uint32_t* bt;   // top before each chunk (nch + 1)
+  TreeRec rec;
   uint32_t nq, nch;
 };
 
@@ -56,16 +77,20 @@ struct TreeLevel {
 // level size against its capacity.
 struct TreeWork {
   uint32_t* parent;  // N
-  uint32_t* tmp;     // N (stack of the top-level / fallback scan)
+  uint32_t* tmp;     // N (fallback stack; top-scan boundary tops)
   uint32_t* chainq;  // N: chain elements of the current level (Q index), chunk-strided
-  uint32_t* chainp;  // N: the same elements' R positions
-  uint32_t* len;     // ceil(N / kTreeChunk) + 1
+  uint32_t* chainp;  // N: their R positions
+  double* chainx;    // N: their coordinates
+  double* chainy;
   uint32_t* fstack;  // kTreeTop
-  uint32_t* Qbuf[kTreeMaxLevels + 1];
-  uint32_t* upbuf[kTreeMaxLevels + 1];
-  uint32_t* offbuf[kTreeMaxLevels + 1];
-  uint32_t* btbuf[kTreeMaxLevels + 1];
-  uint32_t cap[kTreeMaxLevels + 1];  // element capacity of level j's Q / up
+  uint32_t* Qp[kTreeMaxLevels + 1];
+  double* Qx[kTreeMaxLevels + 1];
+  double* Qy[kTreeMaxLevels + 1];
+  uint32_t* up[kTreeMaxLevels + 1];
+  uint32_t* off[kTreeMaxLevels + 1];
+  uint32_t* bt[kTreeMaxLevels + 1];
+  TreeRec rec[kTreeMaxLevels + 1];
+  uint32_t cap[kTreeMaxLevels + 1];  // element capacity of level j
 };
 
 // CTA-wide exclusive scan of cnt uint32 (in place); returns the total.
@@ -104,287 +129,362 @@ __device__ uint32_t tree_scan(uint32_t* a, uint32_t cnt, uint32_t* s_w, uint32_t
   return *s_carry;
 }
 
-// Stage up to kTreeChunk coordinates of run elements pos(0..cnt) into this
-// thread's slots [k][t] (8 independent loads in flight).
-template <int kStride, typename PosF>
-__device__ __forceinline__ void tree_stage(PosF&& pos, int cnt, const double* __restrict__ R_x,
-                                           const double* __restrict__ R_y, double* cx, double* cy,
-                                           uint32_t* cp) {
-  const int t = threadIdx.x;
-  for (int k0 = 0; k0 < cnt; k0 += 8) {
-    uint32_t pp[8];
-    double vx[8], vy[8];
+// The thread's rows, [row][thread] so any mix of rows across a warp is
+// bank-conflict free.
+template <int T>
+struct TreeRows {
+  double* X;
+  double* Y;
+  uint32_t* P;
+  uint8_t* K;
+  __device__ explicit TreeRows(double* base) {
+    X = base;
+    Y = X + kTreeRows * T;
+    P = reinterpret_cast<uint32_t*>(Y + kTreeRows * T);
+    K = reinterpret_cast<uint8_t*>(P + kTreeRows * T);
+  }
+  __device__ __forceinline__ int at(int row) const { return row * T + (int)threadIdx.x; }
+};
+
+// Stage run elements [base, base + cnt) into rows kTreePC + k (16 loads in
+// flight). qp == nullptr: positions are base + k (level 0).
+template <int T>
+__device__ __forceinline__ void tree_stage(const TreeRows<T>& r, const uint32_t* __restrict__ qp,
+                                           const double* __restrict__ qx,
+                                           const double* __restrict__ qy, uint32_t base, int cnt) {
+  for (int k0 = 0; k0 < cnt; k0 += 16) {
+    double vx[16], vy[16];
+    uint32_t vp[16];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) pp[u] = (k0 + u < cnt) ? pos(k0 + u) : 0u;
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      vx[u] = (k0 + u < cnt) ? R_x[pp[u]] : 0.0;
-      vy[u] = (k0 + u < cnt) ? R_y[pp[u]] : 0.0;
+    for (int u = 0; u < 16; ++u) {
+      const bool in = k0 + u < cnt;
+      vx[u] = in ? qx[base + k0 + u] : 0.0;
+      vy[u] = in ? qy[base + k0 + u] : 0.0;
+      vp[u] = in ? (qp ? qp[base + k0 + u] : base + k0 + u) : 0u;
     }
 #pragma unroll
-    for (int u = 0; u < 8; ++u)
+    for (int u = 0; u < 16; ++u)
       if (k0 + u < cnt) {
-        cx[(k0 + u) * kStride + t] = vx[u];
-        cy[(k0 + u) * kStride + t] = vy[u];
-        if (cp) cp[(k0 + u) * kStride + t] = pp[u];
+        const int a = r.at(kTreePC + k0 + u);
+        r.X[a] = vx[u];
+        r.Y[a] = vy[u];
+        r.P[a] = vp[u];
+        r.K[a] = (uint8_t)(k0 + u);
       }
   }
 }
 
-// One thread's stack scan of a staged run on top of a persistent state (top
-// element b1, parent[] links below). The persistent state's top kTreePC
-// elements (positions and coordinates) are first walked into a per-thread
-// shared-memory cache pc[d * kStride + t] (d = depth, 0 = b1), so the pops
-// that reach into it -- divergent, one per thread -- read shared memory;
-// deeper elements come from global memory. Own pushes are kept as run
-// indices in stk[depth * kStride + t]. on_push(k, below_run_index or -1 =
-// persistent top) is called for every push. On return b1 = the persistent
-// part's top. Returns the number of own pushes left.
-constexpr int kTreePC = 8;
-
-template <int kStride>
-struct TreeCache {
-  uint32_t* pos;  // [kTreePC][kStride]
-  double* x;
-  double* y;
-};
-
-template <int kStride, typename OnPush>
-__device__ __forceinline__ int tree_scan_run(int cnt, const double* cx, const double* cy,
-                                             uint32_t& b1, const double* __restrict__ R_x,
-                                             const double* __restrict__ R_y,
-                                             const uint32_t* __restrict__ parent, uint8_t* stk,
-                                             TreeCache<kStride> pc, OnPush&& on_push) {
-  const int t = threadIdx.x;
-  // walk the persistent top into the cache (dependent parent loads, once)
-  int ncached = 0;
-  {
-    uint32_t p = b1;
-    uint32_t pp[kTreePC];
+// Rows [0, n) from boundary record c; returns n, sets B.
+template <int T>
+__device__ __forceinline__ int tree_load_rec(const TreeRows<T>& r, const TreeRec& rec, uint32_t c,
+                                             uint32_t& B) {
+  const int n = (int)rec.n[c];
+  B = rec.below[c];
+  uint32_t vp[kTreePC];
+  double vx[kTreePC], vy[kTreePC];
 #pragma unroll
-    for (int d = 0; d < kTreePC; ++d) {
-      pp[d] = p;
-      if (p != kNone) { ncached = d + 1; p = parent[p]; }
-    }
-    double vx[kTreePC], vy[kTreePC];
-#pragma unroll
-    for (int d = 0; d < kTreePC; ++d) {
-      vx[d] = (d < ncached) ? R_x[pp[d]] : 0.0;
-      vy[d] = (d < ncached) ? R_y[pp[d]] : 0.0;
-    }
-#pragma unroll
-    for (int d = 0; d < kTreePC; ++d) {
-      pc.pos[d * kStride + t] = (d < ncached) ? pp[d] : kNone;
-      pc.x[d * kStride + t] = vx[d];
-      pc.y[d * kStride + t] = vy[d];
-    }
+  for (int d = 0; d < kTreePC; ++d) {
+    vp[d] = rec.pos[(size_t)c * kTreePC + d];
+    vx[d] = rec.x[(size_t)c * kTreePC + d];
+    vy[d] = rec.y[(size_t)c * kTreePC + d];
   }
-  // persistent element at depth d (d >= pd: already popped above it)
-  int pd = 0;  // persistent elements popped
-  uint32_t deep = kNone;  // position at depth pd when pd >= ncached (global walk)
-  auto pers_pos = [&](int d) -> uint32_t {  // d in {pd, pd + 1}
-    if (d < kTreePC) return pc.pos[d * kStride + t];
-    return kNone;  // handled by the caller through `deep`
-  };
-  uint32_t p1 = pers_pos(0);
-  uint32_t p2 = (ncached >= 2) ? pers_pos(1) : kNone;
-  int top = 0;
+#pragma unroll
+  for (int d = 0; d < kTreePC; ++d)
+    if (d < n) {
+      const int a = r.at(d);
+      r.X[a] = vx[d];
+      r.Y[a] = vy[d];
+      r.P[a] = vp[d];
+      r.K[a] = kTreeRec;
+    }
+  return n;
+}
+
+// Boundary record c from the stack rows [0, top) above B.
+template <int T>
+__device__ __forceinline__ void tree_store_rec(const TreeRows<T>& r, int top, uint32_t B,
+                                               const TreeRec& rec, uint32_t c) {
+  const int n = min(top, kTreePC), r0 = top - n;
+  rec.n[c] = (uint32_t)n;
+  rec.below[c] = r0 > 0 ? r.P[r.at(r0 - 1)] : B;
+  for (int d = 0; d < n; ++d) {
+    const int a = r.at(r0 + d);
+    rec.pos[(size_t)c * kTreePC + d] = r.P[a];
+    rec.x[(size_t)c * kTreePC + d] = r.X[a];
+    rec.y[(size_t)c * kTreePC + d] = r.Y[a];
+  }
+}
+
+// One thread's stack scan over the staged points (rows kTreePC + k, k < cnt)
+// on top of rows [0, top) and the chain below B. Every iteration is one pop
+// or one push (a warp of divergent scans costs max over lanes of pushes +
+// pops). on_push(k, position, below position) is called for every push.
+// lo_own ends at the lowest row holding a surviving push of this scan.
+// Returns the final top; B is updated when the scan pops below row 0.
+template <int T, typename OnPush>
+__device__ __forceinline__ int tree_scan_rows(const TreeRows<T>& r, int top, uint32_t& B, int cnt,
+                                              const uint32_t* __restrict__ parent,
+                                              const double* __restrict__ R_x,
+                                              const double* __restrict__ R_y, int& lo_own,
+                                              OnPush&& on_push) {
   double s1x = 0, s1y = 0, s2x = 0, s2y = 0;
-  if (p1 != kNone) { s1x = pc.x[t]; s1y = pc.y[t]; }
-  if (p2 != kNone) {
-    if (kTreePC >= 2) { s2x = pc.x[kStride + t]; s2y = pc.y[kStride + t]; }
+  bool h1, h2;
+  uint32_t q2 = kNone;  // position of s2 while it is B or below (top <= 1)
+  if (top >= 2) {
+    s1x = r.X[r.at(top - 1)]; s1y = r.Y[r.at(top - 1)];
+    s2x = r.X[r.at(top - 2)]; s2y = r.Y[r.at(top - 2)];
+    h1 = h2 = true;
+  } else if (top == 1) {
+    s1x = r.X[r.at(0)]; s1y = r.Y[r.at(0)];
+    h1 = true;
+    h2 = B != kNone;
+    q2 = B;
+    if (h2) { s2x = R_x[B]; s2y = R_y[B]; }
+  } else {
+    h1 = B != kNone;
+    h2 = false;
+    if (h1) {
+      s1x = R_x[B]; s1y = R_y[B];
+      q2 = parent[B];
+      h2 = q2 != kNone;
+      if (h2) { s2x = R_x[q2]; s2y = R_y[q2]; }
+    }
   }
-  // One flat loop, each iteration one pop or one push: a warp of divergent
-  // scans then costs max over lanes of (pushes + pops) iterations instead of
-  // the sum over points of the lanes' largest pop run.
   int k = 0;
   double px = 0, py = 0;
-  if (cnt > 0) { px = cx[t]; py = cy[t]; }
+  if (cnt > 0) { px = r.X[r.at(kTreePC)]; py = r.Y[r.at(kTreePC)]; }
   while (k < cnt) {
-    const bool has2 = (top >= 2) || (top == 1 && p1 != kNone) ||
-                      (top == 0 && p1 != kNone && p2 != kNone);
-    if (has2 && !left_turn(s2x, s2y, s1x, s1y, px, py)) {
-      if (top >= 1) {
-        --top;
-      } else {  // pop the persistent top
-        ++pd;
-        p1 = p2;
-        const int d2 = pd + 1;  // depth of the new second element
-        if (d2 < ncached) {
-          p2 = pc.pos[d2 * kStride + t];
-        } else if (p1 != kNone && d2 >= kTreePC) {
-          p2 = parent[p1];
-          deep = p2;
-        } else {
-          p2 = kNone;
-        }
-      }
+    if (h2 && !left_turn(s2x, s2y, s1x, s1y, px, py)) {
       s1x = s2x; s1y = s2y;
-      if (top >= 2) {
-        const int q = stk[(top - 2) * kStride + t];
-        s2x = cx[q * kStride + t]; s2y = cy[q * kStride + t];
-      } else if (top == 1) {
-        if (p1 != kNone) {
-          if (pd < kTreePC) { s2x = pc.x[pd * kStride + t]; s2y = pc.y[pd * kStride + t]; }
-          else { s2x = R_x[p1]; s2y = R_y[p1]; }
-        }
-      } else {
-        if (p2 != kNone) {
-          const int d2 = pd + 1;
-          if (d2 < kTreePC) { s2x = pc.x[d2 * kStride + t]; s2y = pc.y[d2 * kStride + t]; }
-          else { s2x = R_x[p2]; s2y = R_y[p2]; }
-        }
+      if (top >= 3) {  // common case: the new second element is a row
+        --top;
+        s2x = r.X[r.at(top - 2)]; s2y = r.Y[r.at(top - 2)];
+      } else if (top == 2) {  // new s1 = row 0, s2 = B
+        top = 1;
+        q2 = B;
+        h2 = B != kNone;
+        if (h2) { s2x = R_x[B]; s2y = R_y[B]; }
+      } else if (top == 1) {  // new s1 = B, s2 = parent[B]
+        top = 0;
+        q2 = parent[B];
+        h2 = q2 != kNone;
+        if (h2) { s2x = R_x[q2]; s2y = R_y[q2]; }
+      } else {  // pop B itself
+        B = q2;
+        q2 = parent[B];
+        h2 = q2 != kNone;
+        if (h2) { s2x = R_x[q2]; s2y = R_y[q2]; }
       }
       continue;
     }
-    on_push(k, top ? (int)stk[(top - 1) * kStride + t] : -1, p1);
-    stk[top * kStride + t] = (uint8_t)k;
+    const int a = r.at(top);
+    const uint32_t pp = r.P[r.at(kTreePC + k)];
+    on_push(k, pp, top >= 1 ? r.P[r.at(top - 1)] : B);
+    r.X[a] = px;
+    r.Y[a] = py;
+    r.P[a] = pp;
+    r.K[a] = (uint8_t)k;
+    if (top < lo_own) lo_own = top;
     ++top;
+    if (top == 1) q2 = B;
     s2x = s1x; s2y = s1y;
+    h2 = h1;
     s1x = px; s1y = py;
-    if (++k < cnt) { px = cx[k * kStride + t]; py = cy[k * kStride + t]; }
+    h1 = true;
+    if (++k < cnt) { px = r.X[r.at(kTreePC + k)]; py = r.Y[r.at(kTreePC + k)]; }
   }
-  (void)deep;
-  b1 = p1;
   return top;
 }
 
-// Shared-memory carve-up of one tree kernel: staging (coords, positions,
-// index stack) and the persistent cache, all [element][thread].
-template <int kStride>
-struct TreeSmem {
-  double *cx, *cy;
-  uint32_t* cp;
-  uint8_t* stk;
-  TreeCache<kStride> pc;
-  __device__ explicit TreeSmem(double* base) {
-    cx = base;
-    cy = cx + kTreeChunk * kStride;
-    pc.x = cy + kTreeChunk * kStride;
-    pc.y = pc.x + 8 * kStride;
-    cp = reinterpret_cast<uint32_t*>(pc.y + 8 * kStride);
-    pc.pos = cp + kTreeChunk * kStride;
-    stk = reinterpret_cast<uint8_t*>(pc.pos + 8 * kStride);
-  }
+struct TreeNoPush {
+  __device__ __forceinline__ void operator()(int, uint32_t, uint32_t) const {}
 };
 
+// Chain of a scan from an empty stack: rows [0, top) -> chunk-strided temp
+// (Q index = lo + chunk index, or the position on level 0).
+template <int T>
+__device__ __forceinline__ void tree_put_chain(const TreeRows<T>& r, int top, uint32_t lo,
+                                               bool level0, const TreeWork& w) {
+  for (int i = 0; i < top; ++i) {
+    const int a = r.at(i);
+    const uint32_t p = r.P[a];
+    w.chainq[lo + i] = level0 ? p : lo + r.K[a];
+    w.chainp[lo + i] = p;
+    w.chainx[lo + i] = r.X[a];
+    w.chainy[lo + i] = r.Y[a];
+  }
+}
+
 // ---------------------------------------------------------------------------
-// Level 0, many CTAs: chains of the buffer's chunks (thread per chunk).
+// info[] layout (device, read back once by the host):
+//   [0] no shrink (another strategy)  [1] final stack length  [2] certificate
+//   failures  [3] K  [8..9, 16] diagnostics clocks  [10 + j] size of Q_j
+//   [20..43] diagnostics
 constexpr int kTreeCta = 64;
 constexpr size_t kTreeCtaSmem = tree_smem(kTreeCta);
 
-__global__ void __launch_bounds__(kTreeCta) k_gr_local0(uint32_t N, const double* __restrict__ R_x,
-                                                       const double* __restrict__ R_y,
-                                                       TreeWork w) {
-  extern __shared__ __align__(16) double tsm[];
-  TreeSmem<kTreeCta> sm(tsm);
-  uint8_t* stk = sm.stk;
-  const uint32_t c = blockIdx.x * kTreeCta + threadIdx.x;
-  const uint32_t lo = c * kTreeChunk;
-  if (lo >= N) return;
-  const int cnt = (int)min((uint32_t)kTreeChunk, N - lo);
-  tree_stage<kTreeCta>([&](int k) { return lo + (uint32_t)k; }, cnt, R_x, R_y, sm.cx, sm.cy, nullptr);
-  uint32_t b1 = kNone;
-  const int top = tree_scan_run<kTreeCta>(cnt, sm.cx, sm.cy, b1, R_x, R_y, w.parent, stk, sm.pc,
-                                          [](int, int, uint32_t) {});
-  for (int k = 0; k < top; ++k) {
-    const uint32_t q = lo + stk[k * kTreeCta + threadIdx.x];
-    w.chainq[lo + k] = q;
-    w.chainp[lo + k] = q;
-  }
-  w.offbuf[0][c] = (uint32_t)top;
+__device__ __forceinline__ TreeLevel tree_level(const TreeWork& w, int j, uint32_t nq) {
+  TreeLevel L;
+  L.Qp = w.Qp[j];
+  L.Qx = w.Qx[j];
+  L.Qy = w.Qy[j];
+  L.up = w.up[j];
+  L.off = w.off[j];
+  L.bt = w.bt[j];
+  L.rec = w.rec[j];
+  L.nq = nq;
+  L.nch = (nq + kTreeChunk - 1) / kTreeChunk;
+  return L;
 }
 
-// Middle, ONE CTA: Q_1 from the level-0 chains, levels >= 1 up, the top-level
-// scan, and the down-sweep to level 1 (bt_1). info[0] = 1: no shrink.
+__device__ __forceinline__ uint32_t tree_nq(uint32_t N, const uint32_t* info, int j) {
+  return j == 0 ? N : info[10 + j];
+}
+
+// Up, many CTAs (levels 0 and 1): chains of level j's chunks (thread per
+// chunk) into the chunk-strided temp, lengths into off[j].
+__global__ void __launch_bounds__(kTreeCta) k_gr_up(uint32_t N, int j,
+                                                   const double* __restrict__ R_x,
+                                                   const double* __restrict__ R_y, TreeWork w,
+                                                   const uint32_t* __restrict__ info) {
+  extern __shared__ __align__(16) double tsm[];
+  const TreeRows<kTreeCta> r(tsm);
+  if (j > 0 && info[0]) return;
+  const uint32_t nq = tree_nq(N, info, j);
+  const uint32_t c = blockIdx.x * kTreeCta + threadIdx.x;
+  const uint32_t lo = c * kTreeChunk;
+  if (lo >= nq) return;
+  const int cnt = (int)min((uint32_t)kTreeChunk, nq - lo);
+  if (j == 0) tree_stage<kTreeCta>(r, nullptr, R_x, R_y, lo, cnt);
+  else tree_stage<kTreeCta>(r, w.Qp[j], w.Qx[j], w.Qy[j], lo, cnt);
+  uint32_t B = kNone;
+  int lo_own = kTreeRows;
+  const int top =
+      tree_scan_rows<kTreeCta>(r, 0, B, cnt, w.parent, R_x, R_y, lo_own, TreeNoPush{});
+  tree_put_chain<kTreeCta>(r, top, lo, j == 0, w);
+  w.off[j][c] = (uint32_t)top;
+}
+
+// Exclusive scan of level j's chain lengths (one CTA), Q_{j+1}'s size, and
+// the shrink check (info[0]: the tree strategy declines).
+__global__ void __launch_bounds__(1024) k_gr_scan(uint32_t N, int j, TreeWork w,
+                                                  uint32_t* __restrict__ info) {
+  __shared__ uint32_t s_w[32];
+  __shared__ uint32_t s_carry;
+  if (info[0]) return;
+  const uint32_t nq = tree_nq(N, info, j);
+  const uint32_t nch = (nq + kTreeChunk - 1) / kTreeChunk;
+  const uint32_t total = tree_scan(w.off[j], nch, s_w, &s_carry);
+  if (threadIdx.x == 0) {
+    w.off[j][nch] = total;
+    const bool shrink =
+        (j == 0) ? (total * 20ull <= (uint64_t)nq * 17) : (total * 10ull <= (uint64_t)nq * 9);
+    // (a level-1 list short enough for the top scan needs no shrink)
+    if ((!shrink && !(j >= 1 && nq <= kTreeTop)) || total > w.cap[j + 1]) info[0] = 1;
+    info[11 + j] = total;
+  }
+}
+
+// Level j chains -> Q_{j+1} (up index, position, coordinates): a warp per
+// chunk, lanes over the chain, so loads and stores are coalesced.
+__device__ __forceinline__ void tree_gather_chunk(const TreeWork& w, int j, uint32_t c) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t o = w.off[j][c], ln = w.off[j][c + 1] - o;
+  const uint32_t s = c * kTreeChunk + lane;
+  if (lane < ln) {
+    const uint32_t q = w.chainq[s], p = w.chainp[s];
+    const double x = w.chainx[s], y = w.chainy[s];
+    w.up[j + 1][o + lane] = q;
+    w.Qp[j + 1][o + lane] = p;
+    w.Qx[j + 1][o + lane] = x;
+    w.Qy[j + 1][o + lane] = y;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_gr_gather(uint32_t N, int j, TreeWork w,
+                                                  const uint32_t* __restrict__ info) {
+  if (info[0]) return;
+  const uint32_t nch = (tree_nq(N, info, j) + kTreeChunk - 1) / kTreeChunk;
+  const uint32_t c = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (c < nch) tree_gather_chunk(w, j, c);
+}
+
+// One down step for lower chunk cq: the state before it is the state before
+// the upper chunk holding its chain's first element, scanned over the upper
+// elements in between; pushes write parent[]. Writes the lower top + record.
+template <int T>
+__device__ __forceinline__ void tree_down_one(const TreeRows<T>& r, const TreeLevel& hl,
+                                              const TreeLevel& ll, uint32_t cq,
+                                              const double* __restrict__ R_x,
+                                              const double* __restrict__ R_y, uint32_t* parent) {
+  const uint32_t e = ll.off[cq];
+  const uint32_t c = e / kTreeChunk;
+  const int cnt = (int)(e - c * kTreeChunk);
+  tree_stage<T>(r, hl.Qp, hl.Qx, hl.Qy, c * kTreeChunk, cnt);
+  uint32_t B;
+  const int n0 = tree_load_rec<T>(r, hl.rec, c, B);
+  int lo_own = kTreeRows;
+  const int top = tree_scan_rows<T>(r, n0, B, cnt, parent, R_x, R_y, lo_own,
+                                    [&](int, uint32_t p, uint32_t below) { parent[p] = below; });
+  ll.bt[cq] = top ? r.P[r.at(top - 1)] : B;
+  tree_store_rec<T>(r, top, B, ll.rec, cq);
+}
+
+// Middle, ONE CTA: levels >= 2 up (Q_1 and Q_2 come from the many-CTA
+// kernels), the top-level scan, and the down-sweep to level 2.
 __global__ void __launch_bounds__(kTreeThreads, 1) k_gr_mid(
     const double* __restrict__ R_x, const double* __restrict__ R_y, uint32_t N, TreeWork w,
     uint32_t* __restrict__ info) {
   extern __shared__ __align__(16) double tsm[];
-  TreeSmem<kTreeThreads> sm(tsm);
-  double* cx = sm.cx;
-  double* cy = sm.cy;
-  uint32_t* cp = sm.cp;
-  uint8_t* stk = sm.stk;
+  const TreeRows<kTreeThreads> r(tsm);
   __shared__ uint32_t s_w[32];
   __shared__ uint32_t s_carry;
-  __shared__ TreeLevel L[kTreeMaxLevels + 1];
+  __shared__ uint32_t s_nq[kTreeMaxLevels + 1];
   __shared__ int s_K, s_bad;
   const int t = threadIdx.x;
   long long t_start = clock64();
+  if (info[0]) return;  // level 0 or 1 did not shrink
   if (t == 0) {
-    L[0].Q = nullptr;
-    L[0].up = nullptr;
-    L[0].nq = N;
-    s_K = -1;
+    s_nq[0] = N;
+    s_nq[1] = info[11];
+    s_nq[2] = info[12];
+    s_K = s_nq[1] <= kTreeTop ? 1 : (s_nq[2] <= kTreeTop ? 2 : -1);
     s_bad = 0;
-    info[0] = 0;
-    info[2] = 0;
   }
   __syncthreads();
-  for (int j = 0; j < kTreeMaxLevels; ++j) {
-    const uint32_t nq = L[j].nq;
-    const uint32_t cs = (j == 0) ? kTreeChunk : kTreeChunkHi;
-    const uint32_t nch = (nq + cs - 1) / cs;
-    if (t == 0) {
-      L[j].nch = nch;
-      L[j].off = w.offbuf[j];
-      L[j].bt = w.btbuf[j];
-    }
-    __syncthreads();
-    const uint32_t* Q = L[j].Q;
-    if (j > 0) {  // level-0 chains come from k_gr_local0
-      for (uint32_t c0 = 0; c0 < nch; c0 += kTreeThreads) {
-        const uint32_t c = c0 + t;
-        if (c < nch) {
-          const uint32_t lo = c * cs;
-          const int cnt = (int)min(cs, nq - lo);
-          tree_stage<kTreeThreads>([&](int k) { return Q[lo + k]; }, cnt, R_x, R_y, cx, cy, cp);
-          uint32_t b1 = kNone;
-          const int top = tree_scan_run<kTreeThreads>(cnt, cx, cy, b1, R_x, R_y, w.parent, stk,
-                                                      sm.pc, [](int, int, uint32_t) {});
-          for (int k = 0; k < top; ++k) {
-            const int e = stk[k * kTreeThreads + t];
-            w.chainq[lo + k] = lo + e;
-            w.chainp[lo + k] = cp[e * kTreeThreads + t];
-          }
-          L[j].off[c] = (uint32_t)top;
-        }
+  for (int j = 2; s_K < 0 && j < kTreeMaxLevels; ++j) {
+    const TreeLevel L = tree_level(w, j, s_nq[j]);
+    for (uint32_t c0 = 0; c0 < L.nch; c0 += kTreeThreads) {
+      const uint32_t c = c0 + t;
+      if (c < L.nch) {
+        const uint32_t lo = c * kTreeChunk;
+        const int cnt = (int)min((uint32_t)kTreeChunk, L.nq - lo);
+        tree_stage<kTreeThreads>(r, L.Qp, L.Qx, L.Qy, lo, cnt);
+        uint32_t B = kNone;
+        int lo_own = kTreeRows;
+        const int top = tree_scan_rows<kTreeThreads>(r, 0, B, cnt, w.parent, R_x, R_y, lo_own,
+                                                     TreeNoPush{});
+        tree_put_chain<kTreeThreads>(r, top, lo, false, w);
+        L.off[c] = (uint32_t)top;
       }
     }
     __syncthreads();
-    const uint32_t total = tree_scan(L[j].off, nch, s_w, &s_carry);
+    const uint32_t total = tree_scan(L.off, L.nch, s_w, &s_carry);
     if (t == 0) {
-      L[j].off[nch] = total;
-      const bool shrink =
-          (j == 0) ? (total * 20ull <= (uint64_t)nq * 17) : (total * 10ull <= (uint64_t)nq * 9);
-      if (!shrink || total > w.cap[j + 1] || j + 1 > kTreeMaxLevels - 1) s_bad = 1;
-      L[j + 1].Q = w.Qbuf[j + 1];
-      L[j + 1].up = w.upbuf[j + 1];
-      L[j + 1].nq = total;
+      L.off[L.nch] = total;
+      if (total * 10ull > (uint64_t)L.nq * 9 || total > w.cap[j + 1] || j + 1 > kTreeMaxLevels - 1)
+        s_bad = 1;
+      s_nq[j + 1] = total;
     }
     __syncthreads();
     if (s_bad) break;
-    for (uint32_t c = t; c < nch; c += kTreeThreads) {
-      const uint32_t o = L[j].off[c], ln = L[j].off[c + 1] - o;
-      for (uint32_t k0 = 0; k0 < ln; k0 += 8) {
-        uint32_t qv[8], pv[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          qv[u] = (k0 + u < ln) ? w.chainq[c * cs + k0 + u] : 0u;
-          pv[u] = (k0 + u < ln) ? w.chainp[c * cs + k0 + u] : 0u;
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if (k0 + u < ln) { L[j + 1].Q[o + k0 + u] = pv[u]; L[j + 1].up[o + k0 + u] = qv[u]; }
-      }
+    for (uint32_t c = t >> 5; c < L.nch; c += kTreeThreads / 32) tree_gather_chunk(w, j, c);
+    __syncthreads();
+    if (t == 0) {
+      if (j < 12) info[20 + j] = (uint32_t)(clock64() - t_start);  // diagnostics
+      if (s_nq[j + 1] <= kTreeTop) s_K = j + 1;
     }
     __syncthreads();
-    if (total <= kTreeTop) {
-      if (t == 0) s_K = j + 1;
-      __syncthreads();
-      break;
-    }
   }
   const int K = s_K;
   if (s_bad || K < 1) {  // no shrink: the host takes another strategy
@@ -393,22 +493,26 @@ __global__ void __launch_bounds__(kTreeThreads, 1) k_gr_mid(
   }
   if (t == 0) {
     info[8] = (uint32_t)(clock64() - t_start);
-    for (int j = 0; j <= K && j < 6; ++j) info[10 + j] = L[j].nq;
+    for (int j = 3; j <= K && j < 6; ++j) info[10 + j] = s_nq[j];
   }
-  // ---- top: one thread over Q_K, staged in shared memory by all ----
+  // ---- top: one thread over Q_K (staged in shared memory); then all threads
+  // turn its boundary tops into records by walking the persistent links ----
   {
-    const TreeLevel& tl = L[K];
-    const TreeLevel& ll = L[K - 1];
+    const TreeLevel tl = tree_level(w, K, s_nq[K]);
+    const TreeLevel ll = tree_level(w, K - 1, s_nq[K - 1]);
     const uint32_t nk = tl.nq;  // <= kTreeTop
-    uint32_t* s_p = cp;         // reuse the staging area
-    uint32_t* s_ch = cp + kTreeTop;
-    uint32_t* s_st = cp + 2 * kTreeTop;
+    double* s_x = r.X;
+    double* s_y = r.Y;
+    uint32_t* s_p = r.P;                   // R position of each Q_K element
+    uint32_t* s_ch = r.P + kTreeTop;       // its Q_{K-1} chunk
+    uint32_t* s_par = r.P + 2 * kTreeTop;  // Q_K index below it (kNone: none)
+    uint32_t* s_st = r.P + 3 * kTreeTop;   // the stack (Q_K indices)
+    uint32_t* bk = w.tmp;                  // Q_K index of the top before each boundary
     for (uint32_t k = t; k < nk; k += kTreeThreads) {
-      const uint32_t p = tl.Q[k];
-      s_p[k] = p;
-      s_ch[k] = tl.up[k] / (K - 1 == 0 ? kTreeChunk : kTreeChunkHi);
-      cx[k] = R_x[p];
-      cy[k] = R_y[p];
+      s_p[k] = tl.Qp[k];
+      s_ch[k] = tl.up[k] / kTreeChunk;
+      s_x[k] = tl.Qx[k];
+      s_y[k] = tl.Qy[k];
     }
     __syncthreads();
     if (t == 0) {
@@ -416,91 +520,79 @@ __global__ void __launch_bounds__(kTreeThreads, 1) k_gr_mid(
       double s1x = 0, s1y = 0, s2x = 0, s2y = 0;
       uint32_t next_b = 0;
       for (uint32_t k = 0; k < nk; ++k) {
-        const uint32_t p = s_p[k];
-        const uint32_t tp = top ? s_p[s_st[top - 1]] : kNone;
-        for (; next_b <= s_ch[k]; ++next_b) ll.bt[next_b] = tp;
-        const double px = cx[k], py = cy[k];
+        const uint32_t tk = top ? s_st[top - 1] : kNone;
+        for (; next_b <= s_ch[k]; ++next_b) bk[next_b] = tk;
+        const double px = s_x[k], py = s_y[k];
         while (top >= 2 && !left_turn(s2x, s2y, s1x, s1y, px, py)) {
           --top;
           s1x = s2x; s1y = s2y;
-          if (top >= 2) { const uint32_t q = s_st[top - 2]; s2x = cx[q]; s2y = cy[q]; }
+          if (top >= 2) { const uint32_t q = s_st[top - 2]; s2x = s_x[q]; s2y = s_y[q]; }
         }
-        w.parent[p] = top ? s_p[s_st[top - 1]] : kNone;
+        const uint32_t below = top ? s_st[top - 1] : kNone;
+        s_par[k] = below;
+        w.parent[s_p[k]] = below != kNone ? s_p[below] : kNone;
         s_st[top++] = k;
         s2x = s1x; s2y = s1y;
         s1x = px; s1y = py;
       }
-      const uint32_t tp = top ? s_p[s_st[top - 1]] : kNone;
-      for (; next_b <= ll.nch; ++next_b) ll.bt[next_b] = tp;
+      const uint32_t tk = top ? s_st[top - 1] : kNone;
+      for (; next_b <= ll.nch; ++next_b) bk[next_b] = tk;
       for (int k = 0; k < top; ++k) w.fstack[k] = s_p[s_st[k]];
       info[1] = (uint32_t)top;
+      // every level's boundary after its last chunk holds the final top
+      const uint32_t ftop = top ? s_p[s_st[top - 1]] : kNone;
+      for (int j = 0; j < K; ++j) w.bt[j][(s_nq[j] + kTreeChunk - 1) / kTreeChunk] = ftop;
+    }
+    __syncthreads();
+    for (uint32_t b = t; b < ll.nch; b += kTreeThreads) {
+      uint32_t e[kTreePC];
+      uint32_t q = bk[b];
+      int n = 0;
+      for (; n < kTreePC && q != kNone; ++n) { e[n] = q; q = s_par[q]; }
+      ll.bt[b] = n ? s_p[e[0]] : kNone;
+      ll.rec.n[b] = (uint32_t)n;
+      ll.rec.below[b] = q != kNone ? s_p[q] : kNone;
+      for (int d = 0; d < n; ++d) {  // bottom-aligned: d = 0 deepest
+        const uint32_t qq = e[n - 1 - d];
+        ll.rec.pos[(size_t)b * kTreePC + d] = s_p[qq];
+        ll.rec.x[(size_t)b * kTreePC + d] = s_x[qq];
+        ll.rec.y[(size_t)b * kTreePC + d] = s_y[qq];
+      }
     }
     __syncthreads();
   }
   if (t == 0) info[9] = (uint32_t)(clock64() - t_start);
-  // ---- down: level j -> j-1, for j >= 2 (level 1 -> 0 runs on many CTAs) ----
-  for (int j = K - 1; j >= 2; --j) {
-    const TreeLevel& hl = L[j];
-    const TreeLevel& ll = L[j - 1];
+  // ---- down: level j -> j-1 for j >= 3 (2 -> 1 and 1 -> 0 run on many CTAs) ----
+  for (int j = K - 1; j >= 3; --j) {
+    const TreeLevel hl = tree_level(w, j, s_nq[j]);
+    const TreeLevel ll = tree_level(w, j - 1, s_nq[j - 1]);
     for (uint32_t c0 = 0; c0 < ll.nch; c0 += kTreeThreads) {
       const uint32_t cq = c0 + t;
-      if (cq < ll.nch) {
-        const uint32_t e = ll.off[cq];
-        const uint32_t c = e / kTreeChunkHi;  // level j >= 2 > 0
-        const int cnt = (int)(e - c * kTreeChunkHi);
-        const uint32_t* Qj = hl.Q + c * kTreeChunkHi;
-        tree_stage<kTreeThreads>([&](int k) { return Qj[k]; }, cnt, R_x, R_y, cx, cy, cp);
-        uint32_t b1 = hl.bt[c];
-        const int top = tree_scan_run<kTreeThreads>(
-            cnt, cx, cy, b1, R_x, R_y, w.parent, stk, sm.pc, [&](int k, int below, uint32_t ptop) {
-              w.parent[cp[k * kTreeThreads + t]] = below >= 0 ? cp[below * kTreeThreads + t] : ptop;
-            });
-        ll.bt[cq] = top ? cp[stk[(top - 1) * kTreeThreads + t] * kTreeThreads + t] : b1;
-      }
+      if (cq < ll.nch) tree_down_one<kTreeThreads>(r, hl, ll, cq, R_x, R_y, w.parent);
     }
     __syncthreads();
-    if (t == 0) ll.bt[ll.nch] = hl.bt[hl.nch];
-    __syncthreads();
+    if (t == 0 && j < 12) info[32 + j] = (uint32_t)(clock64() - t_start);  // diagnostics
   }
   if (t == 0) {
-    // K == 1: the top-level scan already wrote the level-0 boundary states;
-    // else the level-0 boundary after the last chunk is the final top
-    if (K >= 2) w.btbuf[0][(N + kTreeChunk - 1) / kTreeChunk] = L[1].bt[L[1].nch];
     info[3] = K;
     info[16] = (uint32_t)(clock64() - t_start);
   }
 }
 
-// Down 1 -> 0, many CTAs: the state before every buffer chunk.
-__global__ void __launch_bounds__(kTreeCta) k_gr_down0(uint32_t N, const double* __restrict__ R_x,
-                                                      const double* __restrict__ R_y, TreeWork w,
-                                                      const uint32_t* __restrict__ info) {
+// Down j -> j-1 (j = 2, 1), many CTAs: the state before every level j-1
+// chunk. Runs when the top level is above j - 1.
+__global__ void __launch_bounds__(kTreeCta) k_gr_down(uint32_t N, int j,
+                                                     const double* __restrict__ R_x,
+                                                     const double* __restrict__ R_y, TreeWork w,
+                                                     const uint32_t* __restrict__ info) {
   extern __shared__ __align__(16) double tsm[];
-  TreeSmem<kTreeCta> sm(tsm);
-  double* cx = sm.cx;
-  double* cy = sm.cy;
-  uint32_t* cp = sm.cp;
-  uint8_t* stk = sm.stk;
-  if (info[0] || info[3] < 2) return;  // K == 1: level-0 states come from the top scan
-  const uint32_t nch0 = (N + kTreeChunk - 1) / kTreeChunk;
+  const TreeRows<kTreeCta> r(tsm);
+  if (info[0] || (int)info[3] <= j) return;
+  const TreeLevel hl = tree_level(w, j, tree_nq(N, info, j));
+  const TreeLevel ll = tree_level(w, j - 1, tree_nq(N, info, j - 1));
   const uint32_t cq = blockIdx.x * kTreeCta + threadIdx.x;
-  if (cq >= nch0) return;
-  const uint32_t* off0 = w.offbuf[0];
-  const uint32_t* bt1 = w.btbuf[1];
-  const uint32_t* Q1 = w.Qbuf[1];
-  const uint32_t e = off0[cq];
-  const uint32_t c = e / kTreeChunkHi;  // chunks of Q_1
-  const int cnt = (int)(e - c * kTreeChunkHi);
-  const uint32_t* Qj = Q1 + c * kTreeChunkHi;
-  const int t = threadIdx.x;
-  tree_stage<kTreeCta>([&](int k) { return Qj[k]; }, cnt, R_x, R_y, cx, cy, cp);
-  uint32_t b1 = bt1[c];
-  const int top = tree_scan_run<kTreeCta>(cnt, cx, cy, b1, R_x, R_y, w.parent, stk, sm.pc,
-                                          [&](int k, int below, uint32_t ptop) {
-                                            w.parent[cp[k * kTreeCta + t]] =
-                                                below >= 0 ? cp[below * kTreeCta + t] : ptop;
-                                          });
-  w.btbuf[0][cq] = top ? cp[stk[(top - 1) * kTreeCta + t] * kTreeCta + t] : b1;
+  if (cq >= ll.nch) return;
+  tree_down_one<kTreeCta>(r, hl, ll, cq, R_x, R_y, w.parent);
 }
 
 // Certificate, many CTAs (thread per buffer chunk); failures counted in info[2].
@@ -509,35 +601,33 @@ __global__ void __launch_bounds__(kTreeCta) k_gr_cert(uint32_t N, const double* 
                                                      uint32_t* __restrict__ info,
                                                      uint32_t debug_corrupt) {
   extern __shared__ __align__(16) double tsm[];
-  TreeSmem<kTreeCta> sm(tsm);
-  double* cx = sm.cx;
-  double* cy = sm.cy;
-  uint8_t* stk = sm.stk;
+  const TreeRows<kTreeCta> r(tsm);
   if (info[0]) return;
   const uint32_t nch0 = (N + kTreeChunk - 1) / kTreeChunk;
   const uint32_t c = blockIdx.x * kTreeCta + threadIdx.x;
   if (c >= nch0) return;
-  const uint32_t* bt = w.btbuf[0];
+  const uint32_t* bt = w.bt[0];
   const uint32_t lo = c * kTreeChunk;
   const int cnt = (int)min((uint32_t)kTreeChunk, N - lo);
-  tree_stage<kTreeCta>([&](int k) { return lo + (uint32_t)k; }, cnt, R_x, R_y, cx, cy, nullptr);
-  uint32_t b1 = bt[c];
-  const int top = tree_scan_run<kTreeCta>(cnt, cx, cy, b1, R_x, R_y, w.parent, stk, sm.pc,
-                                          [](int, int, uint32_t) {});
-  const uint32_t end_top = top ? lo + stk[(top - 1) * kTreeCta + threadIdx.x] : b1;
+  tree_stage<kTreeCta>(r, nullptr, R_x, R_y, lo, cnt);
+  uint32_t B;
+  const int n0 = tree_load_rec<kTreeCta>(r, w.rec[0], c, B);
+  int lo_own = kTreeRows;
+  const int top =
+      tree_scan_rows<kTreeCta>(r, n0, B, cnt, w.parent, R_x, R_y, lo_own, TreeNoPush{});
+  const uint32_t end_top = top ? r.P[r.at(top - 1)] : B;
   uint32_t want = bt[c + 1];
   if (debug_corrupt && c + 1 == nch0) want = bt[c];  // falsified final state
   bool ok = want == end_top;
   // surviving pushes must link as in parent[] (loads issued 8 at a time)
-  for (int k0 = 0; k0 < top && ok; k0 += 8) {
+  for (int k0 = lo_own; k0 < top && ok; k0 += 8) {
     uint32_t lk[8];
 #pragma unroll
-    for (int u = 0; u < 8; ++u)
-      lk[u] = (k0 + u < top) ? w.parent[lo + stk[(k0 + u) * kTreeCta + threadIdx.x]] : 0u;
+    for (int u = 0; u < 8; ++u) lk[u] = (k0 + u < top) ? w.parent[r.P[r.at(k0 + u)]] : 0u;
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const int k = k0 + u;
-      if (k < top) ok = ok && lk[u] == (k ? lo + stk[(k - 1) * kTreeCta + threadIdx.x] : b1);
+      if (k < top) ok = ok && lk[u] == (k ? r.P[r.at(k - 1)] : B);
     }
   }
   if (!ok) atomicAdd(&info[2], 1u);
@@ -576,7 +666,7 @@ __global__ void __launch_bounds__(1024) k_gr_emit(uint32_t N, const double* __re
     return;
   }
   const uint32_t nch0 = (N + kTreeChunk - 1) / kTreeChunk;
-  const uint32_t len = info[1], ftop = w.btbuf[0][nch0];
+  const uint32_t len = info[1], ftop = w.bt[0][nch0];
   bool ok = len > 0 && w.fstack[len - 1] == ftop;
   for (uint32_t k = t; k < len && ok; k += blockDim.x)
     ok = w.parent[w.fstack[k]] == (k ? w.fstack[k - 1] : kNone);

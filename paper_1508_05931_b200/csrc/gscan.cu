@@ -120,7 +120,6 @@ struct gscan_handle {
   uint32_t *sp_gcount = nullptr, *sp_ccount = nullptr, *sp_hcount = nullptr;  // per-CTA emissions
   uint64_t* sp_dup2 = nullptr;   // partitioned hash list (n)
   uint64_t* sp_side_status = nullptr;  // look-back status of the side stream's scan
-  uint32_t* sp_part_cur = nullptr;     // partition cursors of the dup partitioning
   uint32_t* sp_side_work = nullptr;    // work tickets of the two side kernels
   Counters* sp_side_ticket = nullptr;
   bool sp_debug = false, sp_no_dup = false;
@@ -628,15 +627,19 @@ constexpr uint32_t kTreeMaxN = 1u << 22;  // larger buffers: the middle level wo
 int graham_tree(gscan_handle* h, const double* Rx, const double* Ry, const uint32_t* Ri,
                 uint32_t N, bool* done) {
   *done = false;
-  // level capacities: level 1 <= 0.6 N, then <= 0.8x per level (else the kernel declines)
+  // level capacities: level 1 <= 0.85 N, then <= 0.9x per level, levels >= 1
+  // at most kTreeHiCap (else the kernel declines)
   uint64_t caps[kTreeMaxLevels + 1];
-  uint64_t need = 4ull * N + (N / kTreeChunk + 64) + kTreeTop + 64;
   caps[0] = N;
-  for (int j = 1; j <= kTreeMaxLevels; ++j) {
-    caps[j] = (j == 1 ? (uint64_t)N * 17 / 20 : caps[j - 1] * 9 / 10) + 64;
-    need += 2 * caps[j] + 2 * (caps[j - 1] / kTreeChunkHi + 64) + 128;
+  for (int j = 1; j <= kTreeMaxLevels; ++j)
+    caps[j] = std::min<uint64_t>((j == 1 ? (uint64_t)N * 17 / 20 : caps[j - 1] * 9 / 10) + 64,
+                                 kTreeHiCap);
+  auto nchunks = [&](int j) { return caps[j] / kTreeChunk + 2; };
+  uint64_t need = 8ull * N + kTreeTop + 64 * 8;  // parent, tmp, chainq/p, chainx/y
+  for (int j = 0; j <= kTreeMaxLevels; ++j) {
+    if (j >= 1) need += 6 * caps[j] + 4 * 32;                // Qp, Qx, Qy, up
+    need += nchunks(j) * (2 + 2 + 8 + 16 + 16) + 7 * 32;   // off, bt, rec
   }
-  need += 2 * (caps[kTreeMaxLevels] / kTreeChunkHi + 64) + 128;
   if (need > h->gt_cap) {
     dfree(h->gt_pool);
     CU(cudaMalloc(&h->gt_pool, need * 4));
@@ -645,54 +648,69 @@ int graham_tree(gscan_handle* h, const double* Rx, const double* Ry, const uint3
   uint32_t* pool = h->gt_pool;
   uint64_t used = 0;
   auto take = [&](uint64_t cnt) { uint32_t* p = pool + used; used += (cnt + 31) & ~31ull; return p; };
+  auto take_d = [&](uint64_t cnt) { return reinterpret_cast<double*>(take(2 * cnt)); };
   TreeWork w{};
   w.parent = take(N);
   w.tmp = take(N);
   w.chainq = take(N);
   w.chainp = take(N);
-  w.len = take(N / kTreeChunk + 64);
+  w.chainx = take_d(N);
+  w.chainy = take_d(N);
   w.fstack = take(kTreeTop);
   for (int j = 0; j <= kTreeMaxLevels; ++j) {
     w.cap[j] = (uint32_t)caps[j];
     if (j >= 1) {
-      w.Qbuf[j] = take(caps[j]);
-      w.upbuf[j] = take(caps[j]);
+      w.Qp[j] = take(caps[j]);
+      w.Qx[j] = take_d(caps[j]);
+      w.Qy[j] = take_d(caps[j]);
+      w.up[j] = take(caps[j]);
     }
-    w.offbuf[j] = take(caps[j] / (j == 0 ? kTreeChunk : kTreeChunkHi) + 64);
-    w.btbuf[j] = take(caps[j] / (j == 0 ? kTreeChunk : kTreeChunkHi) + 64);
+    const uint64_t nc = nchunks(j);
+    w.off[j] = take(nc);
+    w.bt[j] = take(nc);
+    w.rec[j].n = take(nc);
+    w.rec[j].below = take(nc);
+    w.rec[j].pos = take(nc * kTreePC);
+    w.rec[j].x = take_d(nc * kTreePC);
+    w.rec[j].y = take_d(nc * kTreePC);
   }
+  if (used > need) return fail(h, GSCAN_E_INTERNAL, "tree pool overflow");
   uint32_t* info = h->g_misc + 4;
   const uint32_t nch0 = (N + kTreeChunk - 1) / kTreeChunk;
   const uint32_t g0 = (nch0 + kTreeCta - 1) / kTreeCta;
+  const uint32_t nch1 = (uint32_t)(caps[1] / kTreeChunk + 1);  // upper bound
+  const uint32_t g1 = (nch1 + kTreeCta - 1) / kTreeCta;
   const uint32_t dbg = (h->debug & GSCAN_DEBUG_CORRUPT_CANDIDATE) ? 1u : 0u;
-  {
-    Launch Lk(h, "k_gr_local0");
-    k_gr_local0<<<g0, kTreeCta, kTreeCtaSmem, h->stream>>>(N, Rx, Ry, w);
+  cudaStream_t s = h->stream;
+  CU(cudaMemsetAsync(info, 0, 16 * sizeof(uint32_t), s));
+  for (int j = 0; j < 2; ++j) {  // levels 0 and 1 on many CTAs
+    const uint32_t g = j ? g1 : g0, nch = j ? nch1 : nch0;
+    { Launch Lk(h, "k_gr_up", s); k_gr_up<<<g, kTreeCta, kTreeCtaSmem, s>>>(N, j, Rx, Ry, w, info); }
+    { Launch Lk(h, "k_gr_scan", s); k_gr_scan<<<1, 1024, 0, s>>>(N, j, w, info); }
+    { Launch Lk(h, "k_gr_gather", s); k_gr_gather<<<(nch + 7) / 8, 256, 0, s>>>(N, j, w, info); }
   }
-  {
-    Launch Lk(h, "k_gr_mid");
-    k_gr_mid<<<1, kTreeThreads, kTreeSmem, h->stream>>>(Rx, Ry, N, w, info);
-  }
-  {
-    Launch Lk(h, "k_gr_down0");
-    k_gr_down0<<<g0, kTreeCta, kTreeCtaSmem, h->stream>>>(N, Rx, Ry, w, info);
-  }
-  {
-    Launch Lk(h, "k_gr_cert");
-    k_gr_cert<<<g0, kTreeCta, kTreeCtaSmem, h->stream>>>(N, Rx, Ry, w, info, dbg);
-  }
-  {
-    Launch Lk(h, "k_gr_emit");
-    k_gr_emit<<<1, 1024, 0, h->stream>>>(N, Rx, Ry, Ri, w, info, h->d_out, h->ctr);
-  }
+  { Launch Lk(h, "k_gr_mid", s); k_gr_mid<<<1, kTreeThreads, kTreeSmem, s>>>(Rx, Ry, N, w, info); }
+  { Launch Lk(h, "k_gr_down", s); k_gr_down<<<g1, kTreeCta, kTreeCtaSmem, s>>>(N, 2, Rx, Ry, w, info); }
+  { Launch Lk(h, "k_gr_down", s); k_gr_down<<<g0, kTreeCta, kTreeCtaSmem, s>>>(N, 1, Rx, Ry, w, info); }
+  { Launch Lk(h, "k_gr_cert", s); k_gr_cert<<<g0, kTreeCta, kTreeCtaSmem, s>>>(N, Rx, Ry, w, info, dbg); }
+  { Launch Lk(h, "k_gr_emit", s); k_gr_emit<<<1, 1024, 0, s>>>(N, Rx, Ry, Ri, w, info, h->d_out, h->ctr); }
   CU(cudaGetLastError());
-  uint32_t hi[17];
-  CU(cudaMemcpyAsync(hi, info, sizeof hi, cudaMemcpyDeviceToHost, h->stream));
+  uint32_t hi[52];
+  CU(cudaMemcpyAsync(hi, info, h->sp_debug ? sizeof hi : 17 * sizeof(uint32_t),
+                     cudaMemcpyDeviceToHost, h->stream));
   CU(cudaStreamSynchronize(h->stream));
-  if (h->sp_debug)
+  if (h->sp_debug) {
     fprintf(stderr, "[tree] N=%u K=%u sizes=%u,%u,%u,%u,%u,%u.. cycles: up=%u top=%u down=%u fails=%u\n",
             N, hi[3], hi[10], hi[11], hi[12], hi[13], hi[14], hi[15], hi[8], hi[9] - hi[8],
             hi[16] - hi[9], hi[2]);
+    fprintf(stderr, "[tree] level ends (cycles): up");
+    for (uint32_t j = 0; j < hi[3] && j < 12; ++j) fprintf(stderr, " %u", hi[20 + j]);
+    fprintf(stderr, " | down");
+    for (uint32_t j = hi[3] - 1; j >= 2 && j < 12; --j) fprintf(stderr, " %u", hi[32 + j]);
+    fprintf(stderr, " | scan start/end");
+    for (int j = 0; j < 4; ++j) fprintf(stderr, " %u/%u", hi[44 + 2 * j], hi[45 + 2 * j]);
+    fprintf(stderr, "\n");
+  }
   if (hi[0]) return GSCAN_OK;  // no shrink
   h->graham_fails = hi[2];
   h->graham_path = 8 | (hi[2] ? 4 : 0);
@@ -851,19 +869,18 @@ int sparse_init(gscan_handle* h) {
   CU(cudaMalloc(&h->sp_big, nb * 4));
   CU(cudaMalloc(&h->sp_bigg, nb * 4));
   CU(cudaMalloc(&h->sp_gcount, G * 4));
-  CU(cudaMalloc(&h->sp_side_status, ((kSpParts * G + 1 + kScanTile - 1) / kScanTile + 64) * 8));
+  CU(cudaMalloc(&h->sp_side_status, ((kSpParts * 2 * G + 1 + kScanTile - 1) / kScanTile + 64) * 8));
   CU(cudaMalloc(&h->sp_side_ticket, sizeof(Counters)));
-  CU(cudaMalloc(&h->sp_part_cur, ((size_t)G * kSpParts + 1) * 4));
   CU(cudaMalloc(&h->sp_side_work, 4 * sizeof(uint32_t)));
   CU(cudaMalloc(&h->sp_ccount, G * 4));
-  CU(cudaMalloc(&h->sp_hcount, G * 4));
+  CU(cudaMalloc(&h->sp_hcount, 2 * G * 4));  // two hash lists per F3 CTA
   h->sp_debug = env_flag("GSCAN_SP_DEBUG");
   // measurement hook only: skipping the duplicate check is exact only for
   // duplicate-free inputs
   h->sp_no_dup = env_flag("GSCAN_SP_NODUP");
   CU(cudaMalloc(&h->sp_hist_part, (size_t)G * nb * 4));
   CU(cudaMalloc(&h->sp_phi_part, (size_t)G * nb * 4));
-  CU(cudaMalloc(&h->sp_part_off, ((size_t)G * kSpParts + 1) * 4));
+  CU(cudaMalloc(&h->sp_part_off, ((size_t)2 * G * kSpParts + 1) * 4));
   CU(cudaMalloc(&h->sp_d2, G * sizeof(SpD2)));
   uint32_t** nb_bufs[] = {&h->sp_hist, &h->sp_bstart, &h->sp_glist, &h->sp_gcnt, &h->sp_phimax,
                           &h->sp_prefmax, &h->sp_slice, &h->sp_ccnt, &h->sp_cstart, &h->sp_wcnt,
@@ -1093,7 +1110,7 @@ int sparse_enqueue(gscan_handle* h, const double* xs, const double* ys, uint32_t
 // with them: those latency-bound CTAs get SMs of their own (sparse.cuh
 // side_take). Measured: 16-36 free SMs equally good; two smaller side CTAs
 // per SM, or leaving no SM free, slower.
-constexpr uint32_t kSideFreeSms = 24;
+constexpr uint32_t kSideFreeSms = 32;
 constexpr size_t kSpSideSmem = 180 * 1024;
 static_assert(kSpSideSmem >= kSpDupPartSmem && kSpSideSmem >= kSpDupSlots * 8, "side smem");
 static_assert(kSpSideSmem + 1024 + kTreeCtaSmem + 1024 > 228 * 1024, "tree CTA would fit");
@@ -1104,30 +1121,29 @@ uint32_t side_free_sms() {
 
 int sparse_dup_check(gscan_handle* h, uint32_t n) {
   const uint32_t G = (uint32_t)h->sp_grid;
+  const uint32_t nl = 2 * G;  // hash lists (k_sp_phi: two per CTA)
+  static_assert(kSpPartChunk == 8 * 1024, "k_sp_dup_part: 8 entries per thread");
   const uint32_t cap = sparse_region_cap(h, n);
   CU(cudaEventRecord(h->ev_f3, h->stream));
   CU(cudaStreamWaitEvent(h->side, h->ev_f3, 0));
   {
-    const uint64_t tiles = ((uint64_t)kSpParts * G + 1 + kScanTile - 1) / kScanTile;
+    const uint64_t tiles = ((uint64_t)kSpParts * nl + 1 + kScanTile - 1) / kScanTile;
     CU(cudaMemsetAsync(h->sp_side_status, 0, tiles * 8, h->side));
     CU(cudaMemsetAsync(h->sp_side_ticket, 0, sizeof(Counters), h->side));
     Launch L(h, "k_scan_u32(side)", h->side);
-    k_scan_u32<<<tiles, kBlock, 0, h->side>>>(h->sp_part_off, kSpParts * G, h->sp_part_off,
+    k_scan_u32<<<tiles, kBlock, 0, h->side>>>(h->sp_part_off, kSpParts * nl, h->sp_part_off,
                                              h->sp_side_status, h->sp_side_ticket);
   }
-  CU(cudaMemcpyAsync(h->sp_part_cur, h->sp_part_off, (size_t)kSpParts * G * 4,
-                     cudaMemcpyDeviceToDevice, h->side));
   CU(cudaMemsetAsync(h->sp_side_work, 0, 2 * sizeof(uint32_t), h->side));
   {
     Launch L(h, "k_sp_dup_part", h->side);
-    const uint32_t chunks = (cap + kSpPartChunk - 1) / kSpPartChunk;
     k_sp_dup_part<<<h->sm_count, 1024, kSpSideSmem, h->side>>>(
-        h->sp_dup, h->sp_hcount, cap, chunks, G, h->sp_part_cur, h->sp_st, h->sp_dup2,
-        h->sp_side_work, side_free_sms());
+        h->sp_dup, h->sp_hcount, cap / 2, nl, h->sp_part_off, h->sp_st, h->sp_dup2, h->sp_side_work,
+        side_free_sms());
   }
   {
     Launch L(h, "k_sp_dups", h->side);
-    k_sp_dups<<<h->sm_count, 512, kSpSideSmem, h->side>>>(h->sp_dup2, h->sp_part_off, G, h->sp_st,
+    k_sp_dups<<<h->sm_count, 1024, kSpSideSmem, h->side>>>(h->sp_dup2, h->sp_part_off, nl, h->sp_st,
                                                               h->sp_side_work + 1, side_free_sms());
   }
   CU(cudaEventRecord(h->ev_dup, h->side));
@@ -1393,8 +1409,8 @@ int gscan_create(int device, gscan_handle** out) {
     CU(cudaFuncSetAttribute(k_sp_dup_part, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)kSpSideSmem));
     CU(cudaFuncSetAttribute(k_gr_mid, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTreeSmem));
-    CU(cudaFuncSetAttribute(k_gr_local0, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTreeCtaSmem));
-    CU(cudaFuncSetAttribute(k_gr_down0, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTreeCtaSmem));
+    CU(cudaFuncSetAttribute(k_gr_up, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTreeCtaSmem));
+    CU(cudaFuncSetAttribute(k_gr_down, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTreeCtaSmem));
     CU(cudaFuncSetAttribute(k_gr_cert, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTreeCtaSmem));
     h->sp_grid = h->sm_count;
     h->use_graphs = !env_flag("GSCAN_NO_GRAPH");
@@ -1415,7 +1431,7 @@ int gscan_destroy(gscan_handle* h) {
   if (h->stream) cudaStreamSynchronize(h->stream);
   free_buffers(h);
   dfree(h->partials); dfree(h->ext); dfree(h->ctr); dfree(h->scratch64);
-  dfree(h->sp_th); dfree(h->sp_cdf); dfree(h->sp_cells); dfree(h->sp_big); dfree(h->sp_bigg); dfree(h->sp_gcount); dfree(h->sp_side_status); dfree(h->sp_side_ticket); dfree(h->sp_part_cur); dfree(h->sp_side_work); dfree(h->sp_ccount); dfree(h->sp_hcount); dfree(h->sp_hist_part); dfree(h->sp_phi_part); dfree(h->sp_part_off);
+  dfree(h->sp_th); dfree(h->sp_cdf); dfree(h->sp_cells); dfree(h->sp_big); dfree(h->sp_bigg); dfree(h->sp_gcount); dfree(h->sp_side_status); dfree(h->sp_side_ticket); dfree(h->sp_side_work); dfree(h->sp_ccount); dfree(h->sp_hcount); dfree(h->sp_hist_part); dfree(h->sp_phi_part); dfree(h->sp_part_off);
   dfree(h->sp_d2); dfree(h->sp_hist); dfree(h->sp_bstart); dfree(h->sp_gbits); dfree(h->sp_glist);
   dfree(h->sp_gcnt); dfree(h->sp_phimax); dfree(h->sp_prefmax); dfree(h->sp_slice);
   dfree(h->sp_ccnt); dfree(h->sp_cstart); dfree(h->sp_wcnt); dfree(h->sp_wstart); dfree(h->sp_rlo);

@@ -60,7 +60,7 @@ constexpr uint32_t kSpDupSlotBits = 14;
 constexpr uint32_t kSpDupSlots = 1u << kSpDupSlotBits;  // dup-check hash set slots (smem, 8 B)
 constexpr uint32_t kSpDupRound = 8192;        // entries per hash-set round (load <= 0.5)
 constexpr uint32_t kSpPartChunk = 8192;       // entries per partitioning chunk (smem)
-constexpr size_t kSpDupPartSmem = (size_t)kSpPartChunk * 16 + (size_t)kSpParts * 12;  // in/out + cnt/off/base
+constexpr size_t kSpDupPartSmem = (size_t)kSpPartChunk * 16 + (size_t)kSpParts * 12;  // in/out + cnt/off/cursor
 
 enum : uint32_t {
   kSpFailTie = 1u,        // several points share the maximal dist2
@@ -826,13 +826,17 @@ __global__ void __launch_bounds__(kSpThreads, 1) k_sp_phi(
     float* __restrict__ phi32) {
   extern __shared__ uint32_t s_phi[];  // kSpBuckets
   __shared__ uint32_t s_g[kSpBuckets / 32];
-  __shared__ uint32_t s_part[kSpParts];
-  __shared__ uint32_t s_ng, s_nh;
+  __shared__ uint32_t s_part[2][kSpParts];  // per half-CTA hash list
+  __shared__ uint32_t s_ng, s_nh[2];
   if (st->fail) return;
   for (uint32_t b = threadIdx.x; b < kSpBuckets; b += blockDim.x) s_phi[b] = 0;
   for (uint32_t w = threadIdx.x; w < kSpBuckets / 32; w += blockDim.x) s_g[w] = gbits[w];
-  for (uint32_t p = threadIdx.x; p < kSpParts; p += blockDim.x) s_part[p] = 0;
-  if (threadIdx.x == 0) { s_ng = 0; s_nh = 0; }
+  for (uint32_t p = threadIdx.x; p < 2 * kSpParts; p += blockDim.x) s_part[0][p] = 0;
+  if (threadIdx.x == 0) { s_ng = 0; s_nh[0] = 0; s_nh[1] = 0; }
+  // two hash lists per CTA (threads [0, 256) and [256, 512)) of cap / 2 slots
+  // each, so the duplicate check's work items are finer than the CTAs
+  const uint32_t half = threadIdx.x >= kSpThreads / 2 ? 1u : 0u;
+  const size_t hbase = (size_t)(2 * blockIdx.x + half) * (cap / 2);
   const double lx = st->lx, ly = st->ly;
   const double ux = __dsub_rn(ext->ax, lx), uy = __dsub_rn(ext->ay, ly);
   const uint32_t b_l = st->b_l;
@@ -846,7 +850,7 @@ __global__ void __launch_bounds__(kSpThreads, 1) k_sp_phi(
     uint64_t h = 0;
     if (surv) {
       h = coord_hash64(x, y);
-      atomicAdd(&s_part[(uint32_t)(h >> (64 - kSpPartBits))], 1u);
+      atomicAdd(&s_part[half][(uint32_t)(h >> (64 - kSpPartBits))], 1u);
       double v2;
       const double raw = sp_phi_raw(x, y, lx, ly, ux, uy, &v2);
       plo = fmin(plo, raw);
@@ -860,8 +864,8 @@ __global__ void __launch_bounds__(kSpThreads, 1) k_sp_phi(
         phi32[i] = __int_as_float(0x7fc00000);  // NaN: always a candidate
       }
     }
-    const uint32_t jh = warp_claim(&s_nh, surv);
-    if (surv) hlist[base + jh] = h;
+    const uint32_t jh = warp_claim(&s_nh[half], surv);
+    if (surv) hlist[hbase + jh] = h;
     const uint32_t jg = warp_claim(&s_ng, emit);
     if (emit) { g_idx[base + jg] = i; g_b[base + jg] = b; }
   };
@@ -891,7 +895,7 @@ __global__ void __launch_bounds__(kSpThreads, 1) k_sp_phi(
       gat[k] = false;
       if (!surv) continue;
       ++nh;
-      atomicAdd(&s_part[(uint32_t)(h[k] >> (64 - kSpPartBits))], 1u);
+      atomicAdd(&s_part[half][(uint32_t)(h[k] >> (64 - kSpPartBits))], 1u);
       plo = fmin(plo, raw[k]);
       phi_ = fmax(phi_, raw[k]);
       gat[k] = sp_gathered(s_g, b[k]);
@@ -905,10 +909,10 @@ __global__ void __launch_bounds__(kSpThreads, 1) k_sp_phi(
       }
     }
     const uint32_t lane = threadIdx.x & 31;
-    uint32_t at = warp_scan_claim(&s_nh, nh, lane);
+    uint32_t at = warp_scan_claim(&s_nh[half], nh, lane);
 #pragma unroll
     for (int k = 0; k < 4; ++k)
-      if (b[k] != kSpNoCode) hlist[base + at++] = h[k];
+      if (b[k] != kSpNoCode) hlist[hbase + at++] = h[k];
     if (__any_sync(0xffffffffu, ng != 0)) {
       uint32_t ag = warp_scan_claim(&s_ng, ng, lane);
 #pragma unroll
@@ -963,10 +967,13 @@ __global__ void __launch_bounds__(kSpThreads, 1) k_sp_phi(
   uint32_t* pp = phi_part + (size_t)blockIdx.x * kSpBuckets;
   for (uint32_t b = threadIdx.x; b < kSpBuckets; b += blockDim.x) pp[b] = s_phi[b];
   for (uint32_t p = threadIdx.x; p < kSpParts; p += blockDim.x)
-    part_cnt[(size_t)p * gridDim.x + blockIdx.x] = s_part[p];  // partition-major
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh)  // partition-major over the 2G lists
+      part_cnt[(size_t)p * 2 * gridDim.x + 2 * blockIdx.x + hh] = s_part[hh][p];
   if (threadIdx.x == 0) {
     g_count[blockIdx.x] = s_ng;
-    h_count[blockIdx.x] = s_nh;
+    h_count[2 * blockIdx.x] = s_nh[0];
+    h_count[2 * blockIdx.x + 1] = s_nh[1];
     atomicAdd(&st->n_g, s_ng);
   }
 #pragma unroll
@@ -999,15 +1006,15 @@ __device__ __forceinline__ bool side_take(uint32_t* ticket, uint32_t* s_item, ui
   return w < n_items;
 }
 
-// Duplicate check, step 1: work item (k, c) moves chunk k of F3-CTA c's hash
-// list into the partitions. Within the chunk, entries are grouped by
-// partition in shared memory; each partition's run is reserved with one
-// atomic on the region's cursor (cur[p * C + c], starting at the
-// partition-major exclusive scan of the counts) and written contiguously.
+// Duplicate check, step 1: work item c moves hash list c (F3-CTA c / 2, half
+// c % 2; cap slots each) into the partitions. The list's run of partition p starts at the partition-major
+// exclusive scan of the counts (part_off[p * C + c]); the CTA owns those runs,
+// so the cursors live in shared memory. Chunks of kSpPartChunk entries are
+// grouped by partition in shared memory and written run by run.
 __global__ void __launch_bounds__(1024) k_sp_dup_part(const uint64_t* __restrict__ hlist,
                                                       const uint32_t* __restrict__ h_count,
-                                                      uint32_t cap, uint32_t chunks, uint32_t C,
-                                                      uint32_t* __restrict__ cur,
+                                                      uint32_t cap, uint32_t C,
+                                                      const uint32_t* __restrict__ part_off,
                                                       const SpState* __restrict__ st,
                                                       uint64_t* __restrict__ parted,
                                                       uint32_t* __restrict__ ticket, uint32_t n_free) {
@@ -1016,79 +1023,89 @@ __global__ void __launch_bounds__(1024) k_sp_dup_part(const uint64_t* __restrict
   uint64_t* s_out = s_in + kSpPartChunk;
   uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_out + kSpPartChunk);
   uint32_t* s_off = s_cnt + kSpParts;
-  uint32_t* s_base = s_off + kSpParts;
+  uint32_t* s_cur = s_off + kSpParts;
   __shared__ uint32_t s_w[32];
   __shared__ uint32_t s_item;
   if (st->fail || sm_id() < n_free) return;
-  uint32_t w;
-  while (side_take(ticket, &s_item, chunks * C, w)) {
-    const uint32_t c = w / chunks;
-    const uint32_t c0 = (w % chunks) * kSpPartChunk;
+  uint32_t c;
+  while (side_take(ticket, &s_item, C, c)) {
     const uint32_t cnt = h_count[c];
-    if (c0 >= cnt) continue;  // uniform per CTA
-    const uint32_t len = min(kSpPartChunk, cnt - c0);
-    const uint64_t* src = hlist + (size_t)c * cap + c0;
-    for (uint32_t p = threadIdx.x; p < kSpParts; p += blockDim.x) s_cnt[p] = 0;
+    const uint64_t* src = hlist + (size_t)c * cap;
+    for (uint32_t p = threadIdx.x; p < kSpParts; p += blockDim.x) {
+      s_cur[p] = part_off[(size_t)p * C + c];
+      s_cnt[p] = 0;
+    }
+    // chunk = 8 entries per thread; the next chunk's loads are issued before
+    // the current one is grouped and written
+    uint64_t hv[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const uint32_t t = threadIdx.x + u * blockDim.x;
+      hv[u] = t < cnt ? src[t] : 0ull;
+    }
     __syncthreads();
-    for (uint32_t t0 = threadIdx.x; t0 < len; t0 += 8 * blockDim.x) {
-      uint64_t hv[8];
+    for (uint32_t c0 = 0; c0 < cnt; c0 += kSpPartChunk) {
+      const uint32_t len = min(kSpPartChunk, cnt - c0);
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        const uint32_t t = t0 + u * blockDim.x;
-        hv[u] = t < len ? src[t] : 0ull;
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const uint32_t t = t0 + u * blockDim.x;
+        const uint32_t t = threadIdx.x + u * blockDim.x;
         if (t < len) {
           s_in[t] = hv[u];
           atomicAdd(&s_cnt[(uint32_t)(hv[u] >> (64 - kSpPartBits))], 1u);
         }
       }
-    }
-    __syncthreads();
-    // exclusive scan of the partition counts (kSpParts = 2 x blockDim), and
-    // one reservation per present partition on the region's cursor
-    {
-      const uint32_t a = s_cnt[2 * threadIdx.x], b = s_cnt[2 * threadIdx.x + 1];
-      const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-      uint32_t x = a + b;
+      const uint32_t n0 = c0 + kSpPartChunk;
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
+      for (int u = 0; u < 8; ++u) {
+        const uint32_t t = n0 + threadIdx.x + u * blockDim.x;
+        hv[u] = t < cnt ? src[t] : 0ull;
       }
-      if (lane == 31) s_w[warp] = x;
       __syncthreads();
-      if (warp == 0) {
-        uint32_t v = s_w[lane];
+      // exclusive scan of the partition counts (kSpParts = 2 x blockDim)
+      {
+        const uint32_t a = s_cnt[2 * threadIdx.x], b = s_cnt[2 * threadIdx.x + 1];
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        uint32_t x = a + b;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-          const uint32_t y = __shfl_up_sync(0xffffffffu, v, o);
-          if (lane >= o) v += y;
+          const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+          if (lane >= o) x += y;
         }
-        s_w[lane] = v;
+        if (lane == 31) s_w[warp] = x;
+        __syncthreads();
+        if (warp == 0) {
+          uint32_t v = s_w[lane];
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += y;
+          }
+          s_w[lane] = v;
+        }
+        __syncthreads();
+        const uint32_t ex = x - (a + b) + (warp ? s_w[warp - 1] : 0);
+        s_off[2 * threadIdx.x] = ex;
+        s_off[2 * threadIdx.x + 1] = ex + a;
       }
       __syncthreads();
-      const uint32_t ex = x - (a + b) + (warp ? s_w[warp - 1] : 0);
-      s_off[2 * threadIdx.x] = ex;
-      s_off[2 * threadIdx.x + 1] = ex + a;
-      const uint32_t p0 = 2 * threadIdx.x, p1 = p0 + 1;
-      s_base[p0] = a ? atomicAdd(&cur[(size_t)p0 * C + c], a) : 0u;
-      s_base[p1] = b ? atomicAdd(&cur[(size_t)p1 * C + c], b) : 0u;
-    }
-    __syncthreads();
-    for (uint32_t t = threadIdx.x; t < len; t += blockDim.x) {
-      const uint64_t h = s_in[t];
-      const uint32_t p = (uint32_t)(h >> (64 - kSpPartBits));
-      s_out[atomicAdd(&s_off[p], 1u)] = h;  // s_off[p] ends at the next run's start
-    }
-    __syncthreads();
-    for (uint32_t t = threadIdx.x; t < len; t += blockDim.x) {
-      const uint64_t h = s_out[t];
-      const uint32_t p = (uint32_t)(h >> (64 - kSpPartBits));
-      const uint32_t run0 = s_off[p] - s_cnt[p];
-      parted[s_base[p] + (t - run0)] = h;
+      for (uint32_t t = threadIdx.x; t < len; t += blockDim.x) {
+        const uint64_t h = s_in[t];
+        const uint32_t p = (uint32_t)(h >> (64 - kSpPartBits));
+        s_out[atomicAdd(&s_off[p], 1u)] = h;  // s_off[p] ends at the next run's start
+      }
+      __syncthreads();
+      for (uint32_t t = threadIdx.x; t < len; t += blockDim.x) {
+        const uint64_t h = s_out[t];
+        const uint32_t p = (uint32_t)(h >> (64 - kSpPartBits));
+        const uint32_t run0 = s_off[p] - s_cnt[p];
+        parted[s_cur[p] + (t - run0)] = h;
+      }
+      __syncthreads();
+      for (uint32_t p = threadIdx.x; p < kSpParts; p += blockDim.x) {
+        s_cur[p] += s_cnt[p];
+        s_cnt[p] = 0;
+      }
+      __syncthreads();
     }
   }
 }
@@ -1096,7 +1113,7 @@ __global__ void __launch_bounds__(1024) k_sp_dup_part(const uint64_t* __restrict
 // Duplicate check, step 2: a partition per work item, open-addressing set of
 // its 64-bit hashes in shared memory (in rounds over sub-ranges of the hash);
 // an equal hash means a possible duplicate -> the full path (exact).
-__global__ void __launch_bounds__(512) k_sp_dups(const uint64_t* __restrict__ parted,
+__global__ void __launch_bounds__(1024) k_sp_dups(const uint64_t* __restrict__ parted,
                                                  const uint32_t* __restrict__ part_off,
                                                  uint32_t nparts_cta, SpState* __restrict__ st,
                                                  uint32_t* __restrict__ ticket, uint32_t n_free) {
