@@ -187,9 +187,12 @@ int gscan_last_graham_info(const gscan_handle* h, uint32_t* path, uint32_t* cert
 
 /* Sparse round-2 path of the last call (the default for n >= 65536 with the
  * default toggles): used = 1 when its result was returned; fail_bits != 0
- * when it declined and the full sort ran instead (tie for the farthest point,
- * duplicates, a failed verification, ...); n_walked = points it sorted and
- * walked exactly (gathered + candidates + anchor). */
+ * when it declined and the full sort ran instead: 1 tie for the farthest
+ * point, 4 a region with <= 1 point, 8 possible duplicates, 16 failed
+ * verification, 32 capacity, 64 internal, 128 too few points, 256 too many
+ * walk candidates (near-circular inputs: the full sort is faster);
+ * n_walked = points it sorted and walked exactly (gathered + candidates +
+ * anchor). */
 int gscan_last_sparse_info(const gscan_handle* h, uint32_t* used, uint32_t* fail_bits,
                            uint32_t* n_walked);
 

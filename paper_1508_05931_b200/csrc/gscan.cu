@@ -1024,6 +1024,10 @@ int sparse_enqueue(gscan_handle* h, const double* xs, const double* ys, uint32_t
                                                  h->sp_ccount, drop);
   }
   {
+    Launch L(h, "k_sp_check_cand");
+    k_sp_check_cand<<<1, 32, 0, s>>>(h->sp_st);
+  }
+  {
     Launch L(h, "k_sp_rank_c");
     k_sp_emit_place<1><<<dim3(4, G), 256, 0, s>>>(xs, ys, h->surv, h->sp_eb, h->rank, h->sp_ccount,
                                                   cap, h->sp_ccnt, nullptr, h->ext, h->sp_st,

@@ -71,6 +71,7 @@ enum : uint32_t {
   kSpFailCap = 32u,       // a gathered bucket / dup partition exceeds capacity
   kSpFailInternal = 64u,  // inconsistent counts (should not happen)
   kSpFailFew = 128u,      // too few points for the bucket structure
+  kSpFailMany = 256u,     // too many walk candidates (the full sort is faster)
 };
 
 struct SpD2 {        // per-CTA farthest-point candidate
@@ -1655,6 +1656,15 @@ __global__ void __launch_bounds__(kSpCandThreads, 1) k_sp_cand(
 
 // Walk-array bucket sizes: gathered buckets bring all their points, others
 // their candidates.
+// After F4: with more than m / kSpManyDiv candidates (points near a circle)
+// the candidate sort and walk cost more than the full sort; decline, so the
+// remaining sparse kernels exit at once.
+constexpr uint32_t kSpManyDiv = 8;
+__global__ void k_sp_check_cand(SpState* __restrict__ st) {
+  if (threadIdx.x == 0 && !st->fail && st->n_c > max(st->m / kSpManyDiv, 65536u))
+    atomicOr(&st->fail, kSpFailMany);
+}
+
 __global__ void k_sp_wcount(const uint32_t* __restrict__ gbits, const uint32_t* __restrict__ hist,
                             const uint32_t* __restrict__ ccnt, uint32_t* __restrict__ wcnt) {
   const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;

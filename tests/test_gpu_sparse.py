@@ -11,7 +11,7 @@ import pytest
 
 pytestmark = pytest.mark.gpu
 
-FAIL_TIE, FAIL_DUP, FAIL_VERIFY = 1, 8, 16
+FAIL_TIE, FAIL_DUP, FAIL_VERIFY, FAIL_MANY = 1, 8, 16, 256
 
 
 def _run(engine, oracle_mod, xs, ys, debug=0, **cfg):
@@ -69,7 +69,9 @@ def test_sparse_degenerate_inputs(engine, oracle_mod, kind):
     """Convex position, near-circles, collinear sets and lattices: exact
     whichever way the call resolves (fast path or declined to the sort)."""
     xs, ys = _gen(kind, 200_000, 5)
-    _run(engine, oracle_mod, xs, ys)
+    used, fail, _ = _run(engine, oracle_mod, xs, ys)
+    if kind == "circle":  # every point is a walk candidate: the full sort is faster
+        assert used == 0 and fail & FAIL_MANY, hex(fail)
 
 
 @pytest.mark.parametrize("chunks", [1, 7, 100, 5000])
