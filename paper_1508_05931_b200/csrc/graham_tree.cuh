@@ -42,7 +42,9 @@ namespace gscan {
 
 constexpr int kTreeChunk = 32;      // chunk length on every level
 constexpr int kTreeThreads = 256;   // the middle CTA; chunks are processed in waves of this many
-constexpr uint32_t kTreeTop = 128;  // largest top-level list for the single-thread scan
+constexpr uint32_t kTreeTop = 128;       // levels stop shrinking once this small
+constexpr uint32_t kTreeTopMax = 3072;   // largest top level (a level that stops
+                                         // shrinking is mostly final-hull vertices)
 constexpr int kTreeMaxLevels = 24;
 constexpr int kTreePC = 8;          // stack rows carried in a boundary record
 constexpr int kTreeRows = kTreePC + kTreeChunk;
@@ -82,7 +84,7 @@ struct TreeWork {
   uint32_t* chainp;  // N: their R positions
   double* chainx;    // N: their coordinates
   double* chainy;
-  uint32_t* fstack;  // kTreeTop
+  uint32_t* fstack;  // kTreeTopMax
   uint32_t* Qp[kTreeMaxLevels + 1];
   double* Qx[kTreeMaxLevels + 1];
   double* Qy[kTreeMaxLevels + 1];
@@ -379,8 +381,10 @@ __global__ void __launch_bounds__(1024) k_gr_scan(uint32_t N, int j, TreeWork w,
     w.off[j][nch] = total;
     const bool shrink =
         (j == 0) ? (total * 20ull <= (uint64_t)nq * 17) : (total * 10ull <= (uint64_t)nq * 9);
-    // (a level-1 list short enough for the top scan needs no shrink)
-    if ((!shrink && !(j >= 1 && nq <= kTreeTop)) || total > w.cap[j + 1]) info[0] = 1;
+    // a stalled level is the top level if the warp top scan can take it
+    // (k_gr_mid decides); level 0 must shrink (else the buffer is in convex
+    // position and the junction strategy is the right one)
+    if ((!shrink && (j == 0 || total > kTreeTopMax)) || total > w.cap[j + 1]) info[0] = 1;
     info[11 + j] = total;
   }
 }
@@ -448,10 +452,16 @@ __global__ void __launch_bounds__(kTreeThreads, 1) k_gr_mid(
     s_nq[0] = N;
     s_nq[1] = info[11];
     s_nq[2] = info[12];
-    s_K = s_nq[1] <= kTreeTop ? 1 : (s_nq[2] <= kTreeTop ? 2 : -1);
-    s_bad = 0;
+    // top level: small enough, or the first level that stops shrinking
+    const bool stall2 = (uint64_t)s_nq[2] * 10 > (uint64_t)s_nq[1] * 9;
+    s_K = s_nq[1] <= kTreeTop ? 1 : ((s_nq[2] <= kTreeTop || stall2) ? 2 : -1);
+    s_bad = s_K == 2 && s_nq[2] > kTreeTopMax;
   }
   __syncthreads();
+  if (s_bad) {
+    if (t == 0) { info[0] = 1; info[3] = 0; }
+    return;
+  }
   for (int j = 2; s_K < 0 && j < kTreeMaxLevels; ++j) {
     const TreeLevel L = tree_level(w, j, s_nq[j]);
     for (uint32_t c0 = 0; c0 < L.nch; c0 += kTreeThreads) {
@@ -472,9 +482,12 @@ __global__ void __launch_bounds__(kTreeThreads, 1) k_gr_mid(
     const uint32_t total = tree_scan(L.off, L.nch, s_w, &s_carry);
     if (t == 0) {
       L.off[L.nch] = total;
-      if (total * 10ull > (uint64_t)L.nq * 9 || total > w.cap[j + 1] || j + 1 > kTreeMaxLevels - 1)
+      const bool stall = total * 10ull > (uint64_t)L.nq * 9;
+      if ((stall && total > kTreeTopMax) || total > w.cap[j + 1] || j + 1 > kTreeMaxLevels - 1)
         s_bad = 1;
       s_nq[j + 1] = total;
+      if (stall) s_K = j + 1;  // the top level (before the s_K assignment below)
+      if (j + 1 < 6) info[10 + j + 1] = total;  // diagnostics
     }
     __syncthreads();
     if (s_bad) break;
@@ -495,54 +508,104 @@ __global__ void __launch_bounds__(kTreeThreads, 1) k_gr_mid(
     info[8] = (uint32_t)(clock64() - t_start);
     for (int j = 3; j <= K && j < 6; ++j) info[10 + j] = s_nq[j];
   }
-  // ---- top: one thread over Q_K (staged in shared memory); then all threads
-  // turn its boundary tops into records by walking the persistent links ----
+  // ---- top: warp 0 scans Q_K (<= kTreeTopMax, staged in shared memory),
+  // 32 points per iteration while nothing pops (the scan of k_graham_local);
+  // it records below(k), the element each point is pushed onto. The state
+  // before a Q_{K-1} boundary is "top = the previous element", so all threads
+  // then turn below() into parent[], boundary tops and records. ----
   {
     const TreeLevel tl = tree_level(w, K, s_nq[K]);
     const TreeLevel ll = tree_level(w, K - 1, s_nq[K - 1]);
-    const uint32_t nk = tl.nq;  // <= kTreeTop
-    double* s_x = r.X;
+    const uint32_t nk = tl.nq;
+    double* s_x = r.X;                        // [kTreeTopMax]
     double* s_y = r.Y;
-    uint32_t* s_p = r.P;                   // R position of each Q_K element
-    uint32_t* s_ch = r.P + kTreeTop;       // its Q_{K-1} chunk
-    uint32_t* s_par = r.P + 2 * kTreeTop;  // Q_K index below it (kNone: none)
-    uint32_t* s_st = r.P + 3 * kTreeTop;   // the stack (Q_K indices)
-    uint32_t* bk = w.tmp;                  // Q_K index of the top before each boundary
+    double* st_x = r.X + kTreeTopMax;         // the stack
+    double* st_y = r.Y + kTreeTopMax;
+    uint32_t* s_p = r.P;                      // R position of each Q_K element
+    uint32_t* s_par = r.P + kTreeTopMax;      // below(k) as a Q_K index (kNone: none)
+    uint32_t* st_i = r.P + 2 * kTreeTopMax;   // the stack (Q_K indices)
+    uint32_t* bk = w.tmp;                     // Q_K index of the top before each boundary
     for (uint32_t k = t; k < nk; k += kTreeThreads) {
       s_p[k] = tl.Qp[k];
-      s_ch[k] = tl.up[k] / kTreeChunk;
       s_x[k] = tl.Qx[k];
       s_y[k] = tl.Qy[k];
     }
     __syncthreads();
-    if (t == 0) {
+    if (t < 32) {
+      const int lane = t;
       int top = 0;
-      double s1x = 0, s1y = 0, s2x = 0, s2y = 0;
-      uint32_t next_b = 0;
-      for (uint32_t k = 0; k < nk; ++k) {
-        const uint32_t tk = top ? s_st[top - 1] : kNone;
-        for (; next_b <= s_ch[k]; ++next_b) bk[next_b] = tk;
-        const double px = s_x[k], py = s_y[k];
-        while (top >= 2 && !left_turn(s2x, s2y, s1x, s1y, px, py)) {
-          --top;
-          s1x = s2x; s1y = s2y;
-          if (top >= 2) { const uint32_t q = s_st[top - 2]; s2x = s_x[q]; s2y = s_y[q]; }
+      int i = 0;
+      while (i < (int)nk) {
+        const int j = i + lane;
+        const bool valid = j < (int)nk;
+        const double px = valid ? s_x[j] : 0.0, py = valid ? s_y[j] : 0.0;
+        const int depth = top + lane;  // stack size before pushing j if all earlier lanes pushed
+        bool ok = true;
+        if (valid && depth >= 2) {
+          double ax, ay, bx, by;
+          if (lane >= 2) { ax = s_x[j - 2]; ay = s_y[j - 2]; bx = s_x[j - 1]; by = s_y[j - 1]; }
+          else if (lane == 1) { ax = st_x[top - 1]; ay = st_y[top - 1]; bx = s_x[j - 1]; by = s_y[j - 1]; }
+          else { ax = st_x[top - 2]; ay = st_y[top - 2]; bx = st_x[top - 1]; by = st_y[top - 1]; }
+          ok = left_turn(ax, ay, bx, by, px, py);
         }
-        const uint32_t below = top ? s_st[top - 1] : kNone;
-        s_par[k] = below;
-        w.parent[s_p[k]] = below != kNone ? s_p[below] : kNone;
-        s_st[top++] = k;
-        s2x = s1x; s2y = s1y;
-        s1x = px; s1y = py;
+        const uint32_t fm = __ballot_sync(0xffffffffu, valid && !ok);
+        const int nvalid = min(32, (int)nk - i);
+        const int f = fm ? (__ffs(fm) - 1) : 32;
+        const int commit = min(f, nvalid);
+        if (lane < commit) {
+          st_x[top + lane] = px;
+          st_y[top + lane] = py;
+          st_i[top + lane] = (uint32_t)j;
+          s_par[j] = lane ? (uint32_t)(j - 1) : (top ? st_i[top - 1] : kNone);
+        }
+        top += commit;
+        __syncwarp();
+        if (f < nvalid) {
+          const double fx = __shfl_sync(0xffffffffu, px, f), fy = __shfl_sync(0xffffffffu, py, f);
+          int newtop;
+          int dhi = top - 1;
+          while (true) {
+            const int d = dhi - lane;
+            const bool l = d >= 1 && left_turn(st_x[d - 1], st_y[d - 1], st_x[d], st_y[d], fx, fy);
+            const uint32_t m = __ballot_sync(0xffffffffu, l);
+            if (m) { newtop = dhi - (__ffs(m) - 1) + 1; break; }
+            if (dhi - 31 <= 1) { newtop = min(top, 1); break; }
+            dhi -= 32;
+          }
+          if (lane == 0) {
+            st_x[newtop] = fx;
+            st_y[newtop] = fy;
+            st_i[newtop] = (uint32_t)(i + f);
+            s_par[i + f] = newtop ? st_i[newtop - 1] : kNone;
+          }
+          top = newtop + 1;
+          i += f + 1;
+        } else {
+          i += nvalid;
+        }
+        __syncwarp();
       }
-      const uint32_t tk = top ? s_st[top - 1] : kNone;
-      for (; next_b <= ll.nch; ++next_b) bk[next_b] = tk;
-      for (int k = 0; k < top; ++k) w.fstack[k] = s_p[s_st[k]];
-      info[1] = (uint32_t)top;
-      // every level's boundary after its last chunk holds the final top
-      const uint32_t ftop = top ? s_p[s_st[top - 1]] : kNone;
-      for (int j = 0; j < K; ++j) w.bt[j][(s_nq[j] + kTreeChunk - 1) / kTreeChunk] = ftop;
+      for (int k = lane; k < top; k += 32) w.fstack[k] = s_p[st_i[k]];
+      if (lane == 0) {
+        info[1] = (uint32_t)top;
+        // every level's boundary after its last chunk holds the final top
+        const uint32_t ftop = top ? s_p[st_i[top - 1]] : kNone;
+        for (int j = 0; j < K; ++j) w.bt[j][(s_nq[j] + kTreeChunk - 1) / kTreeChunk] = ftop;
+      }
     }
+    __syncthreads();
+    for (uint32_t k = t; k < nk; k += kTreeThreads) {
+      const uint32_t below = s_par[k];
+      w.parent[s_p[k]] = below != kNone ? s_p[below] : kNone;
+      // boundaries b in (chunk(k - 1), chunk(k)] start at element k
+      const uint32_t ch = tl.up[k] / kTreeChunk;
+      const uint32_t b0 = k ? tl.up[k - 1] / kTreeChunk + 1 : 0;
+      for (uint32_t b = b0; b <= ch; ++b) bk[b] = k ? k - 1 : kNone;
+      if (k + 1 == nk)
+        for (uint32_t b = ch + 1; b <= ll.nch; ++b) bk[b] = k;
+    }
+    if (nk == 0)
+      for (uint32_t b = t; b <= ll.nch; b += kTreeThreads) bk[b] = kNone;
     __syncthreads();
     for (uint32_t b = t; b < ll.nch; b += kTreeThreads) {
       uint32_t e[kTreePC];

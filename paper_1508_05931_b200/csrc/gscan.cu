@@ -635,7 +635,7 @@ int graham_tree(gscan_handle* h, const double* Rx, const double* Ry, const uint3
     caps[j] = std::min<uint64_t>((j == 1 ? (uint64_t)N * 17 / 20 : caps[j - 1] * 9 / 10) + 64,
                                  kTreeHiCap);
   auto nchunks = [&](int j) { return caps[j] / kTreeChunk + 2; };
-  uint64_t need = 8ull * N + kTreeTop + 64 * 8;  // parent, tmp, chainq/p, chainx/y
+  uint64_t need = 8ull * N + kTreeTopMax + 64 * 8;  // parent, tmp, chainq/p, chainx/y, fstack
   for (int j = 0; j <= kTreeMaxLevels; ++j) {
     if (j >= 1) need += 6 * caps[j] + 4 * 32;                // Qp, Qx, Qy, up
     need += nchunks(j) * (2 + 2 + 8 + 16 + 16) + 7 * 32;   // off, bt, rec
@@ -656,7 +656,7 @@ int graham_tree(gscan_handle* h, const double* Rx, const double* Ry, const uint3
   w.chainp = take(N);
   w.chainx = take_d(N);
   w.chainy = take_d(N);
-  w.fstack = take(kTreeTop);
+  w.fstack = take(kTreeTopMax);
   for (int j = 0; j <= kTreeMaxLevels; ++j) {
     w.cap[j] = (uint32_t)caps[j];
     if (j >= 1) {
@@ -711,7 +711,11 @@ int graham_tree(gscan_handle* h, const double* Rx, const double* Ry, const uint3
     for (int j = 0; j < 4; ++j) fprintf(stderr, " %u/%u", hi[44 + 2 * j], hi[45 + 2 * j]);
     fprintf(stderr, "\n");
   }
-  if (hi[0]) return GSCAN_OK;  // no shrink
+  if (hi[0]) {  // no shrink
+    if (h->sp_debug)
+      fprintf(stderr, "[tree] declined: sizes %u,%u,%u,%u,%u\n", N, hi[11], hi[12], hi[13], hi[14]);
+    return GSCAN_OK;
+  }
   h->graham_fails = hi[2];
   h->graham_path = 8 | (hi[2] ? 4 : 0);
   if (!hi[2] && (h->debug & GSCAN_DEBUG_FORCE_FALLBACK)) return graham_seq_fallback(h, Rx, Ry, Ri);

@@ -153,17 +153,16 @@ def test_full_sort_path_still_exact(engine, oracle_mod):
 
 @pytest.mark.parametrize("kind", ["square", "disk"])
 def test_graham_tree_strategy(engine, oracle_mod, kind):
-    """Round-2 output of squares is pop-heavy: the tree strategy runs and its
-    certificate holds (disks keep longer convex runs and may take another
-    strategy); a falsified candidate falls back exactly."""
+    """Round-2 output of squares and disks is pop-heavy: the tree strategy
+    runs and its certificate holds (a disk's levels stop shrinking at its
+    many hull vertices: the warp top scan takes the stalled level); a
+    falsified candidate falls back exactly."""
     from paper_1508_05931_b200 import _native as N
 
     xs, ys = _gen(kind, 1_000_000, 2)
     _run(engine, oracle_mod, xs, ys)
     path, fails = engine.graham_info()
-    assert fails == 0 and not (path & 4), (path, fails)
-    if kind == "square":
-        assert path == 8, path
+    assert fails == 0 and path == 8, (path, fails)
     _run(engine, oracle_mod, xs, ys, debug=N.DEBUG_CORRUPT_CANDIDATE)
     path, fails = engine.graham_info()
     assert (path & 4) and fails > 0, (path, fails)
