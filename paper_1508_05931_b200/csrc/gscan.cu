@@ -957,6 +957,10 @@ int sparse_enqueue(gscan_handle* h, const double* xs, const double* ys, uint32_t
 #undef A2
   }
   {
+    Launch L(h, "k_sp_check_r1");
+    k_sp_check_r1<<<1, 32, 0, s>>>(h->ctr, n, h->sp_st);
+  }
+  {
     Launch L(h, "k_sp_reduce_hist");
     k_sp_reduce_cols<false><<<(nb + 255) / 256, 256, 0, s>>>(h->sp_hist_part, G, nb, h->sp_hist);
   }

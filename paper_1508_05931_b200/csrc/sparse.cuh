@@ -1656,6 +1656,14 @@ __global__ void __launch_bounds__(kSpCandThreads, 1) k_sp_cand(
 
 // Walk-array bucket sizes: gathered buckets bring all their points, others
 // their candidates.
+// After F2: when >= 90% of the points survive round 1 (points in near-convex
+// position: circles, thin annuli) nearly all of them become walk candidates;
+// decline before F3.
+__global__ void k_sp_check_r1(const Counters* __restrict__ ctr, uint32_t n,
+                              SpState* __restrict__ st) {
+  if (threadIdx.x == 0 && (uint64_t)ctr->n1 * 10 > (uint64_t)n * 9) atomicOr(&st->fail, kSpFailMany);
+}
+
 // After F4: with more than m / kSpManyDiv candidates (points near a circle)
 // the candidate sort and walk cost more than the full sort; decline, so the
 // remaining sparse kernels exit at once.
