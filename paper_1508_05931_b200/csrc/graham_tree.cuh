@@ -50,6 +50,7 @@ constexpr int kTreePC = 8;          // stack rows carried in a boundary record
 constexpr int kTreeRows = kTreePC + kTreeChunk;
 constexpr uint32_t kTreeHiCap = 1u << 18;  // level >= 1 capacity (larger: another strategy)
 constexpr uint8_t kTreeRec = 0xff;  // chunk index of a row loaded from a record
+constexpr int kTreeInfoWords = 48;  // info[] words (cleared by k_gr_setup, read back by the host)
 
 // shared memory: per thread kTreeRows rows of (x, y, position, chunk index)
 constexpr size_t tree_smem(int threads) { return (size_t)kTreeRows * threads * (8 + 8 + 4 + 1); }
@@ -319,9 +320,13 @@ __device__ __forceinline__ void tree_put_chain(const TreeRows<T>& r, int top, ui
 
 // ---------------------------------------------------------------------------
 // info[] layout (device, read back once by the host):
-//   [0] no shrink (another strategy)  [1] final stack length  [2] certificate
-//   failures  [3] K  [8..9, 16] diagnostics clocks  [10 + j] size of Q_j
-//   [20..43] diagnostics
+//   [0] declined (another strategy, or the sparse path failed)  [1] final
+//   stack length  [2] certificate failures  [3] K  [4] N (buffer size, set
+//   by k_gr_setup from the host or from the sparse path's device state)
+//   [8..9, 16] diagnostics clocks  [10 + j] size of Q_j  [20..43] diagnostics
+// Every kernel reads N from info[4], so the whole strategy can be enqueued
+// before N is known on the host (inside the sparse path's CUDA graph); the
+// many-CTA kernels loop grid-stride over chunks.
 constexpr int kTreeCta = 64;
 constexpr size_t kTreeCtaSmem = tree_smem(kTreeCta);
 
@@ -339,42 +344,56 @@ __device__ __forceinline__ TreeLevel tree_level(const TreeWork& w, int j, uint32
   return L;
 }
 
-__device__ __forceinline__ uint32_t tree_nq(uint32_t N, const uint32_t* info, int j) {
-  return j == 0 ? N : info[10 + j];
+__device__ __forceinline__ uint32_t tree_nq(const uint32_t* info, int j) {
+  return j == 0 ? info[4] : info[10 + j];
+}
+
+// Setup: info[] cleared, N = *n_dev (sparse path: its round-2 size) or
+// n_host; declined when `st_fail` (the sparse path failed) is set, when
+// disabled, or when N exceeds the workspace.
+__global__ void k_gr_setup(const uint32_t* __restrict__ n_dev, uint32_t n_host,
+                           const uint32_t* __restrict__ st_fail, uint32_t n_max, uint32_t disable,
+                           uint32_t* __restrict__ info) {
+  const uint32_t t = threadIdx.x;
+  if (t < kTreeInfoWords && t != 4 && t != 0) info[t] = 0;
+  if (t == 0) {
+    const uint32_t N = n_dev ? *n_dev : n_host;
+    info[4] = N;
+    info[0] = (disable || (st_fail && *st_fail) || N == 0 || N > n_max) ? 1u : 0u;
+  }
 }
 
 // Up, many CTAs (levels 0 and 1): chains of level j's chunks (thread per
 // chunk) into the chunk-strided temp, lengths into off[j].
-__global__ void __launch_bounds__(kTreeCta) k_gr_up(uint32_t N, int j,
-                                                   const double* __restrict__ R_x,
+__global__ void __launch_bounds__(kTreeCta) k_gr_up(int j, const double* __restrict__ R_x,
                                                    const double* __restrict__ R_y, TreeWork w,
                                                    const uint32_t* __restrict__ info) {
   extern __shared__ __align__(16) double tsm[];
   const TreeRows<kTreeCta> r(tsm);
-  if (j > 0 && info[0]) return;
-  const uint32_t nq = tree_nq(N, info, j);
-  const uint32_t c = blockIdx.x * kTreeCta + threadIdx.x;
-  const uint32_t lo = c * kTreeChunk;
-  if (lo >= nq) return;
-  const int cnt = (int)min((uint32_t)kTreeChunk, nq - lo);
-  if (j == 0) tree_stage<kTreeCta>(r, nullptr, R_x, R_y, lo, cnt);
-  else tree_stage<kTreeCta>(r, w.Qp[j], w.Qx[j], w.Qy[j], lo, cnt);
-  uint32_t B = kNone;
-  int lo_own = kTreeRows;
-  const int top =
-      tree_scan_rows<kTreeCta>(r, 0, B, cnt, w.parent, R_x, R_y, lo_own, TreeNoPush{});
-  tree_put_chain<kTreeCta>(r, top, lo, j == 0, w);
-  w.off[j][c] = (uint32_t)top;
+  if (info[0]) return;
+  const uint32_t nq = tree_nq(info, j);
+  for (uint32_t c = blockIdx.x * kTreeCta + threadIdx.x; c * kTreeChunk < nq;
+       c += gridDim.x * kTreeCta) {
+    const uint32_t lo = c * kTreeChunk;
+    const int cnt = (int)min((uint32_t)kTreeChunk, nq - lo);
+    if (j == 0) tree_stage<kTreeCta>(r, nullptr, R_x, R_y, lo, cnt);
+    else tree_stage<kTreeCta>(r, w.Qp[j], w.Qx[j], w.Qy[j], lo, cnt);
+    uint32_t B = kNone;
+    int lo_own = kTreeRows;
+    const int top =
+        tree_scan_rows<kTreeCta>(r, 0, B, cnt, w.parent, R_x, R_y, lo_own, TreeNoPush{});
+    tree_put_chain<kTreeCta>(r, top, lo, j == 0, w);
+    w.off[j][c] = (uint32_t)top;
+  }
 }
 
 // Exclusive scan of level j's chain lengths (one CTA), Q_{j+1}'s size, and
 // the shrink check (info[0]: the tree strategy declines).
-__global__ void __launch_bounds__(1024) k_gr_scan(uint32_t N, int j, TreeWork w,
-                                                  uint32_t* __restrict__ info) {
+__global__ void __launch_bounds__(1024) k_gr_scan(int j, TreeWork w, uint32_t* __restrict__ info) {
   __shared__ uint32_t s_w[32];
   __shared__ uint32_t s_carry;
   if (info[0]) return;
-  const uint32_t nq = tree_nq(N, info, j);
+  const uint32_t nq = tree_nq(info, j);
   const uint32_t nch = (nq + kTreeChunk - 1) / kTreeChunk;
   const uint32_t total = tree_scan(w.off[j], nch, s_w, &s_carry);
   if (threadIdx.x == 0) {
@@ -405,12 +424,12 @@ __device__ __forceinline__ void tree_gather_chunk(const TreeWork& w, int j, uint
   }
 }
 
-__global__ void __launch_bounds__(256) k_gr_gather(uint32_t N, int j, TreeWork w,
+__global__ void __launch_bounds__(256) k_gr_gather(int j, TreeWork w,
                                                   const uint32_t* __restrict__ info) {
   if (info[0]) return;
-  const uint32_t nch = (tree_nq(N, info, j) + kTreeChunk - 1) / kTreeChunk;
-  const uint32_t c = blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (c < nch) tree_gather_chunk(w, j, c);
+  const uint32_t nch = (tree_nq(info, j) + kTreeChunk - 1) / kTreeChunk;
+  for (uint32_t c = blockIdx.x * 8 + (threadIdx.x >> 5); c < nch; c += gridDim.x * 8)
+    tree_gather_chunk(w, j, c);
 }
 
 // One down step for lower chunk cq: the state before it is the state before
@@ -437,7 +456,7 @@ __device__ __forceinline__ void tree_down_one(const TreeRows<T>& r, const TreeLe
 // Middle, ONE CTA: levels >= 2 up (Q_1 and Q_2 come from the many-CTA
 // kernels), the top-level scan, and the down-sweep to level 2.
 __global__ void __launch_bounds__(kTreeThreads, 1) k_gr_mid(
-    const double* __restrict__ R_x, const double* __restrict__ R_y, uint32_t N, TreeWork w,
+    const double* __restrict__ R_x, const double* __restrict__ R_y, TreeWork w,
     uint32_t* __restrict__ info) {
   extern __shared__ __align__(16) double tsm[];
   const TreeRows<kTreeThreads> r(tsm);
@@ -447,9 +466,9 @@ __global__ void __launch_bounds__(kTreeThreads, 1) k_gr_mid(
   __shared__ int s_K, s_bad;
   const int t = threadIdx.x;
   long long t_start = clock64();
-  if (info[0]) return;  // level 0 or 1 did not shrink
+  if (info[0]) return;  // declined, or level 0 or 1 did not shrink
   if (t == 0) {
-    s_nq[0] = N;
+    s_nq[0] = info[4];
     s_nq[1] = info[11];
     s_nq[2] = info[12];
     // top level: small enough, or the first level that stops shrinking
@@ -644,56 +663,57 @@ __global__ void __launch_bounds__(kTreeThreads, 1) k_gr_mid(
 
 // Down j -> j-1 (j = 2, 1), many CTAs: the state before every level j-1
 // chunk. Runs when the top level is above j - 1.
-__global__ void __launch_bounds__(kTreeCta) k_gr_down(uint32_t N, int j,
-                                                     const double* __restrict__ R_x,
+__global__ void __launch_bounds__(kTreeCta) k_gr_down(int j, const double* __restrict__ R_x,
                                                      const double* __restrict__ R_y, TreeWork w,
                                                      const uint32_t* __restrict__ info) {
   extern __shared__ __align__(16) double tsm[];
   const TreeRows<kTreeCta> r(tsm);
   if (info[0] || (int)info[3] <= j) return;
-  const TreeLevel hl = tree_level(w, j, tree_nq(N, info, j));
-  const TreeLevel ll = tree_level(w, j - 1, tree_nq(N, info, j - 1));
-  const uint32_t cq = blockIdx.x * kTreeCta + threadIdx.x;
-  if (cq >= ll.nch) return;
-  tree_down_one<kTreeCta>(r, hl, ll, cq, R_x, R_y, w.parent);
+  const TreeLevel hl = tree_level(w, j, tree_nq(info, j));
+  const TreeLevel ll = tree_level(w, j - 1, tree_nq(info, j - 1));
+  for (uint32_t cq = blockIdx.x * kTreeCta + threadIdx.x; cq < ll.nch; cq += gridDim.x * kTreeCta)
+    tree_down_one<kTreeCta>(r, hl, ll, cq, R_x, R_y, w.parent);
 }
 
 // Certificate, many CTAs (thread per buffer chunk); failures counted in info[2].
-__global__ void __launch_bounds__(kTreeCta) k_gr_cert(uint32_t N, const double* __restrict__ R_x,
+__global__ void __launch_bounds__(kTreeCta) k_gr_cert(const double* __restrict__ R_x,
                                                      const double* __restrict__ R_y, TreeWork w,
                                                      uint32_t* __restrict__ info,
                                                      uint32_t debug_corrupt) {
   extern __shared__ __align__(16) double tsm[];
   const TreeRows<kTreeCta> r(tsm);
   if (info[0]) return;
+  const uint32_t N = info[4];
   const uint32_t nch0 = (N + kTreeChunk - 1) / kTreeChunk;
-  const uint32_t c = blockIdx.x * kTreeCta + threadIdx.x;
-  if (c >= nch0) return;
   const uint32_t* bt = w.bt[0];
-  const uint32_t lo = c * kTreeChunk;
-  const int cnt = (int)min((uint32_t)kTreeChunk, N - lo);
-  tree_stage<kTreeCta>(r, nullptr, R_x, R_y, lo, cnt);
-  uint32_t B;
-  const int n0 = tree_load_rec<kTreeCta>(r, w.rec[0], c, B);
-  int lo_own = kTreeRows;
-  const int top =
-      tree_scan_rows<kTreeCta>(r, n0, B, cnt, w.parent, R_x, R_y, lo_own, TreeNoPush{});
-  const uint32_t end_top = top ? r.P[r.at(top - 1)] : B;
-  uint32_t want = bt[c + 1];
-  if (debug_corrupt && c + 1 == nch0) want = bt[c];  // falsified final state
-  bool ok = want == end_top;
-  // surviving pushes must link as in parent[] (loads issued 8 at a time)
-  for (int k0 = lo_own; k0 < top && ok; k0 += 8) {
-    uint32_t lk[8];
+  uint32_t fails = 0;
+  for (uint32_t c = blockIdx.x * kTreeCta + threadIdx.x; c < nch0; c += gridDim.x * kTreeCta) {
+    const uint32_t lo = c * kTreeChunk;
+    const int cnt = (int)min((uint32_t)kTreeChunk, N - lo);
+    tree_stage<kTreeCta>(r, nullptr, R_x, R_y, lo, cnt);
+    uint32_t B;
+    const int n0 = tree_load_rec<kTreeCta>(r, w.rec[0], c, B);
+    int lo_own = kTreeRows;
+    const int top =
+        tree_scan_rows<kTreeCta>(r, n0, B, cnt, w.parent, R_x, R_y, lo_own, TreeNoPush{});
+    const uint32_t end_top = top ? r.P[r.at(top - 1)] : B;
+    uint32_t want = bt[c + 1];
+    if (debug_corrupt && c + 1 == nch0) want = bt[c];  // falsified final state
+    bool ok = want == end_top;
+    // surviving pushes must link as in parent[] (loads issued 8 at a time)
+    for (int k0 = lo_own; k0 < top && ok; k0 += 8) {
+      uint32_t lk[8];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) lk[u] = (k0 + u < top) ? w.parent[r.P[r.at(k0 + u)]] : 0u;
+      for (int u = 0; u < 8; ++u) lk[u] = (k0 + u < top) ? w.parent[r.P[r.at(k0 + u)]] : 0u;
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int k = k0 + u;
-      if (k < top) ok = ok && lk[u] == (k ? r.P[r.at(k - 1)] : B);
+      for (int u = 0; u < 8; ++u) {
+        const int k = k0 + u;
+        if (k < top) ok = ok && lk[u] == (k ? r.P[r.at(k - 1)] : B);
+      }
     }
+    fails += ok ? 0u : 1u;
   }
-  if (!ok) atomicAdd(&info[2], 1u);
+  if (fails) atomicAdd(&info[2], fails);
 }
 
 // Output (one CTA): the top-level scan's final stack is the certified final
@@ -701,13 +721,14 @@ __global__ void __launch_bounds__(kTreeCta) k_gr_cert(uint32_t N, const double* 
 // below it (checked in parallel); otherwise the certified state is walked
 // down its links. Certificate failures: the exact sequential scan (one
 // thread), the reference loop itself.
-__global__ void __launch_bounds__(1024) k_gr_emit(uint32_t N, const double* __restrict__ R_x,
+__global__ void __launch_bounds__(1024) k_gr_emit(const double* __restrict__ R_x,
                                                   const double* __restrict__ R_y,
                                                   const uint32_t* __restrict__ R_i, TreeWork w,
                                                   const uint32_t* __restrict__ info,
                                                   uint32_t* __restrict__ out_idx,
                                                   Counters* __restrict__ ctr) {
   if (info[0]) return;
+  const uint32_t N = info[4];
   const uint32_t t = threadIdx.x;
   if (info[2]) {
     if (t != 0) return;

@@ -47,9 +47,9 @@ struct SpGraphKey {
   bool dup = true;
   // buffers the full-sort path may swap (stage_annotate_sort): the graph bakes
   // their addresses in, so they are part of the key
-  const void* bufs[6] = {};
+  const void* bufs[7] = {};  // + the tree workspace
   bool operator==(const SpGraphKey& o) const {
-    for (int k = 0; k < 6; ++k)
+    for (int k = 0; k < 7; ++k)
       if (bufs[k] != o.bufs[k]) return false;
     return xs == o.xs && ys == o.ys && n == o.n && chunks == o.chunks && debug == o.debug &&
            dup == o.dup;
@@ -146,8 +146,10 @@ struct gscan_handle {
   uint64_t* sp_dup = nullptr;  // per-CTA hash lists (n)
   uint32_t sp_used = 0, sp_fail = 0, sp_walked = 0, sp_calls = 0, sp_fallbacks = 0;
   // Graham tree strategy pool (graham_tree.cuh)
-  uint32_t* gt_pool = nullptr;
-  uint64_t gt_cap = 0;
+  uint32_t* tw_pool = nullptr;  // tree strategy workspace (graham_tree.cuh)
+  uint32_t tw_nmax = 0, tw_nch1 = 0;
+  TreeWork tw{};
+  uint32_t* h_info = nullptr;   // pinned mirror of the tree strategy's info words
 };
 
 namespace {
@@ -187,8 +189,8 @@ void free_buffers(gscan_handle* h) {
   dfree(h->g_keep); dfree(h->g_misc);
   dfree(h->g_stA); dfree(h->g_stB); dfree(h->g_lenA); dfree(h->g_lenB); dfree(h->g_scr);
   dfree(h->sp_eb); dfree(h->sp_Wb); dfree(h->sp_Ws); dfree(h->sp_Rb); dfree(h->sp_Rs); dfree(h->sp_dup);
-  dfree(h->sp_codes); dfree(h->sp_phi32); dfree(h->sp_dup2); dfree(h->gt_pool);
-  h->gt_cap = 0;
+  dfree(h->sp_codes); dfree(h->sp_phi32); dfree(h->sp_dup2); dfree(h->tw_pool);
+  h->tw_nmax = 0;
   h->g_st_cap = 0;
   h->g_len_cap = 0;
   h->cap = 0;
@@ -619,14 +621,18 @@ int graham_prefix(gscan_handle* h, const double* Rx, const double* Ry, const uin
   return GSCAN_OK;
 }
 
-// Tree strategy (graham_tree.cuh) for pop-heavy buffers: one kernel. *done =
-// false when the local chains do not shrink (convex position): the caller then
-// takes the junction / prefix / sequential strategies.
+// Tree strategy (graham_tree.cuh) for pop-heavy buffers. Split in three so the
+// sparse path can enqueue it inside its CUDA graph before the buffer size is
+// known on the host: tree_workspace (allocation for up to n_max points),
+// tree_enqueue (every kernel reads N from the device), tree_finish (after the
+// stream synchronised: *done = false when the tree declined -- convex
+// position, or N beyond the workspace -- and the caller then takes the
+// junction / prefix / sequential strategies).
 constexpr uint32_t kTreeMaxN = 1u << 22;  // larger buffers: the middle level would be too long
 
-int graham_tree(gscan_handle* h, const double* Rx, const double* Ry, const uint32_t* Ri,
-                uint32_t N, bool* done) {
-  *done = false;
+int tree_workspace(gscan_handle* h, uint32_t n_max) {
+  if (h->tw_pool && h->tw_nmax >= n_max) return GSCAN_OK;
+  const uint32_t N = std::max<uint32_t>(n_max, 1024);
   // level capacities: level 1 <= 0.85 N, then <= 0.9x per level, levels >= 1
   // at most kTreeHiCap (else the kernel declines)
   uint64_t caps[kTreeMaxLevels + 1];
@@ -640,16 +646,14 @@ int graham_tree(gscan_handle* h, const double* Rx, const double* Ry, const uint3
     if (j >= 1) need += 6 * caps[j] + 4 * 32;                // Qp, Qx, Qy, up
     need += nchunks(j) * (2 + 2 + 8 + 16 + 16) + 7 * 32;   // off, bt, rec
   }
-  if (need > h->gt_cap) {
-    dfree(h->gt_pool);
-    CU(cudaMalloc(&h->gt_pool, need * 4));
-    h->gt_cap = need;
-  }
-  uint32_t* pool = h->gt_pool;
+  dfree(h->tw_pool);
+  CU(cudaMalloc(&h->tw_pool, need * 4));
+  uint32_t* pool = h->tw_pool;
   uint64_t used = 0;
   auto take = [&](uint64_t cnt) { uint32_t* p = pool + used; used += (cnt + 31) & ~31ull; return p; };
   auto take_d = [&](uint64_t cnt) { return reinterpret_cast<double*>(take(2 * cnt)); };
-  TreeWork w{};
+  TreeWork& w = h->tw;
+  w = TreeWork{};
   w.parent = take(N);
   w.tmp = take(N);
   w.chainq = take(N);
@@ -675,56 +679,71 @@ int graham_tree(gscan_handle* h, const double* Rx, const double* Ry, const uint3
     w.rec[j].y = take_d(nc * kTreePC);
   }
   if (used > need) return fail(h, GSCAN_E_INTERNAL, "tree pool overflow");
+  h->tw_nmax = N;
+  h->tw_nch1 = (uint32_t)(caps[1] / kTreeChunk + 1);
+  return GSCAN_OK;
+}
+
+// Enqueue the whole tree strategy on s. N = *n_dev (the sparse path's round-2
+// size) or n_host; the kernels no-op when *st_fail is set or when disabled.
+// The info words are copied to the pinned h->h_info at the end.
+int tree_enqueue(gscan_handle* h, const double* Rx, const double* Ry, const uint32_t* Ri,
+                 const uint32_t* n_dev, uint32_t n_host, const uint32_t* st_fail, bool disable,
+                 cudaStream_t s) {
+  const TreeWork& w = h->tw;
   uint32_t* info = h->g_misc + 4;
-  const uint32_t nch0 = (N + kTreeChunk - 1) / kTreeChunk;
-  const uint32_t g0 = (nch0 + kTreeCta - 1) / kTreeCta;
-  const uint32_t nch1 = (uint32_t)(caps[1] / kTreeChunk + 1);  // upper bound
-  const uint32_t g1 = (nch1 + kTreeCta - 1) / kTreeCta;
+  const uint32_t nch0 = (h->tw_nmax + kTreeChunk - 1) / kTreeChunk;  // upper bounds
+  const uint32_t gmax = 4 * (uint32_t)h->sm_count;
+  const uint32_t g0 = std::min((nch0 + kTreeCta - 1) / kTreeCta, gmax);
+  const uint32_t g1 = std::min((h->tw_nch1 + kTreeCta - 1) / kTreeCta, gmax);
   const uint32_t dbg = (h->debug & GSCAN_DEBUG_CORRUPT_CANDIDATE) ? 1u : 0u;
-  cudaStream_t s = h->stream;
-  CU(cudaMemsetAsync(info, 0, 16 * sizeof(uint32_t), s));
+  { Launch Lk(h, "k_gr_setup", s); k_gr_setup<<<1, 64, 0, s>>>(n_dev, n_host, st_fail, h->tw_nmax, disable ? 1u : 0u, info); }
   for (int j = 0; j < 2; ++j) {  // levels 0 and 1 on many CTAs
-    const uint32_t g = j ? g1 : g0, nch = j ? nch1 : nch0;
-    { Launch Lk(h, "k_gr_up", s); k_gr_up<<<g, kTreeCta, kTreeCtaSmem, s>>>(N, j, Rx, Ry, w, info); }
-    { Launch Lk(h, "k_gr_scan", s); k_gr_scan<<<1, 1024, 0, s>>>(N, j, w, info); }
-    { Launch Lk(h, "k_gr_gather", s); k_gr_gather<<<(nch + 7) / 8, 256, 0, s>>>(N, j, w, info); }
+    const uint32_t g = j ? g1 : g0, nch = j ? h->tw_nch1 : nch0;
+    { Launch Lk(h, "k_gr_up", s); k_gr_up<<<g, kTreeCta, kTreeCtaSmem, s>>>(j, Rx, Ry, w, info); }
+    { Launch Lk(h, "k_gr_scan", s); k_gr_scan<<<1, 1024, 0, s>>>(j, w, info); }
+    { Launch Lk(h, "k_gr_gather", s); k_gr_gather<<<std::min((nch + 7) / 8, gmax), 256, 0, s>>>(j, w, info); }
   }
-  { Launch Lk(h, "k_gr_mid", s); k_gr_mid<<<1, kTreeThreads, kTreeSmem, s>>>(Rx, Ry, N, w, info); }
-  { Launch Lk(h, "k_gr_down", s); k_gr_down<<<g1, kTreeCta, kTreeCtaSmem, s>>>(N, 2, Rx, Ry, w, info); }
-  { Launch Lk(h, "k_gr_down", s); k_gr_down<<<g0, kTreeCta, kTreeCtaSmem, s>>>(N, 1, Rx, Ry, w, info); }
-  { Launch Lk(h, "k_gr_cert", s); k_gr_cert<<<g0, kTreeCta, kTreeCtaSmem, s>>>(N, Rx, Ry, w, info, dbg); }
-  { Launch Lk(h, "k_gr_emit", s); k_gr_emit<<<1, 1024, 0, s>>>(N, Rx, Ry, Ri, w, info, h->d_out, h->ctr); }
+  { Launch Lk(h, "k_gr_mid", s); k_gr_mid<<<1, kTreeThreads, kTreeSmem, s>>>(Rx, Ry, w, info); }
+  { Launch Lk(h, "k_gr_down", s); k_gr_down<<<g1, kTreeCta, kTreeCtaSmem, s>>>(2, Rx, Ry, w, info); }
+  { Launch Lk(h, "k_gr_down", s); k_gr_down<<<g0, kTreeCta, kTreeCtaSmem, s>>>(1, Rx, Ry, w, info); }
+  { Launch Lk(h, "k_gr_cert", s); k_gr_cert<<<g0, kTreeCta, kTreeCtaSmem, s>>>(Rx, Ry, w, info, dbg); }
+  { Launch Lk(h, "k_gr_emit", s); k_gr_emit<<<1, 1024, 0, s>>>(Rx, Ry, Ri, w, info, h->d_out, h->ctr); }
   CU(cudaGetLastError());
-  uint32_t hi[52];
-  CU(cudaMemcpyAsync(hi, info, h->sp_debug ? sizeof hi : 17 * sizeof(uint32_t),
-                     cudaMemcpyDeviceToHost, h->stream));
-  CU(cudaStreamSynchronize(h->stream));
+  CU(cudaMemcpyAsync(h->h_info, info, kTreeInfoWords * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+  return GSCAN_OK;
+}
+
+// After the stream synchronised (h->h_info current).
+int tree_finish(gscan_handle* h, const double* Rx, const double* Ry, const uint32_t* Ri,
+                bool* done) {
+  *done = false;
+  const uint32_t* hi = h->h_info;
   if (h->sp_debug) {
-    fprintf(stderr, "[tree] N=%u K=%u sizes=%u,%u,%u,%u,%u,%u.. cycles: up=%u top=%u down=%u fails=%u\n",
-            N, hi[3], hi[10], hi[11], hi[12], hi[13], hi[14], hi[15], hi[8], hi[9] - hi[8],
-            hi[16] - hi[9], hi[2]);
+    fprintf(stderr, "[tree] N=%u K=%u declined=%u sizes=%u,%u,%u,%u,%u,%u.. cycles: up=%u top=%u down=%u fails=%u\n",
+            hi[4], hi[3], hi[0], hi[4], hi[11], hi[12], hi[13], hi[14], hi[15], hi[8],
+            hi[9] - hi[8], hi[16] - hi[9], hi[2]);
     fprintf(stderr, "[tree] level ends (cycles): up");
-    for (uint32_t j = 0; j < hi[3] && j < 12; ++j) fprintf(stderr, " %u", hi[20 + j]);
+    for (uint32_t j = 2; j < hi[3] && j < 12; ++j) fprintf(stderr, " %u", hi[20 + j]);
     fprintf(stderr, " | down");
-    for (uint32_t j = hi[3] - 1; j >= 2 && j < 12; --j) fprintf(stderr, " %u", hi[32 + j]);
-    fprintf(stderr, " | scan start/end");
-    for (int j = 0; j < 4; ++j) fprintf(stderr, " %u/%u", hi[44 + 2 * j], hi[45 + 2 * j]);
+    for (uint32_t j = hi[3] - 1; j >= 3 && j < 12; --j) fprintf(stderr, " %u", hi[32 + j]);
     fprintf(stderr, "\n");
   }
-  if (hi[0]) {  // no shrink
-    if (h->sp_debug)
-      fprintf(stderr, "[tree] declined: sizes %u,%u,%u,%u,%u\n", N, hi[11], hi[12], hi[13], hi[14]);
-    return GSCAN_OK;
-  }
+  if (hi[0]) return GSCAN_OK;  // declined
   h->graham_fails = hi[2];
   h->graham_path = 8 | (hi[2] ? 4 : 0);
-  if (!hi[2] && (h->debug & GSCAN_DEBUG_FORCE_FALLBACK)) return graham_seq_fallback(h, Rx, Ry, Ri);
+  if (!hi[2] && (h->debug & GSCAN_DEBUG_FORCE_FALLBACK)) TRY(graham_seq_fallback(h, Rx, Ry, Ri));
   *done = true;
   return GSCAN_OK;
 }
 
+bool tree_forced_off(const gscan_handle* h) {
+  return h->debug & (GSCAN_DEBUG_FORCE_JUNCTION | GSCAN_DEBUG_FORCE_SEQUENTIAL |
+                     GSCAN_DEBUG_FORCE_PREFIX);
+}
+
 int stage_graham(gscan_handle* h, const double* Rx, const double* Ry, const uint32_t* Ri,
-                 uint32_t N) {
+                 uint32_t N, bool skip_tree = false) {
   uint32_t* fail_d = h->g_misc;
   uint32_t* len_d = h->g_misc + 1;
   CU(cudaMemsetAsync(h->g_misc, 0, 16, h->stream));
@@ -735,12 +754,13 @@ int stage_graham(gscan_handle* h, const double* Rx, const double* Ry, const uint
     h->graham_path = 0;
     return GSCAN_OK;
   }
-  const bool forced = h->debug & (GSCAN_DEBUG_FORCE_JUNCTION | GSCAN_DEBUG_FORCE_SEQUENTIAL |
-                                  GSCAN_DEBUG_FORCE_PREFIX);
-  if (!forced && N <= kTreeMaxN) {
+  if (!skip_tree && !tree_forced_off(h) && N <= kTreeMaxN) {
     bool done = false;
-    TRY(graham_tree(h, Rx, Ry, Ri, N, &done));
-    if (done || (h->graham_path & 8)) return GSCAN_OK;
+    TRY(tree_workspace(h, N));
+    TRY(tree_enqueue(h, Rx, Ry, Ri, nullptr, N, nullptr, false, h->stream));
+    CU(cudaStreamSynchronize(h->stream));
+    TRY(tree_finish(h, Rx, Ry, Ri, &done));
+    if (done) return GSCAN_OK;
   }
   const uint32_t nch = (N + kChunk - 1) / kChunk;
   {
@@ -1089,6 +1109,9 @@ int sparse_enqueue(gscan_handle* h, const double* xs, const double* ys, uint32_t
                                                     h->flags, h->sp_st, h->A_x, h->A_y, h->A_i,
                                                     h->sp_Rb, h->sp_Rs, h->status, h->ctr);
   }
+  // the duplicate check (side stream, sparse_dup_check) forks here, so it
+  // overlaps the certificate and the Graham tail
+  TRY(rec_event(h, h->ev_f3, s));
   {
     Launch L(h, "k_sp_rlo");
     k_sp_rlo<<<h->sm_count * 8, kBlock, 0, s>>>(h->sp_Rb, h->sp_st, h->sp_rlo);
@@ -1111,6 +1134,11 @@ int sparse_enqueue(gscan_handle* h, const double* xs, const double* ys, uint32_t
   TRY(rec_event(h, h->ev[4], s));
   CU(cudaMemcpyAsync(h->h_sp, h->sp_st, sizeof(SpState), cudaMemcpyDeviceToHost, s));
   CU(cudaMemcpyAsync(&h->ctr->n2, &h->sp_st->n_r, 4, cudaMemcpyDeviceToDevice, s));
+  // K7/K8 in the same graph: the tree strategy over the round-2 buffer, its
+  // size read on the device; it no-ops when the sparse path failed
+  TRY(tree_enqueue(h, h->A_x, h->A_y, h->A_i, &h->sp_st->n_r, 0, &h->sp_st->fail,
+                   tree_forced_off(h), s));
+  TRY(rec_event(h, h->ev[5], s));
   return GSCAN_OK;
 }
 
@@ -1136,8 +1164,7 @@ int sparse_dup_check(gscan_handle* h, uint32_t n) {
   const uint32_t nl = 2 * G;  // hash lists (k_sp_phi: two per CTA)
   static_assert(kSpPartChunk == 8 * 1024, "k_sp_dup_part: 8 entries per thread");
   const uint32_t cap = sparse_region_cap(h, n);
-  CU(cudaEventRecord(h->ev_f3, h->stream));
-  CU(cudaStreamWaitEvent(h->side, h->ev_f3, 0));
+  CU(cudaStreamWaitEvent(h->side, h->ev_f3, 0));  // recorded after k_sp_compact
   {
     const uint64_t tiles = ((uint64_t)kSpParts * nl + 1 + kScanTile - 1) / kScanTile;
     CU(cudaMemsetAsync(h->sp_side_status, 0, tiles * 8, h->side));
@@ -1181,8 +1208,9 @@ int run_sparse(gscan_handle* h, const double* xs, const double* ys, uint32_t n,
   const bool dup_check = !h->sp_no_dup;
   // one captured graph per (input, n, config): replayed while unchanged
   SpGraphKey key{xs, ys, n, c, h->debug, dup_check};
-  const void* bufs[6] = {h->A_x, h->A_y, h->A_i, h->C_x, h->C_y, h->C_i};
-  for (int k = 0; k < 6; ++k) key.bufs[k] = bufs[k];
+  TRY(tree_workspace(h, std::min<uint32_t>(n, kTreeMaxN)));  // no allocation inside the capture
+  const void* bufs[7] = {h->A_x, h->A_y, h->A_i, h->C_x, h->C_y, h->C_i, h->tw_pool};
+  for (int k = 0; k < 7; ++k) key.bufs[k] = bufs[k];
   if (h->profiling || !h->use_graphs) {
     TRY(sparse_enqueue(h, xs, ys, n, cfg));
   } else {
@@ -1244,8 +1272,16 @@ enqueued:
     ++h->sp_fallbacks;
     return GSCAN_OK;
   }
-  TRY(stage_graham(h, h->A_x, h->A_y, h->A_i, sp.n_r));
-  CU(cudaEventRecord(h->ev[5], s));
+  {
+    h->graham_path = 0;
+    h->graham_fails = 0;
+    bool done = false;
+    TRY(tree_finish(h, h->A_x, h->A_y, h->A_i, &done));
+    if (!done) {  // the tree declined: the other strategies, launched from here
+      TRY(stage_graham(h, h->A_x, h->A_y, h->A_i, sp.n_r, /*skip_tree=*/true));
+      CU(cudaEventRecord(h->ev[5], s));
+    }
+  }
   if (dup_check) {
     // the duplicate check must have passed for the result to count
     CU(cudaStreamWaitEvent(s, h->ev_dup, 0));
@@ -1395,6 +1431,7 @@ int gscan_create(int device, gscan_handle** out) {
     CU(cudaMemset(h->ctr, 0, sizeof(Counters)));
     CU(cudaMalloc(&h->scratch64, 16));
     CU(cudaMallocHost(&h->h_ctr, sizeof(Counters)));
+    CU(cudaMallocHost(&h->h_info, kTreeInfoWords * sizeof(uint32_t)));
     for (auto& e : h->ev) CU(cudaEventCreate(&e));
     CU(cudaFuncSetAttribute(k_graham_candidate_seq, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)kCandSmem));
@@ -1450,6 +1487,8 @@ int gscan_destroy(gscan_handle* h) {
   dfree(h->sp_seglo); dfree(h->sp_seghi); dfree(h->sp_st);
   if (h->h_sp) cudaFreeHost(h->h_sp);
   if (h->h_ctr) cudaFreeHost(h->h_ctr);
+  if (h->h_info) cudaFreeHost(h->h_info);
+  dfree(h->tw_pool);
   if (h->h_out) cudaFreeHost(h->h_out);
   for (auto& e : h->ev) if (e) cudaEventDestroy(e);
   for (auto& k : h->ktimes) { cudaEventDestroy(k.a); cudaEventDestroy(k.b); }
