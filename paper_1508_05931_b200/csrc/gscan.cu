@@ -926,185 +926,251 @@ int rec_event(gscan_handle* h, cudaEvent_t e, cudaStream_t s) {
   return GSCAN_OK;
 }
 
-// Enqueues the whole sparse path up to and including the verification and the
-// duplicate check's join, plus the SpState read-back: no host round trip
-// inside, fixed launch shapes for a given (input, n, config), so run_sparse
-// replays it as one captured CUDA graph.
-int sparse_enqueue(gscan_handle* h, const double* xs, const double* ys, uint32_t n,
-                   const gscan_config& cfg) {
-  const uint32_t nb = kSpBuckets;
-  const uint32_t G = (uint32_t)h->sp_grid;
-  const bool vec = aligned16(xs) && aligned16(ys);
-  const bool drop = (h->debug & GSCAN_DEBUG_SPARSE_DROP) != 0;
-  const uint64_t c = cfg.chunk_count;
-  const uint64_t nslices = 2 * std::min<uint64_t>(c, n);
-  // per-CTA emission region: bound on the points one streaming CTA visits
-  const uint32_t cap = sparse_region_cap(h, n);
-  const size_t smem_nb = (size_t)nb * 4;
-  cudaStream_t s = h->stream;
+// The sparse path as segments over one context. sparse_enqueue runs them all
+// in order (one device, one CUDA graph); the sharded path (gscan_dist_*) runs
+// them per rank with the collectives of SURVEY.md 8e in between.
+struct SpCtx {
+  const double* xs;
+  const double* ys;
+  uint32_t n;       // points of this device
+  uint32_t base;    // global index of point 0 (a shard's offset; 0 on one device)
+  uint64_t chunks;  // cfg.chunk_count
+  uint64_t nslices;
+  uint32_t G, cap, nb;
+  size_t smem_nb;
+  bool vec, drop;
+  const uint32_t* gs;  // storage base of gathered buckets (bstart on one device)
+  cudaStream_t s;
+};
+
+SpCtx sp_ctx(gscan_handle* h, const double* xs, const double* ys, uint32_t n, uint64_t chunks) {
+  SpCtx c{};
+  c.xs = xs;
+  c.ys = ys;
+  c.n = n;
+  c.base = 0;
+  c.chunks = chunks;
+  c.nslices = 2 * std::min<uint64_t>(chunks, n);
+  c.G = (uint32_t)h->sp_grid;
+  c.cap = sparse_region_cap(h, n);  // per-CTA emission region: bound on the points one CTA visits
+  c.nb = kSpBuckets;
+  c.smem_nb = (size_t)kSpBuckets * 4;
+  c.vec = aligned16(xs) && aligned16(ys);
+  c.drop = (h->debug & GSCAN_DEBUG_SPARSE_DROP) != 0;
+  c.gs = h->sp_bstart;
+  c.s = h->stream;
+  return c;
+}
+
+int sp_seg_init(gscan_handle* h, const SpCtx& c) {
+  cudaStream_t s = c.s;
   TRY(rec_event(h, h->ev[0], s));
   CU(cudaMemsetAsync(h->ctr, 0, sizeof(Counters), s));
   CU(cudaMemsetAsync(h->sp_st, 0, sizeof(SpState), s));
-  CU(cudaMemsetAsync(h->sp_gcnt, 0, nb * 4, s));
-  CU(cudaMemsetAsync(h->sp_ccnt, 0, nb * 4, s));
-  CU(cudaMemsetAsync(h->sp_prefmax, 0, nb * 4, s));
-  CU(cudaMemsetAsync(h->sp_slice, 0xff, nb * 4, s));
+  CU(cudaMemsetAsync(h->sp_gcnt, 0, c.nb * 4, s));
+  CU(cudaMemsetAsync(h->sp_ccnt, 0, c.nb * 4, s));
+  CU(cudaMemsetAsync(h->sp_prefmax, 0, c.nb * 4, s));
+  CU(cudaMemsetAsync(h->sp_slice, 0xff, c.nb * 4, s));
   CU(cudaMemsetAsync(h->sp_cells, 0, kSpCells * 4, s));
+  return GSCAN_OK;
+}
+
+int sp_seg_extremes(gscan_handle* h, const SpCtx& c) {
+  const uint32_t grid =
+      std::max(1u, std::min<uint32_t>((c.n + kBlock * 8 - 1) / (kBlock * 8), h->sm_count * 8));
+  Launch L(h, "k_extremes", c.s);
+  if (c.vec) k_extremes<true><<<grid, kBlock, 0, c.s>>>(c.xs, c.ys, c.n, h->partials, h->ext, h->ctr);
+  else k_extremes<false><<<grid, kBlock, 0, c.s>>>(c.xs, c.ys, c.n, h->partials, h->ext, h->ctr);
+  return GSCAN_OK;
+}
+
+int sp_seg_sample(gscan_handle* h, const SpCtx& c) {
+  Launch L(h, "k_sp_sample", c.s);
+  k_sp_sample<<<kSpSample / 1024, 1024, 0, c.s>>>(c.xs, c.ys, c.n, h->ext, h->sp_cells);
+  return GSCAN_OK;
+}
+
+// bucket map from the sample cells, then F2 and P_l from the per-CTA partials
+int sp_seg_f2(gscan_handle* h, const SpCtx& c) {
+  cudaStream_t s = c.s;
   {
-    const uint32_t grid =
-        std::max(1u, std::min<uint32_t>((n + kBlock * 8 - 1) / (kBlock * 8), h->sm_count * 8));
-    Launch L(h, "k_extremes");
-    if (vec) k_extremes<true><<<grid, kBlock, 0, s>>>(xs, ys, n, h->partials, h->ext, h->ctr);
-    else k_extremes<false><<<grid, kBlock, 0, s>>>(xs, ys, n, h->partials, h->ext, h->ctr);
-  }
-  {
-    Launch L(h, "k_sp_sample");
-    k_sp_sample<<<kSpSample / 1024, 1024, 0, s>>>(xs, ys, n, h->ext, h->sp_cells);
-  }
-  {
-    Launch L(h, "k_sp_cdf");
+    Launch L(h, "k_sp_cdf", s);
     k_sp_cdf<<<1, kSpCells / 2, 0, s>>>(h->sp_cells, h->sp_cdf);
   }
   {
-    Launch L(h, "k_sp_theta");
-    k_sp_theta<<<(nb + 1 + 255) / 256, 256, 0, s>>>(h->sp_cdf, h->sp_th, h->sp_st);
+    Launch L(h, "k_sp_theta", s);
+    k_sp_theta<<<(c.nb + 1 + 255) / 256, 256, 0, s>>>(h->sp_cdf, h->sp_th, h->sp_st);
   }
   {
-    Launch L(h, "k_sp_hist");
-#define A2 xs, ys, n, h->ext, h->sp_cdf, h->sp_th, h->sp_codes, h->sp_hist_part, h->sp_d2, h->ctr
-    if (vec) k_sp_hist<true><<<G, kSpThreads, smem_nb, s>>>(A2);
-    else k_sp_hist<false><<<G, kSpThreads, smem_nb, s>>>(A2);
+    Launch L(h, "k_sp_hist", s);
+#define A2 c.xs, c.ys, c.n, h->ext, h->sp_cdf, h->sp_th, h->sp_codes, h->sp_hist_part, h->sp_d2, h->ctr
+    if (c.vec) k_sp_hist<true><<<c.G, kSpThreads, c.smem_nb, s>>>(A2);
+    else k_sp_hist<false><<<c.G, kSpThreads, c.smem_nb, s>>>(A2);
 #undef A2
   }
   {
-    Launch L(h, "k_sp_check_r1");
-    k_sp_check_r1<<<1, 32, 0, s>>>(h->ctr, n, h->sp_st);
+    Launch L(h, "k_sp_check_r1", s);
+    k_sp_check_r1<<<1, 32, 0, s>>>(h->ctr, c.n, h->sp_st);
   }
   {
-    Launch L(h, "k_sp_reduce_hist");
-    k_sp_reduce_cols<false><<<(nb + 255) / 256, 256, 0, s>>>(h->sp_hist_part, G, nb, h->sp_hist);
+    Launch L(h, "k_sp_reduce_hist", s);
+    k_sp_reduce_cols<false><<<(c.nb + 255) / 256, 256, 0, s>>>(h->sp_hist_part, c.G, c.nb, h->sp_hist);
   }
   {
-    Launch L(h, "k_sp_plan_pl");
-    k_sp_plan_pl<<<1, 256, 0, s>>>(xs, ys, h->sp_d2, G, h->sp_st);
+    Launch L(h, "k_sp_plan_pl", s);
+    k_sp_plan_pl<<<1, 256, 0, s>>>(c.xs, c.ys, h->sp_d2, c.G, h->sp_st);
   }
-  TRY(scan_u32(h, h->sp_hist, nb, h->sp_bstart));
+  return GSCAN_OK;
+}
+
+// bucket starts (exact ranks), P_l's bucket and its rank inside it
+int sp_seg_plan(gscan_handle* h, const SpCtx& c) {
+  cudaStream_t s = c.s;
+  TRY(scan_u32(h, h->sp_hist, c.nb, h->sp_bstart));
   {
-    Launch L(h, "k_sp_plan_bl");
+    Launch L(h, "k_sp_plan_bl", s);
     k_sp_plan_bl<<<1, 32, 0, s>>>(h->ext, h->sp_cdf, h->sp_th, h->sp_bstart, h->sp_st);
   }
   {
-    Launch L(h, "k_sp_lrank");
-    k_sp_lrank<<<h->sm_count * 8, 256, 0, s>>>(xs, ys, h->sp_codes, n, h->ext, h->sp_st);
+    Launch L(h, "k_sp_lrank", s);
+    k_sp_lrank<<<h->sm_count * 8, 256, 0, s>>>(c.xs, c.ys, h->sp_codes, c.n, c.base, h->ext,
+                                               h->sp_st);
+  }
+  return GSCAN_OK;
+}
+
+// slice geometry, gathered buckets, then F3 (G in (surv, sp_eb), hash lists in sp_dup)
+int sp_seg_f3(gscan_handle* h, const SpCtx& c) {
+  cudaStream_t s = c.s;
+  {
+    Launch L(h, "k_sp_steps", s);
+    k_sp_steps<<<1, 32, 0, s>>>(h->sp_bstart, c.chunks, h->sp_st);
   }
   {
-    Launch L(h, "k_sp_steps");
-    k_sp_steps<<<1, 32, 0, s>>>(h->sp_bstart, c, h->sp_st);
-  }
-  {
-    Launch L(h, "k_sp_gbits");
-    k_sp_gbits<<<(nb / 32 + 255) / 256, 256, 0, s>>>(h->sp_bstart, h->sp_st, h->sp_gbits,
-                                                     h->sp_glist);
+    Launch L(h, "k_sp_gbits", s);
+    k_sp_gbits<<<(c.nb / 32 + 255) / 256, 256, 0, s>>>(h->sp_bstart, h->sp_st, h->sp_gbits,
+                                                       h->sp_glist);
   }
   TRY(rec_event(h, h->ev[1], s));
-  // F3 -> G in (surv, sp_eb), hash lists in sp_dup
   {
-    Launch L(h, "k_sp_phi");
-#define A3 xs, ys, h->sp_codes, n, cap, h->ext, h->sp_gbits, h->sp_st, h->sp_phi_part, h->surv, \
+    Launch L(h, "k_sp_phi", s);
+#define A3 c.xs, c.ys, h->sp_codes, c.n, c.cap, h->ext, h->sp_gbits, h->sp_st, h->sp_phi_part, h->surv, \
            h->sp_eb, h->sp_gcount, h->sp_dup, h->sp_hcount, h->sp_part_off, h->sp_phi32
-    if (vec) k_sp_phi<true><<<G, kSpThreads, smem_nb, s>>>(A3);
-    else k_sp_phi<false><<<G, kSpThreads, smem_nb, s>>>(A3);
+    if (c.vec) k_sp_phi<true><<<c.G, kSpThreads, c.smem_nb, s>>>(A3);
+    else k_sp_phi<false><<<c.G, kSpThreads, c.smem_nb, s>>>(A3);
 #undef A3
   }
   {
-    Launch L(h, "k_sp_reduce_phi");
-    k_sp_reduce_cols<true><<<(nb + 255) / 256, 256, 0, s>>>(h->sp_phi_part, G, nb, h->sp_phimax);
+    Launch L(h, "k_sp_reduce_phi", s);
+    k_sp_reduce_cols<true><<<(c.nb + 255) / 256, 256, 0, s>>>(h->sp_phi_part, c.G, c.nb, h->sp_phimax);
+  }
+  return GSCAN_OK;
+}
+
+// gathered points (regions (surv, sp_eb, sp_gcount) indexing gx/gy) sorted
+// exactly; slice heads and the per-bucket prefix maxima
+int sp_seg_sortg(gscan_handle* h, const SpCtx& c, const double* gx, const double* gy) {
+  cudaStream_t s = c.s;
+  {
+    Launch L(h, "k_sp_place_g", s);
+    k_sp_emit_place<0><<<dim3(16, c.G), 256, 0, s>>>(gx, gy, h->surv, h->sp_eb, nullptr,
+                                                     h->sp_gcount, c.cap, h->sp_gcnt, c.gs,
+                                                     h->ext, h->sp_st, h->rec);
   }
   {
-    Launch L(h, "k_sp_place_g");
-    k_sp_emit_place<0><<<dim3(16, G), 256, 0, s>>>(xs, ys, h->surv, h->sp_eb, nullptr,
-                                                   h->sp_gcount, cap, h->sp_gcnt, h->sp_bstart,
-                                                   h->ext, h->sp_st, h->rec);
-  }
-  {
-    Launch L(h, "k_sp_sort_gathered");
+    Launch L(h, "k_sp_sort_gathered", s);
     k_sp_sort_gathered<<<h->sm_count * 4, kSpSmallThreads, kSpSmallSmem, s>>>(
-        h->sp_glist, h->sp_bstart, h->sp_hist, h->sp_gcnt, h->rec, h->ext, h->sp_st, h->sp_bigg,
-        h->A_x, h->A_y, h->A_i);
+        h->sp_glist, h->sp_bstart, c.gs, h->sp_hist, h->sp_gcnt, h->rec, h->ext, h->sp_st,
+        h->sp_bigg, h->A_x, h->A_y, h->A_i);
   }
   {
-    Launch L(h, "k_sp_sort_gathered_big");
+    Launch L(h, "k_sp_sort_gathered_big", s);
     k_sp_sort_gathered_big<<<h->sm_count, kSpSortThreads, kSpBigSmem, s>>>(
-        h->sp_bigg, h->sp_bstart, h->sp_hist, h->rec, h->ext, h->sp_st, h->A_x, h->A_y, h->A_i);
+        h->sp_bigg, h->sp_bstart, c.gs, h->sp_hist, h->rec, h->ext, h->sp_st, h->A_x, h->A_y,
+        h->A_i);
   }
   {
-    Launch L(h, "k_sp_slices");
-    k_sp_slices<<<(uint32_t)((nslices * 32 + 255) / 256), 256, 0, s>>>(
-        h->sp_st, h->sp_bstart, h->sp_gbits, h->sp_phimax, h->A_x, h->A_y, h->ext, h->sp_prefmax,
-        h->sp_slice);
+    Launch L(h, "k_sp_slices", s);
+    k_sp_slices<<<(uint32_t)((c.nslices * 32 + 255) / 256), 256, 0, s>>>(
+        h->sp_st, h->sp_bstart, c.gs, h->sp_gbits, h->sp_phimax, h->A_x, h->A_y, h->ext,
+        h->sp_prefmax, h->sp_slice);
   }
   TRY(rec_event(h, h->ev[2], s));
-  // F4 -> C in (surv, sp_eb); codes of candidates marked
+  return GSCAN_OK;
+}
+
+// F4 -> C in (surv, sp_eb); codes of candidates marked
+int sp_seg_f4(gscan_handle* h, const SpCtx& c) {
+  cudaStream_t s = c.s;
   {
-    Launch L(h, "k_sp_cand");
-    k_sp_cand<<<G, kSpCandThreads, smem_nb, s>>>(h->sp_codes, h->sp_phi32, n, cap, h->sp_gbits,
-                                                 h->sp_prefmax, h->sp_st, h->surv, h->sp_eb,
-                                                 h->sp_ccount, drop);
+    Launch L(h, "k_sp_cand", s);
+    k_sp_cand<<<c.G, kSpCandThreads, c.smem_nb, s>>>(h->sp_codes, h->sp_phi32, c.n, c.cap,
+                                                     h->sp_gbits, h->sp_prefmax, h->sp_st, h->surv,
+                                                     h->sp_eb, h->sp_ccount, c.drop);
   }
   {
-    Launch L(h, "k_sp_check_cand");
+    Launch L(h, "k_sp_check_cand", s);
     k_sp_check_cand<<<1, 32, 0, s>>>(h->sp_st);
   }
+  return GSCAN_OK;
+}
+
+// candidates (regions indexing cx/cy) + gathered points, exactly ordered and
+// walked; the round-2 output compacted into A; the certificate's statistics
+int sp_seg_walk(gscan_handle* h, const SpCtx& c, const double* cx, const double* cy,
+                uint32_t n_walk_cap) {
+  cudaStream_t s = c.s;
+  const uint32_t nb = c.nb;
   {
-    Launch L(h, "k_sp_rank_c");
-    k_sp_emit_place<1><<<dim3(4, G), 256, 0, s>>>(xs, ys, h->surv, h->sp_eb, h->rank, h->sp_ccount,
-                                                  cap, h->sp_ccnt, nullptr, h->ext, h->sp_st,
-                                                  h->rec);
+    Launch L(h, "k_sp_rank_c", s);
+    k_sp_emit_place<1><<<dim3(4, c.G), 256, 0, s>>>(cx, cy, h->surv, h->sp_eb, h->rank,
+                                                    h->sp_ccount, c.cap, h->sp_ccnt, nullptr,
+                                                    h->ext, h->sp_st, h->rec);
   }
   TRY(scan_u32(h, h->sp_ccnt, nb, h->sp_cstart));
   {
-    Launch L(h, "k_sp_place_c");
-    k_sp_emit_place<2><<<dim3(4, G), 256, 0, s>>>(xs, ys, h->surv, h->sp_eb, h->rank, h->sp_ccount,
-                                                  cap, nullptr, h->sp_cstart, h->ext, h->sp_st,
-                                                  h->rec);
+    Launch L(h, "k_sp_place_c", s);
+    k_sp_emit_place<2><<<dim3(4, c.G), 256, 0, s>>>(cx, cy, h->surv, h->sp_eb, h->rank,
+                                                    h->sp_ccount, c.cap, nullptr, h->sp_cstart,
+                                                    h->ext, h->sp_st, h->rec);
   }
   {
-    Launch L(h, "k_sp_wcount");
+    Launch L(h, "k_sp_wcount", s);
     k_sp_wcount<<<(nb + 255) / 256, 256, 0, s>>>(h->sp_gbits, h->sp_hist, h->sp_ccnt, h->sp_wcnt);
   }
   TRY(scan_u32(h, h->sp_wcnt, nb, h->sp_wstart));
   {
-    Launch L(h, "k_sp_place_cand");
+    Launch L(h, "k_sp_place_cand", s);
     k_sp_place_cand<<<nb / 8, 256, 0, s>>>(h->rec, h->sp_cstart, h->sp_wstart, h->sp_slice,
                                            h->ext, h->sp_st, h->sp_big, h->C_x, h->C_y, h->C_i,
                                            h->sp_Wb, h->sp_Ws, h->flags);
   }
   {
-    Launch L(h, "k_sp_sort_cand_big");
+    Launch L(h, "k_sp_sort_cand_big", s);
     k_sp_sort_cand_big<<<h->sm_count, kSpSortThreads, kSpBigSmem, s>>>(
         h->sp_big, h->rec, h->sp_cstart, h->sp_wstart, h->sp_slice, h->ext, h->sp_st, h->C_x,
         h->C_y, h->C_i, h->sp_Wb, h->sp_Ws, h->flags);
   }
   {
-    Launch L(h, "k_sp_place_gathered");
+    Launch L(h, "k_sp_place_gathered", s);
     k_sp_place_gathered<<<h->sm_count * 4, 256, 0, s>>>(
-        h->sp_glist, h->sp_bstart, h->sp_hist, h->sp_wstart, h->A_x, h->A_y, h->A_i, h->ext,
+        h->sp_glist, h->sp_bstart, c.gs, h->sp_hist, h->sp_wstart, h->A_x, h->A_y, h->A_i, h->ext,
         h->sp_st, h->C_x, h->C_y, h->C_i, h->sp_Wb, h->sp_Ws, h->flags);
   }
   TRY(rec_event(h, h->ev[3], s));
   {
-    Launch L(h, "k_sp_segments");
+    Launch L(h, "k_sp_segments", s);
     k_sp_segments<<<h->sm_count * 8, kBlock, 0, s>>>(h->sp_Ws, h->sp_st, h->sp_seglo, h->sp_seghi);
   }
   {
-    Launch L(h, "k_sp_walk");
-    k_sp_walk<<<(uint32_t)nslices, kWalkBlock, 0, s>>>(h->C_x, h->C_y, h->sp_seglo, h->sp_seghi,
-                                                       h->sp_st, h->ext, h->flags);
+    Launch L(h, "k_sp_walk", s);
+    k_sp_walk<<<(uint32_t)c.nslices, kWalkBlock, 0, s>>>(h->C_x, h->C_y, h->sp_seglo, h->sp_seghi,
+                                                         h->sp_st, h->ext, h->flags);
   }
   {
-    const uint64_t tiles = (uint64_t)n / kCompactTile + 2;
+    const uint64_t tiles = (uint64_t)n_walk_cap / kCompactTile + 2;
     TRY(reset_lookback(h, tiles));
-    Launch L(h, "k_sp_compact");
+    Launch L(h, "k_sp_compact", s);
     k_sp_compact<<<(uint32_t)tiles, kBlock, 0, s>>>(h->C_x, h->C_y, h->C_i, h->sp_Wb, h->sp_Ws,
                                                     h->flags, h->sp_st, h->A_x, h->A_y, h->A_i,
                                                     h->sp_Rb, h->sp_Rs, h->status, h->ctr);
@@ -1113,24 +1179,35 @@ int sparse_enqueue(gscan_handle* h, const double* xs, const double* ys, uint32_t
   // overlaps the certificate and the Graham tail
   TRY(rec_event(h, h->ev_f3, s));
   {
-    Launch L(h, "k_sp_rlo");
+    Launch L(h, "k_sp_rlo", s);
     k_sp_rlo<<<h->sm_count * 8, kBlock, 0, s>>>(h->sp_Rb, h->sp_st, h->sp_rlo);
   }
   {
-    Launch L(h, "k_sp_cert_stats");
+    Launch L(h, "k_sp_cert_stats", s);
     k_sp_cert_stats<<<h->sm_count, 256, 0, s>>>(h->A_x, h->A_y, h->sp_Rs, h->sp_st);
   }
   {
-    Launch L(h, "k_sp_cert_decide");
-    k_sp_cert_decide<<<1, 32, 0, s>>>(h->sp_st, drop || (h->debug & GSCAN_DEBUG_SPARSE_VERIFY));
+    Launch L(h, "k_sp_cert_decide", s);
+    k_sp_cert_decide<<<1, 32, 0, s>>>(h->sp_st, c.drop || (h->debug & GSCAN_DEBUG_SPARSE_VERIFY));
   }
+  return GSCAN_OK;
+}
+
+// F6 (one device only: it reads every survivor), then the read-back
+int sp_seg_verify(gscan_handle* h, const SpCtx& c) {
+  cudaStream_t s = c.s;
   {
-    Launch L(h, "k_sp_verify");
-#define A6 xs, ys, h->sp_codes, n, h->sp_gbits, h->sp_rlo, h->A_x, h->A_y, h->sp_st
-    if (vec) k_sp_verify<true><<<G, kSpThreads, smem_nb + 4, s>>>(A6);
-    else k_sp_verify<false><<<G, kSpThreads, smem_nb + 4, s>>>(A6);
+    Launch L(h, "k_sp_verify", s);
+#define A6 c.xs, c.ys, h->sp_codes, c.n, h->sp_gbits, h->sp_rlo, h->A_x, h->A_y, h->sp_st
+    if (c.vec) k_sp_verify<true><<<c.G, kSpThreads, c.smem_nb + 4, s>>>(A6);
+    else k_sp_verify<false><<<c.G, kSpThreads, c.smem_nb + 4, s>>>(A6);
 #undef A6
   }
+  return GSCAN_OK;
+}
+
+int sp_seg_tail(gscan_handle* h, const SpCtx& c) {
+  cudaStream_t s = c.s;
   TRY(rec_event(h, h->ev[4], s));
   CU(cudaMemcpyAsync(h->h_sp, h->sp_st, sizeof(SpState), cudaMemcpyDeviceToHost, s));
   CU(cudaMemcpyAsync(&h->ctr->n2, &h->sp_st->n_r, 4, cudaMemcpyDeviceToDevice, s));
@@ -1139,6 +1216,27 @@ int sparse_enqueue(gscan_handle* h, const double* xs, const double* ys, uint32_t
   TRY(tree_enqueue(h, h->A_x, h->A_y, h->A_i, &h->sp_st->n_r, 0, &h->sp_st->fail,
                    tree_forced_off(h), s));
   TRY(rec_event(h, h->ev[5], s));
+  return GSCAN_OK;
+}
+
+// Enqueues the whole sparse path up to and including the verification, the
+// SpState read-back and Graham: no host round trip inside, fixed launch
+// shapes for a given (input, n, config), so run_sparse replays it as one
+// captured CUDA graph.
+int sparse_enqueue(gscan_handle* h, const double* xs, const double* ys, uint32_t n,
+                   const gscan_config& cfg) {
+  const SpCtx c = sp_ctx(h, xs, ys, n, cfg.chunk_count);
+  TRY(sp_seg_init(h, c));
+  TRY(sp_seg_extremes(h, c));
+  TRY(sp_seg_sample(h, c));
+  TRY(sp_seg_f2(h, c));
+  TRY(sp_seg_plan(h, c));
+  TRY(sp_seg_f3(h, c));
+  TRY(sp_seg_sortg(h, c, xs, ys));
+  TRY(sp_seg_f4(h, c));
+  TRY(sp_seg_walk(h, c, xs, ys, n));
+  TRY(sp_seg_verify(h, c));
+  TRY(sp_seg_tail(h, c));
   return GSCAN_OK;
 }
 
@@ -1178,7 +1276,7 @@ int sparse_dup_check(gscan_handle* h, uint32_t n) {
     Launch L(h, "k_sp_dup_part", h->side);
     k_sp_dup_part<<<h->sm_count, 1024, kSpSideSmem, h->side>>>(
         h->sp_dup, h->sp_hcount, cap / 2, nl, h->sp_part_off, h->sp_st, h->sp_dup2, h->sp_side_work,
-        side_free_sms());
+        side_free_sms(), nullptr);
   }
   {
     Launch L(h, "k_sp_dups", h->side);

@@ -698,8 +698,9 @@ __global__ void k_sp_plan_bl(const ExtResult* __restrict__ ext, const double* __
 __global__ void __launch_bounds__(256) k_sp_lrank(const double* __restrict__ xs,
                                                   const double* __restrict__ ys,
                                                   const uint16_t* __restrict__ codes, uint32_t n,
-                                                  const ExtResult* __restrict__ ext,
+                                                  uint32_t base, const ExtResult* __restrict__ ext,
                                                   SpState* __restrict__ st) {
+  // base: global index of point 0 (a shard's offset; 0 on one device)
   if (st->fail) return;
   const uint32_t b_l = st->b_l, l_idx = st->l_idx;
   const double ax = ext->ax, ay = ext->ay;
@@ -724,9 +725,9 @@ __global__ void __launch_bounds__(256) k_sp_lrank(const double* __restrict__ xs,
       for (int h = 0; h < 2; ++h) {
         if (((cw[u] >> (16 * h)) & 0xffffu) != b_l) continue;
         const uint32_t i = 2 * (p0 + u * nth) + h;
-        if (i == l_idx) continue;
+        if (base + i == l_idx) continue;
         const double dx = __dsub_rn(xs[i], ax), dy = __dsub_rn(ys[i], ay);
-        below += key_less(angle_key(dx, dy), dist2_rn(dx, dy), i, lkey, ld2, l_idx);
+        below += key_less(angle_key(dx, dy), dist2_rn(dx, dy), base + i, lkey, ld2, l_idx);
       }
     }
   }
@@ -1018,7 +1019,8 @@ __global__ void __launch_bounds__(1024) k_sp_dup_part(const uint64_t* __restrict
                                                       const uint32_t* __restrict__ part_off,
                                                       const SpState* __restrict__ st,
                                                       uint64_t* __restrict__ parted,
-                                                      uint32_t* __restrict__ ticket, uint32_t n_free) {
+                                                      uint32_t* __restrict__ ticket, uint32_t n_free,
+                                                      const uint64_t* __restrict__ list_base) {
   extern __shared__ __align__(16) unsigned char smem[];
   uint64_t* s_in = reinterpret_cast<uint64_t*>(smem);
   uint64_t* s_out = s_in + kSpPartChunk;
@@ -1031,7 +1033,7 @@ __global__ void __launch_bounds__(1024) k_sp_dup_part(const uint64_t* __restrict
   uint32_t c;
   while (side_take(ticket, &s_item, C, c)) {
     const uint32_t cnt = h_count[c];
-    const uint64_t* src = hlist + (size_t)c * cap;
+    const uint64_t* src = hlist + (list_base ? list_base[c] : (size_t)c * cap);
     for (uint32_t p = threadIdx.x; p < kSpParts; p += blockDim.x) {
       s_cur[p] = part_off[(size_t)p * C + c];
       s_cnt[p] = 0;
@@ -1390,7 +1392,8 @@ constexpr size_t kSpSmallSmem = (size_t)kSpSmallCap * (8 + 8 + 8 + 8 + 4 + 4 + 4
 
 __global__ void __launch_bounds__(kSpSmallThreads) k_sp_sort_gathered(
     const uint32_t* __restrict__ glist, const uint32_t* __restrict__ bstart,
-    const uint32_t* __restrict__ hist, const uint32_t* __restrict__ gcnt,
+    const uint32_t* __restrict__ gs, const uint32_t* __restrict__ hist,
+    const uint32_t* __restrict__ gcnt,
     const PtRec* __restrict__ rec, const ExtResult* __restrict__ ext, SpState* __restrict__ st,
     uint32_t* __restrict__ big, double* __restrict__ A_x, double* __restrict__ A_y,
     uint32_t* __restrict__ A_i) {
@@ -1402,7 +1405,7 @@ __global__ void __launch_bounds__(kSpSmallThreads) k_sp_sort_gathered(
                      kSpSmallCap + 1;
   for (uint32_t g = blockIdx.x; g < ngb; g += gridDim.x) {
     const uint32_t b = glist[g];
-    const uint32_t s0 = bstart[b], cnt = hist[b];
+    const uint32_t s0 = bstart[b], g0 = gs[b], cnt = hist[b];
     if (gcnt[b] != cnt) {  // every point of a gathered bucket must have been emitted
       if (threadIdx.x == 0) { atomicOr(&st->fail, kSpFailInternal); atomicMax(&st->why, 1u); }
       return;
@@ -1415,13 +1418,13 @@ __global__ void __launch_bounds__(kSpSmallThreads) k_sp_sort_gathered(
     __syncthreads();
     for (uint32_t t = threadIdx.x; t < cnt; t += blockDim.x) s_list[t] = 0xffffffffu;
     bool slow = false;
-    const bool dup = cta_sort_bucket_sub<kSpSmallCap>(rec + s0, cnt, ax, ay, smem, &slow,
+    const bool dup = cta_sort_bucket_sub<kSpSmallCap>(rec + g0, cnt, ax, ay, smem, &slow,
                                                       [&](uint32_t r, double x, double y, uint32_t idx) {
-      const uint32_t pos = 1 + s0 + r;
-      A_x[pos] = x;
-      A_y[pos] = y;
-      A_i[pos] = idx;
-      if (idx == l_idx) st->l_check = pos;
+      const uint32_t q = 1 + g0 + r;  // storage; the position is 1 + s0 + r
+      A_x[q] = x;
+      A_y[q] = y;
+      A_i[q] = idx;
+      if (idx == l_idx) st->l_check = 1 + s0 + r;
     });
     if (slow) {
       if (threadIdx.x == 0) big[atomicAdd(&st->n_bigg, 1u)] = b;
@@ -1437,7 +1440,8 @@ constexpr size_t kSpBigSmem = (size_t)kSpGatherCap * (8 + 8 + 8 + 8 + 4 + 4 + 4 
 
 __global__ void __launch_bounds__(kSpSortThreads) k_sp_sort_gathered_big(
     const uint32_t* __restrict__ big, const uint32_t* __restrict__ bstart,
-    const uint32_t* __restrict__ hist, const PtRec* __restrict__ rec,
+    const uint32_t* __restrict__ gs, const uint32_t* __restrict__ hist,
+    const PtRec* __restrict__ rec,
     const ExtResult* __restrict__ ext, SpState* __restrict__ st, double* __restrict__ A_x,
     double* __restrict__ A_y, uint32_t* __restrict__ A_i) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -1448,7 +1452,7 @@ __global__ void __launch_bounds__(kSpSortThreads) k_sp_sort_gathered_big(
                      kSpGatherCap + 1;
   for (uint32_t g = blockIdx.x; g < nbig; g += gridDim.x) {
     const uint32_t b = big[g];
-    const uint32_t s0 = bstart[b], cnt = hist[b];
+    const uint32_t s0 = bstart[b], g0 = gs[b], cnt = hist[b];
     if (cnt > kSpGatherCap) {
       if (threadIdx.x == 0) { atomicOr(&st->fail, kSpFailCap); atomicMax(&st->why, 4u); }
       return;
@@ -1456,13 +1460,13 @@ __global__ void __launch_bounds__(kSpSortThreads) k_sp_sort_gathered_big(
     __syncthreads();
     for (uint32_t t = threadIdx.x; t < cnt; t += blockDim.x) s_list[t] = 0xffffffffu;
     bool slow = false;
-    const bool dup = cta_sort_bucket_sub<kSpGatherCap>(rec + s0, cnt, ax, ay, smem, &slow,
+    const bool dup = cta_sort_bucket_sub<kSpGatherCap>(rec + g0, cnt, ax, ay, smem, &slow,
                                                        [&](uint32_t r, double x, double y, uint32_t idx) {
-      const uint32_t pos = 1 + s0 + r;
-      A_x[pos] = x;
-      A_y[pos] = y;
-      A_i[pos] = idx;
-      if (idx == l_idx) st->l_check = pos;
+      const uint32_t q = 1 + g0 + r;
+      A_x[q] = x;
+      A_y[q] = y;
+      A_i[q] = idx;
+      if (idx == l_idx) st->l_check = 1 + s0 + r;
     });
     if (dup) atomicOr(&st->fail, kSpFailDup);
   }
@@ -1511,7 +1515,8 @@ __device__ __forceinline__ SliceSpan slice_span(const SpState& st, uint32_t s) {
 // when the step was ambiguous) contribute nothing (conservative).
 __global__ void __launch_bounds__(256) k_sp_slices(
     const SpState* __restrict__ st_, const uint32_t* __restrict__ bstart,
-    const uint32_t* __restrict__ gbits, const uint32_t* __restrict__ phimax,
+    const uint32_t* __restrict__ gs, const uint32_t* __restrict__ gbits,
+    const uint32_t* __restrict__ phimax,
     const double* __restrict__ A_x, const double* __restrict__ A_y,
     const ExtResult* __restrict__ ext, uint32_t* __restrict__ prefmax,
     uint32_t* __restrict__ slice_of) {
@@ -1529,9 +1534,10 @@ __global__ void __launch_bounds__(256) k_sp_slices(
   if (sp.right) { h0 = sp.seed; h1 = min(sp.hi, bstart[bs + 1]); }
   else { h0 = max(sp.lo, 1 + bstart[bs]); h1 = sp.seed; }
   double hm = -1e300;
+  const uint32_t qd = gs[bs] - bstart[bs];  // position -> storage in the seed's bucket
   for (uint32_t p = h0 + lane; p <= h1; p += 32) {
     double v2;
-    const double raw = sp_phi_raw(A_x[p], A_y[p], lx, ly, ux, uy, &v2);
+    const double raw = sp_phi_raw(A_x[p + qd], A_y[p + qd], lx, ly, ux, uy, &v2);
     if (v2 >= st.r02) hm = fmax(hm, sp.right ? raw : -raw);
   }
 #pragma unroll
@@ -1785,7 +1791,8 @@ __global__ void __launch_bounds__(kSpSortThreads) k_sp_sort_cand_big(
 // gathered bucket); W[0] = anchor.
 __global__ void __launch_bounds__(256) k_sp_place_gathered(
     const uint32_t* __restrict__ glist, const uint32_t* __restrict__ bstart,
-    const uint32_t* __restrict__ hist, const uint32_t* __restrict__ wstart,
+    const uint32_t* __restrict__ gs, const uint32_t* __restrict__ hist,
+    const uint32_t* __restrict__ wstart,
     const double* __restrict__ A_x, const double* __restrict__ A_y,
     const uint32_t* __restrict__ A_i, const ExtResult* __restrict__ ext, SpState* __restrict__ st_,
     double* __restrict__ W_x, double* __restrict__ W_y, uint32_t* __restrict__ W_i,
@@ -1804,12 +1811,12 @@ __global__ void __launch_bounds__(256) k_sp_place_gathered(
   }
   for (uint32_t g = blockIdx.x; g < st.n_gb; g += gridDim.x) {
     const uint32_t b = glist[g];
-    const uint32_t s0 = bstart[b], cnt = hist[b], w0 = wstart[b];
+    const uint32_t s0 = bstart[b], g0 = gs[b], cnt = hist[b], w0 = wstart[b];
     for (uint32_t r = threadIdx.x; r < cnt; r += blockDim.x) {
-      const uint32_t p = 1 + s0 + r, w = 1 + w0 + r;
-      W_x[w] = A_x[p];
-      W_y[w] = A_y[p];
-      W_i[w] = A_i[p];
+      const uint32_t p = 1 + s0 + r, q = 1 + g0 + r, w = 1 + w0 + r;
+      W_x[w] = A_x[q];
+      W_y[w] = A_y[q];
+      W_i[w] = A_i[q];
       W_b[w] = b;
       W_s[w] = slice_of_pos(st, p);
       flags[w] = 1;
@@ -2213,6 +2220,59 @@ __global__ void __launch_bounds__(kBlock) k_sp_compact(
       out_s[o] = in_s[i];
       ++o;
     }
+  }
+}
+
+
+// ===========================================================================
+// Sharded sparse path (distributed.py): conversions between a
+// rank's per-CTA emission regions and compact records {x, y, global index,
+// bucket} that travel between ranks.
+
+// Regions (e_idx, e_b, e_count; cap slots per region, G regions) -> compact
+// records; *n_out counts (order is arbitrary: the receiver sorts by index).
+__global__ void __launch_bounds__(256) k_sp_export(
+    const double* __restrict__ xs, const double* __restrict__ ys,
+    const uint32_t* __restrict__ e_idx, const uint32_t* __restrict__ e_b,
+    const uint32_t* __restrict__ e_count, uint32_t cap, uint32_t base, const SpState* __restrict__ st,
+    double* __restrict__ ox, double* __restrict__ oy, uint32_t* __restrict__ oi,
+    uint32_t* __restrict__ ob, uint32_t* __restrict__ n_out) {
+  if (st->fail) return;
+  const uint32_t c = blockIdx.y;
+  const uint32_t ne = e_count[c];
+  const size_t rb = (size_t)c * cap;
+  for (uint32_t k0 = blockIdx.x * blockDim.x; k0 < ne; k0 += gridDim.x * blockDim.x) {
+    const uint32_t k = k0 + threadIdx.x;
+    const bool have = k < ne;
+    const uint32_t act = __ballot_sync(0xffffffffu, have);
+    uint32_t at = 0;
+    if ((threadIdx.x & 31) == 0 && act) at = atomicAdd(n_out, (uint32_t)__popc(act));
+    at = __shfl_sync(0xffffffffu, at, 0) + __popc(act & lanemask_lt());
+    if (have) {
+      const uint32_t i = e_idx[rb + k];
+      ox[at] = xs[i];
+      oy[at] = ys[i];
+      oi[at] = base + i;
+      ob[at] = e_b[rb + k];
+    }
+  }
+}
+
+// Compact items j < n (buckets b_in[j]) -> regions: item j goes to region
+// j / per (per = ceil(n / G) <= cap) as index idx0 + j.
+__global__ void __launch_bounds__(256) k_sp_fill_regions(uint32_t n, uint32_t idx0,
+                                                         const uint32_t* __restrict__ b_in,
+                                                         uint32_t G, uint32_t cap,
+                                                         uint32_t* __restrict__ e_idx,
+                                                         uint32_t* __restrict__ e_b,
+                                                         uint32_t* __restrict__ e_count) {
+  const uint32_t per = (n + G - 1) / G;
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < G; c += gridDim.x * blockDim.x)
+    e_count[c] = c * per < n ? min(per, n - c * per) : 0u;
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    const uint32_t c = j / per, k = j - c * per;
+    e_idx[(size_t)c * cap + k] = idx0 + j;
+    e_b[(size_t)c * cap + k] = b_in[j];
   }
 }
 
