@@ -150,6 +150,14 @@ struct gscan_handle {
   uint32_t tw_nmax = 0, tw_nch1 = 0;
   TreeWork tw{};
   uint32_t* h_info = nullptr;   // pinned mirror of the tree strategy's info words
+  // sharded sparse path (gscan_dist_*): this rank's shard and scratch
+  const double* dist_xs = nullptr;
+  const double* dist_ys = nullptr;
+  uint32_t dist_n = 0, dist_base = 0;
+  uint64_t dist_chunks = 0;
+  uint32_t *sp_gs = nullptr, *sp_gsz = nullptr, *dist_ctr = nullptr, *dist_pm = nullptr,
+           *dist_hc = nullptr;
+  uint64_t* dist_lb = nullptr;
 };
 
 namespace {
@@ -261,7 +269,9 @@ int reserve(gscan_handle* h, uint64_t n) {
   CU(cudaMalloc(&h->g_keep, nch * 4));
   CU(cudaMalloc(&h->g_misc, 256));
   const uint64_t tiles = std::max((m + kCompactTile - 1) / kCompactTile,
-                                  (uint64_t)(nb + 2 + kScanTile - 1) / kScanTile) + 64;
+                                  (uint64_t)(nb + 2 + kScanTile - 1) / kScanTile) + 64 +
+                         // the sharded path scans kSpParts x (hash lists | ranks) counts
+                         ((uint64_t)kSpParts * std::max(2 * h->sm_count, 64) + kScanTile) / kScanTile;
   h->status_cap = tiles;
   CU(cudaMalloc(&h->status, tiles * 8));
   CU(cudaMalloc(&h->sp_eb, mr * 4));
@@ -1287,6 +1297,18 @@ int sparse_dup_check(gscan_handle* h, uint32_t n) {
   return GSCAN_OK;
 }
 
+void sp_debug_print(const gscan_handle* h, const char* tag) {
+  const SpState& sp = *h->h_sp;
+  fprintf(stderr, "%s ", tag);
+  fprintf(stderr,
+            "[sparse] fail=%#x m=%u M=%u b_l=%u l=%u/%u l_idx=%u ties=%u step=%u,%u slices=%u+%u "
+            "n_gb=%u n_g=%u max_g=%u n_c=%u n_w=%u n_r=%u dups=%u vfail=%u why=%u bigc=%u cert=%u kmax=%u rho=%.3g phi=[%.4f,%.4f]\n",
+            sp.fail, sp.m, sp.M, sp.b_l, sp.l, sp.l_check, sp.l_idx, sp.ties, sp.step_r, sp.step_l,
+            sp.n_right, sp.n_left, sp.n_gb, sp.n_g, sp.max_g, sp.n_c, sp.n_w, sp.n_r, sp.dups,
+            sp.verify_fail, sp.why, sp.n_bigc, sp.cert, sp.k_max, sqrt(__longlong_as_double_host(sp.rho2_bits)),
+            unord_host(sp.phi_lo), unord_host(sp.phi_hi));
+  }
+
 int run_sparse(gscan_handle* h, const double* xs, const double* ys, uint32_t n,
                const gscan_config& cfg, uint64_t* hull_size, gscan_stats* st, bool* ok) {
   *ok = false;
@@ -1353,15 +1375,7 @@ enqueued:
   if (dup_check) TRY(sparse_dup_check(h, n));
   TRY(sync_counters(h));
   const SpState sp = *h->h_sp;
-  if (h->sp_debug) {
-    fprintf(stderr,
-            "[sparse] fail=%#x m=%u M=%u b_l=%u l=%u/%u l_idx=%u ties=%u step=%u,%u slices=%u+%u "
-            "n_gb=%u n_g=%u max_g=%u n_c=%u n_w=%u n_r=%u dups=%u vfail=%u why=%u bigc=%u cert=%u kmax=%u rho=%.3g phi=[%.4f,%.4f]\n",
-            sp.fail, sp.m, sp.M, sp.b_l, sp.l, sp.l_check, sp.l_idx, sp.ties, sp.step_r, sp.step_l,
-            sp.n_right, sp.n_left, sp.n_gb, sp.n_g, sp.max_g, sp.n_c, sp.n_w, sp.n_r, sp.dups,
-            sp.verify_fail, sp.why, sp.n_bigc, sp.cert, sp.k_max, sqrt(__longlong_as_double_host(sp.rho2_bits)),
-            unord_host(sp.phi_lo), unord_host(sp.phi_hi));
-  }
+  if (h->sp_debug) sp_debug_print(h, "[run]");
   h->sp_fail = sp.fail | ((sp.fail & kSpFailInternal) ? (sp.why << 16) : 0u);
   h->sp_walked = sp.n_w;
   h->sp_cert = sp.cert;
@@ -1470,6 +1484,57 @@ gscan_handle* g_default = nullptr;
 
 // ============================================================================
 // C-ABI
+
+// ---------------------------------------------------------------------------
+// Sharded sparse path. Each rank runs the segments of the
+// sparse path on its shard; the host (distributed.py) does the collectives
+// between the phases: sample cells and the bucket histogram are summed, P_l
+// is the best record over ranks, P_l's in-bucket rank and the phi maxima are
+// reduced, gathered and candidate points travel to rank 0 as records {x, y,
+// global index, bucket}, rank 0 broadcasts the prefix maxima, and the 64-bit
+// hashes are exchanged by partition for the duplicate check. Every exchange is
+// KB-MB sized; no rank ever holds another rank's survivors.
+constexpr uint32_t kDistMaxRanks = 64;
+
+int dist_init(gscan_handle* h) {
+  if (h->sp_gs) return GSCAN_OK;
+  CU(cudaMalloc(&h->sp_gs, (kSpBuckets + 2) * 4));
+  CU(cudaMalloc(&h->sp_gsz, (kSpBuckets + 2) * 4));
+  CU(cudaMalloc(&h->dist_ctr, 64));
+  CU(cudaMalloc(&h->dist_pm, ((size_t)kSpParts * kDistMaxRanks + 2) * 4));
+  CU(cudaMalloc(&h->dist_hc, kDistMaxRanks * 4));
+  CU(cudaMalloc(&h->dist_lb, kDistMaxRanks * 8));
+  return GSCAN_OK;
+}
+
+SpCtx dist_ctx(gscan_handle* h) {
+  SpCtx c = sp_ctx(h, h->dist_xs, h->dist_ys, h->dist_n, h->dist_chunks);
+  c.base = h->dist_base;
+  return c;
+}
+
+int dist_read_state(gscan_handle* h) {
+  CU(cudaMemcpyAsync(h->h_sp, h->sp_st, sizeof(SpState), cudaMemcpyDeviceToHost, h->stream));
+  TRY(sync_counters(h));
+  if (h->sp_debug) sp_debug_print(h, "[dist]");
+  return GSCAN_OK;
+}
+
+// fail word for the host: the internal-error site in the high half
+uint32_t dist_fail(const gscan_handle* h) {
+  const SpState& sp = *h->h_sp;
+  return sp.fail | ((sp.fail & kSpFailInternal) ? (sp.why << 16) : 0u);
+}
+
+int dist_fill(gscan_handle* h, const SpCtx& c, uint32_t n_items, uint32_t idx0, const uint32_t* b,
+              uint32_t* count) {
+  if (n_items > 0 && (n_items + c.G - 1) / c.G > c.cap)
+    return fail(h, GSCAN_E_CAPACITY, "sharded path: %u records exceed the emission regions", n_items);
+  Launch L(h, "k_sp_fill_regions", c.s);
+  k_sp_fill_regions<<<std::max(1u, std::min((n_items + 255) / 256, 4u * h->sm_count)), 256, 0, c.s>>>(
+      n_items, idx0, b, c.G, c.cap, h->surv, h->sp_eb, count);
+  return GSCAN_OK;
+}
 
 extern "C" {
 
@@ -1587,6 +1652,8 @@ int gscan_destroy(gscan_handle* h) {
   if (h->h_ctr) cudaFreeHost(h->h_ctr);
   if (h->h_info) cudaFreeHost(h->h_info);
   dfree(h->tw_pool);
+  dfree(h->sp_gs); dfree(h->sp_gsz); dfree(h->dist_ctr); dfree(h->dist_pm); dfree(h->dist_hc);
+  dfree(h->dist_lb);
   if (h->h_out) cudaFreeHost(h->h_out);
   for (auto& e : h->ev) if (e) cudaEventDestroy(e);
   for (auto& k : h->ktimes) { cudaEventDestroy(k.a); cudaEventDestroy(k.b); }
@@ -1853,6 +1920,219 @@ int gscan_shard_round1(gscan_handle* h, const double* d_xs, const double* d_ys, 
   if (*n_out)
     CU(cudaMemcpyAsync(d_out, h->surv, (size_t)*n_out * 4, cudaMemcpyDeviceToDevice, h->stream));
   CU(cudaStreamSynchronize(h->stream));
+  return GSCAN_OK;
+}
+
+int gscan_dist_begin(gscan_handle* h, const double* d_xs, const double* d_ys, uint64_t n,
+                     uint64_t offset, const gscan_extremes* global, const gscan_config* cfg,
+                     uint32_t* d_cells) {
+  if (!h || !global || !cfg || !d_cells) return GSCAN_E_INVALID;
+  TRY(validate(h, n, *cfg));
+  if (offset + n >= 0xffffffffull) return fail(h, GSCAN_E_TOO_LARGE, "global index beyond 2^32-2");
+  CU(cudaSetDevice(h->device));
+  TRY(reserve(h, n));
+  TRY(sparse_init(h));
+  TRY(dist_init(h));
+  const uint64_t nslices = 2 * std::min<uint64_t>(cfg->chunk_count, n);
+  if (nslices + 2 > h->sp_seg_cap) {
+    dfree(h->sp_seglo);
+    dfree(h->sp_seghi);
+    CU(cudaMalloc(&h->sp_seglo, (nslices + 2) * 4));
+    CU(cudaMalloc(&h->sp_seghi, (nslices + 2) * 4));
+    h->sp_seg_cap = nslices + 2;
+    h->sp_graph_ok = false;
+  }
+  h->dist_xs = d_xs;
+  h->dist_ys = d_ys;
+  h->dist_n = (uint32_t)n;
+  h->dist_base = (uint32_t)offset;
+  h->dist_chunks = cfg->chunk_count;
+  const SpCtx c = dist_ctx(h);
+  TRY(sp_seg_init(h, c));
+  ExtResult q{};
+  for (int k = 0; k < 4; ++k) { q.idx[k] = (uint32_t)global->idx[k]; q.qx[k] = global->x[k]; q.qy[k] = global->y[k]; }
+  q.idx[4] = (uint32_t)global->idx[4];
+  q.ax = global->x[4];
+  q.ay = global->y[4];
+  CU(cudaMemcpyAsync(h->ext, &q, sizeof q, cudaMemcpyHostToDevice, c.s));
+  TRY(sp_seg_sample(h, c));
+  CU(cudaMemcpyAsync(d_cells, h->sp_cells, kSpCells * 4, cudaMemcpyDeviceToDevice, c.s));
+  CU(cudaStreamSynchronize(c.s));
+  return GSCAN_OK;
+}
+
+int gscan_dist_hist(gscan_handle* h, const uint32_t* d_cells, uint32_t* d_hist,
+                    gscan_dist_best* best, uint64_t* n1) {
+  if (!h || !d_cells || !d_hist || !best || !n1) return GSCAN_E_INVALID;
+  const SpCtx c = dist_ctx(h);
+  CU(cudaMemcpyAsync(h->sp_cells, d_cells, kSpCells * 4, cudaMemcpyDeviceToDevice, c.s));
+  TRY(sp_seg_f2(h, c));
+  CU(cudaMemcpyAsync(d_hist, h->sp_hist, kSpBuckets * 4, cudaMemcpyDeviceToDevice, c.s));
+  TRY(dist_read_state(h));
+  const SpState& sp = *h->h_sp;
+  const bool have = sp.l_idx != 0xffffffffu;
+  best->d2_bits = sp.d2max;
+  best->idx = have ? (uint64_t)h->dist_base + sp.l_idx : ~0ull;
+  best->ties = have ? sp.ties : 0;
+  best->pad = 0;
+  best->x = sp.lx;
+  best->y = sp.ly;
+  *n1 = h->h_ctr->n1;
+  return GSCAN_OK;
+}
+
+int gscan_dist_plan(gscan_handle* h, const uint32_t* d_hist, const gscan_dist_best* pl,
+                    uint32_t fail_bits, uint64_t* l_below, uint32_t* fail_out) {
+  if (!h || !d_hist || !pl || !l_below || !fail_out) return GSCAN_E_INVALID;
+  const SpCtx c = dist_ctx(h);
+  CU(cudaMemcpyAsync(h->sp_hist, d_hist, kSpBuckets * 4, cudaMemcpyDeviceToDevice, c.s));
+  k_sp_set_pl<<<1, 1, 0, c.s>>>(h->sp_st, pl->d2_bits, (uint32_t)pl->idx, pl->ties, pl->x, pl->y,
+                                fail_bits);
+  TRY(sp_seg_plan(h, c));
+  TRY(dist_read_state(h));
+  *l_below = h->h_sp->l_below;
+  *fail_out = dist_fail(h);
+  return GSCAN_OK;
+}
+
+int gscan_dist_phi(gscan_handle* h, uint64_t l_below, uint32_t* d_phimax, uint32_t* phi_range,
+                   uint64_t* n_g, uint32_t* fail_out) {
+  if (!h || !d_phimax || !phi_range || !n_g || !fail_out) return GSCAN_E_INVALID;
+  const SpCtx c = dist_ctx(h);
+  k_sp_set_u32<<<1, 1, 0, c.s>>>(&h->sp_st->l_below, (uint32_t)l_below);
+  TRY(sp_seg_f3(h, c));
+  CU(cudaMemcpyAsync(d_phimax, h->sp_phimax, kSpBuckets * 4, cudaMemcpyDeviceToDevice, c.s));
+  TRY(dist_read_state(h));
+  const SpState& sp = *h->h_sp;
+  phi_range[0] = sp.phi_lo;
+  phi_range[1] = sp.phi_hi;
+  *n_g = sp.n_g;
+  *fail_out = dist_fail(h);
+  return GSCAN_OK;
+}
+
+int gscan_dist_export(gscan_handle* h, int candidates, double* d_x, double* d_y, uint32_t* d_idx,
+                      uint32_t* d_b, uint64_t* n_out) {
+  if (!h || !n_out) return GSCAN_E_INVALID;
+  const SpCtx c = dist_ctx(h);
+  CU(cudaMemsetAsync(h->dist_ctr, 0, 4, c.s));
+  {
+    Launch L(h, "k_sp_export", c.s);
+    k_sp_export<<<dim3(8, c.G), 256, 0, c.s>>>(c.xs, c.ys, h->surv, h->sp_eb,
+                                               candidates ? h->sp_ccount : h->sp_gcount, c.cap,
+                                               c.base, h->sp_st, d_x, d_y, d_idx, d_b, h->dist_ctr);
+  }
+  uint32_t cnt = 0;
+  TRY(read_u32(h, h->dist_ctr, &cnt));
+  *n_out = cnt;
+  return GSCAN_OK;
+}
+
+int gscan_dist_slices(gscan_handle* h, const double* d_X, const double* d_Y, uint64_t n_g,
+                      const uint32_t* d_gb, uint64_t l_pos, const uint32_t* d_phimax,
+                      const uint32_t* phi_range, uint32_t* d_prefmax, uint32_t* fail_out) {
+  if (!h || !d_X || !d_Y || !d_phimax || !phi_range || !d_prefmax || !fail_out) return GSCAN_E_INVALID;
+  SpCtx c = dist_ctx(h);
+  if (1 + n_g > h->cap) return fail(h, GSCAN_E_CAPACITY, "sharded path: %llu gathered points exceed rank 0's buffers", (unsigned long long)n_g);
+  CU(cudaMemcpyAsync(h->sp_phimax, d_phimax, kSpBuckets * 4, cudaMemcpyDeviceToDevice, c.s));
+  k_sp_set_phi<<<1, 1, 0, c.s>>>(h->sp_st, phi_range[0], phi_range[1], (uint32_t)l_pos, h->ext, 0u);
+  k_sp_gsize<<<(kSpBuckets + 255) / 256, 256, 0, c.s>>>(h->sp_gbits, h->sp_hist, h->sp_gsz);
+  TRY(scan_u32(h, h->sp_gsz, kSpBuckets, h->sp_gs));
+  TRY(dist_fill(h, c, (uint32_t)n_g, 1, d_gb, h->sp_gcount));
+  c.gs = h->sp_gs;
+  TRY(sp_seg_sortg(h, c, d_X, d_Y));
+  CU(cudaMemcpyAsync(d_prefmax, h->sp_prefmax, kSpBuckets * 4, cudaMemcpyDeviceToDevice, c.s));
+  TRY(dist_read_state(h));
+  *fail_out = dist_fail(h);
+  return GSCAN_OK;
+}
+
+int gscan_dist_cand(gscan_handle* h, const uint32_t* d_prefmax, uint64_t* n_c, uint32_t* fail_out) {
+  if (!h || !d_prefmax || !n_c || !fail_out) return GSCAN_E_INVALID;
+  const SpCtx c = dist_ctx(h);
+  CU(cudaMemcpyAsync(h->sp_prefmax, d_prefmax, kSpBuckets * 4, cudaMemcpyDeviceToDevice, c.s));
+  TRY(sp_seg_f4(h, c));
+  TRY(dist_read_state(h));
+  *n_c = h->h_sp->n_c;
+  *fail_out = dist_fail(h);
+  return GSCAN_OK;
+}
+
+int gscan_dist_finish(gscan_handle* h, const double* d_X, const double* d_Y, uint64_t n_g,
+                      uint64_t n_c, const uint32_t* d_cb, uint32_t* d_hull, uint64_t hull_cap,
+                      uint64_t* hull_n, uint64_t* n_r, uint32_t* fail_out) {
+  if (!h || !d_X || !d_Y || !d_hull || !hull_n || !n_r || !fail_out) return GSCAN_E_INVALID;
+  SpCtx c = dist_ctx(h);
+  c.gs = h->sp_gs;
+  const uint64_t nw = 1 + n_g + n_c;
+  if (nw > h->cap) return fail(h, GSCAN_E_CAPACITY, "sharded path: %llu walk records exceed rank 0's buffers", (unsigned long long)nw);
+  TRY(dist_fill(h, c, (uint32_t)n_c, (uint32_t)(1 + n_g), d_cb, h->sp_ccount));
+  TRY(tree_workspace(h, (uint32_t)std::min<uint64_t>(nw, kTreeMaxN)));
+  TRY(sp_seg_walk(h, c, d_X, d_Y, (uint32_t)nw));
+  k_sp_no_verify<<<1, 32, 0, c.s>>>(h->sp_st);
+  h->graham_path = 0;
+  h->graham_fails = 0;
+  TRY(sp_seg_tail(h, c));
+  TRY(sync_counters(h));
+  const SpState sp = *h->h_sp;
+  *fail_out = dist_fail(h);
+  *n_r = sp.n_r;
+  *hull_n = 0;
+  if (sp.fail) return GSCAN_OK;
+  bool done = false;
+  TRY(tree_finish(h, h->A_x, h->A_y, h->A_i, &done));
+  if (!done) {
+    TRY(stage_graham(h, h->A_x, h->A_y, h->A_i, sp.n_r, /*skip_tree=*/true));
+    TRY(sync_counters(h));
+  }
+  const uint32_t hull = h->h_ctr->hull;
+  if (hull > hull_cap) return fail(h, GSCAN_E_CAPACITY, "hull of %u vertices exceeds out_cap", hull);
+  CU(cudaMemcpyAsync(d_hull, h->d_out, (size_t)hull * 4, cudaMemcpyDeviceToDevice, h->stream));
+  CU(cudaStreamSynchronize(h->stream));
+  *hull_n = hull;
+  return GSCAN_OK;
+}
+
+int gscan_dist_dup_local(gscan_handle* h, uint32_t* d_part_counts, uint64_t* d_parted,
+                         uint64_t* n_hash) {
+  if (!h || !d_part_counts || !d_parted || !n_hash) return GSCAN_E_INVALID;
+  const SpCtx c = dist_ctx(h);
+  const uint32_t nl = 2 * c.G;
+  TRY(scan_u32(h, h->sp_part_off, kSpParts * nl, h->sp_part_off));
+  uint32_t total = 0;
+  TRY(read_u32(h, h->sp_part_off + (size_t)kSpParts * nl, &total));
+  CU(cudaMemsetAsync(h->sp_side_work, 0, 2 * sizeof(uint32_t), c.s));
+  k_sp_set_u32<<<1, 1, 0, c.s>>>(&h->sp_st->fail, 0u);  // the host decided the path globally
+  k_sp_dup_part<<<h->sm_count, 1024, kSpSideSmem, c.s>>>(h->sp_dup, h->sp_hcount, c.cap / 2, nl,
+                                                        h->sp_part_off, h->sp_st, h->sp_dup2,
+                                                        h->sp_side_work, 0u, nullptr);
+  k_sp_part_totals<<<(kSpParts + 255) / 256, 256, 0, c.s>>>(h->sp_part_off, nl, total, d_part_counts);
+  CU(cudaGetLastError());
+  CU(cudaStreamSynchronize(c.s));
+  *d_parted = (uint64_t)(uintptr_t)h->sp_dup2;
+  *n_hash = total;
+  return GSCAN_OK;
+}
+
+int gscan_dist_dup_check(gscan_handle* h, const uint64_t* d_recv, uint64_t n_recv,
+                         const uint32_t* d_counts, uint32_t R, uint32_t* dup_found) {
+  if (!h || !d_counts || !dup_found || R == 0 || R > kDistMaxRanks) return GSCAN_E_INVALID;
+  const SpCtx c = dist_ctx(h);
+  if (n_recv > (uint64_t)h->sp_grid * sparse_region_cap(h, h->dist_n))
+    return fail(h, GSCAN_E_CAPACITY, "sharded duplicate check: %llu hashes received", (unsigned long long)n_recv);
+  k_sp_recv_plan<<<(kSpParts * R + 255) / 256, 256, 0, c.s>>>(d_counts, R, h->dist_pm, h->dist_hc,
+                                                               h->dist_lb);
+  TRY(scan_u32(h, h->dist_pm, kSpParts * R, h->dist_pm));
+  CU(cudaMemsetAsync(h->sp_side_work, 0, 2 * sizeof(uint32_t), c.s));
+  k_sp_set_u32<<<1, 1, 0, c.s>>>(&h->sp_st->fail, 0u);
+  k_sp_dup_part<<<h->sm_count, 1024, kSpSideSmem, c.s>>>(d_recv, h->dist_hc, 0u, R, h->dist_pm,
+                                                        h->sp_st, h->sp_dup, h->sp_side_work, 0u,
+                                                        h->dist_lb);
+  k_sp_dups<<<h->sm_count, 1024, kSpSideSmem, c.s>>>(h->sp_dup, h->dist_pm, R, h->sp_st,
+                                                     h->sp_side_work + 1, 0u);
+  CU(cudaGetLastError());
+  TRY(dist_read_state(h));
+  *dup_found = (h->h_sp->fail & (kSpFailDup | kSpFailCap)) ? 1u : 0u;
   return GSCAN_OK;
 }
 

@@ -1123,7 +1123,7 @@ __global__ void __launch_bounds__(1024) k_sp_dups(const uint64_t* __restrict__ p
   extern __shared__ unsigned long long s_e[];  // kSpDupSlots
   __shared__ uint32_t s_item;
   if (st->fail || sm_id() < n_free) return;
-  const uint32_t total = st->m;
+  const uint32_t total = part_off[(size_t)kSpParts * nparts_cta];  // the scan's total
   bool dup = false, full = false;
   uint32_t p;
   while (side_take(ticket, &s_item, kSpParts, p)) {
@@ -2273,6 +2273,73 @@ __global__ void __launch_bounds__(256) k_sp_fill_regions(uint32_t n, uint32_t id
     const uint32_t c = j / per, k = j - c * per;
     e_idx[(size_t)c * cap + k] = idx0 + j;
     e_b[(size_t)c * cap + k] = b_in[j];
+  }
+}
+
+
+// Host-decided global values into the state (sharded path).
+__global__ void k_sp_set_pl(SpState* __restrict__ st, uint64_t d2, uint32_t l_idx, uint32_t ties,
+                            double lx, double ly, uint32_t fail) {
+  st->d2max = d2;
+  st->l_idx = l_idx;
+  st->ties = ties;
+  st->lx = lx;
+  st->ly = ly;
+  st->fail = fail;
+}
+__global__ void k_sp_set_u32(uint32_t* __restrict__ p, uint32_t v) { *p = v; }
+__global__ void k_sp_set_phi(SpState* __restrict__ st, uint32_t lo, uint32_t hi, uint32_t l_idx,
+                             ExtResult* __restrict__ ext, uint32_t anchor_idx) {
+  st->phi_lo = lo;
+  st->phi_hi = hi;
+  st->l_idx = l_idx;
+  ext->idx[4] = anchor_idx;
+}
+
+// Sizes of the gathered buckets (storage of rank 0's gathered records).
+__global__ void k_sp_gsize(const uint32_t* __restrict__ gbits, const uint32_t* __restrict__ hist,
+                           uint32_t* __restrict__ out) {
+  const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < kSpBuckets) out[b] = sp_gathered(gbits, b) ? hist[b] : 0u;
+}
+
+// Sharded path: without F6, a round-2 result the certificate does not prove
+// is declined.
+__global__ void k_sp_no_verify(SpState* __restrict__ st) {
+  if (threadIdx.x == 0 && st->need_verify) atomicOr(&st->fail, kSpFailVerify);
+}
+
+// Hash counts per partition of this rank (part_off scanned, nl lists).
+__global__ void k_sp_part_totals(const uint32_t* __restrict__ part_off, uint32_t nl,
+                                 uint32_t total, uint32_t* __restrict__ out) {
+  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= kSpParts) return;
+  const uint32_t lo = part_off[(size_t)p * nl];
+  const uint32_t hi = p + 1 < kSpParts ? part_off[(size_t)(p + 1) * nl] : total;
+  out[p] = hi - lo;
+}
+
+// Received hash blocks (R sources; cnt[r * kSpParts + p] entries of
+// partition p from source r, block r = its partitions in order) -> the
+// partition-major count table for the partitioning kernel, block sizes and
+// block bases.
+__global__ void k_sp_recv_plan(const uint32_t* __restrict__ cnt, uint32_t R,
+                               uint32_t* __restrict__ pm, uint32_t* __restrict__ h_count,
+                               uint64_t* __restrict__ list_base) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < kSpParts * R) {
+    const uint32_t p = t / R, r = t - p * R;
+    pm[t] = cnt[(size_t)r * kSpParts + p];
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    uint64_t acc = 0;
+    for (uint32_t r = 0; r < R; ++r) {
+      uint32_t sz = 0;
+      for (uint32_t p = 0; p < kSpParts; ++p) sz += cnt[(size_t)r * kSpParts + p];
+      h_count[r] = sz;
+      list_base[r] = acc;
+      acc += sz;
+    }
   }
 }
 

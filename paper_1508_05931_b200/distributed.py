@@ -2,18 +2,39 @@
 
 Rank r owns a contiguous shard [offset_r, offset_r + n_r) of the input
 (global input order = rank-major), so index ties resolve exactly as on one
-device. The exchange follows the north star's simple form:
-  1. every rank reduces its five extreme points (K1), an all-gather of
-     15 doubles per rank, and every rank combines them with the reference's
-     tie rules (strict compares, lowest global index; prefilter.hpp:28-39,
-     angular.hpp:40-49);
-  2. every rank filters its shard against the GLOBAL quadrilateral (K2) --
-     the round-1 result is therefore identical to the single-device one;
-  3. the survivors (x, y, global index) are gathered to rank 0 in rank order,
-     which runs the rest of the pipeline (round 1 disabled: it already ran).
-Step 3 is an all-gather of the survivor set, which is cheap for disks and
-20M-point squares but not for on-circle inputs; the distributed sample sort /
-multi-select of SURVEY.md 8e is the planned replacement.
+device. Two paths, both exact:
+
+* ``sparse_sharded`` (default): every rank runs the sparse
+  round-2 pipeline (csrc/sparse.cuh) on its own shard through the
+  ``gscan_dist_*`` phases, and only small things move between ranks:
+
+  =====================  ==========================================  =========
+  exchange               what                                         size
+  =====================  ==========================================  =========
+  extremes               5 extreme points per rank (all-gather)       120 B
+  sample cells           pseudo-angle sample histogram (sum)          8 KB
+  bucket histogram       global ranks of every bucket (sum)           192 KB
+  farthest point P_l     best (dist2, index) record per rank          40 B
+  P_l's in-bucket rank   points of its bucket ordered before it       8 B
+  walk-angle maxima      per-bucket phi maximum (max) + phi range     384 KB
+  gathered points        buckets holding slice seeds -> rank 0        ~MBs
+  prefix maxima          candidate thresholds (rank 0 -> all)         384 KB
+  candidates             points the walk can keep -> rank 0           ~MBs
+  duplicate check        64-bit hashes, partition k -> rank k         8 B/pt
+  =====================  ==========================================  =========
+
+  Rank 0 then walks the gathered points and candidates exactly, certifies
+  the skipped points, and runs Graham. No rank ever holds another rank's
+  survivors, so 1B points scale.
+* the survivor gather (``survivor_gather``): K1/K2 per shard, then all
+  survivors to rank 0. It is the exact fallback whenever the sparse path
+  declines (tie for P_l, possible duplicates, a certificate that does not
+  hold, near-convex input, capacity).
+
+The collectives go through a small interface (``Comm``) so that the same
+orchestration runs under NCCL (``TorchComm``, one rank per process) or as R
+simulated ranks inside one process (``LocalComm``, used by the GPU tests on a
+single device).
 """
 from __future__ import annotations
 
@@ -26,9 +47,14 @@ import torch.distributed as dist
 from . import _native as N
 from .hull2d import Engine, PipelineConfig, StageStats
 
+_U32 = torch.int32  # uint32 payloads travel as int32 bit patterns
+_DBG = bool(int(__import__("os").environ.get("GSCAN_DIST_DEBUG", "0") or 0))
+
 
 def _combine(recs: np.ndarray) -> np.ndarray:
-    """recs: (R, 3, 5) = (global idx, x, y) per rank -> (3, 5) global extremes."""
+    """recs: (R, 3, 5) = (global idx, x, y) per rank -> (3, 5) global extremes
+    with the reference's tie rules (strict compares, lowest global index;
+    prefilter.hpp:28-39, angular.hpp:40-49)."""
     out = np.zeros((3, 5))
     R = recs.shape[0]
     for k in range(5):
@@ -56,22 +82,441 @@ def _combine(recs: np.ndarray) -> np.ndarray:
     return out
 
 
-def sharded_hull(eng: Engine, d_xs: torch.Tensor, d_ys: torch.Tensor, offset: int,
-                 cfg: PipelineConfig | None = None, group=None):
-    """Hull of the union of all ranks' shards. Returns (global indices as a
-    numpy uint64 array, StageStats) on rank 0 and (None, None) elsewhere."""
-    cfg = cfg or PipelineConfig()
+def _combine_best(recs) -> tuple[tuple | None, int]:
+    """Per-rank (d2_bits, global idx, ties, x, y) -> the global farthest point
+    (split_regions, angular.hpp:197-204: first maximal dist2 = lowest index
+    among equals) and the number of points at that distance."""
+    best, ties = None, 0
+    for d2, gi, t, x, y in recs:
+        if t == 0:
+            continue
+        if best is None or d2 > best[0]:
+            best, ties = (d2, gi, x, y), t
+        elif d2 == best[0]:
+            ties += t
+            if gi < best[1]:
+                best = (d2, gi, x, y)
+    return best, ties
+
+
+# ---------------------------------------------------------------------------
+# collectives
+class Comm:
+    """Collectives over R ranks. Every method takes one value per rank held by
+    this process (``len(local) == len(self.ranks)``) and returns one per rank."""
+
+    world: int
+    ranks: list[int]
+
+    def allreduce(self, ts: list[torch.Tensor], op: str) -> list[torch.Tensor]:
+        raise NotImplementedError
+
+    def allgather_obj(self, objs: list) -> list:
+        """-> the list of all R objects (same on every rank)."""
+        raise NotImplementedError
+
+    def gather_root(self, ts: list[torch.Tensor]) -> list[torch.Tensor] | None:
+        """Variable-length 1-D tensors -> rank 0 gets all R (rank order); others None."""
+        raise NotImplementedError
+
+    def bcast_root(self, t: torch.Tensor | None, like: list[torch.Tensor]) -> list[torch.Tensor]:
+        raise NotImplementedError
+
+    def all_to_all(self, sends: list[list[torch.Tensor]]) -> list[list[torch.Tensor]]:
+        """sends[k][r] from local rank k to rank r -> recv[k][s] from rank s."""
+        raise NotImplementedError
+
+
+class LocalComm(Comm):
+    """R simulated ranks in one process (tensors on one device)."""
+
+    def __init__(self, world: int):
+        self.world = world
+        self.ranks = list(range(world))
+
+    def allreduce(self, ts, op):
+        st = torch.stack(ts)
+        r = {"sum": lambda: st.sum(0, dtype=st.dtype), "max": lambda: st.max(0).values,
+             "min": lambda: st.min(0).values}[op]()
+        return [r.clone() for _ in ts]
+
+    def allgather_obj(self, objs):
+        return list(objs)
+
+    def gather_root(self, ts):
+        return [t.clone() for t in ts]
+
+    def bcast_root(self, t, like):
+        return [t.clone() for _ in like]
+
+    def all_to_all(self, sends):
+        return [[sends[s][r].clone() for s in range(self.world)] for r in range(self.world)]
+
+
+class TorchComm(Comm):
+    """torch.distributed (NCCL on GPUs, gloo on CPU): this process is one rank."""
+
+    _OPS = {"sum": dist.ReduceOp.SUM, "max": dist.ReduceOp.MAX, "min": dist.ReduceOp.MIN}
+
+    def __init__(self, group=None):
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.ranks = [self.rank]
+
+    def allreduce(self, ts, op):
+        (t,) = ts
+        t = t.clone()
+        dist.all_reduce(t, op=self._OPS[op], group=self.group)
+        return [t]
+
+    def allgather_obj(self, objs):
+        (o,) = objs
+        out = [None] * self.world
+        dist.all_gather_object(out, o, group=self.group)
+        return out
+
+    def gather_root(self, ts):
+        (t,) = ts
+        n = torch.tensor([t.numel()], dtype=torch.int64, device=t.device)
+        ns = torch.empty(self.world, dtype=torch.int64, device=t.device)
+        dist.all_gather_into_tensor(ns, n, group=self.group)
+        ns = ns.tolist()
+        mx = max(max(ns), 1)
+        pad = torch.zeros(mx, dtype=t.dtype, device=t.device)
+        pad[: t.numel()] = t
+        allp = torch.empty(self.world * mx, dtype=t.dtype, device=t.device)
+        dist.all_gather_into_tensor(allp, pad, group=self.group)
+        if self.rank != 0:
+            return None
+        return [allp[r * mx: r * mx + ns[r]].clone() for r in range(self.world)]
+
+    def bcast_root(self, t, like):
+        (ref,) = like
+        buf = t.clone() if self.rank == 0 else torch.empty_like(ref)
+        dist.broadcast(buf, 0, group=self.group)
+        return [buf]
+
+    def all_to_all(self, sends):
+        (row,) = sends
+        sizes = torch.tensor([x.numel() for x in row], dtype=torch.int64, device=row[0].device)
+        rsizes = torch.empty_like(sizes)
+        dist.all_to_all_single(rsizes, sizes, group=self.group)
+        rs = rsizes.tolist()
+        out = torch.empty(sum(rs), dtype=row[0].dtype, device=row[0].device)
+        dist.all_to_all_single(out, torch.cat(list(row)), output_split_sizes=rs,
+                               input_split_sizes=sizes.tolist(), group=self.group)
+        return [list(torch.split(out, rs))]
+
+
+# ---------------------------------------------------------------------------
+def _ck(eng: Engine, rc: int, what: str):
+    if rc:
+        eng._raise(rc, what)
+
+
+def _ready(dev) -> None:
+    """The phases run on the handle's own stream: tensors torch (or NCCL) just
+    wrote must be complete first."""
+    torch.cuda.synchronize(dev)
+
+
+def _extremes(engines, shards, offsets, comm: Comm) -> N.gscan_extremes:
+    recs = []
+    for eng, (dx, dy), off in zip(engines, shards, offsets):
+        ex = N.gscan_extremes()
+        _ready(dx.device)
+        _ck(eng, eng._lib.gscan_shard_extremes(eng.handle, C.c_void_p(dx.data_ptr()),
+                                               C.c_void_p(dy.data_ptr()), dx.numel(), C.byref(ex)),
+            "shard_extremes")
+        recs.append(np.array([[float(off + ex.idx[k]) for k in range(5)], list(ex.x), list(ex.y)]))
+    g = _combine(np.stack(comm.allgather_obj(recs)))
+    gex = N.gscan_extremes()
+    for k in range(5):
+        gex.idx[k] = int(g[0, k])
+        gex.x[k] = g[1, k]
+        gex.y[k] = g[2, k]
+    return gex
+
+
+last_decline = ""  # why the last sparse_sharded call declined (diagnostics)
+
+
+def _declined(why: str):
+    global last_decline
+    last_decline = why
+    return None
+
+
+def _agree(comm: Comm, local_ok: list[bool]) -> bool:
+    """Every rank's verdict -> one decision all ranks take together."""
+    return all(comm.allgather_obj(local_ok))
+
+
+def sparse_sharded(engines: list[Engine], shards, offsets: list[int], n_global: int,
+                   cfg: PipelineConfig, comm: Comm):
+    """The sharded sparse path. Returns ``(hull_global_indices, stats)`` on rank 0
+    and ``(None, None)`` elsewhere when it served the call, or ``None`` when it
+    declined (every rank then gets None and takes the survivor gather)."""
+    global last_decline
+    last_decline = ""
+    dev = shards[0][0].device
+    ccfg = cfg._c()
+    gex = _extremes(engines, shards, offsets, comm)
+    i32 = lambda n: torch.empty(n, dtype=_U32, device=dev)  # noqa: E731
+
+    # 1. sample cells -> sum
+    cells = []
+    for eng, (dx, dy), off in zip(engines, shards, offsets):
+        t = i32(N.SP_CELLS)
+        _ready(dev)
+        _ck(eng, eng._lib.gscan_dist_begin(eng.handle, C.c_void_p(dx.data_ptr()),
+                                           C.c_void_p(dy.data_ptr()), dx.numel(), off, C.byref(gex),
+                                           C.byref(ccfg), C.c_void_p(t.data_ptr())), "dist_begin")
+        cells.append(t)
+    cells = comm.allreduce(cells, "sum")
+
+    # 2. bucket histogram -> sum; farthest point -> best; round-1 survivors -> sum
+    hists, bests, n1s = [], [], []
+    for eng, cl in zip(engines, cells):
+        hst = i32(N.SP_BUCKETS)
+        b = N.gscan_dist_best()
+        n1 = C.c_uint64()
+        _ready(dev)
+        _ck(eng, eng._lib.gscan_dist_hist(eng.handle, C.c_void_p(cl.data_ptr()),
+                                          C.c_void_p(hst.data_ptr()), C.byref(b), C.byref(n1)),
+            "dist_hist")
+        hists.append(hst)
+        bests.append((int(b.d2_bits), int(b.idx), int(b.ties), float(b.x), float(b.y)))
+        n1s.append(int(n1.value))
+    hists = comm.allreduce(hists, "sum")
+    allb = comm.allgather_obj([(bb, n) for bb, n in zip(bests, n1s)])
+    best, ties = _combine_best([x[0] for x in allb])
+    n1 = sum(x[1] for x in allb)
+    fail = 0
+    if best is None:
+        fail |= N.SP_FAIL_FEW
+    elif ties != 1:
+        fail |= N.SP_FAIL_TIE
+    if n1 * 10 > n_global * 9:
+        fail |= N.SP_FAIL_MANY
+    if fail:
+        return _declined(f"P_l: fail bits {fail:#x} (no point, a tie, or >= 90% of the points survive round 1)")
+    pl = N.gscan_dist_best(best[0], best[1], ties, 0, best[2], best[3])
+
+    # 3. P_l's rank inside its bucket -> sum
+    lbs, fails = [], []
+    for eng, hst in zip(engines, hists):
+        lb, f = C.c_uint64(), C.c_uint32()
+        _ready(dev)
+        _ck(eng, eng._lib.gscan_dist_plan(eng.handle, C.c_void_p(hst.data_ptr()), C.byref(pl), 0,
+                                          C.byref(lb), C.byref(f)), "dist_plan")
+        lbs.append(int(lb.value))
+        fails.append(int(f.value))
+    allv = comm.allgather_obj([(a, b) for a, b in zip(lbs, fails)])
+    if any(x[1] for x in allv):
+        return _declined(f"ranking P_l: fail bits {[x[1] for x in allv]}")
+    l_below = sum(x[0] for x in allv)
+
+    # 4. F3: walk-angle maxima -> max, phi range -> min/max; gathered counts
+    phis, rng, ngs, fails = [], [], [], []
+    for eng in engines:
+        pm = i32(N.SP_BUCKETS)
+        pr = (C.c_uint32 * 2)()
+        ng, f = C.c_uint64(), C.c_uint32()
+        _ready(dev)
+        _ck(eng, eng._lib.gscan_dist_phi(eng.handle, l_below, C.c_void_p(pm.data_ptr()), pr,
+                                         C.byref(ng), C.byref(f)), "dist_phi")
+        phis.append(pm.to(torch.int64) & 0xFFFFFFFF)
+        rng.append((int(pr[0]), int(pr[1])))
+        ngs.append(int(ng.value))
+        fails.append(int(f.value))
+    allv = comm.allgather_obj([(a, b) for a, b in zip(rng, fails)])
+    if any(x[1] for x in allv):
+        return _declined(f"F3: fail bits {[x[1] for x in allv]}")
+    if _DBG:
+        print(f"[dist] n1={n1} l_below={l_below} n_g={ngs} hist_sum={int(hists[0].to(torch.int64).sum())}")
+    phi_lo = min(x[0][0] for x in allv)
+    phi_hi = max(x[0][1] for x in allv)
+    phis = comm.allreduce(phis, "max")
+
+    # duplicate check: this rank's hashes by partition; partition range k -> rank k
+    sends, cnts = [], []
+    for eng in engines:
+        pc = i32(N.SP_PARTS)
+        ptr, nh = C.c_uint64(), C.c_uint64()
+        _ready(dev)
+        _ck(eng, eng._lib.gscan_dist_dup_local(eng.handle, C.c_void_p(pc.data_ptr()), C.byref(ptr),
+                                               C.byref(nh)), "dist_dup_local")
+        parted = _wrap_u64(ptr.value, int(nh.value), dev)
+        pcl = pc.to(torch.int64)
+        bounds = [(k * N.SP_PARTS) // comm.world for k in range(comm.world + 1)]
+        offs = torch.zeros(N.SP_PARTS + 1, dtype=torch.int64, device=dev)
+        offs[1:] = torch.cumsum(pcl, 0)
+        row, crow = [], []
+        for k in range(comm.world):
+            a, b = int(offs[bounds[k]]), int(offs[bounds[k + 1]])
+            row.append(parted[a:b].clone())
+            crow.append(pc[bounds[k]:bounds[k + 1]].clone())
+        sends.append(row)
+        cnts.append(crow)
+    recv = comm.all_to_all(sends)
+    rcnt = comm.all_to_all(cnts)
+    dups = []
+    for li, eng in enumerate(engines):
+        k = comm.ranks[li]
+        lo, hi = (k * N.SP_PARTS) // comm.world, ((k + 1) * N.SP_PARTS) // comm.world
+        mat = torch.zeros((comm.world, N.SP_PARTS), dtype=_U32, device=dev)
+        for s in range(comm.world):
+            mat[s, lo:hi] = rcnt[li][s]
+        blob = torch.cat(recv[li]) if sum(x.numel() for x in recv[li]) else torch.zeros(1, dtype=torch.int64, device=dev)
+        nrecv = sum(x.numel() for x in recv[li])
+        d = C.c_uint32()
+        _ready(dev)
+        _ck(eng, eng._lib.gscan_dist_dup_check(eng.handle, C.c_void_p(blob.data_ptr()), nrecv,
+                                               C.c_void_p(mat.data_ptr()), comm.world, C.byref(d)),
+            "dist_dup_check")
+        dups.append(int(d.value))
+    if any(comm.allgather_obj(dups)):
+        return _declined("possible duplicate points (hash partition exchange)")
+
+    # 5. gathered points -> rank 0 (records {x, y, global index, bucket})
+    def export(candidates: int, counts):
+        out = []
+        for eng, cnt in zip(engines, counts):
+            xs = torch.empty(max(cnt, 1), dtype=torch.float64, device=dev)
+            ys = torch.empty_like(xs)
+            gi, gb = i32(max(cnt, 1)), i32(max(cnt, 1))
+            n = C.c_uint64()
+            _ready(dev)
+            _ck(eng, eng._lib.gscan_dist_export(eng.handle, candidates, C.c_void_p(xs.data_ptr()),
+                                                C.c_void_p(ys.data_ptr()), C.c_void_p(gi.data_ptr()),
+                                                C.c_void_p(gb.data_ptr()), C.byref(n)),
+                "dist_export")
+            k = int(n.value)
+            out.append((xs[:k], ys[:k], gi[:k].to(torch.int64) & 0xFFFFFFFF, gb[:k]))
+        return out
+
+    def to_root(recs):
+        parts = [comm.gather_root([r[j] for r in recs]) for j in range(4)]
+        if parts[0] is None:
+            return None
+        x = torch.cat(parts[0])
+        y = torch.cat(parts[1])
+        gi = torch.cat(parts[2])
+        gb = torch.cat(parts[3])
+        order = torch.argsort(gi)
+        return x[order], y[order], gi[order], gb[order]
+
+    groot = to_root(export(0, ngs))
+    if _DBG and groot is not None:
+        print(f"[dist] gathered at root {groot[0].numel()} unique idx {torch.unique(groot[2]).numel()}")
+    root = 0 in comm.ranks
+    r0 = comm.ranks.index(0) if root else None
+    pref = None
+    if root:
+        gx, gy, gg, gb = groot
+        n_g = int(gx.numel())
+        X = torch.cat([torch.tensor([gex.x[4]], dtype=torch.float64, device=dev), gx])
+        Y = torch.cat([torch.tensor([gex.y[4]], dtype=torch.float64, device=dev), gy])
+        lpos = int(torch.searchsorted(gg, torch.tensor([pl.idx], device=dev)).item())
+        eng0 = engines[r0]
+        if lpos < n_g and int(gg[lpos]) == pl.idx:  # P_l is a gathered point
+            pref = i32(N.SP_BUCKETS)
+            pr = (C.c_uint32 * 2)(phi_lo, phi_hi)
+            f = C.c_uint32()
+            pmx = phis[r0].to(_U32)
+            _ready(dev)
+            rc = eng0._lib.gscan_dist_slices(eng0.handle, C.c_void_p(X.data_ptr()),
+                                             C.c_void_p(Y.data_ptr()), n_g,
+                                             C.c_void_p(gb.data_ptr()), 1 + lpos,
+                                             C.c_void_p(pmx.data_ptr()), pr,
+                                             C.c_void_p(pref.data_ptr()), C.byref(f))
+            if rc == N.GSCAN_E_CAPACITY or (rc == 0 and f.value):
+                pref = None
+                _declined(f"dist_slices: rc {rc}, fail bits {f.value:#x}")
+            else:
+                _ck(eng0, rc, "dist_slices")
+    if not _agree(comm, [pref is not None if comm.ranks[k] == 0 else True
+                         for k in range(len(engines))]):
+        return _declined(last_decline or "rank 0 could not sort the gathered points")
+    prefs = comm.bcast_root(pref, [i32(N.SP_BUCKETS) for _ in engines])
+
+    # 6. candidates -> rank 0
+    ncs, fails = [], []
+    for eng, pm in zip(engines, prefs):
+        nc, f = C.c_uint64(), C.c_uint32()
+        _ready(dev)
+        _ck(eng, eng._lib.gscan_dist_cand(eng.handle, C.c_void_p(pm.data_ptr()), C.byref(nc),
+                                          C.byref(f)), "dist_cand")
+        ncs.append(int(nc.value))
+        fails.append(int(f.value))
+    allv = comm.allgather_obj([(a, b) for a, b in zip(ncs, fails)])
+    m_global = int(hists[0].to(torch.int64).sum())
+    if any(x[1] for x in allv) or sum(x[0] for x in allv) > max(m_global // 8, 65536):
+        return _declined(f"F4: fail bits {[x[1] for x in allv]}, candidates {sum(x[0] for x in allv)} of {m_global}")
+    croot = to_root(export(1, ncs))
+
+    # 7. rank 0: walk, certificate, Graham
+    result = None
+    if root:
+        cx, cy, cg, cb = croot
+        n_c = int(cx.numel())
+        X2 = torch.cat([X, cx])
+        Y2 = torch.cat([Y, cy])
+        gidx = torch.cat([torch.tensor([gex.idx[4]], dtype=torch.int64, device=dev), gg, cg])
+        hull = i32(max(1 + n_g + n_c, 1))
+        hn, nr, f = C.c_uint64(), C.c_uint64(), C.c_uint32()
+        _ready(dev)
+        rc = eng0._lib.gscan_dist_finish(eng0.handle, C.c_void_p(X2.data_ptr()),
+                                         C.c_void_p(Y2.data_ptr()), n_g, n_c,
+                                         C.c_void_p(cb.data_ptr()), C.c_void_p(hull.data_ptr()),
+                                         hull.numel(), C.byref(hn), C.byref(nr), C.byref(f))
+        if rc == N.GSCAN_E_CAPACITY or (rc == 0 and f.value):
+            result = None
+            _declined(f"dist_finish: rc {rc}, fail bits {f.value:#x}")
+        else:
+            _ck(eng0, rc, "dist_finish")
+            k = int(hn.value)
+            hv = gidx[hull[:k].to(torch.int64) & 0xFFFFFFFF].cpu().numpy().astype(np.uint64)
+            st = StageStats(n_input=n_global, n_after_round1=n1, n_after_round2=int(nr.value),
+                            hull_size=k)
+            result = (hv, st)
+    if not _agree(comm, [result is not None if comm.ranks[k] == 0 else True
+                         for k in range(len(engines))]):
+        return _declined(last_decline or "rank 0: walk, certificate or Graham declined")
+    return result if root else (None, None)
+
+
+class _DevBuf:
+    """__cuda_array_interface__ view of a device buffer owned by a handle."""
+
+    def __init__(self, ptr: int, n: int):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<i8", "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+def _wrap_u64(ptr: int, n: int, dev) -> torch.Tensor:
+    """n uint64 (as int64) at device address ptr, copied out of the handle."""
+    if n == 0:
+        return torch.zeros(0, dtype=torch.int64, device=dev)
+    return torch.as_tensor(_DevBuf(ptr, n), device=dev).clone()
+
+
+# ---------------------------------------------------------------------------
+def survivor_gather(eng: Engine, d_xs: torch.Tensor, d_ys: torch.Tensor, offset: int,
+                    cfg: PipelineConfig, comm: TorchComm):
+    """K1/K2 per shard, every survivor (x, y, global index) to rank 0, which runs
+    the rest with round 1 disabled (it already ran)."""
     lib = eng._lib
     n = int(d_xs.numel())
-    rank = dist.get_rank(group)
-    world = dist.get_world_size(group)
+    rank, world = comm.rank, comm.world
+    group = comm.group
     dev = d_xs.device
     if cfg.enable_round1:
         ex = N.gscan_extremes()
-        rc = lib.gscan_shard_extremes(eng.handle, C.c_void_p(d_xs.data_ptr()),
-                                      C.c_void_p(d_ys.data_ptr()), n, C.byref(ex))
-        if rc:
-            eng._raise(rc, "shard_extremes")
+        _ck(eng, lib.gscan_shard_extremes(eng.handle, C.c_void_p(d_xs.data_ptr()),
+                                          C.c_void_p(d_ys.data_ptr()), n, C.byref(ex)), "shard_extremes")
         mine = torch.tensor([[float(offset + ex.idx[k]) for k in range(5)], list(ex.x), list(ex.y)],
                             dtype=torch.float64, device=dev)
         allr = torch.empty((world, 3, 5), dtype=torch.float64, device=dev)
@@ -84,11 +529,9 @@ def sharded_hull(eng: Engine, d_xs: torch.Tensor, d_ys: torch.Tensor, offset: in
             gex.y[k] = g[2, k]
         surv = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
         n1 = C.c_uint64()
-        rc = lib.gscan_shard_round1(eng.handle, C.c_void_p(d_xs.data_ptr()),
-                                    C.c_void_p(d_ys.data_ptr()), n, C.byref(gex),
-                                    C.c_void_p(surv.data_ptr()), C.byref(n1))
-        if rc:
-            eng._raise(rc, "shard_round1")
+        _ck(eng, lib.gscan_shard_round1(eng.handle, C.c_void_p(d_xs.data_ptr()),
+                                        C.c_void_p(d_ys.data_ptr()), n, C.byref(gex),
+                                        C.c_void_p(surv.data_ptr()), C.byref(n1)), "shard_round1")
         loc = surv[: n1.value].long()
         sx, sy = d_xs[loc], d_ys[loc]
         sg = loc + offset
@@ -122,3 +565,37 @@ def sharded_hull(eng: Engine, d_xs: torch.Tensor, d_ys: torch.Tensor, offset: in
     hull_global = gidx[out[:k].long()].cpu().numpy().astype(np.uint64)
     stats = StageStats(**{**st.__dict__, "n_input": n_global})
     return hull_global, stats
+
+
+def _default_toggles(cfg: PipelineConfig) -> bool:
+    return cfg.enable_round1 and cfg.enable_round2 and cfg.chunked
+
+
+def sharded_hull(eng: Engine, d_xs: torch.Tensor, d_ys: torch.Tensor, offset: int,
+                 cfg: PipelineConfig | None = None, group=None):
+    """Hull of the union of all ranks' shards. Returns (global indices as a
+    numpy uint64 array, StageStats) on rank 0 and (None, None) elsewhere."""
+    cfg = cfg or PipelineConfig()
+    comm = TorchComm(group)
+    n = int(d_xs.numel())
+    sizes = comm.allgather_obj([n])
+    n_global = sum(sizes)
+    if _default_toggles(cfg) and n_global >= 65536 and min(sizes) > 0 and d_xs.is_cuda:
+        res = sparse_sharded([eng], [(d_xs, d_ys)], [offset], n_global, cfg, comm)
+        if res is not None:
+            return res
+    return survivor_gather(eng, d_xs, d_ys, offset, cfg, comm)
+
+
+def simulate_sharded(engines: list[Engine], xs: torch.Tensor, ys: torch.Tensor,
+                     cfg: PipelineConfig | None = None):
+    """All R ranks in this process on one device (LocalComm): the sharded
+    sparse path exactly as R GPUs would run it. Returns (indices, stats) or
+    None when it declined."""
+    cfg = cfg or PipelineConfig()
+    R = len(engines)
+    n = int(xs.numel())
+    offs = [n * r // R for r in range(R + 1)]
+    shards = [(xs[offs[r]:offs[r + 1]].contiguous(), ys[offs[r]:offs[r + 1]].contiguous())
+              for r in range(R)]
+    return sparse_sharded(engines, shards, offs[:R], n, cfg, LocalComm(R))

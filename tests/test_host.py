@@ -181,3 +181,63 @@ def test_sharded_extremes_exchange_gloo(tmp_path):
     for p, (o, e) in zip(procs, outs):
         assert p.returncode == 0, e[-2000:]
         assert "ok" in o
+
+
+COMM_SCRIPT = r"""
+import sys
+sys.path.insert(0, sys.argv[1])
+import torch, torch.distributed as dist
+from paper_1508_05931_b200.distributed import LocalComm, TorchComm, _combine_best
+dist.init_process_group("gloo", init_method="tcp://127.0.0.1:%s" % sys.argv[2],
+                        rank=int(sys.argv[3]), world_size=2)
+r = dist.get_rank()
+tc, lc = TorchComm(), LocalComm(2)
+# what every rank holds, as LocalComm sees all of them at once
+vals = [torch.tensor([1, -5, 7 + k, 2 ** 31 - 1 - k], dtype=torch.int32) for k in range(2)]
+for op in ("sum", "max", "min"):
+    want = lc.allreduce(vals, op)[0]
+    got = tc.allreduce([vals[r]], op)[0]
+    assert got.dtype == torch.int32 and torch.equal(got, want), (op, got, want)
+objs = [("rank", k, [k] * k) for k in range(2)]
+assert tc.allgather_obj([objs[r]]) == lc.allgather_obj(objs)
+var = [torch.arange(3 + 5 * k, dtype=torch.float64) * (k + 1) for k in range(2)]
+got = tc.gather_root([var[r]])
+if r == 0:
+    assert all(torch.equal(a, b) for a, b in zip(got, lc.gather_root(var)))
+else:
+    assert got is None
+b = tc.bcast_root(var[0] if r == 0 else None, [torch.empty_like(var[0])])[0]
+assert torch.equal(b, var[0])
+sends = [[torch.full((2 + s + 3 * d,), 10 * s + d, dtype=torch.int64) for d in range(2)] for s in range(2)]
+got = tc.all_to_all([sends[r]])[0]
+want = lc.all_to_all(sends)[r]
+assert all(torch.equal(a, b) for a, b in zip(got, want)), (got, want)
+# farthest-point combination: lowest global index among equal dist2, ties summed
+best, ties = _combine_best([(5, 9, 1, 0.0, 0.0), (5, 4, 2, 1.0, 1.0), (3, 1, 1, 2.0, 2.0), (0, 0, 0, 0, 0)])
+assert best == (5, 4, 1.0, 1.0) and ties == 3, (best, ties)
+dist.barrier()
+dist.destroy_process_group()
+print("ok", r)
+"""
+
+
+def test_torch_comm_matches_local_comm_gloo(tmp_path):
+    """The sharded sparse path's collectives (distributed.py TorchComm, the
+    NCCL path) agree with the in-process LocalComm the GPU tests use:
+    dtype-preserving reductions, object all-gather, variable-length gather
+    to rank 0, broadcast, variable-size all-to-all. gloo, world_size 2."""
+    script = tmp_path / "c.py"
+    script.write_text(COMM_SCRIPT)
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    procs = [subprocess.Popen([sys.executable, str(script), str(ROOT), str(port), str(r)],
+                              stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)
+             for r in range(2)]
+    outs = [p.communicate(timeout=240) for p in procs]
+    for p, (o, e) in zip(procs, outs):
+        assert p.returncode == 0, e[-3000:]
+        assert "ok" in o
