@@ -78,3 +78,47 @@ def test_sharded_near_circle_declines(engines, oracle_mod):
 
     xs, ys = generate("circle", 300_000, 3)
     assert _check(engines, oracle_mod, xs, ys, 3) is None
+
+
+NCCL_SCRIPT = r"""
+import os, sys
+sys.path.insert(0, sys.argv[1])
+import numpy as np, torch, torch.distributed as dist
+import oracle
+from paper_1508_05931_b200 import Engine, PipelineConfig, generate
+from paper_1508_05931_b200 import distributed as D
+torch.cuda.set_device(0)
+dist.init_process_group("nccl", init_method="tcp://127.0.0.1:%s" % sys.argv[2], rank=0, world_size=1)
+xs, ys = generate("square", 500_000, 21)
+eng = Engine(0)
+dx, dy = torch.from_numpy(xs).cuda(), torch.from_numpy(ys).cuda()
+got, st = D.sharded_hull(eng, dx, dy, 0, PipelineConfig())
+assert D.last_decline == "", D.last_decline
+want, sw = oracle.full_pipeline(xs, ys)
+assert np.array_equal(got, want)
+assert st.n_after_round2 == sw["n_after_round2"] and st.hull_size == sw["hull_size"]
+dist.destroy_process_group()
+print("ok")
+"""
+
+
+def test_sharded_hull_over_nccl(tmp_path):
+    """sharded_hull through TorchComm on a 1-rank NCCL group: every collective
+    of the multi-GPU run (all_gather_object, all_reduce, all_gather_into_tensor,
+    broadcast, all_to_all_single) on CUDA tensors, and the sparse path serves."""
+    import socket
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    script = tmp_path / "n.py"
+    script.write_text(NCCL_SCRIPT)
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    root = Path(__file__).resolve().parents[1]
+    p = subprocess.run([sys.executable, str(script), str(root), str(port)], capture_output=True,
+                       text=True, timeout=300)
+    assert p.returncode == 0, p.stderr[-3000:]
+    assert "ok" in p.stdout
