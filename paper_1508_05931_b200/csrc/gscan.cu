@@ -915,7 +915,7 @@ int sparse_init(gscan_handle* h) {
   CU(cudaMalloc(&h->sp_hist_part, (size_t)G * nb * 4));
   CU(cudaMalloc(&h->sp_phi_part, (size_t)G * nb * 4));
   CU(cudaMalloc(&h->sp_part_off, ((size_t)2 * G * kSpParts + 1) * 4));
-  CU(cudaMalloc(&h->sp_d2, G * sizeof(SpD2)));
+  CU(cudaMalloc(&h->sp_d2, 2 * G * sizeof(SpD2)));
   uint32_t** nb_bufs[] = {&h->sp_hist, &h->sp_bstart, &h->sp_glist, &h->sp_gcnt, &h->sp_phimax,
                           &h->sp_prefmax, &h->sp_slice, &h->sp_ccnt, &h->sp_cstart, &h->sp_wcnt,
                           &h->sp_wstart, &h->sp_rlo};
@@ -939,6 +939,10 @@ int rec_event(gscan_handle* h, cudaEvent_t e, cudaStream_t s) {
 // The sparse path as segments over one context. sparse_enqueue runs them all
 // in order (one device, one CUDA graph); the sharded path (gscan_dist_*) runs
 // them per rank with the collectives of SURVEY.md 8e in between.
+// F2 without its shared-memory histogram (two CTAs per SM) + a histogram
+// pass over the codes
+constexpr bool kF2Split = true;
+
 struct SpCtx {
   const double* xs;
   const double* ys;
@@ -1011,12 +1015,22 @@ int sp_seg_f2(gscan_handle* h, const SpCtx& c) {
     Launch L(h, "k_sp_theta", s);
     k_sp_theta<<<(c.nb + 1 + 255) / 256, 256, 0, s>>>(h->sp_cdf, h->sp_th, h->sp_st);
   }
+  const uint32_t g2 = kF2Split ? 2 * c.G : c.G;  // F2 CTAs (d2 partials)
   {
     Launch L(h, "k_sp_hist", s);
 #define A2 c.xs, c.ys, c.n, h->ext, h->sp_cdf, h->sp_th, h->sp_codes, h->sp_hist_part, h->sp_d2, h->ctr
-    if (c.vec) k_sp_hist<true><<<c.G, kSpThreads, c.smem_nb, s>>>(A2);
-    else k_sp_hist<false><<<c.G, kSpThreads, c.smem_nb, s>>>(A2);
+    if (kF2Split) {
+      if (c.vec) k_sp_hist<true, false><<<g2, kSpThreads, 0, s>>>(A2);
+      else k_sp_hist<false, false><<<g2, kSpThreads, 0, s>>>(A2);
+    } else {
+      if (c.vec) k_sp_hist<true, true><<<g2, kSpThreads, c.smem_nb, s>>>(A2);
+      else k_sp_hist<false, true><<<g2, kSpThreads, c.smem_nb, s>>>(A2);
+    }
 #undef A2
+  }
+  if (kF2Split) {
+    Launch L(h, "k_sp_hist_codes", s);
+    k_sp_hist_codes<<<c.G, 1024, c.smem_nb, s>>>(h->sp_codes, c.n, h->sp_hist_part);
   }
   {
     Launch L(h, "k_sp_check_r1", s);
@@ -1028,7 +1042,7 @@ int sp_seg_f2(gscan_handle* h, const SpCtx& c) {
   }
   {
     Launch L(h, "k_sp_plan_pl", s);
-    k_sp_plan_pl<<<1, 256, 0, s>>>(c.xs, c.ys, h->sp_d2, c.G, h->sp_st);
+    k_sp_plan_pl<<<1, 256, 0, s>>>(c.xs, c.ys, h->sp_d2, g2, h->sp_st);
   }
   return GSCAN_OK;
 }
@@ -1603,8 +1617,9 @@ int gscan_create(int device, gscan_handle** out) {
     CU(cudaFuncSetAttribute(k_bucket_sort_cta, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             kSortCap * (8 + 8 + 4 + 4)));
     const int nbs = (int)(kSpBuckets * 4);
-    CU(cudaFuncSetAttribute(k_sp_hist<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, nbs));
-    CU(cudaFuncSetAttribute(k_sp_hist<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, nbs));
+    CU(cudaFuncSetAttribute(k_sp_hist<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, nbs));
+    CU(cudaFuncSetAttribute(k_sp_hist<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, nbs));
+    CU(cudaFuncSetAttribute(k_sp_hist_codes, cudaFuncAttributeMaxDynamicSharedMemorySize, nbs));
     CU(cudaFuncSetAttribute(k_sp_phi<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, nbs));
     CU(cudaFuncSetAttribute(k_sp_phi<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, nbs));
     CU(cudaFuncSetAttribute(k_sp_cand, cudaFuncAttributeMaxDynamicSharedMemorySize, nbs));

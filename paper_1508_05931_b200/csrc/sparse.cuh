@@ -447,7 +447,7 @@ __global__ void k_sp_reduce_cols(const uint32_t* __restrict__ part, uint32_t row
 // pseudo-angle, CDF lookup) so the independent FP64 chains interleave; only
 // the rare guard-band case branches (sp_bucket's exact fallback). Same
 // arithmetic, same result as visiting the points one by one.
-template <int B>
+template <int B, bool kHist>
 __device__ __forceinline__ void f2_batch(const double (&x)[B], const double (&y)[B],
                                          const uint32_t (&idx)[B], uint32_t (&code)[B],
                                          const SpQuad& q, const double* s_cdf,
@@ -496,7 +496,7 @@ __device__ __forceinline__ void f2_batch(const double (&x)[B], const double (&y)
       while (b + 1 < kSpBuckets && a >= th[b + 1]) ++b;
     }
     code[k] = b;
-    atomicAdd(&s_hist[b], 1u);
+    if (kHist) atomicAdd(&s_hist[b], 1u);
     const uint64_t d2 = dbits(dist2_rn(dx[k], dy[k]));
     const uint32_t i = idx[k];
     if (bidx == 0xffffffffu || d2 > bd2) { bd2 = d2; bidx = i; bties = 1; }
@@ -509,15 +509,18 @@ __device__ __forceinline__ void f2_batch(const double (&x)[B], const double (&y)
 // The quad test is classify_quad (prefilter.hpp:47-63); n_after_round1 counts
 // every survivor (pipeline.hpp:93); points equal to the anchor leave the
 // buffer (annotate, angular.hpp:118-133) and are not bucketed.
-template <bool kVec>
-__global__ void __launch_bounds__(kSpThreads, 1) k_sp_hist(
+// kHist = false: no shared-memory histogram (the codes are counted by
+// k_sp_hist_codes), so two CTAs fit an SM.
+template <bool kVec, bool kHist>
+__global__ void __launch_bounds__(kSpThreads, kHist ? 1 : 2) k_sp_hist(
     const double* __restrict__ xs, const double* __restrict__ ys, uint32_t n,
     const ExtResult* __restrict__ ext, const double* __restrict__ cdf,
     const double* __restrict__ th, uint16_t* __restrict__ codes, uint32_t* __restrict__ hist_part,
     SpD2* __restrict__ d2part, Counters* __restrict__ ctr) {
-  extern __shared__ uint32_t s_hist[];  // kSpBuckets
+  extern __shared__ uint32_t s_hist[];  // kSpBuckets (kHist)
   __shared__ double s_cdf[kSpCells + 1];
-  for (uint32_t b = threadIdx.x; b < kSpBuckets; b += blockDim.x) s_hist[b] = 0;
+  if (kHist)
+    for (uint32_t b = threadIdx.x; b < kSpBuckets; b += blockDim.x) s_hist[b] = 0;
   for (uint32_t j = threadIdx.x; j <= kSpCells; j += blockDim.x) s_cdf[j] = cdf[j];
   SpQuad q;
   load_quad(ext, q);
@@ -530,7 +533,7 @@ __global__ void __launch_bounds__(kSpThreads, 1) k_sp_hist(
     if (x == q.ax && y == q.ay) return kSpNoCode;
     const double dx = __dsub_rn(x, q.ax), dy = __dsub_rn(y, q.ay);
     const uint32_t b = sp_bucket(dx, dy, s_cdf, th);
-    atomicAdd(&s_hist[b], 1u);
+    if (kHist) atomicAdd(&s_hist[b], 1u);
     const uint64_t d2 = dbits(dist2_rn(dx, dy));
     if (bidx == 0xffffffffu || d2 > bd2) { bd2 = d2; bidx = i; bties = 1; }
     else if (d2 == bd2) { ++bties; if (i < bidx) bidx = i; }
@@ -545,7 +548,7 @@ __global__ void __launch_bounds__(kSpThreads, 1) k_sp_hist(
       uint32_t* c2 = reinterpret_cast<uint32_t*>(codes);
       const uint32_t np = n / 2;
       uint32_t p = tid;
-      constexpr int kP = 4;
+      constexpr int kP = kHist ? 4 : 2;  // the split variant runs twice the warps
       for (; p + (kP - 1) * nth < np; p += kP * nth) {
         double2 vx[kP], vy[kP];
 #pragma unroll
@@ -553,16 +556,29 @@ __global__ void __launch_bounds__(kSpThreads, 1) k_sp_hist(
           vx[u] = __ldcs(&x2[p + u * nth]);
           vy[u] = __ldcs(&y2[p + u * nth]);
         }
+        if (kHist) {
 #pragma unroll
-        for (int g = 0; g < kP; g += 2) {  // batches of 4 points (8 measured slower)
-          const double bx[4] = {vx[g].x, vx[g].y, vx[g + 1].x, vx[g + 1].y};
-          const double by[4] = {vy[g].x, vy[g].y, vy[g + 1].x, vy[g + 1].y};
-          const uint32_t i0 = 2 * (p + g * nth), i1 = 2 * (p + (g + 1) * nth);
-          const uint32_t bi[4] = {i0, i0 + 1, i1, i1 + 1};
-          uint32_t bc[4];
-          f2_batch<4>(bx, by, bi, bc, q, s_cdf, th, s_hist, n1, bd2, bidx, bties);
-          c2[p + g * nth] = bc[0] | (bc[1] << 16);
-          c2[p + (g + 1) * nth] = bc[2] | (bc[3] << 16);
+          for (int g = 0; g < kP; g += 2) {  // batches of 4 points (8 measured slower)
+            const double bx[4] = {vx[g].x, vx[g].y, vx[g + 1].x, vx[g + 1].y};
+            const double by[4] = {vy[g].x, vy[g].y, vy[g + 1].x, vy[g + 1].y};
+            const uint32_t i0 = 2 * (p + g * nth), i1 = 2 * (p + (g + 1) * nth);
+            const uint32_t bi[4] = {i0, i0 + 1, i1, i1 + 1};
+            uint32_t bc[4];
+            f2_batch<4, kHist>(bx, by, bi, bc, q, s_cdf, th, s_hist, n1, bd2, bidx, bties);
+            c2[p + g * nth] = bc[0] | (bc[1] << 16);
+            c2[p + (g + 1) * nth] = bc[2] | (bc[3] << 16);
+          }
+        } else {
+#pragma unroll
+          for (int g = 0; g < kP; ++g) {  // 2-point batches: 64 registers
+            const double bx[2] = {vx[g].x, vx[g].y};
+            const double by[2] = {vy[g].x, vy[g].y};
+            const uint32_t i0 = 2 * (p + g * nth);
+            const uint32_t bi[2] = {i0, i0 + 1};
+            uint32_t bc[2];
+            f2_batch<2, kHist>(bx, by, bi, bc, q, s_cdf, th, s_hist, n1, bd2, bidx, bties);
+            c2[p + g * nth] = bc[0] | (bc[1] << 16);
+          }
         }
       }
       for (; p < np; p += nth) {
@@ -605,6 +621,34 @@ __global__ void __launch_bounds__(kSpThreads, 1) k_sp_hist(
     d2part[blockIdx.x] = SpD2{bd2, bidx, bidx == 0xffffffffu ? 0u : bties};
     if (tot) atomicAdd(&ctr->n1, tot);
   }
+  if (kHist) {
+    uint32_t* hp = hist_part + (size_t)blockIdx.x * kSpBuckets;
+    for (uint32_t b = threadIdx.x; b < kSpBuckets; b += blockDim.x) hp[b] = s_hist[b];
+  }
+}
+
+// Bucket histogram from F2's codes (2 B/pt): per-CTA shared-memory counts.
+__global__ void __launch_bounds__(1024, 1) k_sp_hist_codes(const uint16_t* __restrict__ codes,
+                                                           uint32_t n, uint32_t* __restrict__ hist_part) {
+  extern __shared__ uint32_t s_hist[];  // kSpBuckets
+  for (uint32_t b = threadIdx.x; b < kSpBuckets; b += blockDim.x) s_hist[b] = 0;
+  __syncthreads();
+  const uint4* c8 = reinterpret_cast<const uint4*>(codes);  // 8 codes per 16 B
+  const uint32_t n8 = n / 8;
+  const uint32_t nth = gridDim.x * blockDim.x;
+  for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < n8; p += nth) {
+    const uint4 v = __ldcs(&c8[p]);
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t lo = w[k] & 0xffffu, hi = w[k] >> 16;
+      if (lo != kSpNoCode) atomicAdd(&s_hist[lo], 1u);
+      if (hi != kSpNoCode) atomicAdd(&s_hist[hi], 1u);
+    }
+  }
+  for (uint32_t i = n8 * 8 + blockIdx.x * blockDim.x + threadIdx.x; i < n; i += nth)
+    if (codes[i] != kSpNoCode) atomicAdd(&s_hist[codes[i]], 1u);
+  __syncthreads();
   uint32_t* hp = hist_part + (size_t)blockIdx.x * kSpBuckets;
   for (uint32_t b = threadIdx.x; b < kSpBuckets; b += blockDim.x) hp[b] = s_hist[b];
 }
