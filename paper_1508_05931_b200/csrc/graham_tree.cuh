@@ -40,7 +40,9 @@
 
 namespace gscan {
 
-constexpr int kTreeChunk = 32;      // chunk length on every level
+constexpr int kTreeChunk = 32;      // chunk length on levels >= 1
+constexpr int kTreeChunk0 = 16;     // level 0 (the buffer): the widest level and the certificate
+__host__ __device__ constexpr uint32_t tree_cs(int j) { return j == 0 ? kTreeChunk0 : kTreeChunk; }
 constexpr int kTreeThreads = 256;   // the middle CTA; chunks are processed in waves of this many
 constexpr uint32_t kTreeTop = 128;       // levels stop shrinking once this small
 constexpr uint32_t kTreeTopMax = 3072;   // largest top level (a level that stops
@@ -340,7 +342,7 @@ __device__ __forceinline__ TreeLevel tree_level(const TreeWork& w, int j, uint32
   L.bt = w.bt[j];
   L.rec = w.rec[j];
   L.nq = nq;
-  L.nch = (nq + kTreeChunk - 1) / kTreeChunk;
+  L.nch = (nq + tree_cs(j) - 1) / tree_cs(j);
   return L;
 }
 
@@ -372,10 +374,10 @@ __global__ void __launch_bounds__(kTreeCta) k_gr_up(int j, const double* __restr
   const TreeRows<kTreeCta> r(tsm);
   if (info[0]) return;
   const uint32_t nq = tree_nq(info, j);
-  for (uint32_t c = blockIdx.x * kTreeCta + threadIdx.x; c * kTreeChunk < nq;
-       c += gridDim.x * kTreeCta) {
-    const uint32_t lo = c * kTreeChunk;
-    const int cnt = (int)min((uint32_t)kTreeChunk, nq - lo);
+  const uint32_t cs = tree_cs(j);
+  for (uint32_t c = blockIdx.x * kTreeCta + threadIdx.x; c * cs < nq; c += gridDim.x * kTreeCta) {
+    const uint32_t lo = c * cs;
+    const int cnt = (int)min(cs, nq - lo);
     if (j == 0) tree_stage<kTreeCta>(r, nullptr, R_x, R_y, lo, cnt);
     else tree_stage<kTreeCta>(r, w.Qp[j], w.Qx[j], w.Qy[j], lo, cnt);
     uint32_t B = kNone;
@@ -394,7 +396,7 @@ __global__ void __launch_bounds__(1024) k_gr_scan(int j, TreeWork w, uint32_t* _
   __shared__ uint32_t s_carry;
   if (info[0]) return;
   const uint32_t nq = tree_nq(info, j);
-  const uint32_t nch = (nq + kTreeChunk - 1) / kTreeChunk;
+  const uint32_t nch = (nq + tree_cs(j) - 1) / tree_cs(j);
   const uint32_t total = tree_scan(w.off[j], nch, s_w, &s_carry);
   if (threadIdx.x == 0) {
     w.off[j][nch] = total;
@@ -413,7 +415,7 @@ __global__ void __launch_bounds__(1024) k_gr_scan(int j, TreeWork w, uint32_t* _
 __device__ __forceinline__ void tree_gather_chunk(const TreeWork& w, int j, uint32_t c) {
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t o = w.off[j][c], ln = w.off[j][c + 1] - o;
-  const uint32_t s = c * kTreeChunk + lane;
+  const uint32_t s = c * tree_cs(j) + lane;
   if (lane < ln) {
     const uint32_t q = w.chainq[s], p = w.chainp[s];
     const double x = w.chainx[s], y = w.chainy[s];
@@ -427,7 +429,7 @@ __device__ __forceinline__ void tree_gather_chunk(const TreeWork& w, int j, uint
 __global__ void __launch_bounds__(256) k_gr_gather(int j, TreeWork w,
                                                   const uint32_t* __restrict__ info) {
   if (info[0]) return;
-  const uint32_t nch = (tree_nq(info, j) + kTreeChunk - 1) / kTreeChunk;
+  const uint32_t nch = (tree_nq(info, j) + tree_cs(j) - 1) / tree_cs(j);
   for (uint32_t c = blockIdx.x * 8 + (threadIdx.x >> 5); c < nch; c += gridDim.x * 8)
     tree_gather_chunk(w, j, c);
 }
@@ -550,7 +552,29 @@ __global__ void __launch_bounds__(kTreeThreads, 1) k_gr_mid(
       s_y[k] = tl.Qy[k];
     }
     __syncthreads();
-    if (t < 32) {
+    if (nk <= kTreeTop && t == 0) {  // small (pop-heavy) top level: one thread is faster
+      int top = 0;
+      double s1x = 0, s1y = 0, s2x = 0, s2y = 0;
+      for (uint32_t k = 0; k < nk; ++k) {
+        const double px = s_x[k], py = s_y[k];
+        while (top >= 2 && !left_turn(s2x, s2y, s1x, s1y, px, py)) {
+          --top;
+          s1x = s2x; s1y = s2y;
+          if (top >= 2) { s2x = st_x[top - 2]; s2y = st_y[top - 2]; }
+        }
+        s_par[k] = top ? st_i[top - 1] : kNone;
+        st_x[top] = px;
+        st_y[top] = py;
+        st_i[top++] = k;
+        s2x = s1x; s2y = s1y;
+        s1x = px; s1y = py;
+      }
+      for (int k = 0; k < top; ++k) w.fstack[k] = s_p[st_i[k]];
+      info[1] = (uint32_t)top;
+      const uint32_t ftop = top ? s_p[st_i[top - 1]] : kNone;
+      for (int j = 0; j < K; ++j) w.bt[j][(s_nq[j] + tree_cs(j) - 1) / tree_cs(j)] = ftop;
+    }
+    if (nk > kTreeTop && t < 32) {
       const int lane = t;
       int top = 0;
       int i = 0;
@@ -609,7 +633,7 @@ __global__ void __launch_bounds__(kTreeThreads, 1) k_gr_mid(
         info[1] = (uint32_t)top;
         // every level's boundary after its last chunk holds the final top
         const uint32_t ftop = top ? s_p[st_i[top - 1]] : kNone;
-        for (int j = 0; j < K; ++j) w.bt[j][(s_nq[j] + kTreeChunk - 1) / kTreeChunk] = ftop;
+        for (int j = 0; j < K; ++j) w.bt[j][(s_nq[j] + tree_cs(j) - 1) / tree_cs(j)] = ftop;
       }
     }
     __syncthreads();
@@ -617,8 +641,8 @@ __global__ void __launch_bounds__(kTreeThreads, 1) k_gr_mid(
       const uint32_t below = s_par[k];
       w.parent[s_p[k]] = below != kNone ? s_p[below] : kNone;
       // boundaries b in (chunk(k - 1), chunk(k)] start at element k
-      const uint32_t ch = tl.up[k] / kTreeChunk;
-      const uint32_t b0 = k ? tl.up[k - 1] / kTreeChunk + 1 : 0;
+      const uint32_t ch = tl.up[k] / tree_cs(K - 1);
+      const uint32_t b0 = k ? tl.up[k - 1] / tree_cs(K - 1) + 1 : 0;
       for (uint32_t b = b0; b <= ch; ++b) bk[b] = k ? k - 1 : kNone;
       if (k + 1 == nk)
         for (uint32_t b = ch + 1; b <= ll.nch; ++b) bk[b] = k;
@@ -684,12 +708,12 @@ __global__ void __launch_bounds__(kTreeCta) k_gr_cert(const double* __restrict__
   const TreeRows<kTreeCta> r(tsm);
   if (info[0]) return;
   const uint32_t N = info[4];
-  const uint32_t nch0 = (N + kTreeChunk - 1) / kTreeChunk;
+  const uint32_t nch0 = (N + kTreeChunk0 - 1) / kTreeChunk0;
   const uint32_t* bt = w.bt[0];
   uint32_t fails = 0;
   for (uint32_t c = blockIdx.x * kTreeCta + threadIdx.x; c < nch0; c += gridDim.x * kTreeCta) {
-    const uint32_t lo = c * kTreeChunk;
-    const int cnt = (int)min((uint32_t)kTreeChunk, N - lo);
+    const uint32_t lo = c * kTreeChunk0;
+    const int cnt = (int)min((uint32_t)kTreeChunk0, N - lo);
     tree_stage<kTreeCta>(r, nullptr, R_x, R_y, lo, cnt);
     uint32_t B;
     const int n0 = tree_load_rec<kTreeCta>(r, w.rec[0], c, B);
@@ -749,7 +773,7 @@ __global__ void __launch_bounds__(1024) k_gr_emit(const double* __restrict__ R_x
     ctr->hull = top;
     return;
   }
-  const uint32_t nch0 = (N + kTreeChunk - 1) / kTreeChunk;
+  const uint32_t nch0 = (N + kTreeChunk0 - 1) / kTreeChunk0;
   const uint32_t len = info[1], ftop = w.bt[0][nch0];
   bool ok = len > 0 && w.fstack[len - 1] == ftop;
   for (uint32_t k = t; k < len && ok; k += blockDim.x)

@@ -650,7 +650,7 @@ int tree_workspace(gscan_handle* h, uint32_t n_max) {
   for (int j = 1; j <= kTreeMaxLevels; ++j)
     caps[j] = std::min<uint64_t>((j == 1 ? (uint64_t)N * 17 / 20 : caps[j - 1] * 9 / 10) + 64,
                                  kTreeHiCap);
-  auto nchunks = [&](int j) { return caps[j] / kTreeChunk + 2; };
+  auto nchunks = [&](int j) { return caps[j] / tree_cs(j) + 2; };
   uint64_t need = 8ull * N + kTreeTopMax + 64 * 8;  // parent, tmp, chainq/p, chainx/y, fstack
   for (int j = 0; j <= kTreeMaxLevels; ++j) {
     if (j >= 1) need += 6 * caps[j] + 4 * 32;                // Qp, Qx, Qy, up
@@ -702,7 +702,7 @@ int tree_enqueue(gscan_handle* h, const double* Rx, const double* Ry, const uint
                  cudaStream_t s) {
   const TreeWork& w = h->tw;
   uint32_t* info = h->g_misc + 4;
-  const uint32_t nch0 = (h->tw_nmax + kTreeChunk - 1) / kTreeChunk;  // upper bounds
+  const uint32_t nch0 = (h->tw_nmax + kTreeChunk0 - 1) / kTreeChunk0;  // upper bounds
   const uint32_t gmax = 4 * (uint32_t)h->sm_count;
   const uint32_t g0 = std::min((nch0 + kTreeCta - 1) / kTreeCta, gmax);
   const uint32_t g1 = std::min((h->tw_nch1 + kTreeCta - 1) / kTreeCta, gmax);

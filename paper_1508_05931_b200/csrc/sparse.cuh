@@ -1672,22 +1672,49 @@ __global__ void __launch_bounds__(kSpCandThreads, 1) k_sp_cand(
   };
   const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
   const uint32_t nth = gridDim.x * blockDim.x;
+  const uint32_t lane = threadIdx.x & 31;
   const uint32_t* c2 = reinterpret_cast<const uint32_t*>(codes);
   const float2* p2 = reinterpret_cast<const float2*>(phi32);
   const uint32_t np = n / 2;
   uint32_t p = tid;
-  for (; p + 3 * nth < np; p += 4 * nth) {
+  // main loop, warp-uniform bound: 8 points per thread are tested first; a
+  // warp without a candidate (the common case) claims nothing
+  for (; (p - lane) + 31 + 3 * nth < np; p += 4 * nth) {
     uint32_t vc[4];
     float2 vp[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) vc[u] = __ldcs(&c2[p + u * nth]);
 #pragma unroll
     for (int u = 0; u < 4; ++u) vp[u] = __ldcs(&p2[p + u * nth]);
+    uint32_t em = 0, ne = 0;
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const uint32_t i = 2 * (p + u * nth);
-      visit(vp[u].x, vc[u] & 0xffffu, i);
-      visit(vp[u].y, vc[u] >> 16, i + 1);
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        const uint32_t b = hh ? vc[u] >> 16 : vc[u] & 0xffffu;
+        const float ph = hh ? vp[u].y : vp[u].x;
+        bool e = false;
+        if (b != kSpNoCode) {
+          const float thr = s_thr[b];
+          e = !drop && thr != __int_as_float(0x7f800000) && !((b < b_l ? ph : -ph) < thr);
+        }
+        em |= (e ? 1u : 0u) << (2 * u + hh);
+        ne += e ? 1u : 0u;
+      }
+    }
+    if (__any_sync(0xffffffffu, ne != 0)) {
+      uint32_t at = warp_scan_claim(&s_nc, ne, lane);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh)
+          if ((em >> (2 * u + hh)) & 1u) {
+            const uint32_t i = 2 * (p + u * nth) + hh;
+            c_idx[base + at] = i;
+            c_b[base + at] = hh ? vc[u] >> 16 : vc[u] & 0xffffu;
+            codes[i] = (uint16_t)kSpCandCode;
+            ++at;
+          }
     }
   }
   for (; p < np; p += nth) {
