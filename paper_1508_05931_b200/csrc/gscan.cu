@@ -990,6 +990,12 @@ int sp_seg_init(gscan_handle* h, const SpCtx& c) {
 }
 
 int sp_seg_extremes(gscan_handle* h, const SpCtx& c) {
+  if (c.vec && c.n >= (uint32_t)kExtTile) {  // bulk-copy pipeline, one CTA per SM
+    Launch L(h, "k_extremes_tma", c.s);
+    k_extremes_tma<<<h->sm_count, kExtThreads, kExtSmem, c.s>>>(c.xs, c.ys, c.n, h->partials, h->ext,
+                                                           h->ctr);
+    return GSCAN_OK;
+  }
   const uint32_t grid =
       std::max(1u, std::min<uint32_t>((c.n + kBlock * 8 - 1) / (kBlock * 8), h->sm_count * 8));
   Launch L(h, "k_extremes", c.s);
@@ -1620,6 +1626,7 @@ int gscan_create(int device, gscan_handle** out) {
     CU(cudaFuncSetAttribute(k_sp_hist<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, nbs));
     CU(cudaFuncSetAttribute(k_sp_hist<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, nbs));
     CU(cudaFuncSetAttribute(k_sp_hist_codes, cudaFuncAttributeMaxDynamicSharedMemorySize, nbs));
+    CU(cudaFuncSetAttribute(k_extremes_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kExtSmem));
     CU(cudaFuncSetAttribute(k_sp_phi<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, nbs));
     CU(cudaFuncSetAttribute(k_sp_phi<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, nbs));
     CU(cudaFuncSetAttribute(k_sp_cand, cudaFuncAttributeMaxDynamicSharedMemorySize, nbs));

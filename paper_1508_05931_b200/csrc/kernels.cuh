@@ -45,19 +45,23 @@ struct ExtAcc {
   uint32_t iminx, iminy, imaxx, imaxy, il;
 };
 
+// +/-inf start values: every finite point beats them (non-finite input is a
+// precondition of the reference, SPEC.md), so a push is compare + select.
 __device__ __forceinline__ void ext_init(ExtAcc& a) {
-  a.minx = a.miny = a.ly = a.lx = DBL_MAX;
-  a.maxx = a.maxy = -DBL_MAX;
+  a.minx = a.miny = a.ly = a.lx = __longlong_as_double(0x7ff0000000000000ll);
+  a.maxx = a.maxy = __longlong_as_double((long long)0xfff0000000000000ull);
   a.iminx = a.iminy = a.imaxx = a.imaxy = a.il = 0xffffffffu;
 }
 
 // Within one thread indices only grow, so strict compares keep the first.
 __device__ __forceinline__ void ext_push(ExtAcc& a, double x, double y, uint32_t i) {
-  if (x < a.minx || a.iminx == 0xffffffffu) { a.minx = x; a.iminx = i; }
-  if (y < a.miny || a.iminy == 0xffffffffu) { a.miny = y; a.iminy = i; }
-  if (x > a.maxx || a.imaxx == 0xffffffffu) { a.maxx = x; a.imaxx = i; }
-  if (y > a.maxy || a.imaxy == 0xffffffffu) { a.maxy = y; a.imaxy = i; }
-  if (a.il == 0xffffffffu || y < a.ly || (y == a.ly && x < a.lx)) { a.ly = y; a.lx = x; a.il = i; }
+  const bool b0 = x < a.minx, b1 = y < a.miny, b2 = x > a.maxx, b3 = y > a.maxy;
+  const bool b4 = y < a.ly || (y == a.ly && x < a.lx);
+  a.minx = b0 ? x : a.minx; a.iminx = b0 ? i : a.iminx;
+  a.miny = b1 ? y : a.miny; a.iminy = b1 ? i : a.iminy;
+  a.maxx = b2 ? x : a.maxx; a.imaxx = b2 ? i : a.imaxx;
+  a.maxy = b3 ? y : a.maxy; a.imaxy = b3 ? i : a.imaxy;
+  a.ly = b4 ? y : a.ly; a.lx = b4 ? x : a.lx; a.il = b4 ? i : a.il;
 }
 
 __device__ __forceinline__ bool arg_better_min(double v, uint32_t i, double bv, uint32_t bi) {
@@ -101,6 +105,11 @@ __device__ __forceinline__ ExtAcc ext_shfl(const ExtAcc& a, int o) {
   return b;
 }
 
+__device__ __forceinline__ void ext_finish(ExtAcc acc, const double* __restrict__ xs,
+                                           const double* __restrict__ ys,
+                                           ExtAcc* __restrict__ partials,
+                                           ExtResult* __restrict__ out, Counters* __restrict__ ctr);
+
 // Grid-stride over 128-bit pairs of (xs, ys) with 4 pairs in flight per
 // thread; block partials are reduced by the last CTA to finish.
 template <bool kVec>
@@ -141,15 +150,25 @@ __global__ void __launch_bounds__(kBlock) k_extremes(const double* __restrict__ 
   } else {
     for (uint32_t i = tid; i < n; i += nthreads) ext_push(acc, xs[i], ys[i], i);
   }
+  ext_finish(acc, xs, ys, partials, out, ctr);
+}
+
+// Block reduction of the per-thread accumulators, then the last CTA to finish
+// reduces the block partials and writes the result (any block size <= 1024).
+__device__ __forceinline__ void ext_finish(ExtAcc acc, const double* __restrict__ xs,
+                                           const double* __restrict__ ys,
+                                           ExtAcc* __restrict__ partials,
+                                           ExtResult* __restrict__ out, Counters* __restrict__ ctr) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) ext_merge(acc, ext_shfl(acc, o));
-  __shared__ ExtAcc s_w[kWarps];
+  __shared__ ExtAcc s_w[32];
+  const int nwarps = (int)(blockDim.x >> 5);
   __shared__ bool s_last;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (lane == 0) s_w[warp] = acc;
   __syncthreads();
   if (threadIdx.x == 0) {
-    for (int w = 1; w < kWarps; ++w) ext_merge(acc, s_w[w]);
+    for (int w = 1; w < nwarps; ++w) ext_merge(acc, s_w[w]);
     partials[blockIdx.x] = acc;
     __threadfence();
     const uint32_t t = atomicAdd(&ctr->ext_ticket, 1u);
@@ -161,7 +180,7 @@ __global__ void __launch_bounds__(kBlock) k_extremes(const double* __restrict__ 
   __threadfence();
   ExtAcc a;
   ext_init(a);
-  for (uint32_t b = threadIdx.x; b < gridDim.x; b += kBlock) {
+  for (uint32_t b = threadIdx.x; b < gridDim.x; b += blockDim.x) {
     ExtAcc pb;
     const volatile ExtAcc* vp = &partials[b];
     pb.minx = vp->minx; pb.miny = vp->miny; pb.maxx = vp->maxx; pb.maxy = vp->maxy;
@@ -176,7 +195,7 @@ __global__ void __launch_bounds__(kBlock) k_extremes(const double* __restrict__ 
   if (lane == 0) s_w[warp] = a;
   __syncthreads();
   if (threadIdx.x == 0) {
-    for (int w = 1; w < kWarps; ++w) ext_merge(a, s_w[w]);
+    for (int w = 1; w < nwarps; ++w) ext_merge(a, s_w[w]);
     out->idx[0] = a.iminx; out->idx[1] = a.iminy; out->idx[2] = a.imaxx; out->idx[3] = a.imaxy;
     out->idx[4] = a.il;
     for (int k = 0; k < 4; ++k) { out->qx[k] = xs[out->idx[k]]; out->qy[k] = ys[out->idx[k]]; }
@@ -184,6 +203,72 @@ __global__ void __launch_bounds__(kBlock) k_extremes(const double* __restrict__ 
     out->ay = a.ly;
     ctr->ext_ticket = 0;  // ready for the next launch
   }
+}
+
+// K1 as a bulk-copy pipeline: each CTA (one per SM) streams tiles of
+// kExtTile points of xs and ys through a kExtStages-deep shared-memory ring
+// filled by cp.async.bulk (TMA) and completed on mbarriers, so the bytes in
+// flight do not depend on registers or occupancy. Tiles go to CTAs
+// round-robin; the remainder (< one tile) is read directly by the last CTA.
+// Within a thread indices only grow (tile order, then pair order), as
+// ext_push requires. Needs 16-byte aligned xs, ys.
+constexpr int kExtTile = 4096;    // points per tile (32 KB of x + 32 KB of y)
+constexpr int kExtStages = 3;
+constexpr int kExtThreads = 512;  // 16 warps: the compare/select chains need them
+constexpr size_t kExtSmem = (size_t)kExtStages * kExtTile * 16 + 64;
+
+__global__ void __launch_bounds__(kExtThreads, 1) k_extremes_tma(const double* __restrict__ xs,
+                                                           const double* __restrict__ ys, uint32_t n,
+                                                           ExtAcc* __restrict__ partials,
+                                                           ExtResult* __restrict__ out,
+                                                           Counters* __restrict__ ctr) {
+  extern __shared__ __align__(128) unsigned char ext_smem[];
+  double* sx = reinterpret_cast<double*>(ext_smem);                   // [stage][kExtTile]
+  double* sy = sx + (size_t)kExtStages * kExtTile;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sy + (size_t)kExtStages * kExtTile);
+  const uint32_t ntiles = n / kExtTile;
+  const uint32_t mine = ntiles > blockIdx.x ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0u;
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < kExtStages; ++k) mbar_init(&bar[k], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  auto issue = [&](uint32_t k) {  // this CTA's k-th tile into stage k % kExtStages
+    const uint32_t st = k % kExtStages;
+    const size_t t0 = (size_t)(blockIdx.x + k * gridDim.x) * kExtTile;
+    mbar_expect_tx(&bar[st], 2u * kExtTile * 8u);
+    bulk_g2s(sx + (size_t)st * kExtTile, xs + t0, kExtTile * 8u, &bar[st]);
+    bulk_g2s(sy + (size_t)st * kExtTile, ys + t0, kExtTile * 8u, &bar[st]);
+  };
+  if (threadIdx.x == 0)
+    for (uint32_t k = 0; k < (uint32_t)kExtStages - 1 && k < mine; ++k) issue(k);
+  // four independent accumulators (pair u goes to acc[u % 4]): shorter
+  // dependency chains; each still sees increasing indices
+  ExtAcc acc[4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a) ext_init(acc[a]);
+  for (uint32_t k = 0; k < mine; ++k) {
+    if (threadIdx.x == 0 && k + kExtStages - 1 < mine) issue(k + kExtStages - 1);
+    const uint32_t st = k % kExtStages;
+    mbar_wait(&bar[st], (k / kExtStages) & 1u);
+    const double2* x2 = reinterpret_cast<const double2*>(sx + (size_t)st * kExtTile);
+    const double2* y2 = reinterpret_cast<const double2*>(sy + (size_t)st * kExtTile);
+    const uint32_t i0 = (blockIdx.x + k * gridDim.x) * kExtTile;
+#pragma unroll
+    for (int u = 0; u < kExtTile / 2 / kExtThreads; ++u) {
+      const uint32_t pp = threadIdx.x + u * kExtThreads;
+      const double2 vx = x2[pp], vy = y2[pp];
+      ext_push(acc[u & 3], vx.x, vy.x, i0 + 2 * pp);
+      ext_push(acc[u & 3], vx.y, vy.y, i0 + 2 * pp + 1);
+    }
+    __syncthreads();  // stage st may be refilled
+  }
+  if (blockIdx.x == gridDim.x - 1)
+    for (uint32_t i = ntiles * kExtTile + threadIdx.x; i < n; i += kExtThreads) ext_push(acc[0], xs[i], ys[i], i);
+  ext_merge(acc[0], acc[1]);
+  ext_merge(acc[2], acc[3]);
+  ext_merge(acc[0], acc[2]);
+  ext_finish(acc[0], xs, ys, partials, out, ctr);
 }
 
 // ===========================================================================
