@@ -372,9 +372,10 @@ int stage_round1(gscan_handle* h, const double* xs, const double* ys, uint32_t n
 
 // K1 + fused K2/K3 (pipeline path): extremes, then filter + keys + bucket
 // ranks in one pass. Leaves survivors/keys/ranks and n1, hist filled.
-int stage_round1_keys(gscan_handle* h, const double* xs, const double* ys, uint32_t n, int enable) {
+int stage_round1_keys(gscan_handle* h, const double* xs, const double* ys, uint32_t n, int enable,
+                      bool ext_ready = false) {
   const bool vec = aligned16(xs) && aligned16(ys);
-  {
+  if (!ext_ready) {  // else h->ext already holds this input's extremes (declined sparse attempt)
     const uint32_t grid =
         std::max(1u, std::min<uint32_t>((n + kBlock * 8 - 1) / (kBlock * 8), h->sm_count * 8));
     Launch L(h, "k_extremes");
@@ -955,6 +956,7 @@ struct SpCtx {
   bool vec, drop;
   const uint32_t* gs;  // storage base of gathered buckets (bstart on one device)
   cudaStream_t s;
+  bool sharded;        // a rank of the sharded path (decisions are global there)
 };
 
 SpCtx sp_ctx(gscan_handle* h, const double* xs, const double* ys, uint32_t n, uint64_t chunks) {
@@ -973,6 +975,7 @@ SpCtx sp_ctx(gscan_handle* h, const double* xs, const double* ys, uint32_t n, ui
   c.drop = (h->debug & GSCAN_DEBUG_SPARSE_DROP) != 0;
   c.gs = h->sp_bstart;
   c.s = h->stream;
+  c.sharded = false;
   return c;
 }
 
@@ -1015,7 +1018,8 @@ int sp_seg_f2(gscan_handle* h, const SpCtx& c) {
   cudaStream_t s = c.s;
   {
     Launch L(h, "k_sp_cdf", s);
-    k_sp_cdf<<<1, kSpCells / 2, 0, s>>>(h->sp_cells, h->sp_cdf);
+    k_sp_cdf<<<1, kSpCells / 2, 0, s>>>(h->sp_cells, h->sp_cdf, c.base == 0 && !c.sharded ? c.n : 0u,
+                                        h->sp_st);
   }
   {
     Launch L(h, "k_sp_theta", s);
@@ -1024,7 +1028,8 @@ int sp_seg_f2(gscan_handle* h, const SpCtx& c) {
   const uint32_t g2 = kF2Split ? 2 * c.G : c.G;  // F2 CTAs (d2 partials)
   {
     Launch L(h, "k_sp_hist", s);
-#define A2 c.xs, c.ys, c.n, h->ext, h->sp_cdf, h->sp_th, h->sp_codes, h->sp_hist_part, h->sp_d2, h->ctr
+#define A2 c.xs, c.ys, c.n, h->ext, h->sp_cdf, h->sp_th, h->sp_codes, h->sp_hist_part, h->sp_d2, h->ctr, \
+           h->sp_st
     if (kF2Split) {
       if (c.vec) k_sp_hist<true, false><<<g2, kSpThreads, 0, s>>>(A2);
       else k_sp_hist<false, false><<<g2, kSpThreads, 0, s>>>(A2);
@@ -1036,7 +1041,7 @@ int sp_seg_f2(gscan_handle* h, const SpCtx& c) {
   }
   if (kF2Split) {
     Launch L(h, "k_sp_hist_codes", s);
-    k_sp_hist_codes<<<c.G, 1024, c.smem_nb, s>>>(h->sp_codes, c.n, h->sp_hist_part);
+    k_sp_hist_codes<<<c.G, 1024, c.smem_nb, s>>>(h->sp_codes, c.n, h->sp_hist_part, h->sp_st);
   }
   {
     Launch L(h, "k_sp_check_r1", s);
@@ -1454,14 +1459,16 @@ int run_pipeline(gscan_handle* h, const double* xs, const double* ys, uint64_t n
   h->kt_used = 0;
   h->sp_used = 0;
   h->sp_fail = 0;
+  bool ext_ready = false;
   if (sparse_eligible(h, n64, cfg)) {
     bool ok = false;
     TRY(run_sparse(h, xs, ys, n, cfg, hull_size, st, &ok));
     if (ok) return GSCAN_OK;
+    ext_ready = true;  // K1 ran on this input inside the sparse attempt
   }
   CU(cudaEventRecord(h->ev[0], h->stream));
   CU(cudaMemsetAsync(h->ctr, 0, sizeof(Counters), h->stream));
-  TRY(stage_round1_keys(h, xs, ys, n, cfg.enable_round1));
+  TRY(stage_round1_keys(h, xs, ys, n, cfg.enable_round1, ext_ready));
   CU(cudaEventRecord(h->ev[1], h->stream));
   CU(cudaEventRecord(h->ev[2], h->stream));  // annotate (keys) is fused into round 1
   TRY(stage_annotate_sort(h, xs, ys, n, -1, 3, /*keys_done=*/true));
@@ -1530,6 +1537,7 @@ int dist_init(gscan_handle* h) {
 SpCtx dist_ctx(gscan_handle* h) {
   SpCtx c = sp_ctx(h, h->dist_xs, h->dist_ys, h->dist_n, h->dist_chunks);
   c.base = h->dist_base;
+  c.sharded = true;
   return c;
 }
 

@@ -368,8 +368,12 @@ __global__ void __launch_bounds__(1024) k_sp_sample(const double* __restrict__ x
 
 // One CTA of kSpCells/2 threads (two cells each): inclusive scan of the
 // floored counts -> CDF.
+// n > 0: also the early speed decision -- when >= 95% of the sampled points
+// survive round 1 (near-convex input) nearly all will be walk candidates and
+// the full sort is faster; decline before F2.
 __global__ void __launch_bounds__(kSpCells / 2) k_sp_cdf(const uint32_t* __restrict__ cell_cnt,
-                                                         double* __restrict__ cdf) {
+                                                         double* __restrict__ cdf, uint32_t n,
+                                                         SpState* __restrict__ st) {
   __shared__ double s_w[32];
   const double floor_w = 0.02;  // per-cell floor, in sample units
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -397,7 +401,12 @@ __global__ void __launch_bounds__(kSpCells / 2) k_sp_cdf(const uint32_t* __restr
   const uint32_t j = 2 * threadIdx.x;
   cdf[j + 1] = (incl - b) / tot;
   cdf[j + 2] = (j + 2 == kSpCells) ? 1.0 : incl / tot;
-  if (threadIdx.x == 0) cdf[0] = 0.0;
+  if (threadIdx.x == 0) {
+    cdf[0] = 0.0;
+    const double kept = tot - floor_w * kSpCells;  // sampled round-1 survivors
+    const uint32_t ns = min(n, kSpSample);
+    if (n > 0 && kept * 100.0 > (double)ns * 95.0) atomicOr(&st->fail, kSpFailMany);
+  }
 }
 
 __global__ void __launch_bounds__(256) k_sp_theta(const double* __restrict__ cdf,
@@ -516,8 +525,9 @@ __global__ void __launch_bounds__(kSpThreads, kHist ? 1 : 2) k_sp_hist(
     const double* __restrict__ xs, const double* __restrict__ ys, uint32_t n,
     const ExtResult* __restrict__ ext, const double* __restrict__ cdf,
     const double* __restrict__ th, uint16_t* __restrict__ codes, uint32_t* __restrict__ hist_part,
-    SpD2* __restrict__ d2part, Counters* __restrict__ ctr) {
+    SpD2* __restrict__ d2part, Counters* __restrict__ ctr, const SpState* __restrict__ st) {
   extern __shared__ uint32_t s_hist[];  // kSpBuckets (kHist)
+  if (st->fail) return;  // declined from the sample (k_sp_cdf)
   __shared__ double s_cdf[kSpCells + 1];
   if (kHist)
     for (uint32_t b = threadIdx.x; b < kSpBuckets; b += blockDim.x) s_hist[b] = 0;
@@ -629,8 +639,10 @@ __global__ void __launch_bounds__(kSpThreads, kHist ? 1 : 2) k_sp_hist(
 
 // Bucket histogram from F2's codes (2 B/pt): per-CTA shared-memory counts.
 __global__ void __launch_bounds__(1024, 1) k_sp_hist_codes(const uint16_t* __restrict__ codes,
-                                                           uint32_t n, uint32_t* __restrict__ hist_part) {
+                                                           uint32_t n, uint32_t* __restrict__ hist_part,
+                                                           const SpState* __restrict__ st) {
   extern __shared__ uint32_t s_hist[];  // kSpBuckets
+  if (st->fail) return;
   for (uint32_t b = threadIdx.x; b < kSpBuckets; b += blockDim.x) s_hist[b] = 0;
   __syncthreads();
   const uint4* c8 = reinterpret_cast<const uint4*>(codes);  // 8 codes per 16 B
