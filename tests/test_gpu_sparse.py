@@ -114,13 +114,14 @@ def test_sparse_duplicate_of_interior_point_is_harmless(engine, oracle_mod):
 
 def test_sparse_tie_for_farthest_point_declines(engine, oracle_mod):
     """split_regions takes the FIRST maximal dist2 in sorted order
-    (angular.hpp:197-204); a tie needs the exact order, so the path declines."""
+    (angular.hpp:197-204); a tie needs the exact order, so the path declines.
+    An explicit anchor and two dyadic points make the tie exact in floating
+    point, while round 1 still discards most of the square."""
     xs, ys = _gen("square", 300_000, 7)
-    a = int(np.lexsort((xs, ys))[0])  # anchor: min y, then min x
-    ax, ay = xs[a], ys[a]
-    # two new far points at exactly the same distance from the anchor
-    xs = np.append(xs, [ax + 3.0, ax - 3.0])
-    ys = np.append(ys, [ay + 4.0, ay + 4.0])
+    # anchor (0.5, -0.5); (-0.25, 1) and (1.25, 1): dx = -+0.75, dy = 1.5 ->
+    # dist2 = 2.8125 for both, beyond every corner of the unit square (<= 2.5)
+    xs = np.append(xs, [0.5, -0.25, 1.25])
+    ys = np.append(ys, [-0.5, 1.0, 1.0])
     used, fail, _ = _run(engine, oracle_mod, xs, ys)
     assert used == 0 and fail & FAIL_TIE, hex(fail)
 
