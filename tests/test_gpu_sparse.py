@@ -119,9 +119,11 @@ def test_sparse_tie_for_farthest_point_declines(engine, oracle_mod):
     point, while round 1 still discards most of the square."""
     xs, ys = _gen("square", 300_000, 7)
     # anchor (0.5, -0.5); (-0.25, 1) and (1.25, 1): dx = -+0.75, dy = 1.5 ->
-    # dist2 = 2.8125 for both, beyond every corner of the unit square (<= 2.5)
-    xs = np.append(xs, [0.5, -0.25, 1.25])
-    ys = np.append(ys, [-0.5, 1.0, 1.0])
+    # dist2 = 2.8125 for both, beyond every corner of the unit square (<= 2.5);
+    # (0.5, 1.1) is the top extreme (dist2 2.56), so the quadrilateral is a
+    # proper kite and round 1 keeps only ~12% of the square
+    xs = np.append(xs, [0.5, -0.25, 1.25, 0.5])
+    ys = np.append(ys, [-0.5, 1.0, 1.0, 1.1])
     used, fail, _ = _run(engine, oracle_mod, xs, ys)
     assert used == 0 and fail & FAIL_TIE, hex(fail)
 
