@@ -143,6 +143,7 @@ struct gscan_handle {
   SpState* h_sp = nullptr;  // pinned mirror
   // n-sized
   uint32_t *sp_eb = nullptr, *sp_Wb = nullptr, *sp_Ws = nullptr, *sp_Rb = nullptr, *sp_Rs = nullptr;
+  double *sp_gx = nullptr, *sp_gy = nullptr;  // gathered points' coordinates (F3 region slots)
   uint64_t* sp_dup = nullptr;  // per-CTA hash lists (n)
   uint32_t sp_used = 0, sp_fail = 0, sp_walked = 0, sp_calls = 0, sp_fallbacks = 0;
   // Graham tree strategy pool (graham_tree.cuh)
@@ -196,7 +197,7 @@ void free_buffers(gscan_handle* h) {
   dfree(h->g_parent); dfree(h->g_btop); dfree(h->g_jk); dfree(h->g_je); dfree(h->g_jmin);
   dfree(h->g_keep); dfree(h->g_misc);
   dfree(h->g_stA); dfree(h->g_stB); dfree(h->g_lenA); dfree(h->g_lenB); dfree(h->g_scr);
-  dfree(h->sp_eb); dfree(h->sp_Wb); dfree(h->sp_Ws); dfree(h->sp_Rb); dfree(h->sp_Rs); dfree(h->sp_dup);
+  dfree(h->sp_eb); dfree(h->sp_gx); dfree(h->sp_gy); dfree(h->sp_Wb); dfree(h->sp_Ws); dfree(h->sp_Rb); dfree(h->sp_Rs); dfree(h->sp_dup);
   dfree(h->sp_codes); dfree(h->sp_phi32); dfree(h->sp_dup2); dfree(h->tw_pool);
   h->tw_nmax = 0;
   h->g_st_cap = 0;
@@ -275,6 +276,8 @@ int reserve(gscan_handle* h, uint64_t n) {
   h->status_cap = tiles;
   CU(cudaMalloc(&h->status, tiles * 8));
   CU(cudaMalloc(&h->sp_eb, mr * 4));
+  CU(cudaMalloc(&h->sp_gx, mr * 8));
+  CU(cudaMalloc(&h->sp_gy, mr * 8));
   CU(cudaMalloc(&h->sp_Wb, m * 4));
   CU(cudaMalloc(&h->sp_Ws, m * 4));
   CU(cudaMalloc(&h->sp_Rb, m * 4));
@@ -1090,7 +1093,8 @@ int sp_seg_f3(gscan_handle* h, const SpCtx& c) {
   {
     Launch L(h, "k_sp_phi", s);
 #define A3 c.xs, c.ys, h->sp_codes, c.n, c.cap, h->ext, h->sp_gbits, h->sp_st, h->sp_phi_part, h->surv, \
-           h->sp_eb, h->sp_gcount, h->sp_dup, h->sp_hcount, h->sp_part_off, h->sp_phi32
+           h->sp_eb, h->sp_gcount, h->sp_gx, h->sp_gy, h->sp_dup, h->sp_hcount, h->sp_part_off, \
+           h->sp_phi32
     if (c.vec) k_sp_phi<true><<<c.G, kSpThreads, c.smem_nb, s>>>(A3);
     else k_sp_phi<false><<<c.G, kSpThreads, c.smem_nb, s>>>(A3);
 #undef A3
@@ -1104,13 +1108,16 @@ int sp_seg_f3(gscan_handle* h, const SpCtx& c) {
 
 // gathered points (regions (surv, sp_eb, sp_gcount) indexing gx/gy) sorted
 // exactly; slice heads and the per-bucket prefix maxima
-int sp_seg_sortg(gscan_handle* h, const SpCtx& c, const double* gx, const double* gy) {
+int sp_seg_sortg(gscan_handle* h, const SpCtx& c, const double* gx, const double* gy,
+                 bool region_xy = true) {
   cudaStream_t s = c.s;
   {
     Launch L(h, "k_sp_place_g", s);
     k_sp_emit_place<0><<<dim3(16, c.G), 256, 0, s>>>(gx, gy, h->surv, h->sp_eb, nullptr,
                                                      h->sp_gcount, c.cap, h->sp_gcnt, c.gs,
-                                                     h->ext, h->sp_st, h->rec);
+                                                     h->ext, h->sp_st, h->rec,
+                                                     region_xy ? h->sp_gx : nullptr,
+                                                     region_xy ? h->sp_gy : nullptr);
   }
   {
     Launch L(h, "k_sp_sort_gathered", s);
@@ -2070,7 +2077,7 @@ int gscan_dist_slices(gscan_handle* h, const double* d_X, const double* d_Y, uin
   TRY(scan_u32(h, h->sp_gsz, kSpBuckets, h->sp_gs));
   TRY(dist_fill(h, c, (uint32_t)n_g, 1, d_gb, h->sp_gcount));
   c.gs = h->sp_gs;
-  TRY(sp_seg_sortg(h, c, d_X, d_Y));
+  TRY(sp_seg_sortg(h, c, d_X, d_Y, /*region_xy=*/false));
   CU(cudaMemcpyAsync(d_prefmax, h->sp_prefmax, kSpBuckets * 4, cudaMemcpyDeviceToDevice, c.s));
   TRY(dist_read_state(h));
   *fail_out = dist_fail(h);

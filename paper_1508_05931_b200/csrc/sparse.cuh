@@ -880,6 +880,7 @@ __global__ void __launch_bounds__(kSpThreads, 1) k_sp_phi(
     const uint16_t* __restrict__ codes, uint32_t n, uint32_t cap, const ExtResult* __restrict__ ext,
     const uint32_t* __restrict__ gbits, SpState* __restrict__ st, uint32_t* __restrict__ phi_part,
     uint32_t* __restrict__ g_idx, uint32_t* __restrict__ g_b, uint32_t* __restrict__ g_count,
+    double* __restrict__ g_x, double* __restrict__ g_y,  // gathered coordinates (same slots)
     uint64_t* __restrict__ hlist, uint32_t* __restrict__ h_count, uint32_t* __restrict__ part_cnt,
     float* __restrict__ phi32) {
   extern __shared__ uint32_t s_phi[];  // kSpBuckets
@@ -925,7 +926,7 @@ __global__ void __launch_bounds__(kSpThreads, 1) k_sp_phi(
     const uint32_t jh = warp_claim(&s_nh[half], surv);
     if (surv) hlist[hbase + jh] = h;
     const uint32_t jg = warp_claim(&s_ng, emit);
-    if (emit) { g_idx[base + jg] = i; g_b[base + jg] = b; }
+    if (emit) { g_idx[base + jg] = i; g_b[base + jg] = b; g_x[base + jg] = x; g_y[base + jg] = y; }
   };
   // batch of 4 points: the same work as visit() in branch-free phases, and one
   // warp-scan claim per batch instead of a ballot claim per point
@@ -975,7 +976,13 @@ __global__ void __launch_bounds__(kSpThreads, 1) k_sp_phi(
       uint32_t ag = warp_scan_claim(&s_ng, ng, lane);
 #pragma unroll
       for (int k = 0; k < 4; ++k)
-        if (gat[k]) { g_idx[base + ag] = idx[k]; g_b[base + ag] = b[k]; ++ag; }
+        if (gat[k]) {
+          g_idx[base + ag] = idx[k];
+          g_b[base + ag] = b[k];
+          g_x[base + ag] = x[k];
+          g_y[base + ag] = y[k];
+          ++ag;
+        }
     }
   };
   {
@@ -1231,7 +1238,10 @@ __global__ void __launch_bounds__(256) k_sp_emit_place(
     const uint32_t* __restrict__ e_b, uint32_t* __restrict__ e_rank,
     const uint32_t* __restrict__ e_count, uint32_t cap, uint32_t* __restrict__ cnt,
     const uint32_t* __restrict__ start, const ExtResult* __restrict__ ext,
-    const SpState* __restrict__ st, PtRec* __restrict__ rec) {
+    const SpState* __restrict__ st, PtRec* __restrict__ rec,
+    const double* __restrict__ e_x = nullptr, const double* __restrict__ e_y = nullptr) {
+  // e_x, e_y: the emitted points' coordinates in the region slots (F3 writes
+  // them for gathered points, so no random reads of xs, ys); else xs[i], ys[i]
   if (st->fail) return;
   const uint32_t c = blockIdx.y;
   const uint32_t ne = e_count[c];
@@ -1245,8 +1255,8 @@ __global__ void __launch_bounds__(256) k_sp_emit_place(
     if (kPhase == 1) { e_rank[base + k] = r; continue; }
     const uint32_t i = e_idx[base + k];
     PtRec o;
-    o.x = xs[i];
-    o.y = ys[i];
+    o.x = e_x ? e_x[base + k] : xs[i];
+    o.y = e_y ? e_y[base + k] : ys[i];
     o.key = angle_key(__dsub_rn(o.x, ax), __dsub_rn(o.y, ay));
     o.idx = i;
     o.pad = b;
