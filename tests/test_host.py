@@ -241,3 +241,23 @@ def test_torch_comm_matches_local_comm_gloo(tmp_path):
     for p, (o, e) in zip(procs, outs):
         assert p.returncode == 0, e[-3000:]
         assert "ok" in o
+
+
+@pytest.mark.parametrize("kind,n,seed", [("square", 3000, 1), ("disk", 2000, 2), ("circle", 500, 3),
+                                          ("collinear", 300, 4), ("square", 2, 5), ("square", 1, 6)])
+def test_harness_monotone_chain_matches_oracle(oracle_mod, kind, n, seed):
+    """The harness's self-contained restatement of oracle::monotone_chain
+    (oracle.hpp:40-79) has the oracle's vertex set; strictly_inside agrees
+    with the hull (vertices are not strictly inside, the centroid of a
+    non-degenerate hull is)."""
+    from paper_1508_05931_b200 import generate
+    from paper_1508_05931_b200.harness import monotone_chain, same_vertex_set, strictly_inside
+
+    xs, ys = generate(kind, n, seed)
+    hull = monotone_chain(xs, ys)
+    idx = oracle_mod.monotone_chain(xs, ys).astype(np.int64)
+    assert same_vertex_set(hull, np.stack([xs[idx], ys[idx]], 1))
+    assert not strictly_inside(hull, hull[:, 0], hull[:, 1]).any()
+    if len(hull) >= 3:
+        c = hull.mean(0)
+        assert strictly_inside(hull, np.array([c[0]]), np.array([c[1]]))[0]
