@@ -196,11 +196,15 @@ __device__ __forceinline__ double unord_f(uint32_t u) {
 // compares folded bits, angular.hpp:99-101): equal points hash equally, so
 // equal hashes are the only possible duplicates.
 __device__ __forceinline__ uint64_t coord_hash64(double x, double y) {
-  const uint64_t a = dbits(x == 0.0 ? 0.0 : x), b = dbits(y == 0.0 ? 0.0 : y);
-  uint64_t z = a ^ (b * 0x9e3779b97f4a7c15ull);
-  z ^= z >> 30; z *= 0xbf58476d1ce4e5b9ull;
-  z ^= z >> 27; z *= 0x94d049bb133111ebull;
+  // x + 0.0 folds -0.0 onto +0.0 and leaves every other finite x unchanged
+  const uint64_t a = dbits(__dadd_rn(x, 0.0)), b = dbits(__dadd_rn(y, 0.0));
+  // two odd multipliers and a fold: every input bit reaches the top bits (the
+  // partition) and the low bits; a collision of distinct points only makes
+  // the sparse path decline, never a wrong result
+  uint64_t z = a * 0x9e3779b97f4a7c15ull + b * 0xc2b2ae3d27d4eb4full;
   z ^= z >> 31;
+  z *= 0xbf58476d1ce4e5b9ull;
+  z ^= z >> 29;
   return z == ~0ull ? 0ull : z;  // ~0 marks an empty slot / padding
 }
 
@@ -901,7 +905,7 @@ __global__ void __launch_bounds__(kSpThreads, 1) k_sp_phi(
   const uint32_t b_l = st->b_l;
   const double r02 = st->r02;
   const size_t base = (size_t)blockIdx.x * cap;
-  double plo = 3.0, phi_ = -3.0;
+  float plo = 3.0f, phi_ = -3.0f;  // phi range, already rounded outward (rd / ru)
   __syncthreads();
   auto visit = [&](double x, double y, uint32_t b, uint32_t i) {
     const bool surv = b != kSpNoCode;
@@ -912,8 +916,8 @@ __global__ void __launch_bounds__(kSpThreads, 1) k_sp_phi(
       atomicAdd(&s_part[half][(uint32_t)(h >> (64 - kSpPartBits))], 1u);
       double v2;
       const double raw = sp_phi_raw(x, y, lx, ly, ux, uy, &v2);
-      plo = fmin(plo, raw);
-      phi_ = fmax(phi_, raw);
+      plo = fminf(plo, __double2float_rd(raw));
+      phi_ = fmaxf(phi_, __double2float_ru(raw));
       if (sp_gathered(s_g, b)) {
         emit = true;
       } else if (v2 >= r02) {  // points within r0 of P_l never raise a maximum (certificate)
@@ -955,8 +959,8 @@ __global__ void __launch_bounds__(kSpThreads, 1) k_sp_phi(
       if (!surv) continue;
       ++nh;
       atomicAdd(&s_part[half][(uint32_t)(h[k] >> (64 - kSpPartBits))], 1u);
-      plo = fmin(plo, raw[k]);
-      phi_ = fmax(phi_, raw[k]);
+      plo = fminf(plo, __double2float_rd(raw[k]));
+      phi_ = fmaxf(phi_, __double2float_ru(raw[k]));
       gat[k] = sp_gathered(s_g, b[k]);
       if (gat[k]) {
         ++ng;
@@ -1043,12 +1047,12 @@ __global__ void __launch_bounds__(kSpThreads, 1) k_sp_phi(
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
-    plo = fmin(plo, __shfl_xor_sync(0xffffffffu, plo, o));
-    phi_ = fmax(phi_, __shfl_xor_sync(0xffffffffu, phi_, o));
+    plo = fminf(plo, __shfl_xor_sync(0xffffffffu, plo, o));
+    phi_ = fmaxf(phi_, __shfl_xor_sync(0xffffffffu, phi_, o));
   }
   if ((threadIdx.x & 31) == 0 && plo <= phi_) {
-    atomicMin(&st->phi_lo, ord_f(__double2float_rd(plo)));
-    atomicMax(&st->phi_hi, ord_f(__double2float_ru(phi_)));
+    atomicMin(&st->phi_lo, ord_f(plo));
+    atomicMax(&st->phi_hi, ord_f(phi_));
   }
 }
 
