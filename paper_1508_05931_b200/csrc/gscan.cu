@@ -156,6 +156,7 @@ struct gscan_handle {
   const double* dist_ys = nullptr;
   uint32_t dist_n = 0, dist_base = 0;
   uint64_t dist_chunks = 0;
+  float* sp_thr = nullptr;  // F4 candidate thresholds per bucket
   uint32_t *sp_gs = nullptr, *sp_gsz = nullptr, *dist_ctr = nullptr, *dist_pm = nullptr,
            *dist_hc = nullptr;
   uint64_t* dist_lb = nullptr;
@@ -924,6 +925,7 @@ int sparse_init(gscan_handle* h) {
                           &h->sp_prefmax, &h->sp_slice, &h->sp_ccnt, &h->sp_cstart, &h->sp_wcnt,
                           &h->sp_wstart, &h->sp_rlo};
   for (uint32_t** b : nb_bufs) CU(cudaMalloc(b, (nb + 2) * 4));
+  CU(cudaMalloc(&h->sp_thr, (size_t)nb * 4));
   CU(cudaMalloc(&h->sp_gbits, nb / 8));
   CU(cudaMalloc(&h->sp_st, sizeof(SpState)));
   CU(cudaMallocHost(&h->h_sp, sizeof(SpState)));
@@ -1145,10 +1147,15 @@ int sp_seg_sortg(gscan_handle* h, const SpCtx& c, const double* gx, const double
 int sp_seg_f4(gscan_handle* h, const SpCtx& c) {
   cudaStream_t s = c.s;
   {
+    Launch L(h, "k_sp_thresholds", s);
+    k_sp_thresholds<<<(kSpBuckets + 255) / 256, 256, 0, s>>>(h->sp_gbits, h->sp_prefmax, h->sp_st,
+                                                            h->sp_thr);
+  }
+  {
     Launch L(h, "k_sp_cand", s);
     k_sp_cand<<<c.G, kSpCandThreads, c.smem_nb, s>>>(h->sp_codes, h->sp_phi32, c.n, c.cap,
-                                                     h->sp_gbits, h->sp_prefmax, h->sp_st, h->surv,
-                                                     h->sp_eb, h->sp_ccount, c.drop);
+                                                     h->sp_thr, h->sp_st, h->surv, h->sp_eb,
+                                                     h->sp_ccount, c.drop);
   }
   {
     Launch L(h, "k_sp_check_cand", s);
@@ -1689,7 +1696,7 @@ int gscan_destroy(gscan_handle* h) {
   if (h->h_ctr) cudaFreeHost(h->h_ctr);
   if (h->h_info) cudaFreeHost(h->h_info);
   dfree(h->tw_pool);
-  dfree(h->sp_gs); dfree(h->sp_gsz); dfree(h->dist_ctr); dfree(h->dist_pm); dfree(h->dist_hc);
+  dfree(h->sp_gs); dfree(h->sp_thr); dfree(h->sp_gsz); dfree(h->dist_ctr); dfree(h->dist_pm); dfree(h->dist_hc);
   dfree(h->dist_lb);
   if (h->h_out) cudaFreeHost(h->h_out);
   for (auto& e : h->ev) if (e) cudaEventDestroy(e);

@@ -1663,19 +1663,32 @@ __device__ __forceinline__ bool sp_is_candidate(double ph, uint32_t pm, bool dro
 
 constexpr int kSpCandThreads = 1024;
 
+// Candidate thresholds per bucket: prefmax - tol, rounded down to float (a
+// lower threshold only adds candidates); gathered buckets get +inf (never
+// candidates here).
+__global__ void k_sp_thresholds(const uint32_t* __restrict__ gbits,
+                                const uint32_t* __restrict__ prefmax, const SpState* __restrict__ st,
+                                float* __restrict__ thr) {
+  const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= kSpBuckets || st->fail) return;
+  const bool g = (gbits[b >> 5] >> (b & 31)) & 1u;
+  thr[b] = g ? __int_as_float(0x7f800000) : __double2float_rd(unord_f(prefmax[b]) - kSpTol);
+}
+
 __global__ void __launch_bounds__(kSpCandThreads, 1) k_sp_cand(
     uint16_t* __restrict__ codes, const float* __restrict__ phi32, uint32_t n, uint32_t cap,
-    const uint32_t* __restrict__ gbits, const uint32_t* __restrict__ prefmax,
+    const float* __restrict__ thr_g,
     SpState* __restrict__ st, uint32_t* __restrict__ c_idx, uint32_t* __restrict__ c_b,
     uint32_t* __restrict__ c_count, bool drop) {
   // thresholds prefmax - tol, rounded down to float (a lower threshold only
   // adds candidates); gathered buckets get +inf (never candidates here)
-  extern __shared__ float s_thr[];  // kSpBuckets
+  extern __shared__ __align__(16) float s_thr[];  // kSpBuckets
   __shared__ uint32_t s_nc;
   if (st->fail) return;
-  for (uint32_t b = threadIdx.x; b < kSpBuckets; b += blockDim.x) {
-    const bool g = (gbits[b >> 5] >> (b & 31)) & 1u;
-    s_thr[b] = g ? __int_as_float(0x7f800000) : __double2float_rd(unord_f(prefmax[b]) - kSpTol);
+  {  // thresholds precomputed by k_sp_thresholds: a 16-byte copy into shared memory
+    const float4* t4 = reinterpret_cast<const float4*>(thr_g);
+    float4* s4 = reinterpret_cast<float4*>(s_thr);
+    for (uint32_t q = threadIdx.x; q < kSpBuckets / 4; q += blockDim.x) s4[q] = __ldg(&t4[q]);
   }
   if (threadIdx.x == 0) s_nc = 0;
   const uint32_t b_l = st->b_l;
