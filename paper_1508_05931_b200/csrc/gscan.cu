@@ -1088,8 +1088,7 @@ int sp_seg_f3(gscan_handle* h, const SpCtx& c) {
   }
   {
     Launch L(h, "k_sp_gbits", s);
-    k_sp_gbits<<<(c.nb / 32 + 255) / 256, 256, 0, s>>>(h->sp_bstart, h->sp_st, h->sp_gbits,
-                                                       h->sp_glist);
+    k_sp_gbits<<<c.nb / 256, 256, 0, s>>>(h->sp_bstart, h->sp_st, h->sp_gbits, h->sp_glist);
   }
   TRY(rec_event(h, h->ev[1], s));
   {

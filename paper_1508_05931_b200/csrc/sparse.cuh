@@ -767,30 +767,37 @@ __global__ void __launch_bounds__(256) k_sp_lrank(const double* __restrict__ xs,
   const double ldx = __dsub_rn(st->lx, ax), ldy = __dsub_rn(st->ly, ay);
   const uint64_t lkey = angle_key(ldx, ldy);
   const double ld2 = dist2_rn(ldx, ldy);
-  const uint32_t* c2 = reinterpret_cast<const uint32_t*>(codes);
-  const uint32_t npairs = (n + 1) / 2;
   uint32_t below = 0;
   const uint32_t nth = gridDim.x * blockDim.x;
-  for (uint32_t p0 = blockIdx.x * blockDim.x + threadIdx.x; p0 < npairs; p0 += 8 * nth) {
-    uint32_t cw[8];
+  auto visit = [&](uint32_t code, uint32_t i) {
+    if (code != b_l || base + i == l_idx) return;
+    const double dx = __dsub_rn(xs[i], ax), dy = __dsub_rn(ys[i], ay);
+    below += key_less(angle_key(dx, dy), dist2_rn(dx, dy), base + i, lkey, ld2, l_idx);
+  };
+  // 16-byte loads (8 codes), 4 in flight; the tail below n8 * 8 point by point
+  const uint4* c8 = reinterpret_cast<const uint4*>(codes);
+  const uint32_t n8 = n / 8;
+  const uint32_t key2 = b_l | (b_l << 16);
+  for (uint32_t q0 = blockIdx.x * blockDim.x + threadIdx.x; q0 < n8; q0 += 4 * nth) {
+    uint4 v[4];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const uint32_t p = p0 + u * nth;
-      cw[u] = (p >= npairs) ? 0xffffffffu
-              : (2 * p + 1 < n) ? __ldcs(&c2[p]) : ((uint32_t)codes[2 * p] | 0xffff0000u);
-    }
+    for (int u = 0; u < 4; ++u) v[u] = q0 + u * nth < n8 ? __ldcs(&c8[q0 + u * nth]) : make_uint4(~0u, ~0u, ~0u, ~0u);
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        if (((cw[u] >> (16 * h)) & 0xffffu) != b_l) continue;
-        const uint32_t i = 2 * (p0 + u * nth) + h;
-        if (base + i == l_idx) continue;
-        const double dx = __dsub_rn(xs[i], ax), dy = __dsub_rn(ys[i], ay);
-        below += key_less(angle_key(dx, dy), dist2_rn(dx, dy), base + i, lkey, ld2, l_idx);
+      for (int k = 0; k < 4; ++k) {
+        // SWAR test: does either 16-bit half equal b_l?
+        const uint32_t x = w[k] ^ key2;
+        if ((x & 0xffffu) && (x >> 16)) continue;
+        const uint32_t i = 8 * (q0 + u * nth) + 2 * k;
+        visit(w[k] & 0xffffu, i);
+        visit(w[k] >> 16, i + 1);
       }
     }
   }
+  for (uint32_t i = n8 * 8 + blockIdx.x * blockDim.x + threadIdx.x; i < n; i += nth)
+    visit(codes[i], i);
   if (below) atomicAdd(&st->l_below, below);
 }
 
@@ -814,29 +821,25 @@ __global__ void __launch_bounds__(256) k_sp_gbits(const uint32_t* __restrict__ b
                                                   SpState* __restrict__ st,
                                                   uint32_t* __restrict__ gbits,
                                                   uint32_t* __restrict__ glist) {
-  const uint32_t w = blockIdx.x * blockDim.x + threadIdx.x;
-  if (w >= kSpBuckets / 32) return;
-  const bool ok = !st->fail;
-  const uint32_t b_l = st->b_l, M = st->M, sr = st->step_r, sl = st->step_l;
-  uint32_t bits = 0;
-  if (ok) {
-    for (uint32_t k = 0; k < 32; ++k) {
-      const uint32_t b = w * 32 + k;
-      const uint32_t lo = 1 + bstart[b], hi = bstart[b + 1];
-      if (hi < lo) continue;  // empty
-      bool g = (b == b_l);
+  // a thread per bucket, a warp per bitmap word
+  const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;  // kSpBuckets is a multiple of 256
+  const uint32_t lane = threadIdx.x & 31;
+  bool g = false;
+  if (!st->fail) {
+    const uint32_t b_l = st->b_l, M = st->M, sr = st->step_r, sl = st->step_l;
+    const uint32_t lo = 1 + bstart[b], hi = bstart[b + 1];
+    if (hi >= lo) {  // non-empty
+      g = (b == b_l);
       if (b < b_l) g = has_right_seed(lo, hi, sr);
       if (b > b_l) g = has_left_seed(lo, hi, M, sl);
-      if (g) bits |= 1u << k;
     }
   }
-  gbits[w] = bits;
-  const uint32_t cnt = __popc(bits);
-  if (cnt) {
-    const uint32_t at = atomicAdd(&st->n_gb, cnt);
-    uint32_t k = 0;
-    for (uint32_t bb = bits; bb; bb &= bb - 1) glist[at + k++] = w * 32 + (__ffs(bb) - 1);
-  }
+  const uint32_t bits = __ballot_sync(0xffffffffu, g);
+  if (lane == 0) gbits[b >> 5] = bits;
+  uint32_t at = 0;
+  if (lane == 0 && bits) at = atomicAdd(&st->n_gb, (uint32_t)__popc(bits));
+  at = __shfl_sync(0xffffffffu, at, 0);
+  if (g) glist[at + __popc(bits & lanemask_lt())] = b;
 }
 
 __device__ __forceinline__ bool sp_gathered(const uint32_t* g, uint32_t b) {
