@@ -926,6 +926,8 @@ int sparse_init(gscan_handle* h) {
                           &h->sp_wstart, &h->sp_rlo};
   for (uint32_t** b : nb_bufs) CU(cudaMalloc(b, (nb + 2) * 4));
   CU(cudaMalloc(&h->sp_thr, (size_t)nb * 4));
+  CU(cudaMalloc(&h->sp_gs, (nb + 2) * 4));
+  CU(cudaMalloc(&h->sp_gsz, (nb + 2) * 4));
   CU(cudaMalloc(&h->sp_gbits, nb / 8));
   CU(cudaMalloc(&h->sp_st, sizeof(SpState)));
   CU(cudaMallocHost(&h->h_sp, sizeof(SpState)));
@@ -978,7 +980,7 @@ SpCtx sp_ctx(gscan_handle* h, const double* xs, const double* ys, uint32_t n, ui
   c.smem_nb = (size_t)kSpBuckets * 4;
   c.vec = aligned16(xs) && aligned16(ys);
   c.drop = (h->debug & GSCAN_DEBUG_SPARSE_DROP) != 0;
-  c.gs = h->sp_bstart;
+  c.gs = h->sp_gs;  // compact storage of the gathered buckets (sp_seg_f3 / gscan_dist_slices)
   c.s = h->stream;
   c.sharded = false;
   return c;
@@ -1090,6 +1092,14 @@ int sp_seg_f3(gscan_handle* h, const SpCtx& c) {
     Launch L(h, "k_sp_gbits", s);
     k_sp_gbits<<<c.nb / 256, 256, 0, s>>>(h->sp_bstart, h->sp_st, h->sp_gbits, h->sp_glist);
   }
+  if (!c.sharded) {
+    // gathered buckets stored compactly (gs[b]): their records and sorted
+    // points stay L2-resident instead of being scattered over the global
+    // position range (rank 0 of the sharded path does this in dist_slices)
+    Launch L(h, "k_sp_gsize", s);
+    k_sp_gsize<<<(c.nb + 255) / 256, 256, 0, s>>>(h->sp_gbits, h->sp_hist, h->sp_gsz);
+  }
+  if (!c.sharded) TRY(scan_u32(h, h->sp_gsz, c.nb, h->sp_gs));
   TRY(rec_event(h, h->ev[1], s));
   {
     Launch L(h, "k_sp_phi", s);
@@ -1537,9 +1547,7 @@ gscan_handle* g_default = nullptr;
 constexpr uint32_t kDistMaxRanks = 64;
 
 int dist_init(gscan_handle* h) {
-  if (h->sp_gs) return GSCAN_OK;
-  CU(cudaMalloc(&h->sp_gs, (kSpBuckets + 2) * 4));
-  CU(cudaMalloc(&h->sp_gsz, (kSpBuckets + 2) * 4));
+  if (h->dist_ctr) return GSCAN_OK;
   CU(cudaMalloc(&h->dist_ctr, 64));
   CU(cudaMalloc(&h->dist_pm, ((size_t)kSpParts * kDistMaxRanks + 2) * 4));
   CU(cudaMalloc(&h->dist_hc, kDistMaxRanks * 4));
