@@ -950,6 +950,9 @@ int rec_event(gscan_handle* h, cudaEvent_t e, cudaStream_t s) {
 // F2 without its shared-memory histogram (two CTAs per SM) + a histogram
 // pass over the codes
 constexpr bool kF2Split = true;
+// F3 without its shared-memory bucket maxima (1024 threads) + a maxima pass:
+// measured slower (F3 192 us either way, + 46 us for k_sp_phimax_codes)
+constexpr bool kF3Split = false;
 
 struct SpCtx {
   const double* xs;
@@ -1103,12 +1106,24 @@ int sp_seg_f3(gscan_handle* h, const SpCtx& c) {
   TRY(rec_event(h, h->ev[1], s));
   {
     Launch L(h, "k_sp_phi", s);
+    const uint32_t t3 = kF3Split ? 1024u : (uint32_t)kSpThreads;
+    const size_t sm3 = kF3Split ? 0 : c.smem_nb;
 #define A3 c.xs, c.ys, h->sp_codes, c.n, c.cap, h->ext, h->sp_gbits, h->sp_st, h->sp_phi_part, h->surv, \
            h->sp_eb, h->sp_gcount, h->sp_gx, h->sp_gy, h->sp_dup, h->sp_hcount, h->sp_part_off, \
            h->sp_phi32
-    if (c.vec) k_sp_phi<true><<<c.G, kSpThreads, c.smem_nb, s>>>(A3);
-    else k_sp_phi<false><<<c.G, kSpThreads, c.smem_nb, s>>>(A3);
+    if (kF3Split) {
+      if (c.vec) k_sp_phi<true, false><<<c.G, t3, sm3, s>>>(A3);
+      else k_sp_phi<false, false><<<c.G, t3, sm3, s>>>(A3);
+    } else {
+      if (c.vec) k_sp_phi<true, true><<<c.G, t3, sm3, s>>>(A3);
+      else k_sp_phi<false, true><<<c.G, t3, sm3, s>>>(A3);
+    }
 #undef A3
+  }
+  if (kF3Split) {
+    Launch L(h, "k_sp_phimax_codes", s);
+    k_sp_phimax_codes<<<c.G, 1024, c.smem_nb, s>>>(h->sp_codes, h->sp_phi32, h->sp_gbits, c.n,
+                                                   h->sp_st, h->sp_phi_part);
   }
   {
     Launch L(h, "k_sp_reduce_phi", s);
@@ -1656,8 +1671,9 @@ int gscan_create(int device, gscan_handle** out) {
     CU(cudaFuncSetAttribute(k_sp_hist<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, nbs));
     CU(cudaFuncSetAttribute(k_sp_hist_codes, cudaFuncAttributeMaxDynamicSharedMemorySize, nbs));
     CU(cudaFuncSetAttribute(k_extremes_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kExtSmem));
-    CU(cudaFuncSetAttribute(k_sp_phi<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, nbs));
-    CU(cudaFuncSetAttribute(k_sp_phi<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, nbs));
+    CU(cudaFuncSetAttribute(k_sp_phi<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, nbs));
+    CU(cudaFuncSetAttribute(k_sp_phi<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, nbs));
+    CU(cudaFuncSetAttribute(k_sp_phimax_codes, cudaFuncAttributeMaxDynamicSharedMemorySize, nbs));
     CU(cudaFuncSetAttribute(k_sp_cand, cudaFuncAttributeMaxDynamicSharedMemorySize, nbs));
     CU(cudaFuncSetAttribute(k_sp_verify<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, nbs + 4));
     CU(cudaFuncSetAttribute(k_sp_verify<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, nbs + 4));

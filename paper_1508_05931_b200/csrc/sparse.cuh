@@ -881,8 +881,10 @@ __device__ __forceinline__ uint32_t warp_scan_claim(uint32_t* s_counter, uint32_
 // F3: gathered points are emitted (index, bucket); other survivors fold phi
 // into the per-CTA bucket maximum; every bucketed survivor's 64-bit hash goes
 // to the CTA's hash list, counted per partition.
-template <bool kVec>
-__global__ void __launch_bounds__(kSpThreads, 1) k_sp_phi(
+// kMax = false: no shared-memory bucket maxima (k_sp_phimax_codes computes
+// them from the stored phi), so the CTA runs 1024 threads.
+template <bool kVec, bool kMax>
+__global__ void __launch_bounds__(kMax ? kSpThreads : 1024, 1) k_sp_phi(
     const double* __restrict__ xs, const double* __restrict__ ys,
     const uint16_t* __restrict__ codes, uint32_t n, uint32_t cap, const ExtResult* __restrict__ ext,
     const uint32_t* __restrict__ gbits, SpState* __restrict__ st, uint32_t* __restrict__ phi_part,
@@ -890,18 +892,19 @@ __global__ void __launch_bounds__(kSpThreads, 1) k_sp_phi(
     double* __restrict__ g_x, double* __restrict__ g_y,  // gathered coordinates (same slots)
     uint64_t* __restrict__ hlist, uint32_t* __restrict__ h_count, uint32_t* __restrict__ part_cnt,
     float* __restrict__ phi32) {
-  extern __shared__ uint32_t s_phi[];  // kSpBuckets
+  extern __shared__ uint32_t s_phi[];  // kSpBuckets (kMax)
   __shared__ uint32_t s_g[kSpBuckets / 32];
   __shared__ uint32_t s_part[2][kSpParts];  // per half-CTA hash list
   __shared__ uint32_t s_ng, s_nh[2];
   if (st->fail) return;
-  for (uint32_t b = threadIdx.x; b < kSpBuckets; b += blockDim.x) s_phi[b] = 0;
+  if (kMax)
+    for (uint32_t b = threadIdx.x; b < kSpBuckets; b += blockDim.x) s_phi[b] = 0;
   for (uint32_t w = threadIdx.x; w < kSpBuckets / 32; w += blockDim.x) s_g[w] = gbits[w];
   for (uint32_t p = threadIdx.x; p < 2 * kSpParts; p += blockDim.x) s_part[0][p] = 0;
   if (threadIdx.x == 0) { s_ng = 0; s_nh[0] = 0; s_nh[1] = 0; }
   // two hash lists per CTA (threads [0, 256) and [256, 512)) of cap / 2 slots
   // each, so the duplicate check's work items are finer than the CTAs
-  const uint32_t half = threadIdx.x >= kSpThreads / 2 ? 1u : 0u;
+  const uint32_t half = threadIdx.x >= blockDim.x / 2 ? 1u : 0u;
   const size_t hbase = (size_t)(2 * blockIdx.x + half) * (cap / 2);
   const double lx = st->lx, ly = st->ly;
   const double ux = __dsub_rn(ext->ax, lx), uy = __dsub_rn(ext->ay, ly);
@@ -924,8 +927,11 @@ __global__ void __launch_bounds__(kSpThreads, 1) k_sp_phi(
       if (sp_gathered(s_g, b)) {
         emit = true;
       } else if (v2 >= r02) {  // points within r0 of P_l never raise a maximum (certificate)
-        atomicMax(&s_phi[b], ord_f(__double2float_rd(b < b_l ? raw : -raw)));
-        phi32[i] = __double2float_rn(raw);  // F4 reads it instead of recomputing
+        // stored signed and rounded down: the value the bucket maxima take,
+        // within the certificate's storage error (kSpPhiStoreErr, |phi| < 2)
+        const float sv = __double2float_rd(b < b_l ? raw : -raw);
+        if (kMax) atomicMax(&s_phi[b], ord_f(sv));
+        phi32[i] = sv;  // F4 reads it instead of recomputing
       } else {
         phi32[i] = __int_as_float(0x7fc00000);  // NaN: always a candidate
       }
@@ -968,8 +974,9 @@ __global__ void __launch_bounds__(kSpThreads, 1) k_sp_phi(
       if (gat[k]) {
         ++ng;
       } else if (v2[k] >= r02) {  // points within r0 of P_l never raise a maximum (certificate)
-        atomicMax(&s_phi[b[k]], ord_f(__double2float_rd(b[k] < b_l ? raw[k] : -raw[k])));
-        phi32[idx[k]] = __double2float_rn(raw[k]);  // F4 reads it instead of recomputing
+        const float sv = __double2float_rd(b[k] < b_l ? raw[k] : -raw[k]);
+        if (kMax) atomicMax(&s_phi[b[k]], ord_f(sv));
+        phi32[idx[k]] = sv;  // F4 reads it instead of recomputing
       } else {
         phi32[idx[k]] = __int_as_float(0x7fc00000);  // NaN: always a candidate
       }
@@ -1002,7 +1009,7 @@ __global__ void __launch_bounds__(kSpThreads, 1) k_sp_phi(
       const uint32_t* c2 = reinterpret_cast<const uint32_t*>(codes);
       const uint32_t np = n / 2;
       uint32_t p = tid;
-      constexpr int kP = 4;
+      constexpr int kP = kMax ? 4 : 2;  // fewer loads in flight at 32 warps
       // warp-uniform bound: the batch claims are warp-synchronous
       for (; (p - lane) + 31 + (kP - 1) * nth < np; p += kP * nth) {
         double2 vx[kP], vy[kP];
@@ -1036,8 +1043,10 @@ __global__ void __launch_bounds__(kSpThreads, 1) k_sp_phi(
     }
   }
   __syncthreads();
-  uint32_t* pp = phi_part + (size_t)blockIdx.x * kSpBuckets;
-  for (uint32_t b = threadIdx.x; b < kSpBuckets; b += blockDim.x) pp[b] = s_phi[b];
+  if (kMax) {
+    uint32_t* pp = phi_part + (size_t)blockIdx.x * kSpBuckets;
+    for (uint32_t b = threadIdx.x; b < kSpBuckets; b += blockDim.x) pp[b] = s_phi[b];
+  }
   for (uint32_t p = threadIdx.x; p < kSpParts; p += blockDim.x)
 #pragma unroll
     for (int hh = 0; hh < 2; ++hh)  // partition-major over the 2G lists
@@ -1057,6 +1066,45 @@ __global__ void __launch_bounds__(kSpThreads, 1) k_sp_phi(
     atomicMin(&st->phi_lo, ord_f(plo));
     atomicMax(&st->phi_hi, ord_f(phi_));
   }
+}
+
+// Bucket maxima of the stored walk angles (F3 with kMax = false): a light
+// pass over the codes and phi (6 B/pt) with the shared-memory maxima F3
+// would have kept. Gathered buckets and points within r0 (NaN) are skipped.
+__global__ void __launch_bounds__(1024, 1) k_sp_phimax_codes(const uint16_t* __restrict__ codes,
+                                                             const float* __restrict__ phi32,
+                                                             const uint32_t* __restrict__ gbits,
+                                                             uint32_t n, const SpState* __restrict__ st,
+                                                             uint32_t* __restrict__ phi_part) {
+  extern __shared__ uint32_t s_phi[];  // kSpBuckets
+  __shared__ uint32_t s_g[kSpBuckets / 32];
+  if (st->fail) return;
+  for (uint32_t b = threadIdx.x; b < kSpBuckets; b += blockDim.x) s_phi[b] = 0;
+  for (uint32_t w = threadIdx.x; w < kSpBuckets / 32; w += blockDim.x) s_g[w] = gbits[w];
+  __syncthreads();
+  auto visit = [&](uint32_t b, float ph) {
+    if (b != kSpNoCode && !sp_gathered(s_g, b) && !isnan(ph)) atomicMax(&s_phi[b], ord_f(ph));
+  };
+  const uint4* c8 = reinterpret_cast<const uint4*>(codes);
+  const float4* p4 = reinterpret_cast<const float4*>(phi32);
+  const uint32_t n8 = n / 8, nth = gridDim.x * blockDim.x;
+  for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < n8; q += nth) {
+    const uint4 c = __ldcs(&c8[q]);
+    const uint32_t w[4] = {c.x, c.y, c.z, c.w};
+    if (((w[0] & w[1] & w[2] & w[3]) == 0xffffffffu)) continue;  // no survivor among the 8
+    const float4 a = __ldcs(&p4[2 * q]), bq = __ldcs(&p4[2 * q + 1]);
+    const float f[8] = {a.x, a.y, a.z, a.w, bq.x, bq.y, bq.z, bq.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      visit(w[k] & 0xffffu, f[2 * k]);
+      visit(w[k] >> 16, f[2 * k + 1]);
+    }
+  }
+  for (uint32_t i = n8 * 8 + blockIdx.x * blockDim.x + threadIdx.x; i < n; i += nth)
+    visit(codes[i], phi32[i]);
+  __syncthreads();
+  uint32_t* pp = phi_part + (size_t)blockIdx.x * kSpBuckets;
+  for (uint32_t b = threadIdx.x; b < kSpBuckets; b += blockDim.x) pp[b] = s_phi[b];
 }
 
 __device__ __forceinline__ uint32_t sm_id() {
@@ -1694,7 +1742,6 @@ __global__ void __launch_bounds__(kSpCandThreads, 1) k_sp_cand(
     for (uint32_t q = threadIdx.x; q < kSpBuckets / 4; q += blockDim.x) s4[q] = __ldg(&t4[q]);
   }
   if (threadIdx.x == 0) s_nc = 0;
-  const uint32_t b_l = st->b_l;
   const size_t base = (size_t)blockIdx.x * cap;
   __syncthreads();
   auto visit = [&](float ph, uint32_t b, uint32_t i) {
@@ -1703,7 +1750,7 @@ __global__ void __launch_bounds__(kSpCandThreads, 1) k_sp_cand(
     bool emit = false;
     if (b != kSpNoCode) {
       const float thr = s_thr[b];
-      emit = !drop && thr != __int_as_float(0x7f800000) && !((b < b_l ? ph : -ph) < thr);
+      emit = !drop && thr != __int_as_float(0x7f800000) && !(ph < thr);  // ph is signed
     }
     const uint32_t j = warp_claim(&s_nc, emit);
     if (emit) {
@@ -1738,7 +1785,7 @@ __global__ void __launch_bounds__(kSpCandThreads, 1) k_sp_cand(
         bool e = false;
         if (b != kSpNoCode) {
           const float thr = s_thr[b];
-          e = !drop && thr != __int_as_float(0x7f800000) && !((b < b_l ? ph : -ph) < thr);
+          e = !drop && thr != __int_as_float(0x7f800000) && !(ph < thr);
         }
         em |= (e ? 1u : 0u) << (2 * u + hh);
         ne += e ? 1u : 0u;
