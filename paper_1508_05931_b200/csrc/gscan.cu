@@ -1054,16 +1054,12 @@ int sp_seg_f2(gscan_handle* h, const SpCtx& c) {
     k_sp_hist_codes<<<c.G, 1024, c.smem_nb, s>>>(h->sp_codes, c.n, h->sp_hist_part, h->sp_st);
   }
   {
-    Launch L(h, "k_sp_check_r1", s);
-    k_sp_check_r1<<<1, 32, 0, s>>>(h->ctr, c.n, h->sp_st);
-  }
-  {
     Launch L(h, "k_sp_reduce_hist", s);
     k_sp_reduce_cols<false><<<(c.nb + 255) / 256, 256, 0, s>>>(h->sp_hist_part, c.G, c.nb, h->sp_hist);
   }
   {
     Launch L(h, "k_sp_plan_pl", s);
-    k_sp_plan_pl<<<1, 256, 0, s>>>(c.xs, c.ys, h->sp_d2, g2, h->sp_st);
+    k_sp_plan_pl<<<1, 256, 0, s>>>(c.xs, c.ys, h->sp_d2, g2, h->sp_st, h->ctr, c.n);
   }
   return GSCAN_OK;
 }
@@ -1088,12 +1084,9 @@ int sp_seg_plan(gscan_handle* h, const SpCtx& c) {
 int sp_seg_f3(gscan_handle* h, const SpCtx& c) {
   cudaStream_t s = c.s;
   {
-    Launch L(h, "k_sp_steps", s);
-    k_sp_steps<<<1, 32, 0, s>>>(h->sp_bstart, c.chunks, h->sp_st);
-  }
-  {
     Launch L(h, "k_sp_gbits", s);
-    k_sp_gbits<<<c.nb / 256, 256, 0, s>>>(h->sp_bstart, h->sp_st, h->sp_gbits, h->sp_glist);
+    k_sp_gbits<<<c.nb / 256, 256, 0, s>>>(h->sp_bstart, c.chunks, h->sp_st, h->sp_gbits,
+                                          h->sp_glist);
   }
   if (!c.sharded) {
     // gathered buckets stored compactly (gs[b]): their records and sorted
@@ -1180,10 +1173,6 @@ int sp_seg_f4(gscan_handle* h, const SpCtx& c) {
     k_sp_cand<<<c.G, kSpCandThreads, c.smem_nb, s>>>(h->sp_codes, h->sp_phi32, c.n, c.cap,
                                                      h->sp_thr, h->sp_st, h->surv, h->sp_eb,
                                                      h->sp_ccount, c.drop);
-  }
-  {
-    Launch L(h, "k_sp_check_cand", s);
-    k_sp_check_cand<<<1, 32, 0, s>>>(h->sp_st);
   }
   return GSCAN_OK;
 }

@@ -73,6 +73,8 @@ enum : uint32_t {
   kSpFailFew = 128u,      // too few points for the bucket structure
   kSpFailMany = 256u,     // too many walk candidates (the full sort is faster)
 };
+// more than m / kSpManyDiv candidates after F4: decline (the full sort is faster)
+constexpr uint32_t kSpManyDiv = 8;
 
 struct SpD2 {        // per-CTA farthest-point candidate
   uint64_t d2;       // bits of dist2 (non-negative double: bit order = value order)
@@ -694,7 +696,11 @@ __device__ __forceinline__ bool has_left_seed(uint32_t lo, uint32_t hi, uint32_t
 __global__ void __launch_bounds__(256) k_sp_plan_pl(const double* __restrict__ xs,
                                                     const double* __restrict__ ys,
                                                     const SpD2* __restrict__ d2part, uint32_t nparts,
-                                                    SpState* __restrict__ st) {
+                                                    SpState* __restrict__ st,
+                                                    const Counters* __restrict__ ctr, uint32_t n) {
+  // >= 90% of the points survive round 1 (near-convex input): nearly all would
+  // be walk candidates, the full sort is faster (a speed decision)
+  if (threadIdx.x == 0 && (uint64_t)ctr->n1 * 10 > (uint64_t)n * 9) atomicOr(&st->fail, kSpFailMany);
   __shared__ uint64_t s_d[8];
   __shared__ uint32_t s_i[8], s_t[8];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -801,32 +807,36 @@ __global__ void __launch_bounds__(256) k_sp_lrank(const double* __restrict__ xs,
   if (below) atomicAdd(&st->l_below, below);
 }
 
-// (d) slice geometry from the exact l.
-__global__ void k_sp_steps(const uint32_t* __restrict__ bstart, uint64_t chunk_count,
-                           SpState* __restrict__ st) {
-  if (threadIdx.x != 0 || st->fail) return;
-  const uint32_t l = 1 + bstart[st->b_l] + st->l_below, M = st->M;
-  st->l = l;
-  const uint32_t c = (uint32_t)(chunk_count < 0xffffffffull ? chunk_count : 0xffffffffull);
-  const uint32_t mr = l - 1, ml = M - 1 - l;
-  if (mr < 2 || ml < 2) { st->fail |= kSpFailTiny; return; }
-  st->step_r = cdiv(mr, c);
-  st->n_right = cdiv(mr, st->step_r);
-  st->step_l = cdiv(ml, c);
-  st->n_left = cdiv(ml, st->step_l);
-}
 
 // (e) gathered buckets: P_l's bucket and every bucket holding a seed.
 __global__ void __launch_bounds__(256) k_sp_gbits(const uint32_t* __restrict__ bstart,
-                                                  SpState* __restrict__ st,
+                                                  uint64_t chunk_count, SpState* __restrict__ st,
                                                   uint32_t* __restrict__ gbits,
                                                   uint32_t* __restrict__ glist) {
   // a thread per bucket, a warp per bitmap word
   const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;  // kSpBuckets is a multiple of 256
   const uint32_t lane = threadIdx.x & 31;
   bool g = false;
-  if (!st->fail) {
-    const uint32_t b_l = st->b_l, M = st->M, sr = st->step_r, sl = st->step_l;
+  // slice geometry from the exact l (discard.hpp:90-124), computed by every
+  // thread, stored by one
+  bool ok = !st->fail;
+  const uint32_t b_l = st->b_l, M = st->M;
+  const uint32_t l = 1 + bstart[b_l] + st->l_below;
+  const uint32_t cc = (uint32_t)(chunk_count < 0xffffffffull ? chunk_count : 0xffffffffull);
+  const uint32_t mr = l - 1, ml = M - 1 - l;
+  if (ok && (mr < 2 || ml < 2)) {
+    if (b == 0) atomicOr(&st->fail, kSpFailTiny);
+    ok = false;
+  }
+  const uint32_t sr = ok ? cdiv(mr, cc) : 1u, sl = ok ? cdiv(ml, cc) : 1u;
+  if (ok && b == 0) {
+    st->l = l;
+    st->step_r = sr;
+    st->n_right = cdiv(mr, sr);
+    st->step_l = sl;
+    st->n_left = cdiv(ml, sl);
+  }
+  if (ok) {
     const uint32_t lo = 1 + bstart[b], hi = bstart[b + 1];
     if (hi >= lo) {  // non-empty
       g = (b == b_l);
@@ -1293,11 +1303,17 @@ __global__ void __launch_bounds__(256) k_sp_emit_place(
     const uint32_t* __restrict__ e_b, uint32_t* __restrict__ e_rank,
     const uint32_t* __restrict__ e_count, uint32_t cap, uint32_t* __restrict__ cnt,
     const uint32_t* __restrict__ start, const ExtResult* __restrict__ ext,
-    const SpState* __restrict__ st, PtRec* __restrict__ rec,
+    SpState* __restrict__ st, PtRec* __restrict__ rec,
     const double* __restrict__ e_x = nullptr, const double* __restrict__ e_y = nullptr) {
   // e_x, e_y: the emitted points' coordinates in the region slots (F3 writes
   // them for gathered points, so no random reads of xs, ys); else xs[i], ys[i]
   if (st->fail) return;
+  if (kPhase == 1 && st->n_c > max(st->m / kSpManyDiv, 65536u)) {
+    // after F4: too many candidates (points near a circle); the full sort is
+    // faster -- decline, every CTA sees the same count
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) atomicOr(&st->fail, kSpFailMany);
+    return;
+  }
   const uint32_t c = blockIdx.y;
   const uint32_t ne = e_count[c];
   const size_t base = (size_t)c * cap;
@@ -1820,25 +1836,10 @@ __global__ void __launch_bounds__(kSpCandThreads, 1) k_sp_cand(
   }
 }
 
+
+
 // Walk-array bucket sizes: gathered buckets bring all their points, others
 // their candidates.
-// After F2: when >= 90% of the points survive round 1 (points in near-convex
-// position: circles, thin annuli) nearly all of them become walk candidates;
-// decline before F3.
-__global__ void k_sp_check_r1(const Counters* __restrict__ ctr, uint32_t n,
-                              SpState* __restrict__ st) {
-  if (threadIdx.x == 0 && (uint64_t)ctr->n1 * 10 > (uint64_t)n * 9) atomicOr(&st->fail, kSpFailMany);
-}
-
-// After F4: with more than m / kSpManyDiv candidates (points near a circle)
-// the candidate sort and walk cost more than the full sort; decline, so the
-// remaining sparse kernels exit at once.
-constexpr uint32_t kSpManyDiv = 8;
-__global__ void k_sp_check_cand(SpState* __restrict__ st) {
-  if (threadIdx.x == 0 && !st->fail && st->n_c > max(st->m / kSpManyDiv, 65536u))
-    atomicOr(&st->fail, kSpFailMany);
-}
-
 __global__ void k_sp_wcount(const uint32_t* __restrict__ gbits, const uint32_t* __restrict__ hist,
                             const uint32_t* __restrict__ ccnt, uint32_t* __restrict__ wcnt) {
   const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
