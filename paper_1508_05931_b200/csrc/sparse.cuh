@@ -1836,8 +1836,6 @@ __global__ void __launch_bounds__(kSpCandThreads, 1) k_sp_cand(
   }
 }
 
-
-
 // Walk-array bucket sizes: gathered buckets bring all their points, others
 // their candidates.
 __global__ void k_sp_wcount(const uint32_t* __restrict__ gbits, const uint32_t* __restrict__ hist,
