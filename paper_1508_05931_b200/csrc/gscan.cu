@@ -157,6 +157,11 @@ struct gscan_handle {
   uint32_t dist_n = 0, dist_base = 0;
   uint64_t dist_chunks = 0;
   float* sp_thr = nullptr;  // F4 candidate thresholds per bucket
+  // look-back state of the sparse path's scans, one slot per use, cleared once
+  // per call (sp_seg_init) instead of two memsets per scan
+  uint64_t* lb_status = nullptr;
+  Counters* lb_ctr = nullptr;
+  uint64_t lb_stride = 0;  // status words per slot
   uint32_t *sp_gs = nullptr, *sp_gsz = nullptr, *dist_ctr = nullptr, *dist_pm = nullptr,
            *dist_hc = nullptr;
   uint64_t* dist_lb = nullptr;
@@ -198,7 +203,7 @@ void free_buffers(gscan_handle* h) {
   dfree(h->g_parent); dfree(h->g_btop); dfree(h->g_jk); dfree(h->g_je); dfree(h->g_jmin);
   dfree(h->g_keep); dfree(h->g_misc);
   dfree(h->g_stA); dfree(h->g_stB); dfree(h->g_lenA); dfree(h->g_lenB); dfree(h->g_scr);
-  dfree(h->sp_eb); dfree(h->sp_gx); dfree(h->sp_gy); dfree(h->sp_Wb); dfree(h->sp_Ws); dfree(h->sp_Rb); dfree(h->sp_Rs); dfree(h->sp_dup);
+  dfree(h->lb_status); dfree(h->lb_ctr); dfree(h->sp_eb); dfree(h->sp_gx); dfree(h->sp_gy); dfree(h->sp_Wb); dfree(h->sp_Ws); dfree(h->sp_Rb); dfree(h->sp_Rs); dfree(h->sp_dup);
   dfree(h->sp_codes); dfree(h->sp_phi32); dfree(h->sp_dup2); dfree(h->tw_pool);
   h->tw_nmax = 0;
   h->g_st_cap = 0;
@@ -227,6 +232,9 @@ uint32_t sparse_region_cap(const gscan_handle* h, uint64_t n) {
   }
   return (uint32_t)cap;
 }
+
+// look-back slots of the sparse path's scans (scan_u32_slot)
+enum LbSlot { kLbBstart = 0, kLbGs, kLbCstart, kLbWstart, kLbCompact, kLbSlots };
 
 int reserve(gscan_handle* h, uint64_t n) {
   if (n <= h->cap) return GSCAN_OK;
@@ -276,6 +284,10 @@ int reserve(gscan_handle* h, uint64_t n) {
                          ((uint64_t)kSpParts * std::max(2 * h->sm_count, 64) + kScanTile) / kScanTile;
   h->status_cap = tiles;
   CU(cudaMalloc(&h->status, tiles * 8));
+  h->lb_stride = std::max<uint64_t>((kSpBuckets + 2 + kScanTile - 1) / kScanTile,
+                                    m / kCompactTile + 2) + 2;
+  CU(cudaMalloc(&h->lb_status, (size_t)kLbSlots * h->lb_stride * 8));
+  CU(cudaMalloc(&h->lb_ctr, (size_t)kLbSlots * sizeof(Counters)));
   CU(cudaMalloc(&h->sp_eb, mr * 4));
   CU(cudaMalloc(&h->sp_gx, mr * 8));
   CU(cudaMalloc(&h->sp_gy, mr * 8));
@@ -322,6 +334,17 @@ struct Launch {
     if (kt) cudaEventRecord(kt->b, st);
   }
 };
+
+// Exclusive scan on a pre-cleared look-back slot (no memsets: one graph node).
+int scan_u32_slot(gscan_handle* h, const uint32_t* in, uint32_t n, uint32_t* out, int slot,
+                  cudaStream_t s) {
+  const uint64_t tiles = (n + 1 + kScanTile - 1) / kScanTile;
+  if (tiles > h->lb_stride) return fail(h, GSCAN_E_INTERNAL, "look-back slot too small");
+  Launch L(h, "k_scan_u32", s);
+  k_scan_u32<<<tiles, kBlock, 0, s>>>(in, n, out, h->lb_status + (size_t)slot * h->lb_stride,
+                                      h->lb_ctr + slot);
+  return GSCAN_OK;
+}
 
 int reset_lookback(gscan_handle* h, uint64_t tiles) {
   if (tiles > h->status_cap) return fail(h, GSCAN_E_INTERNAL, "look-back status too small");
@@ -999,6 +1022,8 @@ int sp_seg_init(gscan_handle* h, const SpCtx& c) {
   CU(cudaMemsetAsync(h->sp_prefmax, 0, c.nb * 4, s));
   CU(cudaMemsetAsync(h->sp_slice, 0xff, c.nb * 4, s));
   CU(cudaMemsetAsync(h->sp_cells, 0, kSpCells * 4, s));
+  CU(cudaMemsetAsync(h->lb_status, 0, (size_t)kLbSlots * h->lb_stride * 8, s));
+  CU(cudaMemsetAsync(h->lb_ctr, 0, (size_t)kLbSlots * sizeof(Counters), s));
   return GSCAN_OK;
 }
 
@@ -1067,7 +1092,7 @@ int sp_seg_f2(gscan_handle* h, const SpCtx& c) {
 // bucket starts (exact ranks), P_l's bucket and its rank inside it
 int sp_seg_plan(gscan_handle* h, const SpCtx& c) {
   cudaStream_t s = c.s;
-  TRY(scan_u32(h, h->sp_hist, c.nb, h->sp_bstart));
+  TRY(scan_u32_slot(h, h->sp_hist, c.nb, h->sp_bstart, kLbBstart, s));
   {
     Launch L(h, "k_sp_plan_bl", s);
     k_sp_plan_bl<<<1, 32, 0, s>>>(h->ext, h->sp_cdf, h->sp_th, h->sp_bstart, h->sp_st);
@@ -1095,7 +1120,7 @@ int sp_seg_f3(gscan_handle* h, const SpCtx& c) {
     Launch L(h, "k_sp_gsize", s);
     k_sp_gsize<<<(c.nb + 255) / 256, 256, 0, s>>>(h->sp_gbits, h->sp_hist, h->sp_gsz);
   }
-  if (!c.sharded) TRY(scan_u32(h, h->sp_gsz, c.nb, h->sp_gs));
+  if (!c.sharded) TRY(scan_u32_slot(h, h->sp_gsz, c.nb, h->sp_gs, kLbGs, s));
   TRY(rec_event(h, h->ev[1], s));
   {
     Launch L(h, "k_sp_phi", s);
@@ -1189,7 +1214,7 @@ int sp_seg_walk(gscan_handle* h, const SpCtx& c, const double* cx, const double*
                                                     h->sp_ccount, c.cap, h->sp_ccnt, nullptr,
                                                     h->ext, h->sp_st, h->rec);
   }
-  TRY(scan_u32(h, h->sp_ccnt, nb, h->sp_cstart));
+  TRY(scan_u32_slot(h, h->sp_ccnt, nb, h->sp_cstart, kLbCstart, s));
   {
     Launch L(h, "k_sp_place_c", s);
     k_sp_emit_place<2><<<dim3(4, c.G), 256, 0, s>>>(cx, cy, h->surv, h->sp_eb, h->rank,
@@ -1200,7 +1225,7 @@ int sp_seg_walk(gscan_handle* h, const SpCtx& c, const double* cx, const double*
     Launch L(h, "k_sp_wcount", s);
     k_sp_wcount<<<(nb + 255) / 256, 256, 0, s>>>(h->sp_gbits, h->sp_hist, h->sp_ccnt, h->sp_wcnt);
   }
-  TRY(scan_u32(h, h->sp_wcnt, nb, h->sp_wstart));
+  TRY(scan_u32_slot(h, h->sp_wcnt, nb, h->sp_wstart, kLbWstart, s));
   {
     Launch L(h, "k_sp_place_cand", s);
     k_sp_place_cand<<<nb / 8, 256, 0, s>>>(h->rec, h->sp_cstart, h->sp_wstart, h->sp_slice,
@@ -1231,11 +1256,11 @@ int sp_seg_walk(gscan_handle* h, const SpCtx& c, const double* cx, const double*
   }
   {
     const uint64_t tiles = (uint64_t)n_walk_cap / kCompactTile + 2;
-    TRY(reset_lookback(h, tiles));
+    if (tiles > h->lb_stride) return fail(h, GSCAN_E_INTERNAL, "look-back slot too small");
     Launch L(h, "k_sp_compact", s);
-    k_sp_compact<<<(uint32_t)tiles, kBlock, 0, s>>>(h->C_x, h->C_y, h->C_i, h->sp_Wb, h->sp_Ws,
-                                                    h->flags, h->sp_st, h->A_x, h->A_y, h->A_i,
-                                                    h->sp_Rb, h->sp_Rs, h->status, h->ctr);
+    k_sp_compact<<<(uint32_t)tiles, kBlock, 0, s>>>(
+        h->C_x, h->C_y, h->C_i, h->sp_Wb, h->sp_Ws, h->flags, h->sp_st, h->A_x, h->A_y, h->A_i,
+        h->sp_Rb, h->sp_Rs, h->lb_status + (size_t)kLbCompact * h->lb_stride, h->lb_ctr + kLbCompact);
   }
   // the duplicate check (side stream, sparse_dup_check) forks here, so it
   // overlaps the certificate and the Graham tail
