@@ -11,6 +11,8 @@ from pathlib import Path
 
 _PKG = Path(__file__).resolve().parent
 LIB_PATH = _PKG / "_lib" / "libgscan.so"
+if os.environ.get("GSCAN_LIB"):  # development: an alternative build (tools/micro)
+    LIB_PATH = Path(os.environ["GSCAN_LIB"])
 
 GSCAN_OK = 0
 GSCAN_E_EMPTY_INPUT = 1

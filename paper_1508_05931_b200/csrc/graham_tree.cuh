@@ -40,16 +40,25 @@
 
 namespace gscan {
 
-constexpr int kTreeChunk = 32;      // chunk length on levels >= 1
+#ifndef GSCAN_TREE_CS1
+#define GSCAN_TREE_CS1 32
+#endif
+#ifndef GSCAN_TREE_CS_HI
+#define GSCAN_TREE_CS_HI 32
+#endif
 constexpr int kTreeChunk0 = 16;     // level 0 (the buffer): the widest level and the certificate
-__host__ __device__ constexpr uint32_t tree_cs(int j) { return j == 0 ? kTreeChunk0 : kTreeChunk; }
+constexpr int kTreeChunk = GSCAN_TREE_CS1;     // level 1 (many CTAs)
+constexpr int kTreeChunkHi = GSCAN_TREE_CS_HI;  // levels >= 2 (one CTA)
+__host__ __device__ constexpr uint32_t tree_cs(int j) {
+  return j == 0 ? kTreeChunk0 : (j == 1 ? kTreeChunk : kTreeChunkHi);
+}
 constexpr int kTreeThreads = 256;   // the middle CTA; chunks are processed in waves of this many
 constexpr uint32_t kTreeTop = 128;       // levels stop shrinking once this small
 constexpr uint32_t kTreeTopMax = 3072;   // largest top level (a level that stops
                                          // shrinking is mostly final-hull vertices)
 constexpr int kTreeMaxLevels = 24;
 constexpr int kTreePC = 8;          // stack rows carried in a boundary record
-constexpr int kTreeRows = kTreePC + kTreeChunk;
+constexpr int kTreeRows = kTreePC + (kTreeChunk > kTreeChunkHi ? kTreeChunk : kTreeChunkHi);
 constexpr uint32_t kTreeHiCap = 1u << 18;  // level >= 1 capacity (larger: another strategy)
 constexpr uint8_t kTreeRec = 0xff;  // chunk index of a row loaded from a record
 constexpr int kTreeInfoWords = 48;  // info[] words (cleared by k_gr_setup, read back by the host)
@@ -76,6 +85,7 @@ struct TreeLevel {
   uint32_t* bt;   // top before each chunk (nch + 1)
   TreeRec rec;
   uint32_t nq, nch;
+  uint32_t cs;  // chunk length
 };
 
 // Workspace carved from one device buffer by the host; the kernel checks every
@@ -342,7 +352,8 @@ __device__ __forceinline__ TreeLevel tree_level(const TreeWork& w, int j, uint32
   L.bt = w.bt[j];
   L.rec = w.rec[j];
   L.nq = nq;
-  L.nch = (nq + tree_cs(j) - 1) / tree_cs(j);
+  L.cs = tree_cs(j);
+  L.nch = (nq + L.cs - 1) / L.cs;
   return L;
 }
 
@@ -443,9 +454,9 @@ __device__ __forceinline__ void tree_down_one(const TreeRows<T>& r, const TreeLe
                                               const double* __restrict__ R_x,
                                               const double* __restrict__ R_y, uint32_t* parent) {
   const uint32_t e = ll.off[cq];
-  const uint32_t c = e / kTreeChunk;
-  const int cnt = (int)(e - c * kTreeChunk);
-  tree_stage<T>(r, hl.Qp, hl.Qx, hl.Qy, c * kTreeChunk, cnt);
+  const uint32_t c = e / hl.cs;
+  const int cnt = (int)(e - c * hl.cs);
+  tree_stage<T>(r, hl.Qp, hl.Qx, hl.Qy, c * hl.cs, cnt);
   uint32_t B;
   const int n0 = tree_load_rec<T>(r, hl.rec, c, B);
   int lo_own = kTreeRows;
@@ -488,8 +499,8 @@ __global__ void __launch_bounds__(kTreeThreads, 1) k_gr_mid(
     for (uint32_t c0 = 0; c0 < L.nch; c0 += kTreeThreads) {
       const uint32_t c = c0 + t;
       if (c < L.nch) {
-        const uint32_t lo = c * kTreeChunk;
-        const int cnt = (int)min((uint32_t)kTreeChunk, L.nq - lo);
+        const uint32_t lo = c * L.cs;
+        const int cnt = (int)min(L.cs, L.nq - lo);
         tree_stage<kTreeThreads>(r, L.Qp, L.Qx, L.Qy, lo, cnt);
         uint32_t B = kNone;
         int lo_own = kTreeRows;

@@ -296,7 +296,8 @@ int reserve(gscan_handle* h, uint64_t n) {
   CU(cudaMalloc(&h->sp_Rb, m * 4));
   CU(cudaMalloc(&h->sp_Rs, m * 4));
   CU(cudaMalloc(&h->sp_dup, (mr + 4096) * 8));
-  CU(cudaMalloc(&h->sp_dup2, (m + 4096) * 8));
+  // partitioned hashes: the runs are padded to whole sectors (k_sp_dup_part<true>)
+  CU(cudaMalloc(&h->sp_dup2, (m + 4096 + 3ull * kSpParts * 2 * (uint64_t)h->sm_count) * 8));
   CU(cudaMalloc(&h->sp_codes, (m + 1) * sizeof(uint16_t)));
   CU(cudaMalloc(&h->sp_phi32, (m + 1) * sizeof(float)));
   h->cap = n;
@@ -718,20 +719,24 @@ int tree_workspace(gscan_handle* h, uint32_t n_max) {
   }
   if (used > need) return fail(h, GSCAN_E_INTERNAL, "tree pool overflow");
   h->tw_nmax = N;
-  h->tw_nch1 = (uint32_t)(caps[1] / kTreeChunk + 1);
+  h->tw_nch1 = (uint32_t)(caps[1] / tree_cs(1) + 1);
   return GSCAN_OK;
 }
 
 // Enqueue the whole tree strategy on s. N = *n_dev (the sparse path's round-2
 // size) or n_host; the kernels no-op when *st_fail is set or when disabled.
 // The info words are copied to the pinned h->h_info at the end.
+uint32_t side_free_sms();
 int tree_enqueue(gscan_handle* h, const double* Rx, const double* Ry, const uint32_t* Ri,
                  const uint32_t* n_dev, uint32_t n_host, const uint32_t* st_fail, bool disable,
                  cudaStream_t s) {
   const TreeWork& w = h->tw;
   uint32_t* info = h->g_misc + 4;
   const uint32_t nch0 = (h->tw_nmax + kTreeChunk0 - 1) / kTreeChunk0;  // upper bounds
-  const uint32_t gmax = 4 * (uint32_t)h->sm_count;
+  // the grids loop grid-stride over chunks: one wave on the SMs the side
+  // stream leaves free (CTAs sized by the workspace bound would mostly find
+  // no chunk, in waves, each exit behind a read of info[])
+  const uint32_t gmax = 4 * std::max(side_free_sms(), 16u);
   const uint32_t g0 = std::min((nch0 + kTreeCta - 1) / kTreeCta, gmax);
   const uint32_t g1 = std::min((h->tw_nch1 + kTreeCta - 1) / kTreeCta, gmax);
   const uint32_t dbg = (h->debug & GSCAN_DEBUG_CORRUPT_CANDIDATE) ? 1u : 0u;
@@ -1327,17 +1332,21 @@ int sparse_enqueue(gscan_handle* h, const double* xs, const double* ys, uint32_t
   return GSCAN_OK;
 }
 
-// Duplicate check on the low-priority side stream, after the sparse graph:
-// it overlaps the host read-back and the Graham tail (which leaves most SMs
-// idle) and is joined before the result is accepted.
+// Duplicate check on the low-priority side stream, forked inside the sparse
+// graph after the compaction: it overlaps the certificate and the Graham tail
+// (latency-bound kernels on few SMs) and joins the state read-back.
 // The side kernels run one CTA per SM except on kSideFreeSms SMs, each
 // reserving kSpSideSmem so that no Graham-tail CTA (kTreeCtaSmem) shares an SM
 // with them: those latency-bound CTAs get SMs of their own (sparse.cuh
-// side_take). Measured: 16-36 free SMs equally good; two smaller side CTAs
-// per SM, or leaving no SM free, slower.
+// side_take). Measured (C2): 16-36 free SMs equally good; two smaller side
+// CTAs per SM, or leaving no SM free, slower; a side kernel that only occupies
+// the SMs costs the main path ~30 us, the partitioning's partial-sector stores
+// cost another ~60 us (DRAM read-for-merge) until its runs were padded to
+// whole sectors (k_sp_dup_part<true>); forking later (inside the tree) is slower.
 constexpr uint32_t kSideFreeSms = 32;
-constexpr size_t kSpSideSmem = 180 * 1024;
-static_assert(kSpSideSmem >= kSpDupPartSmem && kSpSideSmem >= kSpDupSlots * 8, "side smem");
+constexpr size_t kSpSideSmem = kSpDupPartSmemPad;  // 208 KB
+static_assert(kSpSideSmem >= kSpDupPartSmem && kSpSideSmem >= kSpDupSmem && kSpSideSmem <= 226 * 1024,
+              "side smem");
 static_assert(kSpSideSmem + 1024 + kTreeCtaSmem + 1024 > 228 * 1024, "tree CTA would fit");
 uint32_t side_free_sms() {
   static const int v = getenv("GSCAN_SIDE_FREE") ? atoi(getenv("GSCAN_SIDE_FREE")) : (int)kSideFreeSms;
@@ -1354,6 +1363,10 @@ int sparse_dup_check(gscan_handle* h, uint32_t n) {
     const uint64_t tiles = ((uint64_t)kSpParts * nl + 1 + kScanTile - 1) / kScanTile;
     CU(cudaMemsetAsync(h->sp_side_status, 0, tiles * 8, h->side));
     CU(cudaMemsetAsync(h->sp_side_ticket, 0, sizeof(Counters), h->side));
+    {
+      Launch L(h, "k_sp_pad4", h->side);
+      k_sp_pad4<<<2 * h->sm_count, 1024, 0, h->side>>>(h->sp_part_off, kSpParts * nl);
+    }
     Launch L(h, "k_scan_u32(side)", h->side);
     k_scan_u32<<<tiles, kBlock, 0, h->side>>>(h->sp_part_off, kSpParts * nl, h->sp_part_off,
                                              h->sp_side_status, h->sp_side_ticket);
@@ -1361,7 +1374,7 @@ int sparse_dup_check(gscan_handle* h, uint32_t n) {
   CU(cudaMemsetAsync(h->sp_side_work, 0, 2 * sizeof(uint32_t), h->side));
   {
     Launch L(h, "k_sp_dup_part", h->side);
-    k_sp_dup_part<<<h->sm_count, 1024, kSpSideSmem, h->side>>>(
+    k_sp_dup_part<true><<<h->sm_count, 1024, kSpSideSmem, h->side>>>(
         h->sp_dup, h->sp_hcount, cap / 2, nl, h->sp_part_off, h->sp_st, h->sp_dup2, h->sp_side_work,
         side_free_sms(), nullptr);
   }
@@ -1449,7 +1462,12 @@ int run_sparse(gscan_handle* h, const double* xs, const double* ys, uint32_t n,
     h->launches += h->sp_graph_launches;
   }
 enqueued:
-  if (dup_check) TRY(sparse_dup_check(h, n));
+  if (dup_check) {
+    // the duplicate check's verdict joins the state read-back: one sync
+    TRY(sparse_dup_check(h, n));
+    CU(cudaStreamWaitEvent(s, h->ev_dup, 0));
+    CU(cudaMemcpyAsync(&h->h_sp->fail, &h->sp_st->fail, 4, cudaMemcpyDeviceToHost, s));
+  }
   TRY(sync_counters(h));
   const SpState sp = *h->h_sp;
   if (h->sp_debug) sp_debug_print(h, "[run]");
@@ -1457,7 +1475,6 @@ enqueued:
   h->sp_walked = sp.n_w;
   h->sp_cert = sp.cert;
   if (sp.fail) {
-    if (dup_check) CU(cudaStreamWaitEvent(s, h->ev_dup, 0));  // side stream done first
     ++h->sp_fallbacks;
     return GSCAN_OK;
   }
@@ -1470,17 +1487,9 @@ enqueued:
       TRY(stage_graham(h, h->A_x, h->A_y, h->A_i, sp.n_r, /*skip_tree=*/true));
       CU(cudaEventRecord(h->ev[5], s));
     }
-  }
-  if (dup_check) {
-    // the duplicate check must have passed for the result to count
-    CU(cudaStreamWaitEvent(s, h->ev_dup, 0));
-    CU(cudaMemcpyAsync(&h->h_sp->fail, &h->sp_st->fail, 4, cudaMemcpyDeviceToHost, s));
-  }
-  TRY(sync_counters(h));
-  if (dup_check && h->h_sp->fail) {
-    h->sp_fail = h->h_sp->fail;
-    ++h->sp_fallbacks;
-    return GSCAN_OK;
+    // the tree's result (hull count) came with the first read-back, unless
+    // more work was launched since
+    if (!done || (h->debug & GSCAN_DEBUG_FORCE_FALLBACK)) TRY(sync_counters(h));
   }
   const Counters& cc = *h->h_ctr;
   *hull_size = cc.hull;
@@ -1699,7 +1708,9 @@ int gscan_create(int device, gscan_handle** out) {
                             (int)kSpBigSmem));
     CU(cudaFuncSetAttribute(k_sp_dups, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)kSpSideSmem));
-    CU(cudaFuncSetAttribute(k_sp_dup_part, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CU(cudaFuncSetAttribute(k_sp_dup_part<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)kSpSideSmem));
+    CU(cudaFuncSetAttribute(k_sp_dup_part<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)kSpSideSmem));
     CU(cudaFuncSetAttribute(k_gr_mid, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTreeSmem));
     CU(cudaFuncSetAttribute(k_gr_up, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTreeCtaSmem));
@@ -2184,7 +2195,7 @@ int gscan_dist_dup_local(gscan_handle* h, uint32_t* d_part_counts, uint64_t* d_p
   TRY(read_u32(h, h->sp_part_off + (size_t)kSpParts * nl, &total));
   CU(cudaMemsetAsync(h->sp_side_work, 0, 2 * sizeof(uint32_t), c.s));
   k_sp_set_u32<<<1, 1, 0, c.s>>>(&h->sp_st->fail, 0u);  // the host decided the path globally
-  k_sp_dup_part<<<h->sm_count, 1024, kSpSideSmem, c.s>>>(h->sp_dup, h->sp_hcount, c.cap / 2, nl,
+  k_sp_dup_part<false><<<h->sm_count, 1024, kSpSideSmem, c.s>>>(h->sp_dup, h->sp_hcount, c.cap / 2, nl,
                                                         h->sp_part_off, h->sp_st, h->sp_dup2,
                                                         h->sp_side_work, 0u, nullptr);
   k_sp_part_totals<<<(kSpParts + 255) / 256, 256, 0, c.s>>>(h->sp_part_off, nl, total, d_part_counts);
@@ -2206,7 +2217,7 @@ int gscan_dist_dup_check(gscan_handle* h, const uint64_t* d_recv, uint64_t n_rec
   TRY(scan_u32(h, h->dist_pm, kSpParts * R, h->dist_pm));
   CU(cudaMemsetAsync(h->sp_side_work, 0, 2 * sizeof(uint32_t), c.s));
   k_sp_set_u32<<<1, 1, 0, c.s>>>(&h->sp_st->fail, 0u);
-  k_sp_dup_part<<<h->sm_count, 1024, kSpSideSmem, c.s>>>(d_recv, h->dist_hc, 0u, R, h->dist_pm,
+  k_sp_dup_part<false><<<h->sm_count, 1024, kSpSideSmem, c.s>>>(d_recv, h->dist_hc, 0u, R, h->dist_pm,
                                                         h->sp_st, h->sp_dup, h->sp_side_work, 0u,
                                                         h->dist_lb);
   k_sp_dups<<<h->sm_count, 1024, kSpSideSmem, c.s>>>(h->sp_dup, h->dist_pm, R, h->sp_st,

@@ -60,7 +60,7 @@ constexpr uint32_t kSpDupSlotBits = 14;
 constexpr uint32_t kSpDupSlots = 1u << kSpDupSlotBits;  // dup-check hash set slots (smem, 8 B)
 constexpr uint32_t kSpDupRound = 8192;        // entries per hash-set round (load <= 0.5)
 constexpr uint32_t kSpPartChunk = 8192;       // entries per partitioning chunk (smem)
-constexpr size_t kSpDupPartSmem = (size_t)kSpPartChunk * 16 + (size_t)kSpParts * 12;  // in/out + cnt/off/cursor
+constexpr size_t kSpDupPartSmem = (size_t)kSpPartChunk * 8 + (size_t)kSpParts * 16;  // out + cnt/off/cursor/base
 
 enum : uint32_t {
   kSpFailTie = 1u,        // several points share the maximal dist2
@@ -1137,10 +1137,21 @@ __device__ __forceinline__ bool side_take(uint32_t* ticket, uint32_t* s_item, ui
 }
 
 // Duplicate check, step 1: work item c moves hash list c (F3-CTA c / 2, half
-// c % 2; cap slots each) into the partitions. The list's run of partition p starts at the partition-major
-// exclusive scan of the counts (part_off[p * C + c]); the CTA owns those runs,
-// so the cursors live in shared memory. Chunks of kSpPartChunk entries are
-// grouped by partition in shared memory and written run by run.
+// c % 2; cap slots each) into the partitions. The list's run of partition p
+// starts at the partition-major exclusive scan of the counts (part_off[p * C
+// + c]); the CTA owns those runs, so the cursors live in shared memory.
+// Chunks of kSpPartChunk entries are grouped by partition in shared memory and
+// written run by run.
+// kPad (the single-GPU check): the counts were rounded up to whole 32-byte
+// sectors (4 entries) before the scan, and every store covers whole, aligned
+// sectors: a partition's last count % 4 entries of a chunk are carried to the
+// next chunk in shared memory, and the list's final carries are written with
+// ~0 padding (skipped by k_sp_dups). Stores of partial sectors cost DRAM
+// read-for-merge traffic that slowed the concurrent main path by ~60 us.
+constexpr size_t kSpDupPartSmemPad = ((size_t)kSpPartChunk + 3 * kSpParts) * 8 +
+                                     (size_t)kSpParts * 3 * 8 + (size_t)kSpParts * 6 * 4;
+
+template <bool kPad>
 __global__ void __launch_bounds__(1024) k_sp_dup_part(const uint64_t* __restrict__ hlist,
                                                       const uint32_t* __restrict__ h_count,
                                                       uint32_t cap, uint32_t C,
@@ -1150,11 +1161,15 @@ __global__ void __launch_bounds__(1024) k_sp_dup_part(const uint64_t* __restrict
                                                       uint32_t* __restrict__ ticket, uint32_t n_free,
                                                       const uint64_t* __restrict__ list_base) {
   extern __shared__ __align__(16) unsigned char smem[];
-  uint64_t* s_in = reinterpret_cast<uint64_t*>(smem);
-  uint64_t* s_out = s_in + kSpPartChunk;
-  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_out + kSpPartChunk);
-  uint32_t* s_off = s_cnt + kSpParts;
-  uint32_t* s_cur = s_off + kSpParts;
+  constexpr uint32_t kOut = kSpPartChunk + (kPad ? 3 * kSpParts : 0);
+  uint64_t* s_out = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* s_carry = s_out + kOut;  // [p * 3 + i] (kPad)
+  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_carry + (kPad ? 3 * kSpParts : 0));
+  uint32_t* s_off = s_cnt + kSpParts;   // where the chunk's entries of p go in s_out
+  uint32_t* s_cur = s_off + kSpParts;   // next parted slot of p
+  uint32_t* s_base = s_cur + kSpParts;  // s_out index t of p -> parted[s_base[p] + t]
+  uint32_t* s_cc = s_base + kSpParts;   // carried entries of p (kPad)
+  uint32_t* s_lim = s_cc + kSpParts;    // s_out indices of p below s_lim[p] are stored (kPad)
   __shared__ uint32_t s_w[32];
   __shared__ uint32_t s_item;
   if (st->fail || sm_id() < n_free) return;
@@ -1165,36 +1180,42 @@ __global__ void __launch_bounds__(1024) k_sp_dup_part(const uint64_t* __restrict
     for (uint32_t p = threadIdx.x; p < kSpParts; p += blockDim.x) {
       s_cur[p] = part_off[(size_t)p * C + c];
       s_cnt[p] = 0;
+      if (kPad) s_cc[p] = 0;
     }
-    // chunk = 8 entries per thread; the next chunk's loads are issued before
-    // the current one is grouped and written
-    uint64_t hv[8];
+    // chunk = 8 entries per thread, kept in registers with their rank among
+    // the chunk's entries of the same partition (the counting atomic's return);
+    // the next chunk's loads are issued before the current one is written
+    uint64_t hv[8], nv[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const uint32_t t = threadIdx.x + u * blockDim.x;
-      hv[u] = t < cnt ? src[t] : 0ull;
+      nv[u] = t < cnt ? src[t] : 0ull;
     }
     __syncthreads();
     for (uint32_t c0 = 0; c0 < cnt; c0 += kSpPartChunk) {
       const uint32_t len = min(kSpPartChunk, cnt - c0);
+      uint32_t rk[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
+        hv[u] = nv[u];
         const uint32_t t = threadIdx.x + u * blockDim.x;
-        if (t < len) {
-          s_in[t] = hv[u];
-          atomicAdd(&s_cnt[(uint32_t)(hv[u] >> (64 - kSpPartBits))], 1u);
-        }
+        rk[u] = t < len ? atomicAdd(&s_cnt[(uint32_t)(hv[u] >> (64 - kSpPartBits))], 1u) : 0u;
       }
       const uint32_t n0 = c0 + kSpPartChunk;
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         const uint32_t t = n0 + threadIdx.x + u * blockDim.x;
-        hv[u] = t < cnt ? src[t] : 0ull;
+        nv[u] = t < cnt ? src[t] : 0ull;
       }
       __syncthreads();
-      // exclusive scan of the partition counts (kSpParts = 2 x blockDim)
+      // exclusive scan of the group sizes (chunk count + carry; kSpParts = 2
+      // x blockDim); the owner of partitions 2t, 2t+1 also places their
+      // carries, clears their counts and advances their cursors
+      uint32_t ntot;
       {
-        const uint32_t a = s_cnt[2 * threadIdx.x], b = s_cnt[2 * threadIdx.x + 1];
+        const uint32_t q0 = 2 * threadIdx.x, q1 = q0 + 1;
+        const uint32_t cc0 = kPad ? s_cc[q0] : 0u, cc1 = kPad ? s_cc[q1] : 0u;
+        const uint32_t a = s_cnt[q0] + cc0, b = s_cnt[q1] + cc1;
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
         uint32_t x = a + b;
 #pragma unroll
@@ -1214,80 +1235,175 @@ __global__ void __launch_bounds__(1024) k_sp_dup_part(const uint64_t* __restrict
           s_w[lane] = v;
         }
         __syncthreads();
-        const uint32_t ex = x - (a + b) + (warp ? s_w[warp - 1] : 0);
-        s_off[2 * threadIdx.x] = ex;
-        s_off[2 * threadIdx.x + 1] = ex + a;
+        ntot = s_w[31];
+        const uint32_t e0 = x - (a + b) + (warp ? s_w[warp - 1] : 0), e1 = e0 + a;
+        const uint32_t c0_ = s_cur[q0], c1_ = s_cur[q1];
+        s_base[q0] = c0_ - e0;
+        s_base[q1] = c1_ - e1;
+        s_cnt[q0] = 0;
+        s_cnt[q1] = 0;
+        if constexpr (kPad) {
+          for (uint32_t i = 0; i < cc0; ++i) s_out[e0 + i] = s_carry[q0 * 3 + i];
+          for (uint32_t i = 0; i < cc1; ++i) s_out[e1 + i] = s_carry[q1 * 3 + i];
+          s_off[q0] = e0 + cc0;
+          s_off[q1] = e1 + cc1;
+          s_lim[q0] = e0 + (a & ~3u);
+          s_lim[q1] = e1 + (b & ~3u);
+          s_cc[q0] = a & 3u;
+          s_cc[q1] = b & 3u;
+          s_cur[q0] = c0_ + (a & ~3u);
+          s_cur[q1] = c1_ + (b & ~3u);
+        } else {
+          s_off[q0] = e0;
+          s_off[q1] = e1;
+          s_cur[q0] = c0_ + a;
+          s_cur[q1] = c1_ + b;
+        }
       }
       __syncthreads();
-      for (uint32_t t = threadIdx.x; t < len; t += blockDim.x) {
-        const uint64_t h = s_in[t];
-        const uint32_t p = (uint32_t)(h >> (64 - kSpPartBits));
-        s_out[atomicAdd(&s_off[p], 1u)] = h;  // s_off[p] ends at the next run's start
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const uint32_t t = threadIdx.x + u * blockDim.x;
+        if (t < len) s_out[s_off[(uint32_t)(hv[u] >> (64 - kSpPartBits))] + rk[u]] = hv[u];
       }
       __syncthreads();
-      for (uint32_t t = threadIdx.x; t < len; t += blockDim.x) {
+      // the next chunk's counting touches only s_cnt, cleared above; its scan
+      // rewrites the other arrays and s_out only after every thread passed
+      // its first barrier, i.e. finished this loop
+      for (uint32_t t = threadIdx.x; t < ntot; t += blockDim.x) {
         const uint64_t h = s_out[t];
         const uint32_t p = (uint32_t)(h >> (64 - kSpPartBits));
-        const uint32_t run0 = s_off[p] - s_cnt[p];
-        parted[s_cur[p] + (t - run0)] = h;
+        if (!kPad || t < s_lim[p]) parted[s_base[p] + t] = h;
+        else s_carry[p * 3 + (t - s_lim[p])] = h;
       }
-      __syncthreads();
+    }
+    __syncthreads();  // the item's carries, cursors and counters are final
+    if (kPad) {  // the list's last partial sectors, padded
       for (uint32_t p = threadIdx.x; p < kSpParts; p += blockDim.x) {
-        s_cur[p] += s_cnt[p];
-        s_cnt[p] = 0;
+        const uint32_t cc = s_cc[p];
+        if (cc) {
+          uint64_t* d = parted + s_cur[p];
+#pragma unroll
+          for (uint32_t i = 0; i < 4; ++i) d[i] = i < cc ? s_carry[p * 3 + i] : ~0ull;
+        }
       }
-      __syncthreads();
     }
   }
 }
 
-// Duplicate check, step 2: a partition per work item, open-addressing set of
-// its 64-bit hashes in shared memory (in rounds over sub-ranges of the hash);
-// an equal hash means a possible duplicate -> the full path (exact).
+// Rounds the partition counts up to whole sectors (4 entries) before the scan
+// (k_sp_dup_part<true>).
+__global__ void k_sp_pad4(uint32_t* __restrict__ a, uint32_t n) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    a[i] = (a[i] + 3u) & ~3u;
+}
+
+// Duplicate check, step 2: a partition per work item, open-addressing set in
+// shared memory. The two 512-thread halves of a CTA take items independently
+// (named barriers), so one half's load and barrier latencies hide behind the
+// other's probing. A slot holds 32 bits: a 17-bit tag (hash bits 14..30; the
+// slot is bits 0..13, the partition the top bits) and the entry's 15-bit
+// index in its partition; equal tags are confirmed on the full 64-bit hash
+// (one load, a few per call). An equal hash means a possible duplicate -> the
+// full path (exact). Partitions over the table's load limit are checked in
+// rounds over sub-ranges of the hash; partitions of 2^15 entries or more
+// (above ~67M round-1 survivors) set kSpFailCap.
+constexpr uint32_t kSpDupTagBits = 17;
+constexpr uint32_t kSpDupIdxBits = 15;
+static_assert(kSpDupSlotBits + kSpDupTagBits <= 64 - kSpPartBits, "tag bits overlap the partition");
+constexpr size_t kSpDupSmem = 2 * (size_t)kSpDupSlots * 4;
+
+__device__ __forceinline__ void named_sync(uint32_t id, uint32_t n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ bool named_sync_or(uint32_t id, uint32_t n, bool v) {
+  uint32_t r;
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\tsetp.ne.u32 p, %1, 0;\n\t"
+      "bar.red.or.pred q, %2, %3, p;\n\tselp.u32 %0, 1, 0, q;\n\t}"
+      : "=r"(r)
+      : "r"((uint32_t)v), "r"(id), "r"(n)
+      : "memory");
+  return r != 0;
+}
+
 __global__ void __launch_bounds__(1024) k_sp_dups(const uint64_t* __restrict__ parted,
                                                  const uint32_t* __restrict__ part_off,
                                                  uint32_t nparts_cta, SpState* __restrict__ st,
                                                  uint32_t* __restrict__ ticket, uint32_t n_free) {
-  extern __shared__ unsigned long long s_e[];  // kSpDupSlots
-  __shared__ uint32_t s_item;
+  extern __shared__ uint32_t s_tab[];  // 2 x kSpDupSlots
+  __shared__ uint32_t s_next[2];
   if (st->fail || sm_id() < n_free) return;
+  constexpr uint32_t kHalf = 512;
+  static_assert(kSpDupRound == 16 * kHalf, "two batches of 8 entries per thread");
+  const uint32_t half = threadIdx.x / kHalf, ht = threadIdx.x % kHalf, bar = 1 + half;
+  uint32_t* tab = s_tab + half * kSpDupSlots;
   const uint32_t total = part_off[(size_t)kSpParts * nparts_cta];  // the scan's total
   bool dup = false, full = false;
-  uint32_t p;
-  while (side_take(ticket, &s_item, kSpParts, p)) {
+  if (ht == 0) s_next[half] = atomicAdd(ticket, 1u);
+  named_sync(bar, kHalf);
+  uint32_t p = s_next[half];
+  while (p < kSpParts) {
     const uint32_t lo = part_off[(size_t)p * nparts_cta];
     const uint32_t hi = (p + 1 < kSpParts) ? part_off[(size_t)(p + 1) * nparts_cta] : total;
-    const uint32_t rounds = (hi - lo + kSpDupRound - 1) / kSpDupRound;
-    bool stop = false;
-    for (uint32_t r = 0; r < rounds; ++r) {
-      for (uint32_t k = threadIdx.x; k < kSpDupSlots; k += blockDim.x) s_e[k] = ~0ull;
-      __syncthreads();
-      for (uint32_t e0 = lo + threadIdx.x; e0 < hi && !dup && !full; e0 += 8 * blockDim.x) {
+    named_sync(bar, kHalf);  // the half has read s_next
+    // the next item's ticket is taken now and read after the closing barrier
+    if (ht == 0) s_next[half] = atomicAdd(ticket, 1u);
+    const uint32_t n = hi - lo;
+    if (n >= (1u << kSpDupIdxBits)) {
+      full = true;
+    } else {
+      const uint32_t rounds = (n + kSpDupRound - 1) / kSpDupRound;
+      for (uint32_t r = 0; r < rounds; ++r) {  // uniform over the half (named barriers)
+        // the first batch's loads are in flight while the table is cleared
         uint64_t hv[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-          const uint32_t e = e0 + u * blockDim.x;
+          const uint32_t e = lo + ht + u * kHalf;
           hv[u] = e < hi ? parted[e] : ~0ull;
         }
+        if (r) named_sync(bar, kHalf);  // the previous round's probes are done
+        uint4* t4 = reinterpret_cast<uint4*>(tab);
+        for (uint32_t k = ht; k < kSpDupSlots / 4; k += kHalf)
+          t4[k] = make_uint4(~0u, ~0u, ~0u, ~0u);
+        named_sync(bar, kHalf);
+        for (uint32_t e0 = lo + ht; e0 < hi; e0 += 8 * kHalf) {
+          if (e0 != lo + ht) {
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const uint64_t h = hv[u];
-          if (h == ~0ull || dup || full) continue;
-          const uint32_t mid = (uint32_t)(h >> 20) & 0xffffu;  // bits below the partition
-          if ((uint32_t)(((uint64_t)mid * rounds) >> 16) != r) continue;
-          uint32_t slot = (uint32_t)h & (kSpDupSlots - 1);
-          for (uint32_t probe = 0;; ++probe) {
-            if (probe == kSpDupSlots / 2) { full = true; break; }
-            const unsigned long long prev = atomicCAS(&s_e[slot], ~0ull, (unsigned long long)h);
-            if (prev == ~0ull) break;
-            if (prev == h) { dup = true; break; }
-            slot = (slot + 1) & (kSpDupSlots - 1);
+            for (int u = 0; u < 8; ++u) {
+              const uint32_t e = e0 + u * kHalf;
+              hv[u] = e < hi ? parted[e] : ~0ull;
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const uint64_t h = hv[u];
+            const uint32_t e = e0 + u * kHalf;
+            if (e >= hi || h == ~0ull || dup || full) continue;  // ~0: sector padding
+            if (rounds > 1) {
+              const uint32_t mid = (uint32_t)(h >> 20) & 0xffffu;  // bits below the partition
+              if ((uint32_t)(((uint64_t)mid * rounds) >> 16) != r) continue;
+            }
+            const uint32_t tag = (uint32_t)(h >> kSpDupSlotBits) & ((1u << kSpDupTagBits) - 1);
+            const uint32_t v = (tag << kSpDupIdxBits) | (e - lo);  // never ~0u: e - lo < 2^15 - 1
+            uint32_t slot = (uint32_t)h & (kSpDupSlots - 1);
+            for (uint32_t probe = 0;; ++probe) {
+              if (probe == kSpDupSlots / 2) { full = true; break; }  // a skewed round
+              const uint32_t prev = atomicCAS(&tab[slot], ~0u, v);
+              if (prev == ~0u) break;
+              if ((prev >> kSpDupIdxBits) == tag &&
+                  parted[lo + (prev & ((1u << kSpDupIdxBits) - 1))] == h) {
+                dup = true;
+                break;
+              }
+              slot = (slot + 1) & (kSpDupSlots - 1);
+            }
           }
         }
       }
-      if (__syncthreads_or(dup || full)) { stop = true; break; }
     }
-    if (stop) break;  // uniform
+    if (named_sync_or(bar, kHalf, dup || full)) break;  // also publishes s_next
+    p = s_next[half];
   }
   if (dup) { atomicAdd(&st->dups, 1u); atomicOr(&st->fail, kSpFailDup); }
   if (full) atomicOr(&st->fail, kSpFailCap);
