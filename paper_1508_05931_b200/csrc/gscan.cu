@@ -1133,7 +1133,7 @@ int sp_seg_f3(gscan_handle* h, const SpCtx& c) {
     const size_t sm3 = kF3Split ? 0 : c.smem_nb;
 #define A3 c.xs, c.ys, h->sp_codes, c.n, c.cap, h->ext, h->sp_gbits, h->sp_st, h->sp_phi_part, h->surv, \
            h->sp_eb, h->sp_gcount, h->sp_gx, h->sp_gy, h->sp_dup, h->sp_hcount, h->sp_part_off, \
-           h->sp_phi32
+           h->sp_phi32, c.sharded ? 0u : 3u
     if (kF3Split) {
       if (c.vec) k_sp_phi<true, false><<<c.G, t3, sm3, s>>>(A3);
       else k_sp_phi<false, false><<<c.G, t3, sm3, s>>>(A3);
@@ -1363,10 +1363,6 @@ int sparse_dup_check(gscan_handle* h, uint32_t n) {
     const uint64_t tiles = ((uint64_t)kSpParts * nl + 1 + kScanTile - 1) / kScanTile;
     CU(cudaMemsetAsync(h->sp_side_status, 0, tiles * 8, h->side));
     CU(cudaMemsetAsync(h->sp_side_ticket, 0, sizeof(Counters), h->side));
-    {
-      Launch L(h, "k_sp_pad4", h->side);
-      k_sp_pad4<<<2 * h->sm_count, 1024, 0, h->side>>>(h->sp_part_off, kSpParts * nl);
-    }
     Launch L(h, "k_scan_u32(side)", h->side);
     k_scan_u32<<<tiles, kBlock, 0, h->side>>>(h->sp_part_off, kSpParts * nl, h->sp_part_off,
                                              h->sp_side_status, h->sp_side_ticket);

@@ -56,9 +56,6 @@ constexpr uint32_t kSpParts = 1u << kSpPartBits;
 constexpr double kSpTol = 1e-6;               // candidate tolerance on phi (pseudo-angle units)
 constexpr double kSpPhiStoreErr = 1.2e-7;     // |phi| <= 2 stored as float: rounding <= 2^-23
 constexpr uint32_t kSpGatherCap = 4096;       // largest bucket sorted in smem
-constexpr uint32_t kSpDupSlotBits = 14;
-constexpr uint32_t kSpDupSlots = 1u << kSpDupSlotBits;  // dup-check hash set slots (smem, 8 B)
-constexpr uint32_t kSpDupRound = 8192;        // entries per hash-set round (load <= 0.5)
 constexpr uint32_t kSpPartChunk = 8192;       // entries per partitioning chunk (smem)
 constexpr size_t kSpDupPartSmem = (size_t)kSpPartChunk * 8 + (size_t)kSpParts * 16;  // out + cnt/off/cursor/base
 
@@ -901,7 +898,9 @@ __global__ void __launch_bounds__(kMax ? kSpThreads : 1024, 1) k_sp_phi(
     uint32_t* __restrict__ g_idx, uint32_t* __restrict__ g_b, uint32_t* __restrict__ g_count,
     double* __restrict__ g_x, double* __restrict__ g_y,  // gathered coordinates (same slots)
     uint64_t* __restrict__ hlist, uint32_t* __restrict__ h_count, uint32_t* __restrict__ part_cnt,
-    float* __restrict__ phi32) {
+    float* __restrict__ phi32, uint32_t pad) {
+  // pad = 3: the partition counts are written rounded up to whole sectors (4
+  // entries; k_sp_dup_part<true>), pad = 0: exact (the sharded exchange)
   extern __shared__ uint32_t s_phi[];  // kSpBuckets (kMax)
   __shared__ uint32_t s_g[kSpBuckets / 32];
   __shared__ uint32_t s_part[2][kSpParts];  // per half-CTA hash list
@@ -1060,7 +1059,7 @@ __global__ void __launch_bounds__(kMax ? kSpThreads : 1024, 1) k_sp_phi(
   for (uint32_t p = threadIdx.x; p < kSpParts; p += blockDim.x)
 #pragma unroll
     for (int hh = 0; hh < 2; ++hh)  // partition-major over the 2G lists
-      part_cnt[(size_t)p * 2 * gridDim.x + 2 * blockIdx.x + hh] = s_part[hh][p];
+      part_cnt[(size_t)p * 2 * gridDim.x + 2 * blockIdx.x + hh] = (s_part[hh][p] + pad) & ~pad;
   if (threadIdx.x == 0) {
     g_count[blockIdx.x] = s_ng;
     h_count[2 * blockIdx.x] = s_nh[0];
@@ -1143,7 +1142,7 @@ __device__ __forceinline__ bool side_take(uint32_t* ticket, uint32_t* s_item, ui
 // Chunks of kSpPartChunk entries are grouped by partition in shared memory and
 // written run by run.
 // kPad (the single-GPU check): the counts were rounded up to whole 32-byte
-// sectors (4 entries) before the scan, and every store covers whole, aligned
+// sectors (4 entries) by k_sp_phi, and every store covers whole, aligned
 // sectors: a partition's last count % 4 entries of a chunk are carried to the
 // next chunk in shared memory, and the list's final carries are written with
 // ~0 padding (skipped by k_sp_dups). Stores of partial sectors cost DRAM
@@ -1291,27 +1290,28 @@ __global__ void __launch_bounds__(1024) k_sp_dup_part(const uint64_t* __restrict
   }
 }
 
-// Rounds the partition counts up to whole sectors (4 entries) before the scan
-// (k_sp_dup_part<true>).
-__global__ void k_sp_pad4(uint32_t* __restrict__ a, uint32_t n) {
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    a[i] = (a[i] + 3u) & ~3u;
-}
-
 // Duplicate check, step 2: a partition per work item, open-addressing set in
-// shared memory. The two 512-thread halves of a CTA take items independently
-// (named barriers), so one half's load and barrier latencies hide behind the
-// other's probing. A slot holds 32 bits: a 17-bit tag (hash bits 14..30; the
-// slot is bits 0..13, the partition the top bits) and the entry's 15-bit
-// index in its partition; equal tags are confirmed on the full 64-bit hash
-// (one load, a few per call). An equal hash means a possible duplicate -> the
-// full path (exact). Partitions over the table's load limit are checked in
-// rounds over sub-ranges of the hash; partitions of 2^15 entries or more
-// (above ~67M round-1 survivors) set kSpFailCap.
+// shared memory. The CTA's kSpDupGroups thread groups take items
+// independently (named barriers), so one group's load and barrier latencies
+// hide behind the others' probing. A slot holds 32 bits: a 17-bit tag (hash
+// bits 32..48; the slot is a range reduction of bits 0..31, the partition the
+// top bits) and the entry's 15-bit index in its partition; equal tags are
+// confirmed on the full 64-bit hash (one load, a few per call). An equal hash
+// means a possible duplicate -> the full path (exact). Partitions over the
+// table's load limit are checked in rounds over sub-ranges of the hash;
+// partitions of 2^15 entries or more (above ~67M round-1 survivors) set
+// kSpFailCap.
+#ifndef GSCAN_DUPS_G
+#define GSCAN_DUPS_G 2
+#endif
+constexpr uint32_t kSpDupGroups = GSCAN_DUPS_G;
+constexpr uint32_t kSpDupGT = 1024 / kSpDupGroups;                       // threads per group
+constexpr uint32_t kSpDupGSlots = kSpDupGroups == 2 ? 16384u : 12288u;  // slots per group table
+constexpr uint32_t kSpDupGRound = 8192;  // entries per round (load <= 0.5 / 0.67)
 constexpr uint32_t kSpDupTagBits = 17;
 constexpr uint32_t kSpDupIdxBits = 15;
-static_assert(kSpDupSlotBits + kSpDupTagBits <= 64 - kSpPartBits, "tag bits overlap the partition");
-constexpr size_t kSpDupSmem = 2 * (size_t)kSpDupSlots * 4;
+static_assert(32 + kSpDupTagBits <= 64 - kSpPartBits, "tag bits overlap the partition");
+constexpr size_t kSpDupSmem = (size_t)kSpDupGroups * kSpDupGSlots * 4;
 
 __device__ __forceinline__ void named_sync(uint32_t id, uint32_t n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
@@ -1331,64 +1331,62 @@ __global__ void __launch_bounds__(1024) k_sp_dups(const uint64_t* __restrict__ p
                                                  const uint32_t* __restrict__ part_off,
                                                  uint32_t nparts_cta, SpState* __restrict__ st,
                                                  uint32_t* __restrict__ ticket, uint32_t n_free) {
-  extern __shared__ uint32_t s_tab[];  // 2 x kSpDupSlots
-  __shared__ uint32_t s_next[2];
+  extern __shared__ uint32_t s_tab[];  // kSpDupGroups x kSpDupGSlots
+  __shared__ uint32_t s_next[kSpDupGroups];
   if (st->fail || sm_id() < n_free) return;
-  constexpr uint32_t kHalf = 512;
-  static_assert(kSpDupRound == 16 * kHalf, "two batches of 8 entries per thread");
-  const uint32_t half = threadIdx.x / kHalf, ht = threadIdx.x % kHalf, bar = 1 + half;
-  uint32_t* tab = s_tab + half * kSpDupSlots;
+  constexpr uint32_t kGT = kSpDupGT, kB = 8;  // entries per thread per batch
+  const uint32_t grp = threadIdx.x / kGT, gt = threadIdx.x % kGT, bar = 1 + grp;
+  uint32_t* tab = s_tab + grp * kSpDupGSlots;
   const uint32_t total = part_off[(size_t)kSpParts * nparts_cta];  // the scan's total
   bool dup = false, full = false;
-  if (ht == 0) s_next[half] = atomicAdd(ticket, 1u);
-  named_sync(bar, kHalf);
-  uint32_t p = s_next[half];
+  if (gt == 0) s_next[grp] = atomicAdd(ticket, 1u);
+  named_sync(bar, kGT);
+  uint32_t p = s_next[grp];
   while (p < kSpParts) {
     const uint32_t lo = part_off[(size_t)p * nparts_cta];
     const uint32_t hi = (p + 1 < kSpParts) ? part_off[(size_t)(p + 1) * nparts_cta] : total;
-    named_sync(bar, kHalf);  // the half has read s_next
+    named_sync(bar, kGT);  // the group has read s_next
     // the next item's ticket is taken now and read after the closing barrier
-    if (ht == 0) s_next[half] = atomicAdd(ticket, 1u);
+    if (gt == 0) s_next[grp] = atomicAdd(ticket, 1u);
     const uint32_t n = hi - lo;
     if (n >= (1u << kSpDupIdxBits)) {
       full = true;
     } else {
-      const uint32_t rounds = (n + kSpDupRound - 1) / kSpDupRound;
-      for (uint32_t r = 0; r < rounds; ++r) {  // uniform over the half (named barriers)
+      const uint32_t rounds = (n + kSpDupGRound - 1) / kSpDupGRound;
+      for (uint32_t r = 0; r < rounds; ++r) {  // uniform over the group (named barriers)
         // the first batch's loads are in flight while the table is cleared
-        uint64_t hv[8];
+        uint64_t hv[kB];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const uint32_t e = lo + ht + u * kHalf;
+        for (uint32_t u = 0; u < kB; ++u) {
+          const uint32_t e = lo + gt + u * kGT;
           hv[u] = e < hi ? parted[e] : ~0ull;
         }
-        if (r) named_sync(bar, kHalf);  // the previous round's probes are done
+        if (r) named_sync(bar, kGT);  // the previous round's probes are done
         uint4* t4 = reinterpret_cast<uint4*>(tab);
-        for (uint32_t k = ht; k < kSpDupSlots / 4; k += kHalf)
-          t4[k] = make_uint4(~0u, ~0u, ~0u, ~0u);
-        named_sync(bar, kHalf);
-        for (uint32_t e0 = lo + ht; e0 < hi; e0 += 8 * kHalf) {
-          if (e0 != lo + ht) {
+        for (uint32_t k = gt; k < kSpDupGSlots / 4; k += kGT) t4[k] = make_uint4(~0u, ~0u, ~0u, ~0u);
+        named_sync(bar, kGT);
+        for (uint32_t e0 = lo + gt; e0 < hi; e0 += kB * kGT) {
+          if (e0 != lo + gt) {
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-              const uint32_t e = e0 + u * kHalf;
+            for (uint32_t u = 0; u < kB; ++u) {
+              const uint32_t e = e0 + u * kGT;
               hv[u] = e < hi ? parted[e] : ~0ull;
             }
           }
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
+          for (uint32_t u = 0; u < kB; ++u) {
             const uint64_t h = hv[u];
-            const uint32_t e = e0 + u * kHalf;
+            const uint32_t e = e0 + u * kGT;
             if (e >= hi || h == ~0ull || dup || full) continue;  // ~0: sector padding
             if (rounds > 1) {
               const uint32_t mid = (uint32_t)(h >> 20) & 0xffffu;  // bits below the partition
               if ((uint32_t)(((uint64_t)mid * rounds) >> 16) != r) continue;
             }
-            const uint32_t tag = (uint32_t)(h >> kSpDupSlotBits) & ((1u << kSpDupTagBits) - 1);
+            const uint32_t tag = (uint32_t)(h >> 32) & ((1u << kSpDupTagBits) - 1);
             const uint32_t v = (tag << kSpDupIdxBits) | (e - lo);  // never ~0u: e - lo < 2^15 - 1
-            uint32_t slot = (uint32_t)h & (kSpDupSlots - 1);
+            uint32_t slot = (uint32_t)(((uint64_t)(uint32_t)h * kSpDupGSlots) >> 32);
             for (uint32_t probe = 0;; ++probe) {
-              if (probe == kSpDupSlots / 2) { full = true; break; }  // a skewed round
+              if (probe == kSpDupGSlots / 2) { full = true; break; }  // a skewed round
               const uint32_t prev = atomicCAS(&tab[slot], ~0u, v);
               if (prev == ~0u) break;
               if ((prev >> kSpDupIdxBits) == tag &&
@@ -1396,14 +1394,14 @@ __global__ void __launch_bounds__(1024) k_sp_dups(const uint64_t* __restrict__ p
                 dup = true;
                 break;
               }
-              slot = (slot + 1) & (kSpDupSlots - 1);
+              slot = slot + 1 == kSpDupGSlots ? 0u : slot + 1;
             }
           }
         }
       }
     }
-    if (named_sync_or(bar, kHalf, dup || full)) break;  // also publishes s_next
-    p = s_next[half];
+    if (named_sync_or(bar, kGT, dup || full)) break;  // also publishes s_next
+    p = s_next[grp];
   }
   if (dup) { atomicAdd(&st->dups, 1u); atomicOr(&st->fail, kSpFailDup); }
   if (full) atomicOr(&st->fail, kSpFailCap);
