@@ -61,7 +61,7 @@ struct gscan_handle {
   cudaStream_t stream = nullptr;
   cudaStream_t side = nullptr;          // duplicate check runs here, overlapping the tail
   cudaStream_t cap_stream = nullptr;    // CUDA graph capture
-  cudaEvent_t ev_f3 = nullptr, ev_dup = nullptr;
+  cudaEvent_t ev_f3 = nullptr, ev_dup = nullptr, ev_part = nullptr;
   bool own_stream = false;
   int sm_count = 148;
   uint64_t cap = 0;  // points
@@ -1152,6 +1152,7 @@ int sp_seg_f3(gscan_handle* h, const SpCtx& c) {
     Launch L(h, "k_sp_reduce_phi", s);
     k_sp_reduce_cols<true><<<(c.nb + 255) / 256, 256, 0, s>>>(h->sp_phi_part, c.G, c.nb, h->sp_phimax);
   }
+  if (!c.sharded) TRY(rec_event(h, h->ev_part, s));  // the side stream's count scan forks here
   return GSCAN_OK;
 }
 
@@ -1358,7 +1359,9 @@ int sparse_dup_check(gscan_handle* h, uint32_t n) {
   const uint32_t nl = 2 * G;  // hash lists (k_sp_phi: two per CTA)
   static_assert(kSpPartChunk == 8 * 1024, "k_sp_dup_part: 8 entries per thread");
   const uint32_t cap = sparse_region_cap(h, n);
-  CU(cudaStreamWaitEvent(h->side, h->ev_f3, 0));  // recorded after k_sp_compact
+  // the scan of the partition counts needs only F3: it overlaps the main
+  // stream's sorts and walk; the partitioning waits for the compaction
+  CU(cudaStreamWaitEvent(h->side, h->ev_part, 0));  // recorded after k_sp_phi
   {
     const uint64_t tiles = ((uint64_t)kSpParts * nl + 1 + kScanTile - 1) / kScanTile;
     CU(cudaMemsetAsync(h->sp_side_status, 0, tiles * 8, h->side));
@@ -1368,6 +1371,7 @@ int sparse_dup_check(gscan_handle* h, uint32_t n) {
                                              h->sp_side_status, h->sp_side_ticket);
   }
   CU(cudaMemsetAsync(h->sp_side_work, 0, 2 * sizeof(uint32_t), h->side));
+  CU(cudaStreamWaitEvent(h->side, h->ev_f3, 0));  // recorded after k_sp_compact
   {
     Launch L(h, "k_sp_dup_part", h->side);
     k_sp_dup_part<true><<<h->sm_count, 1024, kSpSideSmem, h->side>>>(
@@ -1670,6 +1674,7 @@ int gscan_create(int device, gscan_handle** out) {
     }
     CU(cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
     CU(cudaEventCreateWithFlags(&h->ev_f3, cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&h->ev_part, cudaEventDisableTiming));
     CU(cudaEventCreateWithFlags(&h->ev_dup, cudaEventDisableTiming));
     CU(cudaMalloc(&h->partials, sizeof(ExtAcc) * h->sm_count * 8));
     CU(cudaMalloc(&h->ext, sizeof(ExtResult)));
@@ -1749,6 +1754,7 @@ int gscan_destroy(gscan_handle* h) {
   if (h->side) { cudaStreamSynchronize(h->side); cudaStreamDestroy(h->side); }
   if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
   if (h->ev_f3) cudaEventDestroy(h->ev_f3);
+  if (h->ev_part) cudaEventDestroy(h->ev_part);
   if (h->ev_dup) cudaEventDestroy(h->ev_dup);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
   delete h;
