@@ -1723,16 +1723,31 @@ __global__ void __launch_bounds__(kSpSortThreads) k_sp_sort_gathered_big(
   }
 }
 
-// Position -> bucket (the non-empty bucket holding it): largest b with
-// bstart[b] <= pos - 1.
-__device__ __forceinline__ uint32_t bucket_of_pos(const uint32_t* __restrict__ bstart, uint32_t pos) {
-  uint32_t lo = 0, hi = kSpBuckets - 1;
-  while (lo < hi) {
-    const uint32_t mid = (lo + hi + 1) >> 1;
-    if (bstart[mid] <= pos - 1) lo = mid;
-    else hi = mid - 1;
+// Position -> bucket (the non-empty bucket holding it: the largest b with
+// bstart[b] <= pos - 1, else 0) for two positions at once, by a whole warp
+// (pa, pb warp-uniform): each step the 32 lanes probe 32 evenly spaced
+// buckets of the remaining range and the ballot keeps the last one at or
+// below the target,
+// so 4 dependent loads replace a binary search's 16 (bstart is non-decreasing;
+// bucket lo of the range always qualifies).
+__device__ __forceinline__ void bucket_of_pos2_warp(const uint32_t* __restrict__ bstart,
+                                                    uint32_t pa, uint32_t pb, int lane,
+                                                    uint32_t& ba, uint32_t& bb) {
+  uint32_t la = 0, na = kSpBuckets, lb = 0, nb = kSpBuckets;
+  while (na > 1 || nb > 1) {
+    const uint32_t sa = (na + 31) / 32, sb = (nb + 31) / 32;
+    const uint32_t qa = la + lane * sa, qb = lb + lane * sb;
+    const bool oka = lane == 0 || (qa < la + na && bstart[qa] <= pa - 1);
+    const bool okb = lane == 0 || (qb < lb + nb && bstart[qb] <= pb - 1);
+    const uint32_t ma = __ballot_sync(0xffffffffu, oka), mb = __ballot_sync(0xffffffffu, okb);
+    const uint32_t ea = la + na, eb = lb + nb;
+    la += (31 - __clz(ma)) * sa;
+    lb += (31 - __clz(mb)) * sb;
+    na = min(sa, ea - la);
+    nb = min(sb, eb - lb);
   }
-  return lo;
+  ba = la;
+  bb = lb;
 }
 
 // Slice s (global numbering: right 0..n_right-1, left n_right + s): positions
@@ -1779,7 +1794,8 @@ __global__ void __launch_bounds__(256) k_sp_slices(
   const SliceSpan sp = slice_span(st, s);
   const double lx = st.lx, ly = st.ly;
   const double ux = __dsub_rn(ext->ax, lx), uy = __dsub_rn(ext->ay, ly);
-  const uint32_t bs = bucket_of_pos(bstart, sp.seed);
+  uint32_t bs, be;  // the seed's bucket, the bucket of the slice's last walk position
+  bucket_of_pos2_warp(bstart, sp.seed, sp.right ? sp.hi : sp.lo, lane, bs, be);
   // head: slice positions inside the seed's bucket
   uint32_t h0, h1;  // inclusive position range
   if (sp.right) { h0 = sp.seed; h1 = min(sp.hi, bstart[bs + 1]); }
@@ -1797,7 +1813,6 @@ __global__ void __launch_bounds__(256) k_sp_slices(
   // buckets after the seed's bucket up to the bucket holding the slice's last
   // walk position; a non-gathered one there ends exactly at the slice end
   // (otherwise it would hold the next seed and be gathered)
-  const uint32_t be = bucket_of_pos(bstart, sp.right ? sp.hi : sp.lo);
   if (sp.right) {
     for (uint32_t b0 = bs + 1; b0 <= be; b0 += 32) {
       const uint32_t b = b0 + lane;
