@@ -93,6 +93,24 @@ def test_sparse_duplicates_decline(engine, oracle_mod):
     assert used == 0 and fail & FAIL_DUP, hex(fail)
 
 
+@pytest.mark.parametrize("plant", [False, True])
+def test_sparse_duplicate_check_in_rounds(engine, oracle_mod, plant):
+    """36M points: ~18M round-1 survivors, so the duplicate-check partitions
+    (with their sector padding) exceed one hash-set round (k_sp_dups checks
+    them over sub-ranges of the hash). Clean input: the fast path serves.
+    One duplicate pair among the survivors, at opposite ends of the input (so
+    in different hash lists): it is found and the path declines."""
+    xs, ys = _gen("square", 36_000_000, 5)
+    if plant:
+        edge = np.flatnonzero(ys < 0.001)
+        xs[edge[-1]], ys[edge[-1]] = xs[edge[0]], ys[edge[0]]
+    used, fail, _ = _run(engine, oracle_mod, xs, ys)
+    if plant:
+        assert used == 0 and fail & FAIL_DUP, hex(fail)
+    else:
+        assert used == 1 and fail == 0, hex(fail)
+
+
 def test_sparse_duplicate_of_interior_point_is_harmless(engine, oracle_mod):
     """Duplicates of points strictly inside the round-1 quadrilateral never
     reach the buffer (classify_quad, prefilter.hpp:47-63): the fast path stays on."""
