@@ -1129,7 +1129,7 @@ int sp_seg_f3(gscan_handle* h, const SpCtx& c) {
   TRY(rec_event(h, h->ev[1], s));
   {
     Launch L(h, "k_sp_phi", s);
-    const uint32_t t3 = kF3Split ? 1024u : (uint32_t)kSpThreads;
+    const uint32_t t3 = kF3Split ? 1024u : (uint32_t)kSpF3Threads;
     const size_t sm3 = kF3Split ? 0 : c.smem_nb;
 #define A3 c.xs, c.ys, h->sp_codes, c.n, c.cap, h->ext, h->sp_gbits, h->sp_st, h->sp_phi_part, h->surv, \
            h->sp_eb, h->sp_gcount, h->sp_gx, h->sp_gy, h->sp_dup, h->sp_hcount, h->sp_part_off, \

@@ -890,8 +890,18 @@ __device__ __forceinline__ uint32_t warp_scan_claim(uint32_t* s_counter, uint32_
 // to the CTA's hash list, counted per partition.
 // kMax = false: no shared-memory bucket maxima (k_sp_phimax_codes computes
 // them from the stored phi), so the CTA runs 1024 threads.
+#ifndef GSCAN_F3_THREADS
+#define GSCAN_F3_THREADS 512
+#endif
+#ifndef GSCAN_F3_P
+#define GSCAN_F3_P 4
+#endif
+// F3 (k_sp_phi with the bucket maxima): 512 threads, 4 point pairs in flight.
+// Measured on C2 (k_sp_phi 187 us): 640 threads 191 us, 768 threads 207 us
+// (80 registers), 1024 threads with 2 pairs 187 us -- more warps do not help.
+constexpr int kSpF3Threads = GSCAN_F3_THREADS;
 template <bool kVec, bool kMax>
-__global__ void __launch_bounds__(kMax ? kSpThreads : 1024, 1) k_sp_phi(
+__global__ void __launch_bounds__(kMax ? kSpF3Threads : 1024, 1) k_sp_phi(
     const double* __restrict__ xs, const double* __restrict__ ys,
     const uint16_t* __restrict__ codes, uint32_t n, uint32_t cap, const ExtResult* __restrict__ ext,
     const uint32_t* __restrict__ gbits, SpState* __restrict__ st, uint32_t* __restrict__ phi_part,
@@ -1018,7 +1028,7 @@ __global__ void __launch_bounds__(kMax ? kSpThreads : 1024, 1) k_sp_phi(
       const uint32_t* c2 = reinterpret_cast<const uint32_t*>(codes);
       const uint32_t np = n / 2;
       uint32_t p = tid;
-      constexpr int kP = kMax ? 4 : 2;  // fewer loads in flight at 32 warps
+      constexpr int kP = kMax ? GSCAN_F3_P : 2;  // fewer loads in flight at 32 warps
       // warp-uniform bound: the batch claims are warp-synchronous
       for (; (p - lane) + 31 + (kP - 1) * nth < np; p += kP * nth) {
         double2 vx[kP], vy[kP];
