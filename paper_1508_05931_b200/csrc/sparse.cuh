@@ -1308,9 +1308,10 @@ __global__ void __launch_bounds__(1024) k_sp_dup_part(const uint64_t* __restrict
 // top bits) and the entry's 15-bit index in its partition; equal tags are
 // confirmed on the full 64-bit hash (one load, a few per call). An equal hash
 // means a possible duplicate -> the full path (exact). Partitions over the
-// table's load limit are checked in rounds over sub-ranges of the hash;
-// partitions of 2^15 entries or more (above ~67M round-1 survivors) set
-// kSpFailCap.
+// table's load limit are checked in rounds over sub-ranges of the hash.
+// Partitions of 2^15 entries or more (above ~67M round-1 survivors) use an
+// 11-bit tag and a 21-bit index (more confirmations, same result); 2^21 - 1
+// entries or more (above ~4G survivors) set kSpFailCap.
 #ifndef GSCAN_DUPS_G
 #define GSCAN_DUPS_G 2
 #endif
@@ -1318,9 +1319,9 @@ constexpr uint32_t kSpDupGroups = GSCAN_DUPS_G;
 constexpr uint32_t kSpDupGT = 1024 / kSpDupGroups;                       // threads per group
 constexpr uint32_t kSpDupGSlots = kSpDupGroups == 2 ? 16384u : 12288u;  // slots per group table
 constexpr uint32_t kSpDupGRound = 8192;  // entries per round (load <= 0.5 / 0.67)
-constexpr uint32_t kSpDupTagBits = 17;
-constexpr uint32_t kSpDupIdxBits = 15;
-static_assert(32 + kSpDupTagBits <= 64 - kSpPartBits, "tag bits overlap the partition");
+constexpr uint32_t kSpDupIdxBits = 15;     // index bits of a slot (tag: the other 17)
+constexpr uint32_t kSpDupIdxBitsBig = 21;  // partitions of 2^15 entries or more
+static_assert(32 + (32 - kSpDupIdxBits) <= 64 - kSpPartBits, "tag bits overlap the partition");
 constexpr size_t kSpDupSmem = (size_t)kSpDupGroups * kSpDupGSlots * 4;
 
 __device__ __forceinline__ void named_sync(uint32_t id, uint32_t n) {
@@ -1359,7 +1360,13 @@ __global__ void __launch_bounds__(1024) k_sp_dups(const uint64_t* __restrict__ p
     // the next item's ticket is taken now and read after the closing barrier
     if (gt == 0) s_next[grp] = atomicAdd(ticket, 1u);
     const uint32_t n = hi - lo;
-    if (n >= (1u << kSpDupIdxBits)) {
+#ifdef GSCAN_DUPS_FORCE_BIG  // test builds: the large-partition encoding everywhere
+    const uint32_t ib = kSpDupIdxBitsBig;
+#else
+    const uint32_t ib = n < (1u << kSpDupIdxBits) ? kSpDupIdxBits : kSpDupIdxBitsBig;  // uniform
+#endif
+    const uint32_t imask = (1u << ib) - 1, tmask = (1u << (32 - ib)) - 1;
+    if (n >= imask) {
       full = true;
     } else {
       const uint32_t rounds = (n + kSpDupGRound - 1) / kSpDupGRound;
@@ -1392,15 +1399,14 @@ __global__ void __launch_bounds__(1024) k_sp_dups(const uint64_t* __restrict__ p
               const uint32_t mid = (uint32_t)(h >> 20) & 0xffffu;  // bits below the partition
               if ((uint32_t)(((uint64_t)mid * rounds) >> 16) != r) continue;
             }
-            const uint32_t tag = (uint32_t)(h >> 32) & ((1u << kSpDupTagBits) - 1);
-            const uint32_t v = (tag << kSpDupIdxBits) | (e - lo);  // never ~0u: e - lo < 2^15 - 1
+            const uint32_t tag = (uint32_t)(h >> 32) & tmask;
+            const uint32_t v = (tag << ib) | (e - lo);  // never ~0u: e - lo < imask
             uint32_t slot = (uint32_t)(((uint64_t)(uint32_t)h * kSpDupGSlots) >> 32);
             for (uint32_t probe = 0;; ++probe) {
               if (probe == kSpDupGSlots / 2) { full = true; break; }  // a skewed round
               const uint32_t prev = atomicCAS(&tab[slot], ~0u, v);
               if (prev == ~0u) break;
-              if ((prev >> kSpDupIdxBits) == tag &&
-                  parted[lo + (prev & ((1u << kSpDupIdxBits) - 1))] == h) {
+              if ((prev >> ib) == tag && parted[lo + (prev & imask)] == h) {
                 dup = true;
                 break;
               }
