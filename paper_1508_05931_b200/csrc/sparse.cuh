@@ -1234,18 +1234,18 @@ __global__ void __launch_bounds__(1024) k_sp_dup_part(const uint64_t* __restrict
         }
         if (lane == 31) s_w[warp] = x;
         __syncthreads();
-        if (warp == 0) {
-          uint32_t v = s_w[lane];
+        // every warp scans the 32 warp totals itself (no second barrier);
+        // s_w is rewritten only after the next chunk's first barrier
+        uint32_t wv = s_w[lane];
+        const uint32_t w0 = wv;
 #pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, v, o);
-            if (lane >= o) v += y;
-          }
-          s_w[lane] = v;
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, wv, o);
+          if (lane >= o) wv += y;
         }
-        __syncthreads();
-        ntot = s_w[31];
-        const uint32_t e0 = x - (a + b) + (warp ? s_w[warp - 1] : 0), e1 = e0 + a;
+        ntot = __shfl_sync(0xffffffffu, wv, 31);
+        const uint32_t wex = __shfl_sync(0xffffffffu, wv - w0, warp);  // totals of warps < warp
+        const uint32_t e0 = x - (a + b) + wex, e1 = e0 + a;
         const uint32_t c0_ = s_cur[q0], c1_ = s_cur[q1];
         s_base[q0] = c0_ - e0;
         s_base[q1] = c1_ - e1;
