@@ -1353,6 +1353,14 @@ uint32_t side_free_sms() {
   static const int v = getenv("GSCAN_SIDE_FREE") ? atoi(getenv("GSCAN_SIDE_FREE")) : (int)kSideFreeSms;
   return (uint32_t)v;
 }
+// k_sp_dups overlaps only the end of the Graham tail (the one-CTA middle and
+// the down and certificate kernels, few CTAs with work)
+constexpr uint32_t kSideFreeSmsDups = 16;  // measured: 16 (0.974 ms) < 8 < 32 (0.983) < 4, 48
+uint32_t side_free_sms_dups() {
+  static const int v =
+      getenv("GSCAN_SIDE_FREE2") ? atoi(getenv("GSCAN_SIDE_FREE2")) : (int)kSideFreeSmsDups;
+  return (uint32_t)v;
+}
 
 int sparse_dup_check(gscan_handle* h, uint32_t n) {
   const uint32_t G = (uint32_t)h->sp_grid;
@@ -1381,7 +1389,7 @@ int sparse_dup_check(gscan_handle* h, uint32_t n) {
   {
     Launch L(h, "k_sp_dups", h->side);
     k_sp_dups<<<h->sm_count, 1024, kSpSideSmem, h->side>>>(h->sp_dup2, h->sp_part_off, nl, h->sp_st,
-                                                              h->sp_side_work + 1, side_free_sms());
+                                                              h->sp_side_work + 1, side_free_sms_dups());
   }
   CU(cudaEventRecord(h->ev_dup, h->side));
   return GSCAN_OK;
