@@ -1344,6 +1344,7 @@ int sparse_enqueue(gscan_handle* h, const double* xs, const double* ys, uint32_t
 // the SMs costs the main path ~30 us, the partitioning's partial-sector stores
 // cost another ~60 us (DRAM read-for-merge) until its runs were padded to
 // whole sectors (k_sp_dup_part<true>); forking later (inside the tree) is slower.
+// k_sp_dups, which overlaps only the end of the tail, leaves 16 SMs free.
 constexpr uint32_t kSideFreeSms = 32;
 constexpr size_t kSpSideSmem = kSpDupPartSmemPad;  // 208 KB
 static_assert(kSpSideSmem >= kSpDupPartSmem && kSpSideSmem >= kSpDupSmem && kSpSideSmem <= 226 * 1024,
