@@ -1171,7 +1171,7 @@ int sp_seg_sortg(gscan_handle* h, const SpCtx& c, const double* gx, const double
   }
   {
     Launch L(h, "k_sp_sort_gathered", s);
-    k_sp_sort_gathered<<<h->sm_count * 4, kSpSmallThreads, kSpSmallSmem, s>>>(
+    k_sp_sort_gathered<<<h->sm_count * (kSpSmallCap <= 512 ? 8 : 4), kSpSmallThreads, kSpSmallSmem, s>>>(
         h->sp_glist, h->sp_bstart, c.gs, h->sp_hist, h->sp_gcnt, h->rec, h->ext, h->sp_st,
         h->sp_bigg, h->A_x, h->A_y, h->A_i);
   }

@@ -1653,7 +1653,12 @@ __device__ bool cta_sort_bucket_sub(const PtRec* __restrict__ R, uint32_t cnt, d
 // 4 CTAs per SM); clustered or larger buckets go to the bitonic sorter.
 // Exact positions 1 + bstart[b] + rank in the annotated-buffer space A;
 // records P_l's position.
-constexpr uint32_t kSpSmallCap = 1024;
+// 512 (8 CTAs/SM) measured on C2: k_sp_sort_gathered 37 -> 28 us but the
+// buckets of 513-1024 points move to the big sorter (6 -> 14 us); net <= 4 us
+#ifndef GSCAN_SMALL_CAP
+#define GSCAN_SMALL_CAP 1024
+#endif
+constexpr uint32_t kSpSmallCap = GSCAN_SMALL_CAP;
 constexpr int kSpSmallThreads = 256;
 constexpr size_t kSpSmallSmem = (size_t)kSpSmallCap * (8 + 8 + 8 + 8 + 4 + 4 + 4 + 4) + 16;
 
