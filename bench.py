@@ -1,11 +1,13 @@
 #!/usr/bin/env python3
 """Benchmark: Mpoints/s of the 20M-point 2D convex hull on B200 (BASELINE.json).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C1..C5] [--impl ours|reference]
 
-One JSON line on rank 0. A "step" is one full_pipeline over the 20M-point
-uniform-square input (seed 1), the configuration BASELINE.json's metric is
-quoted on (configs[1]). Keys:
+One JSON line on rank 0. A "step" is one full_pipeline over the configured
+input (default C2: the 20M-point uniform square, seed 1, the configuration
+BASELINE.json's metric is quoted on, configs[1]). --gpus N > 1 re-launches
+this script under torch.distributed.run (one rank per GPU, 127.0.0.1) unless
+it already runs under it. Keys:
   value      device-resident throughput: inputs already in HBM, K steps timed
              with CUDA events on the pipeline's stream (max over ranks)
   e2e        same metric through the C-ABI host entry (gscan_hull_f64) with
@@ -16,10 +18,13 @@ quoted on (configs[1]). Keys:
              algorithmic bytes 16 B/point read + 2 B/point bucket code written;
              on the full-sort path k_filter_keys (16 B/point + 16 B/survivor);
              over its event-timed duration, against MEASURED_PEAKS.json hbm_gbs
-  cpu_baseline  the unmodified reference (oracle/_ref) on this host, one full
-             run of the same workload, timed by its own StageStats
-N > 1 runs the sharded pipeline (paper_1508_05931_b200/distributed.py) on the
-same 20M points split across ranks (strong scaling).
+  cpu_baseline  the unmodified reference (oracle/_ref) on this host: median of
+             up to 5 full runs of the same workload (bounded to ~20 s), timed
+             by its own StageStats; host nproc and CPU model stated
+N > 1 runs the sharded pipeline (paper_1508_05931_b200/distributed.py): C1-C4
+split the same points across ranks (strong scaling), C5 (1B points) is the
+sharded config of BASELINE.json (each rank generates and owns its contiguous
+shard of the same 1B-point sequence).
 """
 from __future__ import annotations
 
@@ -44,7 +49,48 @@ CONFIGS = {
     "C2": ("square", 20_000_000, "C2: 20M points uniform in unit square, seed 1"),
     "C3": ("disk", 20_000_000, "C3: 20M points uniform in unit disk, seed 1"),
     "C4": ("circle", 20_000_000, "C4: 20M points on the unit circle, seed 1"),
+    "C5": ("square", 1_000_000_000, "C5: 1B points uniform in unit square, seed 1"),
 }
+KIND_CODE = {"square": 0, "disk": 1, "circle": 2, "collinear": 3}  # datagen.hpp / gscan.h
+SEED = 1
+PIPELINE_CONFIG = "chunk_count=1024, both rounds, chunked"
+
+
+def config_dict(cfgname: str, world: int) -> dict:
+    """The `config` object both arms print (identical, so the driver can pair them)."""
+    kind, n, label = CONFIGS[cfgname]
+    return {"workload": label, "n_points": n, "seed": SEED,
+            "l2": f"inputs ({16 * n / 1e6:.0f} MB) larger than the 126 MB L2; no flush needed"
+            if 16 * n > 126e6 else "inputs fit in L2 (C1: 16 MB); no flush (the reference's own size)",
+            "parallelism": f"sharded x{world}" if world > 1 else "single device",
+            "pipeline_config": PIPELINE_CONFIG}
+
+
+def host_info() -> dict:
+    model = ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model}
+
+
+def relaunch_distributed(args) -> int | None:
+    """--gpus N > 1 outside torchrun: re-exec under torch.distributed.run."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           str(Path(__file__).resolve())] + sys.argv[1:]
+    log("+", " ".join(cmd))
+    return subprocess.call(cmd)
 
 
 def log(*a):
@@ -151,51 +197,73 @@ def golden_for(name: str):
 
 
 def cpu_baseline(xs, ys, n) -> dict:
-    """The reference itself (oracle/_ref) on this host: one full run."""
+    """The reference itself (oracle/_ref) on this host: median of up to 5 full
+    runs (stops early once ~20 s of CPU work is spent), like cli::bench_one's
+    median of repeats (cli.hpp:176-207)."""
     import oracle
 
-    if oracle.ref_available():
-        _, st = oracle.full_pipeline(xs, ys, impl="ref")
-        kind, cores = "reference", 2  # hull2d uses <= 2 threads (parallel.hpp:18-28)
-    else:
-        _, st = oracle.full_pipeline(xs, ys)
-        kind, cores = "port", 1
-    t = st["t_total_ms"]
-    return {"value": round(n / (t * 1e-3) / 1e6, 3), "unit": "Mpoints/s", "cores": cores,
-            "kind": kind, "t_total_ms": round(t, 1),
-            "sample": f"1 full run of the same {n}-point input, timed by StageStats.t_total_ms"}
+    impl = "ref" if oracle.ref_available() else "port"
+    times = []
+    t_start = time.time()
+    while len(times) < 5 and (not times or time.time() - t_start < 20.0):
+        _, st = oracle.full_pipeline(xs, ys, impl=impl)
+        times.append(st["t_total_ms"])
+    t = float(np.median(times))
+    return {"value": round(n / (t * 1e-3) / 1e6, 3), "unit": "Mpoints/s",
+            "cores": 2 if impl == "ref" else 1,  # hull2d uses <= 2 threads (parallel.hpp:18-28)
+            "kind": "reference" if impl == "ref" else "port", "t_total_ms": round(t, 1),
+            "runs_ms": [round(v, 1) for v in times], **host_info(),
+            "sample": f"median of {len(times)} full runs of the same {n}-point input, "
+                      "timed by StageStats.t_total_ms"}
 
 
 def run_reference(args, cfgname):
-    """--impl reference: the reference's own CPU path (oracle/_ref) on host cores."""
+    """--impl reference: the reference's own CPU path (oracle/_ref, the
+    unmodified hull2d headers) on host cores. The input comes from the
+    reference's own generator (datagen.hpp via oracle/_ref), so this arm loads
+    nothing from the product package. Rank 0 only (other ranks exit 0)."""
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
     import oracle
-    from paper_1508_05931_b200 import generate
 
     kind, n, label = CONFIGS[cfgname]
-    xs, ys = generate(kind, n, 1)
     impl = "ref" if oracle.ref_available() else "port"
+    cfg = config_dict(cfgname, world)
+    if n > 200_000_000:
+        # 1B points: ~35 s of single-threaded generation and ~64-100 GB RSS in
+        # the reference (SURVEY.md 8d); each step is a bounded sample instead.
+        n_s = 100_000_000
+        sample = f"{n_s}-point prefix of the same sequence per step (1B exceeds a bounded CPU run)"
+    else:
+        n_s = n
+        sample = f"full {n}-point runs"
+    xs, ys = (oracle.ref_generate(KIND_CODE[kind], n_s, SEED) if impl == "ref"
+              else _port_generate(kind, n_s))
     times = []
     for s in range(args.warmup + args.steps):
         _, st = oracle.full_pipeline(xs, ys, impl=impl)
         if s >= args.warmup:
             times.append(st["t_total_ms"])
     t = float(np.sum(times)) / 1e3
-    value = n * args.steps / t / 1e6
+    value = n_s * args.steps / t / 1e6
     line = {"metric": METRIC, "value": round(value, 4), "unit": "Mpoints/s", "impl": "reference",
-            "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(t * 1e3 / args.steps, 2), "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": label, "n_points": n},
+            "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic", "config": cfg,
             "cpu_baseline": {"value": round(value, 4), "unit": "Mpoints/s",
                              "cores": 2 if impl == "ref" else 1,
-                             "kind": "reference" if impl == "ref" else "port",
-                             "sample": f"{args.steps} timed full runs after {args.warmup} warm-up"},
+                             "kind": "reference" if impl == "ref" else "port", **host_info(),
+                             "sample": f"{args.steps} timed {sample} after {args.warmup} warm-up"},
             "e2e": {"value": round(value, 4), "unit": "Mpoints/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def _port_generate(kind, n):
+    raise RuntimeError("oracle/_ref not built: the reference arm needs the reference's generator")
 
 
 def main():
@@ -207,13 +275,16 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    rc = relaunch_distributed(args)
+    if rc is not None:
+        sys.exit(rc)
     if args.impl == "reference":
         return run_reference(args, args.config)
 
     import torch
     import torch.distributed as dist
 
-    from paper_1508_05931_b200 import Engine, PipelineConfig, generate
+    from paper_1508_05931_b200 import Engine, PipelineConfig
     from paper_1508_05931_b200.distributed import sharded_hull
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -225,23 +296,25 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     kind, n, label = CONFIGS[args.config]
-    xs, ys = generate(kind, n, 1)  # identical bits on every rank (seeded)
     lo = n * rank // world
     hi = n * (rank + 1) // world
     eng = Engine(local)
     eng.reserve(n if world == 1 or rank == 0 else hi - lo)
     stream = torch.cuda.current_stream()
     eng._lib.gscan_set_stream(eng.handle, stream.cuda_stream)
-    d_xs = torch.from_numpy(xs[lo:hi].copy()).cuda()
-    d_ys = torch.from_numpy(ys[lo:hi].copy()).cuda()
-    out = torch.empty(n, dtype=torch.int32, device="cuda")
+    # every rank materialises only its own shard [lo, hi) of the seeded sequence
+    d_xs, d_ys, gen_how = make_shard(eng, kind, n, lo, hi, torch)
+    out = torch.empty(n if world == 1 else 1, dtype=torch.int32, device="cuda")
     cfg = PipelineConfig()
+
+    last = {}
 
     def step():
         if world == 1:
             k, st = eng.hull_device(d_xs.data_ptr(), d_ys.data_ptr(), n, out.data_ptr(), n, cfg)
             return k, st
         hull, st = sharded_hull(eng, d_xs, d_ys, lo, cfg)
+        last["hull"] = hull
         return (len(hull) if hull is not None else 0), st
 
     def barrier():
@@ -257,9 +330,9 @@ def main():
         if world == 1:
             got = out[:k].cpu().numpy().astype(np.uint64)
         else:
-            got, _ = None, None
+            got = last["hull"]
         g = golden_for(args.config)
-        if g is not None and world == 1:
+        if g is not None and got is not None:
             parity = (hull_hash(got) == g["hull_sha256_16"] and st.n_after_round1 == g["n_after_round1"]
                       and st.n_after_round2 == g["n_after_round2"])
     for _ in range(max(args.warmup - 1, 0)):
@@ -305,8 +378,8 @@ def main():
     n1 = st.n_after_round1 if st is not None else None
     roofline = None
     if t_filter:
-        if fkern == "k_sp_hist":  # 16 B/pt read (xs, ys) + 2 B/pt bucket code written
-            alg_bytes = 18 * n_local
+        if fkern == "k_sp_hist":  # 16 B/pt read (xs, ys)
+            alg_bytes = 16 * n_local
         else:
             alg_bytes = 16 * n_local + 16 * (n1 if (world == 1 and n1) else int(0.664 * n_local))
         achieved = alg_bytes / (t_filter * 1e-3) / 1e9
@@ -323,27 +396,69 @@ def main():
                     "kernel": fkern, "kernel_ms": round(t_filter, 4),
                     "algorithmic_bytes": alg_bytes, "peak_source": peak_src}
 
-    # ---- e2e through the C-ABI host entry, pinned host buffers ----
+    # ---- e2e: host buffers in, hull indices out, copies inside the timed region ----
     e2e = None
-    if world == 1:
-        hx = torch.from_numpy(xs).pin_memory()
-        hy = torch.from_numpy(ys).pin_memory()
-        hout = torch.empty(n, dtype=torch.int64).pin_memory()
-        kk = 0
-        for _ in range(2):
-            kk, _ = eng.hull_ptr(hx.data_ptr(), hy.data_ptr(), n, hout.data_ptr(), n, cfg)
-        torch.cuda.synchronize()
+    n_local = hi - lo
+    need = 16 * n_local * 2 + 8 * n
+    try:
+        import psutil
+        avail = psutil.virtual_memory().available
+    except Exception:
+        avail = need * 4
+    if need * 1.5 > avail:
+        e2e = {"value": None, "unit": "Mpoints/s", "h2d_bytes_per_step": 16 * n_local,
+               "d2h_bytes_per_step": None,
+               "skipped": f"pinned host copy of the shard ({need / 1e9:.1f} GB) exceeds host RAM"}
+    else:
+        hx = torch.empty(n_local, dtype=torch.float64).pin_memory()
+        hy = torch.empty(n_local, dtype=torch.float64).pin_memory()
+        hx.copy_(d_xs)
+        hy.copy_(d_ys)
         f0 = torch.cuda.Event(enable_timing=True)
         f1 = torch.cuda.Event(enable_timing=True)
-        f0.record(stream)
-        for _ in range(args.steps):
-            kk, _ = eng.hull_ptr(hx.data_ptr(), hy.data_ptr(), n, hout.data_ptr(), n, cfg)
-        f1.record(stream)
-        torch.cuda.synchronize()
+        if world == 1:
+            # the reference-facing C-ABI host entry gscan_hull_f64 (include/gscan.h)
+            hout = torch.empty(n, dtype=torch.int64).pin_memory()
+            kk = 0
+            for _ in range(2):
+                kk, _ = eng.hull_ptr(hx.data_ptr(), hy.data_ptr(), n, hout.data_ptr(), n, cfg)
+            torch.cuda.synchronize()
+            f0.record(stream)
+            for _ in range(args.steps):
+                kk, _ = eng.hull_ptr(hx.data_ptr(), hy.data_ptr(), n, hout.data_ptr(), n, cfg)
+            f1.record(stream)
+            torch.cuda.synchronize()
+            d2h = 8 * int(kk)
+            path = "gscan_hull_f64 (pinned host buffers)"
+        else:
+            # each rank copies its shard in, sharded_hull returns the index list on rank 0
+            kk = 0
+
+            def e2e_step():
+                d_xs.copy_(hx, non_blocking=True)
+                d_ys.copy_(hy, non_blocking=True)
+                hull, _ = sharded_hull(eng, d_xs, d_ys, lo, cfg)
+                return len(hull) if hull is not None else 0
+
+            for _ in range(2):
+                e2e_step()
+            barrier()
+            f0.record(stream)
+            for _ in range(args.steps):
+                kk = e2e_step()
+            f1.record(stream)
+            barrier()
+            d2h = 8 * int(kk)
+            path = "distributed.sharded_hull (pinned host shard per rank)"
         e2e_ms = f0.elapsed_time(f1) / args.steps
+        if world > 1:
+            tt = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e2e_ms = float(tt.item())
         e2e = {"value": round(n / (e2e_ms * 1e-3) / 1e6, 3), "unit": "Mpoints/s",
-               "h2d_bytes_per_step": 16 * n, "d2h_bytes_per_step": 4 * int(kk),
-               "ms_per_step": round(e2e_ms, 3), "path": "gscan_hull_f64 (pinned host buffers)"}
+               "h2d_bytes_per_step": 16 * n_local, "d2h_bytes_per_step": d2h,
+               "ms_per_step": round(e2e_ms, 3), "path": path}
+        del hx, hy
 
     if rank != 0:
         if world > 1:
@@ -351,16 +466,18 @@ def main():
         return
     cpu = None
     if not args.no_cpu_baseline and world == 1:
-        cpu = cpu_baseline(xs, ys, n)
+        n_cpu = min(n, 20_000_000)
+        hx = d_xs[:n_cpu].cpu().numpy()
+        hy = d_ys[:n_cpu].cpu().numpy()
+        cpu = cpu_baseline(hx, hy, n_cpu)
+        if n_cpu < n:
+            cpu["sample"] += f" (the first {n_cpu} points of the {n}-point sequence: bounded sample)"
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "Mpoints/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic",
-        "config": {"workload": label, "n_points": n, "seed": 1,
-                   "l2": "inputs (320 MB) larger than the 126 MB L2; no flush needed",
-                   "parallelism": f"sharded x{world}" if world > 1 else "single device",
-                   "pipeline_config": "chunk_count=1024, both rounds, chunked"},
+        "data": f"synthetic ({gen_how})",
+        "config": config_dict(args.config, world),
         "parity_vs_golden": parity,
         "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks,
         "gpu_launches": launches, "kernels_ms": kernels, "sparse_path": eng.sparse_info()[0] == 1,
@@ -370,6 +487,26 @@ def main():
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def make_shard(eng, kind, n, lo, hi, torch):
+    """Device-resident SoA shard [lo, hi) of gen_<kind>(n, seed 1)
+    (datagen.hpp:32-71): the on-device mt19937_64 generator for squares
+    (bit-identical to the host sequence), else the host generator."""
+    if kind == "square" and hasattr(eng, "generate_square_device"):
+        d_xs = torch.empty(hi - lo, dtype=torch.float64, device="cuda")
+        d_ys = torch.empty(hi - lo, dtype=torch.float64, device="cuda")
+        eng.generate_square_device(SEED, lo, hi, d_xs.data_ptr(), d_ys.data_ptr())
+        torch.cuda.synchronize()
+        return d_xs, d_ys, "gen_square on the device (mt19937_64, bit-identical to datagen.hpp)"
+    if n > 200_000_000:
+        raise SystemExit(f"{kind} with {n} points needs the on-device generator")
+    from paper_1508_05931_b200 import generate
+
+    xs, ys = generate(kind, n, SEED)  # identical bits on every rank (seeded)
+    d_xs = torch.from_numpy(xs[lo:hi].copy()).cuda()
+    d_ys = torch.from_numpy(ys[lo:hi].copy()).cuda()
+    return d_xs, d_ys, f"gen_{kind} on the host (datagen.hpp sequence)"
 
 
 if __name__ == "__main__":
