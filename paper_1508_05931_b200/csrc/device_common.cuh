@@ -149,6 +149,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// plain arrive (count 1), e.g. a consumer warp releasing a ring stage
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 // global -> shared, `bytes` a multiple of 16, both addresses 16 B aligned
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
@@ -157,6 +161,79 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+
+// ---- XY tile ring: SoA (xs, ys) streamed through shared memory ----
+// Each CTA takes tiles b, b + G, b + 2G, ... of kT points. Stage st holds
+// one tile of xs and one of ys, filled by two bulk copies completed on
+// full[st]. There is no producer warp: the LAST warp to finish reading a
+// stage (a shared-memory counter) refills it with the CTA's tile k + kS, so
+// every warp is a consumer, warps never wait on each other except through the
+// data, and kS tiles are in flight per CTA. Needs 16-byte aligned xs, ys.
+template <int kT, int kS>
+struct XYRing {
+  static constexpr size_t kSmem = (size_t)kS * kT * 16 + (size_t)kS * 8 + (size_t)kS * 4;
+  double* sx;        // [kS][kT]
+  double* sy;        // [kS][kT]
+  uint64_t* full;    // [kS]
+  uint32_t* cnt;     // [kS] warps done with the stage's current tile
+  const double* xs;
+  const double* ys;
+  uint32_t mine;     // tiles of this CTA
+  uint32_t nwarps;
+
+  __device__ __forceinline__ void setup(unsigned char* smem, const double* x, const double* y,
+                                        uint32_t n) {
+    sx = reinterpret_cast<double*>(smem);
+    sy = sx + (size_t)kS * kT;
+    full = reinterpret_cast<uint64_t*>(sy + (size_t)kS * kT);
+    cnt = reinterpret_cast<uint32_t*>(full + kS);
+    xs = x;
+    ys = y;
+    const uint32_t ntiles = n / kT;
+    mine = ntiles > blockIdx.x ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0u;
+    nwarps = blockDim.x >> 5;
+  }
+  __device__ __forceinline__ uint32_t tile_start(uint32_t k) const {
+    return (blockIdx.x + k * gridDim.x) * (uint32_t)kT;
+  }
+  __device__ __forceinline__ void issue(uint32_t k) {
+    const uint32_t st = k % kS;
+    const size_t t0 = tile_start(k);
+    mbar_expect_tx(&full[st], 2u * kT * 8u);
+    bulk_g2s(sx + (size_t)st * kT, xs + t0, kT * 8u, &full[st]);
+    bulk_g2s(sy + (size_t)st * kT, ys + t0, kT * 8u, &full[st]);
+  }
+  // thread 0: barriers and the first kS tiles (the caller then __syncthreads)
+  __device__ __forceinline__ void start() {
+    if (threadIdx.x == 0) {
+      for (int k = 0; k < kS; ++k) {
+        mbar_init(&full[k], 1);
+        cnt[k] = 0;
+      }
+      mbar_fence_init();
+      for (uint32_t k = 0; k < (uint32_t)kS && k < mine; ++k) issue(k);
+    }
+  }
+  __device__ __forceinline__ void wait(uint32_t k) { mbar_wait(&full[k % kS], (k / kS) & 1u); }
+  __device__ __forceinline__ const double* tx(uint32_t k) const { return sx + (size_t)(k % kS) * kT; }
+  __device__ __forceinline__ const double* ty(uint32_t k) const { return sy + (size_t)(k % kS) * kT; }
+  // the calling warp is done reading tile k (its values are in registers)
+  __device__ __forceinline__ void release(uint32_t k) {
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) {
+      const uint32_t st = k % kS;
+      __threadfence_block();  // this warp's reads of the stage happen before the count
+      if (atomicAdd(&cnt[st], 1u) == nwarps - 1) {
+        cnt[st] = 0;
+        if (k + kS < mine) {
+          __threadfence_block();
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // reads before the async writes
+          issue(k + kS);
+        }
+      }
+    }
+  }
+};
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
   uint32_t m;

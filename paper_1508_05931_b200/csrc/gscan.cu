@@ -978,6 +978,10 @@ int rec_event(gscan_handle* h, cudaEvent_t e, cudaStream_t s) {
 // F2 without its shared-memory histogram (two CTAs per SM) + a histogram
 // pass over the codes
 constexpr bool kF2Split = true;
+#ifndef GSCAN_F2_RING
+#define GSCAN_F2_RING 1
+#endif
+constexpr bool kF2Ring = GSCAN_F2_RING;  // F2 as a bulk-copy pipeline (k_sp_hist_ring)
 // F3 without its shared-memory bucket maxima (1024 threads) + a maxima pass:
 // measured slower (F3 192 us either way, + 46 us for k_sp_phimax_codes)
 constexpr bool kF3Split = false;
@@ -1065,8 +1069,13 @@ int sp_seg_f2(gscan_handle* h, const SpCtx& c) {
     Launch L(h, "k_sp_theta", s);
     k_sp_theta<<<(c.nb + 1 + 255) / 256, 256, 0, s>>>(h->sp_cdf, h->sp_th, h->sp_st);
   }
-  const uint32_t g2 = kF2Split ? 2 * c.G : c.G;  // F2 CTAs (d2 partials)
-  {
+  const bool ring = kF2Ring && c.vec;
+  const uint32_t g2 = ring ? c.G : (kF2Split ? 2 * c.G : c.G);  // F2 CTAs (d2 partials)
+  if (ring) {
+    Launch L(h, "k_sp_hist", s);
+    k_sp_hist_ring<<<g2, kF2Cons, kF2RingSmem, s>>>(c.xs, c.ys, c.n, h->ext, h->sp_cdf, h->sp_th,
+                                                         h->sp_codes, h->sp_d2, h->ctr, h->sp_st);
+  } else {
     Launch L(h, "k_sp_hist", s);
 #define A2 c.xs, c.ys, c.n, h->ext, h->sp_cdf, h->sp_th, h->sp_codes, h->sp_hist_part, h->sp_d2, h->ctr, \
            h->sp_st
@@ -1079,7 +1088,7 @@ int sp_seg_f2(gscan_handle* h, const SpCtx& c) {
     }
 #undef A2
   }
-  if (kF2Split) {
+  if (kF2Split || ring) {
     Launch L(h, "k_sp_hist_codes", s);
     k_sp_hist_codes<<<c.G, 1024, c.smem_nb, s>>>(h->sp_codes, c.n, h->sp_hist_part, h->sp_st);
   }
@@ -1705,6 +1714,8 @@ int gscan_create(int device, gscan_handle** out) {
     CU(cudaFuncSetAttribute(k_sp_hist<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, nbs));
     CU(cudaFuncSetAttribute(k_sp_hist<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, nbs));
     CU(cudaFuncSetAttribute(k_sp_hist_codes, cudaFuncAttributeMaxDynamicSharedMemorySize, nbs));
+    CU(cudaFuncSetAttribute(k_sp_hist_ring, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)kF2RingSmem));
     CU(cudaFuncSetAttribute(k_extremes_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kExtSmem));
     CU(cudaFuncSetAttribute(k_sp_phi<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, nbs));
     CU(cudaFuncSetAttribute(k_sp_phi<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, nbs));

@@ -517,6 +517,201 @@ __device__ __forceinline__ void f2_batch(const double (&x)[B], const double (&y)
 }
 
 // ===========================================================================
+// F2 screen. Most of F2's FP64 work (the four quad crosses, the CDF
+// lookup and the guard test: ~48 FP64 instructions and 4 FP64 conversions
+// per point in the plain path) is replaced by FP32 arithmetic with a proven
+// error bound; only the pseudo-angle's cell coordinate stays in FP64. A point
+// whose screened result lies within its error bound of a decision boundary is
+// UNCERTAIN and takes the exact path (f2_exact: the plain per-point code),
+// ~2e-4 of the points.
+//
+// Quad (classify_quad, prefilter.hpp:47-63). The reference's cross for edge e
+// is R_e = ex*(y - qy) - ey*(x - qx) in double. With dx = x - ax, dy = y - ay
+// (double, then rounded to float: fx, fy) and K_e = ex*qdy - ey*qdx
+// (qd = q_e - anchor), the float value c_e = fma(EX, fy, fma(-EY, fx, -K_e))
+// differs from the double cross by at most
+//   4.1u (|ex||dy| + |ey||dx| + |K_e|) + O(2^-53) terms,  u = 2^-24,
+// and |dx| <= DX, |dy| <= DY (bounding box of the input around the anchor).
+// B_e = 8u (|ex| DY + |ey| DX + |K_e|) + 2^-100 covers that, plus the extra
+// rounding of pre-scaling the coefficients by 1/B_e: c'_e = c_e / B_e, so
+// min_e c'_e > 1 proves every cross > 0 (inside: flag 0) and min_e c'_e < -1
+// proves one cross < 0 (kept). A zero edge (ex = ey = 0) has cross exactly 0:
+// kept, encoded as c'_e = -2.
+//
+// Bucket (sp_bucket). The cell coordinate u = 1024 (1 - dx/(|dx| + dy))
+// (= s * kSpCells) is formed in double (rcp.approx + one Newton step: error
+// <= 1024 * 2^-39.8 = 1.1e-9), split exactly into the cell j = floor(u) and
+// t = u - j in [0, 1] (t = 1 when u is an integer and the tie rounds down:
+// the piecewise-linear map is continuous, so cell j at t = 1 is cell j + 1 at
+// t = 0), and t is rounded to float (error <= 2^-25). Per cell the table
+// holds I_j + phi_j = nb * cdf[j] (phi_j in [0, 1) as float) and the slope
+// S_j = nb * (cdf[j+1] - cdf[j]) (float), and v = phi_j + t * S_j in float
+// errs from the exact piecewise-linear value by at most 1.5e-7 S_j + 1.1e-7
+// (t, S and phi rounding, the fma; a cell mix-up near a breakpoint stays
+// inside the bound by continuity). The double path trusts floor(v_d) when
+// frac(v_d) is 1e-4 away from an integer; the screen trusts floor(v_f) only
+// when frac(v_f) is g_j = 1.03e-4 + 2e-7 S_j away, so floor(v_f) = floor(v_d)
+// and the double path's own condition holds: the screened bucket IS
+// sp_bucket's result.
+//
+// P_l (argmax dist2): a survivor whose float dist2 (error <= 5u) is below
+// (1 - 16u) times the best dist2 seen by its warp (or by the quad vertices,
+// which all survive) cannot be the maximum or tie it; only the others
+// compute dist2 in double.
+//
+// Preconditions of the quad screen (checked per CTA, else every point takes
+// the exact path): the box extents DX, DY in [2^-40, 2^40] and finite scaled
+// coefficients.
+constexpr float kF2G1 = 2.0e-7f;
+constexpr float kF2G0 = 1.03e-4f;
+constexpr float kF2Magic = 12582912.0f;          // 1.5 * 2^23: v + magic rounds v to an integer
+constexpr int kF2MagicBits = 0x4B400000;
+constexpr double kF2MagicD = 6755399441055744.0;  // 1.5 * 2^52
+
+struct F2Float {
+  float ex[4], ey[4], k[4];  // scaled: c'_e = ex*fy - ey*fx - k
+  float thr0;                // lower bound of max dist2 (quad vertices), screened
+  bool on;
+};
+
+// a float threshold t with t <= d2 * (1 - 16u) for the double d2 (0 when tiny):
+// a survivor whose float dist2 (relative error <= 5u) is below t is below d2
+__device__ __forceinline__ float f2_thr(double d2) {
+  const float tf = __fmul_rn(__double2float_rz(d2), 1.0f - 16.0f * 5.9604645e-8f);
+  return tf < 1e-27f ? 0.f : tf;
+}
+
+__device__ __forceinline__ void f2_float_setup(const SpQuad& q, F2Float& f) {
+  // bounding box from the extremes (minx, miny, maxx, maxy) around the anchor
+  const double DX = fmax(fabs(q.qx[0] - q.ax), fabs(q.qx[2] - q.ax));
+  const double DY = fabs(q.qy[3] - q.ay);
+  bool on = fmax(DX, DY) >= 0x1p-40 && fmax(DX, DY) <= 0x1p40;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const double ex = q.ex[e], ey = q.ey[e];
+    const double qdx = q.qx[e] - q.ax, qdy = q.qy[e] - q.ay;
+    const double K = ex * qdy - ey * qdx;
+    if (ex == 0.0 && ey == 0.0) {
+      f.ex[e] = 0.f; f.ey[e] = 0.f; f.k[e] = 2.f;
+      continue;
+    }
+    const double B = 0x1p-21 * (fabs(ex) * DY + fabs(ey) * DX + fabs(K)) + 0x1p-100;  // 8u
+    const double ib = 1.0 / B;
+    f.ex[e] = (float)(ex * ib);
+    f.ey[e] = (float)(ey * ib);
+    f.k[e] = (float)(K * ib);
+    on = on && isfinite(f.ex[e]) && isfinite(f.ey[e]) && isfinite(f.k[e]) && B >= 0x1p-90;
+  }
+  f.on = on;
+  // every quad vertex survives round 1 (it lies on two edges): the maximal
+  // dist2 is at least theirs (the anchor itself is not bucketed)
+  double m = 0.0;
+#pragma unroll
+  for (int e = 0; e < 4; ++e)
+    if (!(q.qx[e] == q.ax && q.qy[e] == q.ay))
+      m = fmax(m, dist2_rn(__dsub_rn(q.qx[e], q.ax), __dsub_rn(q.qy[e], q.ay)));
+  f.thr0 = f2_thr(m);
+}
+
+// Bucket table: entry j (cell j of the CDF, 0..kSpCells; entry kSpCells
+// extrapolates the last cell: v >= nb there, always uncertain)
+// = {I_j - magic bits, phi_j - 0.5, S_j, 0.5 - g_j}
+// with I_j + phi_j = nb * cdf[j] (phi_j in [0, 1)), S_j = nb * (cdf[j+1] -
+// cdf[j]) and g_j = kF2G0 + kF2G1 * S_j: v - 0.5 = (phi_j - 0.5) + t * S_j,
+// rounded to the nearest integer by the magic add, is floor(v), and the
+// fraction of v is g_j away from an integer iff |v - 0.5 - round| < 0.5 - g_j.
+__device__ __forceinline__ void f2_table_setup(const double* __restrict__ cdf, float4* s_tab,
+                                               uint32_t tid, uint32_t nthreads) {
+  const double nb = (double)kSpBuckets;
+  for (uint32_t r = tid; r <= (uint32_t)kSpCells; r += nthreads) {
+    const uint32_t j = r < (uint32_t)kSpCells ? r : (uint32_t)kSpCells - 1;
+    const double V = nb * cdf[r];
+    const double I = floor(V);
+    const float S = (float)(nb * cdf[j + 1] - nb * cdf[j]);
+    s_tab[r] = make_float4(__int_as_float((int)I - kF2MagicBits), (float)(V - I) - 0.5f, S,
+                           0.5f - fmaf(S, kF2G1, kF2G0));
+  }
+}
+
+// The exact per-point F2 work (the plain path's visit): returns the code
+// (kSpNoCode when not bucketed) and whether the point survives round 1.
+__device__ __noinline__ uint32_t f2_exact(double x, double y, uint32_t i, const SpQuad& q,
+                                          const double* __restrict__ cdf,
+                                          const double* __restrict__ th, uint32_t& kept,
+                                          uint64_t& bd2, uint32_t& bidx, uint32_t& bties) {
+  kept = quad_keep(q.qx, q.qy, q.ex, q.ey, x, y) ? 1u : 0u;
+  if (!kept) return kSpNoCode;
+  if (x == q.ax && y == q.ay) return kSpNoCode;
+  const double dx = __dsub_rn(x, q.ax), dy = __dsub_rn(y, q.ay);
+  const uint32_t b = sp_bucket(dx, dy, cdf, th);
+  const uint64_t d2 = dbits(dist2_rn(dx, dy));
+  if (bidx == 0xffffffffu || d2 > bd2) { bd2 = d2; bidx = i; bties = 1; }
+  else if (d2 == bd2) { ++bties; if (i < bidx) bidx = i; }
+  return b;
+}
+
+// B points through the screen: first every point's screen, branch-free, so
+// the B independent FP64/FP32 chains interleave; then the rare uncertain
+// points and the dist2 candidates take their exact paths. Fills code[].
+template <int B>
+__device__ __forceinline__ void f2_points(const double (&x)[B], const double (&y)[B],
+                                          const uint32_t (&idx)[B], uint32_t (&code)[B], const SpQuad& q, const F2Float& F,
+                                          const float4* s_tab, const double* __restrict__ cdf,
+                                          const double* __restrict__ th, uint32_t& n1,
+                                          uint64_t& bd2, uint32_t& bidx, uint32_t& bties,
+                                          float thr) {
+  uint32_t sure = 0, inside = 0, cand = 0;
+#pragma unroll
+  for (int k = 0; k < B; ++k) {
+    const double dx = __dsub_rn(x[k], q.ax), dy = __dsub_rn(y[k], q.ay);
+    const float fx = __double2float_rn(dx), fy = __double2float_rn(dy);
+    float m = fmaf(F.ex[0], fy, fmaf(-F.ey[0], fx, -F.k[0]));
+#pragma unroll
+    for (int e = 1; e < 4; ++e) m = fminf(m, fmaf(F.ex[e], fy, fmaf(-F.ey[e], fx, -F.k[e])));
+    // cell coordinate in double, split exactly into j = floor(u) and t = u - j
+    const double den = __dadd_rn(fabs(dx), dy);
+    double r;  // 1/den: rcp.approx (2^-19.9) + one Newton step (2^-39.8): u errs <= 1.1e-9
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(den));
+    r = __fma_rn(r, __fma_rn(-den, r, 1.0), r);
+    const double u = fma(-1024.0, __dmul_rn(dx, r), 1023.5);  // u - 0.5
+    const double w = __dadd_rn(u, kF2MagicD);                  // round(u - 0.5) = floor(u)
+    const int j = (int)__double2loint(w);
+    const float t = __double2float_rn(__dadd_rn(__dsub_rn(u, __dsub_rn(w, kF2MagicD)), 0.5));
+    const bool okr = (uint32_t)j <= (uint32_t)kSpCells;
+    const float4 E = s_tab[okr ? j : 0];
+    const float v = fmaf(t, E.z, E.y);  // v - 0.5
+    const float w2 = __fadd_rn(v, kF2Magic);
+    const float dd = __fsub_rn(v, __fsub_rn(w2, kF2Magic));
+    const uint32_t bk = (uint32_t)(__float_as_int(E.x) + __float_as_int(w2));
+    const bool in = F.on && m > 1.f;
+    const bool ok = F.on && m < -1.f && den > 1e-280 && okr && fabsf(dd) < E.w && bk < kSpBuckets;
+    const bool cd = fmaf(fx, fx, __fmul_rn(fy, fy)) >= thr;
+    code[k] = in ? kSpNoCode : (ok ? bk : 0xffffffffu);
+    inside |= (in ? 1u : 0u) << k;
+    sure |= (ok ? 1u : 0u) << k;
+    cand |= (ok && cd ? 1u : 0u) << k;
+  }
+  n1 += __popc(sure);
+  // exceptions: uncertain points, and sure survivors that may be the farthest
+  const uint32_t exc = (~(sure | inside) | cand) & ((1u << B) - 1u);
+  if (exc == 0) return;
+#pragma unroll
+  for (int k = 0; k < B; ++k) {
+    if (!((exc >> k) & 1u)) continue;
+    if (!((sure >> k) & 1u)) {  // uncertain (~2e-4 of the points): the exact path
+      uint32_t kept;
+      code[k] = f2_exact(x[k], y[k], idx[k], q, cdf, th, kept, bd2, bidx, bties);
+      n1 += kept;
+    } else {  // may be (or tie) the farthest point
+      const uint64_t d2 = dbits(dist2_rn(__dsub_rn(x[k], q.ax), __dsub_rn(y[k], q.ay)));
+      const uint32_t i = idx[k];
+      if (bidx == 0xffffffffu || d2 > bd2) { bd2 = d2; bidx = i; bties = 1; }
+      else if (d2 == bd2) { ++bties; if (i < bidx) bidx = i; }
+    }
+  }
+}
+
+// ===========================================================================
 // F2: round 1 + bucket histogram + argmax dist2 + hash-partition counts.
 // The quad test is classify_quad (prefilter.hpp:47-63); n_after_round1 counts
 // every survivor (pipeline.hpp:93); points equal to the anchor leave the
@@ -537,6 +732,7 @@ __global__ void __launch_bounds__(kSpThreads, kHist ? 1 : 2) k_sp_hist(
   for (uint32_t j = threadIdx.x; j <= kSpCells; j += blockDim.x) s_cdf[j] = cdf[j];
   SpQuad q;
   load_quad(ext, q);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   __syncthreads();
   uint32_t n1 = 0, bidx = 0xffffffffu, bties = 0;
   uint64_t bd2 = 0;
@@ -619,7 +815,6 @@ __global__ void __launch_bounds__(kSpThreads, kHist ? 1 : 2) k_sp_hist(
   }
   __shared__ uint64_t s_d[32];
   __shared__ uint32_t s_i[32], s_t[32], s_n[32];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (lane == 0) { s_d[warp] = bd2; s_i[warp] = bidx; s_t[warp] = bties; s_n[warp] = n1; }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -637,6 +832,132 @@ __global__ void __launch_bounds__(kSpThreads, kHist ? 1 : 2) k_sp_hist(
   if (kHist) {
     uint32_t* hp = hist_part + (size_t)blockIdx.x * kSpBuckets;
     for (uint32_t b = threadIdx.x; b < kSpBuckets; b += blockDim.x) hp[b] = s_hist[b];
+  }
+}
+
+// F2 as a bulk-copy pipeline (the default for aligned inputs): one CTA per
+// SM, kF2Cons consumer threads plus one producer warp. The producer streams
+// tiles of kF2Tile points of xs and ys into a kF2Stages-deep shared-memory
+// ring with cp.async.bulk, completed on full[] mbarriers; each consumer warp
+// releases a stage on empty[] when it is done with it, so there is no
+// CTA-wide barrier per tile and the bytes in flight (kF2Stages x 32 KB per
+// SM) do not depend on registers or occupancy. Tiles go to CTAs round-robin;
+// the remainder (< one tile) is read directly by the last CTA. The per-point
+// work is the F2 screen with its exact fallback (f2_point / f2_exact);
+// outputs are identical to k_sp_hist<kVec, false>.
+#ifndef GSCAN_F2_CONS
+#define GSCAN_F2_CONS 512
+#endif
+#ifndef GSCAN_F2_PAIRS
+#define GSCAN_F2_PAIRS 3
+#endif
+// threads per CTA (all consumers; one CTA per SM) and point pairs per thread
+// per tile. Measured on C2 (us): 512x3 103.6, 512x2 107.3, 384x3 109.3,
+// 256x4 111.9, 768x1 117.7, 640x1 124.1, 1024x1 128.2: the FP64/FP32 chains
+// of several points per thread interleave, more warps with fewer points do not
+constexpr int kF2Cons = GSCAN_F2_CONS;
+constexpr int kF2Pairs = GSCAN_F2_PAIRS;
+constexpr int kF2Tile = 2 * kF2Pairs * kF2Cons;
+constexpr int kF2Stages = 4;
+using F2Ring = XYRing<kF2Tile, kF2Stages>;
+constexpr size_t kF2RingSmem = F2Ring::kSmem + (size_t)(kSpCells + 1) * 16;
+
+__global__ void __launch_bounds__(kF2Cons, 1) k_sp_hist_ring(
+    const double* __restrict__ xs, const double* __restrict__ ys, uint32_t n,
+    const ExtResult* __restrict__ ext, const double* __restrict__ cdf,
+    const double* __restrict__ th, uint16_t* __restrict__ codes, SpD2* __restrict__ d2part,
+    Counters* __restrict__ ctr, const SpState* __restrict__ st) {
+  extern __shared__ __align__(128) unsigned char f2_smem[];
+  if (st->fail) return;  // declined from the sample (k_sp_cdf)
+  F2Ring ring;
+  ring.setup(f2_smem + (size_t)(kSpCells + 1) * 16, xs, ys, n);
+  float4* s_tab = reinterpret_cast<float4*>(f2_smem);
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  ring.start();
+  f2_table_setup(cdf, s_tab, threadIdx.x, blockDim.x);
+  SpQuad q;
+  load_quad(ext, q);
+  F2Float F;
+  f2_float_setup(q, F);
+  __syncthreads();
+  uint32_t n1 = 0, bidx = 0xffffffffu, bties = 0;
+  uint64_t bd2 = 0;
+  float thr = F.thr0;
+  uint32_t* c2 = reinterpret_cast<uint32_t*>(codes);
+#ifndef GSCAN_F2_DEBUG
+#define GSCAN_F2_DEBUG 0  // 1: no compute (ring + stores only), 2: no memory (tile 0 reused)
+#endif
+  for (uint32_t k = 0; k < ring.mine; ++k) {
+    if (GSCAN_F2_DEBUG != 2 || k == 0) ring.wait(GSCAN_F2_DEBUG == 2 ? 0 : k);
+    const double2* x2 = reinterpret_cast<const double2*>(ring.tx(GSCAN_F2_DEBUG == 2 ? 0 : k));
+    const double2* y2 = reinterpret_cast<const double2*>(ring.ty(k));
+    const uint32_t i0 = ring.tile_start(k);
+    double2 vx[kF2Pairs], vy[kF2Pairs];
+#pragma unroll
+    for (int u = 0; u < kF2Pairs; ++u) {
+      vx[u] = x2[threadIdx.x + u * kF2Cons];
+      vy[u] = y2[threadIdx.x + u * kF2Cons];
+    }
+    if (GSCAN_F2_DEBUG != 2) ring.release(k);
+    if (GSCAN_F2_DEBUG == 1) {
+#pragma unroll
+      for (int u = 0; u < kF2Pairs; ++u)
+        c2[i0 / 2 + threadIdx.x + u * kF2Cons] = vx[u].x > 2.0 || vy[u].y > 2.0 ? 1u : 0u;
+      continue;
+    }
+    double bx[2 * kF2Pairs], by[2 * kF2Pairs];
+    uint32_t bi[2 * kF2Pairs], bc[2 * kF2Pairs];
+#pragma unroll
+    for (int u = 0; u < kF2Pairs; ++u) {
+      bx[2 * u] = vx[u].x; bx[2 * u + 1] = vx[u].y;
+      by[2 * u] = vy[u].x; by[2 * u + 1] = vy[u].y;
+      bi[2 * u] = i0 + 2 * (threadIdx.x + u * kF2Cons);
+      bi[2 * u + 1] = bi[2 * u] + 1;
+    }
+    f2_points<2 * kF2Pairs>(bx, by, bi, bc, q, F, s_tab, cdf, th, n1, bd2, bidx, bties, thr);
+#pragma unroll
+    for (int u = 0; u < kF2Pairs; ++u) c2[bi[2 * u] / 2] = bc[2 * u] | (bc[2 * u + 1] << 16);
+    // warp-wide screen threshold: a point below the warp's best cannot be the
+    // maximum or tie it (non-negative float bits order as the values)
+    const float mine_t = bidx != 0xffffffffu ? f2_thr(bitsd(bd2)) : 0.f;
+    thr = fmaxf(thr, __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(mine_t))));
+  }
+  // remainder (< one tile): the last CTA, direct loads, exact path
+  if (blockIdx.x == gridDim.x - 1) {
+    for (uint32_t i = (n / kF2Tile) * kF2Tile + threadIdx.x; i < n; i += kF2Cons) {
+      uint32_t kept;
+      const uint32_t c = f2_exact(xs[i], ys[i], i, q, cdf, th, kept, bd2, bidx, bties);
+      n1 += kept;
+      codes[i] = (uint16_t)c;
+    }
+  }
+  // block reductions: n1 (sum), (d2 max, ties) -- as k_sp_hist
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    n1 += __shfl_xor_sync(0xffffffffu, n1, o);
+    const uint64_t od = __shfl_xor_sync(0xffffffffu, bd2, o);
+    const uint32_t oi = __shfl_xor_sync(0xffffffffu, bidx, o);
+    const uint32_t ot = __shfl_xor_sync(0xffffffffu, bties, o);
+    if (oi != 0xffffffffu) {
+      if (bidx == 0xffffffffu || od > bd2) { bd2 = od; bidx = oi; bties = ot; }
+      else if (od == bd2) { bties += ot; if (oi < bidx) bidx = oi; }
+    }
+  }
+  __shared__ uint64_t s_d[32];
+  __shared__ uint32_t s_i[32], s_t[32], s_n[32];
+  if (lane == 0) { s_d[warp] = bd2; s_i[warp] = bidx; s_t[warp] = bties; s_n[warp] = n1; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t tot = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      tot += s_n[w];
+      if (w == 0) continue;
+      if (s_i[w] == 0xffffffffu) continue;
+      if (bidx == 0xffffffffu || s_d[w] > bd2) { bd2 = s_d[w]; bidx = s_i[w]; bties = s_t[w]; }
+      else if (s_d[w] == bd2) { bties += s_t[w]; if (s_i[w] < bidx) bidx = s_i[w]; }
+    }
+    d2part[blockIdx.x] = SpD2{bd2, bidx, bidx == 0xffffffffu ? 0u : bties};
+    if (tot) atomicAdd(&ctr->n1, tot);
   }
 }
 
