@@ -263,6 +263,18 @@ int gscan_last_sparse_info(const gscan_handle* h, uint32_t* used, uint32_t* fail
 enum { GSCAN_GEN_SQUARE = 0, GSCAN_GEN_DISK = 1, GSCAN_GEN_CIRCLE = 2, GSCAN_GEN_COLLINEAR = 3 };
 /* datagen::gen_* (datagen.hpp:32-91), bit-identical to the reference. */
 int gscan_generate(int kind, uint64_t n, uint64_t seed, double* xs, double* ys);
+/* On-device gen_square (datagen.hpp:32-41): points
+ * [lo, hi) of the reference's gen_square(n, seed) sequence (any n >= hi),
+ * bit-identical to gscan_generate(GSCAN_GEN_SQUARE, ...), written to device
+ * arrays d_xs[0 .. hi-lo), d_ys[0 .. hi-lo) on the handle's stream
+ * (mt19937_64 jump-ahead + per-generator engines; synchronises the stream).
+ * A rank of a sharded run generates only its own shard. */
+int gscan_generate_square_device(gscan_handle* h, uint64_t seed, uint64_t lo, uint64_t hi,
+                                 double* d_xs, double* d_ys);
+/* Host self-check of the generator's mt19937_64 jump-ahead: jumps `blocks`
+ * x 2^20 words and compares the next 312 outputs with a sequentially
+ * advanced std::mt19937_64. Returns the number of mismatches (0 = exact). */
+int gscan_mt64_jump_check(uint64_t seed, uint64_t blocks);
 /* tests/support.hpp:54-63 gen_grid. */
 int gscan_generate_grid(uint64_t n, uint64_t seed, int lo, int hi, double* xs, double* ys);
 

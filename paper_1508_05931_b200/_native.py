@@ -116,6 +116,8 @@ SIGNATURES = {
     "gscan_last_kernel_times": (C.c_int, [_P, C.POINTER(C.c_char_p), _DP, C.c_int]),
     "gscan_generate": (C.c_int, [C.c_int, _U64, _U64, _DP, _DP]),
     "gscan_generate_grid": (C.c_int, [_U64, _U64, C.c_int, C.c_int, _DP, _DP]),
+    "gscan_generate_square_device": (C.c_int, [_P, _U64, _U64, _U64, _P, _P]),
+    "gscan_mt64_jump_check": (C.c_int, [_U64, _U64]),
 }
 
 _lib = None

@@ -24,6 +24,8 @@
 #include "graham.cuh"
 #include "sparse.cuh"
 #include "graham_tree.cuh"
+#include "mtgen.cuh"
+#include "mt64_jump.h"
 
 using namespace gscan;
 
@@ -58,6 +60,11 @@ struct SpGraphKey {
 
 struct gscan_handle {
   int device = 0;
+  // on-device gen_square (mtgen.cuh): engine states per generator, jump table
+  uint64_t* mt_states = nullptr;
+  uint64_t mt_states_cap = 0;  // generators
+  uint64_t* mt_jtab = nullptr;
+  int mt_jtab_nb = 0;
   cudaStream_t stream = nullptr;
   cudaStream_t side = nullptr;          // duplicate check runs here, overlapping the tail
   cudaStream_t cap_stream = nullptr;    // CUDA graph capture
@@ -1763,6 +1770,8 @@ int gscan_destroy(gscan_handle* h) {
   dfree(h->sp_gcnt); dfree(h->sp_phimax); dfree(h->sp_prefmax); dfree(h->sp_slice);
   dfree(h->sp_ccnt); dfree(h->sp_cstart); dfree(h->sp_wcnt); dfree(h->sp_wstart); dfree(h->sp_rlo);
   dfree(h->sp_seglo); dfree(h->sp_seghi); dfree(h->sp_st);
+  if (h->mt_states) cudaFree(h->mt_states);
+  if (h->mt_jtab) cudaFree(h->mt_jtab);
   if (h->h_sp) cudaFreeHost(h->h_sp);
   if (h->h_ctr) cudaFreeHost(h->h_ctr);
   if (h->h_info) cudaFreeHost(h->h_info);
@@ -2249,6 +2258,54 @@ int gscan_dist_dup_check(gscan_handle* h, const uint64_t* d_recv, uint64_t n_rec
   CU(cudaGetLastError());
   TRY(dist_read_state(h));
   *dup_found = (h->h_sp->fail & (kSpFailDup | kSpFailCap)) ? 1u : 0u;
+  return GSCAN_OK;
+}
+
+int gscan_generate_square_device(gscan_handle* h, uint64_t seed, uint64_t lo, uint64_t hi,
+                                 double* d_xs, double* d_ys) {
+  if (!h || hi < lo || ((!d_xs || !d_ys) && hi > lo)) return GSCAN_E_INVALID;
+  if (hi == lo) return GSCAN_OK;
+  if (hi > (1ull << 40)) return fail(h, GSCAN_E_TOO_LARGE, "generator range above 2^40 points");
+  CU(cudaSetDevice(h->device));
+  const uint64_t P = (2 * hi - 1) / kMtL + 1;  // generators 0 .. P-1 (states of all of them)
+  int nb = 0;
+  while ((1ull << nb) < P) ++nb;
+  const int nbt = std::max(nb, 1);
+  if (nbt > h->mt_jtab_nb) {
+    const std::vector<uint64_t>& tab = mt64::jump_table(kMtL, nbt);
+    if (h->mt_jtab) CU(cudaFree(h->mt_jtab));
+    h->mt_jtab = nullptr;
+    CU(cudaMalloc(&h->mt_jtab, tab.size() * 8));
+    CU(cudaMemcpy(h->mt_jtab, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice));
+    h->mt_jtab_nb = nbt;
+  }
+  if (P > h->mt_states_cap) {
+    if (h->mt_states) CU(cudaFree(h->mt_states));
+    h->mt_states = nullptr;
+    CU(cudaMalloc(&h->mt_states, P * kMtN * 8));
+    h->mt_states_cap = P;
+  }
+  static std::once_flag attr;
+  std::call_once(attr, [] {
+    cudaFuncSetAttribute(k_mt_jump, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMtJumpSmem);
+  });
+  uint64_t st0[kMtN];
+  mt64::seed_state(seed, st0);
+  CU(cudaMemcpyAsync(h->mt_states, st0, sizeof(st0), cudaMemcpyHostToDevice, h->stream));
+  for (int b = 0; b < nb; ++b) {
+    const uint64_t half = 1ull << b;
+    const uint64_t count = std::min(half, P - half);
+    Launch L(h, "k_mt_jump");
+    k_mt_jump<<<(uint32_t)count, kMtThreads, kMtJumpSmem, h->stream>>>(
+        h->mt_states, (uint32_t)half, (uint32_t)count, h->mt_jtab + (size_t)b * kMtWords);
+  }
+  const uint64_t g0 = (2 * lo) / kMtL;
+  {
+    Launch L(h, "k_mt_gen");
+    k_mt_gen<<<(uint32_t)(P - g0), kMtThreads, 0, h->stream>>>(h->mt_states, g0, lo, hi, d_xs, d_ys);
+  }
+  CU(cudaGetLastError());
+  CU(cudaStreamSynchronize(h->stream));
   return GSCAN_OK;
 }
 

@@ -255,6 +255,14 @@ class Engine:
             self._raise(rc, "full_pipeline")
         return out_len.value, StageStats._from_c(st)
 
+    def generate_square_device(self, seed: int, lo: int, hi: int, d_xs: int, d_ys: int) -> None:
+        """Points [lo, hi) of gen_square(n >= hi, seed) (datagen.hpp:32-41) into
+        device arrays, bit-identical to the host generator (mtgen.cuh)."""
+        rc = self._lib.gscan_generate_square_device(self._h, int(seed), int(lo), int(hi),
+                                                    C.c_void_p(d_xs), C.c_void_p(d_ys))
+        if rc:
+            self._raise(rc, "generate_square_device")
+
     # -- stage entry points (device pointers) --
     def stage_extremes(self, d_xs: int, d_ys: int, n: int) -> list[int]:
         out = (C.c_uint64 * 5)()

@@ -261,3 +261,12 @@ def test_harness_monotone_chain_matches_oracle(oracle_mod, kind, n, seed):
     if len(hull) >= 3:
         c = hull.mean(0)
         assert strictly_inside(hull, np.array([c[0]]), np.array([c[1]]))[0]
+
+
+def test_mt64_jump_ahead_host():
+    """The on-device generator's jump-ahead (mt64_jump.cpp): the jumped
+    mt19937_64 state reproduces a sequentially advanced std::mt19937_64."""
+    from paper_1508_05931_b200 import _native as N
+    lib = N.load()
+    for seed, blocks in [(1, 0), (1, 1), (1, 6), (7, 37), (2**63 + 5, 3)]:
+        assert lib.gscan_mt64_jump_check(seed, blocks) == 0, (seed, blocks)
