@@ -73,6 +73,12 @@ struct gscan_handle {
   int sm_count = 148;
   uint64_t cap = 0;  // points
   uint64_t nb_cap = 0;
+  // large mode (cap > kFullSortMaxN): the buffers only the full sort needs at
+  // full size are sized for the sparse path's walk (wcap elements), and the
+  // full-sort fallback is unavailable on one device
+  bool large = false;
+  uint64_t wcap = 0;
+  uint64_t host_cap = 0;  // d_xs/d_ys (host entry only), allocated on first use
   std::string err;
   uint64_t launches = 0;
   bool profiling = false;
@@ -124,6 +130,11 @@ struct gscan_handle {
   uint32_t* sp_cells = nullptr;  // sample counts per cell
   uint32_t* sp_big = nullptr;    // candidate buckets for the CTA sorter
   uint32_t* sp_bigg = nullptr;   // gathered buckets for the CTA sorter
+  uint32_t* sp_hugeg = nullptr;  // gathered buckets above kSpGatherCap
+  unsigned char* sp_huge_scr = nullptr;  // their per-CTA global scratch (sm_count areas)
+  uint32_t sp_huge_cap = 0;      // elements per area (0: inputs too small to need it)
+  uint64_t* sp_dup_scr = nullptr;  // duplicate check: sub-partition scratch of large partitions
+  uint32_t sp_dup_scap = 0;        // entries per (CTA, group) area
   uint32_t *sp_gcount = nullptr, *sp_ccount = nullptr, *sp_hcount = nullptr;  // per-CTA emissions
   uint64_t* sp_dup2 = nullptr;   // partitioned hash list (n)
   uint64_t* sp_side_status = nullptr;  // look-back status of the side stream's scan
@@ -202,7 +213,7 @@ void dfree(T*& p) {
 
 void free_buffers(gscan_handle* h) {
   h->sp_graph_ok = false;
-  dfree(h->d_xs); dfree(h->d_ys); dfree(h->surv); dfree(h->keys); dfree(h->rank);
+  dfree(h->surv); dfree(h->keys); dfree(h->rank);
   dfree(h->rec); dfree(h->A_x); dfree(h->A_y); dfree(h->A_i); dfree(h->C_x); dfree(h->C_y);
   dfree(h->C_i); dfree(h->flags); dfree(h->stack); dfree(h->d_out); dfree(h->status);
   dfree(h->hist); dfree(h->bstart); dfree(h->cursor); dfree(h->oversize); dfree(h->best);
@@ -211,7 +222,7 @@ void free_buffers(gscan_handle* h) {
   dfree(h->g_keep); dfree(h->g_misc);
   dfree(h->g_stA); dfree(h->g_stB); dfree(h->g_lenA); dfree(h->g_lenB); dfree(h->g_scr);
   dfree(h->lb_status); dfree(h->lb_ctr); dfree(h->sp_eb); dfree(h->sp_gx); dfree(h->sp_gy); dfree(h->sp_Wb); dfree(h->sp_Ws); dfree(h->sp_Rb); dfree(h->sp_Rs); dfree(h->sp_dup);
-  dfree(h->sp_codes); dfree(h->sp_phi32); dfree(h->sp_dup2); dfree(h->tw_pool);
+  dfree(h->sp_codes); dfree(h->sp_phi32); dfree(h->sp_dup2); dfree(h->tw_pool); dfree(h->sp_huge_scr); dfree(h->sp_dup_scr);
   h->tw_nmax = 0;
   h->g_st_cap = 0;
   h->g_len_cap = 0;
@@ -243,27 +254,41 @@ uint32_t sparse_region_cap(const gscan_handle* h, uint64_t n) {
 // look-back slots of the sparse path's scans (scan_u32_slot)
 enum LbSlot { kLbBstart = 0, kLbGs, kLbCstart, kLbWstart, kLbCompact, kLbSlots };
 
+// Above this many points one device runs the sparse path only: the full
+// sort's per-point buffers (~120 B/pt) would not fit next to the input and
+// the sparse path's own (~50 B/pt) at 1B points. GSCAN_LARGE_MIN (dev/tests)
+// lowers the threshold.
+constexpr uint64_t kFullSortMaxN = 400000000ull;
+
+uint64_t full_sort_max(void) {
+  const char* v = getenv("GSCAN_LARGE_MIN");
+  return (v && *v) ? strtoull(v, nullptr, 10) : kFullSortMaxN;
+}
+
 int reserve(gscan_handle* h, uint64_t n) {
   if (n <= h->cap) return GSCAN_OK;
   free_buffers(h);
   const uint64_t m = n + 1;
-  CU(cudaMalloc(&h->d_xs, m * 8));
-  CU(cudaMalloc(&h->d_ys, m * 8));
+  h->large = n > full_sort_max();
+  // walk-side buffers: full size, or in large mode the sparse path's bound on
+  // gathered + candidate points (checked on the device, k_sp_emit_place)
+  h->wcap = h->large ? std::max<uint64_t>(n / 12, 1ull << 23) : m;
+  const uint64_t mw = h->wcap;
   // the sparse path's emission regions may span more slots than points
   const uint64_t mr = std::max<uint64_t>(m, (uint64_t)h->sp_grid * sparse_region_cap(h, n) + 64);
   CU(cudaMalloc(&h->surv, mr * 4));
-  CU(cudaMalloc(&h->keys, m * 8));
+  CU(cudaMalloc(&h->keys, mw * 8));
   CU(cudaMalloc(&h->rank, mr * 4));
-  CU(cudaMalloc(&h->rec, m * sizeof(PtRec)));
-  CU(cudaMalloc(&h->A_x, m * 8));
-  CU(cudaMalloc(&h->A_y, m * 8));
-  CU(cudaMalloc(&h->A_i, m * 4));
-  CU(cudaMalloc(&h->C_x, m * 8));
-  CU(cudaMalloc(&h->C_y, m * 8));
-  CU(cudaMalloc(&h->C_i, m * 4));
-  CU(cudaMalloc(&h->flags, m));
-  CU(cudaMalloc(&h->stack, m * 4));
-  CU(cudaMalloc(&h->d_out, m * 4));
+  CU(cudaMalloc(&h->rec, mw * sizeof(PtRec)));
+  CU(cudaMalloc(&h->A_x, mw * 8));
+  CU(cudaMalloc(&h->A_y, mw * 8));
+  CU(cudaMalloc(&h->A_i, mw * 4));
+  CU(cudaMalloc(&h->C_x, mw * 8));
+  CU(cudaMalloc(&h->C_y, mw * 8));
+  CU(cudaMalloc(&h->C_i, mw * 4));
+  CU(cudaMalloc(&h->flags, mw));
+  CU(cudaMalloc(&h->stack, mw * 4));
+  CU(cudaMalloc(&h->d_out, mw * 4));
   const uint32_t nb = buckets_for(n);
   h->nb_cap = nb;
   CU(cudaMalloc(&h->hist, (nb + 2) * 4));
@@ -272,13 +297,13 @@ int reserve(gscan_handle* h, uint64_t n) {
   CU(cudaMalloc(&h->oversize, (nb + 2) * 4));
   h->best_cap = (nb + kBucketsPerBlock - 1) / kBucketsPerBlock + kCtaSortGrid + 1;
   CU(cudaMalloc(&h->best, h->best_cap * sizeof(BucketBest)));
-  const uint64_t nch = (m + kChunk - 1) / kChunk + 2;
-  CU(cudaMalloc(&h->g_chain, m * 4));
+  const uint64_t nch = (mw + kChunk - 1) / kChunk + 2;
+  CU(cudaMalloc(&h->g_chain, mw * 4));
   CU(cudaMalloc(&h->g_len, nch * 4));
   CU(cudaMalloc(&h->g_off, (nch + 1) * 4));
-  CU(cudaMalloc(&h->g_q0, m * 4));
-  CU(cudaMalloc(&h->g_q1, m * 4));
-  CU(cudaMalloc(&h->g_parent, m * 4));
+  CU(cudaMalloc(&h->g_q0, mw * 4));
+  CU(cudaMalloc(&h->g_q1, mw * 4));
+  CU(cudaMalloc(&h->g_parent, mw * 4));
   CU(cudaMalloc(&h->g_btop, (nch + 1) * 4));
   CU(cudaMalloc(&h->g_jk, nch * 4));
   CU(cudaMalloc(&h->g_je, nch * 4));
@@ -298,13 +323,31 @@ int reserve(gscan_handle* h, uint64_t n) {
   CU(cudaMalloc(&h->sp_eb, mr * 4));
   CU(cudaMalloc(&h->sp_gx, mr * 8));
   CU(cudaMalloc(&h->sp_gy, mr * 8));
-  CU(cudaMalloc(&h->sp_Wb, m * 4));
-  CU(cudaMalloc(&h->sp_Ws, m * 4));
-  CU(cudaMalloc(&h->sp_Rb, m * 4));
-  CU(cudaMalloc(&h->sp_Rs, m * 4));
+  CU(cudaMalloc(&h->sp_Wb, mw * 4));
+  CU(cudaMalloc(&h->sp_Ws, mw * 4));
+  CU(cudaMalloc(&h->sp_Rb, mw * 4));
+  CU(cudaMalloc(&h->sp_Rs, mw * 4));
   CU(cudaMalloc(&h->sp_dup, (mr + 4096) * 8));
   // partitioned hashes: the runs are padded to whole sectors (k_sp_dup_part<true>)
   CU(cudaMalloc(&h->sp_dup2, (m + 4096 + 3ull * kSpParts * 2 * (uint64_t)h->sm_count) * 8));
+  // gathered buckets above the shared-memory sorter (about n1 / kSpBuckets
+  // points each, n1 / n ~ 1/3 - 2/3 for squares): per-CTA global scratch for
+  // up to 8x the mean bucket of n points (1B square, seed 1: mean gathered
+  // bucket 13.8K, largest 88.7K = 4.4x n / kSpBuckets)
+  h->sp_huge_cap = 0;
+  if (n / kSpBuckets * 8 > kSpGatherCap) {
+    h->sp_huge_cap = (uint32_t)std::max<uint64_t>(2 * kSpGatherCap, 8 * (n / kSpBuckets) + 64);
+    CU(cudaMalloc(&h->sp_huge_scr,
+                  (size_t)h->sm_count * ((size_t)h->sp_huge_cap * kSpHugeBytes + 16)));
+  }
+  // duplicate check of partitions above kSpDupMaxRounds rounds (n1 / kSpParts
+  // hashes each, n1 <= n): sub-partition scratch for up to 2x the mean
+  // partition of n points
+  h->sp_dup_scap = 0;
+  if (n / kSpParts > (uint64_t)kSpDupMaxRounds * kSpDupGRound) {
+    h->sp_dup_scap = (uint32_t)(2 * (n / kSpParts) + 4096);
+    CU(cudaMalloc(&h->sp_dup_scr, (size_t)h->sm_count * kSpDupGroups * h->sp_dup_scap * 8));
+  }
   CU(cudaMalloc(&h->sp_codes, (m + 1) * sizeof(uint16_t)));
   CU(cudaMalloc(&h->sp_phi32, (m + 1) * sizeof(float)));
   h->cap = n;
@@ -942,6 +985,7 @@ int sparse_init(gscan_handle* h) {
   CU(cudaMalloc(&h->sp_cells, kSpCells * 4));
   CU(cudaMalloc(&h->sp_big, nb * 4));
   CU(cudaMalloc(&h->sp_bigg, nb * 4));
+  CU(cudaMalloc(&h->sp_hugeg, nb * 4));
   CU(cudaMalloc(&h->sp_gcount, G * 4));
   CU(cudaMalloc(&h->sp_side_status, ((kSpParts * 2 * G + 1 + kScanTile - 1) / kScanTile + 64) * 8));
   CU(cudaMalloc(&h->sp_side_ticket, sizeof(Counters)));
@@ -1183,7 +1227,8 @@ int sp_seg_sortg(gscan_handle* h, const SpCtx& c, const double* gx, const double
                                                      h->sp_gcount, c.cap, h->sp_gcnt, c.gs,
                                                      h->ext, h->sp_st, h->rec,
                                                      region_xy ? h->sp_gx : nullptr,
-                                                     region_xy ? h->sp_gy : nullptr);
+                                                     region_xy ? h->sp_gy : nullptr,
+                                                     (uint32_t)std::min<uint64_t>(h->wcap, 0xffffffffu));
   }
   {
     Launch L(h, "k_sp_sort_gathered", s);
@@ -1195,7 +1240,13 @@ int sp_seg_sortg(gscan_handle* h, const SpCtx& c, const double* gx, const double
     Launch L(h, "k_sp_sort_gathered_big", s);
     k_sp_sort_gathered_big<<<h->sm_count, kSpSortThreads, kSpBigSmem, s>>>(
         h->sp_bigg, h->sp_bstart, c.gs, h->sp_hist, h->rec, h->ext, h->sp_st, h->A_x, h->A_y,
-        h->A_i);
+        h->A_i, h->sp_hugeg, h->sp_huge_cap);
+  }
+  if (h->sp_huge_cap) {  // inputs large enough for buckets above kSpGatherCap
+    Launch L(h, "k_sp_sort_gathered_huge", s);
+    k_sp_sort_gathered_huge<<<h->sm_count, kSpSortThreads, 0, s>>>(
+        h->sp_hugeg, h->sp_bstart, c.gs, h->sp_hist, h->rec, h->ext, h->sp_st, h->A_x, h->A_y,
+        h->A_i, h->sp_huge_scr, h->sp_huge_cap);
   }
   {
     Launch L(h, "k_sp_slices", s);
@@ -1234,7 +1285,8 @@ int sp_seg_walk(gscan_handle* h, const SpCtx& c, const double* cx, const double*
     Launch L(h, "k_sp_rank_c", s);
     k_sp_emit_place<1><<<dim3(4, c.G), 256, 0, s>>>(cx, cy, h->surv, h->sp_eb, h->rank,
                                                     h->sp_ccount, c.cap, h->sp_ccnt, nullptr,
-                                                    h->ext, h->sp_st, h->rec);
+                                                    h->ext, h->sp_st, h->rec, nullptr, nullptr,
+                                                    (uint32_t)std::min<uint64_t>(h->wcap, 0xffffffffu));
   }
   TRY(scan_u32_slot(h, h->sp_ccnt, nb, h->sp_cstart, kLbCstart, s));
   {
@@ -1258,7 +1310,7 @@ int sp_seg_walk(gscan_handle* h, const SpCtx& c, const double* cx, const double*
     Launch L(h, "k_sp_sort_cand_big", s);
     k_sp_sort_cand_big<<<h->sm_count, kSpSortThreads, kSpBigSmem, s>>>(
         h->sp_big, h->rec, h->sp_cstart, h->sp_wstart, h->sp_slice, h->ext, h->sp_st, h->C_x,
-        h->C_y, h->C_i, h->sp_Wb, h->sp_Ws, h->flags);
+        h->C_y, h->C_i, h->sp_Wb, h->sp_Ws, h->flags, h->sp_huge_scr, h->sp_huge_cap);
   }
   {
     Launch L(h, "k_sp_place_gathered", s);
@@ -1406,7 +1458,8 @@ int sparse_dup_check(gscan_handle* h, uint32_t n) {
   {
     Launch L(h, "k_sp_dups", h->side);
     k_sp_dups<<<h->sm_count, 1024, kSpSideSmem, h->side>>>(h->sp_dup2, h->sp_part_off, nl, h->sp_st,
-                                                              h->sp_side_work + 1, side_free_sms_dups());
+                                                              h->sp_side_work + 1, side_free_sms_dups(),
+                                                              h->sp_dup_scr, h->sp_dup_scap);
   }
   CU(cudaEventRecord(h->ev_dup, h->side));
   return GSCAN_OK;
@@ -1546,10 +1599,20 @@ int run_pipeline(gscan_handle* h, const double* xs, const double* ys, uint64_t n
   h->sp_used = 0;
   h->sp_fail = 0;
   bool ext_ready = false;
+  if (h->large && !sparse_eligible(h, n64, cfg))
+    return fail(h, GSCAN_E_TOO_LARGE,
+                "%llu points: above %llu points one device runs only the default configuration "
+                "(sparse path); shard the input (distributed.sharded_hull)",
+                (unsigned long long)n64, (unsigned long long)full_sort_max());
   if (sparse_eligible(h, n64, cfg)) {
     bool ok = false;
     TRY(run_sparse(h, xs, ys, n, cfg, hull_size, st, &ok));
     if (ok) return GSCAN_OK;
+    if (h->large)
+      return fail(h, GSCAN_E_TOO_LARGE,
+                  "%llu points declined the sparse path (fail bits %#x); the full-sort fallback "
+                  "needs more than one device's memory above %llu points: shard the input",
+                  (unsigned long long)n64, h->sp_fail, (unsigned long long)full_sort_max());
     ext_ready = true;  // K1 ran on this input inside the sparse attempt
   }
   CU(cudaEventRecord(h->ev[0], h->stream));
@@ -1764,8 +1827,9 @@ int gscan_destroy(gscan_handle* h) {
   cudaSetDevice(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
   free_buffers(h);
+  dfree(h->d_xs); dfree(h->d_ys);
   dfree(h->partials); dfree(h->ext); dfree(h->ctr); dfree(h->scratch64);
-  dfree(h->sp_th); dfree(h->sp_cdf); dfree(h->sp_cells); dfree(h->sp_big); dfree(h->sp_bigg); dfree(h->sp_gcount); dfree(h->sp_side_status); dfree(h->sp_side_ticket); dfree(h->sp_side_work); dfree(h->sp_ccount); dfree(h->sp_hcount); dfree(h->sp_hist_part); dfree(h->sp_phi_part); dfree(h->sp_part_off);
+  dfree(h->sp_th); dfree(h->sp_cdf); dfree(h->sp_cells); dfree(h->sp_big); dfree(h->sp_bigg); dfree(h->sp_hugeg); dfree(h->sp_gcount); dfree(h->sp_side_status); dfree(h->sp_side_ticket); dfree(h->sp_side_work); dfree(h->sp_ccount); dfree(h->sp_hcount); dfree(h->sp_hist_part); dfree(h->sp_phi_part); dfree(h->sp_part_off);
   dfree(h->sp_d2); dfree(h->sp_hist); dfree(h->sp_bstart); dfree(h->sp_gbits); dfree(h->sp_glist);
   dfree(h->sp_gcnt); dfree(h->sp_phimax); dfree(h->sp_prefmax); dfree(h->sp_slice);
   dfree(h->sp_ccnt); dfree(h->sp_cstart); dfree(h->sp_wcnt); dfree(h->sp_wstart); dfree(h->sp_rlo);
@@ -1887,6 +1951,14 @@ int gscan_hull_f64(gscan_handle* h, const double* xs, const double* ys, uint64_t
   const gscan_config c = resolve(cfg);
   TRY(validate(h, n, c));
   TRY(reserve(h, n));
+  if (n > h->host_cap) {  // device copy of host input, host entry only
+    dfree(h->d_xs);
+    dfree(h->d_ys);
+    h->host_cap = 0;
+    CU(cudaMalloc(&h->d_xs, (n + 1) * 8));
+    CU(cudaMalloc(&h->d_ys, (n + 1) * 8));
+    h->host_cap = n;
+  }
   CU(cudaMemcpyAsync(h->d_xs, xs, n * 8, cudaMemcpyHostToDevice, h->stream));
   CU(cudaMemcpyAsync(h->d_ys, ys, n * 8, cudaMemcpyHostToDevice, h->stream));
   uint64_t hs = 0;
@@ -1944,6 +2016,7 @@ int gscan_stage_round1(gscan_handle* h, const double* d_xs, const double* d_ys, 
   TRY(validate(h, n, c));
   CU(cudaSetDevice(h->device));
   TRY(reserve(h, n));
+  if (h->large) return fail(h, GSCAN_E_TOO_LARGE, "stage entry points need n <= %llu", (unsigned long long)full_sort_max());
   CU(cudaMemsetAsync(h->ctr, 0, sizeof(Counters), h->stream));
   TRY(stage_round1(h, d_xs, d_ys, (uint32_t)n, 1, nullptr, /*ordered=*/true));
   TRY(sync_counters(h));
@@ -1961,6 +2034,7 @@ int gscan_stage_sorted(gscan_handle* h, const double* d_xs, const double* d_ys, 
   TRY(validate(h, n, c));
   CU(cudaSetDevice(h->device));
   TRY(reserve(h, n));
+  if (h->large) return fail(h, GSCAN_E_TOO_LARGE, "stage entry points need n <= %llu", (unsigned long long)full_sort_max());
   CU(cudaMemsetAsync(h->ctr, 0, sizeof(Counters), h->stream));
   TRY(stage_round1(h, d_xs, d_ys, (uint32_t)n, 0));
   TRY(stage_annotate_sort(h, d_xs, d_ys, (uint32_t)n, -1, -1));
@@ -1983,6 +2057,7 @@ int gscan_stage_discard(gscan_handle* h, const double* d_xs, const double* d_ys,
   TRY(validate(h, n, c));
   CU(cudaSetDevice(h->device));
   TRY(reserve(h, n));
+  if (h->large) return fail(h, GSCAN_E_TOO_LARGE, "stage entry points need n <= %llu", (unsigned long long)full_sort_max());
   CU(cudaMemsetAsync(h->ctr, 0, sizeof(Counters), h->stream));
   TRY(stage_round1(h, d_xs, d_ys, (uint32_t)n, 0));
   TRY(stage_annotate_sort(h, d_xs, d_ys, (uint32_t)n, -1, -1));

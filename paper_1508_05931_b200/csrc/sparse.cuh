@@ -110,6 +110,7 @@ struct SpState {
   double dmax2;        // bounding-box diagonal^2
   uint32_t cert;       // 1: certificate holds (F6 skipped)
   uint32_t n_bigg;     // gathered buckets for the bitonic sorter
+  uint32_t n_hugeg;    // gathered buckets above kSpGatherCap (global-scratch sorter)
 };
 
 // ---------------------------------------------------------------------------
@@ -1659,16 +1660,105 @@ __device__ __forceinline__ bool named_sync_or(uint32_t id, uint32_t n, bool v) {
   return r != 0;
 }
 
+// One group's shared-memory hash-set pass over arr[0, n) (entries ~0 are
+// sector padding): rounds of <= kSpDupGRound entries, each round the entries
+// whose bits 0-15 select it (disjoint from the slot bits 18-31, the tag bits
+// 32-48 and the partition bits 53-63, so a round's entries spread over the
+// whole table). Equal hashes -> *dup; a skewed round -> *full.
+__device__ __forceinline__ void dup_set_pass(const uint64_t* __restrict__ arr, uint32_t n,
+                                             uint32_t* tab, uint32_t gt, uint32_t bar,
+                                             bool& dup, bool& full, SpState* st) {
+  constexpr uint32_t kGT = kSpDupGT, kB = 8;  // entries per thread per batch
+#ifdef GSCAN_DUPS_FORCE_BIG  // test builds: the large-partition encoding everywhere
+  const uint32_t ib = kSpDupIdxBitsBig;
+#else
+  const uint32_t ib = n < (1u << kSpDupIdxBits) ? kSpDupIdxBits : kSpDupIdxBitsBig;  // uniform
+#endif
+  const uint32_t imask = (1u << ib) - 1, tmask = (1u << (32 - ib)) - 1;
+  if (n >= imask) {
+    full = true;
+    if (gt == 0) atomicMax(&st->why, 8u);
+    return;
+  }
+  const uint32_t rounds = (n + kSpDupGRound - 1) / kSpDupGRound;
+  for (uint32_t r = 0; r < rounds; ++r) {  // uniform over the group (named barriers)
+    // the first batch's loads are in flight while the table is cleared
+    uint64_t hv[kB];
+#pragma unroll
+    for (uint32_t u = 0; u < kB; ++u) {
+      const uint32_t e = gt + u * kGT;
+      hv[u] = e < n ? arr[e] : ~0ull;
+    }
+    named_sync(bar, kGT);  // the previous round's (or pass's) probes are done
+    uint4* t4 = reinterpret_cast<uint4*>(tab);
+    for (uint32_t k = gt; k < kSpDupGSlots / 4; k += kGT) t4[k] = make_uint4(~0u, ~0u, ~0u, ~0u);
+    named_sync(bar, kGT);
+    for (uint32_t e0 = gt; e0 < n; e0 += kB * kGT) {
+      if (e0 != gt) {
+#pragma unroll
+        for (uint32_t u = 0; u < kB; ++u) {
+          const uint32_t e = e0 + u * kGT;
+          hv[u] = e < n ? arr[e] : ~0ull;
+        }
+      }
+#pragma unroll
+      for (uint32_t u = 0; u < kB; ++u) {
+        const uint64_t h = hv[u];
+        const uint32_t e = e0 + u * kGT;
+        if (e >= n || h == ~0ull || dup || full) continue;  // ~0: sector padding
+        if (rounds > 1) {
+          const uint32_t mid = (uint32_t)h & 0xffffu;
+          if ((uint32_t)(((uint64_t)mid * rounds) >> 16) != r) continue;
+        }
+        const uint32_t tag = (uint32_t)(h >> 32) & tmask;
+        const uint32_t v = (tag << ib) | e;  // never ~0u: e < imask
+        uint32_t slot = (uint32_t)(((uint64_t)(uint32_t)h * kSpDupGSlots) >> 32);
+        for (uint32_t probe = 0;; ++probe) {
+          if (probe == kSpDupGSlots / 2) {  // a skewed round
+            full = true;
+            atomicMax(&st->why, 9u);
+            break;
+          }
+          const uint32_t prev = atomicCAS(&tab[slot], ~0u, v);
+          if (prev == ~0u) break;
+          if ((prev >> ib) == tag && arr[prev & imask] == h) {
+            dup = true;
+            break;
+          }
+          slot = slot + 1 == kSpDupGSlots ? 0u : slot + 1;
+        }
+      }
+    }
+  }
+}
+
+// Partitions of more than kSpDupMaxRounds rounds (inputs above ~100M points;
+// 1B square: 322K hashes per partition, whose 40 rounds would each re-read the
+// whole partition) are first split by hash bits 0-8 into up to 512
+// sub-partitions of ~kSpDupSubTarget entries in a global scratch area of
+// `gcap` entries per (CTA, group) (L2-resident), then each sub-partition goes
+// through the shared-memory pass in about one round.
+constexpr uint32_t kSpDupMaxRounds = 2;
+constexpr uint32_t kSpDupSubTarget = 6144;
+constexpr uint32_t kSpDupMaxSub = 512;
+
 __global__ void __launch_bounds__(1024) k_sp_dups(const uint64_t* __restrict__ parted,
                                                  const uint32_t* __restrict__ part_off,
                                                  uint32_t nparts_cta, SpState* __restrict__ st,
-                                                 uint32_t* __restrict__ ticket, uint32_t n_free) {
+                                                 uint32_t* __restrict__ ticket, uint32_t n_free,
+                                                 uint64_t* __restrict__ gscr = nullptr,
+                                                 uint32_t gcap = 0) {
   extern __shared__ uint32_t s_tab[];  // kSpDupGroups x kSpDupGSlots
   __shared__ uint32_t s_next[kSpDupGroups];
+  __shared__ uint32_t s_sub[kSpDupGroups][kSpDupMaxSub + 1];  // counts -> offsets
+  __shared__ uint32_t s_cur[kSpDupGroups][kSpDupMaxSub];
   if (st->fail || sm_id() < n_free) return;
-  constexpr uint32_t kGT = kSpDupGT, kB = 8;  // entries per thread per batch
+  constexpr uint32_t kGT = kSpDupGT;
   const uint32_t grp = threadIdx.x / kGT, gt = threadIdx.x % kGT, bar = 1 + grp;
   uint32_t* tab = s_tab + grp * kSpDupGSlots;
+  uint32_t* sub = s_sub[grp];
+  uint32_t* cur = s_cur[grp];
+  uint64_t* scr = gscr ? gscr + (size_t)(blockIdx.x * kSpDupGroups + grp) * gcap : nullptr;
   const uint32_t total = part_off[(size_t)kSpParts * nparts_cta];  // the scan's total
   bool dup = false, full = false;
   if (gt == 0) s_next[grp] = atomicAdd(ticket, 1u);
@@ -1681,61 +1771,43 @@ __global__ void __launch_bounds__(1024) k_sp_dups(const uint64_t* __restrict__ p
     // the next item's ticket is taken now and read after the closing barrier
     if (gt == 0) s_next[grp] = atomicAdd(ticket, 1u);
     const uint32_t n = hi - lo;
-#ifdef GSCAN_DUPS_FORCE_BIG  // test builds: the large-partition encoding everywhere
-    const uint32_t ib = kSpDupIdxBitsBig;
-#else
-    const uint32_t ib = n < (1u << kSpDupIdxBits) ? kSpDupIdxBits : kSpDupIdxBitsBig;  // uniform
-#endif
-    const uint32_t imask = (1u << ib) - 1, tmask = (1u << (32 - ib)) - 1;
-    if (n >= imask) {
-      full = true;
-    } else {
-      const uint32_t rounds = (n + kSpDupGRound - 1) / kSpDupGRound;
-      for (uint32_t r = 0; r < rounds; ++r) {  // uniform over the group (named barriers)
-        // the first batch's loads are in flight while the table is cleared
-        uint64_t hv[kB];
-#pragma unroll
-        for (uint32_t u = 0; u < kB; ++u) {
-          const uint32_t e = lo + gt + u * kGT;
-          hv[u] = e < hi ? parted[e] : ~0ull;
-        }
-        if (r) named_sync(bar, kGT);  // the previous round's probes are done
-        uint4* t4 = reinterpret_cast<uint4*>(tab);
-        for (uint32_t k = gt; k < kSpDupGSlots / 4; k += kGT) t4[k] = make_uint4(~0u, ~0u, ~0u, ~0u);
-        named_sync(bar, kGT);
-        for (uint32_t e0 = lo + gt; e0 < hi; e0 += kB * kGT) {
-          if (e0 != lo + gt) {
-#pragma unroll
-            for (uint32_t u = 0; u < kB; ++u) {
-              const uint32_t e = e0 + u * kGT;
-              hv[u] = e < hi ? parted[e] : ~0ull;
-            }
-          }
-#pragma unroll
-          for (uint32_t u = 0; u < kB; ++u) {
-            const uint64_t h = hv[u];
-            const uint32_t e = e0 + u * kGT;
-            if (e >= hi || h == ~0ull || dup || full) continue;  // ~0: sector padding
-            if (rounds > 1) {
-              const uint32_t mid = (uint32_t)(h >> 20) & 0xffffu;  // bits below the partition
-              if ((uint32_t)(((uint64_t)mid * rounds) >> 16) != r) continue;
-            }
-            const uint32_t tag = (uint32_t)(h >> 32) & tmask;
-            const uint32_t v = (tag << ib) | (e - lo);  // never ~0u: e - lo < imask
-            uint32_t slot = (uint32_t)(((uint64_t)(uint32_t)h * kSpDupGSlots) >> 32);
-            for (uint32_t probe = 0;; ++probe) {
-              if (probe == kSpDupGSlots / 2) { full = true; break; }  // a skewed round
-              const uint32_t prev = atomicCAS(&tab[slot], ~0u, v);
-              if (prev == ~0u) break;
-              if ((prev >> ib) == tag && parted[lo + (prev & imask)] == h) {
-                dup = true;
-                break;
-              }
-              slot = slot + 1 == kSpDupGSlots ? 0u : slot + 1;
-            }
-          }
-        }
+    const uint32_t nrounds = (n + kSpDupGRound - 1) / kSpDupGRound;
+    if (scr && nrounds > kSpDupMaxRounds && n <= gcap) {
+      uint32_t ns = 1;
+      while (ns < kSpDupMaxSub && ns * kSpDupSubTarget < n) ns <<= 1;
+      for (uint32_t k = gt; k <= ns; k += kGT) sub[k] = 0;
+      named_sync(bar, kGT);
+      for (uint32_t e = lo + gt; e < hi; e += kGT) {
+        const uint64_t h = parted[e];
+        if (h != ~0ull) atomicAdd(&sub[(uint32_t)h & (ns - 1)], 1u);
       }
+      named_sync(bar, kGT);
+      if (gt < 32) {  // exclusive scan of the ns counts by one warp
+        uint32_t carry = 0;
+        for (uint32_t base = 0; base < ns; base += 32) {
+          const uint32_t v = base + gt < ns ? sub[base + gt] : 0u;
+          uint32_t x = v;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if ((int)gt >= o) x += y;
+          }
+          if (base + gt < ns) { sub[base + gt] = carry + x - v; cur[base + gt] = carry + x - v; }
+          carry += __shfl_sync(0xffffffffu, x, 31);
+        }
+        if (gt == 0) sub[ns] = carry;
+      }
+      named_sync(bar, kGT);
+      for (uint32_t e = lo + gt; e < hi; e += kGT) {
+        const uint64_t h = parted[e];
+        if (h != ~0ull) scr[atomicAdd(&cur[(uint32_t)h & (ns - 1)], 1u)] = h;
+      }
+      __threadfence_block();
+      named_sync(bar, kGT);
+      for (uint32_t j = 0; j < ns && !dup && !full; ++j)
+        dup_set_pass(scr + sub[j], sub[j + 1] - sub[j], tab, gt, bar, dup, full, st);
+    } else {
+      dup_set_pass(parted + lo, n, tab, gt, bar, dup, full, st);
     }
     if (named_sync_or(bar, kGT, dup || full)) break;  // also publishes s_next
     p = s_next[grp];
@@ -1755,10 +1827,21 @@ __global__ void __launch_bounds__(256) k_sp_emit_place(
     const uint32_t* __restrict__ e_count, uint32_t cap, uint32_t* __restrict__ cnt,
     const uint32_t* __restrict__ start, const ExtResult* __restrict__ ext,
     SpState* __restrict__ st, PtRec* __restrict__ rec,
-    const double* __restrict__ e_x = nullptr, const double* __restrict__ e_y = nullptr) {
+    const double* __restrict__ e_x = nullptr, const double* __restrict__ e_y = nullptr,
+    uint32_t wcap = 0xffffffffu) {
   // e_x, e_y: the emitted points' coordinates in the region slots (F3 writes
   // them for gathered points, so no random reads of xs, ys); else xs[i], ys[i]
   if (st->fail) return;
+  // the walk-side buffers hold wcap elements (large inputs, gscan.cu reserve):
+  // gathered points, then gathered + candidate points, must fit
+  if ((kPhase == 0 && (uint64_t)st->n_g + 2 > wcap) ||
+      (kPhase == 1 && (uint64_t)st->n_g + st->n_c + 2 > wcap)) {
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
+      atomicOr(&st->fail, kSpFailCap);
+      atomicMax(&st->why, 7u);
+    }
+    return;
+  }
   if (kPhase == 1 && st->n_c > max(st->m / kSpManyDiv, 65536u)) {
     // after F4: too many candidates (points near a circle); the full sort is
     // faster -- decline, every CTA sees the same count
@@ -1858,18 +1941,24 @@ __device__ bool cta_sort_bucket(const PtRec* __restrict__ R, uint32_t cnt, doubl
 // out(rank, x, y, idx) receives every element; returns true when two elements
 // are equal points (annotate's dedup would drop one). Sub-buckets above
 // kSubMax members (clustered keys) flag `slow`: the caller re-sorts bitonically.
-template <uint32_t kCap, typename Out>
+// `smem` may also be a global-memory scratch area (k_sp_sort_gathered_huge):
+// the arrays are then laid out for `cap` elements instead of kCap.
+// In global memory the counts and the member list are built with atomics,
+// which are performed in L2: their reads bypass L1 (kGlobal, __ldcg).
+template <uint32_t kCap, bool kGlobal = false, typename Out>
 __device__ bool cta_sort_bucket_sub(const PtRec* __restrict__ R, uint32_t cnt, double ax, double ay,
-                                    unsigned char* smem, bool* slow, Out&& out) {
+                                    unsigned char* smem, bool* slow, Out&& out,
+                                    uint32_t cap = kCap) {
+  auto ld = [](const uint32_t* p) -> uint32_t { return kGlobal ? __ldcg(p) : *p; };
   constexpr uint32_t kSubMax = kCap;  // never slow: clustered keys cost O(k^2) in their group
   uint64_t* s_key = reinterpret_cast<uint64_t*>(smem);
-  double* s_d2 = reinterpret_cast<double*>(s_key + kCap);
-  double* s_x = s_d2 + kCap;
-  double* s_y = s_x + kCap;
-  uint32_t* s_idx = reinterpret_cast<uint32_t*>(s_y + kCap);
-  uint32_t* s_sub = s_idx + kCap;     // element -> sub-bucket
-  uint32_t* s_start = s_sub + kCap;   // sub-bucket counts -> starts (kCap + 1)
-  uint32_t* s_list = s_start + kCap + 1;  // members grouped by sub-bucket
+  double* s_d2 = reinterpret_cast<double*>(s_key + cap);
+  double* s_x = s_d2 + cap;
+  double* s_y = s_x + cap;
+  uint32_t* s_idx = reinterpret_cast<uint32_t*>(s_y + cap);
+  uint32_t* s_sub = s_idx + cap;     // element -> sub-bucket
+  uint32_t* s_start = s_sub + cap;   // sub-bucket counts -> starts (cap + 1)
+  uint32_t* s_list = s_start + cap + 1;  // members grouped by sub-bucket
   __shared__ uint64_t s_kmin, s_kmax;
   __shared__ uint32_t s_w[32], s_big;
   if (threadIdx.x == 0) { s_kmin = ~0ull; s_kmax = 0; s_big = 0; }
@@ -1913,7 +2002,7 @@ __device__ bool cta_sort_bucket_sub(const PtRec* __restrict__ R, uint32_t cnt, d
     uint32_t carry = 0;
     for (uint32_t base = 0; base < cnt; base += blockDim.x) {
       const uint32_t i = base + threadIdx.x;
-      const uint32_t v = i < cnt ? s_start[i] : 0u;
+      const uint32_t v = i < cnt ? ld(&s_start[i]) : 0u;
       if (v > kSubMax) s_big = 1;
       uint32_t x = v;
 #pragma unroll
@@ -1946,7 +2035,7 @@ __device__ bool cta_sort_bucket_sub(const PtRec* __restrict__ R, uint32_t cnt, d
   for (uint32_t t = threadIdx.x; t < cnt; t += blockDim.x) {
     const uint32_t j = s_sub[t];
     // claim a slot: the group's first free position (groups are tiny)
-    const uint32_t g0 = s_start[j], g1 = s_start[j + 1];
+    const uint32_t g0 = ld(&s_start[j]), g1 = ld(&s_start[j + 1]);
     for (uint32_t q = g0; q < g1; ++q)
       if (atomicCAS(&s_list[q], 0xffffffffu, t) == 0xffffffffu) break;
   }
@@ -1954,13 +2043,13 @@ __device__ bool cta_sort_bucket_sub(const PtRec* __restrict__ R, uint32_t cnt, d
   bool dup = false;
   for (uint32_t t = threadIdx.x; t < cnt; t += blockDim.x) {
     const uint32_t j = s_sub[t];
-    const uint32_t g0 = s_start[j], g1 = s_start[j + 1];
+    const uint32_t g0 = ld(&s_start[j]), g1 = ld(&s_start[j + 1]);
     const uint64_t kt = s_key[t];
     const double dt = s_d2[t];
     const uint32_t it = s_idx[t];
     uint32_t r = g0;
     for (uint32_t q = g0; q < g1; ++q) {
-      const uint32_t u = s_list[q];
+      const uint32_t u = ld(&s_list[q]);
       if (u == t) continue;
       r += key_less(s_key[u], s_d2[u], s_idx[u], kt, dt, it);
       dup |= (s_key[u] == kt && s_d2[u] == dt && s_x[u] == s_x[t] && s_y[u] == s_y[t]);
@@ -2036,7 +2125,8 @@ __global__ void __launch_bounds__(kSpSortThreads) k_sp_sort_gathered_big(
     const uint32_t* __restrict__ gs, const uint32_t* __restrict__ hist,
     const PtRec* __restrict__ rec,
     const ExtResult* __restrict__ ext, SpState* __restrict__ st, double* __restrict__ A_x,
-    double* __restrict__ A_y, uint32_t* __restrict__ A_i) {
+    double* __restrict__ A_y, uint32_t* __restrict__ A_i, uint32_t* __restrict__ huge,
+    uint32_t huge_cap) {
   extern __shared__ __align__(16) unsigned char smem[];
   if (st->fail) return;
   const uint32_t nbig = st->n_bigg, l_idx = st->l_idx;
@@ -2046,9 +2136,13 @@ __global__ void __launch_bounds__(kSpSortThreads) k_sp_sort_gathered_big(
   for (uint32_t g = blockIdx.x; g < nbig; g += gridDim.x) {
     const uint32_t b = big[g];
     const uint32_t s0 = bstart[b], g0 = gs[b], cnt = hist[b];
-    if (cnt > kSpGatherCap) {
-      if (threadIdx.x == 0) { atomicOr(&st->fail, kSpFailCap); atomicMax(&st->why, 4u); }
-      return;
+    if (cnt > kSpGatherCap) {  // above the shared-memory sorter: global scratch (below)
+      if (cnt > huge_cap) {  // no scratch (small input) or too large for it: decline
+        if (threadIdx.x == 0) { atomicOr(&st->fail, kSpFailCap); atomicMax(&st->why, 4u); }
+        return;
+      }
+      if (threadIdx.x == 0) huge[atomicAdd(&st->n_hugeg, 1u)] = b;
+      continue;
     }
     __syncthreads();
     for (uint32_t t = threadIdx.x; t < cnt; t += blockDim.x) s_list[t] = 0xffffffffu;
@@ -2061,6 +2155,52 @@ __global__ void __launch_bounds__(kSpSortThreads) k_sp_sort_gathered_big(
       A_i[q] = idx;
       if (idx == l_idx) st->l_check = 1 + s0 + r;
     });
+    if (dup) atomicOr(&st->fail, kSpFailDup);
+  }
+}
+
+// Gathered buckets above kSpGatherCap (inputs above ~80M points, where the
+// fixed kSpBuckets buckets hold ~n/48K points each): the same O(n)
+// sub-bucket sort, its arrays in a per-CTA global-memory scratch area of
+// `cap` elements (kSpHugeBytes per element, L2-resident at these sizes). A
+// bucket above `cap`, or a sub-bucket above kSpGatherCap members (clustered
+// keys), declines (kSpFailCap).
+constexpr size_t kSpHugeBytes = 8 + 8 + 8 + 8 + 4 + 4 + 4 + 4;
+
+__global__ void __launch_bounds__(kSpSortThreads) k_sp_sort_gathered_huge(
+    const uint32_t* __restrict__ huge, const uint32_t* __restrict__ bstart,
+    const uint32_t* __restrict__ gs, const uint32_t* __restrict__ hist,
+    const PtRec* __restrict__ rec, const ExtResult* __restrict__ ext, SpState* __restrict__ st,
+    double* __restrict__ A_x, double* __restrict__ A_y, uint32_t* __restrict__ A_i,
+    unsigned char* __restrict__ scratch, uint32_t cap) {
+  if (st->fail) return;
+  const uint32_t nh = st->n_hugeg, l_idx = st->l_idx;
+  const double ax = ext->ax, ay = ext->ay;
+  unsigned char* scr = scratch + (size_t)blockIdx.x * ((size_t)cap * kSpHugeBytes + 16);
+  uint32_t* s_list = reinterpret_cast<uint32_t*>(scr + (size_t)cap * (8 + 8 + 8 + 8 + 4 + 4)) + cap + 1;
+  for (uint32_t g = blockIdx.x; g < nh; g += gridDim.x) {
+    const uint32_t b = huge[g];
+    const uint32_t s0 = bstart[b], g0 = gs[b], cnt = hist[b];
+    if (cnt > cap) {
+      if (threadIdx.x == 0) { atomicOr(&st->fail, kSpFailCap); atomicMax(&st->why, 4u); }
+      return;
+    }
+    __syncthreads();
+    for (uint32_t t = threadIdx.x; t < cnt; t += blockDim.x) s_list[t] = 0xffffffffu;
+    __threadfence_block();
+    bool slow = false;
+    const bool dup = cta_sort_bucket_sub<kSpGatherCap, true>(rec + g0, cnt, ax, ay, scr, &slow,
+                                                       [&](uint32_t r, double x, double y, uint32_t idx) {
+      const uint32_t q = 1 + g0 + r;
+      A_x[q] = x;
+      A_y[q] = y;
+      A_i[q] = idx;
+      if (idx == l_idx) st->l_check = 1 + s0 + r;
+    }, cap);
+    if (slow) {
+      if (threadIdx.x == 0) { atomicOr(&st->fail, kSpFailCap); atomicMax(&st->why, 6u); }
+      return;
+    }
     if (dup) atomicOr(&st->fail, kSpFailDup);
   }
 }
@@ -2386,33 +2526,49 @@ __global__ void __launch_bounds__(kSpSortThreads) k_sp_sort_cand_big(
     const uint32_t* __restrict__ slice_of, const ExtResult* __restrict__ ext,
     SpState* __restrict__ st, double* __restrict__ W_x, double* __restrict__ W_y,
     uint32_t* __restrict__ W_i, uint32_t* __restrict__ W_b, uint32_t* __restrict__ W_s,
-    uint8_t* __restrict__ flags) {
+    uint8_t* __restrict__ flags, unsigned char* __restrict__ scratch, uint32_t scap) {
   extern __shared__ __align__(16) unsigned char smem[];
   if (st->fail) return;
   const uint32_t nbig = st->n_bigc;
   const double ax = ext->ax, ay = ext->ay;
   uint32_t* s_list = reinterpret_cast<uint32_t*>(smem + (size_t)kSpGatherCap * (8 + 8 + 8 + 8 + 4 + 4)) +
                      kSpGatherCap + 1;
+  // buckets above kSpGatherCap (large inputs): the global scratch area of
+  // this CTA (k_sp_sort_gathered_huge's, which has finished by now)
+  unsigned char* scr = scratch ? scratch + (size_t)blockIdx.x * ((size_t)scap * kSpHugeBytes + 16) : nullptr;
+  uint32_t* g_list = scr ? reinterpret_cast<uint32_t*>(scr + (size_t)scap * (8 + 8 + 8 + 8 + 4 + 4)) + scap + 1
+                         : nullptr;
   for (uint32_t g = blockIdx.x; g < nbig; g += gridDim.x) {
     const uint32_t b = big[g];
     const uint32_t c0 = cstart[b], cnt = cstart[b + 1] - c0;
-    if (cnt > kSpGatherCap) {
+    const bool huge = cnt > kSpGatherCap;
+    if (huge && cnt > scap) {
       if (threadIdx.x == 0) { atomicOr(&st->fail, kSpFailCap); atomicMax(&st->why, 5u); }
       return;
     }
     const uint32_t w0 = 1 + wstart[b], sl = slice_of[b];
-    __syncthreads();
-    for (uint32_t t = threadIdx.x; t < cnt; t += blockDim.x) s_list[t] = 0xffffffffu;
-    bool slow = false;
-    const bool dup = cta_sort_bucket_sub<kSpGatherCap>(crec + c0, cnt, ax, ay, smem, &slow,
-                                                       [&](uint32_t r, double x, double y, uint32_t idx) {
+    auto out = [&](uint32_t r, double x, double y, uint32_t idx) {
       W_x[w0 + r] = x;
       W_y[w0 + r] = y;
       W_i[w0 + r] = idx;
       W_b[w0 + r] = b;
       W_s[w0 + r] = sl;
       flags[w0 + r] = 1;
-    });
+    };
+    __syncthreads();
+    bool slow = false, dup;
+    if (!huge) {
+      for (uint32_t t = threadIdx.x; t < cnt; t += blockDim.x) s_list[t] = 0xffffffffu;
+      dup = cta_sort_bucket_sub<kSpGatherCap>(crec + c0, cnt, ax, ay, smem, &slow, out);
+    } else {
+      for (uint32_t t = threadIdx.x; t < cnt; t += blockDim.x) g_list[t] = 0xffffffffu;
+      __threadfence_block();
+      dup = cta_sort_bucket_sub<kSpGatherCap, true>(crec + c0, cnt, ax, ay, scr, &slow, out, scap);
+      if (slow) {
+        if (threadIdx.x == 0) { atomicOr(&st->fail, kSpFailCap); atomicMax(&st->why, 6u); }
+        return;
+      }
+    }
     if (dup) atomicOr(&st->fail, kSpFailDup);
   }
 }
