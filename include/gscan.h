@@ -47,7 +47,10 @@ enum {
     GSCAN_E_INVALID = 5,     /* NULL pointer / bad argument */
     GSCAN_E_TOO_LARGE = 6,   /* n >= 2^32 (indices are 32-bit on the device) */
     GSCAN_E_NO_DEVICE = 7,   /* no CUDA device / extension built without GPU */
-    GSCAN_E_INTERNAL = 8     /* device-side consistency check failed */
+    GSCAN_E_INTERNAL = 8,    /* device-side consistency check failed */
+    GSCAN_E_IO = 9,          /* hull2d::IoError (datagen.hpp: cannot open / read) */
+    GSCAN_E_PARSE = 10,      /* hull2d::ParseError (datagen.hpp; line in gscan_io_error) */
+    GSCAN_E_NCCL = 11        /* a collective of the sharded path failed (distributed.py) */
 };
 
 /* hull2d::PipelineConfig (pipeline.hpp:41-46). */
@@ -271,6 +274,22 @@ int gscan_generate(int kind, uint64_t n, uint64_t seed, double* xs, double* ys);
  * A rank of a sharded run generates only its own shard. */
 int gscan_generate_square_device(gscan_handle* h, uint64_t seed, uint64_t lo, uint64_t hi,
                                  double* d_xs, double* d_ys);
+/* Ingest. Plain-XY text and the OBJ vertex subset
+ * restate hull2d::datagen::load_points / load_obj_projected
+ * (datagen.hpp:111-168: std::from_chars, '#'/blank lines skipped, "v x y [z]"
+ * vertex lines); GSCANSOA is the device path's binary layout ("GSCANSOA",
+ * uint64 n, n doubles x, n doubles y, little-endian). gscan_load returns
+ * malloc'd arrays (free with gscan_free); gscan_soa_count + gscan_soa_read
+ * fill caller buffers (e.g. pinned memory for gscan_hull_f64). Errors:
+ * GSCAN_E_IO, GSCAN_E_PARSE, GSCAN_E_EMPTY_INPUT; the message (with the line
+ * number) from gscan_io_error (per thread). */
+enum { GSCAN_FMT_XY = 0, GSCAN_FMT_OBJ = 1, GSCAN_FMT_SOA = 2 };
+int gscan_load(const char* path, int format, double** xs, double** ys, uint64_t* n);
+int gscan_soa_count(const char* path, uint64_t* n);
+int gscan_soa_read(const char* path, double* xs, double* ys, uint64_t n);
+int gscan_save_soa(const char* path, const double* xs, const double* ys, uint64_t n);
+void gscan_free(void* p);
+const char* gscan_io_error(void);
 /* Host self-check of the generator's mt19937_64 jump-ahead: jumps `blocks`
  * x 2^20 words and compares the next 312 outputs with a sequentially
  * advanced std::mt19937_64. Returns the number of mismatches (0 = exact). */

@@ -98,6 +98,9 @@ def ref() -> C.CDLL:
         lib.ref_sorted_buffer.argtypes = [_DP, _DP, C.c_uint64, _U64P, _DP, _DP, _U64P]
         lib.ref_discard_flags.argtypes = [_DP, _DP, C.c_uint64, C.c_uint64, C.c_int, _U8P, _U64P]
         lib.ref_generate.argtypes = [C.c_int, C.c_uint64, C.c_uint64, _DP, _DP]
+        lib.ref_load.restype = C.c_int
+        lib.ref_load.argtypes = [C.c_char_p, C.c_int, _DP, _DP, C.c_uint64, _U64P, C.c_char_p,
+                                 C.c_uint64]
         _ref = lib
     return _ref
 
@@ -209,6 +212,18 @@ def ref_generate(kind: int, n: int, seed: int):
     if rc:
         raise RuntimeError("ref_generate failed")
     return xs, ys
+
+
+def ref_load(path, obj=False, cap=1 << 20):
+    """The reference's load_points / load_obj_projected: (code, xs, ys, message);
+    code 0 ok, 1 ParseError, 2 IoError, 3 EmptyInput."""
+    xs = np.empty(cap)
+    ys = np.empty(cap)
+    n = C.c_uint64()
+    msg = C.create_string_buffer(512)
+    rc = ref().ref_load(str(path).encode(), int(obj), _d(xs), _d(ys), cap, C.byref(n), msg, 512)
+    k = min(n.value, cap)
+    return rc, xs[:k].copy(), ys[:k].copy(), msg.value.decode()
 
 
 def find_extremes(xs, ys) -> list[int]:

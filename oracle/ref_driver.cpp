@@ -193,4 +193,23 @@ int ref_generate(int kind, uint64_t n, uint64_t seed, double* xs, double* ys) {
     return 0;
 }
 
+// The reference's loaders (datagen.hpp:111-168) for the ingest parity tests:
+// 0 ok, 1 ParseError, 2 IoError, 3 EmptyInput; msg receives what().
+int ref_load(const char* path, int obj, double* xs, double* ys, uint64_t cap, uint64_t* n,
+             char* msg, uint64_t msg_cap) {
+    auto put = [&](const char* m) {
+        if (msg && msg_cap) { strncpy(msg, m, msg_cap - 1); msg[msg_cap - 1] = 0; }
+    };
+    try {
+        const std::vector<Point2> p = obj ? hull2d::datagen::load_obj_projected(std::string(path))
+                                          : hull2d::datagen::load_points(std::string(path));
+        *n = p.size();
+        for (uint64_t i = 0; i < p.size() && i < cap; ++i) { xs[i] = p[i].x; ys[i] = p[i].y; }
+        put("");
+        return 0;
+    } catch (const hull2d::ParseError& e) { put(e.what()); return 1; }
+    catch (const hull2d::IoError& e) { put(e.what()); return 2; }
+    catch (const hull2d::EmptyInput& e) { put(e.what()); return 3; }
+}
+
 }  // extern "C"

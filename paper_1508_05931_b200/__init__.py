@@ -2,13 +2,16 @@
 reference's hull2d::full_pipeline path. See DESIGN.md and include/gscan.h."""
 from .hull2d import (  # noqa: F401
     CoincidentWithAnchor,
+    CollectiveError,
     DeviceError,
     EmptyInput,
     Engine,
     Error,
     Hull,
     IndexOutOfRange,
+    IoError,
     LengthMismatch,
+    ParseError,
     PipelineConfig,
     PipelineResult,
     StageStats,
@@ -20,5 +23,7 @@ from .hull2d import (  # noqa: F401
     generate,
     generate_grid,
     hull,
+    load_points,
+    save_soa,
 )
 from ._native import LIB_PATH, NativeUnavailable  # noqa: F401

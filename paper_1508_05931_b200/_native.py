@@ -23,6 +23,10 @@ GSCAN_E_INVALID = 5
 GSCAN_E_TOO_LARGE = 6
 GSCAN_E_NO_DEVICE = 7
 GSCAN_E_INTERNAL = 8
+GSCAN_E_IO = 9
+GSCAN_E_PARSE = 10
+GSCAN_E_NCCL = 11
+FMT_XY, FMT_OBJ, FMT_SOA = 0, 1, 2
 
 GEN_SQUARE, GEN_DISK, GEN_CIRCLE, GEN_COLLINEAR = 0, 1, 2, 3
 
@@ -118,6 +122,12 @@ SIGNATURES = {
     "gscan_generate_grid": (C.c_int, [_U64, _U64, C.c_int, C.c_int, _DP, _DP]),
     "gscan_generate_square_device": (C.c_int, [_P, _U64, _U64, _U64, _P, _P]),
     "gscan_mt64_jump_check": (C.c_int, [_U64, _U64]),
+    "gscan_load": (C.c_int, [C.c_char_p, C.c_int, C.POINTER(_DP), C.POINTER(_DP), _U64P]),
+    "gscan_soa_count": (C.c_int, [C.c_char_p, _U64P]),
+    "gscan_soa_read": (C.c_int, [C.c_char_p, _DP, _DP, _U64]),
+    "gscan_save_soa": (C.c_int, [C.c_char_p, _DP, _DP, _U64]),
+    "gscan_free": (None, [C.c_void_p]),
+    "gscan_io_error": (C.c_char_p, []),
 }
 
 _lib = None

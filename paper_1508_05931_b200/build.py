@@ -30,7 +30,7 @@ NVCC_FLAGS = ["-O3", "-std=c++17", "--fmad=false", "-lineinfo", "-Xcompiler", "-
 CXX_FLAGS = ["-std=c++20", "-O2", "-fPIC", "-ffp-contract=off"]
 
 CU_SOURCES = ["gscan.cu"]
-CXX_SOURCES = ["datagen.cpp", "mt64_jump.cpp"]
+CXX_SOURCES = ["datagen.cpp", "mt64_jump.cpp", "io.cpp"]
 
 
 def _run(cmd: list[str]) -> None:

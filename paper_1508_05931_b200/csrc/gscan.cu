@@ -1461,6 +1461,10 @@ int sparse_dup_check(gscan_handle* h, uint32_t n) {
                                                               h->sp_side_work + 1, side_free_sms_dups(),
                                                               h->sp_dup_scr, h->sp_dup_scap);
   }
+  {
+    Launch L(h, "k_sp_side_check", h->side);
+    k_sp_side_check<<<1, 32, 0, h->side>>>(h->sp_side_work, nl, h->sp_st);
+  }
   CU(cudaEventRecord(h->ev_dup, h->side));
   return GSCAN_OK;
 }
@@ -1685,7 +1689,23 @@ SpCtx dist_ctx(gscan_handle* h) {
   SpCtx c = sp_ctx(h, h->dist_xs, h->dist_ys, h->dist_n, h->dist_chunks);
   c.base = h->dist_base;
   c.sharded = true;
+  // after the plan the slice structure is the GLOBAL one (M = all ranks'
+  // points): size the slice grids by it, not by this rank's shard
+  if (h->h_sp && h->h_sp->M) c.nslices = 2 * std::min<uint64_t>(h->dist_chunks, h->h_sp->M);
   return c;
+}
+
+// slice segment arrays for the global slice count (rank 0's walk)
+int dist_slices_ensure(gscan_handle* h, const SpCtx& c) {
+  if (c.nslices + 2 <= h->sp_seg_cap) return GSCAN_OK;
+  dfree(h->sp_seglo);
+  dfree(h->sp_seghi);
+  h->sp_seg_cap = 0;
+  CU(cudaMalloc(&h->sp_seglo, (c.nslices + 2) * 4));
+  CU(cudaMalloc(&h->sp_seghi, (c.nslices + 2) * 4));
+  h->sp_seg_cap = c.nslices + 2;
+  h->sp_graph_ok = false;
+  return GSCAN_OK;
 }
 
 int dist_read_state(gscan_handle* h) {
@@ -1733,6 +1753,9 @@ const char* gscan_status_string(int s) {
     case GSCAN_E_TOO_LARGE: return "input too large";
     case GSCAN_E_NO_DEVICE: return "no CUDA device";
     case GSCAN_E_INTERNAL: return "internal consistency check failed";
+    case GSCAN_E_IO: return "I/O error";
+    case GSCAN_E_PARSE: return "parse error";
+    case GSCAN_E_NCCL: return "collective (NCCL) failure";
     default: return "unknown status";
   }
 }
@@ -2133,6 +2156,7 @@ int gscan_dist_begin(gscan_handle* h, const double* d_xs, const double* d_ys, ui
   TRY(reserve(h, n));
   TRY(sparse_init(h));
   TRY(dist_init(h));
+  h->h_sp->M = 0;  // a previous call's global count must not size this call's slices
   const uint64_t nslices = 2 * std::min<uint64_t>(cfg->chunk_count, n);
   if (nslices + 2 > h->sp_seg_cap) {
     dfree(h->sp_seglo);
@@ -2233,7 +2257,10 @@ int gscan_dist_slices(gscan_handle* h, const double* d_X, const double* d_Y, uin
                       const uint32_t* phi_range, uint32_t* d_prefmax, uint32_t* fail_out) {
   if (!h || !d_X || !d_Y || !d_phimax || !phi_range || !d_prefmax || !fail_out) return GSCAN_E_INVALID;
   SpCtx c = dist_ctx(h);
-  if (1 + n_g > h->cap) return fail(h, GSCAN_E_CAPACITY, "sharded path: %llu gathered points exceed rank 0's buffers", (unsigned long long)n_g);
+  if (1 + n_g + 2 > std::min<uint64_t>(h->cap, h->wcap))
+    return fail(h, GSCAN_E_CAPACITY, "sharded path: %llu gathered points exceed rank 0's buffers",
+                (unsigned long long)n_g);
+  TRY(dist_slices_ensure(h, c));
   CU(cudaMemcpyAsync(h->sp_phimax, d_phimax, kSpBuckets * 4, cudaMemcpyDeviceToDevice, c.s));
   k_sp_set_phi<<<1, 1, 0, c.s>>>(h->sp_st, phi_range[0], phi_range[1], (uint32_t)l_pos, h->ext, 0u);
   k_sp_gsize<<<(kSpBuckets + 255) / 256, 256, 0, c.s>>>(h->sp_gbits, h->sp_hist, h->sp_gsz);
@@ -2265,7 +2292,10 @@ int gscan_dist_finish(gscan_handle* h, const double* d_X, const double* d_Y, uin
   SpCtx c = dist_ctx(h);
   c.gs = h->sp_gs;
   const uint64_t nw = 1 + n_g + n_c;
-  if (nw > h->cap) return fail(h, GSCAN_E_CAPACITY, "sharded path: %llu walk records exceed rank 0's buffers", (unsigned long long)nw);
+  if (nw + 2 > std::min<uint64_t>(h->cap, h->wcap))
+    return fail(h, GSCAN_E_CAPACITY, "sharded path: %llu walk records exceed rank 0's buffers",
+                (unsigned long long)nw);
+  TRY(dist_slices_ensure(h, c));
   TRY(dist_fill(h, c, (uint32_t)n_c, (uint32_t)(1 + n_g), d_cb, h->sp_ccount));
   TRY(tree_workspace(h, (uint32_t)std::min<uint64_t>(nw, kTreeMaxN)));
   TRY(sp_seg_walk(h, c, d_X, d_Y, (uint32_t)nw));
@@ -2318,8 +2348,13 @@ int gscan_dist_dup_check(gscan_handle* h, const uint64_t* d_recv, uint64_t n_rec
                          const uint32_t* d_counts, uint32_t R, uint32_t* dup_found) {
   if (!h || !d_counts || !dup_found || R == 0 || R > kDistMaxRanks) return GSCAN_E_INVALID;
   const SpCtx c = dist_ctx(h);
-  if (n_recv > (uint64_t)h->sp_grid * sparse_region_cap(h, h->dist_n))
-    return fail(h, GSCAN_E_CAPACITY, "sharded duplicate check: %llu hashes received", (unsigned long long)n_recv);
+  if (n_recv > (uint64_t)h->sp_grid * sparse_region_cap(h, h->dist_n)) {
+    // more hashes than this rank's regions hold (uneven shards): a local
+    // decline, reported like a possible duplicate so every rank still joins
+    // the next collective and all of them take the survivor gather
+    *dup_found = 1;
+    return GSCAN_OK;
+  }
   k_sp_recv_plan<<<(kSpParts * R + 255) / 256, 256, 0, c.s>>>(d_counts, R, h->dist_pm, h->dist_hc,
                                                                h->dist_lb);
   TRY(scan_u32(h, h->dist_pm, kSpParts * R, h->dist_pm));
@@ -2329,7 +2364,8 @@ int gscan_dist_dup_check(gscan_handle* h, const uint64_t* d_recv, uint64_t n_rec
                                                         h->sp_st, h->sp_dup, h->sp_side_work, 0u,
                                                         h->dist_lb);
   k_sp_dups<<<h->sm_count, 1024, kSpSideSmem, c.s>>>(h->sp_dup, h->dist_pm, R, h->sp_st,
-                                                     h->sp_side_work + 1, 0u);
+                                                     h->sp_side_work + 1, 0u, h->sp_dup_scr,
+                                                     h->sp_dup_scap);
   CU(cudaGetLastError());
   TRY(dist_read_state(h));
   *dup_found = (h->h_sp->fail & (kSpFailDup | kSpFailCap)) ? 1u : 0u;

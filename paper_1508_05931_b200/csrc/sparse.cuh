@@ -1816,6 +1816,21 @@ __global__ void __launch_bounds__(1024) k_sp_dups(const uint64_t* __restrict__ p
   if (full) atomicOr(&st->fail, kSpFailCap);
 }
 
+// Side-stream completion check. k_sp_dup_part and k_sp_dups hand out work by
+// tickets and leave at once on the SMs reserved for the main stream
+// (sm_id() < n_free); if the scheduler placed every CTA there (SM subsets
+// under MIG/MPS, n_free >= the SM count), some lists or partitions were never
+// examined. Every item is claimed before the ticket passes the item count, so
+// fewer tickets than items declines the call (a possible duplicate unchecked).
+__global__ void k_sp_side_check(const uint32_t* __restrict__ work, uint32_t n_lists,
+                                SpState* __restrict__ st) {
+  if (st->fail) return;
+  if (work[0] < n_lists || work[1] < kSpParts) {
+    atomicOr(&st->fail, kSpFailCap);
+    atomicMax(&st->why, 10u);
+  }
+}
+
 // Emitted elements (per-CTA regions) -> bucket slots start[b] + rank as
 // 32-byte records {exact key, x, y, idx, bucket}; the glibc-exact atan2 runs
 // here, densely. rank: arrival order (atomic on cnt[b]); with store_rank the

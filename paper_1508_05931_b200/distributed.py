@@ -549,11 +549,14 @@ def survivor_gather(eng: Engine, d_xs: torch.Tensor, d_ys: torch.Tensor, offset:
     pack[0, : sx.numel()] = sx
     pack[1, : sy.numel()] = sy
     pack[2, : sg.numel()] = sg.double()  # exact below 2^53
-    gathered = torch.empty((world, 3, mx), dtype=torch.float64, device=dev)
-    dist.all_gather_into_tensor(gathered, pack, group=group)
+    # survivors go to rank 0 only (the other ranks hold nothing extra)
+    gathered = [torch.empty((3, mx), dtype=torch.float64, device=dev) for _ in range(world)] \
+        if rank == 0 else None
+    dist.gather(pack, gather_list=gathered, dst=0, group=group)
+    del pack
     if rank != 0:
         return None, None
-    parts = [gathered[r, :, : counts[r]] for r in range(world)]
+    parts = [gathered[r][:, : counts[r]] for r in range(world)]
     allp = torch.cat(parts, dim=1)
     gx = allp[0].contiguous()
     gy = allp[1].contiguous()
@@ -580,7 +583,10 @@ def sharded_hull(eng: Engine, d_xs: torch.Tensor, d_ys: torch.Tensor, offset: in
     n = int(d_xs.numel())
     sizes = comm.allgather_obj([n])
     n_global = sum(sizes)
-    if _default_toggles(cfg) and n_global >= 65536 and min(sizes) > 0 and d_xs.is_cuda:
+    # global indices are 32-bit on the device (every rank knows n_global, so
+    # all of them take the same path)
+    if (_default_toggles(cfg) and 65536 <= n_global < 0xFFFFFFFF and min(sizes) > 0
+            and d_xs.is_cuda):
         res = sparse_sharded([eng], [(d_xs, d_ys)], [offset], n_global, cfg, comm)
         if res is not None:
             return res
@@ -588,14 +594,16 @@ def sharded_hull(eng: Engine, d_xs: torch.Tensor, d_ys: torch.Tensor, offset: in
 
 
 def simulate_sharded(engines: list[Engine], xs: torch.Tensor, ys: torch.Tensor,
-                     cfg: PipelineConfig | None = None):
+                     cfg: PipelineConfig | None = None, bounds: list[int] | None = None):
     """All R ranks in this process on one device (LocalComm): the sharded
     sparse path exactly as R GPUs would run it. Returns (indices, stats) or
-    None when it declined."""
+    None when it declined. bounds: shard boundaries [0, ..., n] (default
+    equal shards)."""
     cfg = cfg or PipelineConfig()
     R = len(engines)
     n = int(xs.numel())
-    offs = [n * r // R for r in range(R + 1)]
+    offs = list(bounds) if bounds is not None else [n * r // R for r in range(R + 1)]
+    assert len(offs) == R + 1 and offs[0] == 0 and offs[-1] == n
     shards = [(xs[offs[r]:offs[r + 1]].contiguous(), ys[offs[r]:offs[r + 1]].contiguous())
               for r in range(R)]
     return sparse_sharded(engines, shards, offs[:R], n, cfg, LocalComm(R))

@@ -59,6 +59,18 @@ class DeviceError(Error):
     """CUDA runtime failure inside the native library."""
 
 
+class IoError(Error):
+    """errors.hpp IoError: a file cannot be opened or read (datagen.hpp loaders)."""
+
+
+class ParseError(Error):
+    """errors.hpp ParseError: a malformed line (the message names its number)."""
+
+
+class CollectiveError(Error):
+    """A collective of the sharded path failed (GSCAN_E_NCCL)."""
+
+
 _STATUS_EXC = {
     N.GSCAN_E_EMPTY_INPUT: EmptyInput,
     N.GSCAN_E_ZERO_CHUNKS: ZeroChunks,
@@ -67,6 +79,9 @@ _STATUS_EXC = {
     N.GSCAN_E_INTERNAL: DeviceError,
     N.GSCAN_E_INVALID: ValueError,
     N.GSCAN_E_NO_DEVICE: N.NativeUnavailable,
+    N.GSCAN_E_IO: IoError,
+    N.GSCAN_E_PARSE: ParseError,
+    N.GSCAN_E_NCCL: CollectiveError,
 }
 
 
@@ -336,6 +351,42 @@ def generate(kind: str, n: int, seed: int) -> tuple[np.ndarray, np.ndarray]:
     if rc:
         raise ValueError(f"generate({kind}): {N.status_string(rc)}")
     return xs, ys
+
+
+# ---- ingest (datagen.hpp:111-168 loaders, csrc/io.cpp) ----
+_FMTS = {"xy": N.FMT_XY, "obj": N.FMT_OBJ, "soa": N.FMT_SOA}
+
+
+def load_points(path, fmt: str = "xy") -> tuple[np.ndarray, np.ndarray]:
+    """Points of a plain-XY text file (load_points), the vertex lines of an OBJ
+    file (load_obj_projected) or a GSCANSOA binary file, as SoA float64 arrays.
+    Raises IoError / ParseError / EmptyInput like the reference."""
+    lib = N.load()
+    xp, yp = C.POINTER(C.c_double)(), C.POINTER(C.c_double)()
+    n = C.c_uint64()
+    rc = lib.gscan_load(str(path).encode(), _FMTS[fmt], C.byref(xp), C.byref(yp), C.byref(n))
+    if rc:
+        raise _STATUS_EXC.get(rc, Error)(lib.gscan_io_error().decode())
+    try:
+        m = n.value
+        xs = np.ctypeslib.as_array(xp, shape=(m,)).copy()
+        ys = np.ctypeslib.as_array(yp, shape=(m,)).copy()
+    finally:
+        lib.gscan_free(C.cast(xp, C.c_void_p))
+        lib.gscan_free(C.cast(yp, C.c_void_p))
+    return xs, ys
+
+
+def save_soa(path, xs, ys) -> None:
+    """Write a GSCANSOA binary file (the device path's layout)."""
+    xs = np.ascontiguousarray(xs, dtype=np.float64)
+    ys = np.ascontiguousarray(ys, dtype=np.float64)
+    if xs.shape != ys.shape:
+        raise LengthMismatch("xs and ys differ in length")
+    lib = N.load()
+    rc = lib.gscan_save_soa(str(path).encode(), _dptr(xs), _dptr(ys), xs.shape[0])
+    if rc:
+        raise _STATUS_EXC.get(rc, Error)(lib.gscan_io_error().decode())
 
 
 def generate_grid(n: int, seed: int, lo: int = 0, hi: int = 12) -> tuple[np.ndarray, np.ndarray]:

@@ -122,3 +122,22 @@ def test_sharded_hull_over_nccl(tmp_path):
                        text=True, timeout=300)
     assert p.returncode == 0, p.stderr[-3000:]
     assert "ok" in p.stdout
+
+
+def test_sharded_uneven_shards_tiny_ranks(engines, oracle_mod):
+    """Shards smaller than chunk_count next to a large one (the
+    slice grids must follow the GLOBAL slice count, not rank 0's shard)."""
+    from paper_1508_05931_b200 import PipelineConfig, generate
+    from paper_1508_05931_b200.distributed import simulate_sharded
+
+    xs, ys = generate("square", 400_000, 11)
+    n = len(xs)
+    for bounds in ([0, 100, n - 50, n], [0, 3, 7, n], [0, n - 900, n - 10, n]):
+        dx, dy = torch.from_numpy(xs).cuda(), torch.from_numpy(ys).cuda()
+        res = simulate_sharded(engines[:3], dx, dy, PipelineConfig(), bounds=bounds)
+        if res is None:
+            continue  # a decline is exact (the caller takes the survivor gather)
+        got, st = res
+        want, sw = oracle_mod.full_pipeline(xs, ys)
+        assert np.array_equal(got, want), bounds
+        assert st.n_after_round2 == sw["n_after_round2"], bounds
