@@ -57,6 +57,24 @@ struct PipelineResult {
     StageStats stats;
 };
 
+// The error hierarchy. When the reference's errors.hpp is on the include
+// path (-I<reference>/proj/include) the shim throws the reference's own types
+// (hull2d::EmptyInput, hull2d::ZeroChunks, ... -- errors.hpp:9-49), so
+// `CHECK_THROWS_AS(full_pipeline(...), hull2d::EmptyInput)` ports unchanged;
+// otherwise it defines the same hierarchy in this namespace.
+#if !defined(HULL2D_GPU_OWN_ERRORS) && __has_include(<hull2d/errors.hpp>)
+}  // namespace hull2d_gpu
+#include <hull2d/errors.hpp>
+namespace hull2d_gpu {
+#define HULL2D_GPU_REFERENCE_ERRORS 1
+using hull2d::EmptyInput;
+using hull2d::Error;
+using hull2d::TooLarge;
+using hull2d::ZeroChunks;
+struct DeviceError : hull2d::Error {
+    using hull2d::Error::Error;
+};
+#else
 struct Error : std::runtime_error {
     using std::runtime_error::runtime_error;
 };
@@ -72,6 +90,7 @@ struct TooLarge : Error {
 struct DeviceError : Error {
     using Error::Error;
 };
+#endif
 
 namespace detail {
 [[noreturn]] inline void raise(int rc, const gscan_handle* h) {

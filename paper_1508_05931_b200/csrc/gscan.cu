@@ -31,6 +31,18 @@ using namespace gscan;
 
 namespace {
 
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// ~ns of GPU time (profiling mode only; see run_sparse)
+__global__ void k_busy_wait(unsigned long long ns) {
+  const unsigned long long t0 = globaltimer_ns();
+  while (globaltimer_ns() - t0 < ns) __nanosleep(1000);
+}
+
 constexpr double kPi = 3.14159265358979323846;
 
 struct KernelTime {
@@ -1504,6 +1516,10 @@ int run_sparse(gscan_handle* h, const double* xs, const double* ys, uint32_t n,
   const void* bufs[7] = {h->A_x, h->A_y, h->A_i, h->C_x, h->C_y, h->C_i, h->tw_pool};
   for (int k = 0; k < 7; ++k) key.bufs[k] = bufs[k];
   if (h->profiling || !h->use_graphs) {
+    // profiling: a short busy kernel first keeps the stream occupied while the
+    // host enqueues the per-kernel events and launches, so each event pair
+    // brackets its kernel and not the host's launch latency
+    if (h->profiling) k_busy_wait<<<1, 32, 0, s>>>(200000ull);
     TRY(sparse_enqueue(h, xs, ys, n, cfg));
   } else {
     if (!h->sp_graph_ok || !(key == h->sp_key)) {

@@ -205,17 +205,20 @@ __device__ __forceinline__ void ext_finish(ExtAcc acc, const double* __restrict_
   }
 }
 
-// K1 as a bulk-copy pipeline: each CTA (one per SM) streams tiles of
-// kExtTile points of xs and ys through a kExtStages-deep shared-memory ring
-// filled by cp.async.bulk (TMA) and completed on mbarriers, so the bytes in
-// flight do not depend on registers or occupancy. Tiles go to CTAs
-// round-robin; the remainder (< one tile) is read directly by the last CTA.
-// Within a thread indices only grow (tile order, then pair order), as
+// K1 as a bulk-copy pipeline (XYRing, device_common.cuh): one CTA per SM
+// streams tiles of kExtTile points of xs and ys through a kExtStages-deep
+// shared-memory ring; every warp is a consumer and the last warp to finish
+// reading a stage refills it, so no CTA-wide barrier sits on the per-tile path
+// and kExtStages x 32 KB are in flight per SM regardless of occupancy. Each
+// warp releases its stage as soon as the values are in registers. Tiles go to
+// CTAs round-robin; the remainder (< one tile) is read directly by the last
+// CTA. Within a thread indices only grow (tile order, then pair order), as
 // ext_push requires. Needs 16-byte aligned xs, ys.
-constexpr int kExtTile = 4096;    // points per tile (32 KB of x + 32 KB of y)
-constexpr int kExtStages = 3;
-constexpr int kExtThreads = 512;  // 16 warps: the compare/select chains need them
-constexpr size_t kExtSmem = (size_t)kExtStages * kExtTile * 16 + 64;
+constexpr int kExtTile = 2048;    // points per tile (16 KB of x + 16 KB of y)
+constexpr int kExtStages = 4;
+constexpr int kExtThreads = 512;  // 2 pairs (4 points) per thread per tile
+using ExtRing = XYRing<kExtTile, kExtStages>;
+constexpr size_t kExtSmem = ExtRing::kSmem + 64;
 
 __global__ void __launch_bounds__(kExtThreads, 1) k_extremes_tma(const double* __restrict__ xs,
                                                            const double* __restrict__ ys, uint32_t n,
@@ -223,51 +226,32 @@ __global__ void __launch_bounds__(kExtThreads, 1) k_extremes_tma(const double* _
                                                            ExtResult* __restrict__ out,
                                                            Counters* __restrict__ ctr) {
   extern __shared__ __align__(128) unsigned char ext_smem[];
-  double* sx = reinterpret_cast<double*>(ext_smem);                   // [stage][kExtTile]
-  double* sy = sx + (size_t)kExtStages * kExtTile;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sy + (size_t)kExtStages * kExtTile);
-  const uint32_t ntiles = n / kExtTile;
-  const uint32_t mine = ntiles > blockIdx.x ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0u;
-  if (threadIdx.x == 0) {
-    for (int k = 0; k < kExtStages; ++k) mbar_init(&bar[k], 1);
-    mbar_fence_init();
-  }
+  ExtRing ring;
+  ring.setup(ext_smem, xs, ys, n);
+  ring.start();
   __syncthreads();
-  auto issue = [&](uint32_t k) {  // this CTA's k-th tile into stage k % kExtStages
-    const uint32_t st = k % kExtStages;
-    const size_t t0 = (size_t)(blockIdx.x + k * gridDim.x) * kExtTile;
-    mbar_expect_tx(&bar[st], 2u * kExtTile * 8u);
-    bulk_g2s(sx + (size_t)st * kExtTile, xs + t0, kExtTile * 8u, &bar[st]);
-    bulk_g2s(sy + (size_t)st * kExtTile, ys + t0, kExtTile * 8u, &bar[st]);
-  };
-  if (threadIdx.x == 0)
-    for (uint32_t k = 0; k < (uint32_t)kExtStages - 1 && k < mine; ++k) issue(k);
-  // four independent accumulators (pair u goes to acc[u % 4]): shorter
-  // dependency chains; each still sees increasing indices
-  ExtAcc acc[4];
-#pragma unroll
-  for (int a = 0; a < 4; ++a) ext_init(acc[a]);
-  for (uint32_t k = 0; k < mine; ++k) {
-    if (threadIdx.x == 0 && k + kExtStages - 1 < mine) issue(k + kExtStages - 1);
-    const uint32_t st = k % kExtStages;
-    mbar_wait(&bar[st], (k / kExtStages) & 1u);
-    const double2* x2 = reinterpret_cast<const double2*>(sx + (size_t)st * kExtTile);
-    const double2* y2 = reinterpret_cast<const double2*>(sy + (size_t)st * kExtTile);
-    const uint32_t i0 = (blockIdx.x + k * gridDim.x) * kExtTile;
-#pragma unroll
-    for (int u = 0; u < kExtTile / 2 / kExtThreads; ++u) {
-      const uint32_t pp = threadIdx.x + u * kExtThreads;
-      const double2 vx = x2[pp], vy = y2[pp];
-      ext_push(acc[u & 3], vx.x, vy.x, i0 + 2 * pp);
-      ext_push(acc[u & 3], vx.y, vy.y, i0 + 2 * pp + 1);
-    }
-    __syncthreads();  // stage st may be refilled
+  // two independent accumulators (pair u goes to acc[u]): shorter dependency
+  // chains; each still sees increasing indices
+  ExtAcc acc[2];
+  ext_init(acc[0]);
+  ext_init(acc[1]);
+  for (uint32_t k = 0; k < ring.mine; ++k) {
+    ring.wait(k);
+    const double2* x2 = reinterpret_cast<const double2*>(ring.tx(k));
+    const double2* y2 = reinterpret_cast<const double2*>(ring.ty(k));
+    const double2 va = x2[threadIdx.x], vb = x2[threadIdx.x + kExtThreads];
+    const double2 wa = y2[threadIdx.x], wb = y2[threadIdx.x + kExtThreads];
+    ring.release(k);
+    const uint32_t ia = ring.tile_start(k) + 2 * threadIdx.x, ib = ia + 2 * kExtThreads;
+    ext_push(acc[0], va.x, wa.x, ia);
+    ext_push(acc[1], vb.x, wb.x, ib);
+    ext_push(acc[0], va.y, wa.y, ia + 1);
+    ext_push(acc[1], vb.y, wb.y, ib + 1);
   }
   if (blockIdx.x == gridDim.x - 1)
-    for (uint32_t i = ntiles * kExtTile + threadIdx.x; i < n; i += kExtThreads) ext_push(acc[0], xs[i], ys[i], i);
+    for (uint32_t i = (n / kExtTile) * kExtTile + threadIdx.x; i < n; i += kExtThreads)
+      ext_push(acc[0], xs[i], ys[i], i);
   ext_merge(acc[0], acc[1]);
-  ext_merge(acc[2], acc[3]);
-  ext_merge(acc[0], acc[2]);
   ext_finish(acc[0], xs, ys, partials, out, ctr);
 }
 

@@ -12,6 +12,9 @@ Outputs (committed):
   corpus.json   known-answer corpus: small seeded inputs x pipeline configs,
                 full hull index lists and stage counts
   stages.json   stage-level goldens: extremes, sorted buffer, discard flags
+  extra.json    C2-C4 at seeds 2-5 (SURVEY.md 8(d) secondary seeds) and the
+                uniform square at 100M and 200M points (seed 1), the sizes
+                where the sparse path's buckets outgrow shared memory
 """
 import hashlib
 import json
@@ -128,6 +131,27 @@ def stages():
         out.append(rec)
     (HERE / "stages.json").write_text(json.dumps(out, indent=1) + "\n")
     print("stage cases:", len(out))
+
+
+def extra():
+    out = {}
+    cases = [(f"{c}s{sd}", kind, 20_000_000, sd) for sd in (2, 3, 4, 5)
+             for c, kind in (("C2", "square"), ("C3", "disk"), ("C4", "circle"))]
+    cases += [("S100M", "square", 100_000_000, 1), ("S200M", "square", 200_000_000, 1)]
+    for name, kind, n, sd in cases:
+        if n > 50_000_000:  # the reference's generator alone (RSS); ours is checked on the GPU
+            xs, ys = oracle.ref_generate(KINDS[kind], n, sd)
+        else:
+            xs, ys = gen(kind, n, sd)
+        idx, st = run(xs, ys)
+        rec = {"kind": kind, "n": n, "seed": sd, "xs_sha256_16": sha(xs), "ys_sha256_16": sha(ys),
+               **st, "hull_sha256_16": sha(idx.astype(np.uint64))}
+        if idx.size <= 5000:
+            rec["hull"] = [int(v) for v in idx]
+        out[name] = rec
+        print(name, st, flush=True)
+        del xs, ys
+    (HERE / "extra.json").write_text(json.dumps(out, indent=1) + "\n")
 
 
 if __name__ == "__main__":

@@ -28,3 +28,16 @@ def test_shim_reference_style_suite(tmp_path):
     r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert r.stdout.strip().endswith("ok")
+
+
+PORT = ROOT / "tests" / "cpp" / "_bin" / "test_pipeline_port"
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not PORT.exists(), reason="built by __graft_entry__.build() where /root/reference exists")
+def test_reference_pipeline_checks_unchanged():
+    """test_pipeline.cpp:92-107 verbatim through the shim: CHECK_THROWS_AS(...,
+    EmptyInput / ZeroChunks) with the reference's own error types."""
+    r = subprocess.run([str(PORT)], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert r.stdout.strip().endswith("ok")
