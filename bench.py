@@ -371,7 +371,9 @@ def main():
     eng.set_profiling(False)
     kernels = {k2: round(float(np.mean(v)) * (len(v) / reps), 4) for k2, v in kt.items()}
     peak, peak_src = peaks()
-    fkern = "k_sp_hist" if "k_sp_hist" in kt else "k_filter_keys"
+    # the filter pass of the path that served the call: F2 on the sparse path;
+    # k_filter_keys when the sparse path declined (its k_sp_hist then exits at once)
+    fkern = "k_sp_hist" if eng.sparse_info()[0] == 1 and "k_sp_hist" in kt else "k_filter_keys"
     filt = kt.get(fkern, [])
     t_filter = float(np.mean(filt)) if filt else None
     n_local = hi - lo
@@ -381,6 +383,7 @@ def main():
         if fkern == "k_sp_hist":  # 16 B/pt read (xs, ys)
             alg_bytes = 16 * n_local
         else:
+            # 16 B/pt read + (survivor index, key, rank) = 16 B/survivor written
             alg_bytes = 16 * n_local + 16 * (n1 if (world == 1 and n1) else int(0.664 * n_local))
         achieved = alg_bytes / (t_filter * 1e-3) / 1e9
         traffic = None
