@@ -266,6 +266,8 @@ uint32_t sparse_region_cap(const gscan_handle* h, uint64_t n) {
 // look-back slots of the sparse path's scans (scan_u32_slot)
 enum LbSlot { kLbBstart = 0, kLbGs, kLbCstart, kLbWstart, kLbCompact, kLbSlots };
 
+constexpr uint64_t kSparseMinN = 1u << 16;  // smaller inputs take the full sort
+
 // Above this many points one device runs the sparse path only: the full
 // sort's per-point buffers (~120 B/pt) would not fit next to the input and
 // the sparse path's own (~50 B/pt) at 1B points. GSCAN_LARGE_MIN (dev/tests)
@@ -347,7 +349,7 @@ int reserve(gscan_handle* h, uint64_t n) {
   // up to 8x the mean bucket of n points (1B square, seed 1: mean gathered
   // bucket 13.8K, largest 88.7K = 4.4x n / kSpBuckets)
   h->sp_huge_cap = 0;
-  if (n / kSpBuckets * 8 > kSpGatherCap) {
+  if (n >= kSparseMinN) {
     h->sp_huge_cap = (uint32_t)std::max<uint64_t>(2 * kSpGatherCap, 8 * (n / kSpBuckets) + 64);
     CU(cudaMalloc(&h->sp_huge_scr,
                   (size_t)h->sm_count * ((size_t)h->sp_huge_cap * kSpHugeBytes + 16)));
@@ -969,7 +971,6 @@ float ev_ms(cudaEvent_t a, cudaEvent_t b) {
 // ---------------------------------------------------------------------------
 // Sparse round-2 path (sparse.cuh). Returns GSCAN_OK with *ok = false when the
 // path declined (fail bits in h->sp_fail): the caller then runs the full sort.
-constexpr uint64_t kSparseMinN = 1u << 16;
 
 bool sparse_eligible(const gscan_handle* h, uint64_t n, const gscan_config& cfg) {
   return n >= kSparseMinN && cfg.enable_round1 && cfg.enable_round2 && cfg.chunked &&

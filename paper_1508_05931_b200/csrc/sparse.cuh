@@ -195,16 +195,25 @@ __device__ __forceinline__ double unord_f(uint32_t u) {
 // 64-bit coordinate hash with -0.0 folded onto +0.0 (annotate's CoordSet
 // compares folded bits, angular.hpp:99-101): equal points hash equally, so
 // equal hashes are the only possible duplicates.
+// splitmix64's finalizer: a bijection of 64-bit words with full avalanche
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z ^= z >> 30;
+  z *= 0xbf58476d1ce4e5b9ull;
+  z ^= z >> 27;
+  z *= 0x94d049bb133111ebull;
+  z ^= z >> 31;
+  return z;
+}
+
 __device__ __forceinline__ uint64_t coord_hash64(double x, double y) {
   // x + 0.0 folds -0.0 onto +0.0 and leaves every other finite x unchanged
   const uint64_t a = dbits(__dadd_rn(x, 0.0)), b = dbits(__dadd_rn(y, 0.0));
-  // two odd multipliers and a fold: every input bit reaches the top bits (the
-  // partition) and the low bits; a collision of distinct points only makes
-  // the sparse path decline, never a wrong result
-  uint64_t z = a * 0x9e3779b97f4a7c15ull + b * 0xc2b2ae3d27d4eb4full;
-  z ^= z >> 31;
-  z *= 0xbf58476d1ce4e5b9ull;
-  z ^= z >> 29;
+  // mix(mix(a) + b): for a fixed x a bijection in y, and x's bits are spread
+  // over all 64 before y is added, so structured inputs (integer lattices,
+  // whose doubles share ~40 trailing zero bits) do not collide -- a linear
+  // a*C1 + b*C2 kept only their top bits. A collision of distinct points only
+  // makes the sparse path decline, never a wrong result.
+  const uint64_t z = mix64(mix64(a) + b);
   return z == ~0ull ? 0ull : z;  // ~0 marks an empty slot / padding
 }
 
