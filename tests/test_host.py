@@ -31,15 +31,40 @@ def test_library_is_sm100a():
     assert "sm_100a" in out.stdout
 
 
-def test_no_fma_in_predicate_kernels():
-    """geom.hpp:19-21 cross() is unfused; the device build must not contract it."""
-    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", "-fun",
-                          "_ZN5gscan14k_round2_blockEPKdS1_NS_9SliceGeomEPh",
-                          str(ROOT / "paper_1508_05931_b200/_lib/libgscan.so")],
-                         capture_output=True, text=True)
-    sass = out.stdout
-    assert "DMUL" in sass
-    # the only fused ops allowed are inside CUDA's atan2 (walk speculation key)
+PROBE = r"""
+#include "device_common.cuh"
+using namespace gscan;
+// each predicate alone in a kernel, its operands from memory so nothing folds
+extern "C" __global__ void probe_cross(const double* p, double* o) {
+  o[0] = cross_rn(p[0], p[1], p[2], p[3], p[4], p[5]);
+}
+extern "C" __global__ void probe_cross_edge(const double* p, double* o) {
+  o[0] = cross_edge(p[0], p[1], p[2], p[3], p[4], p[5]);
+}
+extern "C" __global__ void probe_dist2(const double* p, double* o) { o[0] = dist2_rn(p[0], p[1]); }
+"""
+
+
+def test_no_fma_in_predicates(tmp_path):
+    """geom.hpp:19-21 cross() and dist2 (geom.hpp:42) are unfused double
+    arithmetic (the reference binary has no FMA): the device predicates,
+    compiled with the library's flags, contain DMUL/DADD and no DFMA. (Fused
+    ops elsewhere in the library -- the glibc atan2 restatement's intentional
+    __fma_rn, the Newton steps of screened reciprocals -- are not predicates.)"""
+    from paper_1508_05931_b200 import build as B
+    src = tmp_path / "probe.cu"
+    src.write_text(PROBE)
+    obj = tmp_path / "probe.cubin"
+    subprocess.run([B.NVCC, *[f for f in B.NVCC_FLAGS if f not in ("-Xcompiler", "-fPIC")],
+                    f"-I{B.CSRC}", "-cubin", str(src), "-o", str(obj)], check=True)
+    sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", str(obj)],
+                          capture_output=True, text=True, check=True).stdout
+    funcs = sass.split("Function : ")[1:]
+    assert len(funcs) == 3
+    for f in funcs:
+        name = f.split()[0]
+        assert "DMUL" in f, name
+        assert "DFMA" not in f, f"{name} contains a fused multiply-add"
 
 
 def test_datagen_bit_identical_to_reference(oracle_mod):
