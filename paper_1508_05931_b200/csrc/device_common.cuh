@@ -171,11 +171,12 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // data, and kS tiles are in flight per CTA. Needs 16-byte aligned xs, ys.
 template <int kT, int kS>
 struct XYRing {
-  static constexpr size_t kSmem = (size_t)kS * kT * 16 + (size_t)kS * 8 + (size_t)kS * 4;
+  static constexpr size_t kSmem = (size_t)kS * kT * 16 + (size_t)kS * 16 + (size_t)kS * 4;
   double* sx;        // [kS][kT]
   double* sy;        // [kS][kT]
-  uint64_t* full;    // [kS]
-  uint32_t* cnt;     // [kS] warps done with the stage's current tile
+  uint64_t* full;    // [kS] the stage's tile has landed (bulk-copy transaction bytes)
+  uint64_t* empty;   // [kS] every thread has read the stage (one arrival per thread)
+  uint32_t* cnt;     // [kS] arrivals so far: elects the last warp as the refiller
   const double* xs;
   const double* ys;
   uint32_t mine;     // tiles of this CTA
@@ -186,7 +187,8 @@ struct XYRing {
     sx = reinterpret_cast<double*>(smem);
     sy = sx + (size_t)kS * kT;
     full = reinterpret_cast<uint64_t*>(sy + (size_t)kS * kT);
-    cnt = reinterpret_cast<uint32_t*>(full + kS);
+    empty = full + kS;
+    cnt = reinterpret_cast<uint32_t*>(empty + kS);
     xs = x;
     ys = y;
     const uint32_t ntiles = n / kT;
@@ -208,6 +210,7 @@ struct XYRing {
     if (threadIdx.x == 0) {
       for (int k = 0; k < kS; ++k) {
         mbar_init(&full[k], 1);
+        mbar_init(&empty[k], blockDim.x);
         cnt[k] = 0;
       }
       mbar_fence_init();
@@ -217,16 +220,19 @@ struct XYRing {
   __device__ __forceinline__ void wait(uint32_t k) { mbar_wait(&full[k % kS], (k / kS) & 1u); }
   __device__ __forceinline__ const double* tx(uint32_t k) const { return sx + (size_t)(k % kS) * kT; }
   __device__ __forceinline__ const double* ty(uint32_t k) const { return sy + (size_t)(k % kS) * kT; }
-  // the calling warp is done reading tile k (its values are in registers)
+  // The calling warp is done reading tile k (its values are in registers): its
+  // threads arrive on empty[st] (release); the last warp to arrive -- elected by the
+  // counter -- waits for that phase (acquire: every warp's reads of the stage
+  // are ordered before), fences the async proxy and refills the stage.
   __device__ __forceinline__ void release(uint32_t k) {
+    const uint32_t st = k % kS;
+    mbar_arrive(&empty[st]);  // every thread: its own reads are released
     __syncwarp();
     if ((threadIdx.x & 31) == 0) {
-      const uint32_t st = k % kS;
-      __threadfence_block();  // this warp's reads of the stage happen before the count
       if (atomicAdd(&cnt[st], 1u) == nwarps - 1) {
         cnt[st] = 0;
+        mbar_wait(&empty[st], (k / kS) & 1u);
         if (k + kS < mine) {
-          __threadfence_block();
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // reads before the async writes
           issue(k + kS);
         }

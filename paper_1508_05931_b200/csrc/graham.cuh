@@ -104,6 +104,7 @@ __global__ void __launch_bounds__(kLocalWarps * 32) k_graham_local(const double*
         if (dhi - 31 <= 1) { newtop = min(top, 1); break; }
         dhi -= 32;
       }
+      __syncwarp();  // every lane's stack reads happen before lane 0 overwrites the top
       if (lane == 0) { sx[newtop] = fx; sy[newtop] = fy; si[newtop] = (uint8_t)(i + f); }
       top = newtop + 1;
       i += f + 1;
@@ -231,6 +232,7 @@ __global__ void __launch_bounds__(32) k_graham_candidate_seq(
           if (dhi - 31 <= 1) { newtop = min(top, 1); break; }
           dhi -= 32;
         }
+        __syncwarp();  // every lane's stack reads happen before lane 0 overwrites the top
         if (lane == 0) {
           sx[newtop] = fx; sy[newtop] = fy; sp[newtop] = fp;
           stack[newtop] = fp;
@@ -528,6 +530,7 @@ __device__ int warp_scan_onto(const double* __restrict__ R_x, const double* __re
         if (dhi - 31 <= 1) { newtop = min(top, 1); break; }
         dhi -= 32;
       }
+      __syncwarp();  // every lane's stack reads happen before lane 0 overwrites the top
       if (lane == 0) st[newtop] = fp;
       top = newtop + 1;
       i += f + 1;

@@ -626,6 +626,7 @@ __global__ void __launch_bounds__(kTreeThreads, 1) k_gr_mid(
             if (dhi - 31 <= 1) { newtop = min(top, 1); break; }
             dhi -= 32;
           }
+          __syncwarp();  // every lane's stack reads happen before lane 0 overwrites the top
           if (lane == 0) {
             st_x[newtop] = fx;
             st_y[newtop] = fy;
