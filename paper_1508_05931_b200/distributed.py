@@ -115,6 +115,12 @@ class Comm:
         """-> the list of all R objects (same on every rank)."""
         raise NotImplementedError
 
+    def allgather_i64(self, rows: list) -> np.ndarray:
+        """Fixed-length int64 rows (one per local rank, same length everywhere)
+        -> (R, L) int64 array on every rank: one tensor all-gather, no pickling.
+        Doubles travel as their bit patterns (_i64 / _f64)."""
+        raise NotImplementedError
+
     def gather_root(self, ts: list[torch.Tensor]) -> list[torch.Tensor] | None:
         """Variable-length 1-D tensors -> rank 0 gets all R (rank order); others None."""
         raise NotImplementedError
@@ -143,6 +149,9 @@ class LocalComm(Comm):
     def allgather_obj(self, objs):
         return list(objs)
 
+    def allgather_i64(self, rows):
+        return np.stack([np.asarray(r, dtype=np.int64) for r in rows])
+
     def gather_root(self, ts):
         return [t.clone() for t in ts]
 
@@ -163,12 +172,20 @@ class TorchComm(Comm):
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
         self.ranks = [self.rank]
+        # gloo (CPU backend, e.g. ranks sharing one GPU in tests) stages device
+        # tensors through host memory; NCCL moves them directly
+        self.stage = dist.get_backend(group) == "gloo"
+        self.cdev = torch.device("cpu") if self.stage else torch.device(
+            "cuda", torch.cuda.current_device())
+
+    def _out(self, t):  # a tensor as the backend takes it
+        return t.cpu() if self.stage else t
 
     def allreduce(self, ts, op):
         (t,) = ts
-        t = t.clone()
-        dist.all_reduce(t, op=self._OPS[op], group=self.group)
-        return [t]
+        w = self._out(t).clone()
+        dist.all_reduce(w, op=self._OPS[op], group=self.group)
+        return [w.to(t.device)]
 
     def allgather_obj(self, objs):
         (o,) = objs
@@ -176,40 +193,78 @@ class TorchComm(Comm):
         dist.all_gather_object(out, o, group=self.group)
         return out
 
+    def allgather_i64(self, rows):
+        (r,) = rows
+        t = torch.as_tensor(np.asarray(r, dtype=np.int64), device=self.cdev)
+        out = torch.empty((self.world, t.numel()), dtype=torch.int64, device=self.cdev)
+        if self.stage:
+            dist.all_gather(list(out.unbind(0)), t, group=self.group)
+        else:
+            dist.all_gather_into_tensor(out, t, group=self.group)
+        return out.cpu().numpy()
+
     def gather_root(self, ts):
         (t,) = ts
-        n = torch.tensor([t.numel()], dtype=torch.int64, device=t.device)
-        ns = torch.empty(self.world, dtype=torch.int64, device=t.device)
-        dist.all_gather_into_tensor(ns, n, group=self.group)
-        ns = ns.tolist()
+        ns = self.allgather_i64([[t.numel()]])[:, 0].tolist()
         mx = max(max(ns), 1)
-        pad = torch.zeros(mx, dtype=t.dtype, device=t.device)
-        pad[: t.numel()] = t
-        allp = torch.empty(self.world * mx, dtype=t.dtype, device=t.device)
-        dist.all_gather_into_tensor(allp, pad, group=self.group)
+        pad = torch.zeros(mx, dtype=t.dtype, device=self.cdev)
+        pad[: t.numel()] = self._out(t)
+        bufs = [torch.empty(mx, dtype=t.dtype, device=self.cdev) for _ in range(self.world)] \
+            if self.rank == 0 else None
+        dist.gather(pad, gather_list=bufs, dst=0, group=self.group)
         if self.rank != 0:
             return None
-        return [allp[r * mx: r * mx + ns[r]].clone() for r in range(self.world)]
+        return [bufs[r][: ns[r]].to(t.device) for r in range(self.world)]
 
     def bcast_root(self, t, like):
         (ref,) = like
-        buf = t.clone() if self.rank == 0 else torch.empty_like(ref)
+        buf = self._out(t).clone() if self.rank == 0 else torch.empty_like(self._out(ref))
         dist.broadcast(buf, 0, group=self.group)
-        return [buf]
+        return [buf.to(ref.device)]
 
     def all_to_all(self, sends):
         (row,) = sends
-        sizes = torch.tensor([x.numel() for x in row], dtype=torch.int64, device=row[0].device)
-        rsizes = torch.empty_like(sizes)
-        dist.all_to_all_single(rsizes, sizes, group=self.group)
-        rs = rsizes.tolist()
-        out = torch.empty(sum(rs), dtype=row[0].dtype, device=row[0].device)
-        dist.all_to_all_single(out, torch.cat(list(row)), output_split_sizes=rs,
-                               input_split_sizes=sizes.tolist(), group=self.group)
-        return [list(torch.split(out, rs))]
+        dev = row[0].device
+        sizes = [int(x.numel()) for x in row]
+        rs = [int(v) for v in self.allgather_i64([sizes])[:, self.rank]]
+        out = torch.empty(sum(rs), dtype=row[0].dtype, device=self.cdev)
+        if self.stage:  # gloo: point-to-point through host memory
+            outs = list(torch.split(out, rs))
+            reqs = []
+            for r in range(self.world):
+                if r == self.rank:
+                    outs[r].copy_(row[r].cpu())
+                    continue
+                reqs.append(dist.isend(row[r].cpu().contiguous(), r, group=self.group))
+                reqs.append(dist.irecv(outs[r], r, group=self.group))
+            for q in reqs:
+                q.wait()
+        else:
+            dist.all_to_all_single(out, torch.cat(list(row)), output_split_sizes=rs,
+                                   input_split_sizes=sizes, group=self.group)
+        return [[x.to(dev) for x in torch.split(out, rs)]]
 
 
 # ---------------------------------------------------------------------------
+def _i64(x: float) -> int:
+    """A double's bit pattern as int64 (exact through the int64 collectives)."""
+    return int(np.array([x], dtype=np.float64).view(np.int64)[0])
+
+
+def _f64(v) -> float:
+    return float(np.array([v], dtype=np.int64).view(np.float64)[0])
+
+
+def _u64(v) -> int:
+    return int(v) & 0xFFFFFFFFFFFFFFFF
+
+
+def _s64(v) -> int:
+    """A uint64 as the int64 with the same bits (for the int64 collectives)."""
+    v = int(v) & 0xFFFFFFFFFFFFFFFF
+    return v - (1 << 64) if v >= 1 << 63 else v
+
+
 def _ck(eng: Engine, rc: int, what: str):
     if rc:
         eng._raise(rc, what)
@@ -229,8 +284,12 @@ def _extremes(engines, shards, offsets, comm: Comm) -> N.gscan_extremes:
         _ck(eng, eng._lib.gscan_shard_extremes(eng.handle, C.c_void_p(dx.data_ptr()),
                                                C.c_void_p(dy.data_ptr()), dx.numel(), C.byref(ex)),
             "shard_extremes")
-        recs.append(np.array([[float(off + ex.idx[k]) for k in range(5)], list(ex.x), list(ex.y)]))
-    g = _combine(np.stack(comm.allgather_obj(recs)))
+        recs.append([off + ex.idx[k] for k in range(5)] + [_i64(v) for v in ex.x]
+                    + [_i64(v) for v in ex.y])
+    allr = comm.allgather_i64(recs)  # (R, 15): global indices, x bits, y bits
+    g = _combine(np.stack([np.array([[float(r[k]) for k in range(5)],
+                                     [_f64(r[5 + k]) for k in range(5)],
+                                     [_f64(r[10 + k]) for k in range(5)]]) for r in allr]))
     gex = N.gscan_extremes()
     for k in range(5):
         gex.idx[k] = int(g[0, k])
@@ -250,7 +309,7 @@ def _declined(why: str):
 
 def _agree(comm: Comm, local_ok: list[bool]) -> bool:
     """Every rank's verdict -> one decision all ranks take together."""
-    return all(comm.allgather_obj(local_ok))
+    return bool(comm.allgather_i64([[int(bool(v))] for v in local_ok]).all())
 
 
 def sparse_sharded(engines: list[Engine], shards, offsets: list[int], n_global: int,
@@ -290,9 +349,12 @@ def sparse_sharded(engines: list[Engine], shards, offsets: list[int], n_global: 
         bests.append((int(b.d2_bits), int(b.idx), int(b.ties), float(b.x), float(b.y)))
         n1s.append(int(n1.value))
     hists = comm.allreduce(hists, "sum")
-    allb = comm.allgather_obj([(bb, n) for bb, n in zip(bests, n1s)])
-    best, ties = _combine_best([x[0] for x in allb])
-    n1 = sum(x[1] for x in allb)
+    rows = [[_s64(bb[0]), _s64(bb[1]), bb[2], _i64(bb[3]), _i64(bb[4]), n]
+            for bb, n in zip(bests, n1s)]
+    allb = comm.allgather_i64(rows)
+    best, ties = _combine_best([(_u64(r[0]), _u64(r[1]), int(r[2]), _f64(r[3]), _f64(r[4]))
+                                for r in allb])
+    n1 = int(allb[:, 5].sum())
     fail = 0
     if best is None:
         fail |= N.SP_FAIL_FEW
@@ -313,10 +375,10 @@ def sparse_sharded(engines: list[Engine], shards, offsets: list[int], n_global: 
                                           C.byref(lb), C.byref(f)), "dist_plan")
         lbs.append(int(lb.value))
         fails.append(int(f.value))
-    allv = comm.allgather_obj([(a, b) for a, b in zip(lbs, fails)])
-    if any(x[1] for x in allv):
-        return _declined(f"ranking P_l: fail bits {[x[1] for x in allv]}")
-    l_below = sum(x[0] for x in allv)
+    allv = comm.allgather_i64([[a, b] for a, b in zip(lbs, fails)])
+    if allv[:, 1].any():
+        return _declined(f"ranking P_l: fail bits {allv[:, 1].tolist()}")
+    l_below = int(allv[:, 0].sum())
 
     # 4. F3: walk-angle maxima -> max, phi range -> min/max; gathered counts
     phis, rng, ngs, fails = [], [], [], []
@@ -331,13 +393,13 @@ def sparse_sharded(engines: list[Engine], shards, offsets: list[int], n_global: 
         rng.append((int(pr[0]), int(pr[1])))
         ngs.append(int(ng.value))
         fails.append(int(f.value))
-    allv = comm.allgather_obj([(a, b) for a, b in zip(rng, fails)])
-    if any(x[1] for x in allv):
-        return _declined(f"F3: fail bits {[x[1] for x in allv]}")
+    allv = comm.allgather_i64([[a[0], a[1], b] for a, b in zip(rng, fails)])
+    if allv[:, 2].any():
+        return _declined(f"F3: fail bits {allv[:, 2].tolist()}")
     if _DBG:
         print(f"[dist] n1={n1} l_below={l_below} n_g={ngs} hist_sum={int(hists[0].to(torch.int64).sum())}")
-    phi_lo = min(x[0][0] for x in allv)
-    phi_hi = max(x[0][1] for x in allv)
+    phi_lo = int(allv[:, 0].min())
+    phi_hi = int(allv[:, 1].max())
     phis = comm.allreduce(phis, "max")
 
     # duplicate check: this rank's hashes by partition; partition range k -> rank k
@@ -377,7 +439,7 @@ def sparse_sharded(engines: list[Engine], shards, offsets: list[int], n_global: 
                                                C.c_void_p(mat.data_ptr()), comm.world, C.byref(d)),
             "dist_dup_check")
         dups.append(int(d.value))
-    if any(comm.allgather_obj(dups)):
+    if comm.allgather_i64([[d] for d in dups]).any():
         return _declined("possible duplicate points (hash partition exchange)")
 
     # 5. gathered points -> rank 0 (records {x, y, global index, bucket})
@@ -451,10 +513,11 @@ def sparse_sharded(engines: list[Engine], shards, offsets: list[int], n_global: 
                                           C.byref(f)), "dist_cand")
         ncs.append(int(nc.value))
         fails.append(int(f.value))
-    allv = comm.allgather_obj([(a, b) for a, b in zip(ncs, fails)])
+    allv = comm.allgather_i64([[a, b] for a, b in zip(ncs, fails)])
     m_global = int(hists[0].to(torch.int64).sum())
-    if any(x[1] for x in allv) or sum(x[0] for x in allv) > max(m_global // 8, 65536):
-        return _declined(f"F4: fail bits {[x[1] for x in allv]}, candidates {sum(x[0] for x in allv)} of {m_global}")
+    n_cand = int(allv[:, 0].sum())
+    if allv[:, 1].any() or n_cand > max(m_global // 8, 65536):
+        return _declined(f"F4: fail bits {allv[:, 1].tolist()}, candidates {n_cand} of {m_global}")
     croot = to_root(export(1, ncs))
 
     # 7. rank 0: walk, certificate, Graham
@@ -517,11 +580,11 @@ def survivor_gather(eng: Engine, d_xs: torch.Tensor, d_ys: torch.Tensor, offset:
         ex = N.gscan_extremes()
         _ck(eng, lib.gscan_shard_extremes(eng.handle, C.c_void_p(d_xs.data_ptr()),
                                           C.c_void_p(d_ys.data_ptr()), n, C.byref(ex)), "shard_extremes")
-        mine = torch.tensor([[float(offset + ex.idx[k]) for k in range(5)], list(ex.x), list(ex.y)],
-                            dtype=torch.float64, device=dev)
-        allr = torch.empty((world, 3, 5), dtype=torch.float64, device=dev)
-        dist.all_gather_into_tensor(allr, mine, group=group)
-        g = _combine(allr.cpu().numpy())
+        allr = comm.allgather_i64([[offset + ex.idx[k] for k in range(5)] +
+                                   [_i64(v) for v in ex.x] + [_i64(v) for v in ex.y]])
+        g = _combine(np.stack([np.array([[float(r[k]) for k in range(5)],
+                                         [_f64(r[5 + k]) for k in range(5)],
+                                         [_f64(r[10 + k]) for k in range(5)]]) for r in allr]))
         gex = N.gscan_extremes()
         for k in range(5):
             gex.idx[k] = int(g[0, k])
@@ -538,29 +601,16 @@ def survivor_gather(eng: Engine, d_xs: torch.Tensor, d_ys: torch.Tensor, offset:
     else:
         sx, sy = d_xs, d_ys
         sg = torch.arange(offset, offset + n, device=dev, dtype=torch.int64)
-    cnt = torch.tensor([sx.numel(), n], dtype=torch.int64, device=dev)
-    both = torch.empty((world, 2), dtype=torch.int64, device=dev)
-    dist.all_gather_into_tensor(both, cnt, group=group)
-    both = both.cpu().tolist()
-    counts = [b[0] for b in both]
-    n_global = sum(b[1] for b in both)
-    mx = max(counts)
-    pack = torch.zeros((3, mx), dtype=torch.float64, device=dev)
-    pack[0, : sx.numel()] = sx
-    pack[1, : sy.numel()] = sy
-    pack[2, : sg.numel()] = sg.double()  # exact below 2^53
+    n_global = int(comm.allgather_i64([[n]])[:, 0].sum())
     # survivors go to rank 0 only (the other ranks hold nothing extra)
-    gathered = [torch.empty((3, mx), dtype=torch.float64, device=dev) for _ in range(world)] \
-        if rank == 0 else None
-    dist.gather(pack, gather_list=gathered, dst=0, group=group)
-    del pack
+    px = comm.gather_root([sx.contiguous()])
+    py = comm.gather_root([sy.contiguous()])
+    pg = comm.gather_root([sg.contiguous()])
     if rank != 0:
         return None, None
-    parts = [gathered[r][:, : counts[r]] for r in range(world)]
-    allp = torch.cat(parts, dim=1)
-    gx = allp[0].contiguous()
-    gy = allp[1].contiguous()
-    gidx = allp[2].long()
+    gx = torch.cat(px).contiguous()
+    gy = torch.cat(py).contiguous()
+    gidx = torch.cat(pg).long()
     m = int(gx.numel())
     out = torch.empty(max(m, 1), dtype=torch.int32, device=dev)
     rest = PipelineConfig(cfg.chunk_count, False, cfg.enable_round2, cfg.chunked)
@@ -581,7 +631,7 @@ def sharded_hull(eng: Engine, d_xs: torch.Tensor, d_ys: torch.Tensor, offset: in
     cfg = cfg or PipelineConfig()
     comm = TorchComm(group)
     n = int(d_xs.numel())
-    sizes = comm.allgather_obj([n])
+    sizes = comm.allgather_i64([[n]])[:, 0].tolist()
     n_global = sum(sizes)
     # global indices are 32-bit on the device (every rank knows n_global, so
     # all of them take the same path)

@@ -141,3 +141,62 @@ def test_sharded_uneven_shards_tiny_ranks(engines, oracle_mod):
         want, sw = oracle_mod.full_pipeline(xs, ys)
         assert np.array_equal(got, want), bounds
         assert st.n_after_round2 == sw["n_after_round2"], bounds
+
+
+GLOO2_SCRIPT = r"""
+import os, sys
+sys.path.insert(0, sys.argv[1])
+import numpy as np, torch, torch.distributed as dist
+import oracle
+from paper_1508_05931_b200 import Engine, PipelineConfig, generate
+from paper_1508_05931_b200 import distributed as D
+rank = int(sys.argv[3])
+torch.cuda.set_device(0)
+dist.init_process_group("gloo", init_method="tcp://127.0.0.1:%s" % sys.argv[2], rank=rank,
+                        world_size=2)
+kind, n = sys.argv[4], int(sys.argv[5])
+xs, ys = generate(kind, n, 23)
+lo, hi = n * rank // 2, n * (rank + 1) // 2
+eng = Engine(0)
+if rank == 0:
+    eng.reserve(n)
+dx, dy = torch.from_numpy(xs[lo:hi].copy()).cuda(), torch.from_numpy(ys[lo:hi].copy()).cuda()
+got, st = D.sharded_hull(eng, dx, dy, lo, PipelineConfig())
+if rank == 0:
+    want, sw = oracle.full_pipeline(xs, ys)
+    assert np.array_equal(got, want), (got[:8], want[:8])
+    assert st.n_after_round2 == sw["n_after_round2"] and st.hull_size == sw["hull_size"]
+    print("ok", "sparse" if D.last_decline == "" else "declined: " + D.last_decline)
+else:
+    assert got is None
+dist.destroy_process_group()
+"""
+
+
+@pytest.mark.parametrize("kind,n", [("square", 600_000), ("disk", 400_000), ("circle", 100_000)])
+def test_sharded_hull_two_processes_gloo(tmp_path, kind, n):
+    """The full sharded_hull with TorchComm across two real processes (world
+    size 2, gloo staging device tensors through the host, both ranks on
+    cuda:0): every exchange of the multi-GPU path, and the survivor-gather
+    fallback for the circle (near-convex: the sparse path declines)."""
+    import socket
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    script = tmp_path / "g2.py"
+    script.write_text(GLOO2_SCRIPT)
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    root = Path(__file__).resolve().parents[1]
+    procs = [subprocess.Popen([sys.executable, str(script), str(root), str(port), str(r), kind, str(n)],
+                              stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)
+             for r in range(2)]
+    outs = [p.communicate(timeout=600) for p in procs]
+    for p, (o, e) in zip(procs, outs):
+        assert p.returncode == 0, e[-3000:]
+    assert outs[0][0].startswith("ok")
+    if kind != "circle":
+        assert "sparse" in outs[0][0], outs[0][0]
