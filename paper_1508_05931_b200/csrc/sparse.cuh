@@ -208,12 +208,12 @@ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
 __device__ __forceinline__ uint64_t coord_hash64(double x, double y) {
   // x + 0.0 folds -0.0 onto +0.0 and leaves every other finite x unchanged
   const uint64_t a = dbits(__dadd_rn(x, 0.0)), b = dbits(__dadd_rn(y, 0.0));
-  // mix(mix(a) + b): for a fixed x a bijection in y, and x's bits are spread
-  // over all 64 before y is added, so structured inputs (integer lattices,
-  // whose doubles share ~40 trailing zero bits) do not collide -- a linear
-  // a*C1 + b*C2 kept only their top bits. A collision of distinct points only
-  // makes the sparse path decline, never a wrong result.
-  const uint64_t z = mix64(mix64(a) + b);
+  // mix(a + rotl(b, 32)): y's high bits land in the word's low half, where x's
+  // doubles of structured inputs (integer lattices: ~40 trailing zero bits)
+  // are zero, so such inputs do not collide before the bijective mix -- a
+  // linear a*C1 + b*C2 kept only their top bits. A collision of distinct
+  // points only makes the sparse path decline, never a wrong result.
+  const uint64_t z = mix64(a + ((b << 32) | (b >> 32)));
   return z == ~0ull ? 0ull : z;  // ~0 marks an empty slot / padding
 }
 
