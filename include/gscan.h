@@ -253,9 +253,11 @@ int gscan_last_graham_info(const gscan_handle* h, uint32_t* path, uint32_t* cert
  * default toggles): used = 1 when its result was returned; fail_bits != 0
  * when it declined and the full sort ran instead: 1 tie for the farthest
  * point, 4 a region with <= 1 point, 8 possible duplicates, 16 failed
- * verification, 32 capacity (an oversized gathered bucket, or a
- * duplicate-check partition of 2^15 hashes or more: above ~67M round-1
- * survivors), 64 internal, 128 too few points, 256 too many
+ * verification, 32 capacity (a gathered or candidate bucket above its
+ * sorter's scratch -- 8x the mean bucket of n points -- or with clustered
+ * keys; a duplicate-check partition of 2^21 - 1 hashes or more, above ~4G
+ * survivors; walk arrays too small in large mode; unfinished side-stream
+ * work), 64 internal, 128 too few points, 256 too many
  * walk candidates (near-circular inputs: the full sort is faster);
  * n_walked = points it sorted and walked exactly (gathered + candidates +
  * anchor). */
