@@ -147,6 +147,8 @@ struct gscan_handle {
   uint32_t sp_huge_cap = 0;      // elements per area (0: inputs too small to need it)
   uint64_t* sp_dup_scr = nullptr;  // duplicate check: sub-partition scratch of large partitions
   uint32_t sp_dup_scap = 0;        // entries per (CTA, group) area
+  uint32_t* sp_exc = nullptr;      // F2 screen: points for the exact pass
+  uint32_t sp_exc_cap = 0;
   uint32_t *sp_gcount = nullptr, *sp_ccount = nullptr, *sp_hcount = nullptr;  // per-CTA emissions
   uint64_t* sp_dup2 = nullptr;   // partitioned hash list (n)
   uint64_t* sp_side_status = nullptr;  // look-back status of the side stream's scan
@@ -234,7 +236,7 @@ void free_buffers(gscan_handle* h) {
   dfree(h->g_keep); dfree(h->g_misc);
   dfree(h->g_stA); dfree(h->g_stB); dfree(h->g_lenA); dfree(h->g_lenB); dfree(h->g_scr);
   dfree(h->lb_status); dfree(h->lb_ctr); dfree(h->sp_eb); dfree(h->sp_gx); dfree(h->sp_gy); dfree(h->sp_Wb); dfree(h->sp_Ws); dfree(h->sp_Rb); dfree(h->sp_Rs); dfree(h->sp_dup);
-  dfree(h->sp_codes); dfree(h->sp_phi32); dfree(h->sp_dup2); dfree(h->tw_pool); dfree(h->sp_huge_scr); dfree(h->sp_dup_scr);
+  dfree(h->sp_codes); dfree(h->sp_phi32); dfree(h->sp_dup2); dfree(h->tw_pool); dfree(h->sp_huge_scr); dfree(h->sp_dup_scr); dfree(h->sp_exc);
   h->tw_nmax = 0;
   h->g_st_cap = 0;
   h->g_len_cap = 0;
@@ -362,6 +364,9 @@ int reserve(gscan_handle* h, uint64_t n) {
     h->sp_dup_scap = (uint32_t)(2 * (n / kSpParts) + 4096);
     CU(cudaMalloc(&h->sp_dup_scr, (size_t)h->sm_count * kSpDupGroups * h->sp_dup_scap * 8));
   }
+  // F2's uncertain points (~2e-4 of them; more than n/32 declines)
+  h->sp_exc_cap = (uint32_t)(n / 32 + 8192);
+  CU(cudaMalloc(&h->sp_exc, (size_t)h->sp_exc_cap * 4));
   CU(cudaMalloc(&h->sp_codes, (m + 1) * sizeof(uint16_t)));
   CU(cudaMalloc(&h->sp_phi32, (m + 1) * sizeof(float)));
   h->cap = n;
@@ -1046,6 +1051,7 @@ constexpr bool kF2Split = true;
 #define GSCAN_F2_RING 1
 #endif
 constexpr bool kF2Ring = GSCAN_F2_RING;  // F2 as a bulk-copy pipeline (k_sp_hist_ring)
+constexpr uint32_t kF2PatchGrid = 64;    // CTAs (and P_l partials) of k_sp_f2_patch
 // F3 without its shared-memory bucket maxima (1024 threads) + a maxima pass:
 // measured slower (F3 192 us either way, + 46 us for k_sp_phimax_codes)
 constexpr bool kF3Split = false;
@@ -1138,7 +1144,8 @@ int sp_seg_f2(gscan_handle* h, const SpCtx& c) {
   if (ring) {
     Launch L(h, "k_sp_hist", s);
     k_sp_hist_ring<<<g2, kF2Cons, kF2RingSmem, s>>>(c.xs, c.ys, c.n, h->ext, h->sp_cdf, h->sp_th,
-                                                         h->sp_codes, h->sp_d2, h->ctr, h->sp_st);
+                                                         h->sp_codes, h->sp_d2, h->ctr, h->sp_st,
+                                                         h->sp_exc, h->sp_exc_cap);
   } else {
     Launch L(h, "k_sp_hist", s);
 #define A2 c.xs, c.ys, c.n, h->ext, h->sp_cdf, h->sp_th, h->sp_codes, h->sp_hist_part, h->sp_d2, h->ctr, \
@@ -1152,6 +1159,14 @@ int sp_seg_f2(gscan_handle* h, const SpCtx& c) {
     }
 #undef A2
   }
+  uint32_t nparts = g2;  // P_l partials
+  if (ring) {  // the screen's uncertain points, exactly
+    Launch L(h, "k_sp_f2_patch", s);
+    k_sp_f2_patch<<<kF2PatchGrid, 256, 0, s>>>(c.xs, c.ys, h->ext, h->sp_cdf, h->sp_th, h->sp_codes,
+                                              h->sp_exc, h->sp_exc_cap, h->sp_d2 + g2, h->ctr,
+                                              h->sp_st);
+    nparts += kF2PatchGrid;
+  }
   if (kF2Split || ring) {
     Launch L(h, "k_sp_hist_codes", s);
     k_sp_hist_codes<<<c.G, 1024, c.smem_nb, s>>>(h->sp_codes, c.n, h->sp_hist_part, h->sp_st);
@@ -1162,7 +1177,7 @@ int sp_seg_f2(gscan_handle* h, const SpCtx& c) {
   }
   {
     Launch L(h, "k_sp_plan_pl", s);
-    k_sp_plan_pl<<<1, 256, 0, s>>>(c.xs, c.ys, h->sp_d2, g2, h->sp_st, h->ctr, c.n);
+    k_sp_plan_pl<<<1, 256, 0, s>>>(c.xs, c.ys, h->sp_d2, nparts, h->sp_st, h->ctr, c.n);
   }
   return GSCAN_OK;
 }

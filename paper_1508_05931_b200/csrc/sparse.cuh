@@ -111,6 +111,7 @@ struct SpState {
   uint32_t cert;       // 1: certificate holds (F6 skipped)
   uint32_t n_bigg;     // gathered buckets for the bitonic sorter
   uint32_t n_hugeg;    // gathered buckets above kSpGatherCap (global-scratch sorter)
+  uint32_t n_exc;      // F2 points left to the exact pass (k_sp_f2_patch)
 };
 
 // ---------------------------------------------------------------------------
@@ -570,7 +571,7 @@ __device__ __forceinline__ void f2_batch(const double (&x)[B], const double (&y)
 // compute dist2 in double.
 //
 // Preconditions of the quad screen (checked per CTA, else every point takes
-// the exact path): the box extents DX, DY in [2^-40, 2^40] and finite scaled
+// the exact path): the box extents DX, DY in [2^-50, 2^50] and finite scaled
 // coefficients.
 constexpr float kF2G1 = 2.0e-7f;
 constexpr float kF2G0 = 1.03e-4f;
@@ -595,7 +596,7 @@ __device__ __forceinline__ void f2_float_setup(const SpQuad& q, F2Float& f) {
   // bounding box from the extremes (minx, miny, maxx, maxy) around the anchor
   const double DX = fmax(fabs(q.qx[0] - q.ax), fabs(q.qx[2] - q.ax));
   const double DY = fabs(q.qy[3] - q.ay);
-  bool on = fmax(DX, DY) >= 0x1p-40 && fmax(DX, DY) <= 0x1p40;
+  bool on = fmax(DX, DY) >= 0x1p-50 && fmax(DX, DY) <= 0x1p50;
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
     const double ex = q.ex[e], ey = q.ey[e];
@@ -669,7 +670,8 @@ __device__ __forceinline__ void f2_points(const double (&x)[B], const double (&y
                                           const float4* s_tab, const double* __restrict__ cdf,
                                           const double* __restrict__ th, uint32_t& n1,
                                           uint64_t& bd2, uint32_t& bidx, uint32_t& bties,
-                                          float thr) {
+                                          float thr, uint32_t* __restrict__ exc_list,
+                                          uint32_t exc_cap, uint32_t* __restrict__ exc_n) {
   uint32_t sure = 0, inside = 0, cand = 0;
 #pragma unroll
   for (int k = 0; k < B; ++k) {
@@ -708,10 +710,10 @@ __device__ __forceinline__ void f2_points(const double (&x)[B], const double (&y
 #pragma unroll
   for (int k = 0; k < B; ++k) {
     if (!((exc >> k) & 1u)) continue;
-    if (!((sure >> k) & 1u)) {  // uncertain (~2e-4 of the points): the exact path
-      uint32_t kept;
-      code[k] = f2_exact(x[k], y[k], idx[k], q, cdf, th, kept, bd2, bidx, bties);
-      n1 += kept;
+    if (!((sure >> k) & 1u)) {  // uncertain (~2e-4 of the points): listed for the exact pass
+      const uint32_t slot = atomicAdd(exc_n, 1u);
+      if (slot < exc_cap) exc_list[slot] = idx[k];
+      code[k] = kSpNoCode;  // k_sp_f2_patch writes its code
     } else {  // may be (or tie) the farthest point
       const uint64_t d2 = dbits(dist2_rn(__dsub_rn(x[k], q.ax), __dsub_rn(y[k], q.ay)));
       const uint32_t i = idx[k];
@@ -876,7 +878,8 @@ __global__ void __launch_bounds__(kF2Cons, 1) k_sp_hist_ring(
     const double* __restrict__ xs, const double* __restrict__ ys, uint32_t n,
     const ExtResult* __restrict__ ext, const double* __restrict__ cdf,
     const double* __restrict__ th, uint16_t* __restrict__ codes, SpD2* __restrict__ d2part,
-    Counters* __restrict__ ctr, const SpState* __restrict__ st) {
+    Counters* __restrict__ ctr, SpState* __restrict__ st, uint32_t* __restrict__ exc_list,
+    uint32_t exc_cap) {
   extern __shared__ __align__(128) unsigned char f2_smem[];
   if (st->fail) return;  // declined from the sample (k_sp_cdf)
   F2Ring ring;
@@ -924,7 +927,8 @@ __global__ void __launch_bounds__(kF2Cons, 1) k_sp_hist_ring(
       bi[2 * u] = i0 + 2 * (threadIdx.x + u * kF2Cons);
       bi[2 * u + 1] = bi[2 * u] + 1;
     }
-    f2_points<2 * kF2Pairs>(bx, by, bi, bc, q, F, s_tab, cdf, th, n1, bd2, bidx, bties, thr);
+    f2_points<2 * kF2Pairs>(bx, by, bi, bc, q, F, s_tab, cdf, th, n1, bd2, bidx, bties, thr,
+                            exc_list, exc_cap, &st->n_exc);
 #pragma unroll
     for (int u = 0; u < kF2Pairs; ++u) c2[bi[2 * u] / 2] = bc[2 * u] | (bc[2 * u + 1] << 16);
     // warp-wide screen threshold: a point below the warp's best cannot be the
@@ -932,13 +936,11 @@ __global__ void __launch_bounds__(kF2Cons, 1) k_sp_hist_ring(
     const float mine_t = bidx != 0xffffffffu ? f2_thr(bitsd(bd2)) : 0.f;
     thr = fmaxf(thr, __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(mine_t))));
   }
-  // remainder (< one tile): the last CTA, direct loads, exact path
+  // remainder (< one tile): listed for the exact pass as well
   if (blockIdx.x == gridDim.x - 1) {
     for (uint32_t i = (n / kF2Tile) * kF2Tile + threadIdx.x; i < n; i += kF2Cons) {
-      uint32_t kept;
-      const uint32_t c = f2_exact(xs[i], ys[i], i, q, cdf, th, kept, bd2, bidx, bties);
-      n1 += kept;
-      codes[i] = (uint16_t)c;
+      const uint32_t slot = atomicAdd(&st->n_exc, 1u);
+      if (slot < exc_cap) exc_list[slot] = i;
     }
   }
   // block reductions: n1 (sum), (d2 max, ties) -- as k_sp_hist
@@ -963,6 +965,64 @@ __global__ void __launch_bounds__(kF2Cons, 1) k_sp_hist_ring(
       tot += s_n[w];
       if (w == 0) continue;
       if (s_i[w] == 0xffffffffu) continue;
+      if (bidx == 0xffffffffu || s_d[w] > bd2) { bd2 = s_d[w]; bidx = s_i[w]; bties = s_t[w]; }
+      else if (s_d[w] == bd2) { bties += s_t[w]; if (s_i[w] < bidx) bidx = s_i[w]; }
+    }
+    d2part[blockIdx.x] = SpD2{bd2, bidx, bidx == 0xffffffffu ? 0u : bties};
+    if (tot) atomicAdd(&ctr->n1, tot);
+  }
+}
+
+// F2's exact pass over the points its screen left uncertain (and the tail
+// of the last tile): f2_exact per listed point -- round-1 survival, bucket
+// code (a 2-byte store; F2 wrote kSpNoCode there), its dist2 into this
+// kernel's own P_l partials (d2part[blockIdx.x] of the slice passed in). A
+// list that overflowed declines the call (kSpFailCap: only inputs outside
+// the screen's preconditions get there).
+__global__ void __launch_bounds__(256) k_sp_f2_patch(
+    const double* __restrict__ xs, const double* __restrict__ ys,
+    const ExtResult* __restrict__ ext, const double* __restrict__ cdf,
+    const double* __restrict__ th, uint16_t* __restrict__ codes,
+    const uint32_t* __restrict__ exc_list, uint32_t exc_cap, SpD2* __restrict__ d2part,
+    Counters* __restrict__ ctr, SpState* __restrict__ st) {
+  if (st->fail) return;
+  const uint32_t ne = st->n_exc;
+  if (ne > exc_cap) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) { atomicOr(&st->fail, kSpFailCap); atomicMax(&st->why, 11u); }
+    return;
+  }
+  SpQuad q;
+  load_quad(ext, q);
+  uint32_t n1 = 0, bidx = 0xffffffffu, bties = 0;
+  uint64_t bd2 = 0;
+  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += gridDim.x * blockDim.x) {
+    const uint32_t i = exc_list[e];
+    uint32_t kept;
+    const uint32_t c = f2_exact(xs[i], ys[i], i, q, cdf, th, kept, bd2, bidx, bties);
+    n1 += kept;
+    codes[i] = (uint16_t)c;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    n1 += __shfl_xor_sync(0xffffffffu, n1, o);
+    const uint64_t od = __shfl_xor_sync(0xffffffffu, bd2, o);
+    const uint32_t oi = __shfl_xor_sync(0xffffffffu, bidx, o);
+    const uint32_t ot = __shfl_xor_sync(0xffffffffu, bties, o);
+    if (oi != 0xffffffffu) {
+      if (bidx == 0xffffffffu || od > bd2) { bd2 = od; bidx = oi; bties = ot; }
+      else if (od == bd2) { bties += ot; if (oi < bidx) bidx = oi; }
+    }
+  }
+  __shared__ uint64_t s_d[8];
+  __shared__ uint32_t s_i[8], s_t[8], s_n[8];
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) { s_d[warp] = bd2; s_i[warp] = bidx; s_t[warp] = bties; s_n[warp] = n1; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t tot = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      tot += s_n[w];
+      if (w == 0 || s_i[w] == 0xffffffffu) continue;
       if (bidx == 0xffffffffu || s_d[w] > bd2) { bd2 = s_d[w]; bidx = s_i[w]; bties = s_t[w]; }
       else if (s_d[w] == bd2) { bties += s_t[w]; if (s_i[w] < bidx) bidx = s_i[w]; }
     }
