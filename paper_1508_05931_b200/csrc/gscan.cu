@@ -59,6 +59,7 @@ struct SpGraphKey {
   uint64_t chunks = 0;
   uint32_t debug = 0;
   bool dup = true;
+  bool k1_done = false;  // extremes already computed (overlapped ingest)
   // buffers the full-sort path may swap (stage_annotate_sort): the graph bakes
   // their addresses in, so they are part of the key
   const void* bufs[7] = {};  // + the tree workspace
@@ -66,7 +67,7 @@ struct SpGraphKey {
     for (int k = 0; k < 7; ++k)
       if (bufs[k] != o.bufs[k]) return false;
     return xs == o.xs && ys == o.ys && n == o.n && chunks == o.chunks && debug == o.debug &&
-           dup == o.dup;
+           dup == o.dup && k1_done == o.k1_done;
   }
 };
 
@@ -91,6 +92,14 @@ struct gscan_handle {
   bool large = false;
   uint64_t wcap = 0;
   uint64_t host_cap = 0;  // d_xs/d_ys (host entry only), allocated on first use
+  // overlapped ingest: copy stream, per-chunk events, chunk extremes
+  cudaStream_t copy = nullptr;
+  cudaEvent_t ev_chunk[8] = {};
+  ExtResult* ext_parts = nullptr;
+  uint32_t* ext_off = nullptr;
+  ExtAcc* ext_pp = nullptr;       // per-chunk K1 partials (sm_count each)
+  Counters* ext_pctr = nullptr;   // per-chunk tickets
+  bool k1_done = false;           // the next run_sparse may skip K1
   std::string err;
   uint64_t launches = 0;
   bool profiling = false;
@@ -1416,7 +1425,7 @@ int sparse_enqueue(gscan_handle* h, const double* xs, const double* ys, uint32_t
                    const gscan_config& cfg) {
   const SpCtx c = sp_ctx(h, xs, ys, n, cfg.chunk_count);
   TRY(sp_seg_init(h, c));
-  TRY(sp_seg_extremes(h, c));
+  if (!h->k1_done) TRY(sp_seg_extremes(h, c));  // else h->ext came from the ingest
   TRY(sp_seg_sample(h, c));
   TRY(sp_seg_f2(h, c));
   TRY(sp_seg_plan(h, c));
@@ -1527,7 +1536,7 @@ int run_sparse(gscan_handle* h, const double* xs, const double* ys, uint32_t n,
   cudaStream_t s = h->stream;
   const bool dup_check = !h->sp_no_dup;
   // one captured graph per (input, n, config): replayed while unchanged
-  SpGraphKey key{xs, ys, n, c, h->debug, dup_check};
+  SpGraphKey key{xs, ys, n, c, h->debug, dup_check, h->k1_done};
   TRY(tree_workspace(h, std::min<uint32_t>(n, kTreeMaxN)));  // no allocation inside the capture
   const void* bufs[7] = {h->A_x, h->A_y, h->A_i, h->C_x, h->C_y, h->C_i, h->tw_pool};
   for (int k = 0; k < 7; ++k) key.bufs[k] = bufs[k];
@@ -1678,6 +1687,48 @@ int run_pipeline(gscan_handle* h, const double* xs, const double* ys, uint64_t n
     st->t_round2_ms = ev_ms(h->ev[3], h->ev[4]);
     st->t_finalize_ms = ev_ms(h->ev[4], h->ev[5]);
     st->t_total_ms = ev_ms(h->ev[0], h->ev[5]);
+  }
+  return GSCAN_OK;
+}
+
+constexpr uint64_t kIngestMinN = 4u << 20;  // below this one copy + K1 is as fast
+constexpr uint32_t kIngestChunks = 8;
+
+int ingest_overlapped(gscan_handle* h, const double* xs, const double* ys, uint64_t n) {
+  if (!h->copy) {
+    CU(cudaStreamCreateWithFlags(&h->copy, cudaStreamNonBlocking));
+    for (auto& e : h->ev_chunk) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    CU(cudaMalloc(&h->ext_parts, kIngestChunks * sizeof(ExtResult)));
+    CU(cudaMalloc(&h->ext_off, kIngestChunks * 4));
+    CU(cudaMalloc(&h->ext_pp, (size_t)kIngestChunks * h->sm_count * sizeof(ExtAcc)));
+    CU(cudaMalloc(&h->ext_pctr, kIngestChunks * sizeof(Counters)));
+    CU(cudaMemset(h->ext_pctr, 0, kIngestChunks * sizeof(Counters)));
+  }
+  // chunk boundaries on whole K1 tiles (16-byte aligned starts)
+  uint32_t off[kIngestChunks + 1];
+  for (uint32_t k = 0; k <= kIngestChunks; ++k)
+    off[k] = k == kIngestChunks ? (uint32_t)n
+                                : (uint32_t)((n * k / kIngestChunks) / kExtTile * kExtTile);
+  CU(cudaMemcpyAsync(h->ext_off, off, kIngestChunks * 4, cudaMemcpyHostToDevice, h->stream));
+  // the copy stream starts after everything already on the handle's stream
+  CU(cudaEventRecord(h->ev_chunk[0], h->stream));
+  CU(cudaStreamWaitEvent(h->copy, h->ev_chunk[0], 0));
+  for (uint32_t k = 0; k < kIngestChunks; ++k) {
+    const size_t len = (size_t)(off[k + 1] - off[k]) * 8;
+    CU(cudaMemcpyAsync(h->d_xs + off[k], xs + off[k], len, cudaMemcpyHostToDevice, h->copy));
+    CU(cudaMemcpyAsync(h->d_ys + off[k], ys + off[k], len, cudaMemcpyHostToDevice, h->copy));
+    CU(cudaEventRecord(h->ev_chunk[k], h->copy));
+  }
+  for (uint32_t k = 0; k < kIngestChunks; ++k) {
+    CU(cudaStreamWaitEvent(h->stream, h->ev_chunk[k], 0));
+    Launch L(h, "k_extremes_tma(ingest)");
+    k_extremes_tma<<<h->sm_count, kExtThreads, kExtSmem, h->stream>>>(
+        h->d_xs + off[k], h->d_ys + off[k], off[k + 1] - off[k], h->ext_pp + (size_t)k * h->sm_count,
+        h->ext_parts + k, h->ext_pctr + k);
+  }
+  {
+    Launch L(h, "k_ext_merge");
+    k_ext_merge<<<1, 32, 0, h->stream>>>(h->ext_parts, h->ext_off, kIngestChunks, h->ext);
   }
   return GSCAN_OK;
 }
@@ -1883,6 +1934,9 @@ int gscan_destroy(gscan_handle* h) {
   if (h->stream) cudaStreamSynchronize(h->stream);
   free_buffers(h);
   dfree(h->d_xs); dfree(h->d_ys);
+  dfree(h->ext_parts); dfree(h->ext_off); dfree(h->ext_pp); dfree(h->ext_pctr);
+  for (auto& e : h->ev_chunk) if (e) cudaEventDestroy(e);
+  if (h->copy) cudaStreamDestroy(h->copy);
   dfree(h->partials); dfree(h->ext); dfree(h->ctr); dfree(h->scratch64);
   dfree(h->sp_th); dfree(h->sp_cdf); dfree(h->sp_cells); dfree(h->sp_big); dfree(h->sp_bigg); dfree(h->sp_hugeg); dfree(h->sp_gcount); dfree(h->sp_side_status); dfree(h->sp_side_ticket); dfree(h->sp_side_work); dfree(h->sp_ccount); dfree(h->sp_hcount); dfree(h->sp_hist_part); dfree(h->sp_phi_part); dfree(h->sp_part_off);
   dfree(h->sp_d2); dfree(h->sp_hist); dfree(h->sp_bstart); dfree(h->sp_gbits); dfree(h->sp_glist);
@@ -2014,10 +2068,21 @@ int gscan_hull_f64(gscan_handle* h, const double* xs, const double* ys, uint64_t
     CU(cudaMalloc(&h->d_ys, (n + 1) * 8));
     h->host_cap = n;
   }
-  CU(cudaMemcpyAsync(h->d_xs, xs, n * 8, cudaMemcpyHostToDevice, h->stream));
-  CU(cudaMemcpyAsync(h->d_ys, ys, n * 8, cudaMemcpyHostToDevice, h->stream));
   uint64_t hs = 0;
-  TRY(run_pipeline(h, h->d_xs, h->d_ys, n, c, &hs, stats));
+  // Overlapped ingest: the H2D copy in chunks on the
+  // copy stream, K1 on every chunk as it lands (the only stage that does not
+  // need all of the input), a merge, and the sparse path without its K1.
+  const bool overlap = n >= kIngestMinN && sparse_eligible(h, n, c) && !h->profiling;
+  if (overlap) {
+    TRY(ingest_overlapped(h, xs, ys, n));
+    h->k1_done = true;
+  } else {
+    CU(cudaMemcpyAsync(h->d_xs, xs, n * 8, cudaMemcpyHostToDevice, h->stream));
+    CU(cudaMemcpyAsync(h->d_ys, ys, n * 8, cudaMemcpyHostToDevice, h->stream));
+  }
+  const int rc = run_pipeline(h, h->d_xs, h->d_ys, n, c, &hs, stats);
+  h->k1_done = false;
+  TRY(rc);
   if (out_len) *out_len = hs;
   if (hs > out_cap) return fail(h, GSCAN_E_CAPACITY, "hull has %llu vertices, capacity %llu",
                                 (unsigned long long)hs, (unsigned long long)out_cap);

@@ -215,7 +215,10 @@ __device__ __forceinline__ void ext_finish(ExtAcc acc, const double* __restrict_
 // CTA. Within a thread indices only grow (tile order, then pair order), as
 // ext_push requires. Needs 16-byte aligned xs, ys.
 constexpr int kExtTile = 2048;    // points per tile (16 KB of x + 16 KB of y)
-constexpr int kExtStages = 4;
+#ifndef GSCAN_EXT_STAGES
+#define GSCAN_EXT_STAGES 4
+#endif
+constexpr int kExtStages = GSCAN_EXT_STAGES;
 constexpr int kExtThreads = 512;  // 2 pairs (4 points) per thread per tile
 using ExtRing = XYRing<kExtTile, kExtStages>;
 constexpr size_t kExtSmem = ExtRing::kSmem + 64;
@@ -230,11 +233,11 @@ __global__ void __launch_bounds__(kExtThreads, 1) k_extremes_tma(const double* _
   ring.setup(ext_smem, xs, ys, n);
   ring.start();
   __syncthreads();
-  // two independent accumulators (pair u goes to acc[u]): shorter dependency
-  // chains; each still sees increasing indices
-  ExtAcc acc[2];
-  ext_init(acc[0]);
-  ext_init(acc[1]);
+  // four independent accumulators (one per point of a thread's tile share):
+  // shorter dependency chains; each still sees increasing indices
+  ExtAcc acc[4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a) ext_init(acc[a]);
   for (uint32_t k = 0; k < ring.mine; ++k) {
     ring.wait(k);
     const double2* x2 = reinterpret_cast<const double2*>(ring.tx(k));
@@ -245,14 +248,38 @@ __global__ void __launch_bounds__(kExtThreads, 1) k_extremes_tma(const double* _
     const uint32_t ia = ring.tile_start(k) + 2 * threadIdx.x, ib = ia + 2 * kExtThreads;
     ext_push(acc[0], va.x, wa.x, ia);
     ext_push(acc[1], vb.x, wb.x, ib);
-    ext_push(acc[0], va.y, wa.y, ia + 1);
-    ext_push(acc[1], vb.y, wb.y, ib + 1);
+    ext_push(acc[2], va.y, wa.y, ia + 1);
+    ext_push(acc[3], vb.y, wb.y, ib + 1);
   }
   if (blockIdx.x == gridDim.x - 1)
     for (uint32_t i = (n / kExtTile) * kExtTile + threadIdx.x; i < n; i += kExtThreads)
       ext_push(acc[0], xs[i], ys[i], i);
   ext_merge(acc[0], acc[1]);
+  ext_merge(acc[2], acc[3]);
+  ext_merge(acc[0], acc[2]);
   ext_finish(acc[0], xs, ys, partials, out, ctr);
+}
+
+// Overlapped ingest (gscan_hull_f64): K1 ran per H2D chunk (chunk c's points
+// are global indices off[c] ..); merge the chunk results in index order with
+// find_extremes' / select_anchor's rules (strict compares: on equal values
+// the earlier chunk, i.e. the lower index, keeps it).
+__global__ void k_ext_merge(const ExtResult* __restrict__ parts, const uint32_t* __restrict__ off,
+                            uint32_t nparts, ExtResult* __restrict__ out) {
+  if (threadIdx.x != 0) return;
+  ExtResult r = parts[0];
+  for (int k = 0; k < 5; ++k) r.idx[k] += off[0];
+  for (uint32_t c = 1; c < nparts; ++c) {
+    const ExtResult& p = parts[c];
+    if (p.qx[0] < r.qx[0]) { r.qx[0] = p.qx[0]; r.qy[0] = p.qy[0]; r.idx[0] = off[c] + p.idx[0]; }
+    if (p.qy[1] < r.qy[1]) { r.qx[1] = p.qx[1]; r.qy[1] = p.qy[1]; r.idx[1] = off[c] + p.idx[1]; }
+    if (p.qx[2] > r.qx[2]) { r.qx[2] = p.qx[2]; r.qy[2] = p.qy[2]; r.idx[2] = off[c] + p.idx[2]; }
+    if (p.qy[3] > r.qy[3]) { r.qx[3] = p.qx[3]; r.qy[3] = p.qy[3]; r.idx[3] = off[c] + p.idx[3]; }
+    if (p.ay < r.ay || (p.ay == r.ay && p.ax < r.ax)) {
+      r.ax = p.ax; r.ay = p.ay; r.idx[4] = off[c] + p.idx[4];
+    }
+  }
+  *out = r;
 }
 
 // ===========================================================================
