@@ -1496,7 +1496,7 @@ int sparse_dup_check(gscan_handle* h, uint32_t n) {
     Launch L(h, "k_sp_dups", h->side);
     k_sp_dups<<<h->sm_count, 1024, kSpSideSmem, h->side>>>(h->sp_dup2, h->sp_part_off, nl, h->sp_st,
                                                               h->sp_side_work + 1, side_free_sms_dups(),
-                                                              h->sp_dup_scr, h->sp_dup_scap);
+                                                              h->sp_dup_scr, h->sp_dup_scap, true);
   }
   {
     Launch L(h, "k_sp_side_check", h->side);

@@ -214,7 +214,10 @@ __device__ __forceinline__ void ext_finish(ExtAcc acc, const double* __restrict_
 // CTAs round-robin; the remainder (< one tile) is read directly by the last
 // CTA. Within a thread indices only grow (tile order, then pair order), as
 // ext_push requires. Needs 16-byte aligned xs, ys.
-constexpr int kExtTile = 2048;    // points per tile (16 KB of x + 16 KB of y)
+#ifndef GSCAN_EXT_TILE
+#define GSCAN_EXT_TILE 2048
+#endif
+constexpr int kExtTile = GSCAN_EXT_TILE;  // points per tile (2048: 16 KB of x + 16 KB of y)
 #ifndef GSCAN_EXT_STAGES
 #define GSCAN_EXT_STAGES 4
 #endif
@@ -242,14 +245,21 @@ __global__ void __launch_bounds__(kExtThreads, 1) k_extremes_tma(const double* _
     ring.wait(k);
     const double2* x2 = reinterpret_cast<const double2*>(ring.tx(k));
     const double2* y2 = reinterpret_cast<const double2*>(ring.ty(k));
-    const double2 va = x2[threadIdx.x], vb = x2[threadIdx.x + kExtThreads];
-    const double2 wa = y2[threadIdx.x], wb = y2[threadIdx.x + kExtThreads];
+    constexpr int kPairs = kExtTile / 2 / kExtThreads;
+    double2 vx[kPairs], vy[kPairs];
+#pragma unroll
+    for (int u = 0; u < kPairs; ++u) {
+      vx[u] = x2[threadIdx.x + u * kExtThreads];
+      vy[u] = y2[threadIdx.x + u * kExtThreads];
+    }
     ring.release(k);
-    const uint32_t ia = ring.tile_start(k) + 2 * threadIdx.x, ib = ia + 2 * kExtThreads;
-    ext_push(acc[0], va.x, wa.x, ia);
-    ext_push(acc[1], vb.x, wb.x, ib);
-    ext_push(acc[2], va.y, wa.y, ia + 1);
-    ext_push(acc[3], vb.y, wb.y, ib + 1);
+    const uint32_t i0 = ring.tile_start(k) + 2 * threadIdx.x;
+#pragma unroll
+    for (int u = 0; u < kPairs; ++u) {
+      const uint32_t i = i0 + 2 * u * kExtThreads;
+      ext_push(acc[(2 * u) & 3], vx[u].x, vy[u].x, i);
+      ext_push(acc[(2 * u + 1) & 3], vx[u].y, vy[u].y, i + 1);
+    }
   }
   if (blockIdx.x == gridDim.x - 1)
     for (uint32_t i = (n / kExtTile) * kExtTile + threadIdx.x; i < n; i += kExtThreads)

@@ -1816,7 +1816,7 @@ __global__ void __launch_bounds__(1024) k_sp_dups(const uint64_t* __restrict__ p
                                                  uint32_t nparts_cta, SpState* __restrict__ st,
                                                  uint32_t* __restrict__ ticket, uint32_t n_free,
                                                  uint64_t* __restrict__ gscr = nullptr,
-                                                 uint32_t gcap = 0) {
+                                                 uint32_t gcap = 0, bool discard = false) {
   extern __shared__ uint32_t s_tab[];  // kSpDupGroups x kSpDupGSlots
   __shared__ uint32_t s_next[kSpDupGroups];
   __shared__ uint32_t s_sub[kSpDupGroups][kSpDupMaxSub + 1];  // counts -> offsets
@@ -1879,6 +1879,16 @@ __global__ void __launch_bounds__(1024) k_sp_dups(const uint64_t* __restrict__ p
       dup_set_pass(parted + lo, n, tab, gt, bar, dup, full, st);
     }
     if (named_sync_or(bar, kGT, dup || full)) break;  // also publishes s_next
+    if (discard) {
+      // the partition is dead once checked: drop its whole 128-byte lines
+      // from L2 without a write-back (lines shared with a neighbouring
+      // partition stay); otherwise ~100 MB of dirty lines are written back
+      // when the next call's first pass evicts them
+      const size_t l0 = ((size_t)lo * 8 + 127) / 128, l1 = (size_t)hi * 8 / 128;
+      const char* base = reinterpret_cast<const char*>(parted);
+      for (size_t l = l0 + gt; l < l1; l += kGT)
+        asm volatile("discard.global.L2 [%0], 128;" ::"l"(base + l * 128) : "memory");
+    }
     p = s_next[grp];
   }
   if (dup) { atomicAdd(&st->dups, 1u); atomicOr(&st->fail, kSpFailDup); }
