@@ -268,17 +268,26 @@ __device__ __forceinline__ int tree_scan_rows(const TreeRows<T>& r, int top, uin
   int k = 0;
   double px = 0, py = 0;
   if (cnt > 0) { px = r.X[r.at(kTreePC)]; py = r.Y[r.at(kTreePC)]; }
+  // One loop shape for pops and pushes (the lanes of a warp pop and push
+  // independently; separate paths cost a warp both of them per iteration).
+  // Both candidates for the step's one new value -- the new second element
+  // of a pop (row top - 3) and the next staged point of a push (row kTreePC
+  // + k + 1) -- are loaded before the turn test, so their latency overlaps
+  // it. Pops that reach B or the chain below it take the branch with the
+  // global loads.
   while (k < cnt) {
-    if (h2 && !left_turn(s2x, s2y, s1x, s1y, px, py)) {
+    const int a3 = r.at(max(top - 3, 0));
+    const int an = r.at(min(kTreePC + k + 1, kTreeRows - 1));
+    const double l3x = r.X[a3], l3y = r.Y[a3];
+    const double lnx = r.X[an], lny = r.Y[an];
+    const bool pop = h2 && !left_turn(s2x, s2y, s1x, s1y, px, py);
+    if (pop && top < 3 && (top != 2 || B != kNone)) {
       s1x = s2x; s1y = s2y;
-      if (top >= 3) {  // common case: the new second element is a row
-        --top;
-        s2x = r.X[r.at(top - 2)]; s2y = r.Y[r.at(top - 2)];
-      } else if (top == 2) {  // new s1 = row 0, s2 = B
+      if (top == 2) {  // new s1 = row 0, s2 = B
         top = 1;
         q2 = B;
-        h2 = B != kNone;
-        if (h2) { s2x = R_x[B]; s2y = R_y[B]; }
+        h2 = true;
+        s2x = R_x[B]; s2y = R_y[B];
       } else if (top == 1) {  // new s1 = B, s2 = parent[B]
         top = 0;
         q2 = parent[B];
@@ -292,21 +301,31 @@ __device__ __forceinline__ int tree_scan_rows(const TreeRows<T>& r, int top, uin
       }
       continue;
     }
-    const int a = r.at(top);
-    const uint32_t pp = r.P[r.at(kTreePC + k)];
-    on_push(k, pp, top >= 1 ? r.P[r.at(top - 1)] : B);
-    r.X[a] = px;
-    r.Y[a] = py;
-    r.P[a] = pp;
-    r.K[a] = (uint8_t)k;
-    if (top < lo_own) lo_own = top;
-    ++top;
+    if (!pop) {  // push p onto row top (<= kTreePC + k: the rows loaded above stay intact)
+      const int a = r.at(top);
+      const uint32_t pp = r.P[r.at(kTreePC + k)];
+      on_push(k, pp, top >= 1 ? r.P[r.at(top - 1)] : B);
+      r.X[a] = px;
+      r.Y[a] = py;
+      r.P[a] = pp;
+      r.K[a] = (uint8_t)k;
+      if (top < lo_own) lo_own = top;
+    }
+    if (pop) {  // the new second element: row top - 3 (none when top == 2: B is kNone)
+      h2 = top >= 3;
+      --top;
+      s1x = s2x; s1y = s2y;
+      s2x = l3x; s2y = l3y;
+    } else {
+      ++top;
+      s2x = s1x; s2y = s1y;
+      h2 = h1;
+      s1x = px; s1y = py;
+      h1 = true;
+      ++k;
+      px = lnx; py = lny;
+    }
     if (top == 1) q2 = B;
-    s2x = s1x; s2y = s1y;
-    h2 = h1;
-    s1x = px; s1y = py;
-    h1 = true;
-    if (++k < cnt) { px = r.X[r.at(kTreePC + k)]; py = r.Y[r.at(kTreePC + k)]; }
   }
   return top;
 }
@@ -480,6 +499,9 @@ __global__ void __launch_bounds__(kTreeThreads, 1) k_gr_mid(
   const int t = threadIdx.x;
   long long t_start = clock64();
   if (info[0]) return;  // declined, or level 0 or 1 did not shrink
+#ifdef GSCAN_TREE_PRINT
+  __shared__ long long s_clk[64];
+#endif
   if (t == 0) {
     s_nq[0] = info[4];
     s_nq[1] = info[11];
@@ -501,16 +523,31 @@ __global__ void __launch_bounds__(kTreeThreads, 1) k_gr_mid(
       if (c < L.nch) {
         const uint32_t lo = c * L.cs;
         const int cnt = (int)min(L.cs, L.nq - lo);
+#ifdef GSCAN_TREE_PRINT
+        if (t == 0) s_clk[j * 8 + 0] = clock64() - t_start;
+#endif
         tree_stage<kTreeThreads>(r, L.Qp, L.Qx, L.Qy, lo, cnt);
+#ifdef GSCAN_TREE_PRINT
+        if (t == 0) s_clk[j * 8 + 1] = clock64() - t_start;
+#endif
         uint32_t B = kNone;
         int lo_own = kTreeRows;
         const int top = tree_scan_rows<kTreeThreads>(r, 0, B, cnt, w.parent, R_x, R_y, lo_own,
                                                      TreeNoPush{});
+#ifdef GSCAN_TREE_PRINT
+        if (t == 0) s_clk[j * 8 + 2] = clock64() - t_start;
+#endif
         tree_put_chain<kTreeThreads>(r, top, lo, false, w);
         L.off[c] = (uint32_t)top;
+#ifdef GSCAN_TREE_PRINT
+        if (t == 0) s_clk[j * 8 + 3] = clock64() - t_start;
+#endif
       }
     }
     __syncthreads();
+#ifdef GSCAN_TREE_PRINT
+    if (t == 0) s_clk[j * 8 + 4] = clock64() - t_start;
+#endif
     const uint32_t total = tree_scan(L.off, L.nch, s_w, &s_carry);
     if (t == 0) {
       L.off[L.nch] = total;
@@ -523,6 +560,9 @@ __global__ void __launch_bounds__(kTreeThreads, 1) k_gr_mid(
     }
     __syncthreads();
     if (s_bad) break;
+#ifdef GSCAN_TREE_PRINT
+    if (t == 0) s_clk[j * 8 + 5] = clock64() - t_start;
+#endif
     for (uint32_t c = t >> 5; c < L.nch; c += kTreeThreads / 32) tree_gather_chunk(w, j, c);
     __syncthreads();
     if (t == 0) {
@@ -694,6 +734,12 @@ __global__ void __launch_bounds__(kTreeThreads, 1) k_gr_mid(
   if (t == 0) {
     info[3] = K;
     info[16] = (uint32_t)(clock64() - t_start);
+#ifdef GSCAN_TREE_PRINT
+    for (int j = 2; j < 4; ++j) printf("lvl %d: stage %lld-%lld scan -%lld put -%lld | all chunks %lld | offs scan %lld | next level %u\n", j, s_clk[j*8], s_clk[j*8+1], s_clk[j*8+2], s_clk[j*8+3], s_clk[j*8+4], s_clk[j*8+5], info[20 + j]);
+    printf("mid K=%d nq %u %u %u %u %u %u | up2 %u up3 %u up4 %u | upend %u top %u | down %u %u %u | end %u\n", K,
+           s_nq[0], s_nq[1], s_nq[2], s_nq[3], s_nq[4], s_nq[5], info[22], info[23], info[24], info[8], info[9],
+           info[35], info[34], info[33], info[16]);
+#endif
   }
 }
 
