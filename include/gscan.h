@@ -154,63 +154,68 @@ int gscan_shard_round1(gscan_handle* h, const double* d_xs, const double* d_ys, 
 /* ---- sharded sparse path (paper_1508_05931_b200/distributed.py) ----
  *
  * One handle per rank; rank r owns the contiguous shard [offset, offset + n)
- * of the global input (device pointers). The host runs the phases in order
- * and does the collectives between them (the exchanges are KB-MB sized):
- *   1 gscan_dist_begin   global extremes in (from gscan_shard_extremes of all
- *                        ranks); out: sample cells (uint32[2048])     -> sum
- *   2 gscan_dist_hist    cells in; out: bucket histogram (uint32[49152]) -> sum,
- *                        this rank's farthest point (gscan_dist_best)   -> best,
- *                        round-1 survivors                               -> sum
- *   3 gscan_dist_plan    histogram, P_l and the fail bits in; out: points of
- *                        P_l's bucket ordered before it                  -> sum
- *   4 gscan_dist_phi     that count in; out: walk-angle bucket maxima
- *                        (uint32[49152]) -> max, phi range -> min/max, number
- *                        of gathered points; gscan_dist_export(.., 0, ..)
- *                        then writes them as {x, y, global index, bucket} -> rank 0
- *   5 gscan_dist_slices  rank 0: all gathered points (X/Y index 0 = the anchor,
- *                        1.. the gathered points sorted by global index);
- *                        out: prefix maxima (uint32[49152])              -> broadcast
- *   6 gscan_dist_cand    prefix maxima in; out: candidate count;
- *                        gscan_dist_export(.., 1, ..) writes them        -> rank 0
- *   7 gscan_dist_finish  rank 0: candidates appended to X/Y; walk, certificate,
- *                        Graham; out: hull as X/Y indices (the caller maps
- *                        them to global indices)
- *   duplicates: gscan_dist_dup_local (after phase 4) partitions this rank's
- *   64-bit coordinate hashes by their top 11 bits; the host sends partition
- *   range k to rank k; gscan_dist_dup_check checks the received blocks.
- * Any nonzero fail word (or a duplicate) means the caller must take the
- * exact survivor-gather path instead; results are otherwise identical to
- * gscan_hull_f64 on the concatenated input. */
-typedef struct gscan_dist_best {
-    uint64_t d2_bits;  /* dist2 to the anchor (IEEE bits; compares as uint64) */
-    uint64_t idx;      /* global index, UINT64_MAX when the shard has no survivor */
-    uint32_t ties;     /* points of the shard at that distance */
-    uint32_t pad;
-    double x, y;
-} gscan_dist_best;
+ * of the global input (device pointers). The phases are enqueue-only:
+ * nothing waits for the device. Each phase
+ * writes this rank's scalars into a fixed record (gscan_dist_bufs.rec,
+ * rec_len int64 words); the caller all-gathers the records into
+ * gscan_dist_bufs.recs (R x rec_len) and runs the fixed-size collectives in
+ * place on the handle's buffers, all on the handle's stream (NCCL), and the
+ * next phase combines them on the device. The host reads back only the sizes
+ * of the variable-size exchanges, at three points per call:
+ *   gscan_dist_enq_begin       K1 on the shard            rec -> all-gather
+ *   gscan_dist_enq_sample      global extremes; sample    cells -> sum
+ *   gscan_dist_enq_f2          F2                         hist -> sum, rec -> all-gather
+ *   gscan_dist_enq_plan        global P_l; P_l's rank     rec -> all-gather
+ *   gscan_dist_enq_f3          F3                         phimax -> max, rec -> all-gather
+ *   gscan_dist_enq_dup_local   hashes by partition        counts -> all-to-all
+ *   (host sync 1: fail word, gathered counts, hash block sizes)
+ *   hashes -> all-to-all; gscan_dist_enq_dup_check; gscan_dist_enq_export(0)
+ *   -> rank 0; rank 0: gscan_dist_enq_slices; pref -> broadcast
+ *   gscan_dist_enq_cand        F4                         rec -> all-gather
+ *   (host sync 2: fail word, candidate counts)
+ *   gscan_dist_enq_export(1) -> rank 0; rank 0: gscan_dist_root_finish
+ *   (host sync 3: rank 0's status broadcast)
+ *   status 1 (certificate not proved): rlo, rx, ry of rank 0 -> broadcast;
+ *   gscan_dist_enq_verify on every rank (distributed F6), rec -> all-gather.
+ * gscan_dist_buffers is valid after gscan_dist_enq_begin. */
+typedef struct gscan_dist_bufs {
+    int64_t* rec;           /* this rank's record (rec_len words) */
+    int64_t* recs;          /* all ranks' records (max_ranks x rec_len) */
+    int64_t* ext;           /* combined extremes: global index (5), x bits (5), y bits (5) */
+    uint32_t* cells;        /* sample cells (cells_n) */
+    uint32_t* hist;         /* bucket histogram (buckets) */
+    uint32_t* phimax;       /* walk-angle maxima, ordered-float encoding (buckets) */
+    uint32_t* pref;         /* prefix maxima + rank 0's fail word (buckets + 1) */
+    uint32_t* part_counts;  /* hashes per partition (parts) */
+    uint64_t* parted;       /* this rank's hashes, partition-major */
+    uint32_t* rlo;          /* round-2 output offsets per bucket (buckets + 1; rank 0) */
+    double* rx;             /* round-2 output coordinates (rank 0) */
+    double* ry;
+    void* stream;           /* the handle's cudaStream_t */
+    uint64_t rec_len, max_ranks, buckets, cells_n, parts;
+} gscan_dist_bufs;
 
-int gscan_dist_begin(gscan_handle* h, const double* d_xs, const double* d_ys, uint64_t n,
-                     uint64_t offset, const gscan_extremes* global, const gscan_config* cfg,
-                     uint32_t* d_cells);
-int gscan_dist_hist(gscan_handle* h, const uint32_t* d_cells, uint32_t* d_hist,
-                    gscan_dist_best* best, uint64_t* n1);
-int gscan_dist_plan(gscan_handle* h, const uint32_t* d_hist, const gscan_dist_best* pl,
-                    uint32_t fail_bits, uint64_t* l_below, uint32_t* fail_out);
-int gscan_dist_phi(gscan_handle* h, uint64_t l_below, uint32_t* d_phimax, uint32_t* phi_range,
-                   uint64_t* n_g, uint32_t* fail_out);
-int gscan_dist_export(gscan_handle* h, int candidates, double* d_x, double* d_y, uint32_t* d_idx,
-                      uint32_t* d_b, uint64_t* n_out);
-int gscan_dist_slices(gscan_handle* h, const double* d_X, const double* d_Y, uint64_t n_g,
-                      const uint32_t* d_gb, uint64_t l_pos, const uint32_t* d_phimax,
-                      const uint32_t* phi_range, uint32_t* d_prefmax, uint32_t* fail_out);
-int gscan_dist_cand(gscan_handle* h, const uint32_t* d_prefmax, uint64_t* n_c, uint32_t* fail_out);
-int gscan_dist_finish(gscan_handle* h, const double* d_X, const double* d_Y, uint64_t n_g,
-                      uint64_t n_c, const uint32_t* d_cb, uint32_t* d_hull, uint64_t hull_cap,
-                      uint64_t* hull_n, uint64_t* n_r, uint32_t* fail_out);
-int gscan_dist_dup_local(gscan_handle* h, uint32_t* d_part_counts, uint64_t* d_parted,
-                         uint64_t* n_hash);
-int gscan_dist_dup_check(gscan_handle* h, const uint64_t* d_recv, uint64_t n_recv,
-                         const uint32_t* d_counts, uint32_t R, uint32_t* dup_found);
+int gscan_dist_enq_begin(gscan_handle* h, const double* d_xs, const double* d_ys, uint64_t n,
+                         uint64_t offset, const gscan_config* cfg);
+int gscan_dist_buffers(gscan_handle* h, gscan_dist_bufs* bufs);
+int gscan_dist_enq_sample(gscan_handle* h, uint32_t R);
+int gscan_dist_enq_f2(gscan_handle* h);
+int gscan_dist_enq_plan(gscan_handle* h, uint32_t R, uint64_t n_global);
+int gscan_dist_enq_f3(gscan_handle* h, uint32_t R);
+int gscan_dist_enq_dup_local(gscan_handle* h, uint32_t R);
+int gscan_dist_enq_dup_check(gscan_handle* h, const uint64_t* d_recv, uint64_t n_recv,
+                             const uint32_t* d_counts, uint32_t R);
+int gscan_dist_enq_export(gscan_handle* h, int candidates, double* d_x, double* d_y,
+                          uint32_t* d_idx, uint32_t* d_b);
+int gscan_dist_enq_slices(gscan_handle* h, const double* d_X, const double* d_Y, uint64_t n_g,
+                          const uint32_t* d_gb, const int64_t* d_gidx, uint64_t M);
+int gscan_dist_enq_cand(gscan_handle* h);
+int gscan_dist_root_finish(gscan_handle* h, const double* d_X, const double* d_Y, uint64_t n_g,
+                           uint64_t n_c, const uint32_t* d_cb, uint64_t M, uint32_t* d_hull,
+                           uint64_t hull_cap, uint64_t* hull_n, uint64_t* n_r, uint32_t* status,
+                           uint32_t* fail_out);
+int gscan_dist_enq_verify(gscan_handle* h, const uint32_t* d_rlo, const double* d_Rx,
+                          const double* d_Ry);
 
 /* ---- device self-checks ---- */
 

@@ -61,9 +61,13 @@ class gscan_extremes(C.Structure):
     _fields_ = [("idx", C.c_uint64 * 5), ("x", C.c_double * 5), ("y", C.c_double * 5)]
 
 
-class gscan_dist_best(C.Structure):
-    _fields_ = [("d2_bits", C.c_uint64), ("idx", C.c_uint64), ("ties", C.c_uint32),
-                ("pad", C.c_uint32), ("x", C.c_double), ("y", C.c_double)]
+class gscan_dist_bufs(C.Structure):
+    _fields_ = [("rec", C.c_void_p), ("recs", C.c_void_p), ("ext", C.c_void_p),
+                ("cells", C.c_void_p), ("hist", C.c_void_p), ("phimax", C.c_void_p),
+                ("pref", C.c_void_p), ("part_counts", C.c_void_p), ("parted", C.c_void_p),
+                ("rlo", C.c_void_p), ("rx", C.c_void_p), ("ry", C.c_void_p), ("stream", C.c_void_p),
+                ("rec_len", C.c_uint64), ("max_ranks", C.c_uint64), ("buckets", C.c_uint64),
+                ("cells_n", C.c_uint64), ("parts", C.c_uint64)]
 
 
 # sparse-path sizes the sharded phases exchange (csrc/sparse.cuh)
@@ -71,6 +75,7 @@ SP_CELLS = 2048
 SP_BUCKETS = 48 * 1024
 SP_PARTS = 2048
 SP_FAIL_TIE, SP_FAIL_FEW, SP_FAIL_MANY = 1, 128, 256
+SP_FAIL_CAP = 32
 
 # Every symbol include/gscan.h declares, with its ctypes signature.
 _P = C.c_void_p
@@ -95,20 +100,20 @@ SIGNATURES = {
     "gscan_device_atan2": (C.c_int, [_P, _P, _P, _P, _U64]),
     "gscan_shard_extremes": (C.c_int, [_P, _P, _P, _U64, C.POINTER(gscan_extremes)]),
     "gscan_shard_round1": (C.c_int, [_P, _P, _P, _U64, C.POINTER(gscan_extremes), _P, _U64P]),
-    "gscan_dist_begin": (C.c_int, [_P, _P, _P, _U64, _U64, C.POINTER(gscan_extremes),
-                                   C.POINTER(gscan_config), _P]),
-    "gscan_dist_hist": (C.c_int, [_P, _P, _P, C.POINTER(gscan_dist_best), _U64P]),
-    "gscan_dist_plan": (C.c_int, [_P, _P, C.POINTER(gscan_dist_best), C.c_uint32, _U64P,
-                                  C.POINTER(C.c_uint32)]),
-    "gscan_dist_phi": (C.c_int, [_P, _U64, _P, C.POINTER(C.c_uint32), _U64P, C.POINTER(C.c_uint32)]),
-    "gscan_dist_export": (C.c_int, [_P, C.c_int, _P, _P, _P, _P, _U64P]),
-    "gscan_dist_slices": (C.c_int, [_P, _P, _P, _U64, _P, _U64, _P, C.POINTER(C.c_uint32), _P,
-                                    C.POINTER(C.c_uint32)]),
-    "gscan_dist_cand": (C.c_int, [_P, _P, _U64P, C.POINTER(C.c_uint32)]),
-    "gscan_dist_finish": (C.c_int, [_P, _P, _P, _U64, _U64, _P, _P, _U64, _U64P, _U64P,
-                                    C.POINTER(C.c_uint32)]),
-    "gscan_dist_dup_local": (C.c_int, [_P, _P, _U64P, _U64P]),
-    "gscan_dist_dup_check": (C.c_int, [_P, _P, _U64, _P, C.c_uint32, C.POINTER(C.c_uint32)]),
+    "gscan_dist_enq_begin": (C.c_int, [_P, _P, _P, _U64, _U64, C.POINTER(gscan_config)]),
+    "gscan_dist_buffers": (C.c_int, [_P, C.POINTER(gscan_dist_bufs)]),
+    "gscan_dist_enq_sample": (C.c_int, [_P, C.c_uint32]),
+    "gscan_dist_enq_f2": (C.c_int, [_P]),
+    "gscan_dist_enq_plan": (C.c_int, [_P, C.c_uint32, _U64]),
+    "gscan_dist_enq_f3": (C.c_int, [_P, C.c_uint32]),
+    "gscan_dist_enq_dup_local": (C.c_int, [_P, C.c_uint32]),
+    "gscan_dist_enq_dup_check": (C.c_int, [_P, _P, _U64, _P, C.c_uint32]),
+    "gscan_dist_enq_export": (C.c_int, [_P, C.c_int, _P, _P, _P, _P]),
+    "gscan_dist_enq_slices": (C.c_int, [_P, _P, _P, _U64, _P, _P, _U64]),
+    "gscan_dist_enq_cand": (C.c_int, [_P]),
+    "gscan_dist_root_finish": (C.c_int, [_P, _P, _P, _U64, _U64, _P, _U64, _P, _U64, _U64P, _U64P,
+                                         C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]),
+    "gscan_dist_enq_verify": (C.c_int, [_P, _P, _P, _P]),
     "gscan_status_string": (C.c_char_p, [C.c_int]),
     "gscan_last_error": (C.c_char_p, [_P]),
     "gscan_last_launch_count": (_U64, [_P]),

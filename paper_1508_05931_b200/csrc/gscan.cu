@@ -206,6 +206,11 @@ struct gscan_handle {
   uint32_t *sp_gs = nullptr, *sp_gsz = nullptr, *dist_ctr = nullptr, *dist_pm = nullptr,
            *dist_hc = nullptr;
   uint64_t* dist_lb = nullptr;
+  // device-side data plane (gscan_dist_enq_*): this rank's record, the
+  // gathered records of all ranks, the combined extremes, partition counts
+  // and the prefix-maxima broadcast block
+  int64_t *dist_rec = nullptr, *dist_recs = nullptr, *dist_ext = nullptr;
+  uint32_t *dist_pc = nullptr, *dist_pref = nullptr;
 };
 
 namespace {
@@ -1765,6 +1770,12 @@ int dist_init(gscan_handle* h) {
   CU(cudaMalloc(&h->dist_pm, ((size_t)kSpParts * kDistMaxRanks + 2) * 4));
   CU(cudaMalloc(&h->dist_hc, kDistMaxRanks * 4));
   CU(cudaMalloc(&h->dist_lb, kDistMaxRanks * 8));
+  CU(cudaMalloc(&h->dist_rec, kDistRecLen * 8));
+  CU(cudaMalloc(&h->dist_recs, (size_t)kDistMaxRanks * kDistRecLen * 8));
+  CU(cudaMalloc(&h->dist_ext, 16 * 8));
+  CU(cudaMalloc(&h->dist_pc, kSpParts * 4));
+  CU(cudaMalloc(&h->dist_pref, (kSpBuckets + 1) * 4));
+  CU(cudaMemset(h->dist_rec, 0, kDistRecLen * 8));
   return GSCAN_OK;
 }
 
@@ -1788,13 +1799,6 @@ int dist_slices_ensure(gscan_handle* h, const SpCtx& c) {
   CU(cudaMalloc(&h->sp_seghi, (c.nslices + 2) * 4));
   h->sp_seg_cap = c.nslices + 2;
   h->sp_graph_ok = false;
-  return GSCAN_OK;
-}
-
-int dist_read_state(gscan_handle* h) {
-  CU(cudaMemcpyAsync(h->h_sp, h->sp_st, sizeof(SpState), cudaMemcpyDeviceToHost, h->stream));
-  TRY(sync_counters(h));
-  if (h->sp_debug) sp_debug_print(h, "[dist]");
   return GSCAN_OK;
 }
 
@@ -1951,6 +1955,7 @@ int gscan_destroy(gscan_handle* h) {
   dfree(h->tw_pool);
   dfree(h->sp_gs); dfree(h->sp_thr); dfree(h->sp_gsz); dfree(h->dist_ctr); dfree(h->dist_pm); dfree(h->dist_hc);
   dfree(h->dist_lb);
+  dfree(h->dist_rec); dfree(h->dist_recs); dfree(h->dist_ext); dfree(h->dist_pc); dfree(h->dist_pref);
   if (h->h_out) cudaFreeHost(h->h_out);
   for (auto& e : h->ev) if (e) cudaEventDestroy(e);
   for (auto& k : h->ktimes) { cudaEventDestroy(k.a); cudaEventDestroy(k.b); }
@@ -2243,17 +2248,21 @@ int gscan_shard_round1(gscan_handle* h, const double* d_xs, const double* d_ys, 
   return GSCAN_OK;
 }
 
-int gscan_dist_begin(gscan_handle* h, const double* d_xs, const double* d_ys, uint64_t n,
-                     uint64_t offset, const gscan_extremes* global, const gscan_config* cfg,
-                     uint32_t* d_cells) {
-  if (!h || !global || !cfg || !d_cells) return GSCAN_E_INVALID;
+// ---- device-side data plane: enqueue-only phases (include/gscan.h) ----
+// Nothing below waits for the device; the caller runs the collectives on
+// the handle's stream between the phases and reads sizes back only where a
+// variable-size exchange needs them.
+
+int gscan_dist_enq_begin(gscan_handle* h, const double* d_xs, const double* d_ys, uint64_t n,
+                         uint64_t offset, const gscan_config* cfg) {
+  if (!h || !cfg) return GSCAN_E_INVALID;
   TRY(validate(h, n, *cfg));
   if (offset + n >= 0xffffffffull) return fail(h, GSCAN_E_TOO_LARGE, "global index beyond 2^32-2");
   CU(cudaSetDevice(h->device));
   TRY(reserve(h, n));
   TRY(sparse_init(h));
   TRY(dist_init(h));
-  h->h_sp->M = 0;  // a previous call's global count must not size this call's slices
+  h->h_sp->M = 0;
   const uint64_t nslices = 2 * std::min<uint64_t>(cfg->chunk_count, n);
   if (nslices + 2 > h->sp_seg_cap) {
     dfree(h->sp_seglo);
@@ -2270,124 +2279,171 @@ int gscan_dist_begin(gscan_handle* h, const double* d_xs, const double* d_ys, ui
   h->dist_chunks = cfg->chunk_count;
   const SpCtx c = dist_ctx(h);
   TRY(sp_seg_init(h, c));
-  ExtResult q{};
-  for (int k = 0; k < 4; ++k) { q.idx[k] = (uint32_t)global->idx[k]; q.qx[k] = global->x[k]; q.qy[k] = global->y[k]; }
-  q.idx[4] = (uint32_t)global->idx[4];
-  q.ax = global->x[4];
-  q.ay = global->y[4];
-  CU(cudaMemcpyAsync(h->ext, &q, sizeof q, cudaMemcpyHostToDevice, c.s));
+  TRY(sp_seg_extremes(h, c));
+  k_dist_rec_ext<<<1, 32, 0, c.s>>>(h->ext, c.base, h->dist_rec);
+  CU(cudaGetLastError());
+  return GSCAN_OK;
+}
+
+int gscan_dist_buffers(gscan_handle* h, gscan_dist_bufs* b) {
+  if (!h || !b) return GSCAN_E_INVALID;
+  if (!h->dist_rec) return fail(h, GSCAN_E_INVALID, "gscan_dist_buffers before gscan_dist_enq_begin");
+  b->rec = h->dist_rec;
+  b->recs = h->dist_recs;
+  b->ext = h->dist_ext;
+  b->cells = h->sp_cells;
+  b->hist = h->sp_hist;
+  b->phimax = h->sp_phimax;
+  b->pref = h->dist_pref;
+  b->part_counts = h->dist_pc;
+  b->parted = h->sp_dup2;
+  b->rlo = h->sp_rlo;
+  b->rx = h->A_x;
+  b->ry = h->A_y;
+  b->stream = h->stream;
+  b->rec_len = kDistRecLen;
+  b->max_ranks = kDistMaxRanks;
+  b->buckets = kSpBuckets;
+  b->cells_n = kSpCells;
+  b->parts = kSpParts;
+  return GSCAN_OK;
+}
+
+int gscan_dist_enq_sample(gscan_handle* h, uint32_t R) {
+  if (!h || R == 0 || R > kDistMaxRanks || !h->dist_rec) return GSCAN_E_INVALID;
+  const SpCtx c = dist_ctx(h);
+  k_dist_apply_ext<<<1, 32, 0, c.s>>>(h->dist_recs, R, h->ext, h->dist_ext);
   TRY(sp_seg_sample(h, c));
-  CU(cudaMemcpyAsync(d_cells, h->sp_cells, kSpCells * 4, cudaMemcpyDeviceToDevice, c.s));
-  CU(cudaStreamSynchronize(c.s));
+  CU(cudaGetLastError());
   return GSCAN_OK;
 }
 
-int gscan_dist_hist(gscan_handle* h, const uint32_t* d_cells, uint32_t* d_hist,
-                    gscan_dist_best* best, uint64_t* n1) {
-  if (!h || !d_cells || !d_hist || !best || !n1) return GSCAN_E_INVALID;
+int gscan_dist_enq_f2(gscan_handle* h) {
+  if (!h || !h->dist_rec) return GSCAN_E_INVALID;
   const SpCtx c = dist_ctx(h);
-  CU(cudaMemcpyAsync(h->sp_cells, d_cells, kSpCells * 4, cudaMemcpyDeviceToDevice, c.s));
   TRY(sp_seg_f2(h, c));
-  CU(cudaMemcpyAsync(d_hist, h->sp_hist, kSpBuckets * 4, cudaMemcpyDeviceToDevice, c.s));
-  TRY(dist_read_state(h));
-  const SpState& sp = *h->h_sp;
-  const bool have = sp.l_idx != 0xffffffffu;
-  best->d2_bits = sp.d2max;
-  best->idx = have ? (uint64_t)h->dist_base + sp.l_idx : ~0ull;
-  best->ties = have ? sp.ties : 0;
-  best->pad = 0;
-  best->x = sp.lx;
-  best->y = sp.ly;
-  *n1 = h->h_ctr->n1;
+  k_dist_rec_f2<<<1, 32, 0, c.s>>>(h->sp_st, h->ctr, c.base, h->dist_rec);
+  CU(cudaGetLastError());
   return GSCAN_OK;
 }
 
-int gscan_dist_plan(gscan_handle* h, const uint32_t* d_hist, const gscan_dist_best* pl,
-                    uint32_t fail_bits, uint64_t* l_below, uint32_t* fail_out) {
-  if (!h || !d_hist || !pl || !l_below || !fail_out) return GSCAN_E_INVALID;
+int gscan_dist_enq_plan(gscan_handle* h, uint32_t R, uint64_t n_global) {
+  if (!h || R == 0 || R > kDistMaxRanks || !h->dist_rec) return GSCAN_E_INVALID;
   const SpCtx c = dist_ctx(h);
-  CU(cudaMemcpyAsync(h->sp_hist, d_hist, kSpBuckets * 4, cudaMemcpyDeviceToDevice, c.s));
-  k_sp_set_pl<<<1, 1, 0, c.s>>>(h->sp_st, pl->d2_bits, (uint32_t)pl->idx, pl->ties, pl->x, pl->y,
-                                fail_bits);
+  k_dist_apply_best<<<1, 32, 0, c.s>>>(h->dist_recs, R, n_global, h->sp_st);
   TRY(sp_seg_plan(h, c));
-  TRY(dist_read_state(h));
-  *l_below = h->h_sp->l_below;
-  *fail_out = dist_fail(h);
+  k_dist_rec_plan<<<1, 32, 0, c.s>>>(h->sp_st, h->dist_rec);
+  CU(cudaGetLastError());
   return GSCAN_OK;
 }
 
-int gscan_dist_phi(gscan_handle* h, uint64_t l_below, uint32_t* d_phimax, uint32_t* phi_range,
-                   uint64_t* n_g, uint32_t* fail_out) {
-  if (!h || !d_phimax || !phi_range || !n_g || !fail_out) return GSCAN_E_INVALID;
+int gscan_dist_enq_f3(gscan_handle* h, uint32_t R) {
+  if (!h || R == 0 || R > kDistMaxRanks || !h->dist_rec) return GSCAN_E_INVALID;
   const SpCtx c = dist_ctx(h);
-  k_sp_set_u32<<<1, 1, 0, c.s>>>(&h->sp_st->l_below, (uint32_t)l_below);
+  k_dist_apply_plan<<<1, 32, 0, c.s>>>(h->dist_recs, R, h->sp_st);
   TRY(sp_seg_f3(h, c));
-  CU(cudaMemcpyAsync(d_phimax, h->sp_phimax, kSpBuckets * 4, cudaMemcpyDeviceToDevice, c.s));
-  TRY(dist_read_state(h));
-  const SpState& sp = *h->h_sp;
-  phi_range[0] = sp.phi_lo;
-  phi_range[1] = sp.phi_hi;
-  *n_g = sp.n_g;
-  *fail_out = dist_fail(h);
+  k_dist_rec_f3<<<1, 32, 0, c.s>>>(h->sp_st, h->dist_rec);
+  CU(cudaGetLastError());
   return GSCAN_OK;
 }
 
-int gscan_dist_export(gscan_handle* h, int candidates, double* d_x, double* d_y, uint32_t* d_idx,
-                      uint32_t* d_b, uint64_t* n_out) {
-  if (!h || !n_out) return GSCAN_E_INVALID;
+int gscan_dist_enq_dup_local(gscan_handle* h, uint32_t R) {
+  if (!h || R == 0 || R > kDistMaxRanks || !h->dist_rec) return GSCAN_E_INVALID;
+  const SpCtx c = dist_ctx(h);
+  const uint32_t nl = 2 * c.G;
+  k_dist_apply_f3<<<1, 32, 0, c.s>>>(h->dist_recs, R, h->sp_st);
+  TRY(scan_u32(h, h->sp_part_off, kSpParts * nl, h->sp_part_off));
+  CU(cudaMemsetAsync(h->sp_side_work, 0, 2 * sizeof(uint32_t), c.s));
+  k_sp_dup_part<false><<<h->sm_count, 1024, kSpSideSmem, c.s>>>(h->sp_dup, h->sp_hcount, c.cap / 2, nl,
+                                                        h->sp_part_off, h->sp_st, h->sp_dup2,
+                                                        h->sp_side_work, 0u, nullptr);
+  k_dist_part_totals<<<(kSpParts + 255) / 256, 256, 0, c.s>>>(h->sp_part_off, nl, h->dist_pc);
+  CU(cudaGetLastError());
+  return GSCAN_OK;
+}
+
+int gscan_dist_enq_dup_check(gscan_handle* h, const uint64_t* d_recv, uint64_t n_recv,
+                             const uint32_t* d_counts, uint32_t R) {
+  if (!h || !d_counts || R == 0 || R > kDistMaxRanks || !h->dist_rec) return GSCAN_E_INVALID;
+  const SpCtx c = dist_ctx(h);
+  if (n_recv > (uint64_t)h->sp_grid * sparse_region_cap(h, h->dist_n)) {
+    // more hashes than this rank's regions hold (uneven shards): a decline
+    // every rank learns from the next record exchange
+    k_dist_set_fail<<<1, 32, 0, c.s>>>(h->sp_st, kSpFailCap, 13u);
+    return GSCAN_OK;
+  }
+  k_sp_recv_plan<<<(kSpParts * R + 255) / 256, 256, 0, c.s>>>(d_counts, R, h->dist_pm, h->dist_hc,
+                                                               h->dist_lb);
+  TRY(scan_u32(h, h->dist_pm, kSpParts * R, h->dist_pm));
+  CU(cudaMemsetAsync(h->sp_side_work, 0, 2 * sizeof(uint32_t), c.s));
+  k_sp_dup_part<false><<<h->sm_count, 1024, kSpSideSmem, c.s>>>(d_recv, h->dist_hc, 0u, R, h->dist_pm,
+                                                        h->sp_st, h->sp_dup, h->sp_side_work, 0u,
+                                                        h->dist_lb);
+  k_sp_dups<<<h->sm_count, 1024, kSpSideSmem, c.s>>>(h->sp_dup, h->dist_pm, R, h->sp_st,
+                                                     h->sp_side_work + 1, 0u, h->sp_dup_scr,
+                                                     h->sp_dup_scap);
+  CU(cudaGetLastError());
+  return GSCAN_OK;
+}
+
+int gscan_dist_enq_export(gscan_handle* h, int candidates, double* d_x, double* d_y, uint32_t* d_idx,
+                          uint32_t* d_b) {
+  if (!h || !h->dist_rec) return GSCAN_E_INVALID;
   const SpCtx c = dist_ctx(h);
   CU(cudaMemsetAsync(h->dist_ctr, 0, 4, c.s));
-  {
-    Launch L(h, "k_sp_export", c.s);
-    k_sp_export<<<dim3(8, c.G), 256, 0, c.s>>>(c.xs, c.ys, h->surv, h->sp_eb,
-                                               candidates ? h->sp_ccount : h->sp_gcount, c.cap,
-                                               c.base, h->sp_st, d_x, d_y, d_idx, d_b, h->dist_ctr);
-  }
-  uint32_t cnt = 0;
-  TRY(read_u32(h, h->dist_ctr, &cnt));
-  *n_out = cnt;
+  Launch L(h, "k_sp_export", c.s);
+  k_sp_export<<<dim3(8, c.G), 256, 0, c.s>>>(c.xs, c.ys, h->surv, h->sp_eb,
+                                             candidates ? h->sp_ccount : h->sp_gcount, c.cap, c.base,
+                                             h->sp_st, d_x, d_y, d_idx, d_b, h->dist_ctr);
+  CU(cudaGetLastError());
   return GSCAN_OK;
 }
 
-int gscan_dist_slices(gscan_handle* h, const double* d_X, const double* d_Y, uint64_t n_g,
-                      const uint32_t* d_gb, uint64_t l_pos, const uint32_t* d_phimax,
-                      const uint32_t* phi_range, uint32_t* d_prefmax, uint32_t* fail_out) {
-  if (!h || !d_X || !d_Y || !d_phimax || !phi_range || !d_prefmax || !fail_out) return GSCAN_E_INVALID;
+int gscan_dist_enq_slices(gscan_handle* h, const double* d_X, const double* d_Y, uint64_t n_g,
+                          const uint32_t* d_gb, const int64_t* d_gidx, uint64_t M) {
+  if (!h || !d_X || !d_Y || !h->dist_rec) return GSCAN_E_INVALID;
+  h->h_sp->M = (uint32_t)M;  // the global slice structure sizes rank 0's grids
   SpCtx c = dist_ctx(h);
   if (1 + n_g + 2 > std::min<uint64_t>(h->cap, h->wcap))
     return fail(h, GSCAN_E_CAPACITY, "sharded path: %llu gathered points exceed rank 0's buffers",
                 (unsigned long long)n_g);
   TRY(dist_slices_ensure(h, c));
-  CU(cudaMemcpyAsync(h->sp_phimax, d_phimax, kSpBuckets * 4, cudaMemcpyDeviceToDevice, c.s));
-  k_sp_set_phi<<<1, 1, 0, c.s>>>(h->sp_st, phi_range[0], phi_range[1], (uint32_t)l_pos, h->ext, 0u);
+  k_dist_find_pl<<<1, 32, 0, c.s>>>(d_gidx, (uint32_t)n_g, h->sp_st, h->ext);
   k_sp_gsize<<<(kSpBuckets + 255) / 256, 256, 0, c.s>>>(h->sp_gbits, h->sp_hist, h->sp_gsz);
   TRY(scan_u32(h, h->sp_gsz, kSpBuckets, h->sp_gs));
   TRY(dist_fill(h, c, (uint32_t)n_g, 1, d_gb, h->sp_gcount));
   c.gs = h->sp_gs;
   TRY(sp_seg_sortg(h, c, d_X, d_Y, /*region_xy=*/false));
-  CU(cudaMemcpyAsync(d_prefmax, h->sp_prefmax, kSpBuckets * 4, cudaMemcpyDeviceToDevice, c.s));
-  TRY(dist_read_state(h));
-  *fail_out = dist_fail(h);
+  k_dist_pref_out<<<(kSpBuckets + 256) / 256, 256, 0, c.s>>>(h->sp_prefmax, h->sp_st, h->dist_pref);
+  CU(cudaGetLastError());
   return GSCAN_OK;
 }
 
-int gscan_dist_cand(gscan_handle* h, const uint32_t* d_prefmax, uint64_t* n_c, uint32_t* fail_out) {
-  if (!h || !d_prefmax || !n_c || !fail_out) return GSCAN_E_INVALID;
+int gscan_dist_enq_cand(gscan_handle* h) {
+  if (!h || !h->dist_rec) return GSCAN_E_INVALID;
   const SpCtx c = dist_ctx(h);
-  CU(cudaMemcpyAsync(h->sp_prefmax, d_prefmax, kSpBuckets * 4, cudaMemcpyDeviceToDevice, c.s));
+  k_dist_pref_in<<<(kSpBuckets + 255) / 256, 256, 0, c.s>>>(h->dist_pref, h->sp_prefmax, h->sp_st);
   TRY(sp_seg_f4(h, c));
-  TRY(dist_read_state(h));
-  *n_c = h->h_sp->n_c;
-  *fail_out = dist_fail(h);
+  k_dist_rec_f4<<<1, 32, 0, c.s>>>(h->sp_st, h->dist_rec);
+  CU(cudaGetLastError());
   return GSCAN_OK;
 }
 
-int gscan_dist_finish(gscan_handle* h, const double* d_X, const double* d_Y, uint64_t n_g,
-                      uint64_t n_c, const uint32_t* d_cb, uint32_t* d_hull, uint64_t hull_cap,
-                      uint64_t* hull_n, uint64_t* n_r, uint32_t* fail_out) {
-  if (!h || !d_X || !d_Y || !d_hull || !hull_n || !n_r || !fail_out) return GSCAN_E_INVALID;
+// Rank 0: walk, certificate and Graham (synchronises). *status: 0 the hull
+// is final, 1 the certificate did not hold (every rank runs F6 on its shard:
+// gscan_dist_enq_verify), 2 declined (fail bits in *fail_out).
+int gscan_dist_root_finish(gscan_handle* h, const double* d_X, const double* d_Y, uint64_t n_g,
+                           uint64_t n_c, const uint32_t* d_cb, uint64_t M, uint32_t* d_hull,
+                           uint64_t hull_cap, uint64_t* hull_n, uint64_t* n_r, uint32_t* status,
+                           uint32_t* fail_out) {
+  if (!h || !d_X || !d_Y || !d_hull || !hull_n || !n_r || !status || !fail_out || !h->dist_rec)
+    return GSCAN_E_INVALID;
+  h->h_sp->M = (uint32_t)M;
   SpCtx c = dist_ctx(h);
   c.gs = h->sp_gs;
+  *status = 2;
+  *hull_n = 0;
+  *n_r = 0;
   const uint64_t nw = 1 + n_g + n_c;
   if (nw + 2 > std::min<uint64_t>(h->cap, h->wcap))
     return fail(h, GSCAN_E_CAPACITY, "sharded path: %llu walk records exceed rank 0's buffers",
@@ -2396,7 +2452,6 @@ int gscan_dist_finish(gscan_handle* h, const double* d_X, const double* d_Y, uin
   TRY(dist_fill(h, c, (uint32_t)n_c, (uint32_t)(1 + n_g), d_cb, h->sp_ccount));
   TRY(tree_workspace(h, (uint32_t)std::min<uint64_t>(nw, kTreeMaxN)));
   TRY(sp_seg_walk(h, c, d_X, d_Y, (uint32_t)nw));
-  k_sp_no_verify<<<1, 32, 0, c.s>>>(h->sp_st);
   h->graham_path = 0;
   h->graham_fails = 0;
   TRY(sp_seg_tail(h, c));
@@ -2404,7 +2459,6 @@ int gscan_dist_finish(gscan_handle* h, const double* d_X, const double* d_Y, uin
   const SpState sp = *h->h_sp;
   *fail_out = dist_fail(h);
   *n_r = sp.n_r;
-  *hull_n = 0;
   if (sp.fail) return GSCAN_OK;
   bool done = false;
   TRY(tree_finish(h, h->A_x, h->A_y, h->A_i, &done));
@@ -2417,55 +2471,26 @@ int gscan_dist_finish(gscan_handle* h, const double* d_X, const double* d_Y, uin
   CU(cudaMemcpyAsync(d_hull, h->d_out, (size_t)hull * 4, cudaMemcpyDeviceToDevice, h->stream));
   CU(cudaStreamSynchronize(h->stream));
   *hull_n = hull;
+  *status = sp.need_verify ? 1u : 0u;
   return GSCAN_OK;
 }
 
-int gscan_dist_dup_local(gscan_handle* h, uint32_t* d_part_counts, uint64_t* d_parted,
-                         uint64_t* n_hash) {
-  if (!h || !d_part_counts || !d_parted || !n_hash) return GSCAN_E_INVALID;
+int gscan_dist_enq_verify(gscan_handle* h, const uint32_t* d_rlo, const double* d_Rx,
+                          const double* d_Ry) {
+  if (!h || !d_rlo || !d_Rx || !d_Ry || !h->dist_rec) return GSCAN_E_INVALID;
   const SpCtx c = dist_ctx(h);
-  const uint32_t nl = 2 * c.G;
-  TRY(scan_u32(h, h->sp_part_off, kSpParts * nl, h->sp_part_off));
-  uint32_t total = 0;
-  TRY(read_u32(h, h->sp_part_off + (size_t)kSpParts * nl, &total));
-  CU(cudaMemsetAsync(h->sp_side_work, 0, 2 * sizeof(uint32_t), c.s));
-  k_sp_set_u32<<<1, 1, 0, c.s>>>(&h->sp_st->fail, 0u);  // the host decided the path globally
-  k_sp_dup_part<false><<<h->sm_count, 1024, kSpSideSmem, c.s>>>(h->sp_dup, h->sp_hcount, c.cap / 2, nl,
-                                                        h->sp_part_off, h->sp_st, h->sp_dup2,
-                                                        h->sp_side_work, 0u, nullptr);
-  k_sp_part_totals<<<(kSpParts + 255) / 256, 256, 0, c.s>>>(h->sp_part_off, nl, total, d_part_counts);
-  CU(cudaGetLastError());
-  CU(cudaStreamSynchronize(c.s));
-  *d_parted = (uint64_t)(uintptr_t)h->sp_dup2;
-  *n_hash = total;
-  return GSCAN_OK;
-}
-
-int gscan_dist_dup_check(gscan_handle* h, const uint64_t* d_recv, uint64_t n_recv,
-                         const uint32_t* d_counts, uint32_t R, uint32_t* dup_found) {
-  if (!h || !d_counts || !dup_found || R == 0 || R > kDistMaxRanks) return GSCAN_E_INVALID;
-  const SpCtx c = dist_ctx(h);
-  if (n_recv > (uint64_t)h->sp_grid * sparse_region_cap(h, h->dist_n)) {
-    // more hashes than this rank's regions hold (uneven shards): a local
-    // decline, reported like a possible duplicate so every rank still joins
-    // the next collective and all of them take the survivor gather
-    *dup_found = 1;
-    return GSCAN_OK;
+  if (d_rlo != h->sp_rlo)
+    CU(cudaMemcpyAsync(h->sp_rlo, d_rlo, (kSpBuckets + 1) * 4, cudaMemcpyDeviceToDevice, c.s));
+  k_dist_verify_prep<<<1, 32, 0, c.s>>>(h->sp_st);
+  {
+    Launch L(h, "k_sp_verify", c.s);
+#define A6 c.xs, c.ys, h->sp_codes, c.n, h->sp_gbits, h->sp_rlo, d_Rx, d_Ry, h->sp_st
+    if (c.vec) k_sp_verify<true><<<c.G, kSpThreads, c.smem_nb + 4, c.s>>>(A6);
+    else k_sp_verify<false><<<c.G, kSpThreads, c.smem_nb + 4, c.s>>>(A6);
+#undef A6
   }
-  k_sp_recv_plan<<<(kSpParts * R + 255) / 256, 256, 0, c.s>>>(d_counts, R, h->dist_pm, h->dist_hc,
-                                                               h->dist_lb);
-  TRY(scan_u32(h, h->dist_pm, kSpParts * R, h->dist_pm));
-  CU(cudaMemsetAsync(h->sp_side_work, 0, 2 * sizeof(uint32_t), c.s));
-  k_sp_set_u32<<<1, 1, 0, c.s>>>(&h->sp_st->fail, 0u);
-  k_sp_dup_part<false><<<h->sm_count, 1024, kSpSideSmem, c.s>>>(d_recv, h->dist_hc, 0u, R, h->dist_pm,
-                                                        h->sp_st, h->sp_dup, h->sp_side_work, 0u,
-                                                        h->dist_lb);
-  k_sp_dups<<<h->sm_count, 1024, kSpSideSmem, c.s>>>(h->sp_dup, h->dist_pm, R, h->sp_st,
-                                                     h->sp_side_work + 1, 0u, h->sp_dup_scr,
-                                                     h->sp_dup_scap);
+  k_dist_rec_ver<<<1, 32, 0, c.s>>>(h->sp_st, h->dist_rec);
   CU(cudaGetLastError());
-  TRY(dist_read_state(h));
-  *dup_found = (h->h_sp->fail & (kSpFailDup | kSpFailCap)) ? 1u : 0u;
   return GSCAN_OK;
 }
 

@@ -3157,46 +3157,11 @@ __global__ void __launch_bounds__(256) k_sp_fill_regions(uint32_t n, uint32_t id
 }
 
 
-// Host-decided global values into the state (sharded path).
-__global__ void k_sp_set_pl(SpState* __restrict__ st, uint64_t d2, uint32_t l_idx, uint32_t ties,
-                            double lx, double ly, uint32_t fail) {
-  st->d2max = d2;
-  st->l_idx = l_idx;
-  st->ties = ties;
-  st->lx = lx;
-  st->ly = ly;
-  st->fail = fail;
-}
-__global__ void k_sp_set_u32(uint32_t* __restrict__ p, uint32_t v) { *p = v; }
-__global__ void k_sp_set_phi(SpState* __restrict__ st, uint32_t lo, uint32_t hi, uint32_t l_idx,
-                             ExtResult* __restrict__ ext, uint32_t anchor_idx) {
-  st->phi_lo = lo;
-  st->phi_hi = hi;
-  st->l_idx = l_idx;
-  ext->idx[4] = anchor_idx;
-}
-
 // Sizes of the gathered buckets (storage of rank 0's gathered records).
 __global__ void k_sp_gsize(const uint32_t* __restrict__ gbits, const uint32_t* __restrict__ hist,
                            uint32_t* __restrict__ out) {
   const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b < kSpBuckets) out[b] = sp_gathered(gbits, b) ? hist[b] : 0u;
-}
-
-// Sharded path: without F6, a round-2 result the certificate does not prove
-// is declined.
-__global__ void k_sp_no_verify(SpState* __restrict__ st) {
-  if (threadIdx.x == 0 && st->need_verify) atomicOr(&st->fail, kSpFailVerify);
-}
-
-// Hash counts per partition of this rank (part_off scanned, nl lists).
-__global__ void k_sp_part_totals(const uint32_t* __restrict__ part_off, uint32_t nl,
-                                 uint32_t total, uint32_t* __restrict__ out) {
-  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= kSpParts) return;
-  const uint32_t lo = part_off[(size_t)p * nl];
-  const uint32_t hi = p + 1 < kSpParts ? part_off[(size_t)(p + 1) * nl] : total;
-  out[p] = hi - lo;
 }
 
 // Received hash blocks (R sources; cnt[r * kSpParts + p] entries of
@@ -3221,6 +3186,231 @@ __global__ void k_sp_recv_plan(const uint32_t* __restrict__ cnt, uint32_t R,
       acc += sz;
     }
   }
+}
+
+// ===========================================================================
+// Sharded path, device-side data plane (gscan_dist_enq_*): every rank writes
+// its per-phase scalars into a fixed record of kDistRecLen int64 words; the
+// host all-gathers the records on the handle's stream (NCCL) and the next
+// phase combines them ON THE DEVICE, so a call needs host round trips only
+// where a variable-size exchange needs its sizes. Word layout:
+//   [0, 15)   extremes: global index (5), x bits (5), y bits (5)
+//   [16, 23)  F2: dist2 bits, global index of P_l (-1: none), ties, x bits,
+//             y bits, round-1 survivors, fail (locally decided P_l bits masked)
+//   [24, 27)  plan: points of P_l's bucket ordered before it, fail, M
+//   [28, 32)  F3: phi_lo, phi_hi, gathered points, fail
+//   [36, 38)  F4: candidates, fail (includes the duplicate check)
+//   [40, 42)  F6: points that would not be discarded, fail
+constexpr int kDistRecLen = 64;
+constexpr int kRxExt = 0, kRxF2 = 16, kRxPlan = 24, kRxF3 = 28, kRxF4 = 36, kRxVer = 40;
+
+__global__ void k_dist_rec_ext(const ExtResult* __restrict__ ext, uint32_t base,
+                               int64_t* __restrict__ rec) {
+  if (threadIdx.x != 0) return;
+  for (int k = 0; k < 4; ++k) {
+    rec[kRxExt + k] = (int64_t)base + ext->idx[k];
+    rec[kRxExt + 5 + k] = (int64_t)dbits(ext->qx[k]);
+    rec[kRxExt + 10 + k] = (int64_t)dbits(ext->qy[k]);
+  }
+  rec[kRxExt + 4] = (int64_t)base + ext->idx[4];
+  rec[kRxExt + 9] = (int64_t)dbits(ext->ax);
+  rec[kRxExt + 14] = (int64_t)dbits(ext->ay);
+}
+
+// Global extremes from R records with find_extremes' / select_anchor's rules
+// (strict compares; equal values: the lowest global index; prefilter.hpp:28-39,
+// angular.hpp:40-49). ext_out: the combined record (host/rank 0 reads it).
+__global__ void k_dist_apply_ext(const int64_t* __restrict__ recs, uint32_t R,
+                                 ExtResult* __restrict__ ext, int64_t* __restrict__ ext_out) {
+  if (threadIdx.x != 0) return;
+  for (int k = 0; k < 5; ++k) {
+    int64_t bi = recs[kRxExt + k];
+    double bx = bitsd((uint64_t)recs[kRxExt + 5 + k]), by = bitsd((uint64_t)recs[kRxExt + 10 + k]);
+    for (uint32_t r = 1; r < R; ++r) {
+      const int64_t* q = recs + (size_t)r * kDistRecLen;
+      const int64_t gi = q[kRxExt + k];
+      const double x = bitsd((uint64_t)q[kRxExt + 5 + k]), y = bitsd((uint64_t)q[kRxExt + 10 + k]);
+      bool better;
+      if (k == 0) better = x < bx || (x == bx && gi < bi);
+      else if (k == 1) better = y < by || (y == by && gi < bi);
+      else if (k == 2) better = x > bx || (x == bx && gi < bi);
+      else if (k == 3) better = y > by || (y == by && gi < bi);
+      else better = y < by || (y == by && (x < bx || (x == bx && gi < bi)));
+      if (better) { bi = gi; bx = x; by = y; }
+    }
+    ext->idx[k] = (uint32_t)bi;
+    if (k < 4) { ext->qx[k] = bx; ext->qy[k] = by; }
+    else { ext->ax = bx; ext->ay = by; }
+    ext_out[k] = bi;
+    ext_out[5 + k] = (int64_t)dbits(bx);
+    ext_out[10 + k] = (int64_t)dbits(by);
+  }
+}
+
+__global__ void k_dist_rec_f2(const SpState* __restrict__ st, const Counters* __restrict__ ctr,
+                              uint32_t base, int64_t* __restrict__ rec) {
+  if (threadIdx.x != 0) return;
+  const bool have = st->l_idx != 0xffffffffu;
+  rec[kRxF2 + 0] = (int64_t)st->d2max;
+  rec[kRxF2 + 1] = have ? (int64_t)base + st->l_idx : -1;
+  rec[kRxF2 + 2] = have ? st->ties : 0;
+  rec[kRxF2 + 3] = (int64_t)dbits(st->lx);
+  rec[kRxF2 + 4] = (int64_t)dbits(st->ly);
+  rec[kRxF2 + 5] = ctr->n1;
+  // P_l's tie / none / too-many bits are decided again over all ranks
+  rec[kRxF2 + 6] = st->fail & ~(kSpFailTie | kSpFailFew | kSpFailMany);
+}
+
+// The global farthest point (split_regions, angular.hpp:197-204: the first
+// maximal dist2 = the lowest global index among equals), its tie count and
+// the global fail bits, into every rank's state.
+__global__ void k_dist_apply_best(const int64_t* __restrict__ recs, uint32_t R, uint64_t n_global,
+                                  SpState* __restrict__ st) {
+  if (threadIdx.x != 0) return;
+  bool found = false;
+  uint64_t bd = 0, n1 = 0;
+  int64_t bi = -1, bx = 0, by = 0;
+  uint32_t ties = 0, fail = 0;
+  for (uint32_t r = 0; r < R; ++r) {
+    const int64_t* q = recs + (size_t)r * kDistRecLen + kRxF2;
+    n1 += (uint64_t)q[5];
+    fail |= (uint32_t)q[6];
+    const uint32_t t = (uint32_t)q[2];
+    if (t == 0) continue;
+    const uint64_t d2 = (uint64_t)q[0];
+    if (!found || d2 > bd) {
+      found = true; bd = d2; bi = q[1]; bx = q[3]; by = q[4]; ties = t;
+    } else if (d2 == bd) {
+      ties += t;
+      if (q[1] < bi) { bi = q[1]; bx = q[3]; by = q[4]; }
+    }
+  }
+  if (!found) fail |= kSpFailFew;
+  else if (ties != 1) fail |= kSpFailTie;
+  if (n1 * 10 > n_global * 9) fail |= kSpFailMany;
+  st->d2max = bd;
+  st->l_idx = found ? (uint32_t)bi : 0xffffffffu;
+  st->ties = ties;
+  st->lx = bitsd((uint64_t)bx);
+  st->ly = bitsd((uint64_t)by);
+  st->fail = fail;
+}
+
+__global__ void k_dist_rec_plan(const SpState* __restrict__ st, int64_t* __restrict__ rec) {
+  if (threadIdx.x != 0) return;
+  rec[kRxPlan + 0] = st->l_below;
+  rec[kRxPlan + 1] = st->fail;
+  rec[kRxPlan + 2] = st->M;
+}
+
+__global__ void k_dist_apply_plan(const int64_t* __restrict__ recs, uint32_t R,
+                                  SpState* __restrict__ st) {
+  if (threadIdx.x != 0) return;
+  uint64_t lb = 0;
+  uint32_t fail = 0;
+  for (uint32_t r = 0; r < R; ++r) {
+    lb += (uint64_t)recs[(size_t)r * kDistRecLen + kRxPlan + 0];
+    fail |= (uint32_t)recs[(size_t)r * kDistRecLen + kRxPlan + 1];
+  }
+  st->l_below = (uint32_t)lb;
+  st->fail |= fail;
+}
+
+__global__ void k_dist_rec_f3(const SpState* __restrict__ st, int64_t* __restrict__ rec) {
+  if (threadIdx.x != 0) return;
+  rec[kRxF3 + 0] = st->phi_lo;
+  rec[kRxF3 + 1] = st->phi_hi;
+  rec[kRxF3 + 2] = st->n_g;
+  rec[kRxF3 + 3] = st->fail;
+}
+
+// phi range over all ranks (ordered-float encodings compare as uint32)
+__global__ void k_dist_apply_f3(const int64_t* __restrict__ recs, uint32_t R,
+                                SpState* __restrict__ st) {
+  if (threadIdx.x != 0) return;
+  uint32_t lo = 0xffffffffu, hi = 0, fail = 0;
+  for (uint32_t r = 0; r < R; ++r) {
+    const int64_t* q = recs + (size_t)r * kDistRecLen + kRxF3;
+    lo = min(lo, (uint32_t)q[0]);
+    hi = max(hi, (uint32_t)q[1]);
+    fail |= (uint32_t)q[3];
+  }
+  st->phi_lo = lo;
+  st->phi_hi = hi;
+  st->fail |= fail;
+}
+
+// Hash counts per partition (part_off scanned over nl lists; its total at
+// part_off[kSpParts * nl]).
+__global__ void k_dist_part_totals(const uint32_t* __restrict__ part_off, uint32_t nl,
+                                   uint32_t* __restrict__ out) {
+  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= kSpParts) return;
+  const uint32_t lo = part_off[(size_t)p * nl];
+  const uint32_t hi = part_off[(size_t)(p + 1) * nl];
+  out[p] = hi - lo;
+}
+
+__global__ void k_dist_set_fail(SpState* __restrict__ st, uint32_t bits, uint32_t why) {
+  if (threadIdx.x != 0) return;
+  st->fail |= bits;
+  if (why) atomicMax(&st->why, why);
+}
+
+// Rank 0, before sorting the gathered points: P_l's position in X (index 0
+// = the anchor, 1.. the gathered points sorted by global index gi[0, n_g)).
+__global__ void k_dist_find_pl(const int64_t* __restrict__ gi, uint32_t n_g,
+                               SpState* __restrict__ st, ExtResult* __restrict__ ext) {
+  if (threadIdx.x != 0 || st->fail) return;
+  const int64_t want = st->l_idx;
+  uint32_t lo = 0, hi = n_g;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) / 2;
+    if (gi[mid] < want) lo = mid + 1;
+    else hi = mid;
+  }
+  if (lo < n_g && gi[lo] == want) {
+    st->l_idx = 1 + lo;
+    ext->idx[4] = 0;
+  } else {  // P_l is always in a gathered bucket; anything else is inconsistent
+    st->fail |= kSpFailInternal;
+    atomicMax(&st->why, 12u);
+  }
+}
+
+// Rank 0's prefix maxima and its fail word -> the broadcast block
+__global__ void k_dist_pref_out(const uint32_t* __restrict__ prefmax, const SpState* __restrict__ st,
+                                uint32_t* __restrict__ out) {
+  for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b <= kSpBuckets; b += gridDim.x * blockDim.x)
+    out[b] = b < kSpBuckets ? prefmax[b] : st->fail;
+}
+
+// ... and back on every rank (before F4)
+__global__ void k_dist_pref_in(const uint32_t* __restrict__ in, uint32_t* __restrict__ prefmax,
+                               SpState* __restrict__ st) {
+  for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < kSpBuckets; b += gridDim.x * blockDim.x)
+    prefmax[b] = in[b];
+  if (blockIdx.x == 0 && threadIdx.x == 0) st->fail |= in[kSpBuckets];
+}
+
+__global__ void k_dist_rec_f4(const SpState* __restrict__ st, int64_t* __restrict__ rec) {
+  if (threadIdx.x != 0) return;
+  rec[kRxF4 + 0] = st->n_c;
+  rec[kRxF4 + 1] = st->fail;
+}
+
+// Distributed F6: rank 0's round-2 output and bucket offsets are broadcast;
+// every rank verifies its own shard's skipped points against them.
+__global__ void k_dist_verify_prep(SpState* __restrict__ st) {
+  if (threadIdx.x != 0) return;
+  st->need_verify = 1;
+  st->verify_fail = 0;
+}
+
+__global__ void k_dist_rec_ver(const SpState* __restrict__ st, int64_t* __restrict__ rec) {
+  if (threadIdx.x != 0) return;
+  rec[kRxVer + 0] = st->verify_fail;
+  rec[kRxVer + 1] = st->fail;
 }
 
 }  // namespace gscan

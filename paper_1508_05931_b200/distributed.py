@@ -6,7 +6,12 @@ device. Two paths, both exact:
 
 * ``sparse_sharded`` (default): every rank runs the sparse
   round-2 pipeline (csrc/sparse.cuh) on its own shard through the
-  ``gscan_dist_*`` phases, and only small things move between ranks:
+  enqueue-only ``gscan_dist_enq_*`` phases, and only small things move
+  between ranks. Device-side data plane: per-phase records are all-gathered
+  and combined by the next phase on the device, the fixed-size collectives
+  run in place on the handle's buffers, all on one stream; the host waits
+  for the device three times per call (sizes of the variable exchanges, the
+  candidate counts, rank 0's verdict):
 
   =====================  ==========================================  =========
   exchange               what                                         size
@@ -24,12 +29,13 @@ device. Two paths, both exact:
   =====================  ==========================================  =========
 
   Rank 0 then walks the gathered points and candidates exactly, certifies
-  the skipped points, and runs Graham. No rank ever holds another rank's
-  survivors, so 1B points scale.
+  the skipped points (when the certificate does not hold, every rank runs
+  F6 on its own shard against rank 0's broadcast round-2 output), and runs
+  Graham. No rank ever holds another rank's survivors, so 1B points scale.
 * the survivor gather (``survivor_gather``): K1/K2 per shard, then all
   survivors to rank 0. It is the exact fallback whenever the sparse path
-  declines (tie for P_l, possible duplicates, a certificate that does not
-  hold, near-convex input, capacity).
+  declines (tie for P_l, possible duplicates, a failed distributed F6,
+  near-convex input, capacity).
 
 The collectives go through a small interface (``Comm``) so that the same
 orchestration runs under NCCL (``TorchComm``, one rank per process) or as R
@@ -82,23 +88,6 @@ def _combine(recs: np.ndarray) -> np.ndarray:
     return out
 
 
-def _combine_best(recs) -> tuple[tuple | None, int]:
-    """Per-rank (d2_bits, global idx, ties, x, y) -> the global farthest point
-    (split_regions, angular.hpp:197-204: first maximal dist2 = lowest index
-    among equals) and the number of points at that distance."""
-    best, ties = None, 0
-    for d2, gi, t, x, y in recs:
-        if t == 0:
-            continue
-        if best is None or d2 > best[0]:
-            best, ties = (d2, gi, x, y), t
-        elif d2 == best[0]:
-            ties += t
-            if gi < best[1]:
-                best = (d2, gi, x, y)
-    return best, ties
-
-
 # ---------------------------------------------------------------------------
 # collectives
 class Comm:
@@ -111,18 +100,16 @@ class Comm:
     def allreduce(self, ts: list[torch.Tensor], op: str) -> list[torch.Tensor]:
         raise NotImplementedError
 
-    def allgather_obj(self, objs: list) -> list:
-        """-> the list of all R objects (same on every rank)."""
-        raise NotImplementedError
-
     def allgather_i64(self, rows: list) -> np.ndarray:
         """Fixed-length int64 rows (one per local rank, same length everywhere)
         -> (R, L) int64 array on every rank: one tensor all-gather, no pickling.
         Doubles travel as their bit patterns (_i64 / _f64)."""
         raise NotImplementedError
 
-    def gather_root(self, ts: list[torch.Tensor]) -> list[torch.Tensor] | None:
-        """Variable-length 1-D tensors -> rank 0 gets all R (rank order); others None."""
+    def gather_root(self, ts: list[torch.Tensor], sizes: list[int] | None = None) -> list[torch.Tensor] | None:
+        """Variable-length 1-D tensors -> rank 0 gets all R (rank order); others
+        None. sizes: every rank's length when the caller knows them (no size
+        exchange)."""
         raise NotImplementedError
 
     def bcast_root(self, t: torch.Tensor | None, like: list[torch.Tensor]) -> list[torch.Tensor]:
@@ -130,6 +117,26 @@ class Comm:
 
     def all_to_all(self, sends: list[list[torch.Tensor]]) -> list[list[torch.Tensor]]:
         """sends[k][r] from local rank k to rank r -> recv[k][s] from rank s."""
+        raise NotImplementedError
+
+    # in-place device collectives, ordered on the current stream (no host wait
+    # under NCCL): the device-side data plane of sparse_sharded
+    def allreduce_(self, ts: list[torch.Tensor], op: str) -> None:
+        raise NotImplementedError
+
+    def allgather_(self, rows: list[torch.Tensor], outs: list[torch.Tensor]) -> None:
+        """rows[k] (L) of local rank k -> every outs[k] (R * L), rank-major."""
+        raise NotImplementedError
+
+    def bcast_(self, ts: list[torch.Tensor]) -> None:
+        """Rank 0's tensor into every rank's (same shape)."""
+        raise NotImplementedError
+
+    def all_to_all_flat(self, inps: list[torch.Tensor], send_sizes: list[list[int]],
+                        recv_sizes: list[list[int]]) -> list[torch.Tensor]:
+        """inps[k]: local rank k's blocks for ranks 0..R-1 back to back
+        (send_sizes[k][r] elements each) -> per local rank the blocks from
+        ranks 0..R-1 back to back (recv_sizes[k][s] each; sizes known)."""
         raise NotImplementedError
 
 
@@ -146,13 +153,10 @@ class LocalComm(Comm):
              "min": lambda: st.min(0).values}[op]()
         return [r.clone() for _ in ts]
 
-    def allgather_obj(self, objs):
-        return list(objs)
-
     def allgather_i64(self, rows):
         return np.stack([np.asarray(r, dtype=np.int64) for r in rows])
 
-    def gather_root(self, ts):
+    def gather_root(self, ts, sizes=None):
         return [t.clone() for t in ts]
 
     def bcast_root(self, t, like):
@@ -160,6 +164,26 @@ class LocalComm(Comm):
 
     def all_to_all(self, sends):
         return [[sends[s][r].clone() for s in range(self.world)] for r in range(self.world)]
+
+    def allreduce_(self, ts, op):
+        st = torch.stack(ts)
+        r = {"sum": lambda: st.sum(0, dtype=st.dtype), "max": lambda: st.max(0).values,
+             "min": lambda: st.min(0).values}[op]()
+        for t in ts:
+            t.copy_(r)
+
+    def allgather_(self, rows, outs):
+        cat = torch.cat(rows)
+        for o in outs:
+            o.copy_(cat)
+
+    def bcast_(self, ts):
+        for t in ts[1:]:
+            t.copy_(ts[0])
+
+    def all_to_all_flat(self, inps, send_sizes, recv_sizes):
+        blocks = [list(torch.split(inp[: sum(sz)], sz)) for inp, sz in zip(inps, send_sizes)]
+        return [torch.cat([blocks[s][r] for s in range(self.world)]) for r in range(self.world)]
 
 
 class TorchComm(Comm):
@@ -187,12 +211,6 @@ class TorchComm(Comm):
         dist.all_reduce(w, op=self._OPS[op], group=self.group)
         return [w.to(t.device)]
 
-    def allgather_obj(self, objs):
-        (o,) = objs
-        out = [None] * self.world
-        dist.all_gather_object(out, o, group=self.group)
-        return out
-
     def allgather_i64(self, rows):
         (r,) = rows
         t = torch.as_tensor(np.asarray(r, dtype=np.int64), device=self.cdev)
@@ -203,9 +221,9 @@ class TorchComm(Comm):
             dist.all_gather_into_tensor(out, t, group=self.group)
         return out.cpu().numpy()
 
-    def gather_root(self, ts):
+    def gather_root(self, ts, sizes=None):
         (t,) = ts
-        ns = self.allgather_i64([[t.numel()]])[:, 0].tolist()
+        ns = list(sizes) if sizes is not None else self.allgather_i64([[t.numel()]])[:, 0].tolist()
         mx = max(max(ns), 1)
         pad = torch.zeros(mx, dtype=t.dtype, device=self.cdev)
         pad[: t.numel()] = self._out(t)
@@ -244,6 +262,55 @@ class TorchComm(Comm):
                                    input_split_sizes=sizes, group=self.group)
         return [[x.to(dev) for x in torch.split(out, rs)]]
 
+    def allreduce_(self, ts, op):
+        (t,) = ts
+        if self.stage:
+            w = t.cpu()
+            dist.all_reduce(w, op=self._OPS[op], group=self.group)
+            t.copy_(w)
+        else:
+            dist.all_reduce(t, op=self._OPS[op], group=self.group)
+
+    def allgather_(self, rows, outs):
+        (r,), (o,) = rows, outs
+        if self.stage:
+            w = torch.empty((self.world, r.numel()), dtype=r.dtype)
+            dist.all_gather(list(w.unbind(0)), r.cpu(), group=self.group)
+            o.copy_(w.view(-1))
+        else:
+            dist.all_gather_into_tensor(o, r, group=self.group)
+
+    def bcast_(self, ts):
+        (t,) = ts
+        if self.stage:
+            w = t.cpu()
+            dist.broadcast(w, 0, group=self.group)
+            t.copy_(w)
+        else:
+            dist.broadcast(t, 0, group=self.group)
+
+    def all_to_all_flat(self, inps, send_sizes, recv_sizes):
+        (inp,), (ss,), (rs,) = inps, send_sizes, recv_sizes
+        ss, rs = [int(v) for v in ss], [int(v) for v in rs]
+        out = torch.empty(sum(rs), dtype=inp.dtype, device=inp.device)
+        if self.stage:  # gloo: point-to-point through host memory
+            src = list(torch.split(inp[: sum(ss)].cpu(), ss))
+            outs = list(torch.split(torch.empty(sum(rs), dtype=inp.dtype), rs))
+            reqs = []
+            for r in range(self.world):
+                if r == self.rank:
+                    outs[r].copy_(src[r])
+                    continue
+                reqs.append(dist.isend(src[r].contiguous(), r, group=self.group))
+                reqs.append(dist.irecv(outs[r], r, group=self.group))
+            for q in reqs:
+                q.wait()
+            out.copy_(torch.cat(outs))
+        else:
+            dist.all_to_all_single(out, inp[: sum(ss)], output_split_sizes=rs,
+                                   input_split_sizes=ss, group=self.group)
+        return [out]
+
 
 # ---------------------------------------------------------------------------
 def _i64(x: float) -> int:
@@ -255,47 +322,9 @@ def _f64(v) -> float:
     return float(np.array([v], dtype=np.int64).view(np.float64)[0])
 
 
-def _u64(v) -> int:
-    return int(v) & 0xFFFFFFFFFFFFFFFF
-
-
-def _s64(v) -> int:
-    """A uint64 as the int64 with the same bits (for the int64 collectives)."""
-    v = int(v) & 0xFFFFFFFFFFFFFFFF
-    return v - (1 << 64) if v >= 1 << 63 else v
-
-
 def _ck(eng: Engine, rc: int, what: str):
     if rc:
         eng._raise(rc, what)
-
-
-def _ready(dev) -> None:
-    """The phases run on the handle's own stream: tensors torch (or NCCL) just
-    wrote must be complete first."""
-    torch.cuda.synchronize(dev)
-
-
-def _extremes(engines, shards, offsets, comm: Comm) -> N.gscan_extremes:
-    recs = []
-    for eng, (dx, dy), off in zip(engines, shards, offsets):
-        ex = N.gscan_extremes()
-        _ready(dx.device)
-        _ck(eng, eng._lib.gscan_shard_extremes(eng.handle, C.c_void_p(dx.data_ptr()),
-                                               C.c_void_p(dy.data_ptr()), dx.numel(), C.byref(ex)),
-            "shard_extremes")
-        recs.append([off + ex.idx[k] for k in range(5)] + [_i64(v) for v in ex.x]
-                    + [_i64(v) for v in ex.y])
-    allr = comm.allgather_i64(recs)  # (R, 15): global indices, x bits, y bits
-    g = _combine(np.stack([np.array([[float(r[k]) for k in range(5)],
-                                     [_f64(r[5 + k]) for k in range(5)],
-                                     [_f64(r[10 + k]) for k in range(5)]]) for r in allr]))
-    gex = N.gscan_extremes()
-    for k in range(5):
-        gex.idx[k] = int(g[0, k])
-        gex.x[k] = g[1, k]
-        gex.y[k] = g[2, k]
-    return gex
 
 
 last_decline = ""  # why the last sparse_sharded call declined (diagnostics)
@@ -307,263 +336,275 @@ def _declined(why: str):
     return None
 
 
-def _agree(comm: Comm, local_ok: list[bool]) -> bool:
-    """Every rank's verdict -> one decision all ranks take together."""
-    return bool(comm.allgather_i64([[int(bool(v))] for v in local_ok]).all())
+# ---------------------------------------------------------------------------
+# device-side data plane: record words (include/gscan.h, sparse.cuh kRx*)
+_RX_F2, _RX_PLAN, _RX_F3, _RX_F4, _RX_VER = 16, 24, 28, 36, 40
+_SIGN = -(1 << 31)  # int32 0x80000000: unsigned order <-> signed order
+
+
+def _view(ptr: int, n: int, dtype: torch.dtype, dev) -> torch.Tensor:
+    """A torch view (no copy) of n elements of a handle-owned device buffer."""
+    ts = {torch.int64: "<i8", torch.int32: "<i4", torch.float64: "<f8"}[dtype]
+    if n == 0:
+        return torch.empty(0, dtype=dtype, device=dev)
+    return torch.as_tensor(_DevBuf(ptr, n, ts), device=dev)
+
+
+class _Bufs:
+    """One rank's gscan_dist_bufs as device tensor views."""
+
+    def __init__(self, eng: Engine, R: int, dev):
+        b = N.gscan_dist_bufs()
+        _ck(eng, eng._lib.gscan_dist_buffers(eng.handle, C.byref(b)), "dist_buffers")
+        self.raw = b
+        self.L = int(b.rec_len)
+        self.rec = _view(b.rec, self.L, torch.int64, dev)
+        self.recs = _view(b.recs, R * self.L, torch.int64, dev)
+        self.ext = _view(b.ext, 15, torch.int64, dev)
+        self.cells = _view(b.cells, int(b.cells_n), torch.int32, dev)
+        self.hist = _view(b.hist, int(b.buckets), torch.int32, dev)
+        self.phimax = _view(b.phimax, int(b.buckets), torch.int32, dev)
+        self.pref = _view(b.pref, int(b.buckets) + 1, torch.int32, dev)
+        self.part_counts = _view(b.part_counts, int(b.parts), torch.int32, dev)
+
+
+def _bind_stream(engines: list[Engine], dev) -> torch.cuda.Stream:
+    """One torch stream for every handle of this process: the phases, the
+    collectives and the torch ops between them are then ordered on it without
+    host waits (simulated ranks share it, so they serialise on it too)."""
+    s = getattr(engines[0], "_dist_stream", None)
+    if s is None or any(getattr(e, "_dist_stream", None) is not s for e in engines):
+        s = torch.cuda.Stream(dev)
+        for e in engines:
+            _ck(e, e._lib.gscan_set_stream(e.handle, C.c_void_p(s.cuda_stream)), "set_stream")
+            e._dist_stream = s
+    return s
 
 
 def sparse_sharded(engines: list[Engine], shards, offsets: list[int], n_global: int,
                    cfg: PipelineConfig, comm: Comm):
     """The sharded sparse path. Returns ``(hull_global_indices, stats)`` on rank 0
     and ``(None, None)`` elsewhere when it served the call, or ``None`` when it
-    declined (every rank then gets None and takes the survivor gather)."""
+    declined (every rank then gets None and takes the survivor gather).
+
+    Device-side data plane: the ``gscan_dist_enq_*`` phases only enqueue;
+    each writes a fixed record that the next phase combines on the device
+    after an all-gather, and the fixed-size exchanges run in place on the
+    handle's buffers, all on one stream. The host waits for the device at
+    three points (sizes of the hash all-to-all and of the gathered points;
+    candidate counts; rank 0's verdict), plus one when the certificate does
+    not hold and the shards run F6."""
     global last_decline
     last_decline = ""
     dev = shards[0][0].device
+    stream = _bind_stream(engines, dev)
+    stream.wait_stream(torch.cuda.current_stream(dev))  # the shards were written there
+    with torch.cuda.stream(stream):
+        return _sparse_sharded(engines, shards, offsets, n_global, cfg, comm, dev)
+
+
+def _sparse_sharded(engines, shards, offsets, n_global, cfg, comm, dev):
+    R = comm.world
     ccfg = cfg._c()
-    gex = _extremes(engines, shards, offsets, comm)
-    i32 = lambda n: torch.empty(n, dtype=_U32, device=dev)  # noqa: E731
-
-    # 1. sample cells -> sum
-    cells = []
+    bufs = []
     for eng, (dx, dy), off in zip(engines, shards, offsets):
-        t = i32(N.SP_CELLS)
-        _ready(dev)
-        _ck(eng, eng._lib.gscan_dist_begin(eng.handle, C.c_void_p(dx.data_ptr()),
-                                           C.c_void_p(dy.data_ptr()), dx.numel(), off, C.byref(gex),
-                                           C.byref(ccfg), C.c_void_p(t.data_ptr())), "dist_begin")
-        cells.append(t)
-    cells = comm.allreduce(cells, "sum")
+        _ck(eng, eng._lib.gscan_dist_enq_begin(eng.handle, C.c_void_p(dx.data_ptr()),
+                                               C.c_void_p(dy.data_ptr()), dx.numel(), off,
+                                               C.byref(ccfg)), "dist_enq_begin")
+        bufs.append(_Bufs(eng, R, dev))
+    L = bufs[0].L
 
-    # 2. bucket histogram -> sum; farthest point -> best; round-1 survivors -> sum
-    hists, bests, n1s = [], [], []
-    for eng, cl in zip(engines, cells):
-        hst = i32(N.SP_BUCKETS)
-        b = N.gscan_dist_best()
-        n1 = C.c_uint64()
-        _ready(dev)
-        _ck(eng, eng._lib.gscan_dist_hist(eng.handle, C.c_void_p(cl.data_ptr()),
-                                          C.c_void_p(hst.data_ptr()), C.byref(b), C.byref(n1)),
-            "dist_hist")
-        hists.append(hst)
-        bests.append((int(b.d2_bits), int(b.idx), int(b.ties), float(b.x), float(b.y)))
-        n1s.append(int(n1.value))
-    hists = comm.allreduce(hists, "sum")
-    rows = [[_s64(bb[0]), _s64(bb[1]), bb[2], _i64(bb[3]), _i64(bb[4]), n]
-            for bb, n in zip(bests, n1s)]
-    allb = comm.allgather_i64(rows)
-    best, ties = _combine_best([(_u64(r[0]), _u64(r[1]), int(r[2]), _f64(r[3]), _f64(r[4]))
-                                for r in allb])
-    n1 = int(allb[:, 5].sum())
-    fail = 0
-    if best is None:
-        fail |= N.SP_FAIL_FEW
-    elif ties != 1:
-        fail |= N.SP_FAIL_TIE
-    if n1 * 10 > n_global * 9:
-        fail |= N.SP_FAIL_MANY
+    def gather_recs():
+        comm.allgather_([b.rec for b in bufs], [b.recs for b in bufs])
+
+    def each(fn, what, *args):
+        for eng in engines:
+            _ck(eng, getattr(eng._lib, fn)(eng.handle, *args), what)
+
+    # extremes -> global (device); sample cells -> sum; F2: histogram -> sum,
+    # P_l records; plan: P_l's in-bucket rank; F3: walk-angle maxima -> max
+    gather_recs()
+    each("gscan_dist_enq_sample", "dist_enq_sample", R)
+    comm.allreduce_([b.cells for b in bufs], "sum")
+    each("gscan_dist_enq_f2", "dist_enq_f2")
+    comm.allreduce_([b.hist for b in bufs], "sum")
+    gather_recs()
+    each("gscan_dist_enq_plan", "dist_enq_plan", R, n_global)
+    gather_recs()
+    each("gscan_dist_enq_f3", "dist_enq_f3", R)
+    for b in bufs:
+        b.phimax.bitwise_xor_(_SIGN)
+    comm.allreduce_([b.phimax for b in bufs], "max")
+    for b in bufs:
+        b.phimax.bitwise_xor_(_SIGN)
+    gather_recs()
+
+    # duplicate check, step 1: hashes by partition; partition range k -> rank k
+    each("gscan_dist_enq_dup_local", "dist_enq_dup_local", R)
+    P = N.SP_PARTS
+    bounds = [(k * P) // R for k in range(R + 1)]
+    widths = [bounds[r + 1] - bounds[r] for r in range(R)]
+    send_tot, cnt_recv = [], []
+    for li, b in enumerate(bufs):
+        pc = b.part_counts.to(torch.int64)
+        send_tot.append(torch.stack([pc[bounds[r]:bounds[r + 1]].sum() for r in range(R)]))
+    me = comm.ranks
+    cnt_recv = comm.all_to_all_flat([b.part_counts for b in bufs], [widths] * len(bufs),
+                                    [[widths[k]] * R for k in me])
+    recv_tot = [c.to(torch.int64).view(R, widths[k]).sum(1) for c, k in zip(cnt_recv, me)]
+
+    # host sync 1
+    pack = torch.cat([bufs[0].recs[: R * L]] + send_tot + recv_tot).cpu().numpy()
+    recs = pack[: R * L].reshape(R, L)
+    off = R * L
+    send_sz = [pack[off + R * k: off + R * (k + 1)].tolist() for k in range(len(bufs))]
+    off += R * len(bufs)
+    recv_sz = [pack[off + R * k: off + R * (k + 1)].tolist() for k in range(len(bufs))]
+    fail = int(np.bitwise_or.reduce(recs[:, _RX_F3 + 3]))
     if fail:
-        return _declined(f"P_l: fail bits {fail:#x} (no point, a tie, or >= 90% of the points survive round 1)")
-    pl = N.gscan_dist_best(best[0], best[1], ties, 0, best[2], best[3])
-
-    # 3. P_l's rank inside its bucket -> sum
-    lbs, fails = [], []
-    for eng, hst in zip(engines, hists):
-        lb, f = C.c_uint64(), C.c_uint32()
-        _ready(dev)
-        _ck(eng, eng._lib.gscan_dist_plan(eng.handle, C.c_void_p(hst.data_ptr()), C.byref(pl), 0,
-                                          C.byref(lb), C.byref(f)), "dist_plan")
-        lbs.append(int(lb.value))
-        fails.append(int(f.value))
-    allv = comm.allgather_i64([[a, b] for a, b in zip(lbs, fails)])
-    if allv[:, 1].any():
-        return _declined(f"ranking P_l: fail bits {allv[:, 1].tolist()}")
-    l_below = int(allv[:, 0].sum())
-
-    # 4. F3: walk-angle maxima -> max, phi range -> min/max; gathered counts
-    phis, rng, ngs, fails = [], [], [], []
-    for eng in engines:
-        pm = i32(N.SP_BUCKETS)
-        pr = (C.c_uint32 * 2)()
-        ng, f = C.c_uint64(), C.c_uint32()
-        _ready(dev)
-        _ck(eng, eng._lib.gscan_dist_phi(eng.handle, l_below, C.c_void_p(pm.data_ptr()), pr,
-                                         C.byref(ng), C.byref(f)), "dist_phi")
-        phis.append(pm.to(torch.int64) & 0xFFFFFFFF)
-        rng.append((int(pr[0]), int(pr[1])))
-        ngs.append(int(ng.value))
-        fails.append(int(f.value))
-    allv = comm.allgather_i64([[a[0], a[1], b] for a, b in zip(rng, fails)])
-    if allv[:, 2].any():
-        return _declined(f"F3: fail bits {allv[:, 2].tolist()}")
+        return _declined(f"fail bits {fail:#x} (P_l, its rank or F3)")
+    n1 = int(recs[:, _RX_F2 + 5].sum())
+    M = int(recs[0, _RX_PLAN + 2])
+    n_g = [int(v) for v in recs[:, _RX_F3 + 2]]
     if _DBG:
-        print(f"[dist] n1={n1} l_below={l_below} n_g={ngs} hist_sum={int(hists[0].to(torch.int64).sum())}")
-    phi_lo = int(allv[:, 0].min())
-    phi_hi = int(allv[:, 1].max())
-    phis = comm.allreduce(phis, "max")
+        print(f"[dist] n1={n1} M={M} n_g={n_g}")
 
-    # duplicate check: this rank's hashes by partition; partition range k -> rank k
-    sends, cnts = [], []
-    for eng in engines:
-        pc = i32(N.SP_PARTS)
-        ptr, nh = C.c_uint64(), C.c_uint64()
-        _ready(dev)
-        _ck(eng, eng._lib.gscan_dist_dup_local(eng.handle, C.c_void_p(pc.data_ptr()), C.byref(ptr),
-                                               C.byref(nh)), "dist_dup_local")
-        parted = _wrap_u64(ptr.value, int(nh.value), dev)
-        pcl = pc.to(torch.int64)
-        bounds = [(k * N.SP_PARTS) // comm.world for k in range(comm.world + 1)]
-        offs = torch.zeros(N.SP_PARTS + 1, dtype=torch.int64, device=dev)
-        offs[1:] = torch.cumsum(pcl, 0)
-        row, crow = [], []
-        for k in range(comm.world):
-            a, b = int(offs[bounds[k]]), int(offs[bounds[k + 1]])
-            row.append(parted[a:b].clone())
-            crow.append(pc[bounds[k]:bounds[k + 1]].clone())
-        sends.append(row)
-        cnts.append(crow)
-    recv = comm.all_to_all(sends)
-    rcnt = comm.all_to_all(cnts)
-    dups = []
-    for li, eng in enumerate(engines):
-        k = comm.ranks[li]
-        lo, hi = (k * N.SP_PARTS) // comm.world, ((k + 1) * N.SP_PARTS) // comm.world
-        mat = torch.zeros((comm.world, N.SP_PARTS), dtype=_U32, device=dev)
-        for s in range(comm.world):
-            mat[s, lo:hi] = rcnt[li][s]
-        blob = torch.cat(recv[li]) if sum(x.numel() for x in recv[li]) else torch.zeros(1, dtype=torch.int64, device=dev)
-        nrecv = sum(x.numel() for x in recv[li])
-        d = C.c_uint32()
-        _ready(dev)
-        _ck(eng, eng._lib.gscan_dist_dup_check(eng.handle, C.c_void_p(blob.data_ptr()), nrecv,
-                                               C.c_void_p(mat.data_ptr()), comm.world, C.byref(d)),
-            "dist_dup_check")
-        dups.append(int(d.value))
-    if comm.allgather_i64([[d] for d in dups]).any():
-        return _declined("possible duplicate points (hash partition exchange)")
+    # duplicate check, step 2: the hash blocks; the receiver checks its partitions
+    parted = [_view(b.raw.parted, max(int(sum(sz)), 1), torch.int64, dev)[: int(sum(sz))]
+              for b, sz in zip(bufs, send_sz)]
+    recv = comm.all_to_all_flat(parted, send_sz, recv_sz)
+    for li, (eng, k) in enumerate(zip(engines, me)):
+        lo, hi = bounds[k], bounds[k + 1]
+        mat = torch.zeros((R, P), dtype=_U32, device=dev)
+        mat[:, lo:hi] = cnt_recv[li].view(R, hi - lo)
+        blob = recv[li] if recv[li].numel() else torch.zeros(1, dtype=torch.int64, device=dev)
+        _ck(eng, eng._lib.gscan_dist_enq_dup_check(eng.handle, C.c_void_p(blob.data_ptr()),
+                                                   int(recv[li].numel()), C.c_void_p(mat.data_ptr()),
+                                                   R), "dist_enq_dup_check")
 
-    # 5. gathered points -> rank 0 (records {x, y, global index, bucket})
-    def export(candidates: int, counts):
+    # gathered points -> rank 0 (records {x, y, global index, bucket}; sizes known)
+    def export(which: int, counts: list[int]):
         out = []
-        for eng, cnt in zip(engines, counts):
+        for eng, k in zip(engines, me):
+            cnt = counts[k]
             xs = torch.empty(max(cnt, 1), dtype=torch.float64, device=dev)
             ys = torch.empty_like(xs)
-            gi, gb = i32(max(cnt, 1)), i32(max(cnt, 1))
-            n = C.c_uint64()
-            _ready(dev)
-            _ck(eng, eng._lib.gscan_dist_export(eng.handle, candidates, C.c_void_p(xs.data_ptr()),
-                                                C.c_void_p(ys.data_ptr()), C.c_void_p(gi.data_ptr()),
-                                                C.c_void_p(gb.data_ptr()), C.byref(n)),
-                "dist_export")
-            k = int(n.value)
-            out.append((xs[:k], ys[:k], gi[:k].to(torch.int64) & 0xFFFFFFFF, gb[:k]))
-        return out
-
-    def to_root(recs):
-        parts = [comm.gather_root([r[j] for r in recs]) for j in range(4)]
+            gi = torch.empty(max(cnt, 1), dtype=_U32, device=dev)
+            gb = torch.empty_like(gi)
+            _ck(eng, eng._lib.gscan_dist_enq_export(eng.handle, which, C.c_void_p(xs.data_ptr()),
+                                                    C.c_void_p(ys.data_ptr()),
+                                                    C.c_void_p(gi.data_ptr()),
+                                                    C.c_void_p(gb.data_ptr())), "dist_enq_export")
+            out.append((xs[:cnt], ys[:cnt], gi[:cnt], gb[:cnt]))
+        parts = [comm.gather_root([r[j] for r in out], sizes=counts) for j in range(4)]
         if parts[0] is None:
             return None
-        x = torch.cat(parts[0])
-        y = torch.cat(parts[1])
-        gi = torch.cat(parts[2])
+        x, y = torch.cat(parts[0]), torch.cat(parts[1])
+        gi = torch.cat(parts[2]).to(torch.int64) & 0xFFFFFFFF
         gb = torch.cat(parts[3])
         order = torch.argsort(gi)
-        return x[order], y[order], gi[order], gb[order]
+        return x[order], y[order], gi[order], gb[order].contiguous()
 
-    groot = to_root(export(0, ngs))
-    if _DBG and groot is not None:
-        print(f"[dist] gathered at root {groot[0].numel()} unique idx {torch.unique(groot[2]).numel()}")
-    root = 0 in comm.ranks
-    r0 = comm.ranks.index(0) if root else None
-    pref = None
+    groot = export(0, n_g)
+    root = 0 in me
+    r0 = me.index(0) if root else None
     if root:
+        eng0, b0 = engines[r0], bufs[r0]
         gx, gy, gg, gb = groot
-        n_g = int(gx.numel())
-        X = torch.cat([torch.tensor([gex.x[4]], dtype=torch.float64, device=dev), gx])
-        Y = torch.cat([torch.tensor([gex.y[4]], dtype=torch.float64, device=dev), gy])
-        lpos = int(torch.searchsorted(gg, torch.tensor([pl.idx], device=dev)).item())
-        eng0 = engines[r0]
-        if lpos < n_g and int(gg[lpos]) == pl.idx:  # P_l is a gathered point
-            pref = i32(N.SP_BUCKETS)
-            pr = (C.c_uint32 * 2)(phi_lo, phi_hi)
-            f = C.c_uint32()
-            pmx = phis[r0].to(_U32)
-            _ready(dev)
-            rc = eng0._lib.gscan_dist_slices(eng0.handle, C.c_void_p(X.data_ptr()),
-                                             C.c_void_p(Y.data_ptr()), n_g,
-                                             C.c_void_p(gb.data_ptr()), 1 + lpos,
-                                             C.c_void_p(pmx.data_ptr()), pr,
-                                             C.c_void_p(pref.data_ptr()), C.byref(f))
-            if rc == N.GSCAN_E_CAPACITY or (rc == 0 and f.value):
-                pref = None
-                _declined(f"dist_slices: rc {rc}, fail bits {f.value:#x}")
-            else:
-                _ck(eng0, rc, "dist_slices")
-    if not _agree(comm, [pref is not None if comm.ranks[k] == 0 else True
-                         for k in range(len(engines))]):
-        return _declined(last_decline or "rank 0 could not sort the gathered points")
-    prefs = comm.bcast_root(pref, [i32(N.SP_BUCKETS) for _ in engines])
+        ng = int(sum(n_g))
+        X = torch.cat([b0.ext[9:10].view(torch.float64), gx])
+        Y = torch.cat([b0.ext[14:15].view(torch.float64), gy])
+        rc = eng0._lib.gscan_dist_enq_slices(eng0.handle, C.c_void_p(X.data_ptr()),
+                                             C.c_void_p(Y.data_ptr()), ng, C.c_void_p(gb.data_ptr()),
+                                             C.c_void_p(gg.data_ptr()), M)
+        if rc == N.GSCAN_E_CAPACITY:  # rank 0 cannot hold them: every rank declines after F4
+            b0.pref[-1].fill_(N.SP_FAIL_CAP)
+        else:
+            _ck(eng0, rc, "dist_enq_slices")
+    comm.bcast_([b.pref for b in bufs])
+    each("gscan_dist_enq_cand", "dist_enq_cand")
+    gather_recs()
 
-    # 6. candidates -> rank 0
-    ncs, fails = [], []
-    for eng, pm in zip(engines, prefs):
-        nc, f = C.c_uint64(), C.c_uint32()
-        _ready(dev)
-        _ck(eng, eng._lib.gscan_dist_cand(eng.handle, C.c_void_p(pm.data_ptr()), C.byref(nc),
-                                          C.byref(f)), "dist_cand")
-        ncs.append(int(nc.value))
-        fails.append(int(f.value))
-    allv = comm.allgather_i64([[a, b] for a, b in zip(ncs, fails)])
-    m_global = int(hists[0].to(torch.int64).sum())
-    n_cand = int(allv[:, 0].sum())
-    if allv[:, 1].any() or n_cand > max(m_global // 8, 65536):
-        return _declined(f"F4: fail bits {allv[:, 1].tolist()}, candidates {n_cand} of {m_global}")
-    croot = to_root(export(1, ncs))
+    # host sync 2
+    recs = bufs[0].recs[: R * L].view(R, L).cpu().numpy()
+    fail = int(np.bitwise_or.reduce(recs[:, _RX_F4 + 1]))
+    n_c = [int(v) for v in recs[:, _RX_F4]]
+    if fail or sum(n_c) > max((M - 1) // 8, 65536):
+        return _declined(f"F4 / duplicate check / rank 0: fail bits {fail:#x}, candidates "
+                         f"{sum(n_c)} of {M - 1}")
+    croot = export(1, n_c)
 
-    # 7. rank 0: walk, certificate, Graham
-    result = None
+    # rank 0: walk, certificate, Graham (its own host wait); its verdict to every rank
+    msg = torch.zeros(3, dtype=torch.int64, device=dev)
+    hull_x = None
     if root:
         cx, cy, cg, cb = croot
-        n_c = int(cx.numel())
-        X2 = torch.cat([X, cx])
-        Y2 = torch.cat([Y, cy])
-        gidx = torch.cat([torch.tensor([gex.idx[4]], dtype=torch.int64, device=dev), gg, cg])
-        hull = i32(max(1 + n_g + n_c, 1))
-        hn, nr, f = C.c_uint64(), C.c_uint64(), C.c_uint32()
-        _ready(dev)
-        rc = eng0._lib.gscan_dist_finish(eng0.handle, C.c_void_p(X2.data_ptr()),
-                                         C.c_void_p(Y2.data_ptr()), n_g, n_c,
-                                         C.c_void_p(cb.data_ptr()), C.c_void_p(hull.data_ptr()),
-                                         hull.numel(), C.byref(hn), C.byref(nr), C.byref(f))
-        if rc == N.GSCAN_E_CAPACITY or (rc == 0 and f.value):
-            result = None
-            _declined(f"dist_finish: rc {rc}, fail bits {f.value:#x}")
+        X2, Y2 = torch.cat([X, cx]), torch.cat([Y, cy])
+        gidx = torch.cat([b0.ext[4:5], gg, cg])
+        hull = torch.empty(max(X2.numel(), 1), dtype=_U32, device=dev)
+        hn, nr, stat, f = C.c_uint64(), C.c_uint64(), C.c_uint32(), C.c_uint32()
+        rc = eng0._lib.gscan_dist_root_finish(eng0.handle, C.c_void_p(X2.data_ptr()),
+                                              C.c_void_p(Y2.data_ptr()), ng, int(sum(n_c)),
+                                              C.c_void_p(cb.data_ptr()), M,
+                                              C.c_void_p(hull.data_ptr()), hull.numel(),
+                                              C.byref(hn), C.byref(nr), C.byref(stat), C.byref(f))
+        if rc == N.GSCAN_E_CAPACITY:
+            stat.value = 2
+            _declined(f"dist_root_finish: {eng0._lib.gscan_last_error(eng0.handle).decode()}")
         else:
-            _ck(eng0, rc, "dist_finish")
-            k = int(hn.value)
-            hv = gidx[hull[:k].to(torch.int64) & 0xFFFFFFFF].cpu().numpy().astype(np.uint64)
-            st = StageStats(n_input=n_global, n_after_round1=n1, n_after_round2=int(nr.value),
-                            hull_size=k)
-            result = (hv, st)
-    if not _agree(comm, [result is not None if comm.ranks[k] == 0 else True
-                         for k in range(len(engines))]):
+            _ck(eng0, rc, "dist_root_finish")
+            if stat.value == 2:
+                _declined(f"rank 0 walk / certificate / Graham: fail bits {f.value:#x}")
+        status, n_r, k = int(stat.value), int(nr.value), int(hn.value)
+        msg[0], msg[1] = status, n_r  # device fills, no host wait
+        if status != 2:
+            hull_x = gidx[hull[:k].to(torch.int64) & 0xFFFFFFFF]
+    msgs = [msg if comm.ranks[k] == 0 else torch.zeros(3, dtype=torch.int64, device=dev)
+            for k in range(len(engines))]
+    comm.bcast_(msgs)
+    if not root:
+        status, n_r, _ = (int(v) for v in msgs[0].cpu().tolist())  # host sync 3
+    if status == 2:
         return _declined(last_decline or "rank 0: walk, certificate or Graham declined")
-    return result if root else (None, None)
+    if status == 1:
+        # the certificate did not prove the skipped points: every rank checks
+        # its own (distributed F6) against rank 0's round-2 output
+        nb = N.SP_BUCKETS
+        vb = []
+        for b, k in zip(bufs, me):
+            if k == 0:
+                vb.append((_view(b.raw.rlo, nb + 1, torch.int32, dev),
+                           _view(b.raw.rx, n_r, torch.float64, dev),
+                           _view(b.raw.ry, n_r, torch.float64, dev)))
+            else:
+                vb.append((torch.empty(nb + 1, dtype=torch.int32, device=dev),
+                           torch.empty(n_r, dtype=torch.float64, device=dev),
+                           torch.empty(n_r, dtype=torch.float64, device=dev)))
+        for j in range(3):
+            comm.bcast_([v[j] for v in vb])
+        for eng, (rl, rx, ry) in zip(engines, vb):
+            _ck(eng, eng._lib.gscan_dist_enq_verify(eng.handle, C.c_void_p(rl.data_ptr()),
+                                                    C.c_void_p(rx.data_ptr()),
+                                                    C.c_void_p(ry.data_ptr())), "dist_enq_verify")
+        gather_recs()
+        recs = bufs[0].recs[: R * L].view(R, L).cpu().numpy()  # host sync 4
+        vfail = int(np.bitwise_or.reduce(recs[:, _RX_VER + 1]))
+        if vfail:
+            return _declined(f"distributed F6: {int(recs[:, _RX_VER].sum())} skipped points "
+                             f"would not be discarded (fail bits {vfail:#x})")
+    if not root:
+        return None, None
+    hv = hull_x.cpu().numpy().astype(np.uint64)  # the output
+    return hv, StageStats(n_input=n_global, n_after_round1=n1, n_after_round2=n_r,
+                          hull_size=int(hv.size))
 
 
 class _DevBuf:
     """__cuda_array_interface__ view of a device buffer owned by a handle."""
 
-    def __init__(self, ptr: int, n: int):
-        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<i8", "data": (ptr, False),
+    def __init__(self, ptr: int, n: int, typestr: str = "<i8"):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, False),
                                          "version": 3, "strides": None}
-
-
-def _wrap_u64(ptr: int, n: int, dev) -> torch.Tensor:
-    """n uint64 (as int64) at device address ptr, copied out of the handle."""
-    if n == 0:
-        return torch.zeros(0, dtype=torch.int64, device=dev)
-    return torch.as_tensor(_DevBuf(ptr, n), device=dev).clone()
 
 
 # ---------------------------------------------------------------------------

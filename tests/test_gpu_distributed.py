@@ -200,3 +200,42 @@ def test_sharded_hull_two_processes_gloo(tmp_path, kind, n):
     assert outs[0][0].startswith("ok")
     if kind != "circle":
         assert "sparse" in outs[0][0], outs[0][0]
+
+
+def test_sharded_distributed_verification(engines, oracle_mod):
+    """Rank 0's certificate forced off (GSCAN_DEBUG_SPARSE_VERIFY): every rank
+    runs F6 on its own shard against rank 0's broadcast round-2 output
+    (distributed F6), and the sharded path still serves, bit-exact."""
+    from paper_1508_05931_b200 import _native as N
+    from paper_1508_05931_b200 import distributed as D
+    from paper_1508_05931_b200 import generate
+
+    xs, ys = generate("disk", 500_000, 21)
+    engines[0].set_debug(N.DEBUG_SPARSE_VERIFY)
+    try:
+        st = _check(engines, oracle_mod, xs, ys, 3)
+    finally:
+        engines[0].set_debug(0)
+    assert st is not None, f"declined: {D.last_decline}"
+
+
+def test_sharded_host_waits(engines, oracle_mod, monkeypatch):
+    """The device-side data plane: one call reads device data back on the
+    host at most four times (three verdict points and the output)."""
+    from paper_1508_05931_b200 import distributed as D
+    from paper_1508_05931_b200 import generate
+
+    xs, ys = generate("square", 400_000, 5)
+    calls = []
+    real_cpu = torch.Tensor.cpu
+
+    def counting_cpu(self, *a, **k):
+        if self.is_cuda:
+            calls.append(tuple(self.shape))
+        return real_cpu(self, *a, **k)
+
+    monkeypatch.setattr(torch.Tensor, "cpu", counting_cpu)
+    st = _check(engines, oracle_mod, xs, ys, 4)
+    monkeypatch.undo()
+    assert st is not None, D.last_decline
+    assert len(calls) <= 4, calls

@@ -212,7 +212,7 @@ COMM_SCRIPT = r"""
 import sys
 sys.path.insert(0, sys.argv[1])
 import torch, torch.distributed as dist
-from paper_1508_05931_b200.distributed import LocalComm, TorchComm, _combine_best
+from paper_1508_05931_b200.distributed import LocalComm, TorchComm
 dist.init_process_group("gloo", init_method="tcp://127.0.0.1:%s" % sys.argv[2],
                         rank=int(sys.argv[3]), world_size=2)
 r = dist.get_rank()
@@ -223,23 +223,44 @@ for op in ("sum", "max", "min"):
     want = lc.allreduce(vals, op)[0]
     got = tc.allreduce([vals[r]], op)[0]
     assert got.dtype == torch.int32 and torch.equal(got, want), (op, got, want)
-objs = [("rank", k, [k] * k) for k in range(2)]
-assert tc.allgather_obj([objs[r]]) == lc.allgather_obj(objs)
+    # in place (the device-side data plane's form)
+    loc = [v.clone() for v in vals]
+    lc.allreduce_(loc, op)
+    mine = vals[r].clone()
+    tc.allreduce_([mine], op)
+    assert torch.equal(mine, loc[r]) and torch.equal(loc[0], loc[1]), (op, mine, loc)
+# fixed records: all-gather into a rank-major block
+rows = [torch.arange(4, dtype=torch.int64) + 100 * k for k in range(2)]
+outs = [torch.zeros(8, dtype=torch.int64) for _ in range(2)]
+lc.allgather_(rows, outs)
+mine = torch.zeros(8, dtype=torch.int64)
+tc.allgather_([rows[r]], [mine])
+assert torch.equal(mine, outs[r]) and torch.equal(mine, torch.cat(rows)), mine
 var = [torch.arange(3 + 5 * k, dtype=torch.float64) * (k + 1) for k in range(2)]
-got = tc.gather_root([var[r]])
-if r == 0:
-    assert all(torch.equal(a, b) for a, b in zip(got, lc.gather_root(var)))
-else:
-    assert got is None
+for sizes in (None, [3, 8]):
+    got = tc.gather_root([var[r]], sizes=sizes)
+    if r == 0:
+        assert all(torch.equal(a, b) for a, b in zip(got, lc.gather_root(var)))
+    else:
+        assert got is None
 b = tc.bcast_root(var[0] if r == 0 else None, [torch.empty_like(var[0])])[0]
 assert torch.equal(b, var[0])
+ib = [var[0].clone(), torch.zeros_like(var[0])]
+lc.bcast_(ib)
+mine = var[0].clone() if r == 0 else torch.zeros_like(var[0])
+tc.bcast_([mine])
+assert torch.equal(mine, var[0]) and torch.equal(ib[1], var[0])
 sends = [[torch.full((2 + s + 3 * d,), 10 * s + d, dtype=torch.int64) for d in range(2)] for s in range(2)]
 got = tc.all_to_all([sends[r]])[0]
 want = lc.all_to_all(sends)[r]
 assert all(torch.equal(a, b) for a, b in zip(got, want)), (got, want)
-# farthest-point combination: lowest global index among equal dist2, ties summed
-best, ties = _combine_best([(5, 9, 1, 0.0, 0.0), (5, 4, 2, 1.0, 1.0), (3, 1, 1, 2.0, 2.0), (0, 0, 0, 0, 0)])
-assert best == (5, 4, 1.0, 1.0) and ties == 3, (best, ties)
+# flat blocks with sizes known on both sides
+flat = [torch.cat(sends[s]) for s in range(2)]
+ss = [[2 + s + 3 * d for d in range(2)] for s in range(2)]
+rs = [[2 + s + 3 * d for s in range(2)] for d in range(2)]
+got = tc.all_to_all_flat([flat[r]], [ss[r]], [rs[r]])[0]
+want = lc.all_to_all_flat(flat, ss, rs)[r]
+assert torch.equal(got, want) and torch.equal(want, torch.cat([sends[s][r] for s in range(2)])), (got, want)
 dist.barrier()
 dist.destroy_process_group()
 print("ok", r)
