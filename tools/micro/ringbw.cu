@@ -3,6 +3,7 @@
 // copies each) on full[] mbarriers; C consumer warps read the tile from
 // shared memory and release it on empty[]. Sweeps T, S, CTAs per SM.
 #include <cstdio>
+#include <cstdlib>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -149,11 +150,24 @@ void run(const double* xs, const double* ys, uint32_t n, double* out, int sms, i
          n * 16.0 / (best * 1e-3) / 1e9, e ? cudaGetErrorString(e) : "");
 }
 
+__global__ void k_fill(double* a, uint32_t n, uint64_t seed) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    uint64_t z = (i + seed * 0x9E3779B97F4A7C15ull) * 0xBF58476D1CE4E5B9ull;
+    z ^= z >> 31; z *= 0x94D049BB133111EBull; z ^= z >> 29;
+    a[i] = (z >> 11) * 0x1.0p-53;
+  }
+}
+
 int main() {
   const uint32_t n = 20000000;
   double *xs, *ys, *out;
   cudaMalloc(&xs, n * 8ull); cudaMalloc(&ys, n * 8ull); cudaMalloc(&out, 8);
   cudaMemset(xs, 0, n * 8ull); cudaMemset(ys, 0, n * 8ull);
+  if (getenv("RINGBW_RANDOM")) {  // uniform doubles in [0, 1) instead of zeros
+    k_fill<<<1184, 256>>>(xs, n, 1);
+    k_fill<<<1184, 256>>>(ys, n, 2);
+    cudaDeviceSynchronize();
+  }
   int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   for (int work : {0, 8, 32}) {
     run_last<3072, 4, 16>(xs, ys, n, out, sms, work);
