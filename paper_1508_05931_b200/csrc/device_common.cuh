@@ -247,4 +247,76 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
   return m;
 }
 
+// Tiles of kBlock x ITEMS items in STRIPED order (item (k, t) = base + k *
+// kBlock + t): every warp-wide load and store of a row is coalesced. The
+// exclusive scan of the ITEMS x kWarps row counts (row-major = index order),
+// by warp 0: s_rows[r] becomes the exclusive offset of row r and
+// s_rows[ITEMS * kWarps] the tile total. All threads call it.
+template <int ITEMS>
+__device__ __forceinline__ uint32_t striped_rows_scan(uint32_t* s_rows) {
+  __syncthreads();  // the row counts are written
+  if ((threadIdx.x >> 5) == 0) {
+    const uint32_t lane = threadIdx.x & 31;
+    uint32_t carry = 0;
+#pragma unroll
+    for (int b = 0; b < ITEMS * kWarps; b += 32) {
+      const bool in = b + (int)lane < ITEMS * kWarps;
+      const uint32_t v = in ? s_rows[b + lane] : 0u;
+      uint32_t x = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if ((int)lane >= o) x += y;
+      }
+      if (in) s_rows[b + lane] = carry + x - v;
+      carry += __shfl_sync(0xffffffffu, x, 31);
+    }
+    if (lane == 0) s_rows[ITEMS * kWarps] = carry;
+  }
+  __syncthreads();
+  return s_rows[ITEMS * kWarps];
+}
+
+// Ranks (index order) of the kept items of a striped tile; returns the tile's
+// kept count. s_rows: ITEMS * kWarps + 1 words.
+template <int ITEMS>
+__device__ __forceinline__ uint32_t striped_keep_ranks(const bool (&keep)[ITEMS], uint32_t (&rank)[ITEMS],
+                                                       uint32_t* s_rows) {
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t bal[ITEMS];
+#pragma unroll
+  for (int k = 0; k < ITEMS; ++k) {
+    bal[k] = __ballot_sync(0xffffffffu, keep[k]);
+    if (lane == 0) s_rows[k * kWarps + warp] = __popc(bal[k]);
+  }
+  const uint32_t total = striped_rows_scan<ITEMS>(s_rows);
+#pragma unroll
+  for (int k = 0; k < ITEMS; ++k) rank[k] = s_rows[k * kWarps + warp] + __popc(bal[k] & lanemask_lt());
+  return total;
+}
+
+// Exclusive prefix (index order) of per-item counts of a striped tile;
+// returns the tile total.
+template <int ITEMS>
+__device__ __forceinline__ uint32_t striped_exclusive(const uint32_t (&v)[ITEMS], uint32_t (&ex)[ITEMS],
+                                                      uint32_t* s_rows) {
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t incl[ITEMS];
+#pragma unroll
+  for (int k = 0; k < ITEMS; ++k) {
+    uint32_t x = v[k];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if ((int)lane >= o) x += y;
+    }
+    incl[k] = x;
+    if (lane == 31) s_rows[k * kWarps + warp] = x;
+  }
+  const uint32_t total = striped_rows_scan<ITEMS>(s_rows);
+#pragma unroll
+  for (int k = 0; k < ITEMS; ++k) ex[k] = s_rows[k * kWarps + warp] + incl[k] - v[k];
+  return total;
+}
+
 }  // namespace gscan

@@ -317,31 +317,37 @@ __global__ void k_graham_junction_apply(const uint32_t* __restrict__ chain,
                                         uint32_t* __restrict__ parent, uint32_t* __restrict__ btop,
                                         uint32_t* __restrict__ keep_len,
                                         uint32_t* __restrict__ fail) {
-  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+  // a warp per chunk: the chain's links are independent, so the lanes write
+  // them together (coalesced chain reads; a thread per chunk walking its
+  // chain was bound by the strided loads)
+  const uint32_t c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t lane = threadIdx.x & 31;
   if (c > nchunks) return;
   if (c == nchunks) {  // boundary after the last chunk
-    btop[nchunks] = chain[(nchunks - 1) * kChunk + chain_len[nchunks - 1] - 1];
+    if (lane == 0) btop[nchunks] = chain[(nchunks - 1) * kChunk + chain_len[nchunks - 1] - 1];
     return;
   }
   const uint32_t* L = chain + c * kChunk;
   const int len = chain_len[c];
   const int e = je[c];
-  const int kill_top = (c + 1 < nchunks) ? (int)jk[c + 1] : 0;  // popped by the next junction
-  if (c > 0) {
-    const int la = chain_len[c - 1];
-    const int e_prev = je[c - 1];
-    const int k = jk[c];
-    if (jmin[c] < e_prev || (c >= 2 && la - k <= e_prev)) atomicAdd(fail, 1u);
-    const int below = la - 1 - k;  // A's top after the junction pops (c == 1 may empty A)
-    parent[L[e]] = (below >= 0) ? chain[(c - 1) * kChunk + below] : kNone;
-    btop[c] = chain[(c - 1) * kChunk + la - 1];
-  } else {
-    parent[L[0]] = kNone;
-    btop[0] = kNone;
+  if (lane == 0) {
+    const int kill_top = (c + 1 < nchunks) ? (int)jk[c + 1] : 0;  // popped by the next junction
+    if (c > 0) {
+      const int la = chain_len[c - 1];
+      const int e_prev = je[c - 1];
+      const int k = jk[c];
+      if (jmin[c] < e_prev || (c >= 2 && la - k <= e_prev)) atomicAdd(fail, 1u);
+      const int below = la - 1 - k;  // A's top after the junction pops (c == 1 may empty A)
+      parent[L[e]] = (below >= 0) ? chain[(c - 1) * kChunk + below] : kNone;
+      btop[c] = chain[(c - 1) * kChunk + la - 1];
+    } else {
+      parent[L[0]] = kNone;
+      btop[0] = kNone;
+    }
+    if (e + kill_top > len - 1 && c + 1 < nchunks) atomicAdd(fail, 1u);
+    keep_len[c] = (uint32_t)max(0, len - kill_top - e);
   }
-  for (int i = e + 1; i < len; ++i) parent[L[i]] = L[i - 1];
-  if (e + kill_top > len - 1 && c + 1 < nchunks) atomicAdd(fail, 1u);
-  keep_len[c] = (uint32_t)max(0, len - kill_top - e);
+  for (int i = e + 1 + (int)lane; i < len; i += 32) parent[L[i]] = L[i - 1];
 }
 
 __global__ void k_graham_junction_emit(const uint32_t* __restrict__ chain,

@@ -909,7 +909,7 @@ int stage_graham(gscan_handle* h, const double* Rx, const double* Ry, const uint
     }
     {
       Launch L(h, "k_graham_junction_apply");
-      k_graham_junction_apply<<<(nch + 1 + 127) / 128, 128, 0, h->stream>>>(
+      k_graham_junction_apply<<<(nch + 1 + 7) / 8, 256, 0, h->stream>>>(
           h->g_chain, h->g_len, nch, h->g_jk, h->g_je, h->g_jmin, h->g_parent, h->g_btop,
           h->g_keep, fail_d);
     }

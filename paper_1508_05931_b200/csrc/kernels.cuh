@@ -603,6 +603,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_filter_keys(
 // ===========================================================================
 // Device-wide exclusive scan of uint32 counts (decoupled look-back); used for
 // bucket offsets. out[i] = sum(in[0..i)); out[n] = total when n_out > n.
+// Tiles are striped (coalesced loads and stores; striped_exclusive).
 constexpr int kScanItems = 8;
 constexpr int kScanTile = kBlock * kScanItems;
 
@@ -610,30 +611,27 @@ __global__ void __launch_bounds__(kBlock) k_scan_u32(const uint32_t* __restrict_
                                                      uint32_t* __restrict__ out,
                                                      uint64_t* __restrict__ status,
                                                      Counters* __restrict__ ctr) {
-  __shared__ uint32_t s_tile, s_warp[kWarps], s_excl;
+  __shared__ uint32_t s_tile, s_excl, s_rows[kScanItems * kWarps + 1];
   if (threadIdx.x == 0) s_tile = atomicAdd(&ctr->tile_ticket, 1u);
   __syncthreads();
   const uint32_t tile = s_tile;
-  const uint32_t base = tile * kScanTile + threadIdx.x * kScanItems;
-  uint32_t v[kScanItems];
-  uint32_t sum = 0;
+  const uint32_t base = tile * kScanTile;  // striped: item (k, t) = base + k * kBlock + t
+  uint32_t v[kScanItems], ex[kScanItems];
 #pragma unroll
   for (int k = 0; k < kScanItems; ++k) {
-    v[k] = (base + k < n) ? in[base + k] : 0u;
-    sum += v[k];
+    const uint32_t i = base + k * kBlock + threadIdx.x;
+    v[k] = i < n ? in[i] : 0u;
   }
-  uint32_t total;
-  const uint32_t texcl = block_exclusive_scan(sum, s_warp, &total);
+  const uint32_t total = striped_exclusive<kScanItems>(v, ex, s_rows);
   if (threadIdx.x < 32) {
     const uint64_t e = lookback_exclusive(status, tile, total);
     if (threadIdx.x == 0) s_excl = (uint32_t)e;
   }
   __syncthreads();
-  uint32_t run = s_excl + texcl;
 #pragma unroll
   for (int k = 0; k < kScanItems; ++k) {
-    if (base + k <= n) out[base + k] = run;  // out[n] = grand total
-    run += v[k];
+    const uint32_t i = base + k * kBlock + threadIdx.x;
+    if (i <= n) out[i] = s_excl + ex[k];  // out[n] = grand total
   }
 }
 
@@ -1020,26 +1018,22 @@ __global__ void __launch_bounds__(kBlock) k_compact_xyi(
     uint32_t n_host, double* __restrict__ out_x, double* __restrict__ out_y,
     uint32_t* __restrict__ out_i, uint64_t* __restrict__ status, Counters* __restrict__ ctr,
     uint32_t* __restrict__ n_out) {
-  __shared__ uint32_t s_tile, s_warp[kWarps], s_excl;
+  __shared__ uint32_t s_tile, s_excl, s_rows[kCompactItems * kWarps + 1];
   const uint32_t n = n_dev ? *n_dev : n_host;
   if (threadIdx.x == 0) s_tile = atomicAdd(&ctr->tile_ticket, 1u);
   __syncthreads();
   const uint32_t tile = s_tile;
-  const uint32_t base = tile * kCompactTile;
-  // blocked arrangement: thread t owns items base + t*kItems .. +kItems-1
-  const uint32_t first = base + threadIdx.x * kCompactItems;
+  const uint32_t base = tile * kCompactTile;  // striped: item (k, t) = base + k * kBlock + t
   bool keep[kCompactItems];
-  uint32_t cnt = 0;
 #pragma unroll
   for (int k = 0; k < kCompactItems; ++k) {
-    const uint32_t i = first + k;
+    const uint32_t i = base + k * kBlock + threadIdx.x;
     bool kp = false;
     if (i < n) kp = (kMode == 0) ? (in_i[i] != kDead) : (flags[i] != 0);
     keep[k] = kp;
-    cnt += kp;
   }
-  uint32_t total;
-  const uint32_t texcl = block_exclusive_scan(cnt, s_warp, &total);
+  uint32_t rk[kCompactItems];
+  const uint32_t total = striped_keep_ranks<kCompactItems>(keep, rk, s_rows);
   if (threadIdx.x < 32) {
     const uint64_t e = lookback_exclusive(status, tile, total);
     if (threadIdx.x == 0) {
@@ -1048,15 +1042,13 @@ __global__ void __launch_bounds__(kBlock) k_compact_xyi(
     }
   }
   __syncthreads();
-  uint32_t o = s_excl + texcl;
 #pragma unroll
   for (int k = 0; k < kCompactItems; ++k) {
     if (keep[k]) {
-      const uint32_t i = first + k;
+      const uint32_t i = base + k * kBlock + threadIdx.x, o = s_excl + rk[k];
       out_x[o] = in_x[i];
       out_y[o] = in_y[i];
       out_i[o] = in_i[i];
-      ++o;
     }
   }
 }

@@ -3061,25 +3061,22 @@ __global__ void __launch_bounds__(kBlock) k_sp_compact(
     double* __restrict__ out_x, double* __restrict__ out_y, uint32_t* __restrict__ out_i,
     uint32_t* __restrict__ out_b, uint32_t* __restrict__ out_s, uint64_t* __restrict__ status,
     Counters* __restrict__ ctr) {
-  __shared__ uint32_t s_tile, s_warp[kWarps], s_excl;
+  __shared__ uint32_t s_tile, s_excl, s_rows[kCompactItems * kWarps + 1];
   if (st->fail) return;
   const uint32_t n = st->n_w;
   if (threadIdx.x == 0) s_tile = atomicAdd(&ctr->tile_ticket, 1u);
   __syncthreads();
   const uint32_t tile = s_tile;
-  const uint32_t base = tile * kCompactTile;
+  const uint32_t base = tile * kCompactTile;  // striped: item (k, t) = base + k * kBlock + t
   if (base >= n) return;
-  const uint32_t first = base + threadIdx.x * kCompactItems;
   bool keep[kCompactItems];
-  uint32_t cnt = 0;
 #pragma unroll
   for (int k = 0; k < kCompactItems; ++k) {
-    const uint32_t i = first + k;
+    const uint32_t i = base + k * kBlock + threadIdx.x;
     keep[k] = i < n && flags[i] != 0;
-    cnt += keep[k];
   }
-  uint32_t total;
-  const uint32_t texcl = block_exclusive_scan(cnt, s_warp, &total);
+  uint32_t rk[kCompactItems];
+  const uint32_t total = striped_keep_ranks<kCompactItems>(keep, rk, s_rows);
   if (threadIdx.x < 32) {
     const uint64_t e = lookback_exclusive(status, tile, total);
     if (threadIdx.x == 0) {
@@ -3088,17 +3085,15 @@ __global__ void __launch_bounds__(kBlock) k_sp_compact(
     }
   }
   __syncthreads();
-  uint32_t o = s_excl + texcl;
 #pragma unroll
   for (int k = 0; k < kCompactItems; ++k) {
     if (keep[k]) {
-      const uint32_t i = first + k;
+      const uint32_t i = base + k * kBlock + threadIdx.x, o = s_excl + rk[k];
       out_x[o] = in_x[i];
       out_y[o] = in_y[i];
       out_i[o] = in_i[i];
       out_b[o] = in_b[i];
       out_s[o] = in_s[i];
-      ++o;
     }
   }
 }
