@@ -350,15 +350,31 @@ __global__ void k_graham_junction_apply(const uint32_t* __restrict__ chain,
   for (int i = e + 1 + (int)lane; i < len; i += 32) parent[L[i]] = L[i - 1];
 }
 
-__global__ void k_graham_junction_emit(const uint32_t* __restrict__ chain,
-                                       const uint32_t* __restrict__ je,
-                                       const uint32_t* __restrict__ keep_len,
-                                       const uint32_t* __restrict__ off, uint32_t nchunks,
-                                       uint32_t* __restrict__ stack) {
-  const uint32_t c = blockIdx.x * (blockDim.x / kChunk) + threadIdx.x / kChunk;
-  const uint32_t k = threadIdx.x % kChunk;
+__global__ void __launch_bounds__(256) k_graham_junction_emit(const uint32_t* __restrict__ chain,
+                                                           const uint32_t* __restrict__ je,
+                                                           const uint32_t* __restrict__ keep_len,
+                                                           const uint32_t* __restrict__ off,
+                                                           uint32_t nchunks,
+                                                           uint32_t* __restrict__ stack) {
+  // a warp per chunk, kChunk / 32 elements per lane: the chunk's offsets are
+  // read once and the element copies are independent (in flight together)
+  const uint32_t c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t lane = threadIdx.x & 31;
   if (c >= nchunks) return;
-  if (k < keep_len[c]) stack[off[c] + k] = chain[c * kChunk + je[c] + k];
+  const uint32_t len = keep_len[c], o = off[c];
+  const uint32_t* src = chain + (size_t)c * kChunk + je[c];
+  constexpr int kPer = kChunk / 32;
+  uint32_t v[kPer];
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {
+    const uint32_t k = lane + 32u * u;
+    v[u] = k < len ? src[k] : 0u;
+  }
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {
+    const uint32_t k = lane + 32u * u;
+    if (k < len) stack[o + k] = v[u];
+  }
 }
 
 // Step 3: certificate. Thread per chunk: replay the chunk's points from the
@@ -643,8 +659,19 @@ __global__ void k_graham_emit(const uint32_t* __restrict__ stack, const uint32_t
                               const uint32_t* __restrict__ R_i, uint32_t* __restrict__ out_idx,
                               Counters* __restrict__ ctr) {
   const uint32_t len = *len_dev;
-  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < len; k += gridDim.x * blockDim.x)
-    out_idx[k] = R_i[stack[k]];
+  const uint32_t nth = gridDim.x * blockDim.x;
+  uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  for (; k + 3 * nth < len; k += 4 * nth) {  // four independent gathers in flight
+    uint32_t p[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) p[u] = stack[k + u * nth];
+    uint32_t q[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) q[u] = R_i[p[u]];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) out_idx[k + u * nth] = q[u];
+  }
+  for (; k < len; k += nth) out_idx[k] = R_i[stack[k]];
   if (blockIdx.x == 0 && threadIdx.x == 0) ctr->hull = len;
 }
 

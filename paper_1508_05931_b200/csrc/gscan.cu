@@ -929,7 +929,7 @@ int stage_graham(gscan_handle* h, const double* Rx, const double* Ry, const uint
     TRY(scan_u32(h, h->g_keep, nch, h->g_off));
     {
       Launch L(h, "k_graham_junction_emit");
-      k_graham_junction_emit<<<(nch + 7) / 8, 8 * kChunk, 0, h->stream>>>(
+      k_graham_junction_emit<<<(nch + 7) / 8, 256, 0, h->stream>>>(
           h->g_chain, h->g_je, h->g_keep, h->g_off, nch, h->stack);
     }
     CU(cudaMemcpyAsync(len_d, h->g_off + nch, 4, cudaMemcpyDeviceToDevice, h->stream));
