@@ -1708,8 +1708,13 @@ __global__ void __launch_bounds__(1024) k_sp_dup_part(const uint64_t* __restrict
 #endif
 constexpr uint32_t kSpDupGroups = GSCAN_DUPS_G;
 constexpr uint32_t kSpDupGT = 1024 / kSpDupGroups;                       // threads per group
-constexpr uint32_t kSpDupGSlots = kSpDupGroups == 2 ? 16384u : 12288u;  // slots per group table
-constexpr uint32_t kSpDupGRound = 8192;  // entries per round (load <= 0.5 / 0.67)
+// slots per group table: C2 measured 16384 -> 103 us, 20480 -> 92, 24576 -> 88,
+// 26624 -> 89 (k_sp_dups; shorter probe runs, the warp loops max over lanes)
+#ifndef GSCAN_DUPS_SLOTS
+#define GSCAN_DUPS_SLOTS (kSpDupGroups == 2 ? 24576u : 12288u)
+#endif
+constexpr uint32_t kSpDupGSlots = GSCAN_DUPS_SLOTS;
+constexpr uint32_t kSpDupGRound = 8192;  // entries per round (load <= 1/3 at 24576 slots)
 constexpr uint32_t kSpDupIdxBits = 15;     // index bits of a slot (tag: the other 17)
 constexpr uint32_t kSpDupIdxBitsBig = 21;  // partitions of 2^15 entries or more
 static_assert(32 + (32 - kSpDupIdxBits) <= 64 - kSpPartBits, "tag bits overlap the partition");
