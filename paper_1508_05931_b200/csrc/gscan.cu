@@ -38,6 +38,9 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
 }
 
 // ~ns of GPU time (profiling mode only; see run_sparse)
+#ifdef GSCAN_STAMP
+__global__ void k_stamp(unsigned long long* p) { *p = globaltimer_ns(); }
+#endif
 __global__ void k_busy_wait(unsigned long long ns) {
   const unsigned long long t0 = globaltimer_ns();
   while (globaltimer_ns() - t0 < ns) __nanosleep(1000);
@@ -1586,7 +1589,26 @@ int run_sparse(gscan_handle* h, const double* xs, const double* ys, uint32_t n,
       h->sp_key = key;
       h->sp_graph_ok = true;
     }
+#ifdef GSCAN_STAMP  // diagnostics build: when each stream finished, relative to the graph's start
+    static unsigned long long* stamp = nullptr;
+    if (!stamp) cudaMallocManaged(&stamp, 64);
+    k_stamp<<<1, 1, 0, s>>>(stamp + 2);
+#endif
     CU(cudaGraphLaunch(h->sp_graph_exec, s));
+#ifdef GSCAN_STAMP
+    k_stamp<<<1, 1, 0, s>>>(stamp + 0);
+    if (dup_check) {
+      TRY(sparse_dup_check(h, n));
+      k_stamp<<<1, 1, 0, h->side>>>(stamp + 1);
+      CU(cudaStreamWaitEvent(s, h->ev_dup, 0));
+      CU(cudaMemcpyAsync(&h->h_sp->fail, &h->sp_st->fail, 4, cudaMemcpyDeviceToHost, s));
+    }
+    TRY(sync_counters(h));
+    fprintf(stderr, "[stamp] main %.1f us side %.1f us\n", (stamp[0] - stamp[2]) / 1e3,
+            (stamp[1] - stamp[2]) / 1e3);
+    h->launches += h->sp_graph_launches;
+    goto read_back;
+#endif
     h->launches += h->sp_graph_launches;
   }
 enqueued:
@@ -1597,6 +1619,9 @@ enqueued:
     CU(cudaMemcpyAsync(&h->h_sp->fail, &h->sp_st->fail, 4, cudaMemcpyDeviceToHost, s));
   }
   TRY(sync_counters(h));
+#ifdef GSCAN_STAMP
+read_back:
+#endif
   const SpState sp = *h->h_sp;
   if (h->sp_debug) sp_debug_print(h, "[run]");
   h->sp_fail = sp.fail | ((sp.fail & kSpFailInternal) ? (sp.why << 16) : 0u);
