@@ -1,3 +1,4 @@
+#include <chrono>
 // Host orchestration and C-ABI of the B200 gScan hull path (include/gscan.h).
 //
 // One call = the reference's full_pipeline (pipeline.hpp:72-123) as a chain
@@ -40,7 +41,34 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
 // ~ns of GPU time (profiling mode only; see run_sparse)
 #ifdef GSCAN_STAMP
 __global__ void k_stamp(unsigned long long* p) { *p = globaltimer_ns(); }
+double g_host[4], g_host_prev_gap = 0, g_host_last_exit = 0;
+void host_mark(int k) {
+  const double t = std::chrono::duration<double, std::micro>(
+                       std::chrono::steady_clock::now().time_since_epoch()).count();
+  static std::vector<double> hrows;
+  if (k == 0 && g_host_last_exit > 0) {
+    hrows.push_back(g_host[1] - g_host[0]);
+    hrows.push_back(g_host[2] - g_host[1]);
+    hrows.push_back(g_host[3] - g_host[2]);
+    hrows.push_back(t - g_host_last_exit);
+    if (hrows.size() == 4 * 40) {
+      for (size_t r = 0; r < hrows.size(); r += 4)
+        fprintf(stderr, "[host] entry->launch %.1f, launch->sync return %.1f, sync return->exit %.1f, exit->entry %.1f us\n",
+                hrows[r], hrows[r + 1], hrows[r + 2], hrows[r + 3]);
+      hrows.clear();
+    }
+  }
+  g_host[k] = t;
+  if (k == 3) g_host_last_exit = t;
+}
 #endif
+// The hull (count read on the device) into the caller's buffer, capacity-bounded.
+__global__ void k_copy_out(const uint32_t* __restrict__ src, const Counters* __restrict__ ctr,
+                           uint32_t* __restrict__ dst, uint64_t cap) {
+  const uint64_t k = min((uint64_t)ctr->hull, cap);
+  for (uint64_t i = blockIdx.x * blockDim.x + threadIdx.x; i < k; i += gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
 __global__ void k_busy_wait(unsigned long long ns) {
   const unsigned long long t0 = globaltimer_ns();
   while (globaltimer_ns() - t0 < ns) __nanosleep(1000);
@@ -122,6 +150,11 @@ struct gscan_handle {
   uint8_t* flags = nullptr;
   uint32_t* stack = nullptr;
   uint32_t* d_out = nullptr;
+  // the caller's device output of the current gscan_hull_f64_device call:
+  // the sparse path copies the hull there on the device before its one sync
+  uint32_t* user_out = nullptr;
+  uint64_t user_cap = 0;
+  bool user_out_done = false;
   uint64_t* status = nullptr;
   uint64_t status_cap = 0;
   uint32_t *hist = nullptr, *bstart = nullptr, *cursor = nullptr, *oversize = nullptr;
@@ -1050,6 +1083,19 @@ int sparse_init(gscan_handle* h) {
 
 // Event record usable inside stream capture (as an external event node, so
 // elapsed times still work after graph launches) and outside of it.
+// Stage boundary k (0..5) of the sparse path: inside a captured graph a
+// one-thread kernel stores %globaltimer into the counters (read back with
+// them), since six cudaEventElapsedTime calls cost ~17 us of host time per
+// call; outside a capture (profiling, no graphs) an event.
+__global__ void k_tstamp(Counters* __restrict__ ctr, int k) { ctr->tstamp[k] = globaltimer_ns(); }
+int stage_mark(gscan_handle* h, int k, cudaStream_t s) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  CU(cudaStreamIsCapturing(s, &cs));
+  if (cs == cudaStreamCaptureStatusActive) k_tstamp<<<1, 1, 0, s>>>(h->ctr, k);
+  else CU(cudaEventRecord(h->ev[k], s));
+  return GSCAN_OK;
+}
+
 int rec_event(gscan_handle* h, cudaEvent_t e, cudaStream_t s) {
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   CU(cudaStreamIsCapturing(s, &cs));
@@ -1110,8 +1156,8 @@ SpCtx sp_ctx(gscan_handle* h, const double* xs, const double* ys, uint32_t n, ui
 
 int sp_seg_init(gscan_handle* h, const SpCtx& c) {
   cudaStream_t s = c.s;
-  TRY(rec_event(h, h->ev[0], s));
   CU(cudaMemsetAsync(h->ctr, 0, sizeof(Counters), s));
+  TRY(stage_mark(h, 0, s));
   CU(cudaMemsetAsync(h->sp_st, 0, sizeof(SpState), s));
   CU(cudaMemsetAsync(h->sp_gcnt, 0, c.nb * 4, s));
   CU(cudaMemsetAsync(h->sp_ccnt, 0, c.nb * 4, s));
@@ -1231,7 +1277,7 @@ int sp_seg_f3(gscan_handle* h, const SpCtx& c) {
     k_sp_gsize<<<(c.nb + 255) / 256, 256, 0, s>>>(h->sp_gbits, h->sp_hist, h->sp_gsz);
   }
   if (!c.sharded) TRY(scan_u32_slot(h, h->sp_gsz, c.nb, h->sp_gs, kLbGs, s));
-  TRY(rec_event(h, h->ev[1], s));
+  TRY(stage_mark(h, 1, s));
   {
     Launch L(h, "k_sp_phi", s);
     const uint32_t t3 = kF3Split ? 1024u : (uint32_t)kSpF3Threads;
@@ -1299,7 +1345,7 @@ int sp_seg_sortg(gscan_handle* h, const SpCtx& c, const double* gx, const double
         h->sp_st, h->sp_bstart, c.gs, h->sp_gbits, h->sp_phimax, h->A_x, h->A_y, h->ext,
         h->sp_prefmax, h->sp_slice);
   }
-  TRY(rec_event(h, h->ev[2], s));
+  TRY(stage_mark(h, 2, s));
   return GSCAN_OK;
 }
 
@@ -1363,7 +1409,7 @@ int sp_seg_walk(gscan_handle* h, const SpCtx& c, const double* cx, const double*
         h->sp_glist, h->sp_bstart, c.gs, h->sp_hist, h->sp_wstart, h->A_x, h->A_y, h->A_i, h->ext,
         h->sp_st, h->C_x, h->C_y, h->C_i, h->sp_Wb, h->sp_Ws, h->flags);
   }
-  TRY(rec_event(h, h->ev[3], s));
+  TRY(stage_mark(h, 3, s));
   {
     Launch L(h, "k_sp_segments", s);
     k_sp_segments<<<h->sm_count * 8, kBlock, 0, s>>>(h->sp_Ws, h->sp_st, h->sp_seglo, h->sp_seghi);
@@ -1414,14 +1460,14 @@ int sp_seg_verify(gscan_handle* h, const SpCtx& c) {
 
 int sp_seg_tail(gscan_handle* h, const SpCtx& c) {
   cudaStream_t s = c.s;
-  TRY(rec_event(h, h->ev[4], s));
+  TRY(stage_mark(h, 4, s));
   CU(cudaMemcpyAsync(h->h_sp, h->sp_st, sizeof(SpState), cudaMemcpyDeviceToHost, s));
   CU(cudaMemcpyAsync(&h->ctr->n2, &h->sp_st->n_r, 4, cudaMemcpyDeviceToDevice, s));
   // K7/K8 in the same graph: the tree strategy over the round-2 buffer, its
   // size read on the device; it no-ops when the sparse path failed
   TRY(tree_enqueue(h, h->A_x, h->A_y, h->A_i, &h->sp_st->n_r, 0, &h->sp_st->fail,
                    tree_forced_off(h), s));
-  TRY(rec_event(h, h->ev[5], s));
+  TRY(stage_mark(h, 5, s));
   return GSCAN_OK;
 }
 
@@ -1548,7 +1594,8 @@ int run_sparse(gscan_handle* h, const double* xs, const double* ys, uint32_t n,
   TRY(tree_workspace(h, std::min<uint32_t>(n, kTreeMaxN)));  // no allocation inside the capture
   const void* bufs[7] = {h->A_x, h->A_y, h->A_i, h->C_x, h->C_y, h->C_i, h->tw_pool};
   for (int k = 0; k < 7; ++k) key.bufs[k] = bufs[k];
-  if (h->profiling || !h->use_graphs) {
+  bool graph_path = !(h->profiling || !h->use_graphs);
+  if (!graph_path) {
     // profiling: a short busy kernel first keeps the stream occupied while the
     // host enqueues the per-kernel events and launches, so each event pair
     // brackets its kernel and not the host's launch latency
@@ -1579,6 +1626,7 @@ int run_sparse(gscan_handle* h, const double* xs, const double* ys, uint32_t n,
           fprintf(stderr, "[sparse] graph capture disabled: %s / %s / %s\n", h->err.c_str(),
                   cudaGetErrorString(ce), cudaGetErrorString(ie));
         h->use_graphs = false;
+        graph_path = false;
         h->launches = l0;
         if (h->sp_graph_exec) { cudaGraphExecDestroy(h->sp_graph_exec); h->sp_graph_exec = nullptr; }
         TRY(sparse_enqueue(h, xs, ys, n, cfg));
@@ -1590,12 +1638,14 @@ int run_sparse(gscan_handle* h, const double* xs, const double* ys, uint32_t n,
       h->sp_graph_ok = true;
     }
 #ifdef GSCAN_STAMP  // diagnostics build: when each stream finished, relative to the graph's start
+    host_mark(1);
     static unsigned long long* stamp = nullptr;
-    if (!stamp) cudaMallocManaged(&stamp, 64);
+    if (!stamp) cudaHostAlloc(&stamp, 64, cudaHostAllocMapped);
     k_stamp<<<1, 1, 0, s>>>(stamp + 2);
 #endif
     CU(cudaGraphLaunch(h->sp_graph_exec, s));
 #ifdef GSCAN_STAMP
+    if (h->user_out) k_copy_out<<<8, 256, 0, s>>>(h->d_out, h->ctr, h->user_out, h->user_cap);
     k_stamp<<<1, 1, 0, s>>>(stamp + 0);
     if (dup_check) {
       TRY(sparse_dup_check(h, n));
@@ -1604,14 +1654,29 @@ int run_sparse(gscan_handle* h, const double* xs, const double* ys, uint32_t n,
       CU(cudaMemcpyAsync(&h->h_sp->fail, &h->sp_st->fail, 4, cudaMemcpyDeviceToHost, s));
     }
     TRY(sync_counters(h));
-    fprintf(stderr, "[stamp] main %.1f us side %.1f us\n", (stamp[0] - stamp[2]) / 1e3,
-            (stamp[1] - stamp[2]) / 1e3);
+    host_mark(2);
+    static unsigned long long prev_end = 0;
+    static std::vector<double> rows;
+    rows.push_back((stamp[0] - stamp[2]) / 1e3);
+    rows.push_back((stamp[1] - stamp[2]) / 1e3);
+    rows.push_back(prev_end ? (stamp[2] - prev_end) / 1e3 : 0.0);
+    prev_end = std::max(stamp[0], stamp[1]);
+    if (rows.size() == 3 * 1000) {  // one print per 1000 calls (printing widens its own gap)
+      for (size_t r = 0; r < rows.size(); r += 3)
+        fprintf(stderr, "[stamp] main %.1f us side %.1f us gap before %.1f us\n", rows[r], rows[r + 1], rows[r + 2]);
+      rows.clear();
+
+    }
     h->launches += h->sp_graph_launches;
     goto read_back;
 #endif
     h->launches += h->sp_graph_launches;
   }
 enqueued:
+  if (h->user_out) {  // the tree's hull straight into the caller's buffer (no second sync)
+    k_copy_out<<<8, 256, 0, s>>>(h->d_out, h->ctr, h->user_out, h->user_cap);
+    CU(cudaGetLastError());
+  }
   if (dup_check) {
     // the duplicate check's verdict joins the state read-back: one sync
     TRY(sparse_dup_check(h, n));
@@ -1636,9 +1701,11 @@ read_back:
     h->graham_fails = 0;
     bool done = false;
     TRY(tree_finish(h, h->A_x, h->A_y, h->A_i, &done));
+    h->user_out_done = done && h->user_out && !(h->debug & GSCAN_DEBUG_FORCE_FALLBACK);
     if (!done) {  // the tree declined: the other strategies, launched from here
       TRY(stage_graham(h, h->A_x, h->A_y, h->A_i, sp.n_r, /*skip_tree=*/true));
-      CU(cudaEventRecord(h->ev[5], s));
+      if (graph_path) k_tstamp<<<1, 1, 0, s>>>(h->ctr, 5);
+      else CU(cudaEventRecord(h->ev[5], s));
     }
     // the tree's result (hull count) came with the first read-back, unless
     // more work was launched since
@@ -1651,12 +1718,23 @@ read_back:
     st->n_after_round1 = cc.n1;
     st->n_after_round2 = sp.n_r;
     st->hull_size = cc.hull;
-    st->t_round1_ms = ev_ms(h->ev[0], h->ev[1]);
-    st->t_annotate_ms = ev_ms(h->ev[1], h->ev[2]);
-    st->t_sort_ms = ev_ms(h->ev[2], h->ev[3]);
-    st->t_round2_ms = ev_ms(h->ev[3], h->ev[4]);
-    st->t_finalize_ms = ev_ms(h->ev[4], h->ev[5]);
-    st->t_total_ms = ev_ms(h->ev[0], h->ev[5]);
+    if (graph_path) {  // the graph's stage stamps, read back with the counters
+      const uint64_t* t = cc.tstamp;
+      auto ms = [&](int a, int b) { return (float)((double)(t[b] - t[a]) * 1e-6); };
+      st->t_round1_ms = ms(0, 1);
+      st->t_annotate_ms = ms(1, 2);
+      st->t_sort_ms = ms(2, 3);
+      st->t_round2_ms = ms(3, 4);
+      st->t_finalize_ms = ms(4, 5);
+      st->t_total_ms = ms(0, 5);
+    } else {
+      st->t_round1_ms = ev_ms(h->ev[0], h->ev[1]);
+      st->t_annotate_ms = ev_ms(h->ev[1], h->ev[2]);
+      st->t_sort_ms = ev_ms(h->ev[2], h->ev[3]);
+      st->t_round2_ms = ev_ms(h->ev[3], h->ev[4]);
+      st->t_finalize_ms = ev_ms(h->ev[4], h->ev[5]);
+      st->t_total_ms = ev_ms(h->ev[0], h->ev[5]);
+    }
   }
   h->sp_used = 1;
   *ok = true;
@@ -2071,14 +2149,25 @@ int gscan_hull_f64_device(gscan_handle* h, const double* d_xs, const double* d_y
   CU(cudaSetDevice(h->device));
   const gscan_config c = resolve(cfg);
   uint64_t hs = 0;
-  TRY(run_pipeline(h, d_xs, d_ys, n, c, &hs, stats));
+#ifdef GSCAN_STAMP
+  host_mark(0);
+#endif
+  h->user_out = d_out_idx;
+  h->user_cap = out_cap;
+  h->user_out_done = false;
+  const int rc = run_pipeline(h, d_xs, d_ys, n, c, &hs, stats);
+  h->user_out = nullptr;
+  TRY(rc);
   if (out_len) *out_len = hs;
   if (hs > out_cap) return fail(h, GSCAN_E_CAPACITY, "hull has %llu vertices, capacity %llu",
                                 (unsigned long long)hs, (unsigned long long)out_cap);
-  if (d_out_idx && hs) {
+  if (d_out_idx && hs && !h->user_out_done) {
     CU(cudaMemcpyAsync(d_out_idx, h->d_out, hs * 4, cudaMemcpyDeviceToDevice, h->stream));
     CU(cudaStreamSynchronize(h->stream));
   }
+#ifdef GSCAN_STAMP
+  host_mark(3);
+#endif
   return GSCAN_OK;
 }
 

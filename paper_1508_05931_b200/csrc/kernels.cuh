@@ -33,6 +33,7 @@ struct Counters {
   uint32_t graham_fail; // certificate failures (diagnostics)
   uint32_t anchor_dups; // survivors coinciding with the anchor
   uint32_t pad[5];
+  uint64_t tstamp[6];   // stage boundaries (%globaltimer ns) of a graph-replayed call
 };
 
 // ===========================================================================
