@@ -1154,18 +1154,54 @@ SpCtx sp_ctx(gscan_handle* h, const double* xs, const double* ys, uint32_t n, ui
   return c;
 }
 
+// The call's cleared state in one kernel (one graph node instead of nine
+// memset nodes): segments of 32-bit words set to a value.
+struct InitSegs {
+  uint32_t* p[9];
+  uint64_t words[9];
+  uint32_t val[9];
+};
+__global__ void __launch_bounds__(256) k_sp_init(InitSegs g) {
+  const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
+#pragma unroll 1
+  for (int k = 0; k < 9; ++k) {
+    uint32_t* p = g.p[k];
+    const uint64_t n = g.words[k];
+    const uint32_t v = g.val[k];
+    // 16-byte stores where aligned (every segment starts 16-byte aligned)
+    uint4* p4 = reinterpret_cast<uint4*>(p);
+    const uint64_t n4 = n / 4;
+    for (uint64_t i = tid; i < n4; i += nth) p4[i] = make_uint4(v, v, v, v);
+    for (uint64_t i = n4 * 4 + tid; i < n; i += nth) p[i] = v;
+  }
+}
+
 int sp_seg_init(gscan_handle* h, const SpCtx& c) {
   cudaStream_t s = c.s;
-  CU(cudaMemsetAsync(h->ctr, 0, sizeof(Counters), s));
+  static_assert(sizeof(Counters) % 16 == 0 && sizeof(SpState) % 4 == 0, "init segments");
+  InitSegs g{};
+  int k = 0;
+  auto seg = [&](void* p, uint64_t bytes, uint32_t v) {
+    g.p[k] = static_cast<uint32_t*>(p);
+    g.words[k] = bytes / 4;
+    g.val[k] = v;
+    ++k;
+  };
+  seg(h->ctr, sizeof(Counters), 0u);
+  seg(h->sp_st, sizeof(SpState), 0u);
+  seg(h->sp_gcnt, c.nb * 4ull, 0u);
+  seg(h->sp_ccnt, c.nb * 4ull, 0u);
+  seg(h->sp_prefmax, c.nb * 4ull, 0u);
+  seg(h->sp_slice, c.nb * 4ull, 0xffffffffu);
+  seg(h->sp_cells, kSpCells * 4ull, 0u);
+  seg(h->lb_status, (uint64_t)kLbSlots * h->lb_stride * 8, 0u);
+  seg(h->lb_ctr, (uint64_t)kLbSlots * sizeof(Counters), 0u);
+  {
+    Launch L(h, "k_sp_init", s);
+    k_sp_init<<<2 * h->sm_count, 256, 0, s>>>(g);
+  }
   TRY(stage_mark(h, 0, s));
-  CU(cudaMemsetAsync(h->sp_st, 0, sizeof(SpState), s));
-  CU(cudaMemsetAsync(h->sp_gcnt, 0, c.nb * 4, s));
-  CU(cudaMemsetAsync(h->sp_ccnt, 0, c.nb * 4, s));
-  CU(cudaMemsetAsync(h->sp_prefmax, 0, c.nb * 4, s));
-  CU(cudaMemsetAsync(h->sp_slice, 0xff, c.nb * 4, s));
-  CU(cudaMemsetAsync(h->sp_cells, 0, kSpCells * 4, s));
-  CU(cudaMemsetAsync(h->lb_status, 0, (size_t)kLbSlots * h->lb_stride * 8, s));
-  CU(cudaMemsetAsync(h->lb_ctr, 0, (size_t)kLbSlots * sizeof(Counters), s));
   return GSCAN_OK;
 }
 
