@@ -7,6 +7,13 @@
 
 namespace gscan {
 
+// Programmatic dependent launch: kernels of the sparse path's chain are
+// launched with programmatic stream serialization (launch_pdl in gscan.cu),
+// so the next grid is staged while the current one drains; every such kernel
+// first waits here for its predecessor's completion and memory (a no-op when
+// launched normally).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 constexpr int kBlock = 256;   // threads per CTA for the streaming kernels
 constexpr int kWarps = kBlock / 32;
 constexpr uint32_t kDead = 0xffffffffu;        // index marker: duplicate dropped

@@ -386,6 +386,7 @@ __device__ __forceinline__ uint32_t tree_nq(const uint32_t* info, int j) {
 __global__ void k_gr_setup(const uint32_t* __restrict__ n_dev, uint32_t n_host,
                            const uint32_t* __restrict__ st_fail, uint32_t n_max, uint32_t disable,
                            uint32_t* __restrict__ info) {
+  pdl_wait();
   const uint32_t t = threadIdx.x;
   if (t < kTreeInfoWords && t != 4 && t != 0) info[t] = 0;
   if (t == 0) {
@@ -400,6 +401,7 @@ __global__ void k_gr_setup(const uint32_t* __restrict__ n_dev, uint32_t n_host,
 __global__ void __launch_bounds__(kTreeCta) k_gr_up(int j, const double* __restrict__ R_x,
                                                    const double* __restrict__ R_y, TreeWork w,
                                                    const uint32_t* __restrict__ info) {
+  pdl_wait();
   extern __shared__ __align__(16) double tsm[];
   const TreeRows<kTreeCta> r(tsm);
   if (info[0]) return;
@@ -422,6 +424,7 @@ __global__ void __launch_bounds__(kTreeCta) k_gr_up(int j, const double* __restr
 // Exclusive scan of level j's chain lengths (one CTA), Q_{j+1}'s size, and
 // the shrink check (info[0]: the tree strategy declines).
 __global__ void __launch_bounds__(1024) k_gr_scan(int j, TreeWork w, uint32_t* __restrict__ info) {
+  pdl_wait();
   __shared__ uint32_t s_w[32];
   __shared__ uint32_t s_carry;
   if (info[0]) return;
@@ -458,6 +461,7 @@ __device__ __forceinline__ void tree_gather_chunk(const TreeWork& w, int j, uint
 
 __global__ void __launch_bounds__(256) k_gr_gather(int j, TreeWork w,
                                                   const uint32_t* __restrict__ info) {
+  pdl_wait();
   if (info[0]) return;
   const uint32_t nch = (tree_nq(info, j) + tree_cs(j) - 1) / tree_cs(j);
   for (uint32_t c = blockIdx.x * 8 + (threadIdx.x >> 5); c < nch; c += gridDim.x * 8)
@@ -490,6 +494,7 @@ __device__ __forceinline__ void tree_down_one(const TreeRows<T>& r, const TreeLe
 __global__ void __launch_bounds__(kTreeThreads, 1) k_gr_mid(
     const double* __restrict__ R_x, const double* __restrict__ R_y, TreeWork w,
     uint32_t* __restrict__ info) {
+  pdl_wait();
   extern __shared__ __align__(16) double tsm[];
   const TreeRows<kTreeThreads> r(tsm);
   __shared__ uint32_t s_w[32];
@@ -748,6 +753,7 @@ __global__ void __launch_bounds__(kTreeThreads, 1) k_gr_mid(
 __global__ void __launch_bounds__(kTreeCta) k_gr_down(int j, const double* __restrict__ R_x,
                                                      const double* __restrict__ R_y, TreeWork w,
                                                      const uint32_t* __restrict__ info) {
+  pdl_wait();
   extern __shared__ __align__(16) double tsm[];
   const TreeRows<kTreeCta> r(tsm);
   if (info[0] || (int)info[3] <= j) return;
@@ -762,6 +768,7 @@ __global__ void __launch_bounds__(kTreeCta) k_gr_cert(const double* __restrict__
                                                      const double* __restrict__ R_y, TreeWork w,
                                                      uint32_t* __restrict__ info,
                                                      uint32_t debug_corrupt) {
+  pdl_wait();
   extern __shared__ __align__(16) double tsm[];
   const TreeRows<kTreeCta> r(tsm);
   if (info[0]) return;
@@ -809,6 +816,7 @@ __global__ void __launch_bounds__(1024) k_gr_emit(const double* __restrict__ R_x
                                                   const uint32_t* __restrict__ info,
                                                   uint32_t* __restrict__ out_idx,
                                                   Counters* __restrict__ ctr) {
+  pdl_wait();
   if (info[0]) return;
   const uint32_t N = info[4];
   const uint32_t t = threadIdx.x;

@@ -455,13 +455,33 @@ struct Launch {
   }
 };
 
+// A kernel of the sparse path's chain, launched with programmatic stream
+// serialization: the grid is staged while its predecessor drains and starts
+// with pdl_wait() (device_common.cuh). Captured into the sparse graph as a
+// programmatic dependency edge.
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);  // errors: cudaGetLastError
+}
+
 // Exclusive scan on a pre-cleared look-back slot (no memsets: one graph node).
 int scan_u32_slot(gscan_handle* h, const uint32_t* in, uint32_t n, uint32_t* out, int slot,
                   cudaStream_t s) {
   const uint64_t tiles = (n + 1 + kScanTile - 1) / kScanTile;
   if (tiles > h->lb_stride) return fail(h, GSCAN_E_INTERNAL, "look-back slot too small");
   Launch L(h, "k_scan_u32", s);
-  k_scan_u32<<<tiles, kBlock, 0, s>>>(in, n, out, h->lb_status + (size_t)slot * h->lb_stride,
+  launch_pdl(k_scan_u32, tiles, kBlock, 0, s, in, n, out, h->lb_status + (size_t)slot * h->lb_stride,
                                       h->lb_ctr + slot);
   return GSCAN_OK;
 }
@@ -859,18 +879,18 @@ int tree_enqueue(gscan_handle* h, const double* Rx, const double* Ry, const uint
   const uint32_t g0 = std::min((nch0 + kTreeCta - 1) / kTreeCta, gmax);
   const uint32_t g1 = std::min((h->tw_nch1 + kTreeCta - 1) / kTreeCta, gmax);
   const uint32_t dbg = (h->debug & GSCAN_DEBUG_CORRUPT_CANDIDATE) ? 1u : 0u;
-  { Launch Lk(h, "k_gr_setup", s); k_gr_setup<<<1, 64, 0, s>>>(n_dev, n_host, st_fail, h->tw_nmax, disable ? 1u : 0u, info); }
+  { Launch Lk(h, "k_gr_setup", s); launch_pdl(k_gr_setup, 1, 64, 0, s, n_dev, n_host, st_fail, h->tw_nmax, disable ? 1u : 0u, info); }
   for (int j = 0; j < 2; ++j) {  // levels 0 and 1 on many CTAs
     const uint32_t g = j ? g1 : g0, nch = j ? h->tw_nch1 : nch0;
-    { Launch Lk(h, "k_gr_up", s); k_gr_up<<<g, kTreeCta, kTreeCtaSmem, s>>>(j, Rx, Ry, w, info); }
-    { Launch Lk(h, "k_gr_scan", s); k_gr_scan<<<1, 1024, 0, s>>>(j, w, info); }
-    { Launch Lk(h, "k_gr_gather", s); k_gr_gather<<<std::min((nch + 7) / 8, gmax), 256, 0, s>>>(j, w, info); }
+    { Launch Lk(h, "k_gr_up", s); launch_pdl(k_gr_up, g, kTreeCta, kTreeCtaSmem, s, j, Rx, Ry, w, info); }
+    { Launch Lk(h, "k_gr_scan", s); launch_pdl(k_gr_scan, 1, 1024, 0, s, j, w, info); }
+    { Launch Lk(h, "k_gr_gather", s); launch_pdl(k_gr_gather, std::min((nch + 7) / 8, gmax), 256, 0, s, j, w, info); }
   }
-  { Launch Lk(h, "k_gr_mid", s); k_gr_mid<<<1, kTreeThreads, kTreeSmem, s>>>(Rx, Ry, w, info); }
-  { Launch Lk(h, "k_gr_down", s); k_gr_down<<<g1, kTreeCta, kTreeCtaSmem, s>>>(2, Rx, Ry, w, info); }
-  { Launch Lk(h, "k_gr_down", s); k_gr_down<<<g0, kTreeCta, kTreeCtaSmem, s>>>(1, Rx, Ry, w, info); }
-  { Launch Lk(h, "k_gr_cert", s); k_gr_cert<<<g0, kTreeCta, kTreeCtaSmem, s>>>(Rx, Ry, w, info, dbg); }
-  { Launch Lk(h, "k_gr_emit", s); k_gr_emit<<<1, 1024, 0, s>>>(Rx, Ry, Ri, w, info, h->d_out, h->ctr); }
+  { Launch Lk(h, "k_gr_mid", s); launch_pdl(k_gr_mid, 1, kTreeThreads, kTreeSmem, s, Rx, Ry, w, info); }
+  { Launch Lk(h, "k_gr_down", s); launch_pdl(k_gr_down, g1, kTreeCta, kTreeCtaSmem, s, 2, Rx, Ry, w, info); }
+  { Launch Lk(h, "k_gr_down", s); launch_pdl(k_gr_down, g0, kTreeCta, kTreeCtaSmem, s, 1, Rx, Ry, w, info); }
+  { Launch Lk(h, "k_gr_cert", s); launch_pdl(k_gr_cert, g0, kTreeCta, kTreeCtaSmem, s, Rx, Ry, w, info, dbg); }
+  { Launch Lk(h, "k_gr_emit", s); launch_pdl(k_gr_emit, 1, 1024, 0, s, Rx, Ry, Ri, w, info, h->d_out, h->ctr); }
   CU(cudaGetLastError());
   CU(cudaMemcpyAsync(h->h_info, info, kTreeInfoWords * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
   return GSCAN_OK;
@@ -1087,11 +1107,11 @@ int sparse_init(gscan_handle* h) {
 // one-thread kernel stores %globaltimer into the counters (read back with
 // them), since six cudaEventElapsedTime calls cost ~17 us of host time per
 // call; outside a capture (profiling, no graphs) an event.
-__global__ void k_tstamp(Counters* __restrict__ ctr, int k) { ctr->tstamp[k] = globaltimer_ns(); }
+__global__ void k_tstamp(Counters* __restrict__ ctr, int k) { pdl_wait(); ctr->tstamp[k] = globaltimer_ns(); }
 int stage_mark(gscan_handle* h, int k, cudaStream_t s) {
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   CU(cudaStreamIsCapturing(s, &cs));
-  if (cs == cudaStreamCaptureStatusActive) k_tstamp<<<1, 1, 0, s>>>(h->ctr, k);
+  if (cs == cudaStreamCaptureStatusActive) launch_pdl(k_tstamp, 1, 1, 0, s, h->ctr, k);
   else CU(cudaEventRecord(h->ev[k], s));
   return GSCAN_OK;
 }
@@ -1162,6 +1182,7 @@ struct InitSegs {
   uint32_t val[9];
 };
 __global__ void __launch_bounds__(256) k_sp_init(InitSegs g) {
+  pdl_wait();
   const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
 #pragma unroll 1
@@ -1199,7 +1220,7 @@ int sp_seg_init(gscan_handle* h, const SpCtx& c) {
   seg(h->lb_ctr, (uint64_t)kLbSlots * sizeof(Counters), 0u);
   {
     Launch L(h, "k_sp_init", s);
-    k_sp_init<<<2 * h->sm_count, 256, 0, s>>>(g);
+    launch_pdl(k_sp_init, 2 * h->sm_count, 256, 0, s, g);
   }
   TRY(stage_mark(h, 0, s));
   return GSCAN_OK;
@@ -1208,21 +1229,21 @@ int sp_seg_init(gscan_handle* h, const SpCtx& c) {
 int sp_seg_extremes(gscan_handle* h, const SpCtx& c) {
   if (c.vec && c.n >= (uint32_t)kExtTile) {  // bulk-copy pipeline, one CTA per SM
     Launch L(h, "k_extremes_tma", c.s);
-    k_extremes_tma<<<h->sm_count, kExtThreads, kExtSmem, c.s>>>(c.xs, c.ys, c.n, h->partials, h->ext,
+    launch_pdl(k_extremes_tma, h->sm_count, kExtThreads, kExtSmem, c.s, c.xs, c.ys, c.n, h->partials, h->ext,
                                                            h->ctr);
     return GSCAN_OK;
   }
   const uint32_t grid =
       std::max(1u, std::min<uint32_t>((c.n + kBlock * 8 - 1) / (kBlock * 8), h->sm_count * 8));
   Launch L(h, "k_extremes", c.s);
-  if (c.vec) k_extremes<true><<<grid, kBlock, 0, c.s>>>(c.xs, c.ys, c.n, h->partials, h->ext, h->ctr);
-  else k_extremes<false><<<grid, kBlock, 0, c.s>>>(c.xs, c.ys, c.n, h->partials, h->ext, h->ctr);
+  if (c.vec) launch_pdl(k_extremes<true>, grid, kBlock, 0, c.s, c.xs, c.ys, c.n, h->partials, h->ext, h->ctr);
+  else launch_pdl(k_extremes<false>, grid, kBlock, 0, c.s, c.xs, c.ys, c.n, h->partials, h->ext, h->ctr);
   return GSCAN_OK;
 }
 
 int sp_seg_sample(gscan_handle* h, const SpCtx& c) {
   Launch L(h, "k_sp_sample", c.s);
-  k_sp_sample<<<kSpSample / 1024, 1024, 0, c.s>>>(c.xs, c.ys, c.n, h->ext, h->sp_cells);
+  launch_pdl(k_sp_sample, kSpSample / 1024, 1024, 0, c.s, c.xs, c.ys, c.n, h->ext, h->sp_cells);
   return GSCAN_OK;
 }
 
@@ -1231,18 +1252,18 @@ int sp_seg_f2(gscan_handle* h, const SpCtx& c) {
   cudaStream_t s = c.s;
   {
     Launch L(h, "k_sp_cdf", s);
-    k_sp_cdf<<<1, kSpCells / 2, 0, s>>>(h->sp_cells, h->sp_cdf, c.base == 0 && !c.sharded ? c.n : 0u,
+    launch_pdl(k_sp_cdf, 1, kSpCells / 2, 0, s, h->sp_cells, h->sp_cdf, c.base == 0 && !c.sharded ? c.n : 0u,
                                         h->sp_st);
   }
   {
     Launch L(h, "k_sp_theta", s);
-    k_sp_theta<<<(c.nb + 1 + 255) / 256, 256, 0, s>>>(h->sp_cdf, h->sp_th, h->sp_st);
+    launch_pdl(k_sp_theta, (c.nb + 1 + 255) / 256, 256, 0, s, h->sp_cdf, h->sp_th, h->sp_st);
   }
   const bool ring = kF2Ring && c.vec;
   const uint32_t g2 = ring ? c.G : (kF2Split ? 2 * c.G : c.G);  // F2 CTAs (d2 partials)
   if (ring) {
     Launch L(h, "k_sp_hist", s);
-    k_sp_hist_ring<<<g2, kF2Cons, kF2RingSmem, s>>>(c.xs, c.ys, c.n, h->ext, h->sp_cdf, h->sp_th,
+    launch_pdl(k_sp_hist_ring, g2, kF2Cons, kF2RingSmem, s, c.xs, c.ys, c.n, h->ext, h->sp_cdf, h->sp_th,
                                                          h->sp_codes, h->sp_d2, h->ctr, h->sp_st,
                                                          h->sp_exc, h->sp_exc_cap);
   } else {
@@ -1250,33 +1271,33 @@ int sp_seg_f2(gscan_handle* h, const SpCtx& c) {
 #define A2 c.xs, c.ys, c.n, h->ext, h->sp_cdf, h->sp_th, h->sp_codes, h->sp_hist_part, h->sp_d2, h->ctr, \
            h->sp_st
     if (kF2Split) {
-      if (c.vec) k_sp_hist<true, false><<<g2, kSpThreads, 0, s>>>(A2);
-      else k_sp_hist<false, false><<<g2, kSpThreads, 0, s>>>(A2);
+      if (c.vec) launch_pdl(k_sp_hist<true, false>, g2, kSpThreads, 0, s, A2);
+      else launch_pdl(k_sp_hist<false, false>, g2, kSpThreads, 0, s, A2);
     } else {
-      if (c.vec) k_sp_hist<true, true><<<g2, kSpThreads, c.smem_nb, s>>>(A2);
-      else k_sp_hist<false, true><<<g2, kSpThreads, c.smem_nb, s>>>(A2);
+      if (c.vec) launch_pdl(k_sp_hist<true, true>, g2, kSpThreads, c.smem_nb, s, A2);
+      else launch_pdl(k_sp_hist<false, true>, g2, kSpThreads, c.smem_nb, s, A2);
     }
 #undef A2
   }
   uint32_t nparts = g2;  // P_l partials
   if (ring) {  // the screen's uncertain points, exactly
     Launch L(h, "k_sp_f2_patch", s);
-    k_sp_f2_patch<<<kF2PatchGrid, 256, 0, s>>>(c.xs, c.ys, h->ext, h->sp_cdf, h->sp_th, h->sp_codes,
+    launch_pdl(k_sp_f2_patch, kF2PatchGrid, 256, 0, s, c.xs, c.ys, h->ext, h->sp_cdf, h->sp_th, h->sp_codes,
                                               h->sp_exc, h->sp_exc_cap, h->sp_d2 + g2, h->ctr,
                                               h->sp_st);
     nparts += kF2PatchGrid;
   }
   if (kF2Split || ring) {
     Launch L(h, "k_sp_hist_codes", s);
-    k_sp_hist_codes<<<c.G, 1024, c.smem_nb, s>>>(h->sp_codes, c.n, h->sp_hist_part, h->sp_st);
+    launch_pdl(k_sp_hist_codes, c.G, 1024, c.smem_nb, s, h->sp_codes, c.n, h->sp_hist_part, h->sp_st);
   }
   {
     Launch L(h, "k_sp_reduce_hist", s);
-    k_sp_reduce_cols<false><<<(c.nb + 255) / 256, 256, 0, s>>>(h->sp_hist_part, c.G, c.nb, h->sp_hist);
+    launch_pdl(k_sp_reduce_cols<false>, (c.nb + 255) / 256, 256, 0, s, h->sp_hist_part, c.G, c.nb, h->sp_hist);
   }
   {
     Launch L(h, "k_sp_plan_pl", s);
-    k_sp_plan_pl<<<1, 256, 0, s>>>(c.xs, c.ys, h->sp_d2, nparts, h->sp_st, h->ctr, c.n);
+    launch_pdl(k_sp_plan_pl, 1, 256, 0, s, c.xs, c.ys, h->sp_d2, nparts, h->sp_st, h->ctr, c.n);
   }
   return GSCAN_OK;
 }
@@ -1287,11 +1308,11 @@ int sp_seg_plan(gscan_handle* h, const SpCtx& c) {
   TRY(scan_u32_slot(h, h->sp_hist, c.nb, h->sp_bstart, kLbBstart, s));
   {
     Launch L(h, "k_sp_plan_bl", s);
-    k_sp_plan_bl<<<1, 32, 0, s>>>(h->ext, h->sp_cdf, h->sp_th, h->sp_bstart, h->sp_st);
+    launch_pdl(k_sp_plan_bl, 1, 32, 0, s, h->ext, h->sp_cdf, h->sp_th, h->sp_bstart, h->sp_st);
   }
   {
     Launch L(h, "k_sp_lrank", s);
-    k_sp_lrank<<<h->sm_count * 8, 256, 0, s>>>(c.xs, c.ys, h->sp_codes, c.n, c.base, h->ext,
+    launch_pdl(k_sp_lrank, h->sm_count * 8, 256, 0, s, c.xs, c.ys, h->sp_codes, c.n, c.base, h->ext,
                                                h->sp_st);
   }
   return GSCAN_OK;
@@ -1302,7 +1323,7 @@ int sp_seg_f3(gscan_handle* h, const SpCtx& c) {
   cudaStream_t s = c.s;
   {
     Launch L(h, "k_sp_gbits", s);
-    k_sp_gbits<<<c.nb / 256, 256, 0, s>>>(h->sp_bstart, c.chunks, h->sp_st, h->sp_gbits,
+    launch_pdl(k_sp_gbits, c.nb / 256, 256, 0, s, h->sp_bstart, c.chunks, h->sp_st, h->sp_gbits,
                                           h->sp_glist);
   }
   if (!c.sharded) {
@@ -1310,7 +1331,7 @@ int sp_seg_f3(gscan_handle* h, const SpCtx& c) {
     // points stay L2-resident instead of being scattered over the global
     // position range (rank 0 of the sharded path does this in dist_slices)
     Launch L(h, "k_sp_gsize", s);
-    k_sp_gsize<<<(c.nb + 255) / 256, 256, 0, s>>>(h->sp_gbits, h->sp_hist, h->sp_gsz);
+    launch_pdl(k_sp_gsize, (c.nb + 255) / 256, 256, 0, s, h->sp_gbits, h->sp_hist, h->sp_gsz);
   }
   if (!c.sharded) TRY(scan_u32_slot(h, h->sp_gsz, c.nb, h->sp_gs, kLbGs, s));
   TRY(stage_mark(h, 1, s));
@@ -1322,22 +1343,22 @@ int sp_seg_f3(gscan_handle* h, const SpCtx& c) {
            h->sp_eb, h->sp_gcount, h->sp_gx, h->sp_gy, h->sp_dup, h->sp_hcount, h->sp_part_off, \
            h->sp_phi32, c.sharded ? 0u : 3u
     if (kF3Split) {
-      if (c.vec) k_sp_phi<true, false><<<c.G, t3, sm3, s>>>(A3);
-      else k_sp_phi<false, false><<<c.G, t3, sm3, s>>>(A3);
+      if (c.vec) launch_pdl(k_sp_phi<true, false>, c.G, t3, sm3, s, A3);
+      else launch_pdl(k_sp_phi<false, false>, c.G, t3, sm3, s, A3);
     } else {
-      if (c.vec) k_sp_phi<true, true><<<c.G, t3, sm3, s>>>(A3);
-      else k_sp_phi<false, true><<<c.G, t3, sm3, s>>>(A3);
+      if (c.vec) launch_pdl(k_sp_phi<true, true>, c.G, t3, sm3, s, A3);
+      else launch_pdl(k_sp_phi<false, true>, c.G, t3, sm3, s, A3);
     }
 #undef A3
   }
   if (kF3Split) {
     Launch L(h, "k_sp_phimax_codes", s);
-    k_sp_phimax_codes<<<c.G, 1024, c.smem_nb, s>>>(h->sp_codes, h->sp_phi32, h->sp_gbits, c.n,
+    launch_pdl(k_sp_phimax_codes, c.G, 1024, c.smem_nb, s, h->sp_codes, h->sp_phi32, h->sp_gbits, c.n,
                                                    h->sp_st, h->sp_phi_part);
   }
   {
     Launch L(h, "k_sp_reduce_phi", s);
-    k_sp_reduce_cols<true><<<(c.nb + 255) / 256, 256, 0, s>>>(h->sp_phi_part, c.G, c.nb, h->sp_phimax);
+    launch_pdl(k_sp_reduce_cols<true>, (c.nb + 255) / 256, 256, 0, s, h->sp_phi_part, c.G, c.nb, h->sp_phimax);
   }
   if (!c.sharded) TRY(rec_event(h, h->ev_part, s));  // the side stream's count scan forks here
   return GSCAN_OK;
@@ -1350,7 +1371,7 @@ int sp_seg_sortg(gscan_handle* h, const SpCtx& c, const double* gx, const double
   cudaStream_t s = c.s;
   {
     Launch L(h, "k_sp_place_g", s);
-    k_sp_emit_place<0><<<dim3(16, c.G), 256, 0, s>>>(gx, gy, h->surv, h->sp_eb, nullptr,
+    launch_pdl(k_sp_emit_place<0>, dim3(16, c.G), 256, 0, s, gx, gy, h->surv, h->sp_eb, nullptr,
                                                      h->sp_gcount, c.cap, h->sp_gcnt, c.gs,
                                                      h->ext, h->sp_st, h->rec,
                                                      region_xy ? h->sp_gx : nullptr,
@@ -1359,25 +1380,25 @@ int sp_seg_sortg(gscan_handle* h, const SpCtx& c, const double* gx, const double
   }
   {
     Launch L(h, "k_sp_sort_gathered", s);
-    k_sp_sort_gathered<<<h->sm_count * (kSpSmallCap <= 512 ? 8 : 4), kSpSmallThreads, kSpSmallSmem, s>>>(
+    launch_pdl(k_sp_sort_gathered, h->sm_count * (kSpSmallCap <= 512 ? 8 : 4), kSpSmallThreads, kSpSmallSmem, s, 
         h->sp_glist, h->sp_bstart, c.gs, h->sp_hist, h->sp_gcnt, h->rec, h->ext, h->sp_st,
         h->sp_bigg, h->A_x, h->A_y, h->A_i);
   }
   {
     Launch L(h, "k_sp_sort_gathered_big", s);
-    k_sp_sort_gathered_big<<<h->sm_count, kSpSortThreads, kSpBigSmem, s>>>(
+    launch_pdl(k_sp_sort_gathered_big, h->sm_count, kSpSortThreads, kSpBigSmem, s, 
         h->sp_bigg, h->sp_bstart, c.gs, h->sp_hist, h->rec, h->ext, h->sp_st, h->A_x, h->A_y,
         h->A_i, h->sp_hugeg, h->sp_huge_cap);
   }
   if (h->sp_huge_cap) {  // inputs large enough for buckets above kSpGatherCap
     Launch L(h, "k_sp_sort_gathered_huge", s);
-    k_sp_sort_gathered_huge<<<h->sm_count, kSpSortThreads, 0, s>>>(
+    launch_pdl(k_sp_sort_gathered_huge, h->sm_count, kSpSortThreads, 0, s, 
         h->sp_hugeg, h->sp_bstart, c.gs, h->sp_hist, h->rec, h->ext, h->sp_st, h->A_x, h->A_y,
         h->A_i, h->sp_huge_scr, h->sp_huge_cap);
   }
   {
     Launch L(h, "k_sp_slices", s);
-    k_sp_slices<<<(uint32_t)((c.nslices * 32 + 255) / 256), 256, 0, s>>>(
+    launch_pdl(k_sp_slices, (uint32_t)((c.nslices * 32 + 255) / 256), 256, 0, s, 
         h->sp_st, h->sp_bstart, c.gs, h->sp_gbits, h->sp_phimax, h->A_x, h->A_y, h->ext,
         h->sp_prefmax, h->sp_slice);
   }
@@ -1390,12 +1411,12 @@ int sp_seg_f4(gscan_handle* h, const SpCtx& c) {
   cudaStream_t s = c.s;
   {
     Launch L(h, "k_sp_thresholds", s);
-    k_sp_thresholds<<<(kSpBuckets + 255) / 256, 256, 0, s>>>(h->sp_gbits, h->sp_prefmax, h->sp_st,
+    launch_pdl(k_sp_thresholds, (kSpBuckets + 255) / 256, 256, 0, s, h->sp_gbits, h->sp_prefmax, h->sp_st,
                                                             h->sp_thr);
   }
   {
     Launch L(h, "k_sp_cand", s);
-    k_sp_cand<<<c.G, kSpCandThreads, c.smem_nb, s>>>(h->sp_codes, h->sp_phi32, c.n, c.cap,
+    launch_pdl(k_sp_cand, c.G, kSpCandThreads, c.smem_nb, s, h->sp_codes, h->sp_phi32, c.n, c.cap,
                                                      h->sp_thr, h->sp_st, h->surv, h->sp_eb,
                                                      h->sp_ccount, c.drop);
   }
@@ -1410,7 +1431,7 @@ int sp_seg_walk(gscan_handle* h, const SpCtx& c, const double* cx, const double*
   const uint32_t nb = c.nb;
   {
     Launch L(h, "k_sp_rank_c", s);
-    k_sp_emit_place<1><<<dim3(4, c.G), 256, 0, s>>>(cx, cy, h->surv, h->sp_eb, h->rank,
+    launch_pdl(k_sp_emit_place<1>, dim3(4, c.G), 256, 0, s, cx, cy, h->surv, h->sp_eb, h->rank,
                                                     h->sp_ccount, c.cap, h->sp_ccnt, nullptr,
                                                     h->ext, h->sp_st, h->rec, nullptr, nullptr,
                                                     (uint32_t)std::min<uint64_t>(h->wcap, 0xffffffffu));
@@ -1418,48 +1439,49 @@ int sp_seg_walk(gscan_handle* h, const SpCtx& c, const double* cx, const double*
   TRY(scan_u32_slot(h, h->sp_ccnt, nb, h->sp_cstart, kLbCstart, s));
   {
     Launch L(h, "k_sp_place_c", s);
-    k_sp_emit_place<2><<<dim3(4, c.G), 256, 0, s>>>(cx, cy, h->surv, h->sp_eb, h->rank,
+    launch_pdl(k_sp_emit_place<2>, dim3(4, c.G), 256, 0, s, cx, cy, h->surv, h->sp_eb, h->rank,
                                                     h->sp_ccount, c.cap, nullptr, h->sp_cstart,
-                                                    h->ext, h->sp_st, h->rec);
+                                                    h->ext, h->sp_st, h->rec, nullptr, nullptr,
+                                                    0xffffffffu);
   }
   {
     Launch L(h, "k_sp_wcount", s);
-    k_sp_wcount<<<(nb + 255) / 256, 256, 0, s>>>(h->sp_gbits, h->sp_hist, h->sp_ccnt, h->sp_wcnt);
+    launch_pdl(k_sp_wcount, (nb + 255) / 256, 256, 0, s, h->sp_gbits, h->sp_hist, h->sp_ccnt, h->sp_wcnt);
   }
   TRY(scan_u32_slot(h, h->sp_wcnt, nb, h->sp_wstart, kLbWstart, s));
   {
     Launch L(h, "k_sp_place_cand", s);
-    k_sp_place_cand<<<nb / 8, 256, 0, s>>>(h->rec, h->sp_cstart, h->sp_wstart, h->sp_slice,
+    launch_pdl(k_sp_place_cand, nb / 8, 256, 0, s, h->rec, h->sp_cstart, h->sp_wstart, h->sp_slice,
                                            h->ext, h->sp_st, h->sp_big, h->C_x, h->C_y, h->C_i,
                                            h->sp_Wb, h->sp_Ws, h->flags);
   }
   {
     Launch L(h, "k_sp_sort_cand_big", s);
-    k_sp_sort_cand_big<<<h->sm_count, kSpSortThreads, kSpBigSmem, s>>>(
+    launch_pdl(k_sp_sort_cand_big, h->sm_count, kSpSortThreads, kSpBigSmem, s, 
         h->sp_big, h->rec, h->sp_cstart, h->sp_wstart, h->sp_slice, h->ext, h->sp_st, h->C_x,
         h->C_y, h->C_i, h->sp_Wb, h->sp_Ws, h->flags, h->sp_huge_scr, h->sp_huge_cap);
   }
   {
     Launch L(h, "k_sp_place_gathered", s);
-    k_sp_place_gathered<<<h->sm_count * 4, 256, 0, s>>>(
+    launch_pdl(k_sp_place_gathered, h->sm_count * 4, 256, 0, s, 
         h->sp_glist, h->sp_bstart, c.gs, h->sp_hist, h->sp_wstart, h->A_x, h->A_y, h->A_i, h->ext,
         h->sp_st, h->C_x, h->C_y, h->C_i, h->sp_Wb, h->sp_Ws, h->flags);
   }
   TRY(stage_mark(h, 3, s));
   {
     Launch L(h, "k_sp_segments", s);
-    k_sp_segments<<<h->sm_count * 8, kBlock, 0, s>>>(h->sp_Ws, h->sp_st, h->sp_seglo, h->sp_seghi);
+    launch_pdl(k_sp_segments, h->sm_count * 8, kBlock, 0, s, h->sp_Ws, h->sp_st, h->sp_seglo, h->sp_seghi);
   }
   {
     Launch L(h, "k_sp_walk", s);
-    k_sp_walk<<<(uint32_t)c.nslices, kWalkBlock, 0, s>>>(h->C_x, h->C_y, h->sp_seglo, h->sp_seghi,
+    launch_pdl(k_sp_walk, (uint32_t)c.nslices, kWalkBlock, 0, s, h->C_x, h->C_y, h->sp_seglo, h->sp_seghi,
                                                          h->sp_st, h->ext, h->flags);
   }
   {
     const uint64_t tiles = (uint64_t)n_walk_cap / kCompactTile + 2;
     if (tiles > h->lb_stride) return fail(h, GSCAN_E_INTERNAL, "look-back slot too small");
     Launch L(h, "k_sp_compact", s);
-    k_sp_compact<<<(uint32_t)tiles, kBlock, 0, s>>>(
+    launch_pdl(k_sp_compact, (uint32_t)tiles, kBlock, 0, s, 
         h->C_x, h->C_y, h->C_i, h->sp_Wb, h->sp_Ws, h->flags, h->sp_st, h->A_x, h->A_y, h->A_i,
         h->sp_Rb, h->sp_Rs, h->lb_status + (size_t)kLbCompact * h->lb_stride, h->lb_ctr + kLbCompact);
   }
@@ -1468,15 +1490,15 @@ int sp_seg_walk(gscan_handle* h, const SpCtx& c, const double* cx, const double*
   TRY(rec_event(h, h->ev_f3, s));
   {
     Launch L(h, "k_sp_rlo", s);
-    k_sp_rlo<<<h->sm_count * 8, kBlock, 0, s>>>(h->sp_Rb, h->sp_st, h->sp_rlo);
+    launch_pdl(k_sp_rlo, h->sm_count * 8, kBlock, 0, s, h->sp_Rb, h->sp_st, h->sp_rlo);
   }
   {
     Launch L(h, "k_sp_cert_stats", s);
-    k_sp_cert_stats<<<h->sm_count, 256, 0, s>>>(h->A_x, h->A_y, h->sp_Rs, h->sp_st);
+    launch_pdl(k_sp_cert_stats, h->sm_count, 256, 0, s, h->A_x, h->A_y, h->sp_Rs, h->sp_st);
   }
   {
     Launch L(h, "k_sp_cert_decide", s);
-    k_sp_cert_decide<<<1, 32, 0, s>>>(h->sp_st, c.drop || (h->debug & GSCAN_DEBUG_SPARSE_VERIFY));
+    launch_pdl(k_sp_cert_decide, 1, 32, 0, s, h->sp_st, c.drop || (h->debug & GSCAN_DEBUG_SPARSE_VERIFY));
   }
   return GSCAN_OK;
 }
@@ -1487,8 +1509,8 @@ int sp_seg_verify(gscan_handle* h, const SpCtx& c) {
   {
     Launch L(h, "k_sp_verify", s);
 #define A6 c.xs, c.ys, h->sp_codes, c.n, h->sp_gbits, h->sp_rlo, h->A_x, h->A_y, h->sp_st
-    if (c.vec) k_sp_verify<true><<<c.G, kSpThreads, c.smem_nb + 4, s>>>(A6);
-    else k_sp_verify<false><<<c.G, kSpThreads, c.smem_nb + 4, s>>>(A6);
+    if (c.vec) launch_pdl(k_sp_verify<true>, c.G, kSpThreads, c.smem_nb + 4, s, A6);
+    else launch_pdl(k_sp_verify<false>, c.G, kSpThreads, c.smem_nb + 4, s, A6);
 #undef A6
   }
   return GSCAN_OK;
@@ -1697,7 +1719,7 @@ int run_sparse(gscan_handle* h, const double* xs, const double* ys, uint32_t n,
     rows.push_back((stamp[1] - stamp[2]) / 1e3);
     rows.push_back(prev_end ? (stamp[2] - prev_end) / 1e3 : 0.0);
     prev_end = std::max(stamp[0], stamp[1]);
-    if (rows.size() == 3 * 1000) {  // one print per 1000 calls (printing widens its own gap)
+    if (rows.size() == 3 * 24) {  // one print per 24 calls (printing widens its own gap)
       for (size_t r = 0; r < rows.size(); r += 3)
         fprintf(stderr, "[stamp] main %.1f us side %.1f us gap before %.1f us\n", rows[r], rows[r + 1], rows[r + 2]);
       rows.clear();

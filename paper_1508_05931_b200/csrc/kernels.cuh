@@ -119,6 +119,7 @@ __global__ void __launch_bounds__(kBlock) k_extremes(const double* __restrict__ 
                                                      ExtAcc* __restrict__ partials,
                                                      ExtResult* __restrict__ out,
                                                      Counters* __restrict__ ctr) {
+  pdl_wait();
   ExtAcc acc;
   ext_init(acc);
   const uint32_t tid = blockIdx.x * kBlock + threadIdx.x;
@@ -232,6 +233,7 @@ __global__ void __launch_bounds__(kExtThreads, 1) k_extremes_tma(const double* _
                                                            ExtAcc* __restrict__ partials,
                                                            ExtResult* __restrict__ out,
                                                            Counters* __restrict__ ctr) {
+  pdl_wait();
   extern __shared__ __align__(128) unsigned char ext_smem[];
   ExtRing ring;
   ring.setup(ext_smem, xs, ys, n);
@@ -612,6 +614,7 @@ __global__ void __launch_bounds__(kBlock) k_scan_u32(const uint32_t* __restrict_
                                                      uint32_t* __restrict__ out,
                                                      uint64_t* __restrict__ status,
                                                      Counters* __restrict__ ctr) {
+  pdl_wait();
   __shared__ uint32_t s_tile, s_excl, s_rows[kScanItems * kWarps + 1];
   if (threadIdx.x == 0) s_tile = atomicAdd(&ctr->tile_ticket, 1u);
   __syncthreads();

@@ -359,6 +359,7 @@ __global__ void __launch_bounds__(1024) k_sp_sample(const double* __restrict__ x
                                                     const double* __restrict__ ys, uint32_t n,
                                                     const ExtResult* __restrict__ ext,
                                                     uint32_t* __restrict__ cell_cnt) {
+  pdl_wait();
   __shared__ uint32_t s_cnt[kSpCells];
   for (uint32_t j = threadIdx.x; j < kSpCells; j += blockDim.x) s_cnt[j] = 0;
   SpQuad q;
@@ -388,6 +389,7 @@ __global__ void __launch_bounds__(1024) k_sp_sample(const double* __restrict__ x
 __global__ void __launch_bounds__(kSpCells / 2) k_sp_cdf(const uint32_t* __restrict__ cell_cnt,
                                                          double* __restrict__ cdf, uint32_t n,
                                                          SpState* __restrict__ st) {
+  pdl_wait();
   __shared__ double s_w[32];
   const double floor_w = 0.02;  // per-cell floor, in sample units
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -426,6 +428,7 @@ __global__ void __launch_bounds__(kSpCells / 2) k_sp_cdf(const uint32_t* __restr
 __global__ void __launch_bounds__(256) k_sp_theta(const double* __restrict__ cdf,
                                                   double* __restrict__ th,
                                                   SpState* __restrict__ st) {
+  pdl_wait();
   __shared__ double s_cdf[kSpCells + 1];
   for (uint32_t j = threadIdx.x; j <= kSpCells; j += blockDim.x) s_cdf[j] = cdf[j];
   __syncthreads();
@@ -456,6 +459,7 @@ __global__ void __launch_bounds__(256) k_sp_theta(const double* __restrict__ cdf
 template <bool kMax>
 __global__ void k_sp_reduce_cols(const uint32_t* __restrict__ part, uint32_t rows, uint32_t cols,
                                  uint32_t* __restrict__ out) {
+  pdl_wait();
   const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= cols) return;
   uint32_t v = 0;
@@ -736,6 +740,7 @@ __global__ void __launch_bounds__(kSpThreads, kHist ? 1 : 2) k_sp_hist(
     const ExtResult* __restrict__ ext, const double* __restrict__ cdf,
     const double* __restrict__ th, uint16_t* __restrict__ codes, uint32_t* __restrict__ hist_part,
     SpD2* __restrict__ d2part, Counters* __restrict__ ctr, const SpState* __restrict__ st) {
+  pdl_wait();
   extern __shared__ uint32_t s_hist[];  // kSpBuckets (kHist)
   if (st->fail) return;  // declined from the sample (k_sp_cdf)
   __shared__ double s_cdf[kSpCells + 1];
@@ -880,6 +885,7 @@ __global__ void __launch_bounds__(kF2Cons, 1) k_sp_hist_ring(
     const double* __restrict__ th, uint16_t* __restrict__ codes, SpD2* __restrict__ d2part,
     Counters* __restrict__ ctr, SpState* __restrict__ st, uint32_t* __restrict__ exc_list,
     uint32_t exc_cap) {
+  pdl_wait();
   extern __shared__ __align__(128) unsigned char f2_smem[];
   if (st->fail) return;  // declined from the sample (k_sp_cdf)
   F2Ring ring;
@@ -985,6 +991,7 @@ __global__ void __launch_bounds__(256) k_sp_f2_patch(
     const double* __restrict__ th, uint16_t* __restrict__ codes,
     const uint32_t* __restrict__ exc_list, uint32_t exc_cap, SpD2* __restrict__ d2part,
     Counters* __restrict__ ctr, SpState* __restrict__ st) {
+  pdl_wait();
   if (st->fail) return;
   const uint32_t ne = st->n_exc;
   if (ne > exc_cap) {
@@ -1035,6 +1042,7 @@ __global__ void __launch_bounds__(256) k_sp_f2_patch(
 __global__ void __launch_bounds__(1024, 1) k_sp_hist_codes(const uint16_t* __restrict__ codes,
                                                            uint32_t n, uint32_t* __restrict__ hist_part,
                                                            const SpState* __restrict__ st) {
+  pdl_wait();
   extern __shared__ uint32_t s_hist[];  // kSpBuckets
   if (st->fail) return;
   for (uint32_t b = threadIdx.x; b < kSpBuckets; b += blockDim.x) s_hist[b] = 0;
@@ -1086,6 +1094,7 @@ __global__ void __launch_bounds__(256) k_sp_plan_pl(const double* __restrict__ x
                                                     const SpD2* __restrict__ d2part, uint32_t nparts,
                                                     SpState* __restrict__ st,
                                                     const Counters* __restrict__ ctr, uint32_t n) {
+  pdl_wait();
   // >= 90% of the points survive round 1 (near-convex input): nearly all would
   // be walk candidates, the full sort is faster (a speed decision)
   if (threadIdx.x == 0 && (uint64_t)ctr->n1 * 10 > (uint64_t)n * 9) atomicOr(&st->fail, kSpFailMany);
@@ -1130,6 +1139,7 @@ __global__ void __launch_bounds__(256) k_sp_plan_pl(const double* __restrict__ x
 __global__ void k_sp_plan_bl(const ExtResult* __restrict__ ext, const double* __restrict__ cdf,
                              const double* __restrict__ th, const uint32_t* __restrict__ bstart,
                              SpState* __restrict__ st) {
+  pdl_wait();
   if (threadIdx.x != 0) return;
   const uint32_t m = bstart[kSpBuckets];
   st->m = m;
@@ -1154,6 +1164,7 @@ __global__ void __launch_bounds__(256) k_sp_lrank(const double* __restrict__ xs,
                                                   const uint16_t* __restrict__ codes, uint32_t n,
                                                   uint32_t base, const ExtResult* __restrict__ ext,
                                                   SpState* __restrict__ st) {
+  pdl_wait();
   // base: global index of point 0 (a shard's offset; 0 on one device)
   if (st->fail) return;
   const uint32_t b_l = st->b_l, l_idx = st->l_idx;
@@ -1201,6 +1212,7 @@ __global__ void __launch_bounds__(256) k_sp_gbits(const uint32_t* __restrict__ b
                                                   uint64_t chunk_count, SpState* __restrict__ st,
                                                   uint32_t* __restrict__ gbits,
                                                   uint32_t* __restrict__ glist) {
+  pdl_wait();
   // a thread per bucket, a warp per bitmap word
   const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;  // kSpBuckets is a multiple of 256
   const uint32_t lane = threadIdx.x & 31;
@@ -1300,6 +1312,7 @@ __global__ void __launch_bounds__(kMax ? kSpF3Threads : 1024, 1) k_sp_phi(
     double* __restrict__ g_x, double* __restrict__ g_y,  // gathered coordinates (same slots)
     uint64_t* __restrict__ hlist, uint32_t* __restrict__ h_count, uint32_t* __restrict__ part_cnt,
     float* __restrict__ phi32, uint32_t pad) {
+  pdl_wait();
   // pad = 3: the partition counts are written rounded up to whole sectors (4
   // entries; k_sp_dup_part<true>), pad = 0: exact (the sharded exchange)
   extern __shared__ uint32_t s_phi[];  // kSpBuckets (kMax)
@@ -1486,6 +1499,7 @@ __global__ void __launch_bounds__(1024, 1) k_sp_phimax_codes(const uint16_t* __r
                                                              const uint32_t* __restrict__ gbits,
                                                              uint32_t n, const SpState* __restrict__ st,
                                                              uint32_t* __restrict__ phi_part) {
+  pdl_wait();
   extern __shared__ uint32_t s_phi[];  // kSpBuckets
   __shared__ uint32_t s_g[kSpBuckets / 32];
   if (st->fail) return;
@@ -1928,6 +1942,7 @@ __global__ void __launch_bounds__(256) k_sp_emit_place(
     SpState* __restrict__ st, PtRec* __restrict__ rec,
     const double* __restrict__ e_x = nullptr, const double* __restrict__ e_y = nullptr,
     uint32_t wcap = 0xffffffffu) {
+  pdl_wait();
   // e_x, e_y: the emitted points' coordinates in the region slots (F3 writes
   // them for gathered points, so no random reads of xs, ys); else xs[i], ys[i]
   if (st->fail) return;
@@ -2178,6 +2193,7 @@ __global__ void __launch_bounds__(kSpSmallThreads) k_sp_sort_gathered(
     const PtRec* __restrict__ rec, const ExtResult* __restrict__ ext, SpState* __restrict__ st,
     uint32_t* __restrict__ big, double* __restrict__ A_x, double* __restrict__ A_y,
     uint32_t* __restrict__ A_i) {
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char smem[];
   if (st->fail) return;
   const uint32_t ngb = st->n_gb, l_idx = st->l_idx;
@@ -2226,6 +2242,7 @@ __global__ void __launch_bounds__(kSpSortThreads) k_sp_sort_gathered_big(
     const ExtResult* __restrict__ ext, SpState* __restrict__ st, double* __restrict__ A_x,
     double* __restrict__ A_y, uint32_t* __restrict__ A_i, uint32_t* __restrict__ huge,
     uint32_t huge_cap) {
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char smem[];
   if (st->fail) return;
   const uint32_t nbig = st->n_bigg, l_idx = st->l_idx;
@@ -2272,6 +2289,7 @@ __global__ void __launch_bounds__(kSpSortThreads) k_sp_sort_gathered_huge(
     const PtRec* __restrict__ rec, const ExtResult* __restrict__ ext, SpState* __restrict__ st,
     double* __restrict__ A_x, double* __restrict__ A_y, uint32_t* __restrict__ A_i,
     unsigned char* __restrict__ scratch, uint32_t cap) {
+  pdl_wait();
   if (st->fail) return;
   const uint32_t nh = st->n_hugeg, l_idx = st->l_idx;
   const double ax = ext->ax, ay = ext->ay;
@@ -2367,6 +2385,7 @@ __global__ void __launch_bounds__(256) k_sp_slices(
     const double* __restrict__ A_x, const double* __restrict__ A_y,
     const ExtResult* __restrict__ ext, uint32_t* __restrict__ prefmax,
     uint32_t* __restrict__ slice_of) {
+  pdl_wait();
   const SpState st = *st_;
   if (st.fail) return;
   const uint32_t s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -2446,6 +2465,7 @@ constexpr int kSpCandThreads = 1024;
 __global__ void k_sp_thresholds(const uint32_t* __restrict__ gbits,
                                 const uint32_t* __restrict__ prefmax, const SpState* __restrict__ st,
                                 float* __restrict__ thr) {
+  pdl_wait();
   const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= kSpBuckets || st->fail) return;
   const bool g = (gbits[b >> 5] >> (b & 31)) & 1u;
@@ -2457,6 +2477,7 @@ __global__ void __launch_bounds__(kSpCandThreads, 1) k_sp_cand(
     const float* __restrict__ thr_g,
     SpState* __restrict__ st, uint32_t* __restrict__ c_idx, uint32_t* __restrict__ c_b,
     uint32_t* __restrict__ c_count, bool drop) {
+  pdl_wait();
   // thresholds prefmax - tol, rounded down to float (a lower threshold only
   // adds candidates); gathered buckets get +inf (never candidates here)
   extern __shared__ __align__(16) float s_thr[];  // kSpBuckets
@@ -2550,6 +2571,7 @@ __global__ void __launch_bounds__(kSpCandThreads, 1) k_sp_cand(
 // their candidates.
 __global__ void k_sp_wcount(const uint32_t* __restrict__ gbits, const uint32_t* __restrict__ hist,
                             const uint32_t* __restrict__ ccnt, uint32_t* __restrict__ wcnt) {
+  pdl_wait();
   const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b < kSpBuckets) wcnt[b] = sp_gathered(gbits, b) ? hist[b] : ccnt[b];
 }
@@ -2570,6 +2592,7 @@ __global__ void __launch_bounds__(256) k_sp_place_cand(
     const ExtResult* __restrict__ ext, SpState* __restrict__ st, uint32_t* __restrict__ big,
     double* __restrict__ W_x, double* __restrict__ W_y, uint32_t* __restrict__ W_i,
     uint32_t* __restrict__ W_b, uint32_t* __restrict__ W_s, uint8_t* __restrict__ flags) {
+  pdl_wait();
   if (st->fail) return;
   const double ax = ext->ax, ay = ext->ay;
   const int lane = threadIdx.x & 31;
@@ -2626,6 +2649,7 @@ __global__ void __launch_bounds__(kSpSortThreads) k_sp_sort_cand_big(
     SpState* __restrict__ st, double* __restrict__ W_x, double* __restrict__ W_y,
     uint32_t* __restrict__ W_i, uint32_t* __restrict__ W_b, uint32_t* __restrict__ W_s,
     uint8_t* __restrict__ flags, unsigned char* __restrict__ scratch, uint32_t scap) {
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char smem[];
   if (st->fail) return;
   const uint32_t nbig = st->n_bigc;
@@ -2682,6 +2706,7 @@ __global__ void __launch_bounds__(256) k_sp_place_gathered(
     const uint32_t* __restrict__ A_i, const ExtResult* __restrict__ ext, SpState* __restrict__ st_,
     double* __restrict__ W_x, double* __restrict__ W_y, uint32_t* __restrict__ W_i,
     uint32_t* __restrict__ W_b, uint32_t* __restrict__ W_s, uint8_t* __restrict__ flags) {
+  pdl_wait();
   const SpState st = *st_;
   if (st.fail) return;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -2713,6 +2738,7 @@ __global__ void __launch_bounds__(256) k_sp_place_gathered(
 // past its last (slices are contiguous because W is exactly ordered).
 __global__ void k_sp_segments(const uint32_t* __restrict__ W_s, const SpState* __restrict__ st,
                               uint32_t* __restrict__ seg_lo, uint32_t* __restrict__ seg_hi) {
+  pdl_wait();
   if (st->fail) return;
   const uint32_t nw = st->n_w;
   for (uint32_t j = 1 + blockIdx.x * blockDim.x + threadIdx.x; j < nw; j += gridDim.x * blockDim.x) {
@@ -2732,6 +2758,7 @@ __global__ void __launch_bounds__(kWalkBlock) k_sp_walk(
     const uint32_t* __restrict__ seg_lo, const uint32_t* __restrict__ seg_hi,
     const SpState* __restrict__ st_, const ExtResult* __restrict__ ext,
     uint8_t* __restrict__ flags) {
+  pdl_wait();
   const SpState& st = *st_;
   if (st.fail) return;
   const uint32_t slice = blockIdx.x;
@@ -2848,6 +2875,7 @@ __global__ void __launch_bounds__(kWalkBlock) k_sp_walk(
 // R bucket index: rlo[b] = first R position whose bucket >= b (anchor = -1).
 __global__ void k_sp_rlo(const uint32_t* __restrict__ R_b, const SpState* __restrict__ st,
                          uint32_t* __restrict__ rlo) {
+  pdl_wait();
   if (st->fail) return;
   const uint32_t nr = st->n_r;
   for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j <= nr; j += gridDim.x * blockDim.x) {
@@ -2880,6 +2908,7 @@ __global__ void __launch_bounds__(256) k_sp_cert_stats(const double* __restrict_
                                                        const double* __restrict__ R_y,
                                                        const uint32_t* __restrict__ R_s,
                                                        SpState* __restrict__ st) {
+  pdl_wait();
   if (st->fail) return;
   const uint32_t nr = st->n_r;
   const double lx = st->lx, ly = st->ly;
@@ -2916,6 +2945,7 @@ __device__ __forceinline__ double angle_of_pseudo(double ph) {
 }
 
 __global__ void k_sp_cert_decide(SpState* __restrict__ st, bool force_verify) {
+  pdl_wait();
   if (threadIdx.x != 0 || st->fail) return;
   const double eps = 1.1102230246251565e-16;
   const double D = sqrt(st->dmax2) * (1.0 + 1e-9);
@@ -2949,6 +2979,7 @@ __global__ void __launch_bounds__(kSpThreads, 1) k_sp_verify(
     const uint16_t* __restrict__ codes, uint32_t n, const uint32_t* __restrict__ gbits,
     const uint32_t* __restrict__ rlo, const double* __restrict__ R_x,
     const double* __restrict__ R_y, SpState* __restrict__ st) {
+  pdl_wait();
   extern __shared__ uint32_t s_rlo[];  // kSpBuckets + 1
   __shared__ uint32_t s_g[kSpBuckets / 32];
   if (st->fail || !st->need_verify) return;
@@ -3066,6 +3097,7 @@ __global__ void __launch_bounds__(kBlock) k_sp_compact(
     double* __restrict__ out_x, double* __restrict__ out_y, uint32_t* __restrict__ out_i,
     uint32_t* __restrict__ out_b, uint32_t* __restrict__ out_s, uint64_t* __restrict__ status,
     Counters* __restrict__ ctr) {
+  pdl_wait();
   __shared__ uint32_t s_tile, s_excl, s_rows[kCompactItems * kWarps + 1];
   if (st->fail) return;
   const uint32_t n = st->n_w;
@@ -3160,6 +3192,7 @@ __global__ void __launch_bounds__(256) k_sp_fill_regions(uint32_t n, uint32_t id
 // Sizes of the gathered buckets (storage of rank 0's gathered records).
 __global__ void k_sp_gsize(const uint32_t* __restrict__ gbits, const uint32_t* __restrict__ hist,
                            uint32_t* __restrict__ out) {
+  pdl_wait();
   const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b < kSpBuckets) out[b] = sp_gathered(gbits, b) ? hist[b] : 0u;
 }
