@@ -15,7 +15,7 @@ timeout 900 python bench.py --impl reference --steps 3 --warmup 2 > $out/bench_r
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $out/launches.csv \
   python bench.py --steps 2 --warmup 1 --no-cpu-baseline > $out/launch_run.log 2>&1
 timeout 900 ncu --set full --import-source on --clock-control none \
-  -k "regex:k_extremes|k_sp_hist|k_sp_phi|k_sp_cand|k_gr_mid|k_gr_cert|k_gr_up|k_gr_down|k_sp_dup|k_sp_place_g|k_sp_sort_gathered|k_sp_walk" -c 18 -o $out/full \
+  -k "regex:k_extremes|k_sp_hist|k_sp_phi|k_sp_cand|k_gr_mid|k_gr_cert|k_gr_up|k_gr_down|k_sp_dup|k_sp_place_g|k_sp_sort_gathered|k_sp_walk|k_sp_lrank|k_sp_f2_patch" -c 20 -o $out/full \
   python tools/one_call.py square 20000000 1 > $out/full_run.log 2>&1
 ncu -i $out/full.ncu-rep --page raw --csv > $out/full_raw.csv 2>/dev/null
 timeout 900 ncu --set full --clock-control none -k "regex:k_sp_hist_ring|k_extremes_tma" -c 2 -o $out/c5 \
