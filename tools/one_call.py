@@ -1,5 +1,7 @@
 """One C2-sized hull call on device-resident input, the bench's `value` path
-(for ncu captures): python tools/one_call.py [kind] [n] [calls]"""
+(for ncu captures): python tools/one_call.py [kind] [n] [calls]
+ONE_CALL_HOST=1: through the host entry instead (hull_indices: overlapped ingest)."""
+import os
 import sys
 from pathlib import Path
 
@@ -22,5 +24,8 @@ else:
 torch.cuda.synchronize()
 out = torch.empty(n, dtype=torch.int32, device="cuda")
 for _ in range(calls):
-    k, st = eng.hull_device(xs.data_ptr(), ys.data_ptr(), n, out.data_ptr(), n, PipelineConfig())
+    if os.environ.get("ONE_CALL_HOST"):
+        idx, st = eng.hull_indices(xs.cpu().numpy(), ys.cpu().numpy(), PipelineConfig())
+    else:
+        k, st = eng.hull_device(xs.data_ptr(), ys.data_ptr(), n, out.data_ptr(), n, PipelineConfig())
 print(kind, n, st.n_after_round1, st.n_after_round2, st.hull_size, eng.sparse_info(), flush=True)
