@@ -1384,10 +1384,12 @@ __global__ void __launch_bounds__(kMax ? kSpF3Threads : 1024, 1) k_sp_phi(
     }
     uint32_t nh = 0, ng = 0;
     bool gat[4];
+    float pv[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const bool surv = b[k] != kSpNoCode;
       gat[k] = false;
+      pv[k] = 0.0f;  // read by F4 only for bucketed, non-gathered points
       if (!surv) continue;
       ++nh;
       atomicAdd(&s_part[half][(uint32_t)(h[k] >> (64 - kSpPartBits))], 1u);
@@ -1399,11 +1401,15 @@ __global__ void __launch_bounds__(kMax ? kSpF3Threads : 1024, 1) k_sp_phi(
       } else if (v2[k] >= r02) {  // points within r0 of P_l never raise a maximum (certificate)
         const float sv = __double2float_rd(b[k] < b_l ? raw[k] : -raw[k]);
         if (kMax) atomicMax(&s_phi[b[k]], ord_f(sv));
-        phi32[idx[k]] = sv;  // F4 reads it instead of recomputing
+        pv[k] = sv;  // F4 reads it instead of recomputing
       } else {
-        phi32[idx[k]] = __int_as_float(0x7fc00000);  // NaN: always a candidate
+        pv[k] = __int_as_float(0x7fc00000);  // NaN: always a candidate
       }
     }
+    // every point's slot is written (whole sectors: no read-for-merge of
+    // partially written ones when L2 evicts them)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) phi32[idx[k]] = pv[k];
     const uint32_t lane = threadIdx.x & 31;
     uint32_t at = warp_scan_claim(&s_nh[half], nh, lane);
 #pragma unroll
