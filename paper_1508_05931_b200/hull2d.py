@@ -260,11 +260,14 @@ class Engine:
     def hull_device(self, d_xs: int, d_ys: int, n: int, d_out: int, out_cap: int,
                     cfg: PipelineConfig | None = None) -> tuple[int, StageStats]:
         """Device-pointer entry; d_out receives uint32 indices on the device."""
-        c = (cfg or PipelineConfig())._c()
-        st = N.gscan_stats()
-        out_len = C.c_uint64()
-        rc = self._lib.gscan_hull_f64_device(self._h, C.c_void_p(d_xs), C.c_void_p(d_ys), int(n),
-                                             C.byref(c), C.c_void_p(d_out), int(out_cap),
+        cfg = cfg or PipelineConfig()
+        key = (cfg.chunk_count, cfg.enable_round1, cfg.enable_round2, cfg.chunked)
+        cache = getattr(self, "_dev_call", None)
+        if cache is None or cache[0] != key:  # ctypes argument objects, reused per call
+            cache = (key, cfg._c(), N.gscan_stats(), C.c_uint64())
+            self._dev_call = cache
+        _, c, st, out_len = cache
+        rc = self._lib.gscan_hull_f64_device(self._h, d_xs, d_ys, n, C.byref(c), d_out, out_cap,
                                              C.byref(out_len), C.byref(st))
         if rc:
             self._raise(rc, "full_pipeline")
