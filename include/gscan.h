@@ -151,6 +151,22 @@ int gscan_shard_extremes(gscan_handle* h, const double* d_xs, const double* d_ys
 int gscan_shard_round1(gscan_handle* h, const double* d_xs, const double* d_ys, uint64_t n,
                        const gscan_extremes* global, uint32_t* d_out, uint64_t* n_out);
 
+/* Distributed sample sort (the sharded path's survivor fallback, SURVEY.md
+ * 8e: "a distributed sample sort when the survivor set is large", e.g. points
+ * on a circle). Every rank: gscan_shard_round1 -> gscan_shard_keys (the exact
+ * sort key of each survivor: atan2 from the global anchor, bits; UINT64_MAX
+ * for points equal to the anchor) -> survivors routed by key ranges (sampled
+ * splitters; equal keys stay on one rank) -> gscan_stage_sorted on the
+ * received points plus the anchor, in global-index order (the bucket sort +
+ * dedup) -> sorted runs to rank 0, whose concatenation is the reference's
+ * annotated buffer -> rank 0: gscan_hull_sorted (split_regions, round 2,
+ * Graham; d_out = hull as buffer positions). */
+int gscan_shard_keys(gscan_handle* h, const double* d_xs, const double* d_ys, const uint32_t* d_idx,
+                     uint64_t m, const gscan_extremes* global, uint64_t* d_keys);
+int gscan_hull_sorted(gscan_handle* h, const double* d_X, const double* d_Y, uint64_t M,
+                      const gscan_config* cfg, uint32_t* d_out, uint64_t out_cap, uint64_t* hull_n,
+                      uint64_t* n2);
+
 /* ---- sharded sparse path (paper_1508_05931_b200/distributed.py) ----
  *
  * One handle per rank; rank r owns the contiguous shard [offset, offset + n)

@@ -114,6 +114,9 @@ SIGNATURES = {
     "gscan_dist_root_finish": (C.c_int, [_P, _P, _P, _U64, _U64, _P, _U64, _P, _U64, _U64P, _U64P,
                                          C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]),
     "gscan_dist_enq_verify": (C.c_int, [_P, _P, _P, _P]),
+    "gscan_shard_keys": (C.c_int, [_P, _P, _P, _P, _U64, C.POINTER(gscan_extremes), _P]),
+    "gscan_hull_sorted": (C.c_int, [_P, _P, _P, _U64, C.POINTER(gscan_config), _P, _U64, _U64P,
+                                    _U64P]),
     "gscan_status_string": (C.c_char_p, [C.c_int]),
     "gscan_last_error": (C.c_char_p, [_P]),
     "gscan_last_launch_count": (_U64, [_P]),

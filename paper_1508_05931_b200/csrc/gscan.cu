@@ -2398,6 +2398,90 @@ int gscan_shard_extremes(gscan_handle* h, const double* d_xs, const double* d_ys
   return GSCAN_OK;
 }
 
+// ---- distributed sample sort (the survivor fallback of the sharded path) ----
+// Exact sort keys (angular.hpp: atan2 of the vector from the global anchor;
+// kKeyDrop for points equal to the anchor) of a list of this shard's points.
+__global__ void k_dist_keys(const double* __restrict__ xs, const double* __restrict__ ys,
+                            const uint32_t* __restrict__ idx, uint32_t m, double ax, double ay,
+                            uint64_t* __restrict__ keys) {
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < m; j += gridDim.x * blockDim.x) {
+    const uint32_t i = idx[j];
+    const double x = xs[i], y = ys[i];
+    uint64_t key = kKeyDrop;
+    if (!(x == ax && y == ay)) {
+      const double a = glibc_atan2(__dsub_rn(y, ay), __dsub_rn(x, ax));
+      key = (a == 0.0) ? 0ull : dbits(a);
+    }
+    keys[j] = key;
+  }
+}
+
+__global__ void k_sp_set_u32_host(uint32_t* __restrict__ p, uint32_t v) { *p = v; }
+__global__ void k_iota(uint32_t* __restrict__ a, uint32_t m) {
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < m; j += gridDim.x * blockDim.x) a[j] = j;
+}
+
+int gscan_shard_keys(gscan_handle* h, const double* d_xs, const double* d_ys, const uint32_t* d_idx,
+                     uint64_t m, const gscan_extremes* global, uint64_t* d_keys) {
+  if (!h || !global || (m && (!d_xs || !d_ys || !d_idx || !d_keys))) return GSCAN_E_INVALID;
+  if (m >= 0xffffffffull) return fail(h, GSCAN_E_TOO_LARGE, "m = %llu exceeds 2^32-2", (unsigned long long)m);
+  CU(cudaSetDevice(h->device));
+  if (m) {
+    const uint32_t grid = std::max(1u, std::min<uint32_t>((uint32_t)((m + 255) / 256), h->sm_count * 8));
+    Launch L(h, "k_dist_keys");
+    k_dist_keys<<<grid, 256, 0, h->stream>>>(d_xs, d_ys, d_idx, (uint32_t)m, global->x[4], global->y[4],
+                                             d_keys);
+  }
+  CU(cudaGetLastError());
+  CU(cudaStreamSynchronize(h->stream));
+  return GSCAN_OK;
+}
+
+// Round 2 and Graham over an annotated buffer that is already sorted and
+// deduplicated (position 0 = the anchor): the last step of the distributed
+// sample sort on rank 0. *d_out: hull as buffer positions.
+int gscan_hull_sorted(gscan_handle* h, const double* d_X, const double* d_Y, uint64_t M,
+                      const gscan_config* cfg, uint32_t* d_out, uint64_t out_cap, uint64_t* hull_n,
+                      uint64_t* n2) {
+  if (!h || !cfg || !d_X || !d_Y || !d_out || !hull_n || !n2 || M == 0) return GSCAN_E_INVALID;
+  TRY(validate(h, M, *cfg));
+  CU(cudaSetDevice(h->device));
+  TRY(reserve(h, M));
+  if (h->large) return fail(h, GSCAN_E_TOO_LARGE, "sorted buffers above %llu points", (unsigned long long)full_sort_max());
+  const uint32_t m = (uint32_t)M;
+  cudaStream_t s = h->stream;
+  CU(cudaMemsetAsync(h->ctr, 0, sizeof(Counters), s));
+  CU(cudaMemcpyAsync(h->A_x, d_X, (size_t)m * 8, cudaMemcpyDeviceToDevice, s));
+  CU(cudaMemcpyAsync(h->A_y, d_Y, (size_t)m * 8, cudaMemcpyDeviceToDevice, s));
+  const uint32_t grid = std::max(1u, std::min<uint32_t>((m + kBlock - 1) / kBlock, h->sm_count * 8));
+  k_iota<<<grid, kBlock, 0, s>>>(h->A_i, m);
+  k_sp_set_u32_host<<<1, 1, 0, s>>>(&h->ctr->m_total, m);
+  // split_regions (angular.hpp:197-204): the first position of the largest dist2
+  CU(cudaMemsetAsync(h->scratch64, 0, 8, s));
+  CU(cudaMemsetAsync(h->scratch64 + 1, 0xff, 8, s));
+  k_longest_scan<<<grid, kBlock, 0, s>>>(h->A_x, h->A_y, m, h->scratch64,
+                                         reinterpret_cast<uint32_t*>(h->scratch64 + 1), 0);
+  k_longest_scan<<<grid, kBlock, 0, s>>>(h->A_x, h->A_y, m, h->scratch64,
+                                         reinterpret_cast<uint32_t*>(h->scratch64 + 1), 1);
+  CU(cudaMemcpyAsync(&h->ctr->longest, h->scratch64 + 1, 4, cudaMemcpyDeviceToDevice, s));
+  CU(cudaGetLastError());
+  TRY(sync_counters(h));
+  if (m < 2) CU(cudaMemsetAsync(&h->ctr->longest, 0, 4, s));
+  double *Rx, *Ry;
+  uint32_t* Ri;
+  TRY(stage_round2(h, *cfg, &Rx, &Ry, &Ri));
+  TRY(sync_counters(h));
+  TRY(stage_graham(h, Rx, Ry, Ri, h->h_ctr->n2));
+  TRY(sync_counters(h));
+  const uint32_t hull = h->h_ctr->hull;
+  *n2 = h->h_ctr->n2;
+  *hull_n = hull;
+  if (hull > out_cap) return fail(h, GSCAN_E_CAPACITY, "hull of %u vertices exceeds out_cap", hull);
+  CU(cudaMemcpyAsync(d_out, h->d_out, (size_t)hull * 4, cudaMemcpyDeviceToDevice, s));
+  CU(cudaStreamSynchronize(s));
+  return GSCAN_OK;
+}
+
 int gscan_shard_round1(gscan_handle* h, const double* d_xs, const double* d_ys, uint64_t n,
                        const gscan_extremes* global, uint32_t* d_out, uint64_t* n_out) {
   if (!h || !global || !d_out || !n_out) return GSCAN_E_INVALID;

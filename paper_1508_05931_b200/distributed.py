@@ -400,7 +400,9 @@ def sparse_sharded(engines: list[Engine], shards, offsets: list[int], n_global: 
     stream = _bind_stream(engines, dev)
     stream.wait_stream(torch.cuda.current_stream(dev))  # the shards were written there
     with torch.cuda.stream(stream):
-        return _sparse_sharded(engines, shards, offsets, n_global, cfg, comm, dev)
+        res = _sparse_sharded(engines, shards, offsets, n_global, cfg, comm, dev)
+    torch.cuda.current_stream(dev).wait_stream(stream)
+    return res
 
 
 def _sparse_sharded(engines, shards, offsets, n_global, cfg, comm, dev):
@@ -612,6 +614,16 @@ def survivor_gather(eng: Engine, d_xs: torch.Tensor, d_ys: torch.Tensor, offset:
                     cfg: PipelineConfig, comm: TorchComm):
     """K1/K2 per shard, every survivor (x, y, global index) to rank 0, which runs
     the rest with round 1 disabled (it already ran)."""
+    stream = _bind_stream([eng], d_xs.device)  # the handle's work and the torch ops in one order
+    stream.wait_stream(torch.cuda.current_stream(d_xs.device))
+    with torch.cuda.stream(stream):
+        res = _survivor_gather(eng, d_xs, d_ys, offset, cfg, comm)
+    torch.cuda.current_stream(d_xs.device).wait_stream(stream)
+    return res
+
+
+def _survivor_gather(eng: Engine, d_xs: torch.Tensor, d_ys: torch.Tensor, offset: int,
+                     cfg: PipelineConfig, comm: TorchComm):
     lib = eng._lib
     n = int(d_xs.numel())
     rank, world = comm.rank, comm.world
@@ -661,6 +673,148 @@ def survivor_gather(eng: Engine, d_xs: torch.Tensor, d_ys: torch.Tensor, offset:
     return hull_global, stats
 
 
+def sample_sort_sharded(engines: list[Engine], shards, offsets: list[int], n_global: int,
+                        cfg: PipelineConfig, comm: Comm):
+    """The exact fallback as a distributed sample sort ("a
+    distributed sample sort when the survivor set is large", e.g. points on a
+    circle, where the sparse path declines). Every rank keeps its round-1
+    survivors (global quad), keys them exactly (gscan_shard_keys: atan2 from
+    the global anchor) and routes them by key range to the rank that sorts
+    that range (splitters from a key sample; equal keys stay on one rank, so
+    ties and duplicates are resolved where they meet). Each rank sorts and
+    deduplicates its range with the bucket sort (gscan_stage_sorted over the
+    received points plus the anchor, in global-index order: index ties break
+    as on one device). The sorted runs, concatenated in rank order, are the
+    reference's annotated buffer; rank 0 runs split_regions, round 2 and
+    Graham on it (gscan_hull_sorted). Returns (indices, stats) on rank 0,
+    (None, None) elsewhere."""
+    dev = shards[0][0].device
+    stream = _bind_stream(engines, dev)  # the handles' work and the torch ops in one order
+    stream.wait_stream(torch.cuda.current_stream(dev))
+    with torch.cuda.stream(stream):
+        res = _sample_sort(engines, shards, offsets, n_global, cfg, comm, dev)
+    torch.cuda.current_stream(dev).wait_stream(stream)
+    return res
+
+
+def _sample_sort(engines, shards, offsets, n_global, cfg, comm, dev):
+    R = comm.world
+    me = comm.ranks
+    # global extremes (the reference's tie rules)
+    recs = []
+    for eng, (dx, dy), off in zip(engines, shards, offsets):
+        ex = N.gscan_extremes()
+        _ck(eng, eng._lib.gscan_shard_extremes(eng.handle, C.c_void_p(dx.data_ptr()),
+                                               C.c_void_p(dy.data_ptr()), dx.numel(), C.byref(ex)),
+            "shard_extremes")
+        recs.append([off + ex.idx[k] for k in range(5)] + [_i64(v) for v in ex.x]
+                    + [_i64(v) for v in ex.y])
+    allr = comm.allgather_i64(recs)
+    g = _combine(np.stack([np.array([[float(r[k]) for k in range(5)],
+                                     [_f64(r[5 + k]) for k in range(5)],
+                                     [_f64(r[10 + k]) for k in range(5)]]) for r in allr]))
+    gex = N.gscan_extremes()
+    for k in range(5):
+        gex.idx[k] = int(g[0, k])
+        gex.x[k] = g[1, k]
+        gex.y[k] = g[2, k]
+    a_x, a_y, a_i = float(g[1, 4]), float(g[2, 4]), int(g[0, 4])
+    # round-1 survivors and their exact keys; a key sample for the splitters
+    S = 1024
+    kept, n1s, samples = [], [], []
+    for eng, (dx, dy), off in zip(engines, shards, offsets):
+        n = int(dx.numel())
+        surv = torch.empty(max(n, 1), dtype=_U32, device=dev)
+        n1 = C.c_uint64()
+        _ck(eng, eng._lib.gscan_shard_round1(eng.handle, C.c_void_p(dx.data_ptr()),
+                                             C.c_void_p(dy.data_ptr()), n, C.byref(gex),
+                                             C.c_void_p(surv.data_ptr()), C.byref(n1)), "shard_round1")
+        m = int(n1.value)
+        n1s.append(m)
+        keys = torch.empty(max(m, 1), dtype=torch.int64, device=dev)
+        _ck(eng, eng._lib.gscan_shard_keys(eng.handle, C.c_void_p(dx.data_ptr()),
+                                           C.c_void_p(dy.data_ptr()), C.c_void_p(surv.data_ptr()), m,
+                                           C.byref(gex), C.c_void_p(keys.data_ptr())), "shard_keys")
+        loc = surv[:m].to(torch.int64) & 0xFFFFFFFF
+        keys = keys[:m]
+        keep = keys != -1  # points equal to the anchor: annotate drops them
+        loc, keys = loc[keep], keys[keep]
+        kept.append((dx[loc], dy[loc], loc + off, keys))
+        pick = torch.linspace(0, max(keys.numel() - 1, 0), S, device=dev).long() if keys.numel() \
+            else torch.zeros(0, dtype=torch.int64, device=dev)
+        row = keys[pick].tolist() if keys.numel() else []
+        samples.append(row + [np.iinfo(np.int64).max] * (S - len(row)))
+    allS = comm.allgather_i64(samples).ravel()
+    allS = np.sort(allS[allS != np.iinfo(np.int64).max])
+    if allS.size == 0:
+        split = torch.zeros(0, dtype=torch.int64, device=dev)
+    else:
+        split = torch.as_tensor(allS[[(k * allS.size) // R for k in range(1, R)]], device=dev)
+    # route the survivors by key range (counts first: the receivers' sizes)
+    sends, cnts = [], []
+    for (x, y, gi, keys) in kept:
+        dest = torch.searchsorted(split, keys, right=True)
+        order = torch.argsort(dest, stable=True)
+        sends.append((x[order], y[order], gi[order]))
+        cnts.append(torch.bincount(dest, minlength=R).tolist())
+    cm = comm.allgather_i64(cnts)  # (R senders, R receivers)
+    send_sz = [cnts[k] for k in range(len(kept))]
+    recv_sz = [cm[:, r].tolist() for r in me]
+    rx = comm.all_to_all_flat([sd[0] for sd in sends], send_sz, recv_sz)
+    ry = comm.all_to_all_flat([sd[1] for sd in sends], send_sz, recv_sz)
+    rg = comm.all_to_all_flat([sd[2] for sd in sends], send_sz, recv_sz)
+    # each rank: its key range sorted and deduplicated, in global-index order
+    runs = []
+    for eng, x, y, gi in zip(engines, rx, ry, rg):
+        X = torch.cat([torch.tensor([a_x], dtype=torch.float64, device=dev), x])
+        Y = torch.cat([torch.tensor([a_y], dtype=torch.float64, device=dev), y])
+        G = torch.cat([torch.tensor([a_i], dtype=torch.int64, device=dev), gi])
+        o = torch.argsort(G)
+        X, Y, G = X[o].contiguous(), Y[o].contiguous(), G[o]
+        m = int(X.numel())
+        out = torch.empty(m, dtype=_U32, device=dev)
+        ln = C.c_uint64()
+        _ck(eng, eng._lib.gscan_stage_sorted(eng.handle, C.c_void_p(X.data_ptr()),
+                                             C.c_void_p(Y.data_ptr()), m, C.c_void_p(out.data_ptr()),
+                                             C.byref(ln)), "stage_sorted")
+        pos = out[1: int(ln.value)].to(torch.int64) & 0xFFFFFFFF  # 0: the anchor
+        runs.append((X[pos], Y[pos], G[pos]))
+    sizes = comm.allgather_i64([[int(r[0].numel()), n1] for r, n1 in zip(runs, n1s)])
+    rsz = sizes[:, 0].tolist()
+    n1_total = int(sizes[:, 1].sum())
+    parts = [comm.gather_root([r[j] for r in runs], sizes=rsz) for j in range(3)]
+    if parts[0] is None:
+        return None, None
+    eng0 = engines[me.index(0)]
+    BX = torch.cat([torch.tensor([a_x], dtype=torch.float64, device=dev)] + parts[0]).contiguous()
+    BY = torch.cat([torch.tensor([a_y], dtype=torch.float64, device=dev)] + parts[1]).contiguous()
+    BG = torch.cat([torch.tensor([a_i], dtype=torch.int64, device=dev)] + parts[2])
+    M = int(BX.numel())
+    out = torch.empty(M, dtype=_U32, device=dev)
+    hn, n2 = C.c_uint64(), C.c_uint64()
+    ccfg = cfg._c()
+    _ck(eng0, eng0._lib.gscan_hull_sorted(eng0.handle, C.c_void_p(BX.data_ptr()),
+                                          C.c_void_p(BY.data_ptr()), M, C.byref(ccfg),
+                                          C.c_void_p(out.data_ptr()), M, C.byref(hn), C.byref(n2)),
+        "hull_sorted")
+    k = int(hn.value)
+    hv = BG[out[:k].to(torch.int64) & 0xFFFFFFFF].cpu().numpy().astype(np.uint64)
+    return hv, StageStats(n_input=n_global, n_after_round1=n1_total,
+                          n_after_round2=int(n2.value), hull_size=k)
+
+
+def simulate_sample_sort(engines: list[Engine], xs: torch.Tensor, ys: torch.Tensor,
+                         cfg: PipelineConfig | None = None, bounds: list[int] | None = None):
+    """The distributed sample sort with all R ranks in this process (LocalComm)."""
+    cfg = cfg or PipelineConfig()
+    R = len(engines)
+    n = int(xs.numel())
+    offs = list(bounds) if bounds is not None else [n * r // R for r in range(R + 1)]
+    shards = [(xs[offs[r]:offs[r + 1]].contiguous(), ys[offs[r]:offs[r + 1]].contiguous())
+              for r in range(R)]
+    return sample_sort_sharded(engines, shards, offs[:R], n, cfg, LocalComm(R))
+
+
 def _default_toggles(cfg: PipelineConfig) -> bool:
     return cfg.enable_round1 and cfg.enable_round2 and cfg.chunked
 
@@ -681,6 +835,8 @@ def sharded_hull(eng: Engine, d_xs: torch.Tensor, d_ys: torch.Tensor, offset: in
         res = sparse_sharded([eng], [(d_xs, d_ys)], [offset], n_global, cfg, comm)
         if res is not None:
             return res
+    if cfg.enable_round1 and n_global < 0xFFFFFFFF and d_xs.is_cuda and min(sizes) > 0:
+        return sample_sort_sharded([eng], [(d_xs, d_ys)], [offset], n_global, cfg, comm)
     return survivor_gather(eng, d_xs, d_ys, offset, cfg, comm)
 
 

@@ -239,3 +239,41 @@ def test_sharded_host_waits(engines, oracle_mod, monkeypatch):
     monkeypatch.undo()
     assert st is not None, D.last_decline
     assert len(calls) <= 4, calls
+
+
+@pytest.mark.parametrize("kind", ["circle", "square", "disk", "dups"])
+@pytest.mark.parametrize("R", [2, 3, 4])
+def test_sample_sort_matches_oracle(engines, oracle_mod, kind, R):
+    """The distributed sample sort (the sharded path's exact fallback for
+    near-convex inputs): round-1 survivors routed by exact key
+    ranges, sorted and deduplicated per rank, round 2 and Graham on rank 0 --
+    bit-exact against the oracle, duplicates across ranks included."""
+    from paper_1508_05931_b200 import PipelineConfig, generate
+    from paper_1508_05931_b200.distributed import simulate_sample_sort
+
+    n = 200_000
+    if kind == "dups":  # every point twice, the copies in other shards
+        xs, ys = generate("disk", n // 2, R)
+        xs, ys = np.concatenate([xs, xs[::-1]]), np.concatenate([ys, ys[::-1]])
+    else:
+        xs, ys = generate(kind, n, R)
+    for cfg in (dict(), dict(chunk_count=7), dict(enable_round2=False), dict(chunked=False)):
+        dx, dy = torch.from_numpy(xs).cuda(), torch.from_numpy(ys).cuda()
+        got, st = simulate_sample_sort(engines[:R], dx, dy, PipelineConfig(**cfg))
+        want, sw = oracle_mod.full_pipeline(xs, ys, **cfg)
+        assert np.array_equal(got, want), (kind, R, cfg, got[:8], want[:8])
+        for k in ("n_after_round1", "n_after_round2", "hull_size"):
+            assert getattr(st, k) == sw[k], (k, cfg)
+
+
+def test_sample_sort_uneven_shards(engines, oracle_mod):
+    """Shards of 1, 5 and the rest points, and a shard that receives no key range."""
+    from paper_1508_05931_b200 import PipelineConfig, generate
+    from paper_1508_05931_b200.distributed import simulate_sample_sort
+
+    xs, ys = generate("circle", 50_000, 4)
+    dx, dy = torch.from_numpy(xs).cuda(), torch.from_numpy(ys).cuda()
+    got, st = simulate_sample_sort(engines[:3], dx, dy, PipelineConfig(), bounds=[0, 1, 6, 50_000])
+    want, sw = oracle_mod.full_pipeline(xs, ys)
+    assert np.array_equal(got, want)
+    assert st.n_after_round2 == sw["n_after_round2"]
