@@ -827,9 +827,17 @@ __global__ void __launch_bounds__(kBlock) k_bucket_sort_block(
         const uint32_t it = s_idx[t];
         uint32_t r = 0;
         bool is_dead = false;
+        // key_less(j, t), reading dist2, index and coordinates only on equal
+        // keys: equal points have equal keys and dist2 (the anchor's copies
+        // were dropped), so a duplicate is always found in the last branch
         for (uint32_t j = sb; j < se; ++j) {
-          r += key_less(s_key[j], s_d2[j], s_idx[j], kt, dt, it);
-          is_dead |= (s_x[j] == xt && s_y[j] == yt && s_idx[j] < it);
+          const uint64_t kj = s_key[j];
+          if (kj != kt) { r += kj < kt; continue; }
+          const double dj = s_d2[j];
+          if (dj != dt) { r += dj < dt; continue; }
+          const uint32_t ij = s_idx[j];
+          r += ij < it;
+          is_dead |= (ij < it && s_x[j] == xt && s_y[j] == yt);
         }
         const uint32_t pos = 1 + e0 + sb + r;
         A_x[pos] = xt;
