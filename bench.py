@@ -424,6 +424,24 @@ def main():
                     "kernel": fkern, "kernel_ms": round(t_filter, 4),
                     "algorithmic_bytes": alg_bytes, "peak_source": peak_src}
 
+    # ---- sort throughput (keys/s, north star): the sort kernels of the path that served ----
+    sort = None
+    if world == 1:
+        if eng.sparse_info()[0] == 1:  # gathered buckets + walk candidates, placed and sorted exactly
+            names = ("k_sp_place_g", "k_sp_sort_gathered", "k_sp_sort_gathered_big",
+                     "k_sp_sort_gathered_huge", "k_sp_rank_c", "k_sp_place_c", "k_sp_place_cand",
+                     "k_sp_sort_cand_big", "k_sp_place_gathered")
+            nkeys = int(eng.sparse_info()[2])  # the walk array: anchor + gathered + candidates
+            what = "gathered points + walk candidates (sparse path)"
+        else:  # every annotated survivor: bucket offsets, scatter, per-bucket sorts
+            names = ("k_scan_u32", "k_scatter", "k_bucket_sort_block", "k_bucket_sort_cta")
+            nkeys = int(n1) if n1 else 0
+            what = "round-1 survivors (full sort: bucket scatter + per-bucket sorts)"
+        t_sort = sum(kernels.get(k2, 0.0) for k2 in names)
+        if t_sort > 0 and nkeys:
+            sort = {"keys": nkeys, "ms": round(t_sort, 4),
+                    "gkeys_per_s": round(nkeys / (t_sort * 1e-3) / 1e9, 3), "what": what}
+
     # ---- e2e: host buffers in, hull indices out, copies inside the timed region ----
     e2e = None
     n_local = hi - lo
@@ -508,7 +526,7 @@ def main():
         "data": f"synthetic ({gen_how})",
         "config": config_dict(args.config, world),
         "parity_vs_golden": parity,
-        "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks,
+        "e2e": e2e, "roofline": roofline, "sort": sort, "cpu_baseline": cpu, "clocks": clocks,
         "gpu_launches": launches, "kernels_ms": kernels, "sparse_path": eng.sparse_info()[0] == 1,
         "stats": {k2: getattr(st, k2) for k2 in ("n_after_round1", "n_after_round2", "hull_size")}
         if st is not None else None,
