@@ -224,7 +224,14 @@ constexpr int kExtTile = GSCAN_EXT_TILE;  // points per tile (2048: 16 KB of x +
 #define GSCAN_EXT_STAGES 4
 #endif
 constexpr int kExtStages = GSCAN_EXT_STAGES;
-constexpr int kExtThreads = 512;  // 2 pairs (4 points) per thread per tile
+#ifndef GSCAN_EXT_THREADS
+#define GSCAN_EXT_THREADS 512
+#endif
+#ifndef GSCAN_EXT_ACC
+#define GSCAN_EXT_ACC 4
+#endif
+constexpr int kExtThreads = GSCAN_EXT_THREADS;  // 512: 2 pairs (4 points) per thread per tile
+constexpr int kExtAcc = GSCAN_EXT_ACC;          // independent accumulators per thread
 using ExtRing = XYRing<kExtTile, kExtStages>;
 constexpr size_t kExtSmem = ExtRing::kSmem + 64;
 
@@ -241,9 +248,9 @@ __global__ void __launch_bounds__(kExtThreads, 1) k_extremes_tma(const double* _
   __syncthreads();
   // four independent accumulators (one per point of a thread's tile share):
   // shorter dependency chains; each still sees increasing indices
-  ExtAcc acc[4];
+  ExtAcc acc[kExtAcc];
 #pragma unroll
-  for (int a = 0; a < 4; ++a) ext_init(acc[a]);
+  for (int a = 0; a < kExtAcc; ++a) ext_init(acc[a]);
   for (uint32_t k = 0; k < ring.mine; ++k) {
     ring.wait(k);
     const double2* x2 = reinterpret_cast<const double2*>(ring.tx(k));
@@ -260,16 +267,15 @@ __global__ void __launch_bounds__(kExtThreads, 1) k_extremes_tma(const double* _
 #pragma unroll
     for (int u = 0; u < kPairs; ++u) {
       const uint32_t i = i0 + 2 * u * kExtThreads;
-      ext_push(acc[(2 * u) & 3], vx[u].x, vy[u].x, i);
-      ext_push(acc[(2 * u + 1) & 3], vx[u].y, vy[u].y, i + 1);
+      ext_push(acc[(2 * u) % kExtAcc], vx[u].x, vy[u].x, i);
+      ext_push(acc[(2 * u + 1) % kExtAcc], vx[u].y, vy[u].y, i + 1);
     }
   }
   if (blockIdx.x == gridDim.x - 1)
     for (uint32_t i = (n / kExtTile) * kExtTile + threadIdx.x; i < n; i += kExtThreads)
       ext_push(acc[0], xs[i], ys[i], i);
-  ext_merge(acc[0], acc[1]);
-  ext_merge(acc[2], acc[3]);
-  ext_merge(acc[0], acc[2]);
+#pragma unroll
+  for (int a = 1; a < kExtAcc; ++a) ext_merge(acc[0], acc[a]);
   ext_finish(acc[0], xs, ys, partials, out, ctr);
 }
 
