@@ -102,33 +102,6 @@ __device__ __forceinline__ uint64_t lookback_exclusive(uint64_t* status, uint32_
   return excl;
 }
 
-// ---------------------------------------------------------------------------
-// Block-wide exclusive scan of one uint32 per thread (kBlock threads).
-__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* smem_warp,
-                                                         uint32_t* total) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint32_t x = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
-  }
-  if (lane == 31) smem_warp[warp] = x;
-  __syncthreads();
-  if (warp == 0) {
-    uint32_t s = (lane < kWarps) ? smem_warp[lane] : 0;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, s, o);
-      if (lane >= o) s += y;
-    }
-    if (lane < kWarps) smem_warp[lane] = s;  // inclusive warp prefix
-  }
-  __syncthreads();
-  const uint32_t warp_excl = warp ? smem_warp[warp - 1] : 0;
-  if (total) *total = smem_warp[kWarps - 1];
-  return warp_excl + x - v;
-}
 
 // ---- bulk copies (TMA, non-tensor) into shared memory, mbarrier-completed ----
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
