@@ -230,12 +230,18 @@ def cpu_baseline(xs, ys, n) -> dict:
         _, st = oracle.full_pipeline(xs, ys, impl=impl)
         times.append(st["t_total_ms"])
     t = float(np.median(times))
+    # the reference's own baseline hull (cli.hpp:183-186: oracle::monotone_chain), one run
+    t0 = time.perf_counter()
+    oracle.monotone_chain(xs, ys, impl=impl)
+    t_mc = (time.perf_counter() - t0) * 1e3
     return {"value": round(n / (t * 1e-3) / 1e6, 3), "unit": "Mpoints/s",
             "cores": 2 if impl == "ref" else 1,  # hull2d uses <= 2 threads (parallel.hpp:18-28)
             "kind": "reference" if impl == "ref" else "port", "t_total_ms": round(t, 1),
             "runs_ms": [round(v, 1) for v in times], **host_info(),
+            "monotone_chain_ms": round(t_mc, 1),
             "sample": f"median of {len(times)} full runs of the same {n}-point input, "
-                      "timed by StageStats.t_total_ms"}
+                      "timed by StageStats.t_total_ms; monotone_chain_ms: one wall-clock run of "
+                      "the reference's oracle::monotone_chain on it"}
 
 
 def run_reference(args, cfgname):
