@@ -428,7 +428,9 @@ def main():
                     "frac": round(achieved / peak, 4), "traffic": traffic,
                     "traffic_unit": "DRAM bytes per launch (ncu --set full, profiles/)",
                     "kernel": fkern, "kernel_ms": round(t_filter, 4),
-                    "algorithmic_bytes": alg_bytes, "peak_source": peak_src}
+                    "algorithmic_bytes": alg_bytes, "peak_source": peak_src,
+                    # the whole device-resident hull against one 16 B/pt read
+                    "whole_call_frac": round(16 * n / (ms_per_step * 1e-3) / 1e9 / peak, 4)}
 
     # ---- sort throughput (keys/s, north star): the sort kernels of the path that served ----
     sort = None
