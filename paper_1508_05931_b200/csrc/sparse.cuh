@@ -1098,6 +1098,10 @@ __global__ void __launch_bounds__(256) k_sp_plan_pl(const double* __restrict__ x
   // >= 90% of the points survive round 1 (near-convex input): nearly all would
   // be walk candidates, the full sort is faster (a speed decision)
   if (threadIdx.x == 0 && (uint64_t)ctr->n1 * 10 > (uint64_t)n * 9) atomicOr(&st->fail, kSpFailMany);
+  // a call that declined before F2 (k_sp_cdf) or inside it left the partials
+  // of an earlier call: their indices may lie beyond this input
+  __syncthreads();
+  if (*(volatile const uint32_t*)&st->fail) return;  // block-uniform after the barrier
   __shared__ uint64_t s_d[8];
   __shared__ uint32_t s_i[8], s_t[8];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
