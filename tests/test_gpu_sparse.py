@@ -199,3 +199,18 @@ def test_repeated_calls_reuse_the_graph(engine, oracle_mod):
     _run(engine, oracle_mod, xs2, ys2)
     _run(engine, oracle_mod, xs, ys, chunk_count=33)
     _run(engine, oracle_mod, xs, ys)
+
+
+def test_decline_after_a_larger_call(engine, oracle_mod):
+    """A call that declines before F2 (a circle: the sample says near-convex)
+    right after a larger sparse call on the same handle: the P_l partials
+    still hold the earlier call's indices, beyond this input, and must not be
+    read (tools/stress.py found the out-of-bounds read under memcheck)."""
+    from paper_1508_05931_b200 import PipelineConfig, generate
+
+    for kind, n in (("square", 1_500_000), ("circle", 120_000), ("disk", 900_000), ("circle", 70_000)):
+        xs, ys = generate(kind, n, 3)
+        got, st = engine.hull_indices(xs, ys, PipelineConfig())
+        want, sw = oracle_mod.full_pipeline(xs, ys)
+        assert np.array_equal(got, want), kind
+        assert (st.n_after_round1, st.n_after_round2) == (sw["n_after_round1"], sw["n_after_round2"])
