@@ -1,10 +1,12 @@
-"""Randomised parity stress on the device path: python tools/stress.py [cases] [seed]
+"""Randomised parity stress on the device path: python tools/stress.py [cases] [seed] [--sharded]
 
 Random families (uniform square/disk/circle, Gaussian, integer lattices with
 duplicates, clustered blobs, thin annuli, points on a few lines), random sizes
 (65K-1.5M, so both the sparse path and its declines run) and random pipeline
 configs. Every case is compared bit for bit with the CPU oracle (indices and
-stage counts). Prints one line per failure and a summary."""
+stage counts). --sharded: the same cases as 2-4 simulated ranks with random
+shard boundaries (the sharded sparse path, and the distributed sample sort
+when it declines). Prints one line per failure and a summary."""
 import sys
 from pathlib import Path
 
@@ -48,6 +50,7 @@ def make(kind, n):
 
 
 kinds = ["square", "disk", "circle", "gauss", "lattice", "blobs", "annulus", "lines"]
+SHARD_ENGINES = [Engine(0) for _ in range(4)] if "--sharded" in sys.argv else []
 bad, sparse = 0, 0
 for c in range(cases):
     kind = kinds[int(rng.integers(len(kinds)))]
@@ -64,6 +67,27 @@ for c in range(cases):
         continue
     if "-v" in sys.argv:
         print(f"case {c}: {kind} n={n} cfg={cfg} device={dev_entry}", flush=True)
+    if "--sharded" in sys.argv:  # R simulated ranks, random shard boundaries
+        from paper_1508_05931_b200.distributed import simulate_sample_sort, simulate_sharded
+        R = int(rng.integers(2, 5))
+        cuts = np.sort(rng.choice(np.arange(1, n), R - 1, replace=False)).tolist()
+        bounds = [0] + cuts + [n]
+        engs = SHARD_ENGINES[:R]
+        dx, dy = torch.from_numpy(xs).cuda(), torch.from_numpy(ys).cuda()
+        res = simulate_sharded(engs, dx, dy, PipelineConfig(**cfg), bounds=bounds) \
+            if (cfg.get("chunked", True) and cfg.get("enable_round2", True)) else None
+        if res is None:  # declined (or a non-default config): the exact fallback
+            res = simulate_sample_sort(engs, dx, dy, PipelineConfig(**cfg), bounds=bounds)
+        else:
+            sparse += 1
+        got, st = res
+        want, sw = oracle.full_pipeline(xs, ys, **cfg)
+        ok = (np.array_equal(got, want) and st.n_after_round1 == sw["n_after_round1"]
+              and st.n_after_round2 == sw["n_after_round2"] and st.hull_size == sw["hull_size"])
+        if not ok:
+            bad += 1
+            print(f"FAIL case {c}: {kind} n={n} R={R} bounds={bounds} cfg={cfg}", flush=True)
+        continue
     if dev_entry:  # the device entry (graph path) or the host entry (ingest)
         dx, dy = torch.from_numpy(xs).cuda(), torch.from_numpy(ys).cuda()
         out = torch.empty(n, dtype=torch.int32, device="cuda")
