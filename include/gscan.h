@@ -182,7 +182,7 @@ int gscan_hull_sorted(gscan_handle* h, const double* d_X, const double* d_Y, uin
  *   gscan_dist_enq_sample      global extremes; sample    cells -> sum
  *   gscan_dist_enq_f2          F2                         hist -> sum, rec -> all-gather
  *   gscan_dist_enq_plan        global P_l; P_l's rank     rec -> all-gather
- *   gscan_dist_enq_f3          F3                         phimax -> max, rec -> all-gather
+ *   gscan_dist_enq_f3          F3                         phimax -> max (as uint32), rec -> all-gather
  *   gscan_dist_enq_dup_local   hashes by partition        counts -> all-to-all
  *   (host sync 1: fail word, gathered counts, hash block sizes)
  *   hashes -> all-to-all; gscan_dist_enq_dup_check; gscan_dist_enq_export(0)
